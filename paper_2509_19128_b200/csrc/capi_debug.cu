@@ -1,0 +1,70 @@
+// capi_debug.cu -- kernel-level C entry points used by the parity tests and
+// bench.py to exercise single kernels through the same shared library the
+// engine uses (declared in include/streamrl_b200.h, "kernel entry points").
+#include <cuda_runtime.h>
+
+#include "gemm.cuh"
+#include "streamrl_b200.h"
+
+using namespace srl;
+
+namespace {
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? SRL_OK : SRL_CUDA_ERROR; }
+int num_sms() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+}  // namespace
+
+extern "C" int srl_kernel_gemm_bf16(const void* w, const void* x, int32_t M, int32_t N, int32_t K,
+                                    int32_t splits, int32_t epi_kind, const void* bias,
+                                    const float* ssq_in, int32_t ssq_parts, float inv_dim,
+                                    float eps, void* out, float* resid, const void* gain,
+                                    void* xg, float* ssq_out, void* stream) {
+  if (!w || !x || M < 1 || N < 1 || K < 64 || K % 64) return SRL_INVALID_ARGUMENT;
+  const int tok = gemm_tok_tile(M);
+  const CUtensorMap tw = make_tmap_bf16(w, (uint64_t)N, (uint64_t)K, 128);
+  const CUtensorMap tx = make_tmap_bf16(x, (uint64_t)M, (uint64_t)K, (uint32_t)tok);
+  if (splits <= 0) splits = gemm_auto_splits(M, N, K, num_sms());
+  GemmWorkspace ws;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (splits > 1) {
+    ws.partial_floats = gemm_workspace_floats(M, N, splits);
+    ws.counter_count = ((N + 127) / 128) * ((M + tok - 1) / tok);
+    if (cudaMallocAsync(&ws.partials, ws.partial_floats * sizeof(float), st) != cudaSuccess)
+      return SRL_OUT_OF_MEMORY;
+    if (cudaMallocAsync(&ws.counters, ws.counter_count * sizeof(int), st) != cudaSuccess)
+      return SRL_OUT_OF_MEMORY;
+    cudaMemsetAsync(ws.counters, 0, ws.counter_count * sizeof(int), st);
+  }
+  EpiParams epi;
+  epi.kind = epi_kind;
+  epi.ssq_in = ssq_in;
+  epi.ssq_in_parts = ssq_parts;
+  epi.inv_dim = inv_dim;
+  epi.eps = eps;
+  epi.bias = static_cast<const __nv_bfloat16*>(bias);
+  if (epi_kind == EPI_STORE_F32) {
+    epi.out_f32 = static_cast<float*>(out);
+    epi.ld_out = N;
+  } else if (epi_kind == EPI_STORE_BF16) {
+    epi.out_bf16 = static_cast<__nv_bfloat16*>(out);
+    epi.ld_bf16 = N;
+  } else if (epi_kind == EPI_SWIGLU) {
+    epi.out_bf16 = static_cast<__nv_bfloat16*>(out);
+    epi.ld_bf16 = N / 2;
+  } else if (epi_kind == EPI_RESID) {
+    epi.resid = resid;
+    epi.gain = static_cast<const __nv_bfloat16*>(gain);
+    epi.xg = static_cast<__nv_bfloat16*>(xg);
+    epi.ssq_out = ssq_out;
+  }
+  cudaError_t e = gemm_bf16_launch(tw, tx, M, N, K, splits, ws, epi, st);
+  if (splits > 1) {
+    cudaFreeAsync(ws.partials, st);
+    cudaFreeAsync(ws.counters, st);
+  }
+  return cuda_status(e);
+}

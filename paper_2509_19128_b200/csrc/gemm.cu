@@ -1,0 +1,347 @@
+// gemm.cu -- warp-specialised tcgen05 GEMM for sm_100a with fused epilogues.
+//
+// One CTA = 4 warps computes a [128 weight rows x TOK tokens] fp32 tile in
+// TMEM.  warp0/elected lane streams W and X k-blocks with TMA into a STAGES-
+// deep 128B-swizzled ring; warp1/elected lane issues tcgen05.mma (UMMA
+// 128 x TOK x 16) and releases ring slots with tcgen05.commit; afterwards all
+// four warps drain TMEM (tcgen05.ld 32x32b) into a shared tile and run the
+// epilogue.  Skinny decode GEMMs use a deterministic split-K: every split
+// stores its partial tile, the last-arriving CTA sums the partials in split
+// order (so results are bit-reproducible run to run) and runs the epilogue.
+#include <cstdio>
+#include <cstring>
+#include <cstdlib>
+#include <mutex>
+
+#include "gemm.cuh"
+#include "sm100.cuh"
+
+namespace srl {
+using namespace sm100;
+
+namespace {
+
+constexpr int kBlockN = 128;  // weight rows per tile (UMMA M)
+constexpr int kBlockK = 64;   // bf16 elements per 128-B swizzle row
+constexpr int kThreads = 128;
+
+template <int TOK, int STAGES>
+struct Layout {
+  static constexpr int kABytes = kBlockN * kBlockK * 2;
+  static constexpr int kBBytes = TOK * kBlockK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kPitch = kBlockN + 4;
+  static constexpr int kEpiBytes = TOK * kPitch * 4;
+  static constexpr int kMainBytes =
+      STAGES * kStageBytes > kEpiBytes ? STAGES * kStageBytes : kEpiBytes;
+  static constexpr int kBarOffset = kMainBytes;
+  static constexpr int kMiscOffset = kBarOffset + (2 * STAGES + 1) * 8;
+  static constexpr int kRstdOffset = kMiscOffset + 16;
+  static constexpr int kTotal = kRstdOffset + TOK * 4;
+  static constexpr int kAlloc = kTotal + 1024;  // manual 1024-B alignment slack
+};
+
+__device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int TOK, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
+                     int M, int N, int K, int splits, int kb_per_split, float* __restrict__ ws,
+                     int* __restrict__ counters, const EpiParams epi) {
+  using L = Layout<TOK, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kMiscOffset);
+  int* s_flag = reinterpret_cast<int*>(smem + L::kMiscOffset + 4);
+  float* s_rstd = reinterpret_cast<float*>(smem + L::kRstdOffset);
+  float* tile = reinterpret_cast<float*>(smem);  // epilogue view, aliases the ring
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tile = blockIdx.x, split = blockIdx.y, tok_tile = blockIdx.z;
+  const int n_tiles = gridDim.x;
+  const int tile_id = tok_tile * n_tiles + n_tile;
+  const int n0 = n_tile * kBlockN, t0 = tok_tile * TOK;
+  const int kb_total = K / kBlockK;
+  const int kb_begin = split * kb_per_split;
+  const int kb_end = min(kb_total, kb_begin + kb_per_split);
+  const int nkb = kb_end - kb_begin;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tw);
+      tma_prefetch_desc(&tx);
+    }
+    __syncwarp();
+    tmem_alloc<TOK>(tmem_slot);
+  } else if (warp == 1) {
+    if (elect_one()) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      mbar_init(done, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {  // ---- TMA producer
+      const uint64_t w_policy = policy_evict_first();
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* a = smem + s * L::kStageBytes;
+        uint8_t* b = a + L::kABytes;
+        mbar_arrive_expect_tx(&full[s], L::kStageBytes);
+        const int kc = (kb_begin + i) * kBlockK;
+        tma_load_2d_hint(a, &tw, &full[s], kc, n0, w_policy);
+        tma_load_2d(b, &tx, &full[s], kc, t0);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {  // ---- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16_f32(128, TOK);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t a = smem_u32(smem + s * L::kStageBytes);
+        const uint32_t b = a + L::kABytes;
+#pragma unroll
+        for (int kk = 0; kk < kBlockK / 16; ++kk)
+          mma_bf16_ss(tmem, umma_desc_k_sw128(a, kk * 32), umma_desc_k_sw128(b, kk * 32), idesc,
+                      (i | kk) != 0);
+        mma_commit(&empty[s]);
+      }
+      mma_commit(done);
+    }
+    __syncwarp();
+  }
+
+  // ---- drain TMEM: thread = weight row (TMEM lane), columns = tokens
+  mbar_wait(done, 0);
+  tc_fence_after();
+  const int row = threadIdx.x;
+  const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+  const size_t tiles_total = (size_t)n_tiles * gridDim.z;
+  if (splits == 1) {
+#pragma unroll
+    for (int c0 = 0; c0 < TOK; c0 += 16) {
+      uint32_t r[16];
+      tmem_ld_32x32b_x16(lane_addr + c0, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) tile[(c0 + j) * L::kPitch + row] = __uint_as_float(r[j]);
+    }
+  } else {
+    float* mine = ws + ((size_t)split * tiles_total + tile_id) * (size_t)(TOK * kBlockN);
+#pragma unroll
+    for (int c0 = 0; c0 < TOK; c0 += 16) {
+      uint32_t r[16];
+      tmem_ld_32x32b_x16(lane_addr + c0, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) __stcg(&mine[(c0 + j) * kBlockN + row], __uint_as_float(r[j]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_free<TOK>(tmem);
+
+  if (splits > 1) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) *s_flag = (atomicAdd(&counters[tile_id], 1) == splits - 1);
+    __syncthreads();
+    if (!*s_flag) return;
+    __threadfence();
+    for (int j = 0; j < TOK; ++j) {
+      float acc = 0.f;
+      for (int s = 0; s < splits; ++s)
+        acc += __ldcg(&ws[(((size_t)s * tiles_total + tile_id) * TOK + j) * kBlockN + row]);
+      tile[j * L::kPitch + row] = acc;
+    }
+    if (threadIdx.x == 0) counters[tile_id] = 0;  // self-reset for the next launch / graph replay
+  }
+
+  // ---- epilogue
+  for (int j = threadIdx.x; j < TOK; j += kThreads) {
+    float r = 1.f;
+    const int m = t0 + j;
+    if (epi.ssq_in != nullptr && m < M) {
+      float s = 0.f;
+      for (int p = 0; p < epi.ssq_in_parts; ++p) s += epi.ssq_in[(size_t)m * epi.ssq_in_parts + p];
+      r = rsqrtf(s * epi.inv_dim + epi.eps);
+    }
+    s_rstd[j] = r;
+  }
+  __syncthreads();
+
+  if (epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16) {
+    for (int idx = threadIdx.x; idx < TOK * kBlockN; idx += kThreads) {
+      const int j = idx >> 7, c = idx & 127;
+      const int m = t0 + j, n = n0 + c;
+      if (m >= M || n >= N) continue;
+      float v = tile[j * L::kPitch + c] * s_rstd[j];
+      if (epi.bias) v += bf2f(epi.bias[n]);
+      if (epi.kind == EPI_STORE_F32)
+        epi.out_f32[(size_t)m * epi.ld_out + n] = v;
+      else
+        epi.out_bf16[(size_t)m * epi.ld_bf16 + n] = __float2bfloat16(v);
+    }
+  } else if (epi.kind == EPI_SWIGLU) {
+    for (int idx = threadIdx.x; idx < TOK * (kBlockN / 2); idx += kThreads) {
+      const int j = idx >> 6, c = idx & 63;
+      const int m = t0 + j;
+      if (m >= M || n0 + c >= N) continue;
+      const float g = tile[j * L::kPitch + c] * s_rstd[j];
+      const float u = tile[j * L::kPitch + 64 + c] * s_rstd[j];
+      const float a = g / (1.f + expf(-g)) * u;
+      epi.out_bf16[(size_t)m * epi.ld_bf16 + (n0 >> 1) + c] = __float2bfloat16(a);
+    }
+  } else if (epi.kind == EPI_RESID) {
+    for (int idx = threadIdx.x; idx < TOK * kBlockN; idx += kThreads) {
+      const int j = idx >> 7, c = idx & 127;
+      const int m = t0 + j, n = n0 + c;
+      float x = 0.f;
+      if (m < M && n < N) {
+        const size_t o = (size_t)m * N + n;
+        x = epi.resid[o] + tile[j * L::kPitch + c];
+        epi.resid[o] = x;
+        epi.xg[o] = __float2bfloat16(x * bf2f(epi.gain[n]));
+      }
+      tile[j * L::kPitch + c] = x;
+    }
+    __syncthreads();
+    for (int j = warp; j < TOK; j += kThreads / 32) {
+      float s = 0.f;
+      for (int c = lane; c < kBlockN; c += 32) {
+        const float x = tile[j * L::kPitch + c];
+        s += x * x;
+      }
+      s = warp_sum(s);
+      if (lane == 0 && t0 + j < M) epi.ssq_out[(size_t)(t0 + j) * n_tiles + n_tile] = s;
+    }
+  }
+}
+
+template <int TOK, int STAGES>
+cudaError_t launch_impl(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K,
+                        int splits, const GemmWorkspace& ws, const EpiParams& epi,
+                        cudaStream_t stream) {
+  using L = Layout<TOK, STAGES>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(gemm_bf16_kernel<TOK, STAGES>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const int kb = K / kBlockK;
+  const int kb_per = (kb + splits - 1) / splits;
+  const int eff_splits = (kb + kb_per - 1) / kb_per;
+  const int n_tiles = (N + kBlockN - 1) / kBlockN;
+  const int tok_tiles = (M + TOK - 1) / TOK;
+  if (eff_splits > 1) {
+    const size_t need = (size_t)eff_splits * n_tiles * tok_tiles * TOK * kBlockN;
+    if (ws.partials == nullptr || need > ws.partial_floats ||
+        ws.counter_count < n_tiles * tok_tiles)
+      return cudaErrorInvalidValue;
+  }
+  dim3 grid(n_tiles, eff_splits, tok_tiles);
+  gemm_bf16_kernel<TOK, STAGES><<<grid, kThreads, L::kAlloc, stream>>>(
+      tw, tx, M, N, K, eff_splits, kb_per, ws.partials, ws.counters, epi);
+  return cudaGetLastError();
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeFn>(nullptr);
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+}  // namespace
+
+CUtensorMap make_tmap_bf16(const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  EncodeFn enc = get_encode();
+  if (enc == nullptr) {
+    std::fprintf(stderr, "srl: cuTensorMapEncodeTiled unavailable\n");
+    std::abort();
+  }
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    std::fprintf(stderr, "srl: cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu\n", (int)r,
+                 (unsigned long long)rows, (unsigned long long)cols);
+    std::abort();
+  }
+  return m;
+}
+
+int gemm_tok_tile(int M) { return M <= 64 ? 64 : 128; }
+
+int gemm_auto_splits(int M, int N, int K, int num_sms) {
+  const int tok = gemm_tok_tile(M);
+  const int tiles = ((N + kBlockN - 1) / kBlockN) * ((M + tok - 1) / tok);
+  const int kb = K / kBlockK;
+  if (tiles >= num_sms || kb < 4) return 1;
+  int want = (2 * num_sms + tiles - 1) / tiles;
+  int cap = kb / 2;  // at least two k-blocks per split
+  int s = want < cap ? want : cap;
+  return s < 1 ? 1 : s;
+}
+
+size_t gemm_workspace_floats(int M, int N, int splits) {
+  const int tok = gemm_tok_tile(M);
+  return (size_t)splits * ((N + kBlockN - 1) / kBlockN) * ((M + tok - 1) / tok) * tok * kBlockN;
+}
+
+cudaError_t gemm_bf16_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K,
+                             int splits, const GemmWorkspace& ws, const EpiParams& epi,
+                             cudaStream_t stream) {
+  if (M < 1 || N < 1 || K < kBlockK || K % kBlockK != 0 || splits < 1)
+    return cudaErrorInvalidValue;
+  if (epi.kind == EPI_SWIGLU && N % kBlockN != 0) return cudaErrorInvalidValue;
+  if (gemm_tok_tile(M) == 64) return launch_impl<64, 4>(tw, tx, M, N, K, splits, ws, epi, stream);
+  return launch_impl<128, 4>(tw, tx, M, N, K, splits, ws, epi, stream);
+}
+
+}  // namespace srl

@@ -1,0 +1,65 @@
+// gemm.cuh -- host-visible interface of the tcgen05 GEMM used by every
+// projection of the decoder policy (QKV, O, gate/up, down, LM head).
+//
+//   Y[m, n] = epilogue( sum_k X[m, k] * W[n, k] )       X: [M x K] bf16 (tokens)
+//                                                       W: [N x K] bf16 (weights)
+// The kernel is "swap-AB": weight rows fill the UMMA M=128 dimension and the
+// token rows are the UMMA N (64 or 128), so a decode batch of 64 tokens still
+// issues full-height tensor-core tiles while the weights stream from HBM.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace srl {
+
+enum EpiKind : int {
+  EPI_STORE_F32 = 0,   // out_f32[m, n] = rstd[m] * acc (+ bias[n])
+  EPI_RESID = 1,       // resid[m, n] += acc; xg[m, n] = bf16(resid * gain[n]); ssq partials
+  EPI_SWIGLU = 2,      // tile = 64 gate | 64 up rows: act[m, j] = bf16(silu(g) * u), g,u scaled by rstd
+  EPI_STORE_BF16 = 3,  // out_bf16[m, n] = bf16(rstd[m] * acc (+ bias[n]))
+};
+
+struct EpiParams {
+  int kind = EPI_STORE_F32;
+  // Deferred RMSNorm: rstd[m] = rsqrt(sum_p ssq_in[m * ssq_in_parts + p] * inv_dim + eps).
+  const float* ssq_in = nullptr;
+  int ssq_in_parts = 0;
+  float inv_dim = 0.f;
+  float eps = 0.f;
+  const __nv_bfloat16* bias = nullptr;  // [N]
+  float* out_f32 = nullptr;
+  int ld_out = 0;
+  __nv_bfloat16* out_bf16 = nullptr;
+  int ld_bf16 = 0;
+  // EPI_RESID
+  float* resid = nullptr;               // [M x N] fp32, ld = N
+  const __nv_bfloat16* gain = nullptr;  // next RMSNorm gain [N]
+  __nv_bfloat16* xg = nullptr;          // [M x N] bf16
+  float* ssq_out = nullptr;             // [M x ceil(N/128)]
+};
+
+// Build a 2-D bf16 TMA descriptor for a row-major [rows x cols] matrix with a
+// box of [box_rows x 64] elements and 128-B swizzle (the UMMA K-major layout).
+CUtensorMap make_tmap_bf16(const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+
+struct GemmWorkspace {
+  float* partials = nullptr;  // split-K partial tiles
+  size_t partial_floats = 0;
+  int* counters = nullptr;    // per output tile arrival counters (self-resetting)
+  int counter_count = 0;
+};
+
+// Number of output tiles the kernel will use for (M, N); tok_tile is 64 or 128.
+int gemm_tok_tile(int M);
+// Choose a split-K factor that fills the machine for skinny (decode) GEMMs.
+int gemm_auto_splits(int M, int N, int K, int num_sms);
+size_t gemm_workspace_floats(int M, int N, int splits);
+
+// Launch.  tw: W [N x K] (box 128 rows); tx: X [>=M x K] (box gemm_tok_tile(M) rows).
+cudaError_t gemm_bf16_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K,
+                             int splits, const GemmWorkspace& ws, const EpiParams& epi,
+                             cudaStream_t stream);
+
+}  // namespace srl

@@ -1,0 +1,90 @@
+"""tcgen05 GEMM kernel vs a torch fp32 reference (floating-point kernel: the
+one place a torch reference is used).  Tolerance: fp32 accumulation of bf16
+products, rel 2e-3 of the output scale."""
+import pytest
+import torch
+
+from paper_2509_19128_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+EPI_F32, EPI_RESID, EPI_SWIGLU, EPI_BF16 = 0, 1, 2, 3
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def run(w, x, kind, splits=0, bias=None, ssq=None, parts=0, inv_dim=0.0, eps=0.0, out=None,
+        resid=None, gain=None, xg=None, ssq_out=None):
+    M, K = x.shape
+    N = w.shape[0]
+    _lib.call("srl_kernel_gemm_bf16", ptr(w), ptr(x), M, N, K, splits, kind, ptr(bias), ptr(ssq),
+              parts, inv_dim, eps, ptr(out), ptr(resid), ptr(gain), ptr(xg), ptr(ssq_out), None)
+    torch.cuda.synchronize()
+
+
+def close(a, b, tol=2e-3):
+    scale = b.abs().max().item() + 1e-6
+    err = (a.float() - b.float()).abs().max().item()
+    assert err <= tol * scale, f"max err {err} vs scale {scale}"
+
+
+@pytest.mark.parametrize("M,N,K,splits", [(64, 256, 128, 1), (64, 1152, 896, 0), (64, 896, 4864, 0),
+                                          (37, 384, 256, 1), (200, 512, 512, 1), (64, 300, 192, 2),
+                                          (1, 128, 64, 1), (256, 1024, 896, 0)])
+def test_gemm_store_f32(cuda, M, N, K, splits):
+    g = torch.Generator(device=cuda).manual_seed(M * 7 + N)
+    w = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+    x = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    bias = torch.randn(N, device=cuda, generator=g).bfloat16()
+    out = torch.full((M, N), float("nan"), device=cuda)
+    run(w, x, EPI_F32, splits=splits, bias=bias, out=out)
+    ref = x.float() @ w.float().T + bias.float()
+    close(out, ref)
+
+
+def test_gemm_deterministic_splitk(cuda):
+    M, N, K = 64, 1152, 896
+    w = torch.randn(N, K, device=cuda).bfloat16()
+    x = torch.randn(M, K, device=cuda).bfloat16()
+    outs = []
+    for _ in range(3):
+        out = torch.empty(M, N, device=cuda)
+        run(w, x, EPI_F32, splits=7, out=out)
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
+def test_gemm_rmsnorm_scale_and_swiglu(cuda):
+    M, N, K = 64, 1024, 256
+    w = torch.randn(N, K, device=cuda).bfloat16()
+    x = torch.randn(M, K, device=cuda).bfloat16()
+    parts = 2
+    ssq = torch.rand(M, parts, device=cuda) * 50 + 1
+    eps = 1e-6
+    out = torch.empty(M, N // 2, device=cuda, dtype=torch.bfloat16)
+    run(w, x, EPI_SWIGLU, splits=0, ssq=ssq, parts=parts, inv_dim=1.0 / K, eps=eps, out=out)
+    rstd = torch.rsqrt(ssq.sum(1, keepdim=True) / K + eps)
+    y = (x.float() @ w.float().T) * rstd
+    y = y.view(M, N // 128, 2, 64)
+    gte, up = y[:, :, 0, :].reshape(M, -1), y[:, :, 1, :].reshape(M, -1)
+    ref = torch.nn.functional.silu(gte) * up
+    close(out, ref, tol=1e-2)
+
+
+def test_gemm_residual_epilogue(cuda):
+    M, N, K = 64, 896, 896
+    w = torch.randn(N, K, device=cuda).bfloat16()
+    x = torch.randn(M, K, device=cuda).bfloat16()
+    resid = torch.randn(M, N, device=cuda)
+    resid0 = resid.clone()
+    gain = (torch.rand(N, device=cuda) + 0.5).bfloat16()
+    xg = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    ssq = torch.empty(M, 7, device=cuda)
+    run(w, x, EPI_RESID, splits=0, resid=resid, gain=gain, xg=xg, ssq_out=ssq)
+    ref = resid0 + x.float() @ w.float().T
+    close(resid, ref)
+    close(xg, ref * gain.float(), tol=1e-2)
+    ref_ssq = (ref.view(M, 7, 128) ** 2).sum(-1)
+    close(ssq, ref_ssq, tol=3e-3)
