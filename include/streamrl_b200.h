@@ -42,6 +42,182 @@ const char* srl_status_string(int status);
 /* Thread-local human-readable detail of the last failure in this thread. */
 const char* srl_last_error(void);
 
+/* ------------------------------------------------------- policies --- */
+/* A policy checkpoint (the reference `rlmath::Policy` variant,
+ * include/streamrl/policy.hpp:16-82).  Tabular and recurrent policies keep
+ * the reference's fp64 semantics on the device; the decoder policy is the
+ * Qwen2.5-shaped bf16 transformer this framework adds as a third variant of
+ * the same "streamrl.policy/1" document schema (type "decoder"). */
+typedef struct srl_policy srl_policy;
+
+enum { SRL_POLICY_TABULAR = 0, SRL_POLICY_RECURRENT = 1, SRL_POLICY_DECODER = 2 };
+
+/* TabularPolicy (policy.hpp:16-47).  Rows are (prompt id, context window)
+ * keys; row_contexts is [n_rows x context_order], only the first
+ * row_context_lens[r] entries of a row are meaningful.  default_logits may be
+ * NULL (uniform fallback, policy.cpp:62-64). */
+int srl_policy_tabular_create(int32_t vocab_size, int32_t context_order,
+                              const double* default_logits, int32_t n_rows,
+                              const char* const* row_prompt_ids, const int32_t* row_context_lens,
+                              const int32_t* row_contexts, const double* row_logits,
+                              srl_policy** out);
+/* RecurrentToyPolicy (policy.hpp:52-72): row-major fp64 matrices
+ * input_embedding [V x D], recurrence [D x D], output [D x V]. */
+int srl_policy_recurrent_create(int32_t vocab_size, int32_t hidden_dim,
+                                const double* input_embedding, const double* recurrence,
+                                const double* output, srl_policy** out);
+
+/* Decoder policy shape (Qwen2.5 family: RMSNorm, RoPE, GQA, SwiGLU, QKV bias). */
+typedef struct {
+  int32_t vocab_size;
+  int32_t hidden;
+  int32_t layers;
+  int32_t q_heads;
+  int32_t kv_heads;
+  int32_t head_dim;       /* 64 or 128 */
+  int32_t intermediate;
+  int32_t tie_embeddings; /* LM head = embedding matrix */
+  int32_t bos_token;      /* prepended to every stream's prompt */
+  int32_t max_positions;  /* RoPE table length = max KV length per stream */
+  double rope_theta;
+  double rms_eps;
+} srl_decoder_config;
+
+/* Random-init decoder weights on `device` (counter-based SplitMix64
+ * Box-Muller, scale * N(0,1); norm gains 1).  Weights live in one flat bf16
+ * buffer (layout: DESIGN.md "Data layout"). */
+int srl_policy_decoder_create(const srl_decoder_config* cfg, uint64_t init_seed,
+                              double init_scale, int32_t device, srl_policy** out);
+/* Decoder policy from an existing flat bf16 buffer (host or device), copied. */
+int srl_policy_decoder_from_buffer(const srl_decoder_config* cfg, const void* weights,
+                                   size_t nbytes, int32_t weights_on_device, int32_t device,
+                                   srl_policy** out);
+/* Size in bytes of the flat bf16 weight buffer for cfg. */
+size_t srl_decoder_weight_bytes(const srl_decoder_config* cfg);
+/* Device pointer + size of a decoder policy's flat weights (owned by it). */
+int srl_policy_decoder_weights(const srl_policy* p, void** device_ptr, size_t* nbytes);
+/* Element offset (bf16 elements) of a named tensor: "embed", "final_norm",
+ * "lm_head", or "<layer>.<ln1|qkv_w|qkv_b|o_w|ln2|gate_up_w|down_w>". */
+int srl_policy_decoder_offset(const srl_policy* p, const char* name, size_t* offset);
+/* In-place drift w += magnitude * N(0,1) (a stand-in trainer step for
+ * benchmarks; the real trainer path is srl_trainer_*). */
+int srl_policy_decoder_perturb(srl_policy* p, uint64_t seed, double magnitude);
+int srl_policy_type(const srl_policy* p);
+int32_t srl_policy_vocab_size(const srl_policy* p);
+/* validate() (policy.cpp:30-43, 71-82); SRL_INVALID_POLICY with detail. */
+int srl_policy_validate(const srl_policy* p);
+void srl_policy_destroy(srl_policy* p);
+
+/* -------------------------------------------------- generator engine --- */
+/* proto::Engine (include/streamrl/engine.hpp:44-109, src/engine.cpp). */
+typedef struct srl_engine srl_engine;
+
+typedef struct {
+  int32_t max_streams;     /* device stream slots = constant generation batch H */
+  int32_t max_seq_len;     /* KV capacity per stream (bos + prompt + generated) */
+  int32_t greedy;          /* 1: argmax decoding (lowest index on ties) */
+  int32_t rounds_per_sync; /* free-running rounds launched per host sync (>= 1) */
+  int32_t use_graphs;      /* capture decode rounds in CUDA graphs */
+  int32_t device;
+  int32_t event_ring;      /* device event ring depth in rounds (>= rounds_per_sync) */
+  int32_t prefill_budget;  /* max prompt tokens prefilled per round */
+} srl_engine_options;
+
+/* TokenEvent (engine.hpp:22-28); stream id "s<N>" is numeric N here. */
+typedef struct {
+  int64_t stream;
+  int32_t position;
+  int32_t token;
+  double logprob;
+  int32_t weight_version;
+  int32_t reserved;
+} srl_token_event;
+
+/* FinishReason (engine.hpp:30) */
+enum { SRL_FINISH_RUNNING = 0, SRL_FINISH_LENGTH = 1, SRL_FINISH_TERMINATOR = 2,
+       SRL_FINISH_SHUTDOWN = 3 };
+
+/* Engine(Options{policy, recompute_state, start_paused}) (engine.cpp:38-42).
+ * The engine copies the policy; opts may be NULL for defaults. */
+int srl_engine_create(const srl_policy* policy, int32_t recompute_state, int32_t start_paused,
+                      const srl_engine_options* opts, srl_engine** out);
+void srl_engine_destroy(srl_engine* e);
+/* open_stream (engine.cpp:46-61): prompt tokens are used by decoder policies
+ * (bos is prepended); SRL_INVALID_ARGUMENT if max_tokens < 1. */
+int srl_engine_open_stream(srl_engine* e, const char* prompt_id, int32_t max_tokens,
+                           uint64_t seed, int32_t terminator_token, const int32_t* prompt_tokens,
+                           int32_t n_prompt, int64_t* stream_out);
+/* wait_events (engine.cpp:63-77): blocks until >= 1 event or finish, drains
+ * up to cap events; *more = the reference's return value. */
+int srl_engine_wait_events(srl_engine* e, int64_t stream, srl_token_event* buf, int32_t cap,
+                           int32_t* n_out, int32_t* finish_reason, int32_t* more);
+/* apply_weight_update (engine.cpp:79-117).  Returns SRL_VERSION_CONFLICT /
+ * SRL_INVALID_POLICY / SRL_POLICY_MISMATCH without side effects. */
+int srl_engine_apply_weight_update(srl_engine* e, int32_t new_version, const srl_policy* policy,
+                                   int32_t* version_out);
+/* Device-resident update path (decoder): stage new_version, get the standby
+ * weight buffer to receive the broadcast into, then commit (pointer swap at
+ * the next token boundary) or abort.  pause_ms = time the decode stream was
+ * blocked by the swap. */
+int srl_engine_begin_weight_update(srl_engine* e, int32_t new_version, void** standby_device_ptr,
+                                   size_t* nbytes);
+int srl_engine_commit_weight_update(srl_engine* e, int32_t new_version, int32_t* version_out,
+                                    double* pause_ms);
+int srl_engine_abort_weight_update(srl_engine* e);
+/* advance (engine.cpp:174-187): paused engines only (SRL_LOGIC_ERROR). */
+int srl_engine_advance(srl_engine* e, int32_t rounds, int64_t* emitted);
+int srl_engine_pause(srl_engine* e);
+int srl_engine_resume(srl_engine* e);
+int srl_engine_weight_version(const srl_engine* e, int32_t* out);
+int srl_engine_active_streams(const srl_engine* e, int32_t* out);
+int srl_engine_total_streams(const srl_engine* e, int64_t* out);
+int srl_engine_rounds_done(const srl_engine* e, int64_t* out);
+int srl_engine_recompute_state_mode(const srl_engine* e, int32_t* out);
+int srl_engine_set_process_group(srl_engine* e, const char* group_id, const char* const* members,
+                                 int32_t n_members);
+/* *has_group = 0 when no group is set (std::optional empty). */
+int srl_engine_process_group_id(const srl_engine* e, char* buf, size_t cap, int32_t* has_group);
+int srl_engine_stop(srl_engine* e);
+/* Token history of a stream as fed to the KV cache (bos, prompt, generated). */
+int srl_engine_stream_tokens(srl_engine* e, int64_t stream, int32_t* buf, int32_t cap,
+                             int32_t* n_out);
+/* Counters since creation: rounds, tokens, device decode ms, swap pause ms. */
+typedef struct {
+  int64_t rounds;
+  int64_t tokens;
+  int64_t updates;
+  double decode_ms;
+  double last_pause_ms;
+  double max_pause_ms;
+} srl_engine_stats;
+int srl_engine_stats_get(const srl_engine* e, srl_engine_stats* out);
+
+/* ------------------------------------------------------ trainer math --- */
+/* rlmath free functions (include/streamrl/rl_math.hpp:20-121). */
+
+/* policy_logprobs (rl_math.cpp:128-142), computed on the device. */
+int srl_policy_logprobs(const srl_policy* p, const char* prompt_id, const int32_t* tokens,
+                        int32_t n, double* out);
+/* truncated_is_weight (rl_math.cpp:144-150). */
+int srl_truncated_is_weight(double pi_logprob_sum, double mu_logprob_sum, double clamp,
+                            double* out);
+/* ess (rl_math.cpp:152-163): SRL_ESS_UNDEFINED when all weights are zero. */
+int srl_ess(const double* weights, int32_t n, double* out);
+
+/* ---------------------------------------------------------------- lag --- */
+/* Per consumed batch lag statistics on the device (sim.cpp:63-110):
+ * lag = version_before - token_version; hist must hold hist_cap counters.
+ * versions are packed per sequence (device pointers); seq_offsets has
+ * n_seq + 1 entries.  totals = {tokens, lag_sum, max_lag}. */
+int srl_lag_stats(const int32_t* versions, const int64_t* seq_offsets, int32_t n_seq,
+                  int32_t version_before, int64_t* hist, int32_t hist_cap, int64_t* seq_lag_sums,
+                  int64_t* totals, void* stream);
+
+/* --------------------------------------------------------- protocol --- */
+/* crc32 (engine.cpp:257-274) and process_group_id (engine.cpp:276-291). */
+uint32_t srl_crc32(const void* bytes, size_t n);
+int srl_process_group_id(const char* const* members, int32_t n_members, char* buf, size_t cap);
+
 /* ------------------------------------------------ kernel entry points --- */
 /* Single-kernel entry points over device pointers, used by the parity tests
  * and bench.py.  `stream` is a cudaStream_t (NULL = legacy default). */
@@ -55,6 +231,14 @@ int srl_kernel_gemm_bf16(const void* w, const void* x, int32_t M, int32_t N, int
                          const float* ssq_in, int32_t ssq_parts, float inv_dim, float eps,
                          void* out, float* resid, const void* gain, void* xg, float* ssq_out,
                          void* stream);
+
+/* The decode sampler on raw fp32 logits rows (device pointers): row r uses
+ * draw #draw_index[r] of SplitMix64(seeds[r]) (rng.hpp:18-28) and the
+ * inverse CDF of exp(log_softmax) in fp64 (rng.hpp:61-69, engine.cpp:130-138);
+ * greedy = argmax, lowest index on ties.  Writes token and log-prob. */
+int srl_kernel_sample_logits(const float* logits, int32_t vocab, int32_t rows,
+                             const uint64_t* seeds, const int32_t* draw_index, int32_t greedy,
+                             int32_t* tokens_out, double* logprobs_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,193 @@
+"""CPU restatement of the decoder policy (numpy).  TEST INFRASTRUCTURE ONLY.
+
+The reference has no transformer: its "policy model" is
+a tabular or 1-layer tanh RNN policy walked by PolicyWalker
+(/root/reference/proj/core/src/rl_math.cpp:27-82).  This module restates the
+decoder policy this framework adds -- Qwen2.5-shaped, bf16 weights -- with the
+PolicyWalker contract: per-position log-probabilities in the log domain,
+state (the KV cache) carried across checkpoint switches, stale or recomputed
+after a switch (rl_math.cpp:64-73, engine.cpp:103-113).
+
+It rounds to bf16 at exactly the points the device path does (normalised
+activations, q/k/v, attention output, SwiGLU output) and accumulates every
+dot product in fp64, so GPU-vs-oracle differences come only from fp32
+accumulation order.  Parity for the transformer layers is NOT pinned by the
+reference (there is none); it is pinned by central finite differences of
+the backward pass (tests/test_decoder_oracle.py) and by the teacher-forced
+parity tests against the device path.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def bf16_round(x):
+    """Round-to-nearest-even to bfloat16, returned as float32."""
+    a = np.ascontiguousarray(x, dtype=np.float32)
+    b = a.view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    return b.astype(np.uint32).view(np.float32).reshape(a.shape)
+
+
+def bf16_bits_to_f32(u16):
+    return (np.asarray(u16, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def layout(cfg):
+    """Element offsets of the flat weight buffer (csrc/decoder.cu make_layout)."""
+    H, V, L = cfg["hidden"], cfg["vocab_size"], cfg["layers"]
+    nq, nkv, hd, I = cfg["q_heads"], cfg["kv_heads"], cfg["head_dim"], cfg["intermediate"]
+    qkv = (nq + 2 * nkv) * hd
+    cur = 0
+    off = {}
+
+    def take(name, n):
+        nonlocal cur
+        off[name] = (cur, n)
+        cur += (n + 63) // 64 * 64
+
+    take("embed", V * H)
+    for l in range(L):
+        take(f"{l}.ln1", H)
+        take(f"{l}.qkv_w", qkv * H)
+        take(f"{l}.qkv_b", qkv)
+        take(f"{l}.o_w", H * nq * hd)
+        take(f"{l}.ln2", H)
+        take(f"{l}.gate_up_w", 2 * I * H)
+        take(f"{l}.down_w", H * I)
+    take("final_norm", H)
+    if cfg["tie_embeddings"]:
+        off["lm_head"] = off["embed"]
+    else:
+        take("lm_head", V * H)
+    return off, cur
+
+
+class DecoderOracle:
+    """fp64-accumulating decoder forward with a per-stream KV cache."""
+
+    def __init__(self, cfg: dict, weights_u16: np.ndarray, dtype=np.float64):
+        self.cfg = cfg
+        self.dtype = dtype
+        self.off, total = layout(cfg)
+        w = np.asarray(weights_u16)
+        if w.size < total:
+            raise ValueError("weight buffer smaller than the layout")
+        self.w = {}
+        H, I = cfg["hidden"], cfg["intermediate"]
+        nq, nkv, hd = cfg["q_heads"], cfg["kv_heads"], cfg["head_dim"]
+        qkv = (nq + 2 * nkv) * hd
+        shapes = {"embed": (cfg["vocab_size"], H), "lm_head": (cfg["vocab_size"], H),
+                  "final_norm": (H,)}
+        for l in range(cfg["layers"]):
+            shapes.update({f"{l}.ln1": (H,), f"{l}.qkv_w": (qkv, H), f"{l}.qkv_b": (qkv,),
+                           f"{l}.o_w": (H, nq * hd), f"{l}.ln2": (H,),
+                           f"{l}.gate_up_w": (2 * I, H), f"{l}.down_w": (H, I)})
+        for name, (o, n) in self.off.items():
+            self.w[name] = bf16_bits_to_f32(w[o:o + n]).reshape(shapes[name]).astype(dtype)
+        half = hd // 2
+        self.inv_freq = cfg["rope_theta"] ** (-2.0 * np.arange(half) / hd)
+        self.scale = np.float32(1.0 / math.sqrt(hd))
+
+    # ------------------------------------------------------------ pieces
+    def _rstd(self, x):
+        ssq = (x.astype(np.float64) ** 2).sum(-1)
+        return 1.0 / np.sqrt(ssq / self.cfg["hidden"] + self.cfg["rms_eps"])
+
+    def _xg(self, x, gain):
+        return bf16_round(x.astype(np.float32) * gain.astype(np.float32)).astype(self.dtype)
+
+    def _rope(self, x, pos):
+        """x: [..., hd] fp32 values at integer position pos (scalar or [rows])."""
+        hd = self.cfg["head_dim"]
+        half = hd // 2
+        ang = np.asarray(pos, dtype=np.float64)[..., None] * self.inv_freq
+        c = np.cos(ang).astype(np.float32)
+        s = np.sin(ang).astype(np.float32)
+        while c.ndim < x.ndim:
+            c, s = c[..., None, :], s[..., None, :]
+        x1, x2 = x[..., :half].astype(np.float32), x[..., half:].astype(np.float32)
+        return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+
+    def new_cache(self):
+        L = self.cfg["layers"]
+        return {"k": [[] for _ in range(L)], "v": [[] for _ in range(L)], "tokens": []}
+
+    # ------------------------------------------------------------- step
+    def step(self, caches, tokens, positions):
+        """Feed one token per stream (rows), append K/V, return fp64 logits [rows x V]."""
+        cfg, w = self.cfg, self.w
+        H, I = cfg["hidden"], cfg["intermediate"]
+        nq, nkv, hd = cfg["q_heads"], cfg["kv_heads"], cfg["head_dim"]
+        G = nq // nkv
+        tokens = np.asarray(tokens)
+        rows = len(tokens)
+        x = w["embed"][tokens].astype(np.float32)  # fp32 residual stream
+        xg = self._xg(x, w["0.ln1"])
+        rstd = self._rstd(x)
+        for l in range(cfg["layers"]):
+            qkv = (xg @ w[f"{l}.qkv_w"].T) * rstd[:, None] + w[f"{l}.qkv_b"]
+            qkv = qkv.astype(np.float32)
+            q = qkv[:, :nq * hd].reshape(rows, nq, hd)
+            k = qkv[:, nq * hd:(nq + nkv) * hd].reshape(rows, nkv, hd)
+            v = qkv[:, (nq + nkv) * hd:].reshape(rows, nkv, hd)
+            q = bf16_round(self._rope(q, positions))
+            k = bf16_round(self._rope(k, positions))
+            v = bf16_round(v)
+            attn = np.zeros((rows, nq, hd), dtype=np.float64)
+            for r in range(rows):
+                c = caches[r]
+                c["k"][l].append(k[r])
+                c["v"][l].append(v[r])
+                K = np.stack(c["k"][l]).astype(np.float64)  # [T, nkv, hd]
+                Vv = np.stack(c["v"][l]).astype(np.float64)
+                qs = (q[r].astype(np.float32) * self.scale).astype(np.float64)  # [nq, hd]
+                for h in range(nq):
+                    kh = h // G
+                    s = K[:, kh, :] @ qs[h]
+                    p = np.exp(s - s.max())
+                    attn[r, h] = (p @ Vv[:, kh, :]) / p.sum()
+            attn = bf16_round(attn.reshape(rows, nq * hd)).astype(self.dtype)
+            x = (x + attn @ w[f"{l}.o_w"].T).astype(np.float32)
+            xg = self._xg(x, w[f"{l}.ln2"])
+            rstd = self._rstd(x)
+            gu = (xg @ w[f"{l}.gate_up_w"].T) * rstd[:, None]
+            gu = gu.reshape(rows, I // 64, 2, 64)
+            g, u = gu[:, :, 0, :].reshape(rows, I), gu[:, :, 1, :].reshape(rows, I)
+            g32, u32 = g.astype(np.float32), u.astype(np.float32)
+            act = bf16_round(g32 / (np.float32(1) + np.exp(-g32)) * u32).astype(self.dtype)
+            x = (x + act @ w[f"{l}.down_w"].T).astype(np.float32)
+            nxt = w[f"{l + 1}.ln1"] if l + 1 < cfg["layers"] else w["final_norm"]
+            xg = self._xg(x, nxt)
+            rstd = self._rstd(x)
+        for r in range(rows):
+            caches[r]["tokens"].append(int(tokens[r]))
+        return (xg @ w["lm_head"].T) * rstd[:, None]
+
+    def prefill(self, cache, tokens):
+        """Feed a whole prefix into one cache; returns logits of every position."""
+        out = []
+        for p, t in enumerate(tokens):
+            out.append(self.step([cache], [t], [len(cache["tokens"])])[0])
+        return np.stack(out) if out else np.zeros((0, self.cfg["vocab_size"]))
+
+    def recompute(self, cache):
+        """Recompute mode: rebuild the cache from its tokens under these weights."""
+        fresh = self.new_cache()
+        self.prefill(fresh, list(cache["tokens"]))
+        cache.update(fresh)
+
+    @staticmethod
+    def log_softmax(logits):
+        m = logits.max(-1, keepdims=True)
+        return logits - (m + np.log(np.exp(logits - m).sum(-1, keepdims=True)))
+
+    def sequence_logprobs(self, tokens):
+        """policy_logprobs (rl_math.cpp:128-142) of tokens after bos."""
+        cache = self.new_cache()
+        inputs = [self.cfg["bos_token"]] + list(tokens[:-1])
+        logits = self.prefill(cache, inputs)
+        lp = self.log_softmax(logits)
+        return lp[np.arange(len(tokens)), tokens]

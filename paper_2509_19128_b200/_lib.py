@@ -36,12 +36,77 @@ def _error_string(status: int) -> str:
     return lib().srl_status_string(status).decode()
 
 
+
+class DecoderConfigC(C.Structure):
+    _fields_ = [("vocab_size", i32), ("hidden", i32), ("layers", i32), ("q_heads", i32),
+                ("kv_heads", i32), ("head_dim", i32), ("intermediate", i32),
+                ("tie_embeddings", i32), ("bos_token", i32), ("max_positions", i32),
+                ("rope_theta", f64), ("rms_eps", f64)]
+
+
+class EngineOptionsC(C.Structure):
+    _fields_ = [("max_streams", i32), ("max_seq_len", i32), ("greedy", i32),
+                ("rounds_per_sync", i32), ("use_graphs", i32), ("device", i32),
+                ("event_ring", i32), ("prefill_budget", i32)]
+
+
+class TokenEventC(C.Structure):
+    _fields_ = [("stream", i64), ("position", i32), ("token", i32), ("logprob", f64),
+                ("weight_version", i32), ("reserved", i32)]
+
+
+class EngineStatsC(C.Structure):
+    _fields_ = [("rounds", i64), ("tokens", i64), ("updates", i64), ("decode_ms", f64),
+                ("last_pause_ms", f64), ("max_pause_ms", f64)]
+
+
+I = C.c_int
 # name -> (restype, argtypes)
 SIGNATURES: dict[str, tuple] = {
-    "srl_status_string": (cp, [C.c_int]),
+    "srl_status_string": (cp, [I]),
     "srl_last_error": (cp, []),
-    "srl_kernel_gemm_bf16": (C.c_int, [vp, vp, i32, i32, i32, i32, i32, vp, vp, i32, f32, f32,
-                                       vp, vp, vp, vp, vp, vp]),
+    "srl_kernel_gemm_bf16": (I, [vp, vp, i32, i32, i32, i32, i32, vp, vp, i32, f32, f32,
+                                 vp, vp, vp, vp, vp, vp]),
+    "srl_policy_tabular_create": (I, [i32, i32, vp, i32, P(cp), vp, vp, vp, P(vp)]),
+    "srl_policy_recurrent_create": (I, [i32, i32, vp, vp, vp, P(vp)]),
+    "srl_policy_decoder_create": (I, [P(DecoderConfigC), u64, f64, i32, P(vp)]),
+    "srl_policy_decoder_from_buffer": (I, [P(DecoderConfigC), vp, sz, i32, i32, P(vp)]),
+    "srl_decoder_weight_bytes": (sz, [P(DecoderConfigC)]),
+    "srl_policy_decoder_weights": (I, [vp, P(vp), P(sz)]),
+    "srl_policy_decoder_offset": (I, [vp, cp, P(sz)]),
+    "srl_policy_decoder_perturb": (I, [vp, u64, f64]),
+    "srl_policy_type": (I, [vp]),
+    "srl_policy_vocab_size": (i32, [vp]),
+    "srl_policy_validate": (I, [vp]),
+    "srl_policy_destroy": (None, [vp]),
+    "srl_engine_create": (I, [vp, i32, i32, P(EngineOptionsC), P(vp)]),
+    "srl_engine_destroy": (None, [vp]),
+    "srl_engine_open_stream": (I, [vp, cp, i32, u64, i32, vp, i32, P(i64)]),
+    "srl_engine_wait_events": (I, [vp, i64, P(TokenEventC), i32, P(i32), P(i32), P(i32)]),
+    "srl_engine_apply_weight_update": (I, [vp, i32, vp, P(i32)]),
+    "srl_engine_begin_weight_update": (I, [vp, i32, P(vp), P(sz)]),
+    "srl_engine_commit_weight_update": (I, [vp, i32, P(i32), P(f64)]),
+    "srl_engine_abort_weight_update": (I, [vp]),
+    "srl_engine_advance": (I, [vp, i32, P(i64)]),
+    "srl_engine_pause": (I, [vp]),
+    "srl_engine_resume": (I, [vp]),
+    "srl_engine_weight_version": (I, [vp, P(i32)]),
+    "srl_engine_active_streams": (I, [vp, P(i32)]),
+    "srl_engine_total_streams": (I, [vp, P(i64)]),
+    "srl_engine_rounds_done": (I, [vp, P(i64)]),
+    "srl_engine_recompute_state_mode": (I, [vp, P(i32)]),
+    "srl_engine_set_process_group": (I, [vp, cp, P(cp), i32]),
+    "srl_engine_process_group_id": (I, [vp, cp, sz, P(i32)]),
+    "srl_engine_stop": (I, [vp]),
+    "srl_engine_stream_tokens": (I, [vp, i64, vp, i32, P(i32)]),
+    "srl_engine_stats_get": (I, [vp, P(EngineStatsC)]),
+    "srl_policy_logprobs": (I, [vp, cp, vp, i32, vp]),
+    "srl_truncated_is_weight": (I, [f64, f64, f64, P(f64)]),
+    "srl_ess": (I, [vp, i32, P(f64)]),
+    "srl_lag_stats": (I, [vp, vp, i32, i32, vp, i32, vp, vp, vp]),
+    "srl_crc32": (C.c_uint32, [vp, sz]),
+    "srl_process_group_id": (I, [P(cp), i32, cp, sz]),
+    "srl_kernel_sample_logits": (I, [vp, i32, i32, vp, vp, i32, vp, vp, vp]),
 }
 
 

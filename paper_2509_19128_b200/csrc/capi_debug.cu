@@ -3,6 +3,7 @@
 // engine uses (declared in include/streamrl_b200.h, "kernel entry points").
 #include <cuda_runtime.h>
 
+#include "decoder.cuh"
 #include "gemm.cuh"
 #include "streamrl_b200.h"
 
@@ -67,4 +68,15 @@ extern "C" int srl_kernel_gemm_bf16(const void* w, const void* x, int32_t M, int
     cudaFreeAsync(ws.counters, st);
   }
   return cuda_status(e);
+}
+
+extern "C" int srl_kernel_sample_logits(const float* logits, int32_t vocab, int32_t rows,
+                                        const uint64_t* seeds, const int32_t* draw_index,
+                                        int32_t greedy, int32_t* tokens_out, double* logprobs_out,
+                                        void* stream) {
+  if (!logits || vocab < 1 || rows < 0 || !seeds || !draw_index || !tokens_out || !logprobs_out)
+    return SRL_INVALID_ARGUMENT;
+  launch_sample_logits(logits, vocab, rows, seeds, draw_index, greedy, tokens_out, logprobs_out,
+                       static_cast<cudaStream_t>(stream));
+  return cuda_status(cudaGetLastError());
 }

@@ -1,0 +1,506 @@
+// decoder_engine.cpp -- the decoder policy on the device: DecoderRunner (the
+// varlen forward over a row plan: embedding, L x [QKV GEMM -> RoPE/KV append
+// -> paged attention -> O GEMM(+residual, next RMSNorm stats) -> gate/up GEMM
+// (SwiGLU) -> down GEMM(+residual)], LM head, sampler) and DecoderBackend
+// (stream slots at a constant generation batch, prefill of new streams,
+// CUDA-graph decode rounds, double-buffered weights with a pointer swap at
+// token boundaries, optional KV recompute after a swap).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "decoder_engine.hpp"
+
+namespace srl {
+
+namespace {
+int sm_count(int device) {
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  return n;
+}
+}  // namespace
+
+WeightMaps build_weight_maps(const DecoderDims& d, const WeightLayout& lay, const __nv_bfloat16* w) {
+  WeightMaps m;
+  m.qkv.resize(d.L);
+  m.o.resize(d.L);
+  m.gate_up.resize(d.L);
+  m.down.resize(d.L);
+  for (int l = 0; l < d.L; ++l) {
+    const LayerOffsets& o = lay.layers[l];
+    m.qkv[l] = make_tmap_bf16(w + o.qkv_w, d.qkv(), d.H, 128);
+    m.o[l] = make_tmap_bf16(w + o.o_w, d.H, d.qdim(), 128);
+    m.gate_up[l] = make_tmap_bf16(w + o.gate_up_w, 2 * (uint64_t)d.I, d.H, 128);
+    m.down[l] = make_tmap_bf16(w + o.down_w, d.H, d.I, 128);
+  }
+  m.lm_head = make_tmap_bf16(w + lay.lm_head, d.V, d.H, 128);
+  return m;
+}
+
+// ------------------------------------------------------------- runner ---
+DecoderRunner::~DecoderRunner() {
+  for (void* p : allocs_) cudaFree(p);
+}
+
+int DecoderRunner::init(const DecoderDims& dims, const WeightLayout& layout, int slots, int max_seq,
+                        int m_max, int logits_rows, int device, cudaStream_t st) {
+  d = dims;
+  lay = layout;  // offsets only (layers array owned by the weights object)
+  S = slots;
+  max_seq = max_seq;
+  this->max_seq = max_seq;
+  pages_per_seq = (max_seq + kPageTokens - 1) / kPageTokens;
+  M_max = std::max(m_max, slots);
+  this->logits_rows = std::max(logits_rows, slots);
+  dev = device;
+  st_ = st;
+  sms = sm_count(device);
+  const int H = d.H, parts = d.ssq_parts();
+  auto alloc = [&](auto** p, size_t n) -> int {
+    SRL_CUDA(cudaMalloc(p, std::max<size_t>(n, 1) * sizeof(**p)));
+    SRL_CUDA(cudaMemset(*p, 0, std::max<size_t>(n, 1) * sizeof(**p)));
+    allocs_.push_back(*p);
+    return SRL_OK;
+  };
+  int st2;
+  const size_t n_pages = (size_t)S * pages_per_seq;
+  kv_layer_elems = n_pages * d.nkv * kPageTokens * d.hd;
+  if ((st2 = alloc(&x, (size_t)M_max * H)) || (st2 = alloc(&xg, (size_t)M_max * H)) ||
+      (st2 = alloc(&ssq, (size_t)M_max * parts)) || (st2 = alloc(&qkv, (size_t)M_max * d.qkv())) ||
+      (st2 = alloc(&q, (size_t)M_max * d.qdim())) || (st2 = alloc(&attn, (size_t)M_max * d.qdim())) ||
+      (st2 = alloc(&act, (size_t)M_max * d.I)) ||
+      (st2 = alloc(&xg_last, (size_t)this->logits_rows * H)) ||
+      (st2 = alloc(&ssq_last, (size_t)this->logits_rows * parts)) ||
+      (st2 = alloc(&logits, (size_t)this->logits_rows * d.V)) ||
+      (st2 = alloc(&kc, kv_layer_elems * d.L)) || (st2 = alloc(&vc, kv_layer_elems * d.L)) ||
+      (st2 = alloc(&block_table, n_pages)) || (st2 = alloc(&cos_sin, (size_t)max_seq * d.hd)) ||
+      (st2 = alloc(&plan.row_slot, M_max)) || (st2 = alloc(&plan.row_pos, M_max)) ||
+      (st2 = alloc(&plan.row_token, M_max)) || (st2 = alloc(&plan.last_row, std::max(S, this->logits_rows))) ||
+      (st2 = alloc(&next.row_slot, M_max)) || (st2 = alloc(&next.row_pos, M_max)) ||
+      (st2 = alloc(&next.row_token, M_max)) || (st2 = alloc(&next.last_row, std::max(S, this->logits_rows))))
+    return st2;
+  // static page assignment: slot s owns pages [s*pps, (s+1)*pps)
+  std::vector<int32_t> bt(n_pages);
+  for (size_t i = 0; i < n_pages; ++i) bt[i] = (int32_t)i;
+  SRL_CUDA(cudaMemcpy(block_table, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice));
+  launch_rope_table(cos_sin, max_seq, d.hd, (double)d.theta, st_);
+  // activation TMA maps (box 64 and box 128 rows)
+  for (int b = 0; b < 2; ++b) {
+    const uint32_t box = b == 0 ? 64 : 128;
+    xg_map[b] = make_tmap_bf16(xg, M_max, H, box);
+    attn_map[b] = make_tmap_bf16(attn, M_max, d.qdim(), box);
+    act_map[b] = make_tmap_bf16(act, M_max, d.I, box);
+    last_map[b] = make_tmap_bf16(xg_last, this->logits_rows, H, box);
+  }
+  // GEMM workspace: the largest split-K need over every row count we may launch
+  size_t need = 0;
+  int counters = 1;
+  const int shapes[5][2] = {{d.qkv(), H}, {H, d.qdim()}, {2 * d.I, H}, {H, d.I}, {d.V, H}};
+  const int m_hi = std::max(M_max, this->logits_rows);
+  for (int M = 1; M <= m_hi; M = (M < 64) ? 64 : M + 64) {
+    const int tok = gemm_tok_tile(M);
+    for (auto& sh : shapes) {
+      const int sp = gemm_auto_splits(M, sh[0], sh[1], sms);
+      need = std::max(need, sp > 1 ? gemm_workspace_floats(M, sh[0], sp) : 0);
+      counters = std::max(counters, ((sh[0] + 127) / 128) * ((M + tok - 1) / tok));
+    }
+  }
+  gws.partial_floats = need;
+  gws.counter_count = counters;
+  if ((st2 = alloc(&gws.partials, need)) || (st2 = alloc(&gws.counters, counters))) return st2;
+  attn_ws_floats = std::max(attention_ws_floats(d, S, max_seq), attention_ws_floats(d, M_max, max_seq));
+  if ((st2 = alloc(&attn_ws, attn_ws_floats)) || (st2 = alloc(&attn_counters, (size_t)M_max * d.nkv)))
+    return st2;
+  SRL_CUDA(cudaStreamSynchronize(st_));
+  return SRL_OK;
+}
+
+int DecoderRunner::gemm(const CUtensorMap& tw, const CUtensorMap* tx, int M, int N, int K,
+                        const EpiParams& e) {
+  const int splits = gemm_auto_splits(M, N, K, sms);
+  const CUtensorMap& x_map = tx[gemm_tok_tile(M) == 64 ? 0 : 1];
+  const cudaError_t err = gemm_bf16_launch(tw, x_map, M, N, K, splits, gws, e, st_);
+  if (err != cudaSuccess) return cuda_fail(err, "gemm_bf16_launch");
+  return SRL_OK;
+}
+
+int DecoderRunner::forward(int M, const __nv_bfloat16* w, const WeightMaps& wm) {
+  const int H = d.H, parts = d.ssq_parts();
+  const float inv_h = 1.0f / (float)H;
+  launch_embed(w + lay.embed, w + lay.layers[0].ln1, plan.row_token, M, H, d.V, x, xg, ssq, st_);
+  int st;
+  for (int l = 0; l < d.L; ++l) {
+    const LayerOffsets& o = lay.layers[l];
+    EpiParams e;
+    e.kind = EPI_STORE_F32;
+    e.ssq_in = ssq; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d.eps;
+    e.bias = w + o.qkv_b; e.out_f32 = qkv; e.ld_out = d.qkv();
+    if ((st = gemm(wm.qkv[l], xg_map, M, d.qkv(), H, e))) return st;
+    __nv_bfloat16* kcl = kc + kv_layer_elems * l;
+    __nv_bfloat16* vcl = vc + kv_layer_elems * l;
+    launch_rope_append(qkv, d, plan, M, cos_sin, block_table, pages_per_seq, kcl, vcl, q, st_);
+    launch_attention(q, d, plan, M, block_table, pages_per_seq, kcl, vcl, max_seq, attn_ws,
+                     attn_counters, attn_ws_floats, attn, st_);
+    EpiParams r;
+    r.kind = EPI_RESID; r.resid = x; r.gain = w + o.ln2; r.xg = xg; r.ssq_out = ssq;
+    if ((st = gemm(wm.o[l], attn_map, M, H, d.qdim(), r))) return st;
+    EpiParams g;
+    g.kind = EPI_SWIGLU;
+    g.ssq_in = ssq; g.ssq_in_parts = parts; g.inv_dim = inv_h; g.eps = d.eps;
+    g.out_bf16 = act; g.ld_bf16 = d.I;
+    if ((st = gemm(wm.gate_up[l], xg_map, M, 2 * d.I, H, g))) return st;
+    EpiParams r2;
+    r2.kind = EPI_RESID; r2.resid = x; r2.xg = xg; r2.ssq_out = ssq;
+    r2.gain = w + (l + 1 < d.L ? lay.layers[l + 1].ln1 : lay.final_norm);
+    if ((st = gemm(wm.down[l], act_map, M, H, d.I, r2))) return st;
+  }
+  return SRL_OK;
+}
+
+int DecoderRunner::lm_head(int rows, const WeightMaps& wm, bool gathered) {
+  EpiParams e;
+  e.kind = EPI_STORE_F32;
+  e.ssq_in = gathered ? ssq_last : ssq;
+  e.ssq_in_parts = d.ssq_parts();
+  e.inv_dim = 1.0f / (float)d.H;
+  e.eps = d.eps;
+  e.out_f32 = logits;
+  e.ld_out = d.V;
+  return gemm(wm.lm_head, gathered ? last_map : xg_map, rows, d.V, d.H, e);
+}
+
+// ------------------------------------------------------------ backend ---
+DecoderBackend::DecoderBackend(const Policy& p, const srl_engine_options& o) : opts_(o) {
+  (void)p;
+}
+
+DecoderBackend::~DecoderBackend() {
+  if (st_) cudaStreamSynchronize(st_);
+  for (int b = 0; b < 2; ++b)
+    if (exec_[b]) cudaGraphExecDestroy(exec_[b]);
+  if (dev_state_) cudaFree(dev_state_);
+  if (pinned_) cudaFreeHost(pinned_);
+  if (ev_start_) cudaEventDestroy(ev_start_);
+  if (ev_stop_) cudaEventDestroy(ev_stop_);
+  runner_.reset();
+  if (st_) cudaStreamDestroy(st_);
+}
+
+int DecoderBackend::init(const Policy& p) {
+  SRL_CUDA(cudaSetDevice(opts_.device));
+  SRL_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  SRL_CUDA(cudaEventCreate(&ev_start_));
+  SRL_CUDA(cudaEventCreate(&ev_stop_));
+  const DecoderWeights& src = *p.dec;
+  d_ = src.dims;
+  S_ = std::max(1, opts_.max_streams);
+  max_seq_ = std::min(std::max(2, opts_.max_seq_len), d_.max_pos);
+  R_ = std::max(opts_.event_ring, std::max(1, opts_.rounds_per_sync));
+  prefill_budget_ = std::max(opts_.prefill_budget, 1);
+  int st;
+  for (int b = 0; b < 2; ++b) {
+    if ((st = clone_decoder(src, buf_[b]))) return st;
+    maps_[b] = build_weight_maps(d_, buf_[b]->layout, buf_[b]->w);
+  }
+  runner_ = std::make_unique<DecoderRunner>();
+  if ((st = runner_->init(d_, buf_[0]->layout, S_, max_seq_, S_ + prefill_budget_, S_,
+                          opts_.device, st_)))
+    return st;
+  // slot state + ring + counters in one allocation
+  const size_t ints = (size_t)S_ * 6 + 4;
+  const size_t bytes = ints * 4 + (size_t)S_ * 8 + (size_t)S_ * max_seq_ * 4 +
+                       (size_t)R_ * S_ * sizeof(DevEvent) + 256;
+  SRL_CUDA(cudaMalloc(&dev_state_, bytes));
+  SRL_CUDA(cudaMemset(dev_state_, 0, bytes));
+  uint8_t* p8 = static_cast<uint8_t*>(dev_state_);
+  auto take = [&](size_t n) {
+    uint8_t* at = p8;
+    p8 += (n + 15) / 16 * 16;
+    return at;
+  };
+  ring_.ev = reinterpret_cast<DevEvent*>(take((size_t)R_ * S_ * sizeof(DevEvent)));
+  ring_.rounds = R_;
+  ss_.seed = reinterpret_cast<uint64_t*>(take((size_t)S_ * 8));
+  ss_.live = reinterpret_cast<int32_t*>(take((size_t)S_ * 4));
+  ss_.seq_len = reinterpret_cast<int32_t*>(take((size_t)S_ * 4));
+  ss_.gen_count = reinterpret_cast<int32_t*>(take((size_t)S_ * 4));
+  ss_.max_tokens = reinterpret_cast<int32_t*>(take((size_t)S_ * 4));
+  ss_.terminator = reinterpret_cast<int32_t*>(take((size_t)S_ * 4));
+  ss_.history = reinterpret_cast<int32_t*>(take((size_t)S_ * max_seq_ * 4));
+  ss_.max_seq = max_seq_;
+  version_dev_ = reinterpret_cast<int32_t*>(take(4));
+  round_ctr_dev_ = reinterpret_cast<int32_t*>(take(4));
+  // pinned staging: events + plan upload + scalars
+  pinned_bytes_ = (size_t)R_ * S_ * sizeof(DevEvent) + (size_t)(runner_->M_max * 3 + S_ + 64) * 4 +
+                  (size_t)S_ * 64;
+  SRL_CUDA(cudaMallocHost(&pinned_, pinned_bytes_));
+  host_.assign(S_, HostSlot{});
+  // next plan: every slot dead
+  std::vector<int32_t> neg(std::max(runner_->M_max, S_), -1);
+  SRL_CUDA(cudaMemcpy(runner_->next.row_slot, neg.data(), 4 * (size_t)runner_->M_max, cudaMemcpyHostToDevice));
+  SRL_CUDA(cudaMemcpy(runner_->next.last_row, neg.data(), 4 * (size_t)S_, cudaMemcpyHostToDevice));
+  SRL_CUDA(cudaMemcpy(runner_->plan.row_slot, neg.data(), 4 * (size_t)runner_->M_max, cudaMemcpyHostToDevice));
+  SRL_CUDA(cudaMemcpy(runner_->plan.last_row, neg.data(), 4 * (size_t)S_, cudaMemcpyHostToDevice));
+  return SRL_OK;
+}
+
+int DecoderBackend::open_slot(int slot, const StreamSpec& spec) {
+  const int n_prefix = 1 + (int)spec.prompt.size();
+  if (n_prefix + spec.max_tokens > max_seq_)
+    return fail(SRL_INVALID_ARGUMENT, "open_stream: bos + prompt + max_tokens exceeds max_seq_len");
+  HostSlot& h = host_[slot];
+  h = HostSlot{};
+  h.live = true;
+  h.pending = true;
+  h.tokens.push_back(d_.bos);
+  h.tokens.insert(h.tokens.end(), spec.prompt.begin(), spec.prompt.end());
+  h.fed = 0;
+  // device slot state (pinned staging; synchronous so the staging can be reused)
+  int32_t* pi = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(pinned_) + pinned_bytes_ - 64);
+  uint64_t* pu = reinterpret_cast<uint64_t*>(pi + 8);
+  pi[0] = 1; pi[1] = 0; pi[2] = 0; pi[3] = spec.max_tokens; pi[4] = spec.terminator;
+  pu[0] = spec.seed;
+  SRL_CUDA(cudaMemcpyAsync(ss_.live + slot, pi + 0, 4, cudaMemcpyHostToDevice, st_));
+  SRL_CUDA(cudaMemcpyAsync(ss_.seq_len + slot, pi + 1, 4, cudaMemcpyHostToDevice, st_));
+  SRL_CUDA(cudaMemcpyAsync(ss_.gen_count + slot, pi + 2, 4, cudaMemcpyHostToDevice, st_));
+  SRL_CUDA(cudaMemcpyAsync(ss_.max_tokens + slot, pi + 3, 4, cudaMemcpyHostToDevice, st_));
+  SRL_CUDA(cudaMemcpyAsync(ss_.terminator + slot, pi + 4, 4, cudaMemcpyHostToDevice, st_));
+  SRL_CUDA(cudaMemcpyAsync(ss_.seed + slot, pu, 8, cudaMemcpyHostToDevice, st_));
+  SRL_CUDA(cudaMemcpyAsync(ss_.history + (size_t)slot * max_seq_, h.tokens.data(),
+                           4 * h.tokens.size(), cudaMemcpyHostToDevice, st_));
+  SRL_CUDA(cudaStreamSynchronize(st_));
+  any_pending_ = true;
+  return SRL_OK;
+}
+
+void DecoderBackend::close_slot(int slot) {
+  host_[slot].live = false;
+  host_[slot].pending = false;
+  int32_t* pi = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(pinned_) + pinned_bytes_ - 64);
+  pi[0] = 0;
+  cudaMemcpyAsync(ss_.live + slot, pi, 4, cudaMemcpyHostToDevice, st_);
+  cudaStreamSynchronize(st_);
+}
+
+int DecoderBackend::decode_round_eager(int b) {
+  DecoderRunner& r = *runner_;
+  launch_plan_copy(r.plan, r.next, S_, S_, round_ctr_dev_, st_);
+  int st;
+  if ((st = r.forward(S_, buf_[b]->w, maps_[b]))) return st;
+  if ((st = r.lm_head(S_, maps_[b], false))) return st;
+  launch_sample(r.logits, d_.V, S_, r.plan, r.next, ss_, ring_, round_ctr_dev_, version_dev_,
+                opts_.greedy, st_);
+  return SRL_OK;
+}
+
+int DecoderBackend::capture(int b) {
+  cudaGraph_t g = nullptr;
+  SRL_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+  const int st = decode_round_eager(b);
+  const cudaError_t e = cudaStreamEndCapture(st_, &g);
+  if (st != SRL_OK) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  SRL_CUDA(e);
+  SRL_CUDA(cudaGraphInstantiate(&exec_[b], g, 0));
+  cudaGraphDestroy(g);
+  return SRL_OK;
+}
+
+// Prefill round: decode rows for running slots + prompt rows for pending slots.
+int DecoderBackend::prefill_round(int b, std::vector<int>& prefilled) {
+  DecoderRunner& r = *runner_;
+  std::vector<int32_t> rs, rp, rt, last(S_, -1);
+  for (int s = 0; s < S_; ++s) {
+    HostSlot& h = host_[s];
+    if (!h.live || h.pending) continue;
+    last[s] = (int)rs.size();
+    rs.push_back(s);
+    rp.push_back(h.fed);
+    rt.push_back(h.tokens.back());
+  }
+  int budget = prefill_budget_;
+  for (int s = 0; s < S_; ++s) {
+    HostSlot& h = host_[s];
+    if (!h.live || !h.pending) continue;
+    const int n = (int)h.tokens.size();
+    if (n > budget && !prefilled.empty()) continue;  // next round
+    for (int p = 0; p < n; ++p) {
+      rs.push_back(s);
+      rp.push_back(p);
+      rt.push_back(h.tokens[p]);
+    }
+    last[s] = (int)rs.size() - 1;
+    budget -= n;
+    prefilled.push_back(s);
+  }
+  const int M = (int)rs.size();
+  if (M > r.M_max) return fail(SRL_INVALID_ARGUMENT, "prefill exceeds the engine's row budget");
+  int32_t* pin = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(pinned_) + (size_t)R_ * S_ * sizeof(DevEvent));
+  std::memcpy(pin, rs.data(), 4 * M);
+  std::memcpy(pin + M, rp.data(), 4 * M);
+  std::memcpy(pin + 2 * M, rt.data(), 4 * M);
+  std::memcpy(pin + 3 * M, last.data(), 4 * S_);
+  SRL_CUDA(cudaMemcpyAsync(r.next.row_slot, pin, 4 * M, cudaMemcpyHostToDevice, st_));
+  SRL_CUDA(cudaMemcpyAsync(r.next.row_pos, pin + M, 4 * M, cudaMemcpyHostToDevice, st_));
+  SRL_CUDA(cudaMemcpyAsync(r.next.row_token, pin + 2 * M, 4 * M, cudaMemcpyHostToDevice, st_));
+  SRL_CUDA(cudaMemcpyAsync(r.next.last_row, pin + 3 * M, 4 * S_, cudaMemcpyHostToDevice, st_));
+  launch_plan_copy(r.plan, r.next, M, S_, round_ctr_dev_, st_);
+  int st;
+  if ((st = r.forward(M, buf_[b]->w, maps_[b]))) return st;
+  launch_gather_rows(r.xg, r.ssq, r.plan.last_row, S_, d_.H, d_.ssq_parts(), r.xg_last, r.ssq_last, st_);
+  if ((st = r.lm_head(S_, maps_[b], true))) return st;
+  launch_sample(r.logits, d_.V, S_, r.plan, r.next, ss_, ring_, round_ctr_dev_, version_dev_,
+                opts_.greedy, st_);
+  // the staging buffer is reused by the next prefill: keep it ordered
+  SRL_CUDA(cudaStreamSynchronize(st_));
+  return SRL_OK;
+}
+
+int DecoderBackend::run_rounds(int n, std::vector<SlotEvent>& events, double* device_ms) {
+  events.assign((size_t)n * S_, SlotEvent{});
+  int done = 0;
+  while (done < n) {
+    const int batch = std::min(n - done, R_);
+    std::vector<std::vector<int>> prefilled_at(batch);
+    SRL_CUDA(cudaEventRecord(ev_start_, st_));
+    const int64_t c0 = round_ctr_host_;
+    for (int i = 0; i < batch; ++i) {
+      int st;
+      if (any_pending_) {
+        if ((st = prefill_round(active_, prefilled_at[i]))) return st;
+        for (int s : prefilled_at[i]) host_[s].pending = false;
+        any_pending_ = false;
+        for (const HostSlot& h : host_)
+          if (h.live && h.pending) any_pending_ = true;
+      } else if (opts_.use_graphs) {
+        if (!exec_[active_] && (st = capture(active_))) return st;
+        SRL_CUDA(cudaGraphLaunch(exec_[active_], st_));
+      } else {
+        if ((st = decode_round_eager(active_))) return st;
+      }
+      ++round_ctr_host_;
+    }
+    SRL_CUDA(cudaEventRecord(ev_stop_, st_));
+    // copy the batch's ring rows (at most two contiguous ranges)
+    DevEvent* pe = static_cast<DevEvent*>(pinned_);
+    const int r0 = (int)(c0 % R_);
+    const int first = std::min(batch, R_ - r0);
+    SRL_CUDA(cudaMemcpyAsync(pe, ring_.ev + (size_t)r0 * S_, sizeof(DevEvent) * first * S_,
+                             cudaMemcpyDeviceToHost, st_));
+    if (batch > first)
+      SRL_CUDA(cudaMemcpyAsync(pe + (size_t)first * S_, ring_.ev, sizeof(DevEvent) * (batch - first) * S_,
+                               cudaMemcpyDeviceToHost, st_));
+    SRL_CUDA(cudaStreamSynchronize(st_));
+    SRL_CUDA(cudaGetLastError());
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev_start_, ev_stop_);
+    if (device_ms) *device_ms += ms;
+    for (int i = 0; i < batch; ++i) {
+      for (int s = 0; s < S_; ++s) {
+        const DevEvent& e = pe[(size_t)i * S_ + s];
+        SlotEvent& o = events[(size_t)(done + i) * S_ + s];
+        o.flag = e.flag; o.token = e.token; o.position = e.position; o.version = e.version;
+        o.logprob = e.logprob;
+        if (e.flag == 0) continue;
+        HostSlot& h = host_[s];
+        h.fed = (int)h.tokens.size();  // every token so far is now in the KV cache
+        h.tokens.push_back(e.token);
+        if (e.flag >= 2) h.live = false;
+      }
+    }
+    done += batch;
+  }
+  return SRL_OK;
+}
+
+int DecoderBackend::check_update(const Policy& p) {
+  if (!p.dec || !same_decoder_shape(p.dec->cfg, buf_[active_]->cfg))
+    return fail(SRL_POLICY_MISMATCH, "policy_mismatch: decoder shape differs");
+  return SRL_OK;
+}
+
+int DecoderBackend::swap_and_recompute(bool recompute, int version) {
+  active_ ^= 1;
+  int32_t* pi = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(pinned_) + pinned_bytes_ - 64);
+  pi[5] = version;
+  SRL_CUDA(cudaMemcpyAsync(version_dev_, pi + 5, 4, cudaMemcpyHostToDevice, st_));
+  if (recompute) {
+    const int st = recompute_kv();
+    if (st != SRL_OK) return st;
+  }
+  SRL_CUDA(cudaStreamSynchronize(st_));
+  return SRL_OK;
+}
+
+// Recompute mode (engine.cpp:107-113): rebuild every live slot's KV cache
+// from its full prefix under the new weights, chunked by position so each
+// chunk only attends to already-rewritten keys.
+int DecoderBackend::recompute_kv() {
+  DecoderRunner& r = *runner_;
+  int max_fed = 0;
+  for (const HostSlot& h : host_)
+    if (h.live && !h.pending) max_fed = std::max(max_fed, h.fed);
+  std::vector<int32_t> rs, rp, rt;
+  auto flush = [&]() -> int {
+    const int M = (int)rs.size();
+    if (M == 0) return SRL_OK;
+    int32_t* pin = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(pinned_) + (size_t)R_ * S_ * sizeof(DevEvent));
+    std::memcpy(pin, rs.data(), 4 * M);
+    std::memcpy(pin + M, rp.data(), 4 * M);
+    std::memcpy(pin + 2 * M, rt.data(), 4 * M);
+    SRL_CUDA(cudaMemcpyAsync(r.plan.row_slot, pin, 4 * M, cudaMemcpyHostToDevice, st_));
+    SRL_CUDA(cudaMemcpyAsync(r.plan.row_pos, pin + M, 4 * M, cudaMemcpyHostToDevice, st_));
+    SRL_CUDA(cudaMemcpyAsync(r.plan.row_token, pin + 2 * M, 4 * M, cudaMemcpyHostToDevice, st_));
+    const int st = r.forward(M, buf_[active_]->w, maps_[active_]);
+    if (st != SRL_OK) return st;
+    SRL_CUDA(cudaStreamSynchronize(st_));
+    rs.clear(); rp.clear(); rt.clear();
+    return SRL_OK;
+  };
+  for (int p = 0; p < max_fed; ++p) {
+    for (int s = 0; s < S_; ++s) {
+      const HostSlot& h = host_[s];
+      if (!h.live || h.pending || p >= h.fed) continue;
+      if ((int)rs.size() == r.M_max) {
+        const int st = flush();
+        if (st != SRL_OK) return st;
+      }
+      rs.push_back(s);
+      rp.push_back(p);
+      rt.push_back(h.tokens[p]);
+    }
+  }
+  return flush();
+}
+
+int DecoderBackend::apply_update(const Policy& p, bool recompute, int version) {
+  SRL_CUDA(cudaMemcpyAsync(buf_[active_ ^ 1]->w, p.dec->w, p.dec->bytes, cudaMemcpyDeviceToDevice, st_));
+  return swap_and_recompute(recompute, version);
+}
+
+int DecoderBackend::standby(void** ptr, size_t* bytes) {
+  *ptr = buf_[active_ ^ 1]->w;
+  *bytes = buf_[active_ ^ 1]->bytes;
+  return SRL_OK;
+}
+
+int DecoderBackend::commit_standby(bool recompute, int version) {
+  return swap_and_recompute(recompute, version);
+}
+
+int DecoderBackend::slot_history(int slot, std::vector<int32_t>& out) {
+  out = host_[slot].tokens;
+  return SRL_OK;
+}
+
+std::unique_ptr<Backend> make_decoder_backend(const Policy& p, const srl_engine_options& o, int* status) {
+  auto b = std::make_unique<DecoderBackend>(p, o);
+  *status = b->init(p);
+  if (*status != SRL_OK) return nullptr;
+  return b;
+}
+
+}  // namespace srl

@@ -1,0 +1,107 @@
+// decoder_engine.hpp -- DecoderRunner (device buffers + varlen forward) and
+// DecoderBackend (the Engine backend for decoder policies).
+#pragma once
+#include <memory>
+#include <vector>
+
+#include "gemm.cuh"
+#include "runtime.hpp"
+
+namespace srl {
+
+struct WeightMaps {  // TMA descriptors of one flat weight buffer
+  std::vector<CUtensorMap> qkv, o, gate_up, down;
+  CUtensorMap lm_head;
+};
+WeightMaps build_weight_maps(const DecoderDims& d, const WeightLayout& lay, const __nv_bfloat16* w);
+
+// Activations for up to M_max rows, a paged KV cache for S slots x max_seq
+// tokens, and the split-K / split-KV workspaces.
+struct DecoderRunner {
+  DecoderDims d{};
+  WeightLayout lay{};
+  int S = 0, max_seq = 0, pages_per_seq = 0, M_max = 0, logits_rows = 0, dev = 0, sms = 148;
+  size_t kv_layer_elems = 0;
+  float* x = nullptr;             // [M_max x H] fp32 residual stream
+  __nv_bfloat16* xg = nullptr;    // [M_max x H] bf16(x * next RMSNorm gain)
+  float* ssq = nullptr;           // [M_max x ceil(H/128)] partial sums of x^2
+  float* qkv = nullptr;           // [M_max x (nq+2nkv)hd]
+  __nv_bfloat16* q = nullptr;     // [M_max x nq hd] (RoPE applied)
+  __nv_bfloat16* attn = nullptr;  // [M_max x nq hd]
+  __nv_bfloat16* act = nullptr;   // [M_max x I]
+  __nv_bfloat16* xg_last = nullptr;
+  float* ssq_last = nullptr;
+  float* logits = nullptr;        // [logits_rows x V]
+  __nv_bfloat16 *kc = nullptr, *vc = nullptr;  // [L][pages][nkv][64][hd]
+  int32_t* block_table = nullptr;
+  float* cos_sin = nullptr;
+  RoundPlan plan{}, next{};
+  GemmWorkspace gws{};
+  float* attn_ws = nullptr;
+  int* attn_counters = nullptr;
+  size_t attn_ws_floats = 0;
+  CUtensorMap xg_map[2], attn_map[2], act_map[2], last_map[2];
+
+  ~DecoderRunner();
+  int init(const DecoderDims& dims, const WeightLayout& layout, int slots, int max_seq, int m_max,
+           int logits_rows, int device, cudaStream_t st);
+  int forward(int M, const __nv_bfloat16* w, const WeightMaps& wm);
+  int lm_head(int rows, const WeightMaps& wm, bool gathered);
+  int gemm(const CUtensorMap& tw, const CUtensorMap* tx, int M, int N, int K, const EpiParams& e);
+  cudaStream_t stream() const { return st_; }
+
+ private:
+  cudaStream_t st_ = nullptr;
+  std::vector<void*> allocs_;
+};
+
+class DecoderBackend final : public Backend {
+ public:
+  DecoderBackend(const Policy& p, const srl_engine_options& o);
+  ~DecoderBackend() override;
+  int init(const Policy& p);
+  int slots() const override { return S_; }
+  int open_slot(int slot, const StreamSpec& spec) override;
+  void close_slot(int slot) override;
+  int run_rounds(int n, std::vector<SlotEvent>& events, double* device_ms) override;
+  int check_update(const Policy& p) override;
+  int apply_update(const Policy& p, bool recompute, int version) override;
+  int standby(void** ptr, size_t* bytes) override;
+  int commit_standby(bool recompute, int version) override;
+  int slot_history(int slot, std::vector<int32_t>& out) override;
+
+ private:
+  struct HostSlot {
+    bool live = false, pending = false;
+    int fed = 0;                  // tokens already in the KV cache
+    std::vector<int32_t> tokens;  // bos + prompt + generated
+  };
+  int decode_round_eager(int b);
+  int capture(int b);
+  int prefill_round(int b, std::vector<int>& prefilled);
+  int swap_and_recompute(bool recompute, int version);
+  int recompute_kv();
+
+  srl_engine_options opts_;
+  DecoderDims d_{};
+  int S_ = 1, max_seq_ = 2, R_ = 1, prefill_budget_ = 1;
+  std::shared_ptr<DecoderWeights> buf_[2];
+  WeightMaps maps_[2];
+  int active_ = 0;
+  std::unique_ptr<DecoderRunner> runner_;
+  cudaStream_t st_ = nullptr;
+  cudaGraphExec_t exec_[2] = {nullptr, nullptr};
+  cudaEvent_t ev_start_ = nullptr, ev_stop_ = nullptr;
+  void* dev_state_ = nullptr;
+  void* pinned_ = nullptr;
+  size_t pinned_bytes_ = 0;
+  SlotState ss_{};
+  EventRing ring_{};
+  int32_t* version_dev_ = nullptr;
+  int32_t* round_ctr_dev_ = nullptr;
+  int64_t round_ctr_host_ = 0;
+  std::vector<HostSlot> host_;
+  bool any_pending_ = false;
+};
+
+}  // namespace srl

@@ -1,0 +1,115 @@
+"""Trainer math: the ``streamrl::rlmath`` free functions
+(/root/reference/proj/core/include/streamrl/rl_math.hpp:20-121) over the
+native library.  Same names, argument meaning and exceptions: ValueError for
+std::invalid_argument, EssUndefinedError for the all-zero ESS case.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .policy import NativePolicy
+
+
+class EssUndefinedError(ValueError):
+    """EssUndefinedError (rl_math.hpp:30-32)."""
+
+
+def _check(st: int, what: str):
+    if st == 0:
+        return
+    detail = _lib.lib().srl_last_error().decode()
+    if st in (5, 2):
+        raise ValueError(f"{what}: {detail}")
+    if st == 8:
+        raise EssUndefinedError(detail)
+    raise _lib.SrlError(st, f"{what}: {detail}")
+
+
+def policy_logprobs(policy, prompt_id: str, tokens) -> np.ndarray:
+    """log pi(y_t | x, y_<t) for every position (rl_math.cpp:128-142), on the device."""
+    t = np.ascontiguousarray(tokens, dtype=np.int32)
+    out = np.zeros(len(t), dtype=np.float64)
+    with NativePolicy(policy) as h:
+        st = _lib.lib().srl_policy_logprobs(h, prompt_id.encode(), t.ctypes.data, len(t),
+                                            out.ctypes.data)
+    _check(st, "policy_logprobs")
+    return out
+
+
+def truncated_is_weight(pi_logprob_sum: float, mu_logprob_sum: float, clamp: float) -> float:
+    """min(c, exp(pi - mu)) (rl_math.cpp:144-150)."""
+    out = C.c_double()
+    _check(_lib.lib().srl_truncated_is_weight(pi_logprob_sum, mu_logprob_sum, clamp, C.byref(out)),
+           "truncated_is_weight")
+    return out.value
+
+
+def ess(weights) -> float:
+    """(sum w)^2 / (N sum w^2) (rl_math.cpp:152-163)."""
+    a = np.ascontiguousarray(weights, dtype=np.float64)
+    out = C.c_double()
+    _check(_lib.lib().srl_ess(a.ctypes.data if len(a) else None, len(a), C.byref(out)), "ess")
+    return out.value
+
+
+@dataclass
+class Trajectory:
+    """Trajectory (trajectory.hpp:15-25)."""
+
+    prompt_id: str
+    tokens: list
+    behavior_logprobs: list
+    behavior_versions: list
+    reward: float = 0.0
+
+    def validate(self):  # trajectory.cpp:14-25
+        n = len(self.tokens)
+        if n < 1:
+            raise ValueError("Trajectory: empty token sequence")
+        if len(self.behavior_logprobs) != n or len(self.behavior_versions) != n:
+            raise ValueError("Trajectory: field lengths differ")
+        if any(b < a for a, b in zip(self.behavior_versions, self.behavior_versions[1:])):
+            raise ValueError("Trajectory: behavior_versions decrease")
+        if any(np.isnan(self.behavior_logprobs)):
+            raise ValueError("Trajectory: NaN behavior logprob")
+        if not np.isfinite(self.reward):
+            raise ValueError("Trajectory: non-finite reward")
+
+    def length(self) -> int:
+        return len(self.tokens)
+
+    def behavior_logprob_sum(self) -> float:
+        s = 0.0
+        for v in self.behavior_logprobs:
+            s += v
+        return s
+
+
+@dataclass
+class BaselineTable:
+    """Per-(prompt, position) mean reward (trajectory.hpp:29-35)."""
+
+    values: dict = field(default_factory=dict)
+
+    def at(self, prompt_id: str, position: int) -> float:
+        try:
+            return self.values[(prompt_id, position)]
+        except KeyError:
+            raise ValueError(f"BaselineTable: missing cell ({prompt_id}, {position})") from None
+
+
+def fit_baseline(trajectories) -> BaselineTable:
+    """fit_baseline (rl_math.cpp:165-179): exact per-cell mean (host-side actor queue logic)."""
+    if not trajectories:
+        raise ValueError("fit_baseline: no trajectories")
+    cells: dict = {}
+    for t in trajectories:
+        t.validate()
+        for p in range(t.length()):
+            s, n = cells.get((t.prompt_id, p), (0.0, 0))
+            cells[(t.prompt_id, p)] = (s + t.reward, n + 1)
+    return BaselineTable({k: s / n for k, (s, n) in cells.items()})
