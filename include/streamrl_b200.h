@@ -186,11 +186,28 @@ typedef struct {
   int64_t rounds;
   int64_t tokens;
   int64_t updates;
-  double decode_ms;
+  double decode_ms;      /* device time of all rounds (CUDA events on the engine stream) */
   double last_pause_ms;
   double max_pause_ms;
+  int64_t launches;      /* kernels launched by the engine (graph nodes counted) */
 } srl_engine_stats;
 int srl_engine_stats_get(const srl_engine* e, srl_engine_stats* out);
+
+/* Per-kernel-class device time of one decode round, recorded with CUDA events
+ * around every launch of the round after srl_engine_profile_next_round()
+ * (the round runs eagerly instead of from its CUDA graph; it is a real round
+ * and emits events).  Classes: 0 plan, 1 embed, 2 qkv_gemm, 3 rope_kv_append,
+ * 4 attention, 5 o_gemm, 6 gate_up_gemm, 7 down_gemm, 8 lm_head_gemm,
+ * 9 sample. */
+enum { SRL_KERNEL_CLASSES = 10 };
+typedef struct {
+  double ms[SRL_KERNEL_CLASSES];
+  int32_t launches[SRL_KERNEL_CLASSES];
+  int32_t valid;
+  int32_t rows;
+} srl_kernel_profile;
+int srl_engine_profile_next_round(srl_engine* e);
+int srl_engine_kernel_profile(const srl_engine* e, srl_kernel_profile* out);
 
 /* ------------------------------------------------------ trainer math --- */
 /* rlmath free functions (include/streamrl/rl_math.hpp:20-121). */

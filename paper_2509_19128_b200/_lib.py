@@ -57,7 +57,15 @@ class TokenEventC(C.Structure):
 
 class EngineStatsC(C.Structure):
     _fields_ = [("rounds", i64), ("tokens", i64), ("updates", i64), ("decode_ms", f64),
-                ("last_pause_ms", f64), ("max_pause_ms", f64)]
+                ("last_pause_ms", f64), ("max_pause_ms", f64), ("launches", i64)]
+
+
+class KernelProfileC(C.Structure):
+    _fields_ = [("ms", f64 * 10), ("launches", i32 * 10), ("valid", i32), ("rows", i32)]
+
+
+KERNEL_CLASSES = ["plan", "embed", "qkv_gemm", "rope_kv_append", "attention", "o_gemm",
+                  "gate_up_gemm", "down_gemm", "lm_head_gemm", "sample"]
 
 
 I = C.c_int
@@ -107,6 +115,8 @@ SIGNATURES: dict[str, tuple] = {
     "srl_crc32": (C.c_uint32, [vp, sz]),
     "srl_process_group_id": (I, [P(cp), i32, cp, sz]),
     "srl_kernel_sample_logits": (I, [vp, i32, i32, vp, vp, i32, vp, vp, vp]),
+    "srl_engine_profile_next_round": (I, [vp]),
+    "srl_engine_kernel_profile": (I, [vp, P(KernelProfileC)]),
 }
 
 

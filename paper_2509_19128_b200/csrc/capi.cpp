@@ -494,3 +494,15 @@ extern "C" int srl_process_group_id(const char* const* members, int32_t n, char*
   std::snprintf(buf, cap, "pg-%016llx", (unsigned long long)h);
   return SRL_OK;
 }
+
+extern "C" int srl_engine_profile_next_round(srl_engine* e) {
+  if (!e) return fail(SRL_INVALID_ARGUMENT, "profile_next_round");
+  e->e->profile_next_round();
+  return SRL_OK;
+}
+
+extern "C" int srl_engine_kernel_profile(const srl_engine* e, srl_kernel_profile* out) {
+  if (!e || !out) return fail(SRL_INVALID_ARGUMENT, "kernel_profile");
+  if (!e->e->kernel_profile(out)) return fail(SRL_INVALID_ARGUMENT, "no profiled round yet");
+  return SRL_OK;
+}

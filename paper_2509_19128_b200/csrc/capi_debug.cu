@@ -29,17 +29,8 @@ extern "C" int srl_kernel_gemm_bf16(const void* w, const void* x, int32_t M, int
   const CUtensorMap tw = make_tmap_bf16(w, (uint64_t)N, (uint64_t)K, 128);
   const CUtensorMap tx = make_tmap_bf16(x, (uint64_t)M, (uint64_t)K, (uint32_t)tok);
   if (splits <= 0) splits = gemm_auto_splits(M, N, K, num_sms());
-  GemmWorkspace ws;
+  GemmWorkspace ws;  // cluster split-K reduces through DSMEM: no workspace
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (splits > 1) {
-    ws.partial_floats = gemm_workspace_floats(M, N, splits);
-    ws.counter_count = ((N + 127) / 128) * ((M + tok - 1) / tok);
-    if (cudaMallocAsync(&ws.partials, ws.partial_floats * sizeof(float), st) != cudaSuccess)
-      return SRL_OUT_OF_MEMORY;
-    if (cudaMallocAsync(&ws.counters, ws.counter_count * sizeof(int), st) != cudaSuccess)
-      return SRL_OUT_OF_MEMORY;
-    cudaMemsetAsync(ws.counters, 0, ws.counter_count * sizeof(int), st);
-  }
   EpiParams epi;
   epi.kind = epi_kind;
   epi.ssq_in = ssq_in;
@@ -62,12 +53,7 @@ extern "C" int srl_kernel_gemm_bf16(const void* w, const void* x, int32_t M, int
     epi.xg = static_cast<__nv_bfloat16*>(xg);
     epi.ssq_out = ssq_out;
   }
-  cudaError_t e = gemm_bf16_launch(tw, tx, M, N, K, splits, ws, epi, st);
-  if (splits > 1) {
-    cudaFreeAsync(ws.partials, st);
-    cudaFreeAsync(ws.counters, st);
-  }
-  return cuda_status(e);
+  return cuda_status(gemm_bf16_launch(tw, tx, M, N, K, splits, ws, epi, st));
 }
 
 extern "C" int srl_kernel_sample_logits(const float* logits, int32_t vocab, int32_t rows,

@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "decoder.cuh"
+#include "sm100.cuh"
 
 namespace srl {
 
@@ -79,6 +80,7 @@ __global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, const __nv_bfl
                              const int32_t* __restrict__ row_token, int H, int V, float* __restrict__ x,
                              __nv_bfloat16* __restrict__ xg, float* __restrict__ ssq) {
   __shared__ float red[4];
+  sm100::griddep_wait();
   const int m = blockIdx.x;
   int tok = row_token[m];
   const bool ok = tok >= 0 && tok < V;
@@ -106,6 +108,7 @@ __global__ void rope_append_kernel(const float* __restrict__ qkv, int nq, int nk
                                    const int32_t* __restrict__ block_table, int pages_per_seq,
                                    __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
                                    __nv_bfloat16* __restrict__ q_out) {
+  sm100::griddep_wait();
   const int m = blockIdx.x;
   const int slot = row_slot[m];
   if (slot < 0) return;
@@ -140,98 +143,128 @@ __global__ void rope_append_kernel(const float* __restrict__ qkv, int nq, int nk
 }
 
 // --------------------------------------------------------- attention ---
-constexpr int kMaxG = 8;
+// One CTA per (row, kv head, 128-key split); 4 warps x one 32-key tile each.
+// A warp stages its tile's K and V rows (contiguous inside a KV page) with
+// coalesced 16-B loads into shared memory, scores all G = nq/nkv query heads
+// of the group (lane = key), runs an online softmax per head and accumulates
+// P.V with lane = head dims.  Split partials are combined by the last CTA of
+// the (row, head) in split order (deterministic).
+constexpr int kAttnWarps = 4;
+constexpr int kAttnChunk = 32 * kAttnWarps;  // keys per split
 
-template <int HD>
-__global__ void __launch_bounds__(128)
+template <int G, int HD>
+__global__ void __launch_bounds__(32 * kAttnWarps)
     attention_kernel(const __nv_bfloat16* __restrict__ q, int nq, int nkv,
                      const int32_t* __restrict__ row_slot, const int32_t* __restrict__ row_pos,
                      const int32_t* __restrict__ block_table, int pages_per_seq,
                      const __nv_bfloat16* __restrict__ kc, const __nv_bfloat16* __restrict__ vc,
-                     int chunk, float scale, float* __restrict__ ws, int* __restrict__ counters,
+                     float scale, float* __restrict__ ws, int* __restrict__ counters,
                      __nv_bfloat16* __restrict__ out) {
-  constexpr int DPL = HD / 32;  // dims per lane in the PV phase
-  const int m = blockIdx.x, kh = blockIdx.y, split = blockIdx.z, splits = gridDim.z;
-  const int G = nq / nkv;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ float sq[kMaxG][HD];
-  __shared__ float sm_m[4][kMaxG], sm_l[4][kMaxG];
-  __shared__ float sm_acc[4][kMaxG][HD];
+  constexpr int DPL = HD / 32;           // dims per lane in the PV phase
+  constexpr int ROW = HD * 2 + 16;       // padded K row in smem (bytes): conflict-free LDS.128
+  constexpr int VROW = HD * 2;           // V rows are read row-wise: no padding needed
+  constexpr int V4 = HD / 8;             // uint4 per K/V row
+  extern __shared__ __align__(16) uint8_t att_smem[];
+  using SqT = float[G][HD];
+  using SkT = uint8_t[kAttnWarps][32 * ROW];
+  using SvT = uint8_t[kAttnWarps][32 * VROW];
+  using SpT = float[kAttnWarps][G][32];
+  using SmT = float[kAttnWarps][G];
+  using SaT = float[kAttnWarps][G][HD];
+  SqT& sq = *reinterpret_cast<SqT*>(att_smem);
+  SkT& sk = *reinterpret_cast<SkT*>(att_smem + sizeof(SqT));
+  SvT& sv = *reinterpret_cast<SvT*>(att_smem + sizeof(SqT) + sizeof(SkT));
+  SpT& sp = *reinterpret_cast<SpT*>(att_smem + sizeof(SqT) + sizeof(SkT) + sizeof(SvT));
+  SmT& sm_m = *reinterpret_cast<SmT*>(att_smem + sizeof(SqT) + sizeof(SkT) + sizeof(SvT) + sizeof(SpT));
+  SmT& sm_l = *reinterpret_cast<SmT*>(att_smem + sizeof(SqT) + sizeof(SkT) + sizeof(SvT) + sizeof(SpT) + sizeof(SmT));
+  SaT& sm_acc = *reinterpret_cast<SaT*>(att_smem + sizeof(SqT));  // aliases sk after the tiles
+  static_assert(sizeof(SaT) <= sizeof(SkT), "accumulator alias must fit in the K staging area");
   __shared__ int s_last;
-
+  const int m = blockIdx.x, kh = blockIdx.y, split = blockIdx.z, splits = gridDim.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  sm100::griddep_wait();
   const int slot = row_slot[m];
-  if (slot < 0) return;  // padding / finished row: nothing to attend
+  if (slot < 0) return;  // padding / finished row
   const int ctx = row_pos[m] + 1;
-  const int k_begin = split * chunk;
-  const int k_end = min(ctx, k_begin + chunk);
+  const int k_begin = split * kAttnChunk;
+  if (k_begin >= ctx && splits == 1) return;
 
-  for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
-    const int g = i / HD, d = i % HD;
-    sq[g][d] = __bfloat162float(q[(size_t)m * nq * HD + (kh * G + g) * HD + d]) * scale;
-  }
+  for (int i = threadIdx.x; i < G * HD; i += blockDim.x)
+    sq[i / HD][i % HD] = __bfloat162float(q[(size_t)m * nq * HD + (kh * G) * HD + i]) * scale;
   __syncthreads();
 
-  float mrun[kMaxG], lrun[kMaxG], acc[kMaxG][DPL];
+  float mrun[G], lrun[G], acc[G][DPL];
 #pragma unroll
-  for (int g = 0; g < kMaxG; ++g) {
+  for (int g = 0; g < G; ++g) {
     mrun[g] = -INFINITY;
     lrun[g] = 0.f;
 #pragma unroll
     for (int d = 0; d < DPL; ++d) acc[g][d] = 0.f;
   }
-  const int32_t* bt = block_table + (size_t)slot * pages_per_seq;
 
-  for (int t0 = k_begin + warp * 32; t0 < k_end; t0 += 128) {
-    const int key = t0 + lane;
-    const bool valid = key < k_end;
-    float s[kMaxG];
-    if (valid) {
-      const int page = bt[key / kPageTokens];
-      const __nv_bfloat16* krow =
-          kc + (((size_t)page * nkv + kh) * kPageTokens + (key % kPageTokens)) * HD;
-      float kf[HD];
+  const int t0 = k_begin + warp * 32;
+  const int nvalid = max(0, min(32, ctx - t0));
+  if (nvalid > 0) {
+    // tile keys [t0, t0+32) lie in one page (t0 % 32 == 0, 64-token pages)
+    const int page = block_table[(size_t)slot * pages_per_seq + t0 / kPageTokens];
+    const size_t base = (((size_t)page * nkv + kh) * kPageTokens + (t0 % kPageTokens)) * HD;
+    const uint4* kg = reinterpret_cast<const uint4*>(kc + base);
+    const uint4* vg = reinterpret_cast<const uint4*>(vc + base);
+    uint4 kr[V4], vr[V4];
 #pragma unroll
-      for (int v = 0; v < HD / 8; ++v) {
-        const uint4 raw = reinterpret_cast<const uint4*>(krow)[v];
+    for (int i = 0; i < V4; ++i) {  // 32 rows x V4 uint4, lane-strided: coalesced
+      const int e = lane + 32 * i, r = e / V4;
+      if (r < nvalid) { kr[i] = __ldg(kg + e); vr[i] = __ldg(vg + e); }
+    }
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      const int e = lane + 32 * i, r = e / V4, c = e % V4;
+      if (r < nvalid) {
+        *reinterpret_cast<uint4*>(&sk[warp][r * ROW + c * 16]) = kr[i];
+        *reinterpret_cast<uint4*>(&sv[warp][r * VROW + c * 16]) = vr[i];
+      }
+    }
+    __syncwarp();
+    // scores: lane = key
+    float s[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) s[g] = 0.f;
+    if (lane < nvalid) {
+#pragma unroll
+      for (int c = 0; c < V4; ++c) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(&sk[warp][lane * ROW + c * 16]);
         const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+        float kf[8];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 f = __bfloat1622float2(p2[e]);
-          kf[v * 8 + 2 * e] = f.x;
-          kf[v * 8 + 2 * e + 1] = f.y;
+          kf[2 * e] = f.x;
+          kf[2 * e + 1] = f.y;
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float4 qa = *reinterpret_cast<const float4*>(&sq[g][c * 8]);
+          const float4 qb = *reinterpret_cast<const float4*>(&sq[g][c * 8 + 4]);
+          s[g] += qa.x * kf[0] + qa.y * kf[1] + qa.z * kf[2] + qa.w * kf[3] + qb.x * kf[4] +
+                  qb.y * kf[5] + qb.z * kf[6] + qb.w * kf[7];
         }
       }
-#pragma unroll
-      for (int g = 0; g < kMaxG; ++g) {
-        float a = 0.f;
-        if (g < G) {
-#pragma unroll
-          for (int d = 0; d < HD; ++d) a += sq[g][d] * kf[d];
-        }
-        s[g] = a;
-      }
     }
+    // online softmax per head over this tile
 #pragma unroll
-    for (int g = 0; g < kMaxG; ++g) {
-      if (g >= G) break;
-      const float sv = valid ? s[g] : -INFINITY;
-      const float tmax = warp_max(sv);
-      const float mnew = fmaxf(mrun[g], tmax);
-      const float alpha = (mrun[g] == -INFINITY) ? 0.f : __expf(mrun[g] - mnew);
-      const float p = valid ? __expf(sv - mnew) : 0.f;
-      lrun[g] = lrun[g] * alpha + warp_sum(p);
-      mrun[g] = mnew;
-#pragma unroll
-      for (int d = 0; d < DPL; ++d) acc[g][d] *= alpha;
-      s[g] = p;
+    for (int g = 0; g < G; ++g) {
+      const float sv_ = lane < nvalid ? s[g] : -INFINITY;
+      const float mx = warp_max(sv_);
+      const float p = lane < nvalid ? __expf(sv_ - mx) : 0.f;
+      mrun[g] = mx;
+      lrun[g] = warp_sum(p);
+      sp[warp][g][lane] = p;
     }
-    const int nvalid = min(32, k_end - t0);
+    __syncwarp();
+    // P.V: lane = dims
     for (int j = 0; j < nvalid; ++j) {
-      const int kj = t0 + j;
-      const int page = bt[kj / kPageTokens];
-      const __nv_bfloat16* vrow =
-          vc + (((size_t)page * nkv + kh) * kPageTokens + (kj % kPageTokens)) * HD + lane * DPL;
       float vf[DPL];
+      const uint8_t* vrow = &sv[warp][j * VROW + lane * DPL * 2];
       if constexpr (DPL == 2) {
         const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vrow));
         vf[0] = f.x;
@@ -243,34 +276,39 @@ __global__ void __launch_bounds__(128)
         vf[0] = a.x; vf[1] = a.y; vf[2] = b.x; vf[3] = b.y;
       }
 #pragma unroll
-      for (int g = 0; g < kMaxG; ++g) {
-        if (g >= G) break;
-        const float pj = __shfl_sync(0xffffffffu, s[g], j);
+      for (int g = 0; g < G; ++g) {
+        const float pj = sp[warp][g][j];
 #pragma unroll
         for (int d = 0; d < DPL; ++d) acc[g][d] += pj * vf[d];
       }
     }
   }
 
-  // combine the 4 warps of this CTA
-  if (lane == 0)
+  // combine the warps of this CTA (sm_acc aliases the K tiles: wait for all warps)
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
     for (int g = 0; g < G; ++g) {
       sm_m[warp][g] = mrun[g];
       sm_l[warp][g] = lrun[g];
     }
+  }
+#pragma unroll
   for (int g = 0; g < G; ++g)
 #pragma unroll
     for (int d = 0; d < DPL; ++d) sm_acc[warp][g][lane * DPL + d] = acc[g][d];
   __syncthreads();
 
-  const size_t rec = (size_t)G * (HD + 2);
+  constexpr size_t rec = (size_t)G * (HD + 2);
   float* my_ws = ws + (((size_t)m * nkv + kh) * splits + split) * rec;
   for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
     const int g = i / HD, d = i % HD;
     float M = -INFINITY;
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w][g]);
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm_m[w][g]);
     float L = 0.f, A = 0.f;
-    for (int w = 0; w < 4; ++w) {
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) {
       const float a = (sm_m[w][g] == -INFINITY) ? 0.f : __expf(sm_m[w][g] - M);
       L += sm_l[w][g] * a;
       A += sm_acc[w][g][d] * a;
@@ -294,34 +332,32 @@ __global__ void __launch_bounds__(128)
   if (!s_last) return;
   __threadfence();
   const float* base = ws + ((size_t)m * nkv + kh) * splits * rec;
+  const int used = min(splits, (ctx + kAttnChunk - 1) / kAttnChunk);  // later splits are empty
   for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
     const int g = i / HD, d = i % HD;
     float M = -INFINITY;
-    for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, __ldcg(&base[sp * rec + g * (HD + 2)]));
+    for (int sp2 = 0; sp2 < used; ++sp2) M = fmaxf(M, __ldcg(&base[sp2 * rec + g * (HD + 2)]));
     float L = 0.f, A = 0.f;
-    for (int sp = 0; sp < splits; ++sp) {
-      const float ms = __ldcg(&base[sp * rec + g * (HD + 2)]);
+    for (int sp2 = 0; sp2 < used; ++sp2) {
+      const float ms = __ldcg(&base[sp2 * rec + g * (HD + 2)]);
       const float a = (ms == -INFINITY) ? 0.f : __expf(ms - M);
-      L += __ldcg(&base[sp * rec + g * (HD + 2) + 1]) * a;
-      A += __ldcg(&base[sp * rec + g * (HD + 2) + 2 + d]) * a;
+      L += __ldcg(&base[sp2 * rec + g * (HD + 2) + 1]) * a;
+      A += __ldcg(&base[sp2 * rec + g * (HD + 2) + 2 + d]) * a;
     }
     out[(size_t)m * nq * HD + (kh * G + g) * HD + d] = __float2bfloat16(L > 0.f ? A / L : 0.f);
   }
   if (threadIdx.x == 0) counters[cidx] = 0;
 }
 
-int attention_splits(const DecoderDims& d, int M, int max_ctx) {
-  const int ctas = M * d.nkv;
-  int want = (2 * 148 + ctas - 1) / ctas;
-  int cap = (max_ctx + 127) / 128;
-  int s = want < cap ? want : cap;
-  return s < 1 ? 1 : s;
+int attention_splits(const DecoderDims&, int, int max_ctx) {
+  return (max_ctx + kAttnChunk - 1) / kAttnChunk;
 }
 
 // ------------------------------------------------------------- gather ---
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ xg, const float* __restrict__ ssq,
                                    const int32_t* __restrict__ last_row, int H, int parts,
                                    __nv_bfloat16* __restrict__ xg_out, float* __restrict__ ssq_out) {
+  sm100::griddep_wait();
   const int s = blockIdx.x;
   const int r = last_row[s];
   for (int c = threadIdx.x; c < H; c += blockDim.x)
@@ -450,6 +486,7 @@ __global__ void __launch_bounds__(kSampleThreads)
                   RoundPlan next, SlotState ss, EventRing ring, const int32_t* __restrict__ round_ctr,
                   const int32_t* __restrict__ version, int greedy) {
   __shared__ SampleShared sh;
+  sm100::griddep_wait();
   const int s = blockIdx.x;
   const int tid = threadIdx.x;
   const int ri = (*round_ctr - 1) % ring.rounds;
@@ -541,6 +578,7 @@ __global__ void __launch_bounds__(kSampleThreads)
 
 __global__ void plan_copy_kernel(RoundPlan dst, RoundPlan src, int rows, int slots,
                                  int32_t* round_ctr) {
+  sm100::griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) *round_ctr += 1;
   if (i < rows) {
@@ -677,15 +715,17 @@ void launch_rope_table(float* cs, int max_pos, int hd, double theta, cudaStream_
 void launch_embed(const __nv_bfloat16* embed, const __nv_bfloat16* gain, const int32_t* row_token,
                   int M, int H, int V, float* x, __nv_bfloat16* xg, float* ssq, cudaStream_t st) {
   // rows with an out-of-range token (padding / finished slots) embed to zero
-  embed_kernel<<<M, 128, 0, st>>>(embed, gain, row_token, H, V, x, xg, ssq);
+  launch_pdl(embed_kernel, dim3(M), dim3(128), 0, st, dim3(1, 1, 1), embed, gain, row_token, H, V,
+             x, xg, ssq);
 }
 
 void launch_rope_append(const float* qkv, const DecoderDims& d, const RoundPlan& plan, int M,
                         const float* cos_sin, const int32_t* block_table, int pages_per_seq,
                         __nv_bfloat16* kc, __nv_bfloat16* vc, __nv_bfloat16* q_out,
                         cudaStream_t st) {
-  rope_append_kernel<<<M, 128, 0, st>>>(qkv, d.nq, d.nkv, d.hd, plan.row_slot, plan.row_pos,
-                                        cos_sin, block_table, pages_per_seq, kc, vc, q_out);
+  launch_pdl(rope_append_kernel, dim3(M), dim3(128), 0, st, dim3(1, 1, 1), qkv, d.nq, d.nkv, d.hd,
+             (const int32_t*)plan.row_slot, (const int32_t*)plan.row_pos, cos_sin, block_table,
+             pages_per_seq, kc, vc, q_out);
 }
 
 size_t attention_ws_floats(const DecoderDims& d, int M, int max_ctx) {
@@ -693,37 +733,74 @@ size_t attention_ws_floats(const DecoderDims& d, int M, int max_ctx) {
   return (size_t)M * d.nkv * splits * (d.nq / d.nkv) * (d.hd + 2);
 }
 
+template <int G, int HD>
+constexpr size_t attention_smem() {
+  return sizeof(float) * G * HD + (size_t)kAttnWarps * 32 * (HD * 2 + 16) +
+         (size_t)kAttnWarps * 32 * HD * 2 + sizeof(float) * kAttnWarps * G * 32 +
+         2 * sizeof(float) * kAttnWarps * G;
+}
+
+template <int G, int HD>
+void attention_launch_t(dim3 grid, cudaStream_t st, const __nv_bfloat16* q, int nq, int nkv,
+                        const RoundPlan& plan, const int32_t* bt, int pps, const __nv_bfloat16* kc,
+                        const __nv_bfloat16* vc, float scale, float* ws, int* counters,
+                        __nv_bfloat16* out) {
+  constexpr size_t smem = attention_smem<G, HD>();
+  static bool once = [] {
+    cudaFuncSetAttribute(attention_kernel<G, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    return true;
+  }();
+  (void)once;
+  launch_pdl(attention_kernel<G, HD>, grid, dim3(32 * kAttnWarps), smem, st, dim3(1, 1, 1), q, nq,
+             nkv, (const int32_t*)plan.row_slot, (const int32_t*)plan.row_pos, bt, pps, kc, vc,
+             scale, ws, counters, out);
+}
+
+template <int HD>
+void attention_dispatch_g(int G, dim3 grid, cudaStream_t st, const __nv_bfloat16* q, int nq,
+                          int nkv, const RoundPlan& plan, const int32_t* bt, int pps,
+                          const __nv_bfloat16* kc, const __nv_bfloat16* vc, float scale, float* ws,
+                          int* counters, __nv_bfloat16* out) {
+  switch (G) {
+#define SRL_ATTN_G(g) \
+  case g: attention_launch_t<g, HD>(grid, st, q, nq, nkv, plan, bt, pps, kc, vc, scale, ws, counters, out); break;
+    SRL_ATTN_G(1) SRL_ATTN_G(2) SRL_ATTN_G(3) SRL_ATTN_G(4)
+    SRL_ATTN_G(5) SRL_ATTN_G(6) SRL_ATTN_G(7) SRL_ATTN_G(8)
+#undef SRL_ATTN_G
+    default: break;
+  }
+}
+
 void launch_attention(const __nv_bfloat16* q, const DecoderDims& d, const RoundPlan& plan, int M,
                       const int32_t* block_table, int pages_per_seq, const __nv_bfloat16* kc,
                       const __nv_bfloat16* vc, int max_ctx, float* ws, int* counters,
                       size_t ws_floats, __nv_bfloat16* out, cudaStream_t st) {
-  int splits = attention_splits(d, M, max_ctx);
-  if ((size_t)M * d.nkv * splits * (d.nq / d.nkv) * (d.hd + 2) > ws_floats) splits = 1;
-  int chunk = (max_ctx + splits - 1) / splits;
-  chunk = (chunk + 31) / 32 * 32;
+  const int splits = attention_splits(d, M, max_ctx);
+  (void)ws_floats;
   dim3 grid(M, d.nkv, splits);
   const float scale = 1.0f / sqrtf((float)d.hd);
+  const int G = d.nq / d.nkv;
   if (d.hd == 64)
-    attention_kernel<64><<<grid, 128, 0, st>>>(q, d.nq, d.nkv, plan.row_slot, plan.row_pos,
-                                               block_table, pages_per_seq, kc, vc, chunk, scale,
-                                               ws, counters, out);
+    attention_dispatch_g<64>(G, grid, st, q, d.nq, d.nkv, plan, block_table, pages_per_seq, kc,
+                             vc, scale, ws, counters, out);
   else
-    attention_kernel<128><<<grid, 128, 0, st>>>(q, d.nq, d.nkv, plan.row_slot, plan.row_pos,
-                                                block_table, pages_per_seq, kc, vc, chunk, scale,
-                                                ws, counters, out);
+    attention_dispatch_g<128>(G, grid, st, q, d.nq, d.nkv, plan, block_table, pages_per_seq, kc,
+                              vc, scale, ws, counters, out);
 }
 
 void launch_gather_rows(const __nv_bfloat16* xg, const float* ssq, const int32_t* last_row,
                         int slots, int H, int parts, __nv_bfloat16* xg_out, float* ssq_out,
                         cudaStream_t st) {
-  gather_rows_kernel<<<slots, 256, 0, st>>>(xg, ssq, last_row, H, parts, xg_out, ssq_out);
+  launch_pdl(gather_rows_kernel, dim3(slots), dim3(256), 0, st, dim3(1, 1, 1), xg, ssq, last_row, H,
+             parts, xg_out, ssq_out);
 }
 
 void launch_sample(const float* logits, int V, int slots, const RoundPlan& plan,
                    RoundPlan next_plan, SlotState ss, EventRing ring, const int32_t* round_ctr,
                    const int32_t* version, int greedy, cudaStream_t st) {
-  sample_kernel<<<slots, kSampleThreads, 0, st>>>(logits, V, slots, plan, next_plan, ss, ring,
-                                                  round_ctr, version, greedy);
+  launch_pdl(sample_kernel, dim3(slots), dim3(kSampleThreads), 0, st, dim3(1, 1, 1), logits, V,
+             slots, plan, next_plan, ss, ring, round_ctr, version, greedy);
 }
 
 void launch_row_logprobs(const float* logits, int V, int rows, const int32_t* targets, double* out,
@@ -740,7 +817,8 @@ void launch_sample_logits(const float* logits, int V, int rows, const uint64_t* 
 void launch_plan_copy(RoundPlan dst, RoundPlan src, int rows, int slots, int32_t* round_ctr,
                       cudaStream_t st) {
   const int n = rows > slots ? rows : slots;
-  plan_copy_kernel<<<(n + 255) / 256, 256, 0, st>>>(dst, src, rows, slots, round_ctr);
+  launch_pdl(plan_copy_kernel, dim3((n + 255) / 256), dim3(256), 0, st, dim3(1, 1, 1), dst, src,
+             rows, slots, round_ctr);
 }
 
 void launch_lag_stats(const int32_t* versions, const int64_t* seq_offsets, int n_seq,

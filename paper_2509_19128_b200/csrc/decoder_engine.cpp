@@ -38,6 +38,31 @@ WeightMaps build_weight_maps(const DecoderDims& d, const WeightLayout& lay, cons
   return m;
 }
 
+// -------------------------------------------------------------- timer ---
+void KernelTimer::begin(int kind) {
+  while (pool.size() < used + 2) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    pool.push_back(e);
+  }
+  kinds.push_back(kind);
+  cudaEventRecord(pool[used++], st);
+}
+void KernelTimer::end() { cudaEventRecord(pool[used++], st); }
+void KernelTimer::collect(srl_kernel_profile* out) {
+  *out = srl_kernel_profile{};
+  for (size_t i = 0; i < kinds.size(); ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pool[2 * i], pool[2 * i + 1]);
+    out->ms[kinds[i]] += ms;
+    out->launches[kinds[i]] += 1;
+  }
+  out->valid = 1;
+}
+KernelTimer::~KernelTimer() {
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
+}
+
 // ------------------------------------------------------------- runner ---
 DecoderRunner::~DecoderRunner() {
   for (void* p : allocs_) cudaFree(p);
@@ -128,7 +153,9 @@ int DecoderRunner::gemm(const CUtensorMap& tw, const CUtensorMap* tx, int M, int
 int DecoderRunner::forward(int M, const __nv_bfloat16* w, const WeightMaps& wm) {
   const int H = d.H, parts = d.ssq_parts();
   const float inv_h = 1.0f / (float)H;
+  tb(1);
   launch_embed(w + lay.embed, w + lay.layers[0].ln1, plan.row_token, M, H, d.V, x, xg, ssq, st_);
+  te();
   int st;
   for (int l = 0; l < d.L; ++l) {
     const LayerOffsets& o = lay.layers[l];
@@ -136,24 +163,36 @@ int DecoderRunner::forward(int M, const __nv_bfloat16* w, const WeightMaps& wm) 
     e.kind = EPI_STORE_F32;
     e.ssq_in = ssq; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d.eps;
     e.bias = w + o.qkv_b; e.out_f32 = qkv; e.ld_out = d.qkv();
+    tb(2);
     if ((st = gemm(wm.qkv[l], xg_map, M, d.qkv(), H, e))) return st;
+    te();
     __nv_bfloat16* kcl = kc + kv_layer_elems * l;
     __nv_bfloat16* vcl = vc + kv_layer_elems * l;
+    tb(3);
     launch_rope_append(qkv, d, plan, M, cos_sin, block_table, pages_per_seq, kcl, vcl, q, st_);
+    te();
+    tb(4);
     launch_attention(q, d, plan, M, block_table, pages_per_seq, kcl, vcl, max_seq, attn_ws,
                      attn_counters, attn_ws_floats, attn, st_);
+    te();
     EpiParams r;
     r.kind = EPI_RESID; r.resid = x; r.gain = w + o.ln2; r.xg = xg; r.ssq_out = ssq;
+    tb(5);
     if ((st = gemm(wm.o[l], attn_map, M, H, d.qdim(), r))) return st;
+    te();
     EpiParams g;
     g.kind = EPI_SWIGLU;
     g.ssq_in = ssq; g.ssq_in_parts = parts; g.inv_dim = inv_h; g.eps = d.eps;
     g.out_bf16 = act; g.ld_bf16 = d.I;
+    tb(6);
     if ((st = gemm(wm.gate_up[l], xg_map, M, 2 * d.I, H, g))) return st;
+    te();
     EpiParams r2;
     r2.kind = EPI_RESID; r2.resid = x; r2.xg = xg; r2.ssq_out = ssq;
     r2.gain = w + (l + 1 < d.L ? lay.layers[l + 1].ln1 : lay.final_norm);
+    tb(7);
     if ((st = gemm(wm.down[l], act_map, M, H, d.I, r2))) return st;
+    te();
   }
   return SRL_OK;
 }
@@ -167,7 +206,10 @@ int DecoderRunner::lm_head(int rows, const WeightMaps& wm, bool gathered) {
   e.eps = d.eps;
   e.out_f32 = logits;
   e.ld_out = d.V;
-  return gemm(wm.lm_head, gathered ? last_map : xg_map, rows, d.V, d.H, e);
+  tb(8);
+  const int st = gemm(wm.lm_head, gathered ? last_map : xg_map, rows, d.V, d.H, e);
+  te();
+  return st;
 }
 
 // ------------------------------------------------------------ backend ---
@@ -285,12 +327,16 @@ void DecoderBackend::close_slot(int slot) {
 
 int DecoderBackend::decode_round_eager(int b) {
   DecoderRunner& r = *runner_;
+  r.tb(0);
   launch_plan_copy(r.plan, r.next, S_, S_, round_ctr_dev_, st_);
+  r.te();
   int st;
   if ((st = r.forward(S_, buf_[b]->w, maps_[b]))) return st;
   if ((st = r.lm_head(S_, maps_[b], false))) return st;
+  r.tb(9);
   launch_sample(r.logits, d_.V, S_, r.plan, r.next, ss_, ring_, round_ctr_dev_, version_dev_,
                 opts_.greedy, st_);
+  r.te();
   return SRL_OK;
 }
 
@@ -365,6 +411,7 @@ int DecoderBackend::run_rounds(int n, std::vector<SlotEvent>& events, double* de
   while (done < n) {
     const int batch = std::min(n - done, R_);
     std::vector<std::vector<int>> prefilled_at(batch);
+    bool profiled = false;
     SRL_CUDA(cudaEventRecord(ev_start_, st_));
     const int64_t c0 = round_ctr_host_;
     for (int i = 0; i < batch; ++i) {
@@ -375,11 +422,24 @@ int DecoderBackend::run_rounds(int n, std::vector<SlotEvent>& events, double* de
         any_pending_ = false;
         for (const HostSlot& h : host_)
           if (h.live && h.pending) any_pending_ = true;
+        launches_ += 6 * d_.L + 5;
+      } else if (profile_next_) {
+        timer_.st = st_;
+        timer_.reset();
+        runner_->timer = &timer_;
+        st = decode_round_eager(active_);
+        runner_->timer = nullptr;
+        if (st) return st;
+        profile_next_ = false;
+        profiled = true;
+        launches_ += 6 * d_.L + 4;
       } else if (opts_.use_graphs) {
         if (!exec_[active_] && (st = capture(active_))) return st;
         SRL_CUDA(cudaGraphLaunch(exec_[active_], st_));
+        launches_ += 6 * d_.L + 4;
       } else {
         if ((st = decode_round_eager(active_))) return st;
+        launches_ += 6 * d_.L + 4;
       }
       ++round_ctr_host_;
     }
@@ -398,6 +458,10 @@ int DecoderBackend::run_rounds(int n, std::vector<SlotEvent>& events, double* de
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ev_start_, ev_stop_);
     if (device_ms) *device_ms += ms;
+    if (profiled) {
+      timer_.collect(&profile_);
+      profile_.rows = S_;
+    }
     for (int i = 0; i < batch; ++i) {
       for (int s = 0; s < S_; ++s) {
         const DevEvent& e = pe[(size_t)i * S_ + s];

@@ -15,6 +15,19 @@ struct WeightMaps {  // TMA descriptors of one flat weight buffer
 };
 WeightMaps build_weight_maps(const DecoderDims& d, const WeightLayout& lay, const __nv_bfloat16* w);
 
+// CUDA-event timer around individual launches (profiled rounds only).
+struct KernelTimer {
+  std::vector<cudaEvent_t> pool;
+  std::vector<int> kinds;
+  size_t used = 0;
+  cudaStream_t st = nullptr;
+  void begin(int kind);
+  void end();
+  void reset() { used = 0; kinds.clear(); }
+  void collect(srl_kernel_profile* out);
+  ~KernelTimer();
+};
+
 // Activations for up to M_max rows, a paged KV cache for S slots x max_seq
 // tokens, and the split-K / split-KV workspaces.
 struct DecoderRunner {
@@ -41,6 +54,9 @@ struct DecoderRunner {
   int* attn_counters = nullptr;
   size_t attn_ws_floats = 0;
   CUtensorMap xg_map[2], attn_map[2], act_map[2], last_map[2];
+  KernelTimer* timer = nullptr;  // set for a profiled round
+  void tb(int kind) { if (timer) timer->begin(kind); }
+  void te() { if (timer) timer->end(); }
 
   ~DecoderRunner();
   int init(const DecoderDims& dims, const WeightLayout& layout, int slots, int max_seq, int m_max,
@@ -69,6 +85,11 @@ class DecoderBackend final : public Backend {
   int standby(void** ptr, size_t* bytes) override;
   int commit_standby(bool recompute, int version) override;
   int slot_history(int slot, std::vector<int32_t>& out) override;
+  void request_profile() override { profile_next_ = true; }
+  bool kernel_profile(srl_kernel_profile* out) const override {
+    *out = profile_;
+    return profile_.valid != 0;
+  }
 
  private:
   struct HostSlot {
@@ -102,6 +123,9 @@ class DecoderBackend final : public Backend {
   int64_t round_ctr_host_ = 0;
   std::vector<HostSlot> host_;
   bool any_pending_ = false;
+  bool profile_next_ = false;
+  srl_kernel_profile profile_{};
+  KernelTimer timer_;
 };
 
 }  // namespace srl

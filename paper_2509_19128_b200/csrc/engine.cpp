@@ -331,7 +331,19 @@ int Engine::stream_tokens(int64_t id, std::vector<int32_t>& out) {
 
 srl_engine_stats Engine::stats() const {
   std::lock_guard<std::mutex> lk(lock_);
-  return stats_;
+  srl_engine_stats s = stats_;
+  s.launches = backend_->launches();
+  return s;
+}
+
+void Engine::profile_next_round() {
+  std::lock_guard<std::mutex> lk(lock_);
+  backend_->request_profile();
+}
+
+bool Engine::kernel_profile(srl_kernel_profile* out) const {
+  std::lock_guard<std::mutex> lk(lock_);
+  return backend_->kernel_profile(out);
 }
 
 }  // namespace srl

@@ -5,12 +5,21 @@
 // deep 128B-swizzled ring; warp1/elected lane issues tcgen05.mma (UMMA
 // 128 x TOK x 16) and releases ring slots with tcgen05.commit; afterwards all
 // four warps drain TMEM (tcgen05.ld 32x32b) into a shared tile and run the
-// epilogue.  Skinny decode GEMMs use a deterministic split-K: every split
-// stores its partial tile, the last-arriving CTA sums the partials in split
-// order (so results are bit-reproducible run to run) and runs the epilogue.
+// epilogue.
+//
+// Skinny (decode) GEMMs split K across a thread-block cluster of CS CTAs:
+// every CTA stages its fp32 partial tile in its own shared memory, and after a
+// cluster barrier CTA r reduces rows [r*TOK/CS, (r+1)*TOK/CS) by reading the
+// CS partials through distributed shared memory in rank order -- so the
+// result is bit-reproducible and no partial ever touches L2/HBM -- then runs
+// the epilogue for those rows.
+//
+// Programmatic dependent launch: the weights do not depend on the previous
+// kernel, so the producer issues the first STAGES weight tiles before
+// griddepcontrol.wait; only the activation tiles and the epilogue inputs wait.
 #include <cstdio>
-#include <cstring>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "gemm.cuh"
@@ -24,13 +33,14 @@ namespace {
 constexpr int kBlockN = 128;  // weight rows per tile (UMMA M)
 constexpr int kBlockK = 64;   // bf16 elements per 128-B swizzle row
 constexpr int kThreads = 128;
+constexpr int kMaxCluster = 8;
 
 template <int TOK, int STAGES>
 struct Layout {
   static constexpr int kABytes = kBlockN * kBlockK * 2;
   static constexpr int kBBytes = TOK * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kPitch = kBlockN + 4;
+  static constexpr int kPitch = kBlockN + 4;  // floats; rows stay 16-B aligned
   static constexpr int kEpiBytes = TOK * kPitch * 4;
   static constexpr int kMainBytes =
       STAGES * kStageBytes > kEpiBytes ? STAGES * kStageBytes : kEpiBytes;
@@ -52,8 +62,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 template <int TOK, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
-                     int M, int N, int K, int splits, int kb_per_split, float* __restrict__ ws,
-                     int* __restrict__ counters, const EpiParams epi) {
+                     int M, int N, int K, int cs, const EpiParams epi) {
   using L = Layout<TOK, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -62,19 +71,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kMiscOffset);
-  int* s_flag = reinterpret_cast<int*>(smem + L::kMiscOffset + 4);
   float* s_rstd = reinterpret_cast<float*>(smem + L::kRstdOffset);
   float* tile = reinterpret_cast<float*>(smem);  // epilogue view, aliases the ring
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tile = blockIdx.x, split = blockIdx.y, tok_tile = blockIdx.z;
   const int n_tiles = gridDim.x;
-  const int tile_id = tok_tile * n_tiles + n_tile;
   const int n0 = n_tile * kBlockN, t0 = tok_tile * TOK;
   const int kb_total = K / kBlockK;
-  const int kb_begin = split * kb_per_split;
-  const int kb_end = min(kb_total, kb_begin + kb_per_split);
-  const int nkb = kb_end - kb_begin;
+  const int kb_begin = (split * kb_total) / cs;
+  const int nkb = ((split + 1) * kb_total) / cs - kb_begin;  // >= 1 (host: cs <= kb_total)
 
   if (warp == 0) {
     if (elect_one()) {
@@ -98,20 +104,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_launch_dependents();  // the next kernel may start its prologue now
 
   if (warp == 0) {
     if (elect_one()) {  // ---- TMA producer
       const uint64_t w_policy = policy_evict_first();
-      for (int i = 0; i < nkb; ++i) {
+      const int pre = nkb < STAGES ? nkb : STAGES;
+      for (int i = 0; i < pre; ++i) {  // weights first: independent of the previous kernel
+        uint8_t* a = smem + i * L::kStageBytes;
+        mbar_arrive_expect_tx(&full[i], L::kStageBytes);
+        tma_load_2d_hint(a, &tw, &full[i], (kb_begin + i) * kBlockK, n0, w_policy);
+      }
+      griddep_wait();  // activations are produced by the previous kernel
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(smem + i * L::kStageBytes + L::kABytes, &tx, &full[i],
+                    (kb_begin + i) * kBlockK, t0);
+      for (int i = pre; i < nkb; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* a = smem + s * L::kStageBytes;
-        uint8_t* b = a + L::kABytes;
         mbar_arrive_expect_tx(&full[s], L::kStageBytes);
         const int kc = (kb_begin + i) * kBlockK;
         tma_load_2d_hint(a, &tw, &full[s], kc, n0, w_policy);
-        tma_load_2d(b, &tx, &full[s], kc, t0);
+        tma_load_2d(a + L::kABytes, &tx, &full[s], kc, t0);
       }
     }
     __syncwarp();
@@ -136,54 +152,59 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   }
 
-  // ---- drain TMEM: thread = weight row (TMEM lane), columns = tokens
+  // ---- drain TMEM into the shared tile: thread = weight row (TMEM lane)
   mbar_wait(done, 0);
   tc_fence_after();
   const int row = threadIdx.x;
   const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-  const size_t tiles_total = (size_t)n_tiles * gridDim.z;
-  if (splits == 1) {
 #pragma unroll
-    for (int c0 = 0; c0 < TOK; c0 += 16) {
-      uint32_t r[16];
-      tmem_ld_32x32b_x16(lane_addr + c0, r);
-      tmem_ld_wait();
+  for (int c0 = 0; c0 < TOK; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld_32x32b_x16(lane_addr + c0, r);
+    tmem_ld_wait();
 #pragma unroll
-      for (int j = 0; j < 16; ++j) tile[(c0 + j) * L::kPitch + row] = __uint_as_float(r[j]);
-    }
-  } else {
-    float* mine = ws + ((size_t)split * tiles_total + tile_id) * (size_t)(TOK * kBlockN);
-#pragma unroll
-    for (int c0 = 0; c0 < TOK; c0 += 16) {
-      uint32_t r[16];
-      tmem_ld_32x32b_x16(lane_addr + c0, r);
-      tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) __stcg(&mine[(c0 + j) * kBlockN + row], __uint_as_float(r[j]));
-    }
+    for (int j = 0; j < 16; ++j) tile[(c0 + j) * L::kPitch + row] = __uint_as_float(r[j]);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_free<TOK>(tmem);
 
-  if (splits > 1) {
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) *s_flag = (atomicAdd(&counters[tile_id], 1) == splits - 1);
-    __syncthreads();
-    if (!*s_flag) return;
-    __threadfence();
-    for (int j = 0; j < TOK; ++j) {
-      float acc = 0.f;
-      for (int s = 0; s < splits; ++s)
-        acc += __ldcg(&ws[(((size_t)s * tiles_total + tile_id) * TOK + j) * kBlockN + row]);
-      tile[j * L::kPitch + row] = acc;
+  // ---- split-K: reduce this CTA's row slice over the cluster through DSMEM
+  int r0 = 0, r1 = TOK;
+  if (cs > 1) {
+    r0 = (split * TOK) / cs;
+    r1 = ((split + 1) * TOK) / cs;
+    cluster_sync();  // every partial tile is staged
+    const int n4 = (r1 - r0) * (kBlockN / 4);
+    constexpr int kMaxPer = (TOK / 2) * (kBlockN / 4) / kThreads + 1;  // cs >= 2
+    float4 acc[kMaxPer];
+#pragma unroll
+    for (int k = 0; k < kMaxPer; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < cs; ++q) {  // rank order: deterministic
+#pragma unroll
+      for (int k = 0; k < kMaxPer; ++k) {
+        const int i = threadIdx.x + k * kThreads;
+        if (i < n4) {
+          const int j = r0 + i / (kBlockN / 4), c = (i % (kBlockN / 4)) * 4;
+          const float4 v = dsmem_ld_f4(dsmem_map(smem_u32(&tile[j * L::kPitch + c]), q));
+          acc[k].x += v.x; acc[k].y += v.y; acc[k].z += v.z; acc[k].w += v.w;
+        }
+      }
     }
-    if (threadIdx.x == 0) counters[tile_id] = 0;  // self-reset for the next launch / graph replay
+    cluster_sync();  // all remote reads done before anyone overwrites / exits
+#pragma unroll
+    for (int k = 0; k < kMaxPer; ++k) {
+      const int i = threadIdx.x + k * kThreads;
+      if (i < n4) {
+        const int j = r0 + i / (kBlockN / 4), c = (i % (kBlockN / 4)) * 4;
+        *reinterpret_cast<float4*>(&tile[j * L::kPitch + c]) = acc[k];
+      }
+    }
   }
 
-  // ---- epilogue
-  for (int j = threadIdx.x; j < TOK; j += kThreads) {
+  // ---- epilogue over rows [r0, r1)
+  griddep_wait();  // epilogue inputs (ssq, residual) come from earlier kernels
+  for (int j = r0 + threadIdx.x; j < r1; j += kThreads) {
     float r = 1.f;
     const int m = t0 + j;
     if (epi.ssq_in != nullptr && m < M) {
@@ -195,9 +216,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
 
+  const int rows = r1 - r0;
   if (epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16) {
-    for (int idx = threadIdx.x; idx < TOK * kBlockN; idx += kThreads) {
-      const int j = idx >> 7, c = idx & 127;
+    for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
       const int m = t0 + j, n = n0 + c;
       if (m >= M || n >= N) continue;
       float v = tile[j * L::kPitch + c] * s_rstd[j];
@@ -208,8 +230,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         epi.out_bf16[(size_t)m * epi.ld_bf16 + n] = __float2bfloat16(v);
     }
   } else if (epi.kind == EPI_SWIGLU) {
-    for (int idx = threadIdx.x; idx < TOK * (kBlockN / 2); idx += kThreads) {
-      const int j = idx >> 6, c = idx & 63;
+    for (int idx = threadIdx.x; idx < rows * (kBlockN / 2); idx += kThreads) {
+      const int j = r0 + (idx >> 6), c = idx & 63;
       const int m = t0 + j;
       if (m >= M || n0 + c >= N) continue;
       const float g = tile[j * L::kPitch + c] * s_rstd[j];
@@ -218,8 +240,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       epi.out_bf16[(size_t)m * epi.ld_bf16 + (n0 >> 1) + c] = __float2bfloat16(a);
     }
   } else if (epi.kind == EPI_RESID) {
-    for (int idx = threadIdx.x; idx < TOK * kBlockN; idx += kThreads) {
-      const int j = idx >> 7, c = idx & 127;
+    for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
       const int m = t0 + j, n = n0 + c;
       float x = 0.f;
       if (m < M && n < N) {
@@ -231,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile[j * L::kPitch + c] = x;
     }
     __syncthreads();
-    for (int j = warp; j < TOK; j += kThreads / 32) {
+    for (int j = r0 + warp; j < r1; j += kThreads / 32) {
       float s = 0.f;
       for (int c = lane; c < kBlockN; c += 32) {
         const float x = tile[j * L::kPitch + c];
@@ -244,9 +266,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int TOK, int STAGES>
-cudaError_t launch_impl(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K,
-                        int splits, const GemmWorkspace& ws, const EpiParams& epi,
-                        cudaStream_t stream) {
+cudaError_t launch_impl(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int cs,
+                        const EpiParams& epi, cudaStream_t stream) {
   using L = Layout<TOK, STAGES>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -255,21 +276,10 @@ cudaError_t launch_impl(const CUtensorMap& tw, const CUtensorMap& tx, int M, int
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  const int kb = K / kBlockK;
-  const int kb_per = (kb + splits - 1) / splits;
-  const int eff_splits = (kb + kb_per - 1) / kb_per;
   const int n_tiles = (N + kBlockN - 1) / kBlockN;
   const int tok_tiles = (M + TOK - 1) / TOK;
-  if (eff_splits > 1) {
-    const size_t need = (size_t)eff_splits * n_tiles * tok_tiles * TOK * kBlockN;
-    if (ws.partials == nullptr || need > ws.partial_floats ||
-        ws.counter_count < n_tiles * tok_tiles)
-      return cudaErrorInvalidValue;
-  }
-  dim3 grid(n_tiles, eff_splits, tok_tiles);
-  gemm_bf16_kernel<TOK, STAGES><<<grid, kThreads, L::kAlloc, stream>>>(
-      tw, tx, M, N, K, eff_splits, kb_per, ws.partials, ws.counters, epi);
-  return cudaGetLastError();
+  return launch_pdl(gemm_bf16_kernel<TOK, STAGES>, dim3(n_tiles, cs, tok_tiles), dim3(kThreads),
+                    (size_t)L::kAlloc, stream, dim3(1, cs, 1), tw, tx, M, N, K, cs, epi);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -318,30 +328,29 @@ CUtensorMap make_tmap_bf16(const void* ptr, uint64_t rows, uint64_t cols, uint32
 
 int gemm_tok_tile(int M) { return M <= 64 ? 64 : 128; }
 
+// Cluster split-K factor: a power of two <= 8, at least two k-blocks per
+// split, growing while the grid is below ~1.5 waves of the machine.
 int gemm_auto_splits(int M, int N, int K, int num_sms) {
   const int tok = gemm_tok_tile(M);
   const int tiles = ((N + kBlockN - 1) / kBlockN) * ((M + tok - 1) / tok);
   const int kb = K / kBlockK;
-  if (tiles >= num_sms || kb < 4) return 1;
-  int want = (2 * num_sms + tiles - 1) / tiles;
-  int cap = kb / 2;  // at least two k-blocks per split
-  int s = want < cap ? want : cap;
-  return s < 1 ? 1 : s;
+  int cs = 1;
+  while (cs * 2 <= kMaxCluster && kb >= 2 * (cs * 2) && tiles * cs * 2 <= (3 * num_sms) / 2) cs *= 2;
+  return cs;
 }
 
-size_t gemm_workspace_floats(int M, int N, int splits) {
-  const int tok = gemm_tok_tile(M);
-  return (size_t)splits * ((N + kBlockN - 1) / kBlockN) * ((M + tok - 1) / tok) * tok * kBlockN;
-}
+size_t gemm_workspace_floats(int, int, int) { return 0; }  // partials live in DSMEM
 
 cudaError_t gemm_bf16_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K,
-                             int splits, const GemmWorkspace& ws, const EpiParams& epi,
+                             int splits, const GemmWorkspace&, const EpiParams& epi,
                              cudaStream_t stream) {
   if (M < 1 || N < 1 || K < kBlockK || K % kBlockK != 0 || splits < 1)
     return cudaErrorInvalidValue;
   if (epi.kind == EPI_SWIGLU && N % kBlockN != 0) return cudaErrorInvalidValue;
-  if (gemm_tok_tile(M) == 64) return launch_impl<64, 4>(tw, tx, M, N, K, splits, ws, epi, stream);
-  return launch_impl<128, 4>(tw, tx, M, N, K, splits, ws, epi, stream);
+  int cs = 1;
+  while (cs * 2 <= splits && cs * 2 <= kMaxCluster && cs * 2 <= K / kBlockK) cs *= 2;
+  if (gemm_tok_tile(M) == 64) return launch_impl<64, 4>(tw, tx, M, N, K, cs, epi, stream);
+  return launch_impl<128, 4>(tw, tx, M, N, K, cs, epi, stream);
 }
 
 }  // namespace srl

@@ -109,6 +109,9 @@ class Backend {
   virtual int standby(void** ptr, size_t* bytes) { return fail(SRL_INVALID_ARGUMENT, "no standby buffer for this policy type"); }
   virtual int commit_standby(bool recompute, int version) { return fail(SRL_INVALID_ARGUMENT, "no standby buffer"); }
   virtual int slot_history(int slot, std::vector<int32_t>& out) = 0;
+  virtual void request_profile() {}
+  virtual bool kernel_profile(srl_kernel_profile* out) const { return false; }
+  virtual int64_t launches() const { return launches_; }
   virtual int prompt_index(const std::string& prompt_id) { return intern(prompt_id); }
   int intern(const std::string& s) {
     auto it = prompts_.find(s);
@@ -120,6 +123,7 @@ class Backend {
 
  protected:
   std::map<std::string, int> prompts_;
+  int64_t launches_ = 0;
 };
 
 std::unique_ptr<Backend> make_toy_backend(const Policy& p, const srl_engine_options& o, int* status);
@@ -151,6 +155,8 @@ class Engine {
   void stop();
   int stream_tokens(int64_t id, std::vector<int32_t>& out);
   srl_engine_stats stats() const;
+  void profile_next_round();
+  bool kernel_profile(srl_kernel_profile* out) const;
 
  private:
   struct Stream {

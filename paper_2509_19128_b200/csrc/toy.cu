@@ -342,6 +342,7 @@ class ToyBackend final : public Backend {
       cudaEventCreate(&e1);
       cudaEventRecord(e0, st_);
       for (int r = 0; r < batch; ++r) toy_round_kernel<<<S_, kToyThreads, smem, st_>>>(t, S_, r);
+      launches_ += batch;
       cudaEventRecord(e1, st_);
       const size_t cnt = (size_t)batch * S_;
       int32_t* pf = static_cast<int32_t*>(pinned_);

@@ -213,6 +213,15 @@ class Engine:
         _raise_for(_lib.lib().srl_engine_stats_get(self._h, C.byref(s)), "stats")
         return {k: getattr(s, k) for k, _ in s._fields_}
 
+    def profile_next_round(self):
+        """Time every launch of the next decode round with CUDA events."""
+        _raise_for(_lib.lib().srl_engine_profile_next_round(self._h), "profile_next_round")
+
+    def kernel_profile(self) -> dict:
+        p = _lib.KernelProfileC()
+        _raise_for(_lib.lib().srl_engine_kernel_profile(self._h, C.byref(p)), "kernel_profile")
+        return {name: (p.ms[i], p.launches[i]) for i, name in enumerate(_lib.KERNEL_CLASSES)}
+
     def close(self):
         if getattr(self, "_h", None):
             _lib.lib().srl_engine_destroy(self._h)
