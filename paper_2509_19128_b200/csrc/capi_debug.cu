@@ -19,6 +19,9 @@ int num_sms() {
 }
 }  // namespace
 
+static unsigned long long* g_stamps = nullptr;  // debug phase stamps (srl_debug_gemm_stamps)
+extern "C" void srl_debug_gemm_stamps(unsigned long long* device_buf) { g_stamps = device_buf; }
+
 extern "C" int srl_kernel_gemm_bf16(const void* w, const void* x, int32_t M, int32_t N, int32_t K,
                                     int32_t splits, int32_t epi_kind, const void* bias,
                                     const float* ssq_in, int32_t ssq_parts, float inv_dim,
@@ -32,6 +35,7 @@ extern "C" int srl_kernel_gemm_bf16(const void* w, const void* x, int32_t M, int
   GemmWorkspace ws;  // cluster split-K reduces through DSMEM: no workspace
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   EpiParams epi;
+  epi.stamps = g_stamps;
   epi.kind = epi_kind;
   epi.ssq_in = ssq_in;
   epi.ssq_in_parts = ssq_parts;

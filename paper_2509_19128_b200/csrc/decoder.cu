@@ -367,7 +367,7 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ xg, const f
 }
 
 // ------------------------------------------------------------- sample ---
-constexpr int kSampleThreads = 1024;
+constexpr int kSampleThreads = 512;
 
 __device__ double block_sum_d(double v, double* red) {
   // fixed-order reduction: warp tree, then warp 0 over the 32 warp sums
@@ -377,7 +377,7 @@ __device__ double block_sum_d(double v, double* red) {
   __syncthreads();
   if (l == 0) red[w] = v;
   __syncthreads();
-  double t = (threadIdx.x < 32) ? red[l] : 0.0;
+  double t = (threadIdx.x < (blockDim.x >> 5)) ? red[l] : 0.0;  // only warps that exist
   if (w == 0) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
@@ -387,60 +387,113 @@ __device__ double block_sum_d(double v, double* red) {
   return red[32];
 }
 
+constexpr int kTile = 128;  // LM-head GEMM tile width (columns per partial)
+
 struct SampleShared {
   double red[33];
   float fred[32];
   int ired[32];
   double scan[kSampleThreads];
+  int tile;
   int tok;
 };
 
-// Block-wide: log-softmax statistics of one logits row in fp64 and the
-// SplitMix64 inverse-CDF draw with uniform u (rng.hpp:61-69), or greedy
-// argmax (lowest index on ties).  Returns the token; *lse_out = logsumexp.
-__device__ int sample_row(const float* __restrict__ x, int V, double u, int greedy,
-                          SampleShared& sh, double* lse_out) {
-  const int tid = threadIdx.x;
-  // pass 1: max (+argmax), then fp64 sum of exp(x - max)  (numeric.hpp:13-20)
+// Per (row, 128-column tile): max and fp64 sum of exp(x - max).  The LM-head
+// GEMM epilogue (EPI_LOGITS) produces the same statistics; this kernel serves
+// raw logits handed to srl_kernel_sample_logits.
+__global__ void tile_stats_kernel(const float* __restrict__ logits, int V, float* __restrict__ pmax,
+                                  double* __restrict__ psum) {
+  const int row = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = (V + kTile - 1) / kTile;
+  const int t = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (t >= T) return;
+  const float* x = logits + (size_t)row * V + (size_t)t * kTile;
+  float v[4];
   float mx = -INFINITY;
-  int amax = 0x7fffffff;
-  for (int k = tid; k < V; k += kSampleThreads) {
-    const float v = x[k];
-    if (v > mx) { mx = v; amax = k; }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = t * kTile + lane * 4 + i;
+    v[i] = k < V ? x[lane * 4 + i] : -INFINITY;
+    mx = fmaxf(mx, v[i]);
+  }
+  mx = warp_max(mx);
+  double s = 0.0;
+  if (mx != -INFINITY)
+    for (int i = 0; i < 4; ++i) s += exp((double)v[i] - (double)mx);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    pmax[(size_t)row * T + t] = mx;
+    psum[(size_t)row * T + t] = s;
+  }
+}
+
+// Block-wide sampling of one logits row from its tile partials.
+//   lse = M + log(sum_t s_t * exp(m_t - M))                 (numeric.hpp:13-20)
+//   tile masses q_t = s_t * exp(m_t - lse), inclusive scan over thread chunks
+//   the first tile whose walk may cross u is walked element by element with
+//   p_k = exp(x_k - lse) in fp64: the inverse CDF of rng.hpp:61-69 with a
+//   fixed-order (tile, lane) summation; rounding slack past the last element
+//   falls back to V-1 like the reference.
+// Greedy: argmax over the row, lowest index on ties.
+__device__ int sample_row(const float* __restrict__ x, int V, const float* __restrict__ pmax,
+                          const double* __restrict__ psum, double u, int greedy, SampleShared& sh,
+                          double* lse_out) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T = (V + kTile - 1) / kTile;
+  const int C = (T + kSampleThreads - 1) / kSampleThreads;  // tiles per thread (contiguous)
+  const int t0 = tid * C, t1 = min(T, t0 + C);
+  float mx = -INFINITY;
+  int mt = 0x7fffffff;
+  for (int t = t0; t < t1; ++t) {
+    const float v = pmax[t];
+    if (v > mx) { mx = v; mt = t; }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float om = __shfl_xor_sync(0xffffffffu, mx, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, amax, o);
-    if (om > mx || (om == mx && oi < amax)) { mx = om; amax = oi; }
+    const int oi = __shfl_xor_sync(0xffffffffu, mt, o);
+    if (om > mx || (om == mx && oi < mt)) { mx = om; mt = oi; }
   }
-  if ((tid & 31) == 0) { sh.fred[tid >> 5] = mx; sh.ired[tid >> 5] = amax; }
+  if (lane == 0) { sh.fred[warp] = mx; sh.ired[warp] = mt; }
   __syncthreads();
   if (tid < 32) {
-    mx = sh.fred[tid];
-    amax = sh.ired[tid];
+    mx = tid < kSampleThreads / 32 ? sh.fred[tid] : -INFINITY;
+    mt = tid < kSampleThreads / 32 ? sh.ired[tid] : 0x7fffffff;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const float om = __shfl_xor_sync(0xffffffffu, mx, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, amax, o);
-      if (om > mx || (om == mx && oi < amax)) { mx = om; amax = oi; }
+      const int oi = __shfl_xor_sync(0xffffffffu, mt, o);
+      if (om > mx || (om == mx && oi < mt)) { mx = om; mt = oi; }
     }
-    if (tid == 0) { sh.fred[0] = mx; sh.ired[0] = amax; }
+    if (tid == 0) { sh.fred[0] = mx; sh.ired[0] = mt; }
   }
   __syncthreads();
-  const double M = (double)sh.fred[0];
-  const int argmax = sh.ired[0];
+  const float Mf = sh.fred[0];
+  const double M = (double)Mf;
+  const int mtile = sh.ired[0];
   double part = 0.0;
-  for (int k = tid; k < V; k += kSampleThreads) part += exp((double)x[k] - M);
+  for (int t = t0; t < t1; ++t) part += psum[t] * exp((double)pmax[t] - M);
   const double lse = M + log(block_sum_d(part, sh.red));
   *lse_out = lse;
-  if (greedy) return argmax;
 
-  // pass 2: contiguous chunk per thread, inclusive scan of chunk masses
-  const int C = (V + kSampleThreads - 1) / kSampleThreads;
-  const int k0 = tid * C, k1 = min(V, k0 + C);
+  if (greedy) {  // first element equal to the max inside the first max tile
+    if (warp == 0) {
+      int best = 0x7fffffff;
+      for (int i = lane; i < kTile; i += 32) {
+        const int k = mtile * kTile + i;
+        if (k < V && x[k] == Mf) best = min(best, k);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (lane == 0) sh.tok = best == 0x7fffffff ? mtile * kTile : best;
+    }
+    __syncthreads();
+    return sh.tok;
+  }
+
   double mass = 0.0;
-  for (int k = k0; k < k1; ++k) mass += exp((double)x[k] - lse);
+  for (int t = t0; t < t1; ++t) mass += psum[t] * exp((double)pmax[t] - lse);
   sh.scan[tid] = mass;
   __syncthreads();
   for (int o = 1; o < kSampleThreads; o <<= 1) {  // Hillis-Steele, fixed order
@@ -449,40 +502,81 @@ __device__ int sample_row(const float* __restrict__ x, int V, double u, int gree
     sh.scan[tid] += add;
     __syncthreads();
   }
-  // Every thread's result equals a full walk of its chunk from `base`:
-  // u < base means the walk stops at k0; u past the chunk's mass (plus a
-  // margin far above the fp64 rounding of the two summation orders) means
-  // it never stops; otherwise walk.  The first chunk that stops wins.
-  const double base = tid == 0 ? 0.0 : sh.scan[tid - 1];
-  int found = 0x7fffffff;
-  if (k0 < k1) {
-    if (u < base) {
-      found = k0;
-    } else if (u < sh.scan[tid] + 1e-12) {
-      double cum = base;
-      for (int k = k0; k < k1; ++k) {
-        cum += exp((double)x[k] - lse);
-        if (u < cum) { found = k; break; }
+  // first tile whose [base, base + mass + margin) may contain u
+  int cand = 0x7fffffff;
+  {
+    double base = tid == 0 ? 0.0 : sh.scan[tid - 1];
+    if (u < sh.scan[tid] + 1e-12) {
+      for (int t = t0; t < t1; ++t) {
+        const double q = psum[t] * exp((double)pmax[t] - lse);
+        if (u < base + q + 1e-12) { cand = t; break; }
+        base += q;
       }
     }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) found = min(found, __shfl_xor_sync(0xffffffffu, found, o));
+  for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
   __syncthreads();
-  if ((tid & 31) == 0) sh.ired[tid >> 5] = found;
+  if (lane == 0) sh.ired[warp] = cand;
   __syncthreads();
   if (tid < 32) {
-    int f = sh.ired[tid];
+    int c = tid < kSampleThreads / 32 ? sh.ired[tid] : 0x7fffffff;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, o));
-    if (tid == 0) sh.tok = (f == 0x7fffffff) ? V - 1 : f;  // rounding slack -> V-1
+    for (int o = 16; o > 0; o >>= 1) c = min(c, __shfl_xor_sync(0xffffffffu, c, o));
+    if (tid == 0) sh.tile = c;
+  }
+  __syncthreads();
+  // warp 0 walks from the candidate tile; base = prefix of tile masses in the
+  // same (thread chunk, tile) order as the scan
+  if (warp == 0) {
+    int tok = V - 1;
+    int t = sh.tile;
+    if (t != 0x7fffffff) {
+      const int owner = t / C;
+      double base = owner == 0 ? 0.0 : sh.scan[owner - 1];
+      for (int tt = owner * C; tt < t; ++tt) base += psum[tt] * exp((double)pmax[tt] - lse);
+      bool done = false;
+      for (; t < T && !done; ++t) {
+        double p[4];
+        double ls = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int k = t * kTile + lane * 4 + i;
+          p[i] = k < V ? exp((double)x[k] - lse) : 0.0;
+          ls += p[i];
+        }
+        double incl = ls;  // inclusive warp scan of lane sums (fixed order)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double n = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += n;
+        }
+        double cum = base + (incl - ls);
+        int found = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          cum += p[i];
+          const int k = t * kTile + lane * 4 + i;
+          if (found == 0x7fffffff && k < V && u < cum) found = k;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) found = min(found, __shfl_xor_sync(0xffffffffu, found, o));
+        if (found != 0x7fffffff) {
+          tok = found;
+          done = true;
+        }
+        base += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    if (lane == 0) sh.tok = tok;
   }
   __syncthreads();
   return sh.tok;
 }
 
 __global__ void __launch_bounds__(kSampleThreads)
-    sample_kernel(const float* __restrict__ logits, int V, int slots, RoundPlan plan,
+    sample_kernel(const float* __restrict__ logits, const float* __restrict__ pmax,
+                  const double* __restrict__ psum, int V, int slots, RoundPlan plan,
                   RoundPlan next, SlotState ss, EventRing ring, const int32_t* __restrict__ round_ctr,
                   const int32_t* __restrict__ version, int greedy) {
   __shared__ SampleShared sh;
@@ -503,9 +597,10 @@ __global__ void __launch_bounds__(kSampleThreads)
     return;
   }
   const float* x = logits + (size_t)s * V;
+  const int T = (V + kTile - 1) / kTile;
   const double u = splitmix_uniform(ss.seed[s], (uint64_t)ss.gen_count[s]);
   double lse;
-  const int tok = sample_row(x, V, u, greedy, sh, &lse);
+  const int tok = sample_row(x, V, pmax + (size_t)s * T, psum + (size_t)s * T, u, greedy, sh, &lse);
 
   if (tid == 0) {
     const int pos_row = plan.row_pos[r];
@@ -549,7 +644,7 @@ __global__ void __launch_bounds__(kSampleThreads)
   if ((tid & 31) == 0) fred[tid >> 5] = mx;
   __syncthreads();
   if (tid < 32) {
-    float v = warp_max(fred[tid]);
+    float v = warp_max(tid < (kSampleThreads >> 5) ? fred[tid] : -INFINITY);
     if (tid == 0) fred[0] = v;
   }
   __syncthreads();
@@ -561,15 +656,17 @@ __global__ void __launch_bounds__(kSampleThreads)
 }
 
 __global__ void __launch_bounds__(kSampleThreads)
-    sample_logits_kernel(const float* __restrict__ logits, int V, const uint64_t* __restrict__ seeds,
+    sample_logits_kernel(const float* __restrict__ logits, const float* __restrict__ pmax,
+                         const double* __restrict__ psum, int V, const uint64_t* __restrict__ seeds,
                          const int32_t* __restrict__ draw, int greedy, int32_t* __restrict__ tok_out,
                          double* __restrict__ lp_out) {
   __shared__ SampleShared sh;
   const int r = blockIdx.x;
   const float* x = logits + (size_t)r * V;
+  const int T = (V + kTile - 1) / kTile;
   const double u = splitmix_uniform(seeds[r], (uint64_t)draw[r]);
   double lse;
-  const int tok = sample_row(x, V, u, greedy, sh, &lse);
+  const int tok = sample_row(x, V, pmax + (size_t)r * T, psum + (size_t)r * T, u, greedy, sh, &lse);
   if (threadIdx.x == 0) {
     tok_out[r] = tok;
     lp_out[r] = (double)x[tok] - lse;
@@ -796,11 +893,11 @@ void launch_gather_rows(const __nv_bfloat16* xg, const float* ssq, const int32_t
              parts, xg_out, ssq_out);
 }
 
-void launch_sample(const float* logits, int V, int slots, const RoundPlan& plan,
-                   RoundPlan next_plan, SlotState ss, EventRing ring, const int32_t* round_ctr,
-                   const int32_t* version, int greedy, cudaStream_t st) {
-  launch_pdl(sample_kernel, dim3(slots), dim3(kSampleThreads), 0, st, dim3(1, 1, 1), logits, V,
-             slots, plan, next_plan, ss, ring, round_ctr, version, greedy);
+void launch_sample(const float* logits, const float* pmax, const double* psum, int V, int slots,
+                   const RoundPlan& plan, RoundPlan next_plan, SlotState ss, EventRing ring,
+                   const int32_t* round_ctr, const int32_t* version, int greedy, cudaStream_t st) {
+  launch_pdl(sample_kernel, dim3(slots), dim3(kSampleThreads), 0, st, dim3(1, 1, 1), logits, pmax,
+             psum, V, slots, plan, next_plan, ss, ring, round_ctr, version, greedy);
 }
 
 void launch_row_logprobs(const float* logits, int V, int rows, const int32_t* targets, double* out,
@@ -810,8 +907,17 @@ void launch_row_logprobs(const float* logits, int V, int rows, const int32_t* ta
 
 void launch_sample_logits(const float* logits, int V, int rows, const uint64_t* seeds,
                           const int32_t* draw, int greedy, int32_t* tok, double* lp, cudaStream_t st) {
-  if (rows > 0)
-    sample_logits_kernel<<<rows, kSampleThreads, 0, st>>>(logits, V, seeds, draw, greedy, tok, lp);
+  if (rows <= 0) return;
+  const int T = (V + kTile - 1) / kTile;
+  float* pmax = nullptr;
+  double* psum = nullptr;
+  cudaMallocAsync(&pmax, sizeof(float) * (size_t)rows * T, st);
+  cudaMallocAsync(&psum, sizeof(double) * (size_t)rows * T, st);
+  tile_stats_kernel<<<dim3((T + 7) / 8, rows), 256, 0, st>>>(logits, V, pmax, psum);
+  sample_logits_kernel<<<rows, kSampleThreads, 0, st>>>(logits, pmax, psum, V, seeds, draw, greedy,
+                                                        tok, lp);
+  cudaFreeAsync(pmax, st);
+  cudaFreeAsync(psum, st);
 }
 
 void launch_plan_copy(RoundPlan dst, RoundPlan src, int rows, int slots, int32_t* round_ctr,

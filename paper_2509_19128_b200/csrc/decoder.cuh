@@ -103,9 +103,9 @@ void launch_gather_rows(const __nv_bfloat16* xg, const float* ssq, const int32_t
 // fp64 log-softmax + SplitMix64 inverse-CDF (or greedy argmax) sampling of
 // each emitting slot's logits row; emits events, advances slot state and
 // writes next round's decode plan.
-void launch_sample(const float* logits, int V, int slots, const RoundPlan& plan,
-                   RoundPlan next_plan, SlotState ss, EventRing ring, const int32_t* round_ctr,
-                   const int32_t* version, int greedy, cudaStream_t st);
+void launch_sample(const float* logits, const float* pmax, const double* psum, int V, int slots,
+                   const RoundPlan& plan, RoundPlan next_plan, SlotState ss, EventRing ring,
+                   const int32_t* round_ctr, const int32_t* version, int greedy, cudaStream_t st);
 
 // Sampler over raw logits rows (row r draws uniform #draw[r] of seeds[r]).
 void launch_sample_logits(const float* logits, int V, int rows, const uint64_t* seeds,

@@ -7,6 +7,7 @@
 // token boundaries, optional KV recompute after a swap).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "decoder_engine.hpp"
@@ -81,6 +82,7 @@ int DecoderRunner::init(const DecoderDims& dims, const WeightLayout& layout, int
   dev = device;
   st_ = st;
   sms = sm_count(device);
+  unfused_qkv = std::getenv("SRL_UNFUSED_QKV") != nullptr;  // A/B switch: separate RoPE kernel
   const int H = d.H, parts = d.ssq_parts();
   auto alloc = [&](auto** p, size_t n) -> int {
     SRL_CUDA(cudaMalloc(p, std::max<size_t>(n, 1) * sizeof(**p)));
@@ -98,6 +100,8 @@ int DecoderRunner::init(const DecoderDims& dims, const WeightLayout& layout, int
       (st2 = alloc(&xg_last, (size_t)this->logits_rows * H)) ||
       (st2 = alloc(&ssq_last, (size_t)this->logits_rows * parts)) ||
       (st2 = alloc(&logits, (size_t)this->logits_rows * d.V)) ||
+      (st2 = alloc(&lse_max, (size_t)this->logits_rows * ((d.V + 127) / 128))) ||
+      (st2 = alloc(&lse_sum, (size_t)this->logits_rows * ((d.V + 127) / 128))) ||
       (st2 = alloc(&kc, kv_layer_elems * d.L)) || (st2 = alloc(&vc, kv_layer_elems * d.L)) ||
       (st2 = alloc(&block_table, n_pages)) || (st2 = alloc(&cos_sin, (size_t)max_seq * d.hd)) ||
       (st2 = alloc(&plan.row_slot, M_max)) || (st2 = alloc(&plan.row_pos, M_max)) ||
@@ -159,18 +163,25 @@ int DecoderRunner::forward(int M, const __nv_bfloat16* w, const WeightMaps& wm) 
   int st;
   for (int l = 0; l < d.L; ++l) {
     const LayerOffsets& o = lay.layers[l];
-    EpiParams e;
-    e.kind = EPI_STORE_F32;
+    __nv_bfloat16* kcl = kc + kv_layer_elems * l;
+    __nv_bfloat16* vcl = vc + kv_layer_elems * l;
+    EpiParams e;  // QKV + bias + RoPE + paged KV append, fused
+    e.kind = unfused_qkv ? EPI_STORE_F32 : EPI_QKV;
+    e.out_f32 = qkv;
+    e.ld_out = d.qkv();
     e.ssq_in = ssq; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d.eps;
-    e.bias = w + o.qkv_b; e.out_f32 = qkv; e.ld_out = d.qkv();
+    e.bias = w + o.qkv_b;
+    e.nq = d.nq; e.nkv = d.nkv; e.hd = d.hd; e.pages_per_seq = pages_per_seq;
+    e.row_slot = plan.row_slot; e.row_pos = plan.row_pos; e.block_table = block_table;
+    e.cos_sin = cos_sin; e.q_out = q; e.kc = kcl; e.vc = vcl;
     tb(2);
     if ((st = gemm(wm.qkv[l], xg_map, M, d.qkv(), H, e))) return st;
     te();
-    __nv_bfloat16* kcl = kc + kv_layer_elems * l;
-    __nv_bfloat16* vcl = vc + kv_layer_elems * l;
-    tb(3);
-    launch_rope_append(qkv, d, plan, M, cos_sin, block_table, pages_per_seq, kcl, vcl, q, st_);
-    te();
+    if (unfused_qkv) {
+      tb(3);
+      launch_rope_append(qkv, d, plan, M, cos_sin, block_table, pages_per_seq, kcl, vcl, q, st_);
+      te();
+    }
     tb(4);
     launch_attention(q, d, plan, M, block_table, pages_per_seq, kcl, vcl, max_seq, attn_ws,
                      attn_counters, attn_ws_floats, attn, st_);
@@ -199,7 +210,9 @@ int DecoderRunner::forward(int M, const __nv_bfloat16* w, const WeightMaps& wm) 
 
 int DecoderRunner::lm_head(int rows, const WeightMaps& wm, bool gathered) {
   EpiParams e;
-  e.kind = EPI_STORE_F32;
+  e.kind = EPI_LOGITS;
+  e.part_max = lse_max;
+  e.part_sum = lse_sum;
   e.ssq_in = gathered ? ssq_last : ssq;
   e.ssq_in_parts = d.ssq_parts();
   e.inv_dim = 1.0f / (float)d.H;
@@ -334,8 +347,8 @@ int DecoderBackend::decode_round_eager(int b) {
   if ((st = r.forward(S_, buf_[b]->w, maps_[b]))) return st;
   if ((st = r.lm_head(S_, maps_[b], false))) return st;
   r.tb(9);
-  launch_sample(r.logits, d_.V, S_, r.plan, r.next, ss_, ring_, round_ctr_dev_, version_dev_,
-                opts_.greedy, st_);
+  launch_sample(r.logits, r.lse_max, r.lse_sum, d_.V, S_, r.plan, r.next, ss_, ring_,
+                round_ctr_dev_, version_dev_, opts_.greedy, st_);
   r.te();
   return SRL_OK;
 }
@@ -398,8 +411,8 @@ int DecoderBackend::prefill_round(int b, std::vector<int>& prefilled) {
   if ((st = r.forward(M, buf_[b]->w, maps_[b]))) return st;
   launch_gather_rows(r.xg, r.ssq, r.plan.last_row, S_, d_.H, d_.ssq_parts(), r.xg_last, r.ssq_last, st_);
   if ((st = r.lm_head(S_, maps_[b], true))) return st;
-  launch_sample(r.logits, d_.V, S_, r.plan, r.next, ss_, ring_, round_ctr_dev_, version_dev_,
-                opts_.greedy, st_);
+  launch_sample(r.logits, r.lse_max, r.lse_sum, d_.V, S_, r.plan, r.next, ss_, ring_,
+                round_ctr_dev_, version_dev_, opts_.greedy, st_);
   // the staging buffer is reused by the next prefill: keep it ordered
   SRL_CUDA(cudaStreamSynchronize(st_));
   return SRL_OK;

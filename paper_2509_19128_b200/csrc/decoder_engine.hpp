@@ -45,6 +45,8 @@ struct DecoderRunner {
   __nv_bfloat16* xg_last = nullptr;
   float* ssq_last = nullptr;
   float* logits = nullptr;        // [logits_rows x V]
+  float* lse_max = nullptr;       // [logits_rows x ceil(V/128)] per-tile max
+  double* lse_sum = nullptr;      // [logits_rows x ceil(V/128)] per-tile fp64 sum exp(x - max)
   __nv_bfloat16 *kc = nullptr, *vc = nullptr;  // [L][pages][nkv][64][hd]
   int32_t* block_table = nullptr;
   float* cos_sin = nullptr;
@@ -55,6 +57,7 @@ struct DecoderRunner {
   size_t attn_ws_floats = 0;
   CUtensorMap xg_map[2], attn_map[2], act_map[2], last_map[2];
   KernelTimer* timer = nullptr;  // set for a profiled round
+  bool unfused_qkv = false;
   void tb(int kind) { if (timer) timer->begin(kind); }
   void te() { if (timer) timer->end(); }
 

@@ -45,17 +45,41 @@ struct Layout {
   static constexpr int kMainBytes =
       STAGES * kStageBytes > kEpiBytes ? STAGES * kStageBytes : kEpiBytes;
   static constexpr int kBarOffset = kMainBytes;
-  static constexpr int kMiscOffset = kBarOffset + (2 * STAGES + 1) * 8;
+  static constexpr int kMiscOffset = (kBarOffset + (2 * STAGES + 1) * 8 + 15) / 16 * 16;
   static constexpr int kRstdOffset = kMiscOffset + 16;
-  static constexpr int kTotal = kRstdOffset + TOK * 4;
+  static constexpr int kRowOffset = kRstdOffset + TOK * 4;   // per-row slot / pos / page / offset
+  static_assert(kRowOffset % 16 == 0, "int4 row metadata must be 16-B aligned");
+  static constexpr int kTotal = kRowOffset + TOK * 16;
   static constexpr int kAlloc = kTotal + 1024;  // manual 1024-B alignment slack
 };
 
 __device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SRL_STAMP(i)                                                                        \
+  do {                                                                                      \
+    if (epi.stamps != nullptr && threadIdx.x == 0)                                          \
+      epi.stamps[((size_t)blockIdx.z * gridDim.y * gridDim.x + (size_t)blockIdx.y * gridDim.x + \
+                  blockIdx.x) * 8 + (i)] = gtimer();                                          \
+  } while (0)
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 
@@ -72,6 +96,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* done = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kMiscOffset);
   float* s_rstd = reinterpret_cast<float*>(smem + L::kRstdOffset);
+  int4* s_row = reinterpret_cast<int4*>(smem + L::kRowOffset);
   float* tile = reinterpret_cast<float*>(smem);  // epilogue view, aliases the ring
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -81,6 +106,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kb_total = K / kBlockK;
   const int kb_begin = (split * kb_total) / cs;
   const int nkb = ((split + 1) * kb_total) / cs - kb_begin;  // >= 1 (host: cs <= kb_total)
+  SRL_STAMP(0);
 
   if (warp == 0) {
     if (elect_one()) {
@@ -105,6 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   griddep_launch_dependents();  // the next kernel may start its prologue now
+  SRL_STAMP(1);
 
   if (warp == 0) {
     if (elect_one()) {  // ---- TMA producer
@@ -155,19 +182,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ---- drain TMEM into the shared tile: thread = weight row (TMEM lane)
   mbar_wait(done, 0);
   tc_fence_after();
+  SRL_STAMP(2);
   const int row = threadIdx.x;
   const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
 #pragma unroll
-  for (int c0 = 0; c0 < TOK; c0 += 16) {
-    uint32_t r[16];
-    tmem_ld_32x32b_x16(lane_addr + c0, r);
+  for (int c0 = 0; c0 < TOK; c0 += 64) {  // two 32-column loads in flight, one wait
+    uint32_t ra[32], rb[32];
+    tmem_ld_32x32b_x32(lane_addr + c0, ra);
+    tmem_ld_32x32b_x32(lane_addr + c0 + 32, rb);
     tmem_ld_wait();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) tile[(c0 + j) * L::kPitch + row] = __uint_as_float(r[j]);
+    for (int j = 0; j < 32; ++j) tile[(c0 + j) * L::kPitch + row] = __uint_as_float(ra[j]);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) tile[(c0 + 32 + j) * L::kPitch + row] = __uint_as_float(rb[j]);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_free<TOK>(tmem);
+  SRL_STAMP(3);
 
   // ---- split-K: reduce this CTA's row slice over the cluster through DSMEM
   int r0 = 0, r1 = TOK;
@@ -180,14 +212,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     float4 acc[kMaxPer];
 #pragma unroll
     for (int k = 0; k < kMaxPer; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int q = 0; q < cs; ++q) {  // rank order: deterministic
+    // fetch every rank's slice first (all remote loads in flight), then sum in
+    // rank order: deterministic
+    for (int q0 = 0; q0 < cs; q0 += 4) {
+      float4 v[4][kMaxPer];
 #pragma unroll
-      for (int k = 0; k < kMaxPer; ++k) {
-        const int i = threadIdx.x + k * kThreads;
-        if (i < n4) {
-          const int j = r0 + i / (kBlockN / 4), c = (i % (kBlockN / 4)) * 4;
-          const float4 v = dsmem_ld_f4(dsmem_map(smem_u32(&tile[j * L::kPitch + c]), q));
-          acc[k].x += v.x; acc[k].y += v.y; acc[k].z += v.z; acc[k].w += v.w;
+      for (int dq = 0; dq < 4; ++dq) {
+#pragma unroll
+        for (int k = 0; k < kMaxPer; ++k) {
+          const int i = threadIdx.x + k * kThreads;
+          const int q = q0 + dq;
+          if (q < cs && i < n4) {
+            const int j = r0 + i / (kBlockN / 4), c = (i % (kBlockN / 4)) * 4;
+            v[dq][k] = dsmem_ld_f4(dsmem_map(smem_u32(&tile[j * L::kPitch + c]), q));
+          }
+        }
+      }
+#pragma unroll
+      for (int dq = 0; dq < 4; ++dq) {
+#pragma unroll
+        for (int k = 0; k < kMaxPer; ++k) {
+          const int i = threadIdx.x + k * kThreads;
+          if (q0 + dq < cs && i < n4) {
+            acc[k].x += v[dq][k].x; acc[k].y += v[dq][k].y;
+            acc[k].z += v[dq][k].z; acc[k].w += v[dq][k].w;
+          }
         }
       }
     }
@@ -203,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // ---- epilogue over rows [r0, r1)
+  SRL_STAMP(4);
   griddep_wait();  // epilogue inputs (ssq, residual) come from earlier kernels
   for (int j = r0 + threadIdx.x; j < r1; j += kThreads) {
     float r = 1.f;
@@ -213,9 +263,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       r = rsqrtf(s * epi.inv_dim + epi.eps);
     }
     s_rstd[j] = r;
+    if (epi.kind == EPI_QKV) {  // (stamp 5 follows the row-parameter loads)  // KV-cache coordinates of this row
+      int4 rc = make_int4(-1, 0, 0, 0);
+      if (m < M) {
+        rc.x = epi.row_slot[m];
+        rc.y = epi.row_pos[m];
+        if (rc.x >= 0) {
+          rc.z = epi.block_table[(size_t)rc.x * epi.pages_per_seq + rc.y / 64];
+          rc.w = rc.y % 64;
+        }
+      }
+      s_row[j] = rc;
+    }
   }
   __syncthreads();
 
+  SRL_STAMP(5);
   const int rows = r1 - r0;
   if (epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16) {
     for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
@@ -238,6 +301,73 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float u = tile[j * L::kPitch + 64 + c] * s_rstd[j];
       const float a = g / (1.f + expf(-g)) * u;
       epi.out_bf16[(size_t)m * epi.ld_bf16 + (n0 >> 1) + c] = __float2bfloat16(a);
+    }
+  } else if (epi.kind == EPI_QKV) {
+    for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
+      const int n = n0 + c;
+      float v = 0.f;
+      if (t0 + j < M && n < N) v = tile[j * L::kPitch + c] * s_rstd[j] + bf2f(epi.bias[n]);
+      tile[j * L::kPitch + c] = v;
+    }
+    __syncthreads();
+    const int hd = epi.hd, half = hd >> 1;
+    const int qend = epi.nq * hd, kend = (epi.nq + epi.nkv) * hd;
+    for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
+      const int m = t0 + j, n = n0 + c;
+      const int4 rc = s_row[j];
+      if (m >= M || n >= N || rc.x < 0) continue;
+      const int jj = n % hd;
+      const float* row = &tile[j * L::kPitch + (c - jj)];  // this head's hd values
+      float y;
+      if (n < kend) {  // RoPE (rotate pairs (i, i + hd/2)) on q and k
+        const int i = jj < half ? jj : jj - half;
+        const float co = epi.cos_sin[(size_t)rc.y * hd + i];
+        const float si = epi.cos_sin[(size_t)rc.y * hd + half + i];
+        const float x1 = row[i], x2 = row[i + half];
+        y = jj < half ? x1 * co - x2 * si : x2 * co + x1 * si;
+      } else {
+        y = row[jj];
+      }
+      const __nv_bfloat16 b = __float2bfloat16(y);
+      if (n < qend) {
+        epi.q_out[(size_t)m * qend + n] = b;
+      } else {
+        const int kv = n < kend ? n - qend : n - kend;
+        const int kh = kv / hd;
+        const size_t at = (((size_t)rc.z * epi.nkv + kh) * 64 + rc.w) * hd + jj;
+        if (n < kend) epi.kc[at] = b;
+        else epi.vc[at] = b;
+      }
+    }
+  } else if (epi.kind == EPI_LOGITS) {
+    for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
+      const int m = t0 + j, n = n0 + c;
+      float v = -INFINITY;
+      if (m < M && n < N) {
+        v = tile[j * L::kPitch + c] * s_rstd[j];
+        epi.out_f32[(size_t)m * epi.ld_out + n] = v;
+      }
+      tile[j * L::kPitch + c] = v;
+    }
+    __syncthreads();
+    for (int j = r0 + warp; j < r1; j += kThreads / 32) {
+      const float4 x = *reinterpret_cast<const float4*>(&tile[j * L::kPitch + lane * 4]);
+      const float mx = warp_max(fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
+      double s = 0.0;
+      if (mx != -INFINITY) {
+        const double md = (double)mx;
+        s = exp((double)x.x - md) + exp((double)x.y - md) + exp((double)x.z - md) +
+            exp((double)x.w - md);
+      }
+      s = warp_sum_d(s);
+      const int m = t0 + j;
+      if (lane == 0 && m < M) {
+        epi.part_max[(size_t)m * n_tiles + n_tile] = mx;
+        epi.part_sum[(size_t)m * n_tiles + n_tile] = s;
+      }
     }
   } else if (epi.kind == EPI_RESID) {
     for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
@@ -263,6 +393,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0 && t0 + j < M) epi.ssq_out[(size_t)(t0 + j) * n_tiles + n_tile] = s;
     }
   }
+  __syncthreads();
+  SRL_STAMP(6);
 }
 
 template <int TOK, int STAGES>

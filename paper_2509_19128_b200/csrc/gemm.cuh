@@ -19,6 +19,8 @@ enum EpiKind : int {
   EPI_RESID = 1,       // resid[m, n] += acc; xg[m, n] = bf16(resid * gain[n]); ssq partials
   EPI_SWIGLU = 2,      // tile = 64 gate | 64 up rows: act[m, j] = bf16(silu(g) * u), g,u scaled by rstd
   EPI_STORE_BF16 = 3,  // out_bf16[m, n] = bf16(rstd[m] * acc (+ bias[n]))
+  EPI_QKV = 4,         // rstd*acc + bias, RoPE on q/k, q -> bf16 rows, k/v -> paged KV cache
+  EPI_LOGITS = 5,      // out_f32 = rstd*acc; per (row, 128-col tile): max and fp64 sum exp(x - max)
 };
 
 struct EpiParams {
@@ -38,6 +40,20 @@ struct EpiParams {
   const __nv_bfloat16* gain = nullptr;  // next RMSNorm gain [N]
   __nv_bfloat16* xg = nullptr;          // [M x N] bf16
   float* ssq_out = nullptr;             // [M x ceil(N/128)]
+  // EPI_QKV
+  int nq = 0, nkv = 0, hd = 0, pages_per_seq = 0;
+  const int32_t* row_slot = nullptr;    // plan: slot of each row (-1 = padding)
+  const int32_t* row_pos = nullptr;     // plan: position of each row
+  const int32_t* block_table = nullptr; // [slots x pages_per_seq]
+  const float* cos_sin = nullptr;       // [max_pos x hd] (cos | sin)
+  __nv_bfloat16* q_out = nullptr;       // [M x nq*hd]
+  __nv_bfloat16* kc = nullptr;          // [pages][nkv][64][hd] (this layer)
+  __nv_bfloat16* vc = nullptr;
+  // EPI_LOGITS
+  float* part_max = nullptr;            // [M x ceil(N/128)]
+  double* part_sum = nullptr;           // [M x ceil(N/128)]
+  // debug: per-CTA %globaltimer phase stamps [ctas x 8] (null = off)
+  unsigned long long* stamps = nullptr;
 };
 
 // Build a 2-D bf16 TMA descriptor for a row-major [rows x cols] matrix with a
