@@ -221,6 +221,44 @@ int srl_truncated_is_weight(double pi_logprob_sum, double mu_logprob_sum, double
 /* ess (rl_math.cpp:152-163): SRL_ESS_UNDEFINED when all weights are zero. */
 int srl_ess(const double* weights, int32_t n, double* out);
 
+/* ------------------------------------------------ decoder trainer step --- */
+/* IS-REINFORCE for the decoder policy: the reference's
+ * is_reinforce_gradient (rl_math.cpp:211-276) generalised from tabular logits
+ * to every decoder parameter.  Gradient = ascent direction of
+ * J = (1/m) sum_traj sum_t w * A_t * log pi(y_t), stop-gradient on the
+ * truncated IS weight w (sequence level by default, or per token). */
+typedef struct srl_trainer srl_trainer;
+typedef struct {
+  int32_t max_tokens;  /* packed rows per step (sum of sequence lengths - 1) */
+  int32_t device;
+} srl_trainer_options;
+typedef struct {
+  double objective;    /* J at the current weights */
+  double ess;          /* ESS of the IS weights used (rl_math.cpp:152-163) */
+  int32_t clamped;     /* weights truncated at c */
+  int32_t tokens;      /* rows processed */
+  double forward_ms;   /* device time: forward + log-prob recompute */
+  double step_ms;      /* device time: whole step incl. backward */
+} srl_trainer_stats;
+int srl_trainer_create(const srl_policy* decoder_policy, const srl_trainer_options* opts,
+                       srl_trainer** out);
+void srl_trainer_destroy(srl_trainer* t);
+/* tokens: packed sequences (bos + prompt + generated), offsets[n_seq + 1];
+ * loss_begin[q]: index (within the sequence) of the first scored token, >= 1;
+ * behavior_logprobs / advantages: one per token, same packing (entries before
+ * loss_begin ignored); n_trajectories: m.  logprobs_out (optional, packed like
+ * tokens): log pi of every token under the current weights (0 at index 0). */
+int srl_trainer_step(srl_trainer* t, const int32_t* tokens, const int64_t* offsets, int32_t n_seq,
+                     const int32_t* loss_begin, const double* behavior_logprobs,
+                     const double* advantages, int32_t n_trajectories, double clamp,
+                     int32_t granularity, double* logprobs_out, srl_trainer_stats* stats);
+/* fp32 gradient buffer (device, same element layout as the flat weights). */
+int srl_trainer_gradient(srl_trainer* t, void** device_ptr, size_t* n_elems);
+/* Adam ascent step on fp32 master weights; refreshes the bf16 weights. */
+int srl_trainer_apply_adam(srl_trainer* t, double lr, double beta1, double beta2, double eps);
+/* bf16 flat weights (device) -- the payload broadcast to the generators. */
+int srl_trainer_weights(srl_trainer* t, void** device_ptr, size_t* nbytes);
+
 /* ---------------------------------------------------------------- lag --- */
 /* Per consumed batch lag statistics on the device (sim.cpp:63-110):
  * lag = version_before - token_version; hist must hold hist_cap counters.

@@ -60,6 +60,15 @@ class EngineStatsC(C.Structure):
                 ("last_pause_ms", f64), ("max_pause_ms", f64), ("launches", i64)]
 
 
+class TrainerOptionsC(C.Structure):
+    _fields_ = [("max_tokens", i32), ("device", i32)]
+
+
+class TrainerStatsC(C.Structure):
+    _fields_ = [("objective", f64), ("ess", f64), ("clamped", i32), ("tokens", i32),
+                ("forward_ms", f64), ("step_ms", f64)]
+
+
 class KernelProfileC(C.Structure):
     _fields_ = [("ms", f64 * 10), ("launches", i32 * 10), ("valid", i32), ("rows", i32)]
 
@@ -116,6 +125,12 @@ SIGNATURES: dict[str, tuple] = {
     "srl_process_group_id": (I, [P(cp), i32, cp, sz]),
     "srl_kernel_sample_logits": (I, [vp, i32, i32, vp, vp, i32, vp, vp, vp]),
     "srl_engine_profile_next_round": (I, [vp]),
+    "srl_trainer_create": (I, [vp, P(TrainerOptionsC), P(vp)]),
+    "srl_trainer_destroy": (None, [vp]),
+    "srl_trainer_step": (I, [vp, vp, vp, i32, vp, vp, vp, i32, f64, i32, vp, P(TrainerStatsC)]),
+    "srl_trainer_gradient": (I, [vp, P(vp), P(sz)]),
+    "srl_trainer_apply_adam": (I, [vp, f64, f64, f64, f64]),
+    "srl_trainer_weights": (I, [vp, P(vp), P(sz)]),
     "srl_engine_kernel_profile": (I, [vp, P(KernelProfileC)]),
 }
 

@@ -10,12 +10,16 @@
 
 #include "decoder_engine.hpp"
 #include "runtime.hpp"
+#include "trainer.hpp"
 
 struct srl_policy {
   srl::Policy p;
 };
 struct srl_engine {
   std::unique_ptr<srl::Engine> e;
+};
+struct srl_trainer {
+  std::unique_ptr<srl::DecoderTrainer> t;
 };
 
 namespace srl {
@@ -504,5 +508,104 @@ extern "C" int srl_engine_profile_next_round(srl_engine* e) {
 extern "C" int srl_engine_kernel_profile(const srl_engine* e, srl_kernel_profile* out) {
   if (!e || !out) return fail(SRL_INVALID_ARGUMENT, "kernel_profile");
   if (!e->e->kernel_profile(out)) return fail(SRL_INVALID_ARGUMENT, "no profiled round yet");
+  return SRL_OK;
+}
+
+// ------------------------------------------------------------- trainer ---
+extern "C" int srl_trainer_create(const srl_policy* p, const srl_trainer_options* opts,
+                                  srl_trainer** out) {
+  return guarded([&] {
+    if (!p || !out || p->p.type != SRL_POLICY_DECODER)
+      return fail(SRL_INVALID_ARGUMENT, "trainer_create: needs a decoder policy");
+    int st;
+    if ((st = require_device(p->p.dec->device))) return st;
+    srl_trainer_options o{};
+    o.max_tokens = 4096;
+    o.device = p->p.dec->device;
+    if (opts) o = *opts;
+    auto h = std::make_unique<srl_trainer>();
+    h->t = std::make_unique<DecoderTrainer>();
+    if ((st = h->t->init(*p->p.dec, o))) return st;
+    *out = h.release();
+    return (int)SRL_OK;
+  });
+}
+
+extern "C" void srl_trainer_destroy(srl_trainer* t) { delete t; }
+
+extern "C" int srl_trainer_step(srl_trainer* t, const int32_t* tokens, const int64_t* offsets,
+                                int32_t n_seq, const int32_t* loss_begin,
+                                const double* behavior_logprobs, const double* advantages,
+                                int32_t n_trajectories, double clamp, int32_t granularity,
+                                double* logprobs_out, srl_trainer_stats* stats) {
+  return guarded([&] {
+    if (!t || !tokens || !offsets || n_seq < 1 || !loss_begin || !behavior_logprobs || !advantages)
+      return fail(SRL_INVALID_ARGUMENT, "trainer_step: bad arguments");
+    if (clamp <= 0.0 || !std::isfinite(clamp))  // truncated_is_weight (rl_math.cpp:146-147)
+      return fail(SRL_INVALID_ARGUMENT, "truncated_is_weight: clamp must be positive");
+    if (granularity != 0 && granularity != 1) return fail(SRL_INVALID_ARGUMENT, "granularity");
+    TrainBatch b;
+    b.n_trajectories = n_trajectories;
+    b.clamp = clamp;
+    b.granularity = granularity;
+    const DecoderDims& d = t->t->weights().dims;
+    for (int q = 0; q < n_seq; ++q) {
+      const int64_t a = offsets[q], e = offsets[q + 1];
+      const int n = (int)(e - a);
+      if (n < 2 || loss_begin[q] < 1 || loss_begin[q] >= n)
+        return fail(SRL_INVALID_ARGUMENT, "trainer_step: sequence needs a scored token");
+      if (n > d.max_pos) return fail(SRL_INVALID_ARGUMENT, "sequence longer than max_positions");
+      b.seq_start.push_back(b.rows);
+      b.seq_len.push_back(n - 1);
+      b.loss_begin.push_back(loss_begin[q] - 1);
+      for (int p = 0; p + 1 < n; ++p) {
+        const int32_t in = tokens[a + p], tg = tokens[a + p + 1];
+        if (in < 0 || in >= d.V || tg < 0 || tg >= d.V)
+          return fail(SRL_INVALID_ARGUMENT, "token out of vocab range");
+        const double mu = behavior_logprobs[a + p + 1], adv = advantages[a + p + 1];
+        const bool scored = p + 1 >= loss_begin[q];
+        if (scored && (!std::isfinite(mu) || !std::isfinite(adv)))
+          return fail(SRL_INVALID_ARGUMENT, "truncated_is_weight: non-finite log-probability");
+        b.row_slot.push_back(q);
+        b.row_pos.push_back(p);
+        b.row_token.push_back(in);
+        b.row_target.push_back(tg);
+        b.row_mu.push_back(scored ? mu : 0.0);
+        b.row_adv.push_back(scored ? adv : 0.0);
+        if (scored) ++b.n_loss_rows;
+        ++b.rows;
+      }
+    }
+    srl_trainer_stats s{};
+    const int st = t->t->step(b, &s);
+    if (st != SRL_OK) return st;
+    if (stats) *stats = s;
+    if (logprobs_out) {
+      const auto& lp = t->t->last_logprobs();
+      for (int q = 0; q < n_seq; ++q) {
+        logprobs_out[offsets[q]] = 0.0;
+        for (int p = 0; p < b.seq_len[q]; ++p) logprobs_out[offsets[q] + p + 1] = lp[b.seq_start[q] + p];
+      }
+    }
+    return (int)SRL_OK;
+  });
+}
+
+extern "C" int srl_trainer_gradient(srl_trainer* t, void** device_ptr, size_t* n_elems) {
+  if (!t || !device_ptr || !n_elems) return fail(SRL_INVALID_ARGUMENT, "trainer_gradient");
+  *device_ptr = t->t->gradient();
+  *n_elems = t->t->elements();
+  return SRL_OK;
+}
+
+extern "C" int srl_trainer_apply_adam(srl_trainer* t, double lr, double b1, double b2, double eps) {
+  if (!t) return fail(SRL_INVALID_ARGUMENT, "trainer_apply_adam");
+  return t->t->apply_adam((float)lr, (float)b1, (float)b2, (float)eps);
+}
+
+extern "C" int srl_trainer_weights(srl_trainer* t, void** device_ptr, size_t* nbytes) {
+  if (!t || !device_ptr || !nbytes) return fail(SRL_INVALID_ARGUMENT, "trainer_weights");
+  *device_ptr = t->t->weights().w;
+  *nbytes = t->t->weights().bytes;
   return SRL_OK;
 }

@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
                      const int32_t* __restrict__ block_table, int pages_per_seq,
                      const __nv_bfloat16* __restrict__ kc, const __nv_bfloat16* __restrict__ vc,
                      float scale, float* __restrict__ ws, int* __restrict__ counters,
-                     __nv_bfloat16* __restrict__ out) {
+                     __nv_bfloat16* __restrict__ out, float* __restrict__ lse_out) {
   constexpr int DPL = HD / 32;           // dims per lane in the PV phase
   constexpr int ROW = HD * 2 + 16;       // padded K row in smem (bytes): conflict-free LDS.128
   constexpr int VROW = HD * 2;           // V rows are read row-wise: no padding needed
@@ -315,6 +315,7 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
     }
     if (splits == 1) {
       out[(size_t)m * nq * HD + (kh * G + g) * HD + d] = __float2bfloat16(L > 0.f ? A / L : 0.f);
+      if (lse_out != nullptr && d == 0) lse_out[(size_t)m * nq + kh * G + g] = M + logf(L);
     } else {
       my_ws[g * (HD + 2) + 2 + d] = A;
       if (d == 0) {
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
       A += __ldcg(&base[sp2 * rec + g * (HD + 2) + 2 + d]) * a;
     }
     out[(size_t)m * nq * HD + (kh * G + g) * HD + d] = __float2bfloat16(L > 0.f ? A / L : 0.f);
+    if (lse_out != nullptr && d == 0) lse_out[(size_t)m * nq + kh * G + g] = M + logf(L);
   }
   if (threadIdx.x == 0) counters[cidx] = 0;
 }
@@ -841,7 +843,7 @@ template <int G, int HD>
 void attention_launch_t(dim3 grid, cudaStream_t st, const __nv_bfloat16* q, int nq, int nkv,
                         const RoundPlan& plan, const int32_t* bt, int pps, const __nv_bfloat16* kc,
                         const __nv_bfloat16* vc, float scale, float* ws, int* counters,
-                        __nv_bfloat16* out) {
+                        __nv_bfloat16* out, float* lse_out) {
   constexpr size_t smem = attention_smem<G, HD>();
   static bool once = [] {
     cudaFuncSetAttribute(attention_kernel<G, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -851,17 +853,17 @@ void attention_launch_t(dim3 grid, cudaStream_t st, const __nv_bfloat16* q, int 
   (void)once;
   launch_pdl(attention_kernel<G, HD>, grid, dim3(32 * kAttnWarps), smem, st, dim3(1, 1, 1), q, nq,
              nkv, (const int32_t*)plan.row_slot, (const int32_t*)plan.row_pos, bt, pps, kc, vc,
-             scale, ws, counters, out);
+             scale, ws, counters, out, lse_out);
 }
 
 template <int HD>
 void attention_dispatch_g(int G, dim3 grid, cudaStream_t st, const __nv_bfloat16* q, int nq,
                           int nkv, const RoundPlan& plan, const int32_t* bt, int pps,
                           const __nv_bfloat16* kc, const __nv_bfloat16* vc, float scale, float* ws,
-                          int* counters, __nv_bfloat16* out) {
+                          int* counters, __nv_bfloat16* out, float* lse_out) {
   switch (G) {
 #define SRL_ATTN_G(g) \
-  case g: attention_launch_t<g, HD>(grid, st, q, nq, nkv, plan, bt, pps, kc, vc, scale, ws, counters, out); break;
+  case g: attention_launch_t<g, HD>(grid, st, q, nq, nkv, plan, bt, pps, kc, vc, scale, ws, counters, out, lse_out); break;
     SRL_ATTN_G(1) SRL_ATTN_G(2) SRL_ATTN_G(3) SRL_ATTN_G(4)
     SRL_ATTN_G(5) SRL_ATTN_G(6) SRL_ATTN_G(7) SRL_ATTN_G(8)
 #undef SRL_ATTN_G
@@ -872,7 +874,7 @@ void attention_dispatch_g(int G, dim3 grid, cudaStream_t st, const __nv_bfloat16
 void launch_attention(const __nv_bfloat16* q, const DecoderDims& d, const RoundPlan& plan, int M,
                       const int32_t* block_table, int pages_per_seq, const __nv_bfloat16* kc,
                       const __nv_bfloat16* vc, int max_ctx, float* ws, int* counters,
-                      size_t ws_floats, __nv_bfloat16* out, cudaStream_t st) {
+                      size_t ws_floats, __nv_bfloat16* out, cudaStream_t st, float* lse_out) {
   const int splits = attention_splits(d, M, max_ctx);
   (void)ws_floats;
   dim3 grid(M, d.nkv, splits);
@@ -880,10 +882,10 @@ void launch_attention(const __nv_bfloat16* q, const DecoderDims& d, const RoundP
   const int G = d.nq / d.nkv;
   if (d.hd == 64)
     attention_dispatch_g<64>(G, grid, st, q, d.nq, d.nkv, plan, block_table, pages_per_seq, kc,
-                             vc, scale, ws, counters, out);
+                             vc, scale, ws, counters, out, lse_out);
   else
     attention_dispatch_g<128>(G, grid, st, q, d.nq, d.nkv, plan, block_table, pages_per_seq, kc,
-                              vc, scale, ws, counters, out);
+                              vc, scale, ws, counters, out, lse_out);
 }
 
 void launch_gather_rows(const __nv_bfloat16* xg, const float* ssq, const int32_t* last_row,

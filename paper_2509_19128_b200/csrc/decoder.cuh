@@ -92,7 +92,8 @@ void launch_rope_append(const float* qkv, const DecoderDims& d, const RoundPlan&
 void launch_attention(const __nv_bfloat16* q, const DecoderDims& d, const RoundPlan& plan, int M,
                       const int32_t* block_table, int pages_per_seq, const __nv_bfloat16* kc,
                       const __nv_bfloat16* vc, int max_ctx, float* ws, int* counters,
-                      size_t ws_floats, __nv_bfloat16* out, cudaStream_t st);
+                      size_t ws_floats, __nv_bfloat16* out, cudaStream_t st,
+                      float* lse_out = nullptr /* [M x nq] natural-log LSE, for backward */);
 size_t attention_ws_floats(const DecoderDims& d, int M, int max_ctx);
 
 // Gather the last row of each emitting slot (decode rounds use identity).

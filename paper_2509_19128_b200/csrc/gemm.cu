@@ -292,6 +292,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       else
         epi.out_bf16[(size_t)m * epi.ld_bf16 + n] = __float2bfloat16(v);
     }
+  } else if (epi.kind == EPI_ACCUM_F32) {
+    for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
+      const int m = t0 + j, n = n0 + c;
+      if (m >= M || n >= N) continue;
+      epi.out_f32[(size_t)m * epi.ld_out + n] += epi.scale * tile[j * L::kPitch + c];
+    }
   } else if (epi.kind == EPI_SWIGLU) {
     for (int idx = threadIdx.x; idx < rows * (kBlockN / 2); idx += kThreads) {
       const int j = r0 + (idx >> 6), c = idx & 63;

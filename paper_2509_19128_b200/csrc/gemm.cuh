@@ -21,6 +21,7 @@ enum EpiKind : int {
   EPI_STORE_BF16 = 3,  // out_bf16[m, n] = bf16(rstd[m] * acc (+ bias[n]))
   EPI_QKV = 4,         // rstd*acc + bias, RoPE on q/k, q -> bf16 rows, k/v -> paged KV cache
   EPI_LOGITS = 5,      // out_f32 = rstd*acc; per (row, 128-col tile): max and fp64 sum exp(x - max)
+  EPI_ACCUM_F32 = 6,   // out_f32[m, n] += scale * acc  (gradient accumulation)
 };
 
 struct EpiParams {
@@ -52,6 +53,7 @@ struct EpiParams {
   // EPI_LOGITS
   float* part_max = nullptr;            // [M x ceil(N/128)]
   double* part_sum = nullptr;           // [M x ceil(N/128)]
+  float scale = 1.f;                    // EPI_ACCUM_F32
   // debug: per-CTA %globaltimer phase stamps [ctas x 8] (null = off)
   unsigned long long* stamps = nullptr;
 };

@@ -1,0 +1,453 @@
+// train_kernels.cu -- non-GEMM kernels of the decoder trainer step (see
+// train.cuh).  Correctness-first CUDA-core implementations; every reduction
+// over rows that feeds a weight gradient uses fp32 atomics (gradients are
+// compared within tolerance, not bit-exactly).
+#include <cmath>
+
+#include "decoder.cuh"
+#include "train.cuh"
+
+namespace srl {
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block reduce (any blockDim multiple of 32, <= 1024)
+__device__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = threadIdx.x < (blockDim.x >> 5) ? red[l] : 0.f;
+  if (w == 0) {
+    t = warp_sum(t);
+    if (l == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+__device__ double block_sum_dd(double v, double* red) {
+  v = warp_sum_d(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = threadIdx.x < (blockDim.x >> 5) ? red[l] : 0.0;
+  if (w == 0) {
+    t = warp_sum_d(t);
+    if (l == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+template <typename In>
+__global__ void transpose_kernel(const In* __restrict__ src, const float* __restrict__ row_scale,
+                                 int rows, int cols, __nv_bfloat16* __restrict__ dst, int ld) {
+  __shared__ float tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    float v = 0.f;
+    if (r < rows && c < cols) {
+      if constexpr (sizeof(In) == 2) v = __bfloat162float(src[(size_t)r * cols + c]);
+      else v = src[(size_t)r * cols + c];
+      if (row_scale) v *= row_scale[r];
+    }
+    tile[i][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[(size_t)c * ld + r] = __float2bfloat16(tile[threadIdx.x][i]);
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ s, size_t n, __nv_bfloat16* __restrict__ d) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    d[i] = __float2bfloat16(s[i]);
+}
+__global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ s, size_t n, float* __restrict__ d) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    d[i] = __bfloat162float(s[i]);
+}
+__global__ void zero_kernel(float* p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = 0.f;
+}
+
+constexpr int kRowThreads = 256;
+
+__global__ void __launch_bounds__(kRowThreads)
+    loss_dlogits_kernel(const float* __restrict__ logits, const float* __restrict__ pmax,
+                        const double* __restrict__ psum, int V, const int32_t* __restrict__ targets,
+                        const float* __restrict__ coef, double* __restrict__ logprob,
+                        __nv_bfloat16* __restrict__ dlogits) {
+  __shared__ float fred[33];
+  __shared__ double dred[33];
+  const int r = blockIdx.x;
+  const int T = (V + 127) / 128;
+  const float* pm = pmax + (size_t)r * T;
+  const double* ps = psum + (size_t)r * T;
+  float mx = -INFINITY;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) mx = fmaxf(mx, pm[t]);
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) fred[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? fred[threadIdx.x] : -INFINITY;
+    v = warp_max(v);
+    if (threadIdx.x == 0) fred[32] = v;
+  }
+  __syncthreads();
+  const double M = (double)fred[32];
+  double part = 0.0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) part += ps[t] * exp((double)pm[t] - M);
+  const double lse = M + log(block_sum_dd(part, dred));
+  const int tgt = targets[r];
+  const float* x = logits + (size_t)r * V;
+  const float c = coef[r];
+  const float lsef = (float)lse;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    const float p = __expf(x[v] - lsef);
+    dlogits[(size_t)r * V + v] = __float2bfloat16(c * ((v == tgt ? 1.f : 0.f) - p));
+  }
+  if (threadIdx.x == 0) logprob[r] = (double)x[tgt] - lse;
+}
+
+__global__ void __launch_bounds__(kRowThreads)
+    row_rstd_kernel(const float* __restrict__ x, int H, float eps, float* __restrict__ rstd) {
+  __shared__ float red[33];
+  const int r = blockIdx.x;
+  float s = 0.f;
+  for (int k = threadIdx.x; k < H; k += blockDim.x) {
+    const float v = x[(size_t)r * H + k];
+    s += v * v;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) rstd[r] = rsqrtf(s / (float)H + eps);
+}
+
+__global__ void __launch_bounds__(kRowThreads)
+    rmsnorm_bwd_kernel(const float* __restrict__ dzw, const float* __restrict__ x,
+                       const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd, int H,
+                       float* __restrict__ dx, float* __restrict__ dg) {
+  __shared__ float red[33];
+  const int r = blockIdx.x;
+  const float rs = rstd[r];
+  float dr = 0.f;
+  for (int k = threadIdx.x; k < H; k += blockDim.x)
+    dr += dzw[(size_t)r * H + k] * x[(size_t)r * H + k] * __bfloat162float(g[k]);
+  dr = block_sum(dr, red);
+  const float coef = -rs * rs * rs / (float)H * dr;
+  for (int k = threadIdx.x; k < H; k += blockDim.x) {
+    const size_t o = (size_t)r * H + k;
+    const float du = rs * dzw[o];
+    dx[o] += du * __bfloat162float(g[k]) + coef * x[o];
+    atomicAdd(&dg[k], du * x[o]);
+  }
+}
+
+__global__ void swiglu_bwd_kernel(const float* __restrict__ dact, const float* __restrict__ gu,
+                                  int T, int I, __nv_bfloat16* __restrict__ dgu,
+                                  float* __restrict__ dgu_f32) {
+  const size_t n = (size_t)T * I;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const size_t t = e / I;
+    const int j = (int)(e % I);
+    const int blk = j >> 6, c = j & 63;
+    const size_t gi = t * 2 * I + (size_t)blk * 128 + c, ui = gi + 64;
+    const float gv = gu[gi], uv = gu[ui], da = dact[e];
+    const float sg = 1.f / (1.f + expf(-gv));
+    const float silu = gv * sg;
+    const float dg = da * uv * (sg * (1.f + gv * (1.f - sg)));
+    const float du = da * silu;
+    dgu[gi] = __float2bfloat16(dg);
+    dgu[ui] = __float2bfloat16(du);
+    if (dgu_f32) {
+      dgu_f32[gi] = dg;
+      dgu_f32[ui] = du;
+    }
+  }
+}
+
+__global__ void swiglu_fwd_kernel(const float* __restrict__ gu, int T, int I,
+                                  __nv_bfloat16* __restrict__ act) {
+  const size_t n = (size_t)T * I;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const size_t t = e / I;
+    const int j = (int)(e % I);
+    const size_t gi = t * 2 * I + (size_t)(j >> 6) * 128 + (j & 63);
+    const float g = gu[gi], u = gu[gi + 64];
+    act[e] = __float2bfloat16(g / (1.f + expf(-g)) * u);
+  }
+}
+
+// D[t,h] = sum_d dO[t,h,d] * O[t,h,d]
+__global__ void attn_bwd_dot_kernel(const float* __restrict__ d_o, const __nv_bfloat16* __restrict__ o,
+                                    int T, int nq, int hd, float* __restrict__ D) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= T * nq) return;
+  const size_t base = (size_t)warp * hd;
+  float s = 0.f;
+  for (int d = lane; d < hd; d += 32) s += d_o[base + d] * __bfloat162float(o[base + d]);
+  s = warp_sum(s);
+  if (lane == 0) D[warp] = s;
+}
+
+__device__ __forceinline__ const __nv_bfloat16* kv_row(const __nv_bfloat16* c, const int32_t* bt,
+                                                       int pps, int slot, int pos, int nkv, int kh,
+                                                       int hd) {
+  const int page = bt[(size_t)slot * pps + pos / kPageTokens];
+  return c + (((size_t)page * nkv + kh) * kPageTokens + (pos % kPageTokens)) * hd;
+}
+
+// dq: one warp per (row t, q head h); lane holds hd/32 dims.
+__global__ void attn_bwd_dq_kernel(const __nv_bfloat16* __restrict__ q, const float* __restrict__ d_o,
+                                   const float* __restrict__ lse, const float* __restrict__ D,
+                                   const __nv_bfloat16* __restrict__ kc,
+                                   const __nv_bfloat16* __restrict__ vc,
+                                   const int32_t* __restrict__ row_slot,
+                                   const int32_t* __restrict__ row_pos,
+                                   const int32_t* __restrict__ bt, int pps, int T, int nq, int nkv,
+                                   int hd, float scale, float* __restrict__ dqkv) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= T * nq) return;
+  const int t = warp / nq, h = warp % nq, kh = h / (nq / nkv);
+  const int slot = row_slot[t], pos = row_pos[t];
+  const int dpl = hd / 32;
+  float qv[4], dov[4], dq[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < dpl; ++i) {
+    qv[i] = __bfloat162float(q[((size_t)t * nq + h) * hd + lane * dpl + i]);
+    dov[i] = d_o[((size_t)t * nq + h) * hd + lane * dpl + i];
+  }
+  const float l = lse[(size_t)t * nq + h], Dv = D[(size_t)t * nq + h];
+  for (int j = 0; j <= pos; ++j) {
+    const __nv_bfloat16* kr = kv_row(kc, bt, pps, slot, j, nkv, kh, hd);
+    const __nv_bfloat16* vr = kv_row(vc, bt, pps, slot, j, nkv, kh, hd);
+    float s = 0.f, dp = 0.f, kvv[4];
+    for (int i = 0; i < dpl; ++i) {
+      kvv[i] = __bfloat162float(kr[lane * dpl + i]);
+      s += qv[i] * kvv[i];
+      dp += dov[i] * __bfloat162float(vr[lane * dpl + i]);
+    }
+    s = warp_sum(s) * scale;
+    dp = warp_sum(dp);
+    const float p = __expf(s - l);
+    const float ds = p * (dp - Dv) * scale;
+    for (int i = 0; i < dpl; ++i) dq[i] += ds * kvv[i];
+  }
+  const int qkv = (nq + 2 * nkv) * hd;
+  for (int i = 0; i < dpl; ++i) dqkv[(size_t)t * qkv + h * hd + lane * dpl + i] = dq[i];
+}
+
+// dk, dv: one warp per (row t = the key, kv head kh); loops over the query
+// rows of the same sequence at positions >= pos(t) and the G heads.
+__global__ void attn_bwd_dkv_kernel(const __nv_bfloat16* __restrict__ q, const float* __restrict__ d_o,
+                                    const float* __restrict__ lse, const float* __restrict__ D,
+                                    const __nv_bfloat16* __restrict__ kc,
+                                    const __nv_bfloat16* __restrict__ vc,
+                                    const int32_t* __restrict__ row_slot,
+                                    const int32_t* __restrict__ row_pos,
+                                    const int32_t* __restrict__ seq_start,
+                                    const int32_t* __restrict__ seq_len,
+                                    const int32_t* __restrict__ bt, int pps, int T, int nq, int nkv,
+                                    int hd, float scale, float* __restrict__ dqkv) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= T * nkv) return;
+  const int t = warp / nkv, kh = warp % nkv;
+  const int slot = row_slot[t], pos = row_pos[t];
+  const int G = nq / nkv, dpl = hd / 32;
+  const __nv_bfloat16* kr = kv_row(kc, bt, pps, slot, pos, nkv, kh, hd);
+  const __nv_bfloat16* vr = kv_row(vc, bt, pps, slot, pos, nkv, kh, hd);
+  float kvv[4], vvv[4], dk[4] = {0.f, 0.f, 0.f, 0.f}, dv[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < dpl; ++i) {
+    kvv[i] = __bfloat162float(kr[lane * dpl + i]);
+    vvv[i] = __bfloat162float(vr[lane * dpl + i]);
+  }
+  const int s0 = seq_start[slot], L = seq_len[slot];
+  for (int p = pos; p < L; ++p) {
+    const int r = s0 + p;
+    for (int g = 0; g < G; ++g) {
+      const int h = kh * G + g;
+      float qv[4], dov[4], s = 0.f, dp = 0.f;
+      for (int i = 0; i < dpl; ++i) {
+        qv[i] = __bfloat162float(q[((size_t)r * nq + h) * hd + lane * dpl + i]);
+        dov[i] = d_o[((size_t)r * nq + h) * hd + lane * dpl + i];
+        s += qv[i] * kvv[i];
+        dp += dov[i] * vvv[i];
+      }
+      s = warp_sum(s) * scale;
+      dp = warp_sum(dp);
+      const float pr = __expf(s - lse[(size_t)r * nq + h]);
+      const float ds = pr * (dp - D[(size_t)r * nq + h]) * scale;
+      for (int i = 0; i < dpl; ++i) {
+        dk[i] += ds * qv[i];
+        dv[i] += pr * dov[i];
+      }
+    }
+  }
+  const int qkv = (nq + 2 * nkv) * hd;
+  for (int i = 0; i < dpl; ++i) {
+    dqkv[(size_t)t * qkv + nq * hd + kh * hd + lane * dpl + i] = dk[i];
+    dqkv[(size_t)t * qkv + (nq + nkv) * hd + kh * hd + lane * dpl + i] = dv[i];
+  }
+}
+
+__global__ void rope_bwd_kernel(float* __restrict__ dqkv, const int32_t* __restrict__ row_pos,
+                                const float* __restrict__ cs, int nq, int nkv, int hd) {
+  const int t = blockIdx.x, half = hd / 2;
+  const int pos = row_pos[t];
+  float* row = dqkv + (size_t)t * (nq + 2 * nkv) * hd;
+  for (int idx = threadIdx.x; idx < (nq + nkv) * half; idx += blockDim.x) {
+    const int h = idx / half, j = idx % half;
+    const float co = cs[(size_t)pos * hd + j], si = cs[(size_t)pos * hd + half + j];
+    const float d1 = row[h * hd + j], d2 = row[h * hd + j + half];
+    // forward y1 = x1 c - x2 s, y2 = x2 c + x1 s  =>  dx1 = d1 c + d2 s, dx2 = d2 c - d1 s
+    row[h * hd + j] = d1 * co + d2 * si;
+    row[h * hd + j + half] = d2 * co - d1 * si;
+  }
+}
+
+__global__ void colsum_kernel(const float* __restrict__ src, int rows, int cols, float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const int chunk = (rows + gridDim.y - 1) / gridDim.y;
+  const int r0 = blockIdx.y * chunk, r1 = min(rows, r0 + chunk);
+  float s = 0.f;
+  for (int r = r0; r < r1; ++r) s += src[(size_t)r * cols + c];
+  atomicAdd(&out[c], s);
+}
+
+__global__ void embed_bwd_kernel(const float* __restrict__ dx, const int32_t* __restrict__ tokens,
+                                 int H, float* __restrict__ dE) {
+  const int r = blockIdx.x, tok = tokens[r];
+  for (int k = threadIdx.x; k < H; k += blockDim.x) atomicAdd(&dE[(size_t)tok * H + k], dx[(size_t)r * H + k]);
+}
+
+__global__ void adam_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w,
+                            const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
+                            size_t n, float lr, float b1, float b2, float eps, float bc1, float bc2,
+                            float sign) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float upd = (mi / bc1) / (sqrtf(vi / bc2) + eps);
+    const float nw = master[i] + sign * lr * upd;
+    master[i] = nw;
+    w[i] = __float2bfloat16(nw);
+  }
+}
+
+int grid_for(size_t n, int threads) {
+  size_t b = (n + threads - 1) / threads;
+  return (int)(b > 8192 ? 8192 : (b < 1 ? 1 : b));
+}
+
+}  // namespace
+
+void launch_transpose_bf16(const __nv_bfloat16* src, int rows, int cols, __nv_bfloat16* dst,
+                           int ld, cudaStream_t st) {
+  transpose_kernel<__nv_bfloat16><<<dim3((cols + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, st>>>(
+      src, nullptr, rows, cols, dst, ld);
+}
+void launch_transpose_f32_bf16(const float* src, int rows, int cols, __nv_bfloat16* dst, int ld,
+                               cudaStream_t st) {
+  transpose_kernel<float><<<dim3((cols + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, st>>>(
+      src, nullptr, rows, cols, dst, ld);
+}
+void launch_scale_transpose_bf16(const __nv_bfloat16* src, const float* row_scale, int rows,
+                                 int cols, __nv_bfloat16* dst, int ld, cudaStream_t st) {
+  transpose_kernel<__nv_bfloat16><<<dim3((cols + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, st>>>(
+      src, row_scale, rows, cols, dst, ld);
+}
+void launch_swiglu_fwd(const float* gu, int T, int I, __nv_bfloat16* act, cudaStream_t st) {
+  swiglu_fwd_kernel<<<grid_for((size_t)T * I, 256), 256, 0, st>>>(gu, T, I, act);
+}
+void launch_f32_to_bf16(const float* src, size_t n, __nv_bfloat16* dst, cudaStream_t st) {
+  f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(src, n, dst);
+}
+void launch_bf16_to_f32(const __nv_bfloat16* src, size_t n, float* dst, cudaStream_t st) {
+  bf16_to_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(src, n, dst);
+}
+void launch_zero(float* p, size_t n, cudaStream_t st) {
+  zero_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, n);
+}
+void launch_loss_dlogits(const float* logits, const float* pmax, const double* psum, int V,
+                         int rows, const int32_t* targets, const float* coef, double* logprob,
+                         __nv_bfloat16* dlogits, cudaStream_t st) {
+  if (rows > 0)
+    loss_dlogits_kernel<<<rows, kRowThreads, 0, st>>>(logits, pmax, psum, V, targets, coef, logprob,
+                                                      dlogits);
+}
+void launch_rmsnorm_bwd(const float* dzw, const float* x, const __nv_bfloat16* g,
+                        const float* rstd, int T, int H, float* dx, float* dg, cudaStream_t st) {
+  if (T > 0) rmsnorm_bwd_kernel<<<T, kRowThreads, 0, st>>>(dzw, x, g, rstd, H, dx, dg);
+}
+void launch_row_rstd(const float* x, int T, int H, float eps, float* rstd, cudaStream_t st) {
+  if (T > 0) row_rstd_kernel<<<T, kRowThreads, 0, st>>>(x, H, eps, rstd);
+}
+void launch_swiglu_bwd(const float* dact, const float* gu, int T, int I, __nv_bfloat16* dgu,
+                       float* dgu_f32, cudaStream_t st) {
+  swiglu_bwd_kernel<<<grid_for((size_t)T * I, 256), 256, 0, st>>>(dact, gu, T, I, dgu, dgu_f32);
+}
+void launch_attention_bwd(const __nv_bfloat16* q, const __nv_bfloat16* o, const float* d_o,
+                          const float* lse, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
+                          const int32_t* row_slot, const int32_t* row_pos,
+                          const int32_t* seq_start, const int32_t* seq_len,
+                          const int32_t* block_table, int pages_per_seq, int T, int nq, int nkv,
+                          int hd, float* dqkv, cudaStream_t st) {
+  float* D = nullptr;
+  cudaMallocAsync(&D, sizeof(float) * (size_t)T * nq, st);
+  const float scale = 1.0f / sqrtf((float)hd);
+  const int w1 = T * nq, w2 = T * nkv;
+  attn_bwd_dot_kernel<<<(w1 * 32 + 255) / 256, 256, 0, st>>>(d_o, o, T, nq, hd, D);
+  attn_bwd_dq_kernel<<<(w1 * 32 + 255) / 256, 256, 0, st>>>(q, d_o, lse, D, kc, vc, row_slot, row_pos,
+                                                             block_table, pages_per_seq, T, nq, nkv,
+                                                             hd, scale, dqkv);
+  attn_bwd_dkv_kernel<<<(w2 * 32 + 255) / 256, 256, 0, st>>>(q, d_o, lse, D, kc, vc, row_slot,
+                                                              row_pos, seq_start, seq_len,
+                                                              block_table, pages_per_seq, T, nq,
+                                                              nkv, hd, scale, dqkv);
+  cudaFreeAsync(D, st);
+}
+void launch_rope_bwd(float* dqkv, const int32_t* row_pos, const float* cos_sin, int T, int nq,
+                     int nkv, int hd, cudaStream_t st) {
+  if (T > 0) rope_bwd_kernel<<<T, 128, 0, st>>>(dqkv, row_pos, cos_sin, nq, nkv, hd);
+}
+void launch_colsum_accum(const float* src, int rows, int cols, float* out, cudaStream_t st) {
+  dim3 grid((cols + 255) / 256, rows > 1024 ? 64 : (rows + 15) / 16);
+  colsum_kernel<<<grid, 256, 0, st>>>(src, rows, cols, out);
+}
+void launch_embed_bwd(const float* dx, const int32_t* tokens, int T, int H, float* dE,
+                      cudaStream_t st) {
+  if (T > 0) embed_bwd_kernel<<<T, 256, 0, st>>>(dx, tokens, H, dE);
+}
+void launch_adam(float* master, __nv_bfloat16* w, const float* grad, float* m, float* v, size_t n,
+                 float lr, float beta1, float beta2, float eps, float bias1, float bias2,
+                 float sign, cudaStream_t st) {
+  adam_kernel<<<grid_for(n, 256), 256, 0, st>>>(master, w, grad, m, v, n, lr, beta1, beta2, eps,
+                                                bias1, bias2, sign);
+}
+
+}  // namespace srl

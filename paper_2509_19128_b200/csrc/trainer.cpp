@@ -1,10 +1,27 @@
-// trainer.cpp -- trainer-side device computations of the decoder policy:
-// per-token current-policy log-prob recompute (rl_math.cpp:128-142) as a
-// chunked varlen forward over the sequence with the LM head on every row.
+// trainer.cpp -- trainer-side device computations of the decoder policy.
+//
+//  * decoder_policy_logprobs: per-token current-policy log-prob recompute
+//    (rl_math.cpp:128-142) as a chunked varlen forward.
+//  * DecoderTrainer: one truncated-IS REINFORCE step (rl_math.cpp:211-276
+//    generalised from tabular logits to the decoder's parameters):
+//      forward over the packed batch, saving activations
+//      pass 1: LM head -> log pi(y_t) for every row (fp64)
+//      IS weights: w = min(c, exp(sum lp - sum mu)) per sequence, or per token
+//      coef_t = (1/m) * w * A_t  (m = number of trajectories, stop-gradient on w)
+//      pass 2: LM head again per row chunk -> dlogits = coef (onehot - softmax)
+//      backward through the layers (tcgen05 GEMMs on transposed operands for
+//      dX = dY W and dW = dY^T X, CUDA-core RMSNorm / SwiGLU / RoPE /
+//      attention backward) into one fp32 gradient buffer laid out like the
+//      weights -- the ascent direction of J, as in the reference.
+//  * Adam on fp32 master weights writes the bf16 weights that the generator
+//    receives (ncclBroadcast payload).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "decoder_engine.hpp"
+#include "train.cuh"
+#include "trainer.hpp"
 
 namespace srl {
 
@@ -51,6 +68,376 @@ int decoder_policy_logprobs(const DecoderWeights& w, const std::vector<int32_t>&
   cudaFree(dout);
   cudaStreamDestroy(st);
   return status;
+}
+
+// ----------------------------------------------------------- trainer ---
+namespace {
+constexpr int kLogitChunk = 512;  // rows per LM-head pass (logits chunk = 512 x V fp32)
+int pad64(int x) { return (x + 63) / 64 * 64; }
+}  // namespace
+
+DecoderTrainer::~DecoderTrainer() {
+  if (st_) cudaStreamSynchronize(st_);
+  for (void* p : allocs_) cudaFree(p);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+template <typename T>
+int DecoderTrainer::alloc(T** p, size_t n) {
+  SRL_CUDA(cudaMalloc(p, std::max<size_t>(n, 1) * sizeof(T)));
+  SRL_CUDA(cudaMemsetAsync(*p, 0, std::max<size_t>(n, 1) * sizeof(T), st_));
+  allocs_.push_back(*p);
+  return SRL_OK;
+}
+
+int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) {
+  opts_ = o;
+  d_ = w.dims;
+  dev_ = w.device;
+  SRL_CUDA(cudaSetDevice(dev_));
+  SRL_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  int st;
+  if ((st = clone_decoder(w, weights_))) return st;
+  lay_ = weights_->layout;
+  n_ = lay_.total;
+  T_max_ = pad64(std::max(64, o.max_tokens));
+  const int H = d_.H, L = d_.L, I = d_.I, qd = d_.qdim(), qkv = d_.qkv();
+  // fp32 master weights, Adam moments, gradient, transposed bf16 weights
+  if ((st = alloc(&master_, n_)) || (st = alloc(&grad_, n_)) || (st = alloc(&adam_m_, n_)) ||
+      (st = alloc(&adam_v_, n_)) || (st = alloc(&wt_, n_)))
+    return st;
+  launch_bf16_to_f32(weights_->w, n_, master_, st_);
+  // saved activations
+  acts_.resize(L);
+  for (int l = 0; l < L; ++l) {
+    LayerActs& a = acts_[l];
+    if ((st = alloc(&a.x_in, (size_t)T_max_ * H)) || (st = alloc(&a.xg1, (size_t)T_max_ * H)) ||
+        (st = alloc(&a.rstd1, T_max_)) || (st = alloc(&a.q, (size_t)T_max_ * qd)) ||
+        (st = alloc(&a.attn, (size_t)T_max_ * qd)) || (st = alloc(&a.lse, (size_t)T_max_ * d_.nq)) ||
+        (st = alloc(&a.x_mid, (size_t)T_max_ * H)) || (st = alloc(&a.xg2, (size_t)T_max_ * H)) ||
+        (st = alloc(&a.rstd2, T_max_)) || (st = alloc(&a.gu, (size_t)T_max_ * 2 * I)) ||
+        (st = alloc(&a.act, (size_t)T_max_ * I)))
+      return st;
+  }
+  if ((st = alloc(&x_, (size_t)T_max_ * H)) || (st = alloc(&xgF_, (size_t)T_max_ * H)) ||
+      (st = alloc(&rstdF_, T_max_)) || (st = alloc(&ssq_, (size_t)T_max_ * d_.ssq_parts())) ||
+      (st = alloc(&logits_, (size_t)kLogitChunk * d_.V)) ||
+      (st = alloc(&pmax_, (size_t)kLogitChunk * ((d_.V + 127) / 128))) ||
+      (st = alloc(&psum_, (size_t)kLogitChunk * ((d_.V + 127) / 128))) ||
+      (st = alloc(&dlogits_, (size_t)kLogitChunk * d_.V)) ||
+      (st = alloc(&dlogitsT_, (size_t)d_.V * kLogitChunk)) || (st = alloc(&dx_, (size_t)T_max_ * H)) ||
+      (st = alloc(&dz_, (size_t)T_max_ * std::max(H, 2 * I))) ||
+      (st = alloc(&dbig_, (size_t)T_max_ * std::max({2 * I, qkv, qd}))) ||
+      (st = alloc(&dbig_bf_, (size_t)T_max_ * std::max({2 * I, qkv, qd, H}))) ||
+      (st = alloc(&tA_, (size_t)std::max({2 * I, qkv, qd, H, I}) * T_max_)) ||
+      (st = alloc(&tB_, (size_t)std::max({2 * I, qkv, qd, H, I}) * T_max_)) ||
+      (st = alloc(&ones_, T_max_)) || (st = alloc(&row_slot_, T_max_)) ||
+      (st = alloc(&row_pos_, T_max_)) || (st = alloc(&row_tok_, T_max_)) ||
+      (st = alloc(&row_tgt_, T_max_)) || (st = alloc(&coef_, T_max_)) ||
+      (st = alloc(&lp_, T_max_)) || (st = alloc(&cos_sin_, (size_t)d_.max_pos * d_.hd)))
+    return st;
+  launch_rope_table(cos_sin_, d_.max_pos, d_.hd, (double)d_.theta, st_);
+  std::vector<float> ones(T_max_, 1.f);
+  SRL_CUDA(cudaMemcpyAsync(ones_, ones.data(), 4 * (size_t)T_max_, cudaMemcpyHostToDevice, st_));
+  SRL_CUDA(cudaStreamSynchronize(st_));
+  sms_ = 148;
+  cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev_);
+  return SRL_OK;
+}
+
+// C[m, n] (epilogue) = sum_k X[m, k] * W[n, k]; X, W bf16 K-major.
+int DecoderTrainer::gemm(const __nv_bfloat16* X, int x_rows_alloc, int M, const __nv_bfloat16* W,
+                         int N, int K, const EpiParams& e) {
+  const int tok = gemm_tok_tile(M);
+  const CUtensorMap tx = make_tmap_bf16(X, (uint64_t)std::max(x_rows_alloc, M), (uint64_t)K, (uint32_t)tok);
+  const CUtensorMap tw = make_tmap_bf16(W, (uint64_t)N, (uint64_t)K, 128);
+  GemmWorkspace ws;
+  const cudaError_t err = gemm_bf16_launch(tw, tx, M, N, K, gemm_auto_splits(M, N, K, sms_), ws, e, st_);
+  if (err != cudaSuccess) return cuda_fail(err, "trainer gemm");
+  return SRL_OK;
+}
+
+int DecoderTrainer::gemm_store(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K,
+                               float* out) {
+  EpiParams e;
+  e.kind = EPI_STORE_F32;
+  e.out_f32 = out;
+  e.ld_out = N;
+  return gemm(X, M, M, W, N, K, e);
+}
+
+int DecoderTrainer::gemm_accum(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K,
+                               float* out) {
+  EpiParams e;
+  e.kind = EPI_ACCUM_F32;
+  e.out_f32 = out;
+  e.ld_out = N;
+  return gemm(X, M, M, W, N, K, e);
+}
+
+// W^T of every matrix (K-major operands for dX = dY W).
+void DecoderTrainer::transpose_weights() {
+  const __nv_bfloat16* w = weights_->w;
+  auto tr = [&](size_t off, int rows, int cols) {
+    launch_transpose_bf16(w + off, rows, cols, wt_ + off, rows, st_);
+  };
+  for (int l = 0; l < d_.L; ++l) {
+    const LayerOffsets& o = lay_.layers[l];
+    tr(o.qkv_w, d_.qkv(), d_.H);
+    tr(o.o_w, d_.H, d_.qdim());
+    tr(o.gate_up_w, 2 * d_.I, d_.H);
+    tr(o.down_w, d_.H, d_.I);
+  }
+  tr(lay_.lm_head, d_.V, d_.H);
+}
+
+int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
+  const int T = b.rows, Tp = pad64(T);
+  if (T < 1 || Tp > T_max_) return fail(SRL_INVALID_ARGUMENT, "trainer: batch exceeds max_tokens");
+  const int H = d_.H, I = d_.I, L = d_.L, qd = d_.qdim(), qkv = d_.qkv(), V = d_.V;
+  const int parts = d_.ssq_parts();
+  const float inv_h = 1.f / (float)H;
+  const __nv_bfloat16* w = weights_->w;
+  cudaStream_t st = st_;
+  SRL_CUDA(cudaSetDevice(dev_));
+  int s;
+
+  // ---- batch layout: rows (seq, pos); KV pages per sequence
+  const int n_seq = (int)b.seq_len.size();
+  int pps = 1;
+  for (int l : b.seq_len) pps = std::max(pps, (l + kPageTokens - 1) / kPageTokens);
+  const size_t n_pages = (size_t)n_seq * pps;
+  const size_t kv_elems = n_pages * d_.nkv * kPageTokens * d_.hd;
+  if (kv_elems * L > kv_cap_) {
+    if (kc_) { cudaFree(kc_); cudaFree(vc_); }
+    SRL_CUDA(cudaMalloc(&kc_, kv_elems * L * 2));
+    SRL_CUDA(cudaMalloc(&vc_, kv_elems * L * 2));
+    kv_cap_ = kv_elems * L;
+  }
+  std::vector<int32_t> bt(n_pages);
+  for (size_t i = 0; i < n_pages; ++i) bt[i] = (int32_t)i;
+  int32_t *d_bt = nullptr, *d_sstart = nullptr, *d_slen = nullptr;
+  SRL_CUDA(cudaMallocAsync(&d_bt, 4 * n_pages, st));
+  SRL_CUDA(cudaMallocAsync(&d_sstart, 4 * (size_t)n_seq, st));
+  SRL_CUDA(cudaMallocAsync(&d_slen, 4 * (size_t)n_seq, st));
+  SRL_CUDA(cudaMemcpyAsync(d_bt, bt.data(), 4 * n_pages, cudaMemcpyHostToDevice, st));
+  SRL_CUDA(cudaMemcpyAsync(d_sstart, b.seq_start.data(), 4 * (size_t)n_seq, cudaMemcpyHostToDevice, st));
+  SRL_CUDA(cudaMemcpyAsync(d_slen, b.seq_len.data(), 4 * (size_t)n_seq, cudaMemcpyHostToDevice, st));
+  SRL_CUDA(cudaMemcpyAsync(row_slot_, b.row_slot.data(), 4 * (size_t)T, cudaMemcpyHostToDevice, st));
+  SRL_CUDA(cudaMemcpyAsync(row_pos_, b.row_pos.data(), 4 * (size_t)T, cudaMemcpyHostToDevice, st));
+  SRL_CUDA(cudaMemcpyAsync(row_tok_, b.row_token.data(), 4 * (size_t)T, cudaMemcpyHostToDevice, st));
+  SRL_CUDA(cudaMemcpyAsync(row_tgt_, b.row_target.data(), 4 * (size_t)T, cudaMemcpyHostToDevice, st));
+
+  cudaEvent_t e0, e1, e2;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  cudaEventRecord(e0, st);
+
+  // ---- forward with saved activations
+  launch_embed(w + lay_.embed, w + lay_.layers[0].ln1, row_tok_, T, H, V, x_, acts_[0].xg1, ssq_, st);
+  for (int l = 0; l < L; ++l) {
+    LayerActs& a = acts_[l];
+    const LayerOffsets& o = lay_.layers[l];
+    SRL_CUDA(cudaMemcpyAsync(a.x_in, x_, sizeof(float) * T * H, cudaMemcpyDeviceToDevice, st));
+    launch_row_rstd(a.x_in, T, H, d_.eps, a.rstd1, st);
+    __nv_bfloat16* kcl = kc_ + kv_elems * l;
+    __nv_bfloat16* vcl = vc_ + kv_elems * l;
+    EpiParams e;
+    e.kind = EPI_QKV;
+    e.ssq_in = ssq_; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d_.eps;
+    e.bias = w + o.qkv_b;
+    e.nq = d_.nq; e.nkv = d_.nkv; e.hd = d_.hd; e.pages_per_seq = pps;
+    e.row_slot = row_slot_; e.row_pos = row_pos_; e.block_table = d_bt; e.cos_sin = cos_sin_;
+    e.q_out = a.q; e.kc = kcl; e.vc = vcl;
+    if ((s = gemm(a.xg1, T_max_, T, w + o.qkv_w, qkv, H, e))) return s;
+    RoundPlan plan{row_slot_, row_pos_, row_tok_, nullptr};
+    float* attn_ws = nullptr;
+    int* attn_cnt = nullptr;
+    const size_t aws = attention_ws_floats(d_, T, d_.max_pos);
+    SRL_CUDA(cudaMallocAsync(&attn_ws, sizeof(float) * aws, st));
+    SRL_CUDA(cudaMallocAsync(&attn_cnt, sizeof(int) * (size_t)T * d_.nkv, st));
+    SRL_CUDA(cudaMemsetAsync(attn_cnt, 0, sizeof(int) * (size_t)T * d_.nkv, st));
+    int max_ctx = 1;
+    for (int len : b.seq_len) max_ctx = std::max(max_ctx, len);
+    launch_attention(a.q, d_, plan, T, d_bt, pps, kcl, vcl, max_ctx, attn_ws, attn_cnt, aws, a.attn,
+                     st, a.lse);
+    cudaFreeAsync(attn_ws, st);
+    cudaFreeAsync(attn_cnt, st);
+    EpiParams r;
+    r.kind = EPI_RESID; r.resid = x_; r.gain = w + o.ln2; r.xg = a.xg2; r.ssq_out = ssq_;
+    if ((s = gemm(a.attn, T_max_, T, w + o.o_w, H, qd, r))) return s;
+    SRL_CUDA(cudaMemcpyAsync(a.x_mid, x_, sizeof(float) * T * H, cudaMemcpyDeviceToDevice, st));
+    launch_row_rstd(a.x_mid, T, H, d_.eps, a.rstd2, st);
+    EpiParams g;
+    g.kind = EPI_STORE_F32;
+    g.ssq_in = ssq_; g.ssq_in_parts = parts; g.inv_dim = inv_h; g.eps = d_.eps;
+    g.out_f32 = a.gu; g.ld_out = 2 * I;
+    if ((s = gemm(a.xg2, T_max_, T, w + o.gate_up_w, 2 * I, H, g))) return s;
+    launch_swiglu_fwd(a.gu, T, I, a.act, st);
+    EpiParams r2;
+    r2.kind = EPI_RESID; r2.resid = x_; r2.ssq_out = ssq_;
+    r2.xg = l + 1 < L ? acts_[l + 1].xg1 : xgF_;
+    r2.gain = w + (l + 1 < L ? lay_.layers[l + 1].ln1 : lay_.final_norm);
+    if ((s = gemm(a.act, T_max_, T, w + o.down_w, H, I, r2))) return s;
+  }
+  launch_row_rstd(x_, T, H, d_.eps, rstdF_, st);
+
+  // ---- pass 1: log pi(target) of every row
+  const int nT = (V + 127) / 128;
+  for (int c0 = 0; c0 < T; c0 += kLogitChunk) {
+    const int C = std::min(kLogitChunk, T - c0);
+    EpiParams e;
+    e.kind = EPI_LOGITS;
+    e.ssq_in = ssq_ + (size_t)c0 * parts; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d_.eps;
+    e.out_f32 = logits_; e.ld_out = V; e.part_max = pmax_; e.part_sum = psum_;
+    if ((s = gemm(xgF_ + (size_t)c0 * H, C, C, w + lay_.lm_head, V, H, e))) return s;
+    launch_loss_dlogits(logits_, pmax_, psum_, V, C, row_tgt_ + c0, ones_, lp_ + c0, dlogits_, st);
+  }
+  cudaEventRecord(e1, st);
+  std::vector<double> lp(T);
+  SRL_CUDA(cudaMemcpyAsync(lp.data(), lp_, 8 * (size_t)T, cudaMemcpyDeviceToHost, st));
+  SRL_CUDA(cudaStreamSynchronize(st));
+
+  // ---- truncated IS weights and per-row coefficients (host: O(tokens) scalars)
+  std::vector<float> coef(T, 0.f);
+  const double inv_m = 1.0 / (double)std::max(1, b.n_trajectories);
+  std::vector<double> seq_w(n_seq, 1.0);
+  double loss = 0.0, ess_num = 0.0, ess_den = 0.0;
+  int clamped = 0;
+  for (int q = 0; q < n_seq; ++q) {
+    double pi = 0.0, mu = 0.0;
+    for (int p = b.loss_begin[q]; p < b.seq_len[q]; ++p) {
+      pi += lp[b.seq_start[q] + p];
+      mu += b.row_mu[b.seq_start[q] + p];
+    }
+    if (b.granularity == 0) {
+      const double r = std::exp(pi - mu);
+      seq_w[q] = std::min(b.clamp, r);  // truncated_is_weight (rl_math.cpp:144-150)
+      if (r > b.clamp) ++clamped;
+      ess_num += seq_w[q];
+      ess_den += seq_w[q] * seq_w[q];
+    }
+    for (int p = b.loss_begin[q]; p < b.seq_len[q]; ++p) {
+      const int row = b.seq_start[q] + p;
+      double wgt = seq_w[q];
+      if (b.granularity == 1) {
+        const double r = std::exp(lp[row] - b.row_mu[row]);
+        wgt = std::min(b.clamp, r);
+        if (r > b.clamp) ++clamped;
+        ess_num += wgt;
+        ess_den += wgt * wgt;
+      }
+      const double c = inv_m * wgt * b.row_adv[row];
+      coef[row] = (float)c;
+      loss += c * lp[row];
+    }
+  }
+  SRL_CUDA(cudaMemcpyAsync(coef_, coef.data(), 4 * (size_t)T, cudaMemcpyHostToDevice, st));
+
+  // ---- backward
+  launch_zero(grad_, n_, st);
+  transpose_weights();
+  launch_zero(dx_, (size_t)T_max_ * H, st);
+  // pass 2: dlogits per chunk -> d(final xg) and dE(lm_head)
+  float* g_lm = grad_ + lay_.lm_head;
+  for (int c0 = 0; c0 < T; c0 += kLogitChunk) {
+    const int C = std::min(kLogitChunk, T - c0), Cp = pad64(C);
+    EpiParams e;
+    e.kind = EPI_LOGITS;
+    e.ssq_in = ssq_ + (size_t)c0 * parts; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d_.eps;
+    e.out_f32 = logits_; e.ld_out = V; e.part_max = pmax_; e.part_sum = psum_;
+    if ((s = gemm(xgF_ + (size_t)c0 * H, C, C, w + lay_.lm_head, V, H, e))) return s;
+    launch_loss_dlogits(logits_, pmax_, psum_, V, C, row_tgt_ + c0, coef_ + c0, lp_ + c0, dlogits_, st);
+    // dzw[t, h] = sum_v dlogits[t, v] E[v, h]   (W-side operand: E^T [H x V])
+    if ((s = gemm_store(dlogits_, C, wt_ + lay_.lm_head, H, V, dz_))) return s;
+    launch_rmsnorm_bwd(dz_, x_ + (size_t)c0 * H, w + lay_.final_norm, rstdF_ + c0, C, H,
+                       dx_ + (size_t)c0 * H, grad_ + lay_.final_norm, st);
+    // dE[v, h] += sum_t dlogits[t, v] * rstd[t] xg[t, h]
+    SRL_CUDA(cudaMemsetAsync(dlogitsT_, 0, sizeof(__nv_bfloat16) * (size_t)V * Cp, st));
+    SRL_CUDA(cudaMemsetAsync(tB_, 0, sizeof(__nv_bfloat16) * (size_t)H * Cp, st));
+    launch_transpose_bf16(dlogits_, C, V, dlogitsT_, Cp, st);
+    launch_scale_transpose_bf16(xgF_ + (size_t)c0 * H, rstdF_ + c0, C, H, tB_, Cp, st);
+    if ((s = gemm_accum(dlogitsT_, V, tB_, H, Cp, g_lm))) return s;
+  }
+  // layers in reverse; dx_ holds dJ/dx_out of the layer being processed
+  for (int l = L - 1; l >= 0; --l) {
+    LayerActs& a = acts_[l];
+    const LayerOffsets& o = lay_.layers[l];
+    // down: x_out = x_mid + act W_down^T
+    launch_f32_to_bf16(dx_, (size_t)T * H, dbig_bf_, st);                      // dY bf16 [T x H]
+    if ((s = gemm_store(dbig_bf_, T, wt_ + o.down_w, I, H, dz_))) return s;   // dact [T x I]
+    SRL_CUDA(cudaMemsetAsync(tA_, 0, sizeof(__nv_bfloat16) * (size_t)H * Tp, st));
+    SRL_CUDA(cudaMemsetAsync(tB_, 0, sizeof(__nv_bfloat16) * (size_t)I * Tp, st));
+    launch_transpose_f32_bf16(dx_, T, H, tA_, Tp, st);                        // dY^T [H x Tp]
+    launch_transpose_bf16(a.act, T, I, tB_, Tp, st);                           // act^T [I x Tp]
+    if ((s = gemm_accum(tA_, H, tB_, I, Tp, grad_ + o.down_w))) return s;     // dW_down [H x I]
+    // SwiGLU
+    launch_swiglu_bwd(dz_, a.gu, T, I, dbig_bf_, nullptr, st);                 // dgu bf16 [T x 2I]
+    // gate_up: gu = rstd2 * (xg2 W_gu^T)
+    if ((s = gemm_store(dbig_bf_, T, wt_ + o.gate_up_w, H, 2 * I, dz_))) return s;  // dzw [T x H]
+    SRL_CUDA(cudaMemsetAsync(tA_, 0, sizeof(__nv_bfloat16) * (size_t)2 * I * Tp, st));
+    SRL_CUDA(cudaMemsetAsync(tB_, 0, sizeof(__nv_bfloat16) * (size_t)H * Tp, st));
+    launch_transpose_bf16(dbig_bf_, T, 2 * I, tA_, Tp, st);                    // dgu^T
+    launch_scale_transpose_bf16(a.xg2, a.rstd2, T, H, tB_, Tp, st);            // xn2^T
+    if ((s = gemm_accum(tA_, 2 * I, tB_, H, Tp, grad_ + o.gate_up_w))) return s;
+    launch_rmsnorm_bwd(dz_, a.x_mid, w + o.ln2, a.rstd2, T, H, dx_, grad_ + o.ln2, st);
+    // O: x_mid = x_in + attn W_o^T   (dx_ now = dJ/dx_mid)
+    launch_f32_to_bf16(dx_, (size_t)T * H, dbig_bf_, st);
+    if ((s = gemm_store(dbig_bf_, T, wt_ + o.o_w, qd, H, dz_))) return s;     // dO [T x qd]
+    SRL_CUDA(cudaMemsetAsync(tA_, 0, sizeof(__nv_bfloat16) * (size_t)H * Tp, st));
+    SRL_CUDA(cudaMemsetAsync(tB_, 0, sizeof(__nv_bfloat16) * (size_t)qd * Tp, st));
+    launch_transpose_f32_bf16(dx_, T, H, tA_, Tp, st);
+    launch_transpose_bf16(a.attn, T, qd, tB_, Tp, st);
+    if ((s = gemm_accum(tA_, H, tB_, qd, Tp, grad_ + o.o_w))) return s;
+    // attention + RoPE backward -> dqkv (pre-RoPE, pre-bias) fp32
+    launch_attention_bwd(a.q, a.attn, dz_, a.lse, kc_ + kv_elems * l, vc_ + kv_elems * l, row_slot_,
+                         row_pos_, d_sstart, d_slen, d_bt, pps, T, d_.nq, d_.nkv, d_.hd, dbig_, st);
+    launch_rope_bwd(dbig_, row_pos_, cos_sin_, T, d_.nq, d_.nkv, d_.hd, st);
+    launch_colsum_accum(dbig_, T, qkv, grad_ + o.qkv_b, st);
+    launch_f32_to_bf16(dbig_, (size_t)T * qkv, dbig_bf_, st);
+    if ((s = gemm_store(dbig_bf_, T, wt_ + o.qkv_w, H, qkv, dz_))) return s;  // dzw [T x H]
+    SRL_CUDA(cudaMemsetAsync(tA_, 0, sizeof(__nv_bfloat16) * (size_t)qkv * Tp, st));
+    SRL_CUDA(cudaMemsetAsync(tB_, 0, sizeof(__nv_bfloat16) * (size_t)H * Tp, st));
+    launch_transpose_bf16(dbig_bf_, T, qkv, tA_, Tp, st);
+    launch_scale_transpose_bf16(a.xg1, a.rstd1, T, H, tB_, Tp, st);
+    if ((s = gemm_accum(tA_, qkv, tB_, H, Tp, grad_ + o.qkv_w))) return s;
+    launch_rmsnorm_bwd(dz_, a.x_in, w + o.ln1, a.rstd1, T, H, dx_, grad_ + o.ln1, st);
+  }
+  launch_embed_bwd(dx_, row_tok_, T, H, grad_ + lay_.embed, st);
+  cudaEventRecord(e2, st);
+  cudaFreeAsync(d_bt, st);
+  cudaFreeAsync(d_sstart, st);
+  cudaFreeAsync(d_slen, st);
+  SRL_CUDA(cudaStreamSynchronize(st));
+  SRL_CUDA(cudaGetLastError());
+  float fwd_ms = 0.f, all_ms = 0.f;
+  cudaEventElapsedTime(&fwd_ms, e0, e1);
+  cudaEventElapsedTime(&all_ms, e0, e2);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  if (stats) {
+    stats->objective = loss;
+    // ess over the IS weights actually used (rl_math.cpp:152-163)
+    const double nw = b.granularity == 0 ? (double)n_seq : (double)b.n_loss_rows;
+    stats->ess = (ess_den > 0 && nw > 0) ? (ess_num * ess_num) / (nw * ess_den) : 0.0;
+    stats->clamped = clamped;
+    stats->tokens = T;
+    stats->forward_ms = fwd_ms;
+    stats->step_ms = all_ms;
+  }
+  lp_host_ = std::move(lp);
+  return SRL_OK;
+}
+
+int DecoderTrainer::apply_adam(float lr, float beta1, float beta2, float eps) {
+  ++adam_t_;
+  const float b1 = 1.f - std::pow(beta1, (float)adam_t_), b2 = 1.f - std::pow(beta2, (float)adam_t_);
+  launch_adam(master_, weights_->w, grad_, adam_m_, adam_v_, n_, lr, beta1, beta2, eps, b1, b2, +1.f,
+              st_);
+  SRL_CUDA(cudaStreamSynchronize(st_));
+  return SRL_OK;
 }
 
 }  // namespace srl

@@ -1,0 +1,73 @@
+// trainer.hpp -- DecoderTrainer: IS-REINFORCE gradient of the decoder policy
+// on the device (see trainer.cpp).
+#pragma once
+#include <memory>
+#include <vector>
+
+#include "gemm.cuh"
+#include "runtime.hpp"
+
+namespace srl {
+
+// A packed batch of sequences: rows (seq, pos) with input and target token.
+struct TrainBatch {
+  int rows = 0;
+  int n_trajectories = 1;  // m of rl_math.cpp:219 (1/m normalisation)
+  double clamp = 5.0;
+  int granularity = 0;     // 0 Sequence, 1 PerToken (rl_math.hpp:52)
+  int n_loss_rows = 0;
+  std::vector<int32_t> seq_start, seq_len, loss_begin;  // per sequence (rows)
+  std::vector<int32_t> row_slot, row_pos, row_token, row_target;
+  std::vector<double> row_mu, row_adv;  // behaviour log-prob and advantage of each row's target
+};
+
+class DecoderTrainer {
+ public:
+  ~DecoderTrainer();
+  int init(const DecoderWeights& w, const srl_trainer_options& o);
+  int step(const TrainBatch& b, srl_trainer_stats* stats);
+  int apply_adam(float lr, float beta1, float beta2, float eps);
+  float* gradient() const { return grad_; }
+  size_t elements() const { return n_; }
+  DecoderWeights& weights() { return *weights_; }
+  const std::vector<double>& last_logprobs() const { return lp_host_; }
+
+ private:
+  struct LayerActs {
+    float *x_in = nullptr, *rstd1 = nullptr, *lse = nullptr, *x_mid = nullptr, *rstd2 = nullptr,
+          *gu = nullptr;
+    __nv_bfloat16 *xg1 = nullptr, *q = nullptr, *attn = nullptr, *xg2 = nullptr, *act = nullptr;
+  };
+  template <typename T>
+  int alloc(T** p, size_t n);
+  int gemm(const __nv_bfloat16* X, int x_rows_alloc, int M, const __nv_bfloat16* W, int N, int K,
+           const EpiParams& e);
+  int gemm_store(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, float* out);
+  int gemm_accum(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, float* out);
+  void transpose_weights();
+
+  srl_trainer_options opts_{};
+  DecoderDims d_{};
+  WeightLayout lay_{};
+  std::shared_ptr<DecoderWeights> weights_;
+  size_t n_ = 0;
+  int dev_ = 0, T_max_ = 64, sms_ = 148, adam_t_ = 0;
+  cudaStream_t st_ = nullptr;
+  std::vector<void*> allocs_;
+  float *master_ = nullptr, *grad_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;
+  __nv_bfloat16* wt_ = nullptr;  // transposed weights (same offsets)
+  std::vector<LayerActs> acts_;
+  float *x_ = nullptr, *rstdF_ = nullptr, *ssq_ = nullptr, *logits_ = nullptr, *pmax_ = nullptr;
+  double* psum_ = nullptr;
+  __nv_bfloat16 *xgF_ = nullptr, *dlogits_ = nullptr, *dlogitsT_ = nullptr, *dbig_bf_ = nullptr,
+                *tA_ = nullptr, *tB_ = nullptr;
+  float *dx_ = nullptr, *dz_ = nullptr, *dbig_ = nullptr, *ones_ = nullptr, *coef_ = nullptr,
+        *cos_sin_ = nullptr;
+  double* lp_ = nullptr;
+  int32_t *row_slot_ = nullptr, *row_pos_ = nullptr, *row_tok_ = nullptr, *row_tgt_ = nullptr;
+  __nv_bfloat16 *kc_ = nullptr, *vc_ = nullptr;
+  size_t kv_cap_ = 0;
+  std::vector<double> lp_host_;
+};
+
+}  // namespace srl
