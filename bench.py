@@ -126,8 +126,9 @@ def algorithmic_bytes(cfg, rows, ctx_sum):
     qkv = (nq + 2 * nkv) * hd
     b = {}
     b["embed"] = rows * H * (2 + 4 + 2)
-    b["qkv_gemm"] = L * (qkv * H * 2 + rows * H * 2 + rows * qkv * 4)
-    b["rope_kv_append"] = L * rows * (qkv * 4 + nq * hd * 2 + 2 * nkv * hd * 2)
+    # QKV GEMM with the fused bias + RoPE + paged K/V append epilogue
+    b["qkv_gemm"] = L * (qkv * H * 2 + rows * H * 2 + rows * qkv * 2)
+    b["rope_kv_append"] = 0
     b["attention"] = L * (ctx_sum * 2 * nkv * hd * 2 + rows * nq * hd * 2 * 2)
     b["o_gemm"] = L * (H * nq * hd * 2 + rows * nq * hd * 2 + rows * H * (4 + 4 + 2))
     b["gate_up_gemm"] = L * (2 * I * H * 2 + rows * H * 2 + rows * I * 2)
@@ -232,6 +233,7 @@ def main():
     from paper_2509_19128_b200 import _lib
     from paper_2509_19128_b200.engine import Engine
     from paper_2509_19128_b200.policy import DecoderPolicy
+    from paper_2509_19128_b200.weight_sync import EngineStandby, WeightChannel, max_over_ranks
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -264,34 +266,29 @@ def main():
     for i in range(B):
         open_one(i, max(8, args.gen - (i * args.gen) // B))
 
-    version = 0
     token_versions = []  # finished sequences (for lag stats)
     s = torch.cuda.Stream(device=dev)
+    chan = WeightChannel(src=0)
+    standby = EngineStandby(eng, dev)
 
     def step(record):
-        nonlocal version, d2h_bytes
+        nonlocal d2h_bytes
         st0 = eng.stats()
         t_wall = time.perf_counter()
         emitted = eng.advance(R)
-        # in-flight update: trainer weights -> standby buffer -> swap at token boundary
-        version += 1
-        ptr, nbytes = eng.begin_weight_update(version)
-        dst = torch.as_tensor(_Raw(ptr, nbytes), device=dev)
+        # in-flight update: trainer rank 0's weights -> every standby buffer
+        # (ncclBroadcast for N > 1, a device copy at N = 1) -> swap at the next
+        # token boundary; the streams continue on their stale KV cache
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        src, n = payloads[(chan.version + 1) % 2].weights()
+        payload = torch.as_tensor(_Raw(src, n), device=dev)
         with torch.cuda.stream(s):
             e0.record(s)
-            if world > 1:
-                if rank == 0:
-                    src, n = payloads[version % 2].weights()
-                    dst.copy_(torch.as_tensor(_Raw(src, n), device=dev))
-                dist.broadcast(dst, src=0)
-            else:
-                src, n = payloads[version % 2].weights()
-                dst.copy_(torch.as_tensor(_Raw(src, n), device=dev))
+            applied, _, pause = chan.publish(rank, None, payload if rank == 0 else None,
+                                                   engine=standby)
             e1.record(s)
         s.synchronize()
-        res, pause = eng.commit_weight_update(version)
-        assert res.applied, res
+        assert applied, "weight update rejected"
         # actor side: drain events, refill finished streams (constant batch)
         finished = []
         for sid in list(live):
@@ -344,15 +341,13 @@ def main():
     launches = sum(r["launches"] for r in rec)
     pauses = [r["pause_ms"] for r in rec]
     upd = [r["update_ms"] for r in rec]
-    t = torch.tensor([dev_ms, wall_ms, float(tokens)], dtype=torch.float64, device=dev)
+    dev_ms_max = max_over_ranks(dev_ms)
+    wall_ms_max = max_over_ranks(wall_ms)
+    total_tokens = float(tokens)
     if world > 1:
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = t.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        dev_ms_max, wall_ms_max, total_tokens = mx[0].item(), mx[1].item(), sm[2].item()
-    else:
-        dev_ms_max, wall_ms_max, total_tokens = dev_ms, wall_ms, float(tokens)
+        t = torch.tensor([float(tokens)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        total_tokens = t.item()
 
     # lag bookkeeping of the sequences consumed so far (device lag kernel)
     lag = {"max_lag_steps": None}
@@ -364,7 +359,7 @@ def main():
         hist = torch.zeros(4096, dtype=torch.int64, device=dev)
         sums = torch.zeros(len(seqs), dtype=torch.int64, device=dev)
         tot = torch.zeros(4, dtype=torch.int64, device=dev)
-        _lib.call("srl_lag_stats", vers.data_ptr(), offs.data_ptr(), len(seqs), version,
+        _lib.call("srl_lag_stats", vers.data_ptr(), offs.data_ptr(), len(seqs), chan.version,
                   hist.data_ptr(), 4096, sums.data_ptr(), tot.data_ptr(), None)
         torch.cuda.synchronize()
         tt = tot.cpu().tolist()
