@@ -32,8 +32,18 @@ extern "C" int srl_kernel_gemm_bf16(const void* w, const void* x, int32_t M, int
   const CUtensorMap tw = make_tmap_bf16(w, (uint64_t)N, (uint64_t)K, 128);
   const CUtensorMap tx = make_tmap_bf16(x, (uint64_t)M, (uint64_t)K, (uint32_t)tok);
   if (splits <= 0) splits = gemm_auto_splits(M, N, K, num_sms());
-  GemmWorkspace ws;  // cluster split-K reduces through DSMEM: no workspace
+  GemmWorkspace ws;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static float* g_ws = nullptr;
+  static size_t g_ws_floats = 0;
+  const size_t need = gemm_workspace_floats(M, N, splits);
+  if (need > g_ws_floats) {
+    if (g_ws) cudaFree(g_ws);
+    if (cudaMalloc(&g_ws, need * sizeof(float)) != cudaSuccess) return SRL_OUT_OF_MEMORY;
+    g_ws_floats = need;
+  }
+  ws.partials = g_ws;
+  ws.partial_floats = g_ws_floats;
   EpiParams epi;
   epi.stamps = g_stamps;
   epi.kind = epi_kind;

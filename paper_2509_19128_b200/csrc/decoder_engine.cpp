@@ -6,6 +6,7 @@
 // CUDA-graph decode rounds, double-buffered weights with a pointer swap at
 // token boundaries, optional KV recompute after a swap).
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -233,6 +234,11 @@ DecoderBackend::DecoderBackend(const Policy& p, const srl_engine_options& o) : o
 DecoderBackend::~DecoderBackend() {
   if (st_) cudaStreamSynchronize(st_);
   for (int b = 0; b < 2; ++b)
+    if (mk_.wmaps[b]) cudaFree(mk_.wmaps[b]);
+  if (mk_.mem) cudaFree(mk_.mem);
+  if (mk_.ws) cudaFree(mk_.ws);
+  if (mk_.stamps_host) cudaFreeHost(mk_.stamps_host);
+  for (int b = 0; b < 2; ++b)
     if (exec_[b]) cudaGraphExecDestroy(exec_[b]);
   if (dev_state_) cudaFree(dev_state_);
   if (pinned_) cudaFreeHost(pinned_);
@@ -297,6 +303,131 @@ int DecoderBackend::init(const Policy& p) {
   SRL_CUDA(cudaMemcpy(runner_->next.last_row, neg.data(), 4 * (size_t)S_, cudaMemcpyHostToDevice));
   SRL_CUDA(cudaMemcpy(runner_->plan.row_slot, neg.data(), 4 * (size_t)runner_->M_max, cudaMemcpyHostToDevice));
   SRL_CUDA(cudaMemcpy(runner_->plan.last_row, neg.data(), 4 * (size_t)S_, cudaMemcpyHostToDevice));
+  return mega_init();
+}
+
+// Phase table, device tensor maps and counters of the persistent decode
+// kernel.  Off with SRL_MEGAKERNEL=0 (the multi-kernel CUDA-graph round).
+int DecoderBackend::mega_init() {
+  const char* env = std::getenv("SRL_MEGAKERNEL");
+  if ((env && env[0] == '0') || !megakernel_supported(d_, S_)) return SRL_OK;
+  DecoderRunner& r = *runner_;
+  const int grid = r.sms;
+  if (megakernel_occupancy(d_) < 1) return SRL_OK;  // not co-resident: multi-kernel round
+  const int L = d_.L, splits = (max_seq_ + 127) / 128;  // attention_splits(): 128-key splits
+  std::vector<MkPhase> ph;
+  int ctr = 0, items_total = 0;
+  size_t ws = (size_t)S_ * d_.nkv * splits * (d_.nq / d_.nkv) * (d_.hd + 2);
+  auto add = [&](int kind, int layer, int n_items, int cs, int N, int K, int wmap, int xmap,
+                 int counters) {
+    MkPhase f{kind, layer, n_items, cs, N, K, wmap, xmap, ctr, items_total % grid};
+    ctr += counters;
+    items_total += n_items;
+    ph.push_back(f);
+  };
+  auto gemm = [&](int kind, int layer, int N, int K, int wmap, int xmap) {
+    const int cs = megakernel_splits(N, K, grid);
+    const int tiles = (N + 127) / 128;
+    ws = std::max(ws, megakernel_ws_floats(tiles * cs, cs, S_));
+    add(kind, layer, tiles * cs, cs, N, K, wmap, xmap, cs > 1 ? tiles : 0);
+  };
+  add(MK_EMBED, 0, S_, 1, 0, 0, 0, 0, 0);
+  for (int l = 0; l < L; ++l) {
+    gemm(MK_QKV, l, d_.qkv(), d_.H, 4 * l + 0, 0);
+    add(MK_ATTN, l, S_ * d_.nkv * splits, 1, 0, 0, 0, 0, S_ * d_.nkv);
+    gemm(MK_O, l, d_.H, d_.qdim(), 4 * l + 1, 1);
+    gemm(MK_GU, l, 2 * d_.I, d_.H, 4 * l + 2, 0);
+    gemm(MK_DOWN, l, d_.H, d_.I, 4 * l + 3, 2);
+  }
+  gemm(MK_LM, 0, d_.V, d_.H, 4 * L, 0);
+  add(MK_SAMPLE, 0, S_, 1, 0, 0, 0, 0, 0);
+  const int n = (int)ph.size();
+
+  // one allocation: phases | layers | xmaps | phase_done | epoch | tile counters | stamps
+  auto al = [](size_t v) { return (v + 127) / 128 * 128; };
+  const size_t o_ph = 0, o_ly = al(o_ph + sizeof(MkPhase) * n), o_xm = al(o_ly + sizeof(MkLayer) * L),
+               o_pd = al(o_xm + sizeof(CUtensorMap) * 3), o_ep = al(o_pd + 4 * (size_t)n),
+               o_tc = al(o_ep + 4), o_st = al(o_tc + 4 * (size_t)std::max(ctr, 1)),
+               total = al(o_st + 8 * (size_t)(n + 1));
+  SRL_CUDA(cudaMalloc(&mk_.mem, total));
+  SRL_CUDA(cudaMemset(mk_.mem, 0, total));
+  SRL_CUDA(cudaMalloc(&mk_.ws, std::max<size_t>(ws, 1) * sizeof(float)));
+  SRL_CUDA(cudaMallocHost(&mk_.stamps_host, 8 * (size_t)(n + 1)));
+  uint8_t* base = static_cast<uint8_t*>(mk_.mem);
+  std::vector<MkLayer> ly(L);
+  for (int l = 0; l < L; ++l) {
+    const LayerOffsets& o = buf_[0]->layout.layers[l];
+    ly[l] = MkLayer{o.ln1, o.qkv_b, o.ln2};
+  }
+  const CUtensorMap xm[3] = {r.xg_map[0], r.attn_map[0], r.act_map[0]};
+  SRL_CUDA(cudaMemcpy(base + o_ph, ph.data(), sizeof(MkPhase) * n, cudaMemcpyHostToDevice));
+  SRL_CUDA(cudaMemcpy(base + o_ly, ly.data(), sizeof(MkLayer) * L, cudaMemcpyHostToDevice));
+  SRL_CUDA(cudaMemcpy(base + o_xm, xm, sizeof(xm), cudaMemcpyHostToDevice));
+  for (int b = 0; b < 2; ++b) {
+    std::vector<CUtensorMap> wm(4 * L + 1);
+    for (int l = 0; l < L; ++l) {
+      wm[4 * l + 0] = maps_[b].qkv[l];
+      wm[4 * l + 1] = maps_[b].o[l];
+      wm[4 * l + 2] = maps_[b].gate_up[l];
+      wm[4 * l + 3] = maps_[b].down[l];
+    }
+    wm[4 * L] = maps_[b].lm_head;
+    SRL_CUDA(cudaMalloc(&mk_.wmaps[b], sizeof(CUtensorMap) * wm.size()));
+    SRL_CUDA(cudaMemcpy(mk_.wmaps[b], wm.data(), sizeof(CUtensorMap) * wm.size(), cudaMemcpyHostToDevice));
+    MkParams& P = mk_.params[b];
+    P = MkParams{};
+    P.S = S_; P.H = d_.H; P.I = d_.I; P.V = d_.V; P.L = L; P.nq = d_.nq; P.nkv = d_.nkv;
+    P.hd = d_.hd; P.qkv = d_.qkv(); P.parts = d_.ssq_parts(); P.pps = r.pages_per_seq;
+    P.attn_splits = splits; P.greedy = opts_.greedy;
+    P.eps = d_.eps; P.inv_h = 1.0f / (float)d_.H; P.scale = 1.0f / sqrtf((float)d_.hd);
+    P.w = buf_[b]->w;
+    P.wmaps = mk_.wmaps[b];
+    P.xmaps = reinterpret_cast<const CUtensorMap*>(base + o_xm);
+    P.layers = reinterpret_cast<const MkLayer*>(base + o_ly);
+    P.off_embed = buf_[b]->layout.embed;
+    P.off_final_norm = buf_[b]->layout.final_norm;
+    P.x = r.x; P.xg = r.xg; P.ssq = r.ssq; P.q = r.q; P.attn = r.attn; P.act = r.act;
+    P.logits = r.logits; P.lse_max = r.lse_max; P.lse_sum = r.lse_sum;
+    P.kc = r.kc; P.vc = r.vc; P.kv_layer_elems = r.kv_layer_elems;
+    P.block_table = r.block_table; P.cos_sin = r.cos_sin;
+    P.plan = r.plan; P.next = r.next; P.ss = ss_; P.ring = ring_;
+    P.round_ctr = round_ctr_dev_; P.version = version_dev_;
+    P.phase_done = reinterpret_cast<unsigned*>(base + o_pd);
+    P.epoch = reinterpret_cast<unsigned*>(base + o_ep);
+    P.tile_ctr = reinterpret_cast<unsigned*>(base + o_tc);
+    P.ws = mk_.ws;
+    P.phases = reinterpret_cast<const MkPhase*>(base + o_ph);
+    P.n_phases = n;
+    P.stamps = nullptr;
+  }
+  mk_.stamps = reinterpret_cast<unsigned long long*>(base + o_st);
+  mk_.phases = ph;
+  mk_.n_phases = n;
+  mk_.grid = grid;
+  mk_.on = true;
+  return SRL_OK;
+}
+
+int DecoderBackend::mega_round(int b, bool profile) {
+  MkParams p = mk_.params[b];
+  if (profile) p.stamps = mk_.stamps;
+  const cudaError_t e = launch_megakernel(p, d_, mk_.grid, st_);
+  if (e != cudaSuccess) return cuda_fail(e, "launch_megakernel");
+  if (profile) {
+    SRL_CUDA(cudaMemcpyAsync(mk_.stamps_host, mk_.stamps, 8 * (size_t)(mk_.n_phases + 1),
+                             cudaMemcpyDeviceToHost, st_));
+    SRL_CUDA(cudaStreamSynchronize(st_));
+    // phase durations (grid-wide completion as seen by CTA 0) -> kernel classes
+    static const int cls[8] = {1, 2, 4, 5, 6, 7, 8, 9};
+    profile_ = srl_kernel_profile{};
+    for (int i = 0; i < mk_.n_phases; ++i) {
+      const int c = cls[mk_.phases[i].kind];
+      profile_.ms[c] += (double)(mk_.stamps_host[i + 1] - mk_.stamps_host[i]) * 1e-6;
+      profile_.launches[c] += 1;
+    }
+    profile_.valid = 1;
+    profile_.rows = S_;
+  }
   return SRL_OK;
 }
 
@@ -436,6 +567,10 @@ int DecoderBackend::run_rounds(int n, std::vector<SlotEvent>& events, double* de
         for (const HostSlot& h : host_)
           if (h.live && h.pending) any_pending_ = true;
         launches_ += 6 * d_.L + 5;
+      } else if (mk_.on) {
+        if ((st = mega_round(active_, profile_next_))) return st;
+        profile_next_ = false;
+        launches_ += 1;
       } else if (profile_next_) {
         timer_.st = st_;
         timer_.reset();

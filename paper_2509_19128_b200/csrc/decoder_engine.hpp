@@ -4,6 +4,7 @@
 #include <memory>
 #include <vector>
 
+#include "decode_mk.cuh"
 #include "gemm.cuh"
 #include "runtime.hpp"
 
@@ -102,6 +103,9 @@ class DecoderBackend final : public Backend {
   };
   int decode_round_eager(int b);
   int capture(int b);
+  // persistent megakernel decode rounds (decode_mk.cu)
+  int mega_init();
+  int mega_round(int b, bool profile);
   int prefill_round(int b, std::vector<int>& prefilled);
   int swap_and_recompute(bool recompute, int version);
   int recompute_kv();
@@ -129,6 +133,17 @@ class DecoderBackend final : public Backend {
   bool profile_next_ = false;
   srl_kernel_profile profile_{};
   KernelTimer timer_;
+  struct Mega {
+    bool on = false;
+    int grid = 0, n_phases = 0;
+    std::vector<MkPhase> phases;         // host copy (profile class mapping)
+    MkParams params[2]{};                // per weight buffer
+    CUtensorMap* wmaps[2] = {nullptr, nullptr};
+    void* mem = nullptr;                 // phases, layers, xmaps, counters, stamps
+    float* ws = nullptr;
+    unsigned long long* stamps = nullptr;
+    unsigned long long* stamps_host = nullptr;
+  } mk_;
 };
 
 }  // namespace srl

@@ -86,7 +86,7 @@ __device__ __forceinline__ float warp_max(float v) {
 template <int TOK, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
-                     int M, int N, int K, int cs, const EpiParams epi) {
+                     int M, int N, int K, int cs, float* __restrict__ ws, const EpiParams epi) {
   using L = Layout<TOK, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -179,57 +179,68 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   }
 
-  // ---- drain TMEM into the shared tile: thread = weight row (TMEM lane)
+  // ---- drain TMEM: thread = weight row (TMEM lane), columns = tokens.
+  // cs == 1: into the shared tile.  cs > 1: into this split's fp32 partial in
+  // global memory (coalesced across rows), exchanged through L2 -- the DSMEM
+  // port (~20 B/clk/SM) is slower than L2 for whole-tile partials.
   mbar_wait(done, 0);
   tc_fence_after();
-  SRL_STAMP(2);
   const int row = threadIdx.x;
   const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+  const size_t tile_id = (size_t)tok_tile * n_tiles + n_tile;
+  const size_t tiles_total = (size_t)n_tiles * gridDim.z;
+  float* part = cs > 1 ? ws + ((size_t)split * tiles_total + tile_id) * (TOK * kBlockN) : nullptr;
 #pragma unroll
   for (int c0 = 0; c0 < TOK; c0 += 64) {  // two 32-column loads in flight, one wait
     uint32_t ra[32], rb[32];
     tmem_ld_32x32b_x32(lane_addr + c0, ra);
     tmem_ld_32x32b_x32(lane_addr + c0 + 32, rb);
     tmem_ld_wait();
+    if (cs == 1) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) tile[(c0 + j) * L::kPitch + row] = __uint_as_float(ra[j]);
+      for (int j = 0; j < 32; ++j) tile[(c0 + j) * L::kPitch + row] = __uint_as_float(ra[j]);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) tile[(c0 + 32 + j) * L::kPitch + row] = __uint_as_float(rb[j]);
+      for (int j = 0; j < 32; ++j) tile[(c0 + 32 + j) * L::kPitch + row] = __uint_as_float(rb[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) __stcg(&part[(c0 + j) * kBlockN + row], __uint_as_float(ra[j]));
+#pragma unroll
+      for (int j = 0; j < 32; ++j) __stcg(&part[(c0 + 32 + j) * kBlockN + row], __uint_as_float(rb[j]));
+    }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_free<TOK>(tmem);
   SRL_STAMP(3);
 
-  // ---- split-K: reduce this CTA's row slice over the cluster through DSMEM
+  // ---- split-K: after one cluster barrier (release/acquire orders the
+  // global partials), CTA r sums rows [r*TOK/cs, (r+1)*TOK/cs) of all
+  // partials in rank order -- deterministic -- into its shared tile.
   int r0 = 0, r1 = TOK;
   if (cs > 1) {
     r0 = (split * TOK) / cs;
     r1 = ((split + 1) * TOK) / cs;
-    cluster_sync();  // every partial tile is staged
+    cluster_sync();
+    SRL_STAMP(7);
     const int n4 = (r1 - r0) * (kBlockN / 4);
     constexpr int kMaxPer = (TOK / 2) * (kBlockN / 4) / kThreads + 1;  // cs >= 2
     float4 acc[kMaxPer];
 #pragma unroll
     for (int k = 0; k < kMaxPer; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    // fetch every rank's slice first (all remote loads in flight), then sum in
-    // rank order: deterministic
+    const float4* base = reinterpret_cast<const float4*>(ws + tile_id * (TOK * kBlockN)) +
+                         (size_t)r0 * (kBlockN / 4);
+    const size_t split_stride4 = tiles_total * (TOK * kBlockN) / 4;
     for (int q0 = 0; q0 < cs; q0 += 4) {
       float4 v[4][kMaxPer];
 #pragma unroll
-      for (int dq = 0; dq < 4; ++dq) {
+      for (int dq = 0; dq < 4; ++dq)
 #pragma unroll
         for (int k = 0; k < kMaxPer; ++k) {
           const int i = threadIdx.x + k * kThreads;
-          const int q = q0 + dq;
-          if (q < cs && i < n4) {
-            const int j = r0 + i / (kBlockN / 4), c = (i % (kBlockN / 4)) * 4;
-            v[dq][k] = dsmem_ld_f4(dsmem_map(smem_u32(&tile[j * L::kPitch + c]), q));
-          }
+          if (q0 + dq < cs && i < n4) v[dq][k] = __ldcg(base + (size_t)(q0 + dq) * split_stride4 + i);
         }
-      }
 #pragma unroll
-      for (int dq = 0; dq < 4; ++dq) {
+      for (int dq = 0; dq < 4; ++dq)
 #pragma unroll
         for (int k = 0; k < kMaxPer; ++k) {
           const int i = threadIdx.x + k * kThreads;
@@ -238,9 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc[k].z += v[dq][k].z; acc[k].w += v[dq][k].w;
           }
         }
-      }
     }
-    cluster_sync();  // all remote reads done before anyone overwrites / exits
 #pragma unroll
     for (int k = 0; k < kMaxPer; ++k) {
       const int i = threadIdx.x + k * kThreads;
@@ -249,6 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         *reinterpret_cast<float4*>(&tile[j * L::kPitch + c]) = acc[k];
       }
     }
+    __syncthreads();
   }
 
   // ---- epilogue over rows [r0, r1)
@@ -281,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   SRL_STAMP(5);
   const int rows = r1 - r0;
   if (epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16) {
+#pragma unroll 4
     for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
       const int j = r0 + (idx >> 7), c = idx & 127;
       const int m = t0 + j, n = n0 + c;
@@ -300,6 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       epi.out_f32[(size_t)m * epi.ld_out + n] += epi.scale * tile[j * L::kPitch + c];
     }
   } else if (epi.kind == EPI_SWIGLU) {
+#pragma unroll 4
     for (int idx = threadIdx.x; idx < rows * (kBlockN / 2); idx += kThreads) {
       const int j = r0 + (idx >> 6), c = idx & 63;
       const int m = t0 + j;
@@ -377,6 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (epi.kind == EPI_RESID) {
+#pragma unroll 4
     for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
       const int j = r0 + (idx >> 7), c = idx & 127;
       const int m = t0 + j, n = n0 + c;
@@ -406,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int TOK, int STAGES>
 cudaError_t launch_impl(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int cs,
-                        const EpiParams& epi, cudaStream_t stream) {
+                        const GemmWorkspace& ws, const EpiParams& epi, cudaStream_t stream) {
   using L = Layout<TOK, STAGES>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -417,8 +430,12 @@ cudaError_t launch_impl(const CUtensorMap& tw, const CUtensorMap& tx, int M, int
   if (attr_err != cudaSuccess) return attr_err;
   const int n_tiles = (N + kBlockN - 1) / kBlockN;
   const int tok_tiles = (M + TOK - 1) / TOK;
+  if (cs > 1) {
+    const size_t need = (size_t)cs * n_tiles * tok_tiles * TOK * kBlockN;
+    if (ws.partials == nullptr || need > ws.partial_floats) return cudaErrorInvalidValue;
+  }
   return launch_pdl(gemm_bf16_kernel<TOK, STAGES>, dim3(n_tiles, cs, tok_tiles), dim3(kThreads),
-                    (size_t)L::kAlloc, stream, dim3(1, cs, 1), tw, tx, M, N, K, cs, epi);
+                    (size_t)L::kAlloc, stream, dim3(1, cs, 1), tw, tx, M, N, K, cs, ws.partials, epi);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -478,18 +495,24 @@ int gemm_auto_splits(int M, int N, int K, int num_sms) {
   return cs;
 }
 
-size_t gemm_workspace_floats(int, int, int) { return 0; }  // partials live in DSMEM
+size_t gemm_workspace_floats(int M, int N, int splits) {
+  const int tok = gemm_tok_tile(M);
+  int cs = 1;
+  while (cs * 2 <= splits && cs * 2 <= kMaxCluster) cs *= 2;
+  if (cs == 1) return 0;
+  return (size_t)cs * ((N + kBlockN - 1) / kBlockN) * ((M + tok - 1) / tok) * tok * kBlockN;
+}
 
 cudaError_t gemm_bf16_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K,
-                             int splits, const GemmWorkspace&, const EpiParams& epi,
+                             int splits, const GemmWorkspace& ws, const EpiParams& epi,
                              cudaStream_t stream) {
   if (M < 1 || N < 1 || K < kBlockK || K % kBlockK != 0 || splits < 1)
     return cudaErrorInvalidValue;
   if (epi.kind == EPI_SWIGLU && N % kBlockN != 0) return cudaErrorInvalidValue;
   int cs = 1;
   while (cs * 2 <= splits && cs * 2 <= kMaxCluster && cs * 2 <= K / kBlockK) cs *= 2;
-  if (gemm_tok_tile(M) == 64) return launch_impl<64, 4>(tw, tx, M, N, K, cs, epi, stream);
-  return launch_impl<128, 4>(tw, tx, M, N, K, cs, epi, stream);
+  if (gemm_tok_tile(M) == 64) return launch_impl<64, 4>(tw, tx, M, N, K, cs, ws, epi, stream);
+  return launch_impl<128, 4>(tw, tx, M, N, K, cs, ws, epi, stream);
 }
 
 }  // namespace srl

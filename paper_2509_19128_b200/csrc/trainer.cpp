@@ -79,6 +79,9 @@ int pad64(int x) { return (x + 63) / 64 * 64; }
 DecoderTrainer::~DecoderTrainer() {
   if (st_) cudaStreamSynchronize(st_);
   for (void* p : allocs_) cudaFree(p);
+  if (ws_) cudaFree(ws_);
+  if (kc_) cudaFree(kc_);
+  if (vc_) cudaFree(vc_);
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -151,8 +154,17 @@ int DecoderTrainer::gemm(const __nv_bfloat16* X, int x_rows_alloc, int M, const 
   const int tok = gemm_tok_tile(M);
   const CUtensorMap tx = make_tmap_bf16(X, (uint64_t)std::max(x_rows_alloc, M), (uint64_t)K, (uint32_t)tok);
   const CUtensorMap tw = make_tmap_bf16(W, (uint64_t)N, (uint64_t)K, 128);
+  const int splits = gemm_auto_splits(M, N, K, sms_);
+  const size_t need = gemm_workspace_floats(M, N, splits);
+  if (need > ws_floats_) {
+    if (ws_) cudaFree(ws_);
+    SRL_CUDA(cudaMalloc(&ws_, need * sizeof(float)));
+    ws_floats_ = need;
+  }
   GemmWorkspace ws;
-  const cudaError_t err = gemm_bf16_launch(tw, tx, M, N, K, gemm_auto_splits(M, N, K, sms_), ws, e, st_);
+  ws.partials = ws_;
+  ws.partial_floats = ws_floats_;
+  const cudaError_t err = gemm_bf16_launch(tw, tx, M, N, K, splits, ws, e, st_);
   if (err != cudaSuccess) return cuda_fail(err, "trainer gemm");
   return SRL_OK;
 }

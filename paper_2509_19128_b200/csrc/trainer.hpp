@@ -67,6 +67,8 @@ class DecoderTrainer {
   int32_t *row_slot_ = nullptr, *row_pos_ = nullptr, *row_tok_ = nullptr, *row_tgt_ = nullptr;
   __nv_bfloat16 *kc_ = nullptr, *vc_ = nullptr;
   size_t kv_cap_ = 0;
+  float* ws_ = nullptr;  // split-K partials
+  size_t ws_floats_ = 0;
   std::vector<double> lp_host_;
 };
 
