@@ -1,8 +1,15 @@
 // decode_mk.cu -- persistent decode-round megakernel (see decode_mk.cuh).
+//
+// One CTA per SM, 12 warps: warp 0 TMA producer, warp 1 tcgen05.mma issuer,
+// warps 4-11 compute (256 threads, named barrier 1).  Warps 2-3 only hold the
+// TMEM quadrant mapping in place (a warp may only tcgen05.ld the 32 TMEM lanes
+// of quadrant warp_id % 4: compute warps w and w + 4 share a quadrant and
+// drain the two 32-token halves of the 64-column accumulator).
 #include <cmath>
 #include <cstdio>
 
 #include "decode_mk.cuh"
+#include "fastexp.cuh"
 #include "sm100.cuh"
 
 namespace srl {
@@ -13,8 +20,9 @@ namespace {
 constexpr int kTok = 64;   // rows (UMMA N): decode batch <= 64
 constexpr int kBN = 128;   // weight rows per tile (UMMA M)
 constexpr int kBK = 64;    // k-block (128-B swizzle row)
-constexpr int kThreads = 256;
-constexpr int kCT = 128;   // compute threads (warps 4..7)
+constexpr int kThreads = 384;
+constexpr int kCW = 8;     // compute warps (4..11)
+constexpr int kCT = 32 * kCW;
 constexpr int kABytes = kBN * kBK * 2;
 constexpr int kBBytes = kTok * kBK * 2;
 constexpr int kStageBytes = kABytes + kBBytes;
@@ -22,28 +30,45 @@ constexpr int kPitch = kBN + 4;
 constexpr int kTileFloats = kTok * kBN;
 constexpr int kLmTile = 128;
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+constexpr int kMaxSplitPages = 32;  // attention split <= 2048 keys
+constexpr int kMaxCs = 16;          // split-K factor cap (reduce staging)
 
-__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// Bounded spins: a broken schedule traps (the launch fails loudly) instead of
-// hanging the device.
-constexpr long long kSpinLimit = 1ll << 26;
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Bounded spins: a broken schedule traps after ~4 s (the launch fails loudly)
+// instead of hanging the device.
+struct SpinGuard {
+  unsigned n = 0;
+  unsigned long long t0 = 0;
+  __device__ __forceinline__ void tick() {
+    if ((++n & 255u) == 0) {
+      const unsigned long long t = globaltimer();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 4000000000ull) __trap();
+    }
+  }
+};
 __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
-  long long n = 0;
+  SpinGuard g;
   while ((int)(ld_acquire(p) - target) < 0) {
     __nanosleep(32);
-    if (++n > kSpinLimit) __trap();
+    g.tick();
   }
 }
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, 1000000;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, 20000;\n\t"
       "selp.u32 %0, 1, 0, P1;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
@@ -51,18 +76,26 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void mk_wait(uint64_t* bar, uint32_t parity) {
-  long long n = 0;
-  while (!mbar_try(bar, parity))
-    if (++n > kSpinLimit) __trap();
+  SpinGuard g;
+  while (!mbar_try(bar, parity)) g.tick();
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
+// Bulk (non-tensor) async copy global -> shared, completion on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
 __device__ __forceinline__ float wsum(float v) {
 #pragma unroll
@@ -87,134 +120,142 @@ __device__ __forceinline__ double uniform_draw(uint64_t seed, uint64_t n) {
   return (double)(z >> 11) * 0x1.0p-53;
 }
 
-// item index k of CTA c in a phase with `n` items and rotation `rot`
+// first item of CTA c in a phase whose items are dealt round-robin from `rot`
 __device__ __forceinline__ int first_item(int c, int rot, int G) { return ((c - rot) % G + G) % G; }
 
+// Attention item scratch: q, per-warp K/V tiles (cp.async), probabilities,
+// per-warp softmax state, the row's reduced q|k|v; the QKV split partials are
+// staged in the tile area first and the warp accumulators alias it last.
 template <int HD, int G>
 struct AttnSmem {
-  static constexpr int ROW = HD * 2 + 16;
+  static constexpr int KT = HD == 64 ? 32 : 16;  // keys per tile
+  static constexpr int ROW = HD * 2 + 16;        // padded K row (conflict-free LDS.128)
   static constexpr int VROW = HD * 2;
   static constexpr size_t sq = sizeof(float) * G * HD;
-  static constexpr size_t sk = (size_t)4 * 32 * ROW;
-  static constexpr size_t sv = (size_t)4 * 32 * VROW;
-  static constexpr size_t sp = sizeof(float) * 4 * G * 32;
-  static constexpr size_t sml = sizeof(float) * 2 * 4 * G;
-  static constexpr size_t total = sq + sk + sv + sp + sml;
+  static constexpr size_t kbuf = (size_t)KT * ROW, vbuf = (size_t)KT * VROW;
+  static constexpr size_t warp_bytes = kbuf + vbuf;
+  static constexpr size_t tiles = kCW * warp_bytes;
+  static constexpr size_t sp = sizeof(float) * kCW * G * 32;
+  static constexpr size_t sml = sizeof(float) * 2 * kCW * G;
+  static constexpr size_t spage = sizeof(int) * kMaxSplitPages;
+  static constexpr size_t sraw = sizeof(float) * (G + 2) * HD;  // reduced q | k | v of the row
+  static constexpr size_t snew = sizeof(__nv_bfloat16) * 2 * HD;  // the new token's k, v
+  static constexpr size_t total = sq + tiles + sp + sml + spage + sraw + snew;
+  static_assert(sizeof(float) * kCW * G * HD <= tiles, "accumulators alias the tiles");
 };
 
 template <int HD, int G>
 struct MkLayout {
-  static constexpr int STAGES = HD == 64 ? 7 : 5;
+  static constexpr int STAGES = HD == 64 ? 6 : 5;
   static constexpr size_t ring = (size_t)STAGES * kStageBytes;
   static constexpr size_t epi = sizeof(float) * kTok * kPitch;
+  static constexpr size_t stage_red = (size_t)(kTok + kMaxCs) * kBN * 4;  // split-K row slices
   static constexpr size_t att = AttnSmem<HD, G>::total;
-  static constexpr size_t smp = sizeof(double) * (kCT + 33) + 256;
-  static constexpr size_t scratch = epi > att ? (epi > smp ? epi : smp) : (att > smp ? att : smp);
+  static constexpr size_t smp = sizeof(double) * (kCT + 40) + 256;
+  static constexpr size_t gemm_scr = epi + stage_red;
+  static constexpr size_t scratch =
+      gemm_scr > att ? (gemm_scr > smp ? gemm_scr : smp) : (att > smp ? att : smp);
   static constexpr size_t bar = ring + scratch;
-  static constexpr size_t misc = bar + (2 * STAGES + 4) * 8;
+  static constexpr size_t misc = bar + (2 * STAGES + 5) * 8;
   static constexpr size_t rstd = misc + 32;
-  static constexpr size_t rowm = rstd + kTok * 4;
-  static constexpr size_t total = rowm + kTok * 16;
+  static constexpr size_t rows = rstd + kTok * 4;  // round-constant (slot, pos) of every row
+  static constexpr size_t total = rows + kTok * 8;
   static constexpr size_t alloc = total + 1024;
+  static_assert(alloc <= 232448, "shared memory budget");
 };
 
 // ----------------------------------------------------------- compute ---
-// Per-row metadata for the current GEMM phase: rstd (deferred RMSNorm) and,
-// for QKV, the KV-cache coordinates of the row.
-__device__ void mk_rows(const MkParams& P, int kind, float* s_rstd, int4* s_row, int ct) {
+// Deferred RMSNorm: rstd of every row for the GEMMs that consume xg.
+__device__ void mk_rows(const MkParams& P, int kind, float* s_rstd, int ct) {
   for (int j = ct; j < kTok; j += kCT) {
     float r = 1.f;
-    if ((kind == MK_QKV || kind == MK_GU || kind == MK_LM) && j < P.S) {
+    if ((kind == MK_GU || kind == MK_LM) && j < P.S) {
       float s = 0.f;
       for (int p = 0; p < P.parts; ++p) s += P.ssq[(size_t)j * P.parts + p];
       r = rsqrtf(s * P.inv_h + P.eps);
     }
     s_rstd[j] = r;
-    if (kind == MK_QKV) {
-      int4 rc = make_int4(-1, 0, 0, 0);
-      if (j < P.S) {
-        rc.x = P.plan.row_slot[j];
-        rc.y = P.plan.row_pos[j];
-        if (rc.x >= 0) {
-          rc.z = P.block_table[(size_t)rc.x * P.pps + rc.y / kPageTokens];
-          rc.w = rc.y % kPageTokens;
-        }
-      }
-      s_row[j] = rc;
+  }
+}
+
+// LM-head tile statistics: max and fp64 sum of exp(x - max) per row over the
+// tile's 128 columns (the sampler's per-tile partition sums).  Four threads
+// per row, 32 independent exponentials each; the four partial sums combine
+// by a symmetric butterfly, so every lane holds the same, order-fixed value.
+__device__ __noinline__ void mk_lm_stats(const MkParams& P, const float* tile, int n_tile, int N,
+                                         int ct, int r0, int r1) {
+  const int T = (N + kLmTile - 1) / kLmTile;
+  const int j = r0 + (ct >> 2), part = ct & 3;
+  const bool valid = j < r1;  // converged shuffles: invalid quads recompute row r0
+  const float* row = &tile[(valid ? j : r0) * kPitch + part * 32];
+  float4 v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = *reinterpret_cast<const float4*>(row + 4 * q);
+  float mx = -INFINITY;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) mx = fmaxf(mx, fmaxf(fmaxf(v[q].x, v[q].y), fmaxf(v[q].z, v[q].w)));
+  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  if (mx != -INFINITY) {
+    const double md = (double)mx;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      a[0] += exp_nonpos((double)v[q].x - md);
+      a[1] += exp_nonpos((double)v[q].y - md);
+      a[2] += exp_nonpos((double)v[q].z - md);
+      a[3] += exp_nonpos((double)v[q].w - md);
     }
+  }
+  double sm = (a[0] + a[1]) + (a[2] + a[3]);
+  sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+  sm += __shfl_xor_sync(0xffffffffu, sm, 2);
+  if (part == 0 && valid) {
+    P.lse_max[(size_t)j * T + n_tile] = mx;
+    P.lse_sum[(size_t)j * T + n_tile] = sm;
   }
 }
 
 // Fused epilogues on the reduced [64 x 128] tile (rows = tokens, cols = n0..).
 // Rows [r0, r1) of the tile belong to this CTA (split-K row slices).
+// colv: this thread's column constant (next RMSNorm gain), loaded before the
+// accumulator wait.  QKV has no epilogue here: its split partials are
+// reduced by the attention items that consume them.
 __device__ void mk_epilogue(const MkParams& P, const MkPhase& ph, int n_tile, float* tile,
-                            const float* s_rstd, const int4* s_row, int ct, int r0, int r1) {
+                            const float* s_rstd, int ct, int r0, int r1, float colv) {
   const int n0 = n_tile * kBN, N = ph.N, M = r1;
   const int nr = r1 - r0;
   const int cw = ct >> 5, lane = ct & 31;
-  const __nv_bfloat16* w = P.w;
-  if (ph.kind == MK_QKV) {
-    const __nv_bfloat16* bias = w + P.layers[ph.layer].qkv_b;
-#pragma unroll 4
-    for (int idx = ct; idx < nr * kBN; idx += kCT) {
-      const int j = r0 + (idx >> 7), c = idx & 127, n = n0 + c;
-      float v = 0.f;
-      if (n < N) v = tile[j * kPitch + c] * s_rstd[j] + bf2f(bias[n]);
-      tile[j * kPitch + c] = v;
+  if (ph.kind == MK_O || ph.kind == MK_DOWN) {
+    // residual add; column c = ct & 127, the two thread halves take
+    // alternating rows, 8 residual loads in flight per chunk
+    const int c = ct & (kBN - 1), hf = ct >> 7, n = n0 + c;
+    for (int j0 = r0 + hf; j0 < r1; j0 += 16) {
+      float xr[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + 2 * u;
+        xr[u] = (j < r1 && n < N) ? P.x[(size_t)j * N + n] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + 2 * u;
+        if (j >= r1) break;
+        float x = 0.f;
+        if (n < N) {
+          const size_t o = (size_t)j * N + n;
+          x = xr[u] + tile[j * kPitch + c];
+          P.x[o] = x;
+          P.xg[o] = __float2bfloat16(x * colv);
+        }
+        tile[j * kPitch + c] = x;
+      }
     }
     csync();
-    const int hd = P.hd, half = hd >> 1;
-    const int qend = P.nq * hd, kend = (P.nq + P.nkv) * hd;
-    __nv_bfloat16* kc = P.kc + P.kv_layer_elems * ph.layer;
-    __nv_bfloat16* vc = P.vc + P.kv_layer_elems * ph.layer;
-#pragma unroll 4
-    for (int idx = ct; idx < nr * kBN; idx += kCT) {
-      const int j = r0 + (idx >> 7), c = idx & 127, n = n0 + c;
-      const int4 rc = s_row[j];
-      if (n >= N || rc.x < 0) continue;
-      const int jj = n % hd;
-      const float* row = &tile[j * kPitch + (c - jj)];
-      float y;
-      if (n < kend) {
-        const int i = jj < half ? jj : jj - half;
-        const float co = P.cos_sin[(size_t)rc.y * hd + i];
-        const float si = P.cos_sin[(size_t)rc.y * hd + half + i];
-        const float x1 = row[i], x2 = row[i + half];
-        y = jj < half ? x1 * co - x2 * si : x2 * co + x1 * si;
-      } else {
-        y = row[jj];
-      }
-      const __nv_bfloat16 b = __float2bfloat16(y);
-      if (n < qend) {
-        P.q[(size_t)j * qend + n] = b;
-      } else {
-        const int kv = n < kend ? n - qend : n - kend;
-        const size_t at = (((size_t)rc.z * P.nkv + kv / hd) * kPageTokens + rc.w) * hd + (kv % hd);
-        if (n < kend) kc[at] = b;
-        else vc[at] = b;
-      }
-    }
-  } else if (ph.kind == MK_O || ph.kind == MK_DOWN) {
-    const __nv_bfloat16* gain =
-        w + (ph.kind == MK_O ? P.layers[ph.layer].ln2
-                             : (ph.layer + 1 < P.L ? P.layers[ph.layer + 1].ln1 : P.off_final_norm));
-#pragma unroll 4
-    for (int idx = ct; idx < nr * kBN; idx += kCT) {
-      const int j = r0 + (idx >> 7), c = idx & 127, n = n0 + c;
-      float x = 0.f;
-      if (n < N) {
-        const size_t o = (size_t)j * N + n;
-        x = P.x[o] + tile[j * kPitch + c];
-        P.x[o] = x;
-        P.xg[o] = __float2bfloat16(x * bf2f(gain[n]));
-      }
-      tile[j * kPitch + c] = x;
-    }
-    csync();
-    for (int j = r0 + cw; j < M; j += kCT / 32) {
+    for (int j = r0 + cw; j < M; j += kCW) {
       float s = 0.f;
-      for (int c = lane; c < kBN; c += 32) {
-        const float xv = tile[j * kPitch + c];
+      for (int c2 = lane; c2 < kBN; c2 += 32) {
+        const float xv = tile[j * kPitch + c2];
         s += xv * xv;
       }
       s = wsum(s);
@@ -229,64 +270,167 @@ __device__ void mk_epilogue(const MkParams& P, const MkPhase& ph, int n_tile, fl
       P.act[(size_t)j * P.I + (n0 >> 1) + c] = __float2bfloat16(g / (1.f + expf(-g)) * u);
     }
   } else if (ph.kind == MK_LM) {
-#pragma unroll 4
-    for (int idx = ct; idx < nr * kBN; idx += kCT) {
-      const int j = r0 + (idx >> 7), c = idx & 127, n = n0 + c;
-      float v = -INFINITY;
-      if (n < N) {
-        v = tile[j * kPitch + c] * s_rstd[j];
-        P.logits[(size_t)j * N + n] = v;
+    // scale by rstd and store the logits (one float4 per thread per row), keep
+    // the scaled tile for the statistics
+    const int c4 = lane * 4, n = n0 + c4;
+    for (int j = r0 + cw; j < r1; j += kCW) {
+      float4 v = *reinterpret_cast<const float4*>(&tile[j * kPitch + c4]);
+      const float r = s_rstd[j];
+      v.x = n + 0 < N ? v.x * r : -INFINITY;
+      v.y = n + 1 < N ? v.y * r : -INFINITY;
+      v.z = n + 2 < N ? v.z * r : -INFINITY;
+      v.w = n + 3 < N ? v.w * r : -INFINITY;
+      float* dst = P.logits + (size_t)j * N + n;
+      if (n + 3 < N && (N & 3) == 0) {
+        *reinterpret_cast<float4*>(dst) = v;
+      } else {
+        if (n + 0 < N) dst[0] = v.x;
+        if (n + 1 < N) dst[1] = v.y;
+        if (n + 2 < N) dst[2] = v.z;
+        if (n + 3 < N) dst[3] = v.w;
       }
-      tile[j * kPitch + c] = v;
+      *reinterpret_cast<float4*>(&tile[j * kPitch + c4]) = v;
     }
     csync();
-    const int T = (N + kLmTile - 1) / kLmTile;
-    for (int j = r0 + cw; j < M; j += kCT / 32) {
-      const float4 x = *reinterpret_cast<const float4*>(&tile[j * kPitch + lane * 4]);
-      const float mx = wmax(fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
-      double s = 0.0;
-      if (mx != -INFINITY) {
-        const double md = (double)mx;
-        s = exp((double)x.x - md) + exp((double)x.y - md) + exp((double)x.z - md) +
-            exp((double)x.w - md);
-      }
-      s = wsum_d(s);
-      if (lane == 0) {
-        P.lse_max[(size_t)j * T + n_tile] = mx;
-        P.lse_sum[(size_t)j * T + n_tile] = s;
-      }
-    }
+    mk_lm_stats(P, tile, n_tile, N, ct, r0, r1);
   }
 }
 
-// Causal paged GQA attention for (row m, kv head kh, 128-key split) on the 4
-// compute warps (same algorithm as attention_kernel in decoder.cu).
+// Causal paged GQA attention for (row m, kv head kh, key split) on the 8
+// compute warps, with the QKV GEMM's epilogue fused in front:
+//  1. the row's q|k|v columns of every QKV split partial arrive by bulk copy;
+//     their sum (split order) x rstd + bias, RoPE on q and k, bf16 rounding;
+//     the new token's k/v go to the paged cache (and to the tile that holds
+//     its position, so no global round trip is waited on);
+//  2. keys [k0, k1) in KT-key tiles dealt round-robin to the warps (cp.async),
+//     online softmax (lane = key for scores, lane = dims for P.V);
+//  3. warps merged in shared memory; several splits (long contexts) merged by
+//     the last-arriving split in split order (deterministic).
 template <int HD, int G>
-__device__ void mk_attention(const MkParams& P, int layer, int m, int kh, int split, uint8_t* scr,
-                             unsigned* ctr, unsigned ep1, float* ws, int ct, int* s_flag) {
+__device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, int kh, int split,
+                             uint8_t* scr, const int2* s_rows, unsigned* ctr, unsigned ep1,
+                             float* ws, int ct, int* s_flag, uint64_t* cbar, uint32_t& cph) {
   using A = AttnSmem<HD, G>;
-  constexpr int DPL = HD / 32, V4 = HD / 8;
+  constexpr int KT = A::KT, DPL = HD / 32, V4 = HD / 8, PER = KT * V4 / 32;
+  constexpr int W = (G + 2) * HD;            // q heads | k | v of this kv head
+  constexpr int WPT = (W + kCT - 1) / kCT;   // of them per thread
   float(*sq)[HD] = reinterpret_cast<float(*)[HD]>(scr);
-  uint8_t(*sk)[32 * A::ROW] = reinterpret_cast<uint8_t(*)[32 * A::ROW]>(scr + A::sq);
-  uint8_t(*sv)[32 * A::VROW] = reinterpret_cast<uint8_t(*)[32 * A::VROW]>(scr + A::sq + A::sk);
-  float(*sp)[G][32] = reinterpret_cast<float(*)[G][32]>(scr + A::sq + A::sk + A::sv);
-  float(*sm_m)[G] = reinterpret_cast<float(*)[G]>(scr + A::sq + A::sk + A::sv + A::sp);
-  float(*sm_l)[G] = reinterpret_cast<float(*)[G]>(scr + A::sq + A::sk + A::sv + A::sp + sizeof(float) * 4 * G);
-  float(*sm_acc)[G][HD] = reinterpret_cast<float(*)[G][HD]>(scr + A::sq);  // aliases sk
+  uint8_t* tiles = scr + A::sq;
+  float(*sp)[G][32] = reinterpret_cast<float(*)[G][32]>(scr + A::sq + A::tiles);
+  float(*sm_m)[G] = reinterpret_cast<float(*)[G]>(scr + A::sq + A::tiles + A::sp);
+  float(*sm_l)[G] = reinterpret_cast<float(*)[G]>(scr + A::sq + A::tiles + A::sp + sizeof(float) * kCW * G);
+  int* spage = reinterpret_cast<int*>(scr + A::sq + A::tiles + A::sp + A::sml);
+  float* sraw = reinterpret_cast<float*>(scr + A::sq + A::tiles + A::sp + A::sml + A::spage);
+  __nv_bfloat16* snew = reinterpret_cast<__nv_bfloat16*>(scr + A::sq + A::tiles + A::sp + A::sml +
+                                                         A::spage + A::sraw);
+  float(*sm_acc)[G][HD] = reinterpret_cast<float(*)[G][HD]>(tiles);  // after the tiles are consumed
   const int warp = ct >> 5, lane = ct & 31;
   const int splits = P.attn_splits, nq = P.nq, nkv = P.nkv;
-  const int slot = P.plan.row_slot[m];
+  const int slot = s_rows[m].x;
   if (slot < 0) {  // every split still arrives: the counters are monotonic
     if (splits > 1 && ct == 0) atomicAdd(&ctr[m * nkv + kh], 1u);
     return;
   }
-  const int ctx = P.plan.row_pos[m] + 1;
-  const int k_begin = split * 128;
+  const int pos = s_rows[m].y;  // position of the new token; ctx = pos + 1 keys
+  const int ctx = pos + 1;
+  const int k0 = split * P.attn_chunk;
+  const int k1 = min(ctx, k0 + P.attn_chunk);
+  const int nkeys = max(0, k1 - k0);
+  const int ntiles = (nkeys + KT - 1) / KT;
+  const bool owner = pos >= k0 && pos < k0 + P.attn_chunk;  // this split holds the new key
+  const int qend = nq * HD, kend = qend + nkv * HD;
+
+  // ---- (1) operands: split partials (bulk), pages, bias, rope, rstd -- all in flight
+  float* stage = reinterpret_cast<float*>(tiles);  // [qkv_cs][W], free until the K/V tiles
+  if (ct == 0) {
+    fence_proxy_async_global();
+    mbar_arrive_expect_tx(cbar, (uint32_t)(qkv_cs * W * 4));
+    const float* part = P.qkv_part + (size_t)m * P.qkv;
+    const size_t pstride = (size_t)P.S * P.qkv;
+    for (int q = 0; q < qkv_cs; ++q) {
+      const float* src = part + q * pstride;
+      float* dst = stage + q * W;
+      bulk_g2s(dst, src + kh * G * HD, G * HD * 4, cbar);
+      bulk_g2s(dst + G * HD, src + qend + kh * HD, HD * 4, cbar);
+      bulk_g2s(dst + (G + 1) * HD, src + kend + kh * HD, HD * 4, cbar);
+    }
+  }
+  const int pg0 = k0 / kPageTokens;
+  for (int i = ct; i < (nkeys + kPageTokens - 1) / kPageTokens; i += kCT)
+    spage[i] = P.block_table[(size_t)slot * P.pps + pg0 + i];
+  constexpr int half = HD / 2;
+  const __nv_bfloat16* bias = P.w + P.layers[layer].qkv_b;
+  float bia[WPT], co[WPT], si[WPT];
+#pragma unroll
+  for (int u = 0; u < WPT; ++u) {
+    const int idx = ct + u * kCT;
+    bia[u] = 0.f;
+    co[u] = 1.f;
+    si[u] = 0.f;
+    if (idx < W) {
+      const int col = idx < G * HD ? kh * G * HD + idx
+                      : idx < (G + 1) * HD ? qend + kh * HD + (idx - G * HD)
+                                           : kend + kh * HD + (idx - (G + 1) * HD);
+      bia[u] = bf2f(bias[col]);
+      if (idx < (G + 1) * HD) {
+        const int jj = idx % HD, i = jj < half ? jj : jj - half;
+        co[u] = P.cos_sin[(size_t)pos * HD + i];
+        si[u] = P.cos_sin[(size_t)pos * HD + half + i];
+      }
+    }
+  }
+  const int cpage = P.block_table[(size_t)slot * P.pps + pos / kPageTokens];
+  float ss = 0.f;
+  for (int p = 0; p < P.parts; ++p) ss += P.ssq[(size_t)m * P.parts + p];
+  const float rstd = rsqrtf(ss * P.inv_h + P.eps);
+  mk_wait(cbar, cph);
+  cph ^= 1;
+#pragma unroll
+  for (int u = 0; u < WPT; ++u) {
+    const int idx = ct + u * kCT;
+    if (idx < W) {
+      float v = 0.f;
+      for (int q = 0; q < qkv_cs; ++q) v += stage[q * W + idx];
+      sraw[idx] = v * rstd + bia[u];
+    }
+  }
+  csync();
+  {
+    const size_t at = (((size_t)cpage * nkv + kh) * kPageTokens + (pos % kPageTokens)) * HD;
+    __nv_bfloat16* kcw = P.kc + P.kv_layer_elems * layer;
+    __nv_bfloat16* vcw = P.vc + P.kv_layer_elems * layer;
+#pragma unroll
+    for (int u = 0; u < WPT; ++u) {
+      const int idx = ct + u * kCT;
+      if (idx >= W) continue;
+      const int jj = idx % HD, base = idx - jj;
+      float y;
+      if (idx < (G + 1) * HD) {  // RoPE (rotate pairs (i, i + hd/2)) on q heads and k
+        const int i = jj < half ? jj : jj - half;
+        const float x1 = sraw[base + i], x2 = sraw[base + i + half];
+        y = jj < half ? x1 * co[u] - x2 * si[u] : x2 * co[u] + x1 * si[u];
+      } else {
+        y = sraw[idx];
+      }
+      const __nv_bfloat16 b = __float2bfloat16(y);
+      if (idx < G * HD) {
+        sq[idx / HD][jj] = bf2f(b) * P.scale;
+      } else if (idx < (G + 1) * HD) {
+        snew[jj] = b;
+        if (owner) kcw[at + jj] = b;
+      } else {
+        snew[HD + jj] = b;
+        if (owner) vcw[at + jj] = b;
+      }
+    }
+  }
+  csync();
+
+  // ---- (2) keys: each warp streams its tiles
   const __nv_bfloat16* kc = P.kc + P.kv_layer_elems * layer;
   const __nv_bfloat16* vc = P.vc + P.kv_layer_elems * layer;
-  for (int i = ct; i < G * HD; i += kCT)
-    sq[i / HD][i % HD] = bf2f(P.q[(size_t)m * nq * HD + (kh * G) * HD + i]) * P.scale;
-  csync();
+  uint8_t* kb = tiles + warp * A::warp_bytes;
+  uint8_t* vb = kb + A::kbuf;
   float mrun[G], lrun[G], acc[G][DPL];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -295,35 +439,41 @@ __device__ void mk_attention(const MkParams& P, int layer, int m, int kh, int sp
 #pragma unroll
     for (int d = 0; d < DPL; ++d) acc[g][d] = 0.f;
   }
-  const int t0 = k_begin + warp * 32;
-  const int nvalid = max(0, min(32, ctx - t0));
-  if (nvalid > 0) {
-    const int page = P.block_table[(size_t)slot * P.pps + t0 / kPageTokens];
-    const size_t base = (((size_t)page * nkv + kh) * kPageTokens + (t0 % kPageTokens)) * HD;
-    const uint4* kg = reinterpret_cast<const uint4*>(kc + base);
-    const uint4* vg = reinterpret_cast<const uint4*>(vc + base);
-    uint4 kr[V4], vr[V4];
+  for (int t = warp; t < ntiles; t += kCW) {
+    const int key0 = k0 + t * KT;
+    const int nv = min(KT, k1 - key0);
+    {
+      const int page = spage[key0 / kPageTokens - pg0];
+      const size_t base = (((size_t)page * nkv + kh) * kPageTokens + (key0 % kPageTokens)) * HD;
+      const uint4* kg = reinterpret_cast<const uint4*>(kc + base);
+      const uint4* vg = reinterpret_cast<const uint4*>(vc + base);
 #pragma unroll
-    for (int i = 0; i < V4; ++i) {
-      const int e = lane + 32 * i, r = e / V4;
-      if (r < nvalid) { kr[i] = kg[e]; vr[i] = vg[e]; }
-    }
-#pragma unroll
-    for (int i = 0; i < V4; ++i) {
-      const int e = lane + 32 * i, r = e / V4, c = e % V4;
-      if (r < nvalid) {
-        *reinterpret_cast<uint4*>(&sk[warp][r * A::ROW + c * 16]) = kr[i];
-        *reinterpret_cast<uint4*>(&sv[warp][r * A::VROW + c * 16]) = vr[i];
+      for (int i = 0; i < PER; ++i) {
+        const int e = lane + 32 * i, r = e / V4, c = e % V4;
+        if (r < nv) {
+          cp_async16(kb + r * A::ROW + c * 16, kg + e);
+          cp_async16(vb + r * A::VROW + c * 16, vg + e);
+        }
       }
+      cp_async_commit();
+      cp_async_wait_all();
     }
     __syncwarp();
+    if (owner && pos >= key0 && pos < key0 + nv) {  // the new key from shared memory
+      const int r = pos - key0;
+      for (int d = lane; d < HD; d += 32) {
+        reinterpret_cast<__nv_bfloat16*>(kb + r * A::ROW)[d] = snew[d];
+        reinterpret_cast<__nv_bfloat16*>(vb + r * A::VROW)[d] = snew[HD + d];
+      }
+      __syncwarp();
+    }
     float s[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) s[g] = 0.f;
-    if (lane < nvalid) {
+    if (lane < nv) {
 #pragma unroll
       for (int c = 0; c < V4; ++c) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(&sk[warp][lane * A::ROW + c * 16]);
+        const uint4 raw = *reinterpret_cast<const uint4*>(kb + lane * A::ROW + c * 16);
         const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
         float kf[8];
 #pragma unroll
@@ -342,18 +492,21 @@ __device__ void mk_attention(const MkParams& P, int layer, int m, int kh, int sp
       }
     }
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float sv_ = lane < nvalid ? s[g] : -INFINITY;
-      const float mx = wmax(sv_);
-      const float p = lane < nvalid ? __expf(sv_ - mx) : 0.f;
-      mrun[g] = mx;
-      lrun[g] = wsum(p);
+    for (int g = 0; g < G; ++g) {  // online softmax
+      const float sv_ = lane < nv ? s[g] : -INFINITY;
+      const float mn = fmaxf(mrun[g], wmax(sv_));
+      const float corr = mrun[g] == -INFINITY ? 0.f : __expf(mrun[g] - mn);
+      const float p = lane < nv ? __expf(sv_ - mn) : 0.f;
+      lrun[g] = lrun[g] * corr + wsum(p);
+      mrun[g] = mn;
+#pragma unroll
+      for (int d = 0; d < DPL; ++d) acc[g][d] *= corr;
       sp[warp][g][lane] = p;
     }
     __syncwarp();
-    for (int j = 0; j < nvalid; ++j) {
+    for (int j = 0; j < nv; ++j) {
       float vf[DPL];
-      const uint8_t* vrow = &sv[warp][j * A::VROW + lane * DPL * 2];
+      const uint8_t* vrow = vb + j * A::VROW + lane * DPL * 2;
       if constexpr (DPL == 2) {
         const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vrow));
         vf[0] = f.x;
@@ -361,8 +514,8 @@ __device__ void mk_attention(const MkParams& P, int layer, int m, int kh, int sp
       } else {
         const uint2 raw = *reinterpret_cast<const uint2*>(vrow);
         const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-        const float2 a = __bfloat1622float2(p2[0]), b = __bfloat1622float2(p2[1]);
-        vf[0] = a.x; vf[1] = a.y; vf[2] = b.x; vf[3] = b.y;
+        const float2 a = __bfloat1622float2(p2[0]), c2 = __bfloat1622float2(p2[1]);
+        vf[0] = a.x; vf[1] = a.y; vf[2] = c2.x; vf[3] = c2.y;
       }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
@@ -371,8 +524,11 @@ __device__ void mk_attention(const MkParams& P, int layer, int m, int kh, int sp
         for (int d = 0; d < DPL; ++d) acc[g][d] += pj * vf[d];
       }
     }
+    __syncwarp();
   }
-  csync();  // sm_acc aliases the K tiles
+
+  // ---- (3) merge the warps, then the splits
+  csync();  // sm_acc aliases the tiles
   if (lane == 0) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -391,10 +547,10 @@ __device__ void mk_attention(const MkParams& P, int layer, int m, int kh, int sp
     const int g = i / HD, d = i % HD;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w][g]);
+    for (int w = 0; w < kCW; ++w) M = fmaxf(M, sm_m[w][g]);
     float L = 0.f, Acc = 0.f;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
+    for (int w = 0; w < kCW; ++w) {
       const float a = (sm_m[w][g] == -INFINITY) ? 0.f : __expf(sm_m[w][g] - M);
       L += sm_l[w][g] * a;
       Acc += sm_acc[w][g][d] * a;
@@ -419,11 +575,10 @@ __device__ void mk_attention(const MkParams& P, int layer, int m, int kh, int sp
     *s_flag = (atomicAdd(&ctr[m * nkv + kh], 1u) + 1u == ep1 * (unsigned)splits);
   }
   csync();
-  const bool last = *s_flag;
-  if (last) {
+  if (*s_flag) {
     __threadfence();
     const float* base = ws + ((size_t)m * nkv + kh) * splits * rec;
-    const int used = min(splits, (ctx + 127) / 128);
+    const int used = min(splits, (ctx + P.attn_chunk - 1) / P.attn_chunk);
     for (int i = ct; i < G * HD; i += kCT) {
       const int g = i / HD, d = i % HD;
       float M = -INFINITY;
@@ -441,7 +596,8 @@ __device__ void mk_attention(const MkParams& P, int layer, int m, int kh, int sp
   csync();
 }
 
-// plan copy + embedding + first RMSNorm statistics for row m
+// plan copy + embedding + first RMSNorm statistics for row m.  red: one
+// partial per (128-column part, warp-quarter of the part).
 __device__ void mk_embed(const MkParams& P, int m, int ct, float* red) {
   if (ct == 0) {
     P.plan.row_slot[m] = P.next.row_slot[m];
@@ -453,8 +609,9 @@ __device__ void mk_embed(const MkParams& P, int m, int ct, float* red) {
   const bool ok = tok >= 0 && tok < P.V;
   const __nv_bfloat16* E = P.w + P.off_embed;
   const __nv_bfloat16* g = P.w + P.layers[0].ln1;
-  for (int p = 0; p < P.parts; ++p) {
-    const int c = p * 128 + ct;
+  const int cols = P.parts * 128;
+#pragma unroll 4
+  for (int c = ct; c < cols; c += kCT) {  // a warp's 32 columns lie in one part
     float v = 0.f;
     if (c < P.H) {
       v = ok ? bf2f(E[(size_t)tok * P.H + c]) : 0.f;
@@ -462,20 +619,22 @@ __device__ void mk_embed(const MkParams& P, int m, int ct, float* red) {
       P.xg[(size_t)m * P.H + c] = __float2bfloat16(v * bf2f(g[c]));
     }
     const float s = wsum(v * v);
-    if ((ct & 31) == 0) red[ct >> 5] = s;
-    csync();
-    if (ct == 0) P.ssq[(size_t)m * P.parts + p] = red[0] + red[1] + red[2] + red[3];
-    csync();
+    if ((ct & 31) == 0) red[c >> 5] = s;
   }
+  csync();
+  for (int p = ct; p < P.parts; p += kCT)
+    P.ssq[(size_t)m * P.parts + p] = red[p * 4] + red[p * 4 + 1] + red[p * 4 + 2] + red[p * 4 + 3];
+  csync();
 }
 
-// Sampling of slot s from the LM-head tile partials (128 threads): same
-// algorithm as sample_row in decoder.cu.
+// Sampling of slot s from the LM-head tile partials (same algorithm as
+// sample_row in decoder.cu, 256 threads): lse from the tile (max, sum)
+// pairs, then the tile walk of the inverse CDF.
 __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
   double* scan = reinterpret_cast<double*>(scr);
   double* red = scan + kCT;
-  int* iv = reinterpret_cast<int*>(red + 33);
-  float* fv = reinterpret_cast<float*>(iv + 8);
+  int* iv = reinterpret_cast<int*>(red + 16);
+  float* fv = reinterpret_cast<float*>(iv + 16);
   const int warp = ct >> 5, lane = ct & 31;
   const int V = P.V;
   const int ri = (*P.round_ctr - 1) % P.ring.rounds;
@@ -512,7 +671,7 @@ __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
   if (lane == 0) { fv[warp] = mx; iv[warp] = mt; }
   csync();
   if (ct == 0) {
-    for (int w = 1; w < 4; ++w)
+    for (int w = 1; w < kCW; ++w)
       if (fv[w] > fv[0] || (fv[w] == fv[0] && iv[w] < iv[0])) { fv[0] = fv[w]; iv[0] = iv[w]; }
   }
   csync();
@@ -524,7 +683,9 @@ __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
   part = wsum_d(part);
   if (lane == 0) red[warp] = part;
   csync();
-  const double lse = M + log(red[0] + red[1] + red[2] + red[3]);
+  double tot = 0.0;
+  for (int w = 0; w < kCW; ++w) tot += red[w];
+  const double lse = M + log(tot);
   csync();
   const double u = uniform_draw(P.ss.seed[s], (uint64_t)P.ss.gen_count[s]);
   int tok;
@@ -537,10 +698,10 @@ __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-      if (lane == 0) iv[4] = best == 0x7fffffff ? mtile * kLmTile : best;
+      if (lane == 0) iv[kCW] = best == 0x7fffffff ? mtile * kLmTile : best;
     }
     csync();
-    tok = iv[4];
+    tok = iv[kCW];
   } else {
     double mass = 0.0;
     for (int t = t0; t < t1; ++t) mass += psum[t] * exp((double)pmax[t] - lse);
@@ -568,7 +729,8 @@ __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
     if (lane == 0) iv[warp] = cand;
     csync();
     if (warp == 0) {
-      int t = min(min(iv[0], iv[1]), min(iv[2], iv[3]));
+      int t = 0x7fffffff;
+      for (int w = 0; w < kCW; ++w) t = min(t, iv[w]);
       int tk = V - 1;
       if (t != 0x7fffffff) {
         const int owner = t / C;
@@ -607,10 +769,10 @@ __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
           base += __shfl_sync(0xffffffffu, incl, 31);
         }
       }
-      if (lane == 0) iv[4] = tk;
+      if (lane == 0) iv[kCW] = tk;
     }
     csync();
-    tok = iv[4];
+    tok = iv[kCW];
   }
   if (ct == 0) {
     const int pos_row = P.plan.row_pos[r];
@@ -654,11 +816,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
+  uint64_t* cbar = tempty + 2;  // compute warps' bulk-copy barrier
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Lo::misc);
   int* s_flag = reinterpret_cast<int*>(smem + Lo::misc + 4);
-  float* s_red = reinterpret_cast<float*>(smem + Lo::misc + 8);  // 4 floats
   float* s_rstd = reinterpret_cast<float*>(smem + Lo::rstd);
-  int4* s_row = reinterpret_cast<int4*>(smem + Lo::rowm);
+  int2* s_rows = reinterpret_cast<int2*>(smem + Lo::rows);
 
   const int warp = threadIdx.x >> 5;
   const int GR = gridDim.x, c = blockIdx.x;
@@ -677,6 +839,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], kCT);
       }
+      mbar_init(cbar, 1);
       fence_barrier_init();
     }
     __syncwarp();
@@ -716,6 +879,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             wait_count(&P.phase_done[p - 1], target);
             fence_proxy_async_global();  // generic-proxy results -> TMA reads
             dep_ok = true;
+            if (P.trace) P.trace[((size_t)p * GR + c) * 16 + 4] = globaltimer();
           }
           for (int k = 0; k < pre; ++k) {
             const int st = (s0 + k) % STAGES;
@@ -770,6 +934,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
   } else if (warp >= 4) {
     // ------------------------------------------------------ compute
     const int ct = threadIdx.x - 128, cw = ct >> 5;
+    const int col = ct & (kBN - 1);      // accumulator lane (= output column) drained
+    const int hf = cw >> 2;              // token half [32 hf, 32 hf + 32) drained
+    uint32_t cph = 0;                    // cbar phase
+    bool rows_ready = false;
     const bool stamp = P.stamps != nullptr && c == 0 && ct == 0;
     int acc = 0;
     uint32_t aph = 0;
@@ -783,79 +951,126 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
         }
         csync();
       }
+      unsigned long long* tr = P.trace ? P.trace + ((size_t)p * GR + c) * 16 : nullptr;
+      if (tr && ct == 0) {
+        tr[0] = globaltimer();
+        tr[8] = clock64();
+      }
       if (F.kind == MK_EMBED) {
         if (c == 0 && ct == 0) *P.round_ctr += 1;
-        for (int m = first_item(c, F.rot, GR); m < F.n_items; m += GR) mk_embed(P, m, ct, s_red);
+        for (int m = first_item(c, F.rot, GR); m < F.n_items; m += GR)
+          mk_embed(P, m, ct, reinterpret_cast<float*>(scratch));
       } else if (F.kind == MK_ATTN) {
+        if (!rows_ready) {  // the round's plan, once per CTA
+          for (int j = ct; j < P.S; j += kCT) s_rows[j] = make_int2(P.plan.row_slot[j], P.plan.row_pos[j]);
+          csync();
+          rows_ready = true;
+        }
         for (int i = first_item(c, F.rot, GR); i < F.n_items; i += GR) {
           const int split = i % P.attn_splits;
           const int rest = i / P.attn_splits;
-          mk_attention<HD, G>(P, F.layer, rest / P.nkv, rest % P.nkv, split, scratch,
-                              P.tile_ctr + F.ctr_base, ep1, P.ws, ct, s_flag);
+          const long long a_c0 = clock64();
+          mk_attention<HD, G>(P, F.layer, F.cs, rest / P.nkv, rest % P.nkv, split, scratch, s_rows,
+                              P.tile_ctr + F.ctr_base, ep1, P.ws, ct, s_flag, cbar, cph);
+          if (tr && ct == 0 && tr[10] == 0) tr[10] = clock64() - a_c0;
         }
       } else if (F.kind == MK_SAMPLE) {
         for (int s = first_item(c, F.rot, GR); s < F.n_items; s += GR) mk_sample(P, s, ct, scratch);
       } else {
-        mk_rows(P, F.kind, s_rstd, s_row, ct);
+        mk_rows(P, F.kind, s_rstd, ct);
         for (int i = first_item(c, F.rot, GR); i < F.n_items; i += GR) {
           const int tile_n = i / F.cs, split = i % F.cs;
+          float colv = 0.f;
+          if (tile_n * kBN + col < F.N) {
+            const __nv_bfloat16* w = P.w;
+            if (F.kind == MK_O) colv = bf2f(w[P.layers[F.layer].ln2 + tile_n * kBN + col]);
+            else if (F.kind == MK_DOWN)
+              colv = bf2f(w[(F.layer + 1 < P.L ? P.layers[F.layer + 1].ln1 : P.off_final_norm) +
+                            tile_n * kBN + col]);
+          }
           mk_wait(&tfull[acc], aph);
           tc_fence_after();
-          const uint32_t lane_addr = tmem + acc * kTok + ((uint32_t)(cw * 32) << 16);
-          uint32_t ra[32], rb[32];
-          tmem_ld_32x32b_x32(lane_addr, ra);
-          tmem_ld_32x32b_x32(lane_addr + 32, rb);
+          if (tr && ct == 0 && tr[1] == 0) tr[1] = globaltimer();
+          uint32_t ra[32];
+          tmem_ld_32x32b_x32(tmem + acc * kTok + hf * 32 + ((uint32_t)((cw & 3) * 32) << 16), ra);
           tmem_ld_wait();
           tc_fence_before();
           mbar_arrive(&tempty[acc]);  // accumulator free for the MMA warp
           if (++acc == 2) { acc = 0; aph ^= 1; }
+          const int j0 = hf * 32;  // tokens of ra
           int r0 = 0, r1 = P.S;
+          if (F.kind == MK_QKV) {
+            // raw split partial [split][row][col]; the attention items reduce it
+            if (tile_n * kBN + col < F.N) {
+              float* part = P.qkv_part + ((size_t)split * P.S) * P.qkv + tile_n * kBN + col;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j0 + j < P.S) __stcg(&part[(size_t)(j0 + j) * P.qkv], __uint_as_float(ra[j]));
+            }
+            continue;
+          }
           if (F.cs == 1) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) tile[j * kPitch + ct] = __uint_as_float(ra[j]);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) tile[(32 + j) * kPitch + ct] = __uint_as_float(rb[j]);
+            for (int j = 0; j < 32; ++j) tile[(j0 + j) * kPitch + col] = __uint_as_float(ra[j]);
           } else {
             // publish this split's partial (rows < S), wait for the tile's other
             // splits, then reduce this split's row slice in split order
             float* part = P.ws + (size_t)i * kTileFloats;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (j < P.S) __stcg(&part[j * kBN + ct], __uint_as_float(ra[j]));
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (32 + j < P.S) __stcg(&part[(32 + j) * kBN + ct], __uint_as_float(rb[j]));
+              if (j0 + j < P.S) __stcg(&part[(j0 + j) * kBN + col], __uint_as_float(ra[j]));
+            fence_proxy_async_global();
+            r0 = (split * P.S) / F.cs;
+            r1 = ((split + 1) * P.S) / F.cs;
+            const int nr = r1 - r0;
+            float* stage = tile + kTok * kPitch;  // [cs][nr][128]
             csync();
             if (ct == 0) {
               unsigned* tc = &P.tile_ctr[F.ctr_base + tile_n];
               __threadfence();
               atomicAdd(tc, 1u);
               wait_count(tc, ep1 * (unsigned)F.cs);
-            }
-            csync();
-            r0 = (split * P.S) / F.cs;
-            r1 = ((split + 1) * P.S) / F.cs;
-            const float4* b4 = reinterpret_cast<const float4*>(P.ws + (size_t)tile_n * F.cs * kTileFloats);
-            for (int e = r0 * (kBN / 4) + ct; e < r1 * (kBN / 4); e += kCT) {
-              float4 a = __ldcg(b4 + e);
-              for (int q = 1; q < F.cs; ++q) {
-                const float4 v = __ldcg(b4 + (size_t)q * (kTileFloats / 4) + e);
-                a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+              if (tr && tr[2] == 0) tr[2] = globaltimer();
+              if (nr > 0) {
+                fence_proxy_async_global();
+                mbar_arrive_expect_tx(cbar, (uint32_t)(F.cs * nr * kBN * 4));
+                const float* src = P.ws + (size_t)tile_n * F.cs * kTileFloats + (size_t)r0 * kBN;
+                for (int q = 0; q < F.cs; ++q)
+                  bulk_g2s(stage + (size_t)q * nr * kBN, src + (size_t)q * kTileFloats, nr * kBN * 4, cbar);
               }
-              const int j = e / (kBN / 4), cc = (e % (kBN / 4)) * 4;
-              *reinterpret_cast<float4*>(&tile[j * kPitch + cc]) = a;
+            }
+            if (nr > 0) {
+              mk_wait(cbar, cph);
+              cph ^= 1;
+              const float4* s4 = reinterpret_cast<const float4*>(stage);
+              for (int e = ct; e < nr * (kBN / 4); e += kCT) {
+                float4 a = s4[e];
+                for (int q = 1; q < F.cs; ++q) {
+                  const float4 v = s4[(size_t)q * nr * (kBN / 4) + e];
+                  a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+                }
+                const int j = r0 + e / (kBN / 4), cc = (e % (kBN / 4)) * 4;
+                *reinterpret_cast<float4*>(&tile[j * kPitch + cc]) = a;
+              }
             }
           }
+          if (tr && ct == 0 && tr[5] == 0) tr[5] = globaltimer();
           csync();
-          if (r1 > r0) mk_epilogue(P, F, tile_n, tile, s_rstd, s_row, ct, r0, r1);
+          if (r1 > r0) mk_epilogue(P, F, tile_n, tile, s_rstd, ct, r0, r1, colv);
           csync();
+          if (tr && ct == 0 && tr[6] == 0) tr[6] = globaltimer();
         }
       }
       fence_proxy_async_global();  // later phases read these results with TMA
       csync();
       if (ct == 0) {
+        if (tr) {
+          tr[3] = globaltimer();
+          tr[9] = clock64();
+        }
         __threadfence();
         atomicAdd(&P.phase_done[p], 1u);
+        if (tr) tr[7] = globaltimer();
       }
     }
     if (stamp) {
@@ -905,6 +1120,11 @@ cudaError_t launch_t(const MkParams& p, int grid, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, decode_megakernel<HD, G>, p);
 }
 
+template <int HD, int G>
+int qkv_cap_t() {
+  return (int)(AttnSmem<HD, G>::tiles / ((size_t)(G + 2) * HD * 4));
+}
+
 }  // namespace
 
 int megakernel_splits(int N, int K, int grid) {
@@ -913,7 +1133,7 @@ int megakernel_splits(int N, int K, int grid) {
   const int tiles = (N + kBN - 1) / kBN, kb = K / kBK;
   int best = 1;
   long best_cost = (long)((tiles + grid - 1) / grid) * kb * 24;
-  for (int cs = 2; cs <= kb && tiles * cs <= grid; ++cs) {
+  for (int cs = 2; cs <= kb && cs <= kMaxCs && tiles * cs <= grid; ++cs) {
     const long cost = (long)((kb + cs - 1) / cs) * 24 + 40;
     if (cost < best_cost) {
       best_cost = cost;
@@ -921,6 +1141,15 @@ int megakernel_splits(int N, int K, int grid) {
     }
   }
   return best;
+}
+
+int megakernel_qkv_splits(const DecoderDims& d, int grid) {
+  const int G = d.nq / d.nkv;
+  int cap = 1;
+  if (d.hd == 64) cap = G == 2 ? qkv_cap_t<64, 2>() : qkv_cap_t<64, 7>();
+  else cap = G == 6 ? qkv_cap_t<128, 6>() : qkv_cap_t<128, 7>();
+  const int cs = megakernel_splits(d.qkv(), d.H, grid);
+  return cs < cap ? cs : cap;
 }
 
 size_t megakernel_ws_floats(int n_items, int cs, int rows) {

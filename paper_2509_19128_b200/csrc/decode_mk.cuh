@@ -23,6 +23,8 @@
 
 namespace srl {
 
+constexpr int kMkAttnChunk = 1024;  // keys per attention item (longer contexts split)
+
 enum MkKind : int { MK_EMBED = 0, MK_QKV = 1, MK_ATTN = 2, MK_O = 3, MK_GU = 4, MK_DOWN = 5,
                     MK_LM = 6, MK_SAMPLE = 7 };
 
@@ -30,7 +32,7 @@ struct MkPhase {
   int kind;
   int layer;
   int n_items;  // work items (GEMM: n_tiles * cs)
-  int cs;       // split-K factor (GEMM)
+  int cs;       // split-K factor (GEMM); ATTN: the QKV phase's split-K factor
   int N, K;     // GEMM shape
   int wmap;     // weight tensor-map index
   int xmap;     // activation tensor-map index: 0 xg, 1 attn, 2 act
@@ -43,7 +45,7 @@ struct MkLayer {
 };
 
 struct MkParams {
-  int S, H, I, V, L, nq, nkv, hd, qkv, parts, pps, attn_splits, greedy;
+  int S, H, I, V, L, nq, nkv, hd, qkv, parts, pps, attn_splits, attn_chunk, greedy;
   float eps, inv_h, scale;
   const __nv_bfloat16* w;       // flat weights (active buffer)
   const CUtensorMap* wmaps;     // [4 * L + 1]: per layer qkv, o, gate_up, down; then lm_head
@@ -72,15 +74,20 @@ struct MkParams {
   unsigned* epoch;              // rounds completed by this kernel (device scalar)
   unsigned* tile_ctr;           // split-K / split-KV arrival counters (monotonic)
   float* ws;                    // split-K and split-KV partials
+  float* qkv_part;              // QKV split partials [cs][S][qkv] (reduced by attention)
   const MkPhase* phases;
   int n_phases;
   unsigned long long* stamps;   // profiling: [n_phases + 1] globaltimer (ns) or nullptr
+  int dbg;                      // experiments: bit0 skip logits store, bit1 skip LM stats
+  unsigned long long* trace;    // debugging: [n_phases][grid][8] per-CTA timestamps or nullptr
 };
 
 // Host: can this config run the megakernel (rows <= 64, supported G/HD)?
 bool megakernel_supported(const DecoderDims& d, int slots);
 // Split-K factor of a GEMM phase on `grid` CTAs (one wave unless cs = 1).
 int megakernel_splits(int N, int K, int grid);
+// QKV split-K factor (capped by the attention items' partial staging).
+int megakernel_qkv_splits(const DecoderDims& d, int grid);
 // Floats of split partials a phase needs.
 size_t megakernel_ws_floats(int n_items, int cs, int rows);
 size_t megakernel_smem_bytes(const DecoderDims& d);

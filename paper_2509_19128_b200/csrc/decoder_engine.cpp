@@ -237,6 +237,8 @@ DecoderBackend::~DecoderBackend() {
     if (mk_.wmaps[b]) cudaFree(mk_.wmaps[b]);
   if (mk_.mem) cudaFree(mk_.mem);
   if (mk_.ws) cudaFree(mk_.ws);
+  if (mk_.qkv_part) cudaFree(mk_.qkv_part);
+  if (mk_.trace) cudaFree(mk_.trace);
   if (mk_.stamps_host) cudaFreeHost(mk_.stamps_host);
   for (int b = 0; b < 2; ++b)
     if (exec_[b]) cudaGraphExecDestroy(exec_[b]);
@@ -314,7 +316,7 @@ int DecoderBackend::mega_init() {
   DecoderRunner& r = *runner_;
   const int grid = r.sms;
   if (megakernel_occupancy(d_) < 1) return SRL_OK;  // not co-resident: multi-kernel round
-  const int L = d_.L, splits = (max_seq_ + 127) / 128;  // attention_splits(): 128-key splits
+  const int L = d_.L, splits = (max_seq_ + kMkAttnChunk - 1) / kMkAttnChunk;
   std::vector<MkPhase> ph;
   int ctr = 0, items_total = 0;
   size_t ws = (size_t)S_ * d_.nkv * splits * (d_.nq / d_.nkv) * (d_.hd + 2);
@@ -331,10 +333,13 @@ int DecoderBackend::mega_init() {
     ws = std::max(ws, megakernel_ws_floats(tiles * cs, cs, S_));
     add(kind, layer, tiles * cs, cs, N, K, wmap, xmap, cs > 1 ? tiles : 0);
   };
+  // QKV: raw split partials only (no counters); the attention items reduce them
+  const int qkv_cs = megakernel_qkv_splits(d_, grid);
+  const int qkv_tiles = (d_.qkv() + 127) / 128;
   add(MK_EMBED, 0, S_, 1, 0, 0, 0, 0, 0);
   for (int l = 0; l < L; ++l) {
-    gemm(MK_QKV, l, d_.qkv(), d_.H, 4 * l + 0, 0);
-    add(MK_ATTN, l, S_ * d_.nkv * splits, 1, 0, 0, 0, 0, S_ * d_.nkv);
+    add(MK_QKV, l, qkv_tiles * qkv_cs, qkv_cs, d_.qkv(), d_.H, 4 * l + 0, 0, 0);
+    add(MK_ATTN, l, S_ * d_.nkv * splits, qkv_cs, 0, 0, 0, 0, S_ * d_.nkv);
     gemm(MK_O, l, d_.H, d_.qdim(), 4 * l + 1, 1);
     gemm(MK_GU, l, 2 * d_.I, d_.H, 4 * l + 2, 0);
     gemm(MK_DOWN, l, d_.H, d_.I, 4 * l + 3, 2);
@@ -352,6 +357,7 @@ int DecoderBackend::mega_init() {
   SRL_CUDA(cudaMalloc(&mk_.mem, total));
   SRL_CUDA(cudaMemset(mk_.mem, 0, total));
   SRL_CUDA(cudaMalloc(&mk_.ws, std::max<size_t>(ws, 1) * sizeof(float)));
+  SRL_CUDA(cudaMalloc(&mk_.qkv_part, (size_t)qkv_cs * S_ * d_.qkv() * sizeof(float)));
   SRL_CUDA(cudaMallocHost(&mk_.stamps_host, 8 * (size_t)(n + 1)));
   uint8_t* base = static_cast<uint8_t*>(mk_.mem);
   std::vector<MkLayer> ly(L);
@@ -378,7 +384,7 @@ int DecoderBackend::mega_init() {
     P = MkParams{};
     P.S = S_; P.H = d_.H; P.I = d_.I; P.V = d_.V; P.L = L; P.nq = d_.nq; P.nkv = d_.nkv;
     P.hd = d_.hd; P.qkv = d_.qkv(); P.parts = d_.ssq_parts(); P.pps = r.pages_per_seq;
-    P.attn_splits = splits; P.greedy = opts_.greedy;
+    P.attn_splits = splits; P.attn_chunk = kMkAttnChunk; P.greedy = opts_.greedy;
     P.eps = d_.eps; P.inv_h = 1.0f / (float)d_.H; P.scale = 1.0f / sqrtf((float)d_.hd);
     P.w = buf_[b]->w;
     P.wmaps = mk_.wmaps[b];
@@ -396,11 +402,14 @@ int DecoderBackend::mega_init() {
     P.epoch = reinterpret_cast<unsigned*>(base + o_ep);
     P.tile_ctr = reinterpret_cast<unsigned*>(base + o_tc);
     P.ws = mk_.ws;
+    P.qkv_part = mk_.qkv_part;
     P.phases = reinterpret_cast<const MkPhase*>(base + o_ph);
     P.n_phases = n;
     P.stamps = nullptr;
+    if (const char* dbg = std::getenv("SRL_MK_DBG")) P.dbg = std::atoi(dbg);
   }
   mk_.stamps = reinterpret_cast<unsigned long long*>(base + o_st);
+  if (std::getenv("SRL_MK_TRACE")) SRL_CUDA(cudaMalloc(&mk_.trace, 128 * (size_t)n * grid));
   mk_.phases = ph;
   mk_.n_phases = n;
   mk_.grid = grid;
@@ -411,6 +420,10 @@ int DecoderBackend::mega_init() {
 int DecoderBackend::mega_round(int b, bool profile) {
   MkParams p = mk_.params[b];
   if (profile) p.stamps = mk_.stamps;
+  if (profile && mk_.trace) {
+    p.trace = mk_.trace;
+    SRL_CUDA(cudaMemsetAsync(mk_.trace, 0, 128 * (size_t)mk_.n_phases * mk_.grid, st_));
+  }
   const cudaError_t e = launch_megakernel(p, d_, mk_.grid, st_);
   if (e != cudaSuccess) return cuda_fail(e, "launch_megakernel");
   if (profile) {
@@ -427,6 +440,21 @@ int DecoderBackend::mega_round(int b, bool profile) {
     }
     profile_.valid = 1;
     profile_.rows = S_;
+    if (mk_.trace) {  // debugging dump: kind, cs, n_items per phase then the raw stamps
+      const size_t nt = 16 * (size_t)mk_.n_phases * mk_.grid;
+      std::vector<unsigned long long> h(nt);
+      SRL_CUDA(cudaMemcpy(h.data(), mk_.trace, 8 * nt, cudaMemcpyDeviceToHost));
+      if (FILE* f = std::fopen(std::getenv("SRL_MK_TRACE"), "wb")) {
+        const int hdr[2] = {mk_.n_phases, mk_.grid};
+        std::fwrite(hdr, sizeof(hdr), 1, f);
+        for (const MkPhase& f2 : mk_.phases) {
+          const int row[3] = {f2.kind, f2.cs, f2.n_items};
+          std::fwrite(row, sizeof(row), 1, f);
+        }
+        std::fwrite(h.data(), 8, nt, f);
+        std::fclose(f);
+      }
+    }
   }
   return SRL_OK;
 }

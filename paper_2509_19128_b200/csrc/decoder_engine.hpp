@@ -141,8 +141,10 @@ class DecoderBackend final : public Backend {
     CUtensorMap* wmaps[2] = {nullptr, nullptr};
     void* mem = nullptr;                 // phases, layers, xmaps, counters, stamps
     float* ws = nullptr;
+    float* qkv_part = nullptr;
     unsigned long long* stamps = nullptr;
     unsigned long long* stamps_host = nullptr;
+    unsigned long long* trace = nullptr;  // SRL_MK_TRACE=<file>: per-CTA phase timestamps
   } mk_;
 };
 
