@@ -79,6 +79,61 @@ __device__ __forceinline__ void mk_wait(uint64_t* bar, uint32_t parity) {
   SpinGuard g;
   while (!mbar_try(bar, parity)) g.tick();
 }
+// first item of CTA c in a phase whose items are dealt round-robin from `rot`
+__device__ __forceinline__ int first_item(int c, int rot, int G) { return ((c - rot) % G + G) % G; }
+
+// L2 prefetch of one weight tile (no shared memory, no completion).
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* m, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ bool is_gemm(int kind) {
+  return kind == MK_QKV || kind == MK_O || kind == MK_GU || kind == MK_DOWN || kind == MK_LM;
+}
+
+// Walks this CTA's weight k-blocks in the producer's load order (phase, item,
+// k-block); the L2 prefetch stream runs a bounded distance ahead of the loads.
+struct WeightCursor {
+  int p = 0, i = 0, k = 0, kb0 = 0, nkb = 0;
+  bool live = false;
+  __device__ bool enter_item(const MkParams& P, int GR) {  // (p, i) valid -> k range
+    const MkPhase& F = P.phases[p];
+    const int kbt = F.K / 64, split = i % F.cs;
+    kb0 = (split * kbt) / F.cs;
+    nkb = ((split + 1) * kbt) / F.cs - kb0;
+    k = 0;
+    (void)GR;
+    return nkb > 0;
+  }
+  __device__ bool seek_phase(const MkParams& P, int c, int GR) {  // from phase p on
+    for (; p < P.n_phases; ++p) {
+      const MkPhase& F = P.phases[p];
+      if (!is_gemm(F.kind)) continue;
+      i = first_item(c, F.rot, GR);
+      if (i < F.n_items && enter_item(P, GR)) return live = true;
+    }
+    return live = false;
+  }
+  __device__ void start(const MkParams& P, int c, int GR) {
+    p = 0;
+    seek_phase(P, c, GR);
+  }
+  __device__ void next(const MkParams& P, int c, int GR) {
+    if (++k < nkb) return;
+    const MkPhase& F = P.phases[p];
+    for (i += GR; i < F.n_items; i += GR)
+      if (enter_item(P, GR)) return;
+    ++p;
+    seek_phase(P, c, GR);
+  }
+  __device__ void prefetch(const MkParams& P) const {
+    const MkPhase& F = P.phases[p];
+    tma_prefetch_l2(&P.wmaps[F.wmap], (kb0 + k) * 64, (i / F.cs) * 128);
+  }
+};
+
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -120,8 +175,6 @@ __device__ __forceinline__ double uniform_draw(uint64_t seed, uint64_t n) {
   return (double)(z >> 11) * 0x1.0p-53;
 }
 
-// first item of CTA c in a phase whose items are dealt round-robin from `rot`
-__device__ __forceinline__ int first_item(int c, int rot, int G) { return ((c - rot) % G + G) % G; }
 
 // Attention item scratch: q, per-warp K/V tiles (cp.async), probabilities,
 // per-warp softmax state, the row's reduced q|k|v; the QKV split partials are
@@ -309,8 +362,10 @@ __device__ void mk_epilogue(const MkParams& P, const MkPhase& ph, int n_tile, fl
 template <int HD, int G>
 __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, int kh, int split,
                              uint8_t* scr, const int2* s_rows, unsigned* ctr, unsigned ep1,
-                             float* ws, int ct, int* s_flag, uint64_t* cbar, uint32_t& cph) {
+                             float* ws, int ct, int* s_flag, uint64_t* cbar, uint32_t& cph,
+                             unsigned long long* tr) {
   using A = AttnSmem<HD, G>;
+  const long long c_start = clock64();
   constexpr int KT = A::KT, DPL = HD / 32, V4 = HD / 8, PER = KT * V4 / 32;
   constexpr int W = (G + 2) * HD;            // q heads | k | v of this kv head
   constexpr int WPT = (W + kCT - 1) / kCT;   // of them per thread
@@ -342,18 +397,10 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
 
   // ---- (1) operands: split partials (bulk), pages, bias, rope, rstd -- all in flight
   float* stage = reinterpret_cast<float*>(tiles);  // [qkv_cs][W], free until the K/V tiles
-  if (ct == 0) {
+  if (ct == 0) {  // the row's partials are contiguous: [m][kh][split][W]
     fence_proxy_async_global();
     mbar_arrive_expect_tx(cbar, (uint32_t)(qkv_cs * W * 4));
-    const float* part = P.qkv_part + (size_t)m * P.qkv;
-    const size_t pstride = (size_t)P.S * P.qkv;
-    for (int q = 0; q < qkv_cs; ++q) {
-      const float* src = part + q * pstride;
-      float* dst = stage + q * W;
-      bulk_g2s(dst, src + kh * G * HD, G * HD * 4, cbar);
-      bulk_g2s(dst + G * HD, src + qend + kh * HD, HD * 4, cbar);
-      bulk_g2s(dst + (G + 1) * HD, src + kend + kh * HD, HD * 4, cbar);
-    }
+    bulk_g2s(stage, P.qkv_part + ((size_t)m * nkv + kh) * qkv_cs * W, qkv_cs * W * 4, cbar);
   }
   const int pg0 = k0 / kPageTokens;
   for (int i = ct; i < (nkeys + kPageTokens - 1) / kPageTokens; i += kCT)
@@ -426,6 +473,7 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
   }
   csync();
 
+  if (tr && ct == 0 && tr[11] == 0) tr[11] = clock64() - c_start;
   // ---- (2) keys: each warp streams its tiles
   const __nv_bfloat16* kc = P.kc + P.kv_layer_elems * layer;
   const __nv_bfloat16* vc = P.vc + P.kv_layer_elems * layer;
@@ -528,7 +576,9 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
   }
 
   // ---- (3) merge the warps, then the splits
+  if (tr && ct == 0 && tr[12] == 0) tr[12] = clock64() - c_start;
   csync();  // sm_acc aliases the tiles
+  if (tr && ct == 0 && tr[13] == 0) tr[13] = clock64() - c_start;
   if (lane == 0) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -567,6 +617,7 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
   }
   if (splits == 1) {
     csync();
+    if (tr && ct == 0 && tr[14] == 0) tr[14] = clock64() - c_start;
     return;
   }
   csync();
@@ -855,6 +906,18 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t ph = 0;
+      WeightCursor pf;  // L2 prefetch stream, pf_blocks k-blocks ahead of the loads
+      pf.start(P, c, GR);
+      int ahead = 0;
+      auto load_issued = [&]() {
+        --ahead;
+        while (pf.live && ahead < P.pf_blocks) {
+          pf.prefetch(P);
+          pf.next(P, c, GR);
+          ++ahead;
+        }
+      };
+      load_issued();
       for (int p = 0; p < P.n_phases; ++p) {
         const MkPhase& F = P.phases[p];
         if (F.kind == MK_EMBED || F.kind == MK_ATTN || F.kind == MK_SAMPLE) continue;
@@ -873,6 +936,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             mk_wait(&empty[stage], ph ^ 1);
             mbar_arrive_expect_tx(&full[stage], kStageBytes);
             tma_load_2d_hint(smem + stage * kStageBytes, tw, &full[stage], (kb0 + k) * kBK, n0, pol);
+            load_issued();
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
           if (!dep_ok) {
@@ -891,6 +955,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             uint8_t* a = smem + stage * kStageBytes;
             tma_load_2d_hint(a, tw, &full[stage], (kb0 + k) * kBK, n0, pol);
             tma_load_2d(a + kABytes, tx, &full[stage], (kb0 + k) * kBK, 0);
+            load_issued();
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
         }
@@ -933,7 +998,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
     __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------ compute
-    const int ct = threadIdx.x - 128, cw = ct >> 5;
+    const int ct = threadIdx.x - 128, cw = ct >> 5, lane = ct & 31;
     const int col = ct & (kBN - 1);      // accumulator lane (= output column) drained
     const int hf = cw >> 2;              // token half [32 hf, 32 hf + 32) drained
     uint32_t cph = 0;                    // cbar phase
@@ -971,7 +1036,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           const int rest = i / P.attn_splits;
           const long long a_c0 = clock64();
           mk_attention<HD, G>(P, F.layer, F.cs, rest / P.nkv, rest % P.nkv, split, scratch, s_rows,
-                              P.tile_ctr + F.ctr_base, ep1, P.ws, ct, s_flag, cbar, cph);
+                              P.tile_ctr + F.ctr_base, ep1, P.ws, ct, s_flag, cbar, cph, tr);
           if (tr && ct == 0 && tr[10] == 0) tr[10] = clock64() - a_c0;
         }
       } else if (F.kind == MK_SAMPLE) {
@@ -1001,11 +1066,19 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           int r0 = 0, r1 = P.S;
           if (F.kind == MK_QKV) {
             // raw split partial [split][row][col]; the attention items reduce it
-            if (tile_n * kBN + col < F.N) {
-              float* part = P.qkv_part + ((size_t)split * P.S) * P.qkv + tile_n * kBN + col;
+            const int n = tile_n * kBN + col;
+            if (n < F.N) {  // consumer layout [row][kv head][split][q heads | k | v]
+              const int hd = P.hd, qend = P.nq * hd, kend = qend + P.nkv * hd;
+              const int Wr = (P.nq / P.nkv + 2) * hd;
+              int kh, idx;
+              if (n < qend) { kh = n / hd / (P.nq / P.nkv); idx = n - kh * (P.nq / P.nkv) * hd; }
+              else if (n < kend) { kh = (n - qend) / hd; idx = (P.nq / P.nkv) * hd + (n - qend) % hd; }
+              else { kh = (n - kend) / hd; idx = (P.nq / P.nkv + 1) * hd + (n - kend) % hd; }
+              float* part = P.qkv_part + ((size_t)kh * F.cs + split) * Wr + idx;
+              const size_t rstride = (size_t)P.nkv * F.cs * Wr;
 #pragma unroll
               for (int j = 0; j < 32; ++j)
-                if (j0 + j < P.S) __stcg(&part[(size_t)(j0 + j) * P.qkv], __uint_as_float(ra[j]));
+                if (j0 + j < P.S) __stcg(&part[(size_t)(j0 + j) * rstride], __uint_as_float(ra[j]));
             }
             continue;
           }
@@ -1025,18 +1098,20 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             const int nr = r1 - r0;
             float* stage = tile + kTok * kPitch;  // [cs][nr][128]
             csync();
-            if (ct == 0) {
-              unsigned* tc = &P.tile_ctr[F.ctr_base + tile_n];
-              __threadfence();
-              atomicAdd(tc, 1u);
-              wait_count(tc, ep1 * (unsigned)F.cs);
-              if (tr && tr[2] == 0) tr[2] = globaltimer();
-              if (nr > 0) {
+            if (cw == 0) {  // warp 0: arrive, wait for the other splits, fetch the slices
+              if (lane == 0) {
+                unsigned* tc = &P.tile_ctr[F.ctr_base + tile_n];
+                __threadfence();
+                atomicAdd(tc, 1u);
+                wait_count(tc, ep1 * (unsigned)F.cs);
+                if (tr && tr[2] == 0) tr[2] = globaltimer();
+                if (nr > 0) mbar_arrive_expect_tx(cbar, (uint32_t)(F.cs * nr * kBN * 4));
+              }
+              __syncwarp();
+              if (nr > 0 && lane < F.cs) {  // one bulk copy per lane, issued in parallel
                 fence_proxy_async_global();
-                mbar_arrive_expect_tx(cbar, (uint32_t)(F.cs * nr * kBN * 4));
                 const float* src = P.ws + (size_t)tile_n * F.cs * kTileFloats + (size_t)r0 * kBN;
-                for (int q = 0; q < F.cs; ++q)
-                  bulk_g2s(stage + (size_t)q * nr * kBN, src + (size_t)q * kTileFloats, nr * kBN * 4, cbar);
+                bulk_g2s(stage + (size_t)lane * nr * kBN, src + (size_t)lane * kTileFloats, nr * kBN * 4, cbar);
               }
             }
             if (nr > 0) {

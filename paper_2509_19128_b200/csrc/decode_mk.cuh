@@ -74,11 +74,12 @@ struct MkParams {
   unsigned* epoch;              // rounds completed by this kernel (device scalar)
   unsigned* tile_ctr;           // split-K / split-KV arrival counters (monotonic)
   float* ws;                    // split-K and split-KV partials
-  float* qkv_part;              // QKV split partials [cs][S][qkv] (reduced by attention)
+  float* qkv_part;              // QKV split partials [S][nkv][cs][(G+2) hd] (reduced by attention)
   const MkPhase* phases;
   int n_phases;
   unsigned long long* stamps;   // profiling: [n_phases + 1] globaltimer (ns) or nullptr
-  int dbg;                      // experiments: bit0 skip logits store, bit1 skip LM stats
+  int dbg;                      // experiments
+  int pf_blocks;                // L2 weight prefetch distance (16 KB k-blocks per CTA)
   unsigned long long* trace;    // debugging: [n_phases][grid][8] per-CTA timestamps or nullptr
 };
 

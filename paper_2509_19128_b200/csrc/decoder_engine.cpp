@@ -327,14 +327,22 @@ int DecoderBackend::mega_init() {
     items_total += n_items;
     ph.push_back(f);
   };
+  auto cs_env = [](int kind) {  // tuning overrides: SRL_MK_CS_{QKV,O,GU,DOWN,LM}
+    static const char* names[7] = {nullptr, "SRL_MK_CS_QKV", nullptr, "SRL_MK_CS_O", "SRL_MK_CS_GU",
+                                   "SRL_MK_CS_DOWN", "SRL_MK_CS_LM"};
+    const char* v = names[kind] ? std::getenv(names[kind]) : nullptr;
+    return v ? std::max(1, std::min(16, std::atoi(v))) : 0;
+  };
   auto gemm = [&](int kind, int layer, int N, int K, int wmap, int xmap) {
-    const int cs = megakernel_splits(N, K, grid);
+    int cs = megakernel_splits(N, K, grid);
+    if (const int o = cs_env(kind)) cs = std::min(o, K / 64);
     const int tiles = (N + 127) / 128;
     ws = std::max(ws, megakernel_ws_floats(tiles * cs, cs, S_));
     add(kind, layer, tiles * cs, cs, N, K, wmap, xmap, cs > 1 ? tiles : 0);
   };
   // QKV: raw split partials only (no counters); the attention items reduce them
-  const int qkv_cs = megakernel_qkv_splits(d_, grid);
+  int qkv_cs = megakernel_qkv_splits(d_, grid);
+  if (const char* v = std::getenv("SRL_MK_CS_QKV")) qkv_cs = std::max(1, std::min(qkv_cs, std::atoi(v)));
   const int qkv_tiles = (d_.qkv() + 127) / 128;
   add(MK_EMBED, 0, S_, 1, 0, 0, 0, 0, 0);
   for (int l = 0; l < L; ++l) {
@@ -407,6 +415,8 @@ int DecoderBackend::mega_init() {
     P.n_phases = n;
     P.stamps = nullptr;
     if (const char* dbg = std::getenv("SRL_MK_DBG")) P.dbg = std::atoi(dbg);
+    P.pf_blocks = 0;  // L2 weight prefetch: off (measured slower; SRL_MK_PF_KB to experiment)
+    if (const char* pf = std::getenv("SRL_MK_PF_KB")) P.pf_blocks = std::max(0, std::atoi(pf) / 16);
   }
   mk_.stamps = reinterpret_cast<unsigned long long*>(base + o_st);
   if (std::getenv("SRL_MK_TRACE")) SRL_CUDA(cudaMalloc(&mk_.trace, 128 * (size_t)n * grid));
@@ -448,7 +458,7 @@ int DecoderBackend::mega_round(int b, bool profile) {
         const int hdr[2] = {mk_.n_phases, mk_.grid};
         std::fwrite(hdr, sizeof(hdr), 1, f);
         for (const MkPhase& f2 : mk_.phases) {
-          const int row[3] = {f2.kind, f2.cs, f2.n_items};
+          const int row[4] = {f2.kind, f2.cs, f2.n_items, f2.rot};
           std::fwrite(row, sizeof(row), 1, f);
         }
         std::fwrite(h.data(), 8, nt, f);
