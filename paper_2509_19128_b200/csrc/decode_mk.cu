@@ -39,6 +39,12 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -57,9 +63,35 @@ struct SpinGuard {
     }
   }
 };
+// Acquire-load polling (measured faster than relaxed polling + one fence).
 __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
   SpinGuard g;
   while ((int)(ld_acquire(p) - target) < 0) {
+    __nanosleep(32);
+    g.tick();
+  }
+}
+// Phase barrier: kBarLanes sub-counters per phase (CTA c arrives on c %
+// kBarLanes), a waiter sums them.  One lane measured fastest (several acquire
+// loads per poll cost more than the arrival serialisation they avoid).
+#ifndef SRL_BAR_LANES
+#define SRL_BAR_LANES 1
+#endif
+constexpr int kBarLanes = SRL_BAR_LANES;
+__device__ __forceinline__ void phase_arrive(unsigned* pd, int p, int c) {
+  atomicAdd(&pd[p * kBarLanes + (c % kBarLanes)], 1u);
+}
+__device__ __forceinline__ void phase_wait(const unsigned* pd, int p, unsigned target) {
+  SpinGuard g;
+  const unsigned* b = pd + p * kBarLanes;
+  while (true) {
+    unsigned v[kBarLanes];
+#pragma unroll
+    for (int k = 0; k < kBarLanes; ++k) v[k] = ld_acquire(b + k);
+    unsigned s = 0;
+#pragma unroll
+    for (int k = 0; k < kBarLanes; ++k) s += v[k];
+    if ((int)(s - target) >= 0) return;
     __nanosleep(32);
     g.tick();
   }
@@ -274,8 +306,9 @@ __device__ __noinline__ void mk_lm_stats(const MkParams& P, const float* tile, i
 // colv: this thread's column constant (next RMSNorm gain), loaded before the
 // accumulator wait.  QKV has no epilogue here: its split partials are
 // reduced by the attention items that consume them.
-__device__ void mk_epilogue(const MkParams& P, const MkPhase& ph, int n_tile, float* tile,
-                            const float* s_rstd, int ct, int r0, int r1, float colv) {
+__device__ __forceinline__ void mk_epilogue(const MkParams& P, const MkPhase& ph, int n_tile,
+                                            float* tile, const float* s_rstd, int ct, int r0,
+                                            int r1, float colv) {
   const int n0 = n_tile * kBN, N = ph.N, M = r1;
   const int nr = r1 - r0;
   const int cw = ct >> 5, lane = ct & 31;
@@ -940,7 +973,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
           if (!dep_ok) {
-            wait_count(&P.phase_done[p - 1], target);
+            phase_wait(P.phase_done, p - 1, target);
             fence_proxy_async_global();  // generic-proxy results -> TMA reads
             dep_ok = true;
             if (P.trace) P.trace[((size_t)p * GR + c) * 16 + 4] = globaltimer();
@@ -1011,7 +1044,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
       const MkPhase& F = P.phases[p];
       if (p > 0) {  // results of the previous phase, grid-wide
         if (ct == 0) {
-          wait_count(&P.phase_done[p - 1], target);
+          phase_wait(P.phase_done, p - 1, target);
           if (stamp) P.stamps[p] = globaltimer();
         }
         csync();
@@ -1144,12 +1177,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           tr[9] = clock64();
         }
         __threadfence();
-        atomicAdd(&P.phase_done[p], 1u);
+        phase_arrive(P.phase_done, p, c);
         if (tr) tr[7] = globaltimer();
       }
     }
     if (stamp) {
-      wait_count(&P.phase_done[P.n_phases - 1], target);
+      phase_wait(P.phase_done, P.n_phases - 1, target);
       P.stamps[P.n_phases] = globaltimer();
     }
   }

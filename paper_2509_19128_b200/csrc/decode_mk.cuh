@@ -70,7 +70,7 @@ struct MkParams {
   EventRing ring;
   int32_t* round_ctr;
   const int32_t* version;
-  unsigned* phase_done;         // [n_phases] monotonic arrival counters
+  unsigned* phase_done;         // [n_phases][8] monotonic arrival counters
   unsigned* epoch;              // rounds completed by this kernel (device scalar)
   unsigned* tile_ctr;           // split-K / split-KV arrival counters (monotonic)
   float* ws;                    // split-K and split-KV partials

@@ -359,7 +359,7 @@ int DecoderBackend::mega_init() {
   // one allocation: phases | layers | xmaps | phase_done | epoch | tile counters | stamps
   auto al = [](size_t v) { return (v + 127) / 128 * 128; };
   const size_t o_ph = 0, o_ly = al(o_ph + sizeof(MkPhase) * n), o_xm = al(o_ly + sizeof(MkLayer) * L),
-               o_pd = al(o_xm + sizeof(CUtensorMap) * 3), o_ep = al(o_pd + 4 * (size_t)n),
+               o_pd = al(o_xm + sizeof(CUtensorMap) * 3), o_ep = al(o_pd + 4 * 8 * (size_t)n)  /* room for 8 barrier lanes */,
                o_tc = al(o_ep + 4), o_st = al(o_tc + 4 * (size_t)std::max(ctr, 1)),
                total = al(o_st + 8 * (size_t)(n + 1));
   SRL_CUDA(cudaMalloc(&mk_.mem, total));
