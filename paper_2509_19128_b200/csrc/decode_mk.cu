@@ -44,6 +44,14 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
 __device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -348,12 +356,15 @@ __device__ __forceinline__ void mk_epilogue(const MkParams& P, const MkPhase& ph
       if (lane == 0) P.ssq[(size_t)j * P.parts + n_tile] = s;
     }
   } else if (ph.kind == MK_GU) {
-#pragma unroll 4
-    for (int idx = ct; idx < nr * (kBN / 2); idx += kCT) {
-      const int j = r0 + (idx >> 6), c = idx & 63;
-      const float g = tile[j * kPitch + c] * s_rstd[j];
-      const float u = tile[j * kPitch + 64 + c] * s_rstd[j];
-      P.act[(size_t)j * P.I + (n0 >> 1) + c] = __float2bfloat16(g / (1.f + expf(-g)) * u);
+#pragma unroll 2
+    for (int idx = ct; idx < nr * (kBN / 4); idx += kCT) {  // two columns per thread
+      const int j = r0 + (idx >> 5), c = (idx & 31) * 2;
+      const float r = s_rstd[j];
+      const float2 g2 = *reinterpret_cast<const float2*>(&tile[j * kPitch + c]);
+      const float2 u2 = *reinterpret_cast<const float2*>(&tile[j * kPitch + 64 + c]);
+      const float g0 = g2.x * r, g1 = g2.y * r, u0 = u2.x * r, u1 = u2.y * r;
+      *reinterpret_cast<__nv_bfloat162*>(&P.act[(size_t)j * P.I + (n0 >> 1) + c]) =
+          __floats2bfloat162_rn(g0 / (1.f + expf(-g0)) * u0, g1 / (1.f + expf(-g1)) * u1);
     }
   } else if (ph.kind == MK_LM) {
     // scale by rstd and store the logits (one float4 per thread per row), keep
@@ -903,6 +914,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
   uint64_t* cbar = tempty + 2;  // compute warps' bulk-copy barrier
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Lo::misc);
   int* s_flag = reinterpret_cast<int*>(smem + Lo::misc + 4);
+  int* s_seen = reinterpret_cast<int*>(smem + Lo::misc + 8);  // last phase seen complete
   float* s_rstd = reinterpret_cast<float*>(smem + Lo::rstd);
   int2* s_rows = reinterpret_cast<int2*>(smem + Lo::rows);
 
@@ -911,6 +923,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
   const unsigned ep1 = *P.epoch + 1u;
   const unsigned target = ep1 * (unsigned)GR;
 
+  if (threadIdx.x == 64) *s_seen = 0;
   if (warp == 0) {
     tmem_alloc<128>(tmem_slot);  // two 64-column fp32 accumulators
   } else if (warp == 1) {
@@ -939,23 +952,34 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t ph = 0;
-      WeightCursor pf;  // L2 prefetch stream, pf_blocks k-blocks ahead of the loads
-      pf.start(P, c, GR);
-      int ahead = 0;
-      auto load_issued = [&]() {
-        --ahead;
-        while (pf.live && ahead < P.pf_blocks) {
-          pf.prefetch(P);
-          pf.next(P, c, GR);
-          ++ahead;
+      // Targeted L2 prefetch (SRL_MK_PF=1): when a GEMM phase starts, the
+      // k-blocks of the next GEMM phase's items that the shared-memory ring
+      // cannot hold are pulled into L2, so they stream at L2 rather than HBM
+      // latency once that phase's barrier opens.  (LM head: first item only.)
+      auto prefetch_next_gemm = [&](int p0) {
+        for (int q = p0 + 1; q < P.n_phases; ++q) {
+          const MkPhase& Q = P.phases[q];
+          if (!is_gemm(Q.kind)) continue;
+          const int kbt = Q.K / kBK;
+          int n_items = 0;
+          for (int i = first_item(c, Q.rot, GR); i < Q.n_items; i += GR) {
+            const int split = i % Q.cs;
+            const int kb0 = (split * kbt) / Q.cs, nkb = ((split + 1) * kbt) / Q.cs - kb0;
+            for (int k = (n_items == 0 ? STAGES : 0); k < nkb; ++k)
+              tma_prefetch_l2(&P.wmaps[Q.wmap], (kb0 + k) * kBK, (i / Q.cs) * kBN);
+            if (Q.kind == MK_LM && ++n_items >= 1) break;
+            ++n_items;
+          }
+          return;
         }
       };
-      load_issued();
+      auto load_issued = [&]() {};
       for (int p = 0; p < P.n_phases; ++p) {
         const MkPhase& F = P.phases[p];
         if (F.kind == MK_EMBED || F.kind == MK_ATTN || F.kind == MK_SAMPLE) continue;
         const CUtensorMap* tw = &P.wmaps[F.wmap];
         const CUtensorMap* tx = &P.xmaps[F.xmap];
+        if (P.pf_blocks > 0) prefetch_next_gemm(p);
         bool dep_ok = false;
         const int kb_total = F.K / kBK;
         for (int i = first_item(c, F.rot, GR); i < F.n_items; i += GR) {
@@ -973,7 +997,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
           if (!dep_ok) {
-            phase_wait(P.phase_done, p - 1, target);
+            // the compute warps' poller publishes each completed phase here
+            // (one global poller per CTA)
+            {
+              SpinGuard g;
+              while (ld_acquire_cta(s_seen) < p) g.tick();
+            }
             fence_proxy_async_global();  // generic-proxy results -> TMA reads
             dep_ok = true;
             if (P.trace) P.trace[((size_t)p * GR + c) * 16 + 4] = globaltimer();
@@ -1045,6 +1074,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
       if (p > 0) {  // results of the previous phase, grid-wide
         if (ct == 0) {
           phase_wait(P.phase_done, p - 1, target);
+          st_release_cta(s_seen, p);
           if (stamp) P.stamps[p] = globaltimer();
         }
         csync();
