@@ -120,7 +120,7 @@ __device__ __forceinline__ void mk_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try(bar, parity)) g.tick();
 }
 // first item of CTA c in a phase whose items are dealt round-robin from `rot`
-__device__ __forceinline__ int first_item(int c, int rot, int G) { return ((c - rot) % G + G) % G; }
+__device__ __forceinline__ int first_item(int c, int rot, int G) { return c >= rot ? c - rot : c - rot + G; }
 
 // L2 prefetch of one weight tile (no shared memory, no completion).
 __device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* m, int32_t c0, int32_t c1) {
@@ -132,47 +132,6 @@ __device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* m, int32_t c0
 __device__ __forceinline__ bool is_gemm(int kind) {
   return kind == MK_QKV || kind == MK_O || kind == MK_GU || kind == MK_DOWN || kind == MK_LM;
 }
-
-// Walks this CTA's weight k-blocks in the producer's load order (phase, item,
-// k-block); the L2 prefetch stream runs a bounded distance ahead of the loads.
-struct WeightCursor {
-  int p = 0, i = 0, k = 0, kb0 = 0, nkb = 0;
-  bool live = false;
-  __device__ bool enter_item(const MkParams& P, int GR) {  // (p, i) valid -> k range
-    const MkPhase& F = P.phases[p];
-    const int kbt = F.K / 64, split = i % F.cs;
-    kb0 = (split * kbt) / F.cs;
-    nkb = ((split + 1) * kbt) / F.cs - kb0;
-    k = 0;
-    (void)GR;
-    return nkb > 0;
-  }
-  __device__ bool seek_phase(const MkParams& P, int c, int GR) {  // from phase p on
-    for (; p < P.n_phases; ++p) {
-      const MkPhase& F = P.phases[p];
-      if (!is_gemm(F.kind)) continue;
-      i = first_item(c, F.rot, GR);
-      if (i < F.n_items && enter_item(P, GR)) return live = true;
-    }
-    return live = false;
-  }
-  __device__ void start(const MkParams& P, int c, int GR) {
-    p = 0;
-    seek_phase(P, c, GR);
-  }
-  __device__ void next(const MkParams& P, int c, int GR) {
-    if (++k < nkb) return;
-    const MkPhase& F = P.phases[p];
-    for (i += GR; i < F.n_items; i += GR)
-      if (enter_item(P, GR)) return;
-    ++p;
-    seek_phase(P, c, GR);
-  }
-  __device__ void prefetch(const MkParams& P) const {
-    const MkPhase& F = P.phases[p];
-    tma_prefetch_l2(&P.wmaps[F.wmap], (kb0 + k) * 64, (i / F.cs) * 128);
-  }
-};
 
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -281,23 +240,24 @@ __device__ __noinline__ void mk_lm_stats(const MkParams& P, const float* tile, i
   const int j = r0 + (ct >> 2), part = ct & 3;
   const bool valid = j < r1;  // converged shuffles: invalid quads recompute row r0
   const float* row = &tile[(valid ? j : r0) * kPitch + part * 32];
-  float4 v[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) v[q] = *reinterpret_cast<const float4*>(row + 4 * q);
   float mx = -INFINITY;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) mx = fmaxf(mx, fmaxf(fmaxf(v[q].x, v[q].y), fmaxf(v[q].z, v[q].w)));
+  for (int q = 0; q < 8; ++q) {
+    const float4 v = *reinterpret_cast<const float4*>(row + 4 * q);
+    mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+  }
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
   mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
   double a[4] = {0.0, 0.0, 0.0, 0.0};
   if (mx != -INFINITY) {
     const double md = (double)mx;
-#pragma unroll
+#pragma unroll 2
     for (int q = 0; q < 8; ++q) {
-      a[0] += exp_nonpos((double)v[q].x - md);
-      a[1] += exp_nonpos((double)v[q].y - md);
-      a[2] += exp_nonpos((double)v[q].z - md);
-      a[3] += exp_nonpos((double)v[q].w - md);
+      const float4 v = *reinterpret_cast<const float4*>(row + 4 * q);
+      a[0] += exp_nonpos((double)v.x - md);
+      a[1] += exp_nonpos((double)v.y - md);
+      a[2] += exp_nonpos((double)v.z - md);
+      a[3] += exp_nonpos((double)v.w - md);
     }
   }
   double sm = (a[0] + a[1]) + (a[2] + a[3]);
@@ -481,6 +441,7 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
     const int idx = ct + u * kCT;
     if (idx < W) {
       float v = 0.f;
+#pragma unroll 1
       for (int q = 0; q < qkv_cs; ++q) v += stage[q * W + idx];
       sraw[idx] = v * rstd + bia[u];
     }
@@ -722,14 +683,19 @@ __device__ void mk_embed(const MkParams& P, int m, int ct, float* red) {
   csync();
 }
 
-// Sampling of slot s from the LM-head tile partials (same algorithm as
-// sample_row in decoder.cu, 256 threads): lse from the tile (max, sum)
-// pairs, then the tile walk of the inverse CDF.
-__device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
-  double* scan = reinterpret_cast<double*>(scr);
-  double* red = scan + kCT;
-  int* iv = reinterpret_cast<int*>(red + 16);
-  float* fv = reinterpret_cast<float*>(iv + 16);
+// Sampling of slot s from the LM-head tile partials (256 threads): the tile
+// (max, sum) pairs of the row are loaded once into registers; lse; then the
+// inverse CDF: tile masses, block exclusive scan (warp shuffles), first tile
+// whose range may hold u (1e-12 margin), and warp 0 walks that tile element
+// by element in fp64 (the sampler of decoder.cu, same numerics class).
+constexpr int kSampleC = 8;  // tiles per thread held in registers (V <= 262144)
+__device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr, unsigned long long* tr) {
+  const long long c0 = clock64();
+  auto stampc = [&](int k) { if (tr && ct == 0 && tr[k] == 0) tr[k] = clock64() - c0; };
+  double* wtot = reinterpret_cast<double*>(scr);  // [kCW]
+  double* red = wtot + kCW;                       // [kCW]
+  int* iv = reinterpret_cast<int*>(red + kCW);    // [kCW + 1]
+  float* fv = reinterpret_cast<float*>(iv + kCW + 2);
   const int warp = ct >> 5, lane = ct & 31;
   const int V = P.V;
   const int ri = (*P.round_ctr - 1) % P.ring.rounds;
@@ -747,16 +713,27 @@ __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
   }
   const float* x = P.logits + (size_t)s * V;
   const int T = (V + kLmTile - 1) / kLmTile;
-  const float* pmax = P.lse_max + (size_t)s * T;
-  const double* psum = P.lse_sum + (size_t)s * T;
-  const int C = (T + kCT - 1) / kCT;
+  const int C = (T + kCT - 1) / kCT;  // <= kSampleC
   const int t0 = ct * C, t1 = min(T, t0 + C);
+  float pm[kSampleC];
+  double ps[kSampleC];
+#pragma unroll
+  for (int q = 0; q < kSampleC; ++q) {
+    const bool ok = q < C && t0 + q < t1;
+    pm[q] = ok ? P.lse_max[(size_t)s * T + t0 + q] : -INFINITY;
+    ps[q] = ok ? P.lse_sum[(size_t)s * T + t0 + q] : 0.0;
+  }
+  const uint64_t seed = P.ss.seed[s];
+  const int gen0 = P.ss.gen_count[s];
+  // the event's scalars, loaded now (off the critical path)
+  const int pos_row = P.plan.row_pos[r];
+  const int term = P.ss.terminator[s], maxtok = P.ss.max_tokens[s], ver = *P.version;
+  stampc(10);
   float mx = -INFINITY;
   int mt = 0x7fffffff;
-  for (int t = t0; t < t1; ++t) {
-    const float v = pmax[t];
-    if (v > mx) { mx = v; mt = t; }
-  }
+#pragma unroll
+  for (int q = 0; q < kSampleC; ++q)
+    if (pm[q] > mx) { mx = pm[q]; mt = t0 + q; }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float om = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -765,24 +742,26 @@ __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
   }
   if (lane == 0) { fv[warp] = mx; iv[warp] = mt; }
   csync();
-  if (ct == 0) {
-    for (int w = 1; w < kCW; ++w)
-      if (fv[w] > fv[0] || (fv[w] == fv[0] && iv[w] < iv[0])) { fv[0] = fv[w]; iv[0] = iv[w]; }
-  }
-  csync();
-  const float Mf = fv[0];
+  float Mf = fv[0];
+  int mtile = iv[0];
+  for (int w = 1; w < kCW; ++w)
+    if (fv[w] > Mf || (fv[w] == Mf && iv[w] < mtile)) { Mf = fv[w]; mtile = iv[w]; }
   const double M = (double)Mf;
-  const int mtile = iv[0];
   double part = 0.0;
-  for (int t = t0; t < t1; ++t) part += psum[t] * exp((double)pmax[t] - M);
+  double em[kSampleC];  // s_t * exp(m_t - M): reused for the tile masses
+#pragma unroll
+  for (int q = 0; q < kSampleC; ++q) {
+    em[q] = ps[q] * exp_nonpos_call((double)pm[q] - M);
+    part += em[q];
+  }
   part = wsum_d(part);
   if (lane == 0) red[warp] = part;
   csync();
   double tot = 0.0;
   for (int w = 0; w < kCW; ++w) tot += red[w];
   const double lse = M + log(tot);
-  csync();
-  const double u = uniform_draw(P.ss.seed[s], (uint64_t)P.ss.gen_count[s]);
+  const double u = uniform_draw(seed, (uint64_t)gen0);
+  stampc(11);
   int tok;
   if (P.greedy) {
     if (warp == 0) {
@@ -798,39 +777,57 @@ __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
     csync();
     tok = iv[kCW];
   } else {
-    double mass = 0.0;
-    for (int t = t0; t < t1; ++t) mass += psum[t] * exp((double)pmax[t] - lse);
-    scan[ct] = mass;
-    csync();
-    for (int o = 1; o < kCT; o <<= 1) {
-      const double add = ct >= o ? scan[ct - o] : 0.0;
-      csync();
-      scan[ct] += add;
-      csync();
+    double mass[kSampleC];
+    double mine = 0.0;
+    const double scale = exp_nonpos_call(M - lse);  // tile mass = s_t exp(m_t - M) exp(M - lse)
+#pragma unroll
+    for (int q = 0; q < kSampleC; ++q) {
+      mass[q] = em[q] * scale;
+      mine += mass[q];
     }
+    // exclusive scan of the threads' masses: warp shuffles, then warp totals
+    double incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double n = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += n;
+    }
+    if (lane == 31) wtot[warp] = incl;
+    csync();
+    double off = 0.0;
+    for (int w = 0; w < warp; ++w) off += wtot[w];
+    const double excl = off + (incl - mine);
     int cand = 0x7fffffff;
-    {
-      double base = ct == 0 ? 0.0 : scan[ct - 1];
-      if (u < scan[ct] + 1e-12) {
-        for (int t = t0; t < t1; ++t) {
-          const double q = psum[t] * exp((double)pmax[t] - lse);
-          if (u < base + q + 1e-12) { cand = t; break; }
-          base += q;
+    if (u < excl + mine + 1e-12) {
+      double base = excl;
+#pragma unroll
+      for (int q = 0; q < kSampleC; ++q) {
+        if (cand == 0x7fffffff && t0 + q < t1) {
+          if (u < base + mass[q] + 1e-12) cand = t0 + q;
+          base += mass[q];
         }
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
     if (lane == 0) iv[warp] = cand;
+    // the candidate's base: the owner thread's exclusive prefix + its earlier tiles
     csync();
+    int t = 0x7fffffff;
+    for (int w = 0; w < kCW; ++w) t = min(t, iv[w]);
+    if (t != 0x7fffffff && ct == t / C) {
+      double base = excl;
+#pragma unroll
+      for (int q = 0; q < kSampleC; ++q)
+        if (t0 + q < t) base += mass[q];
+      red[0] = base;
+    }
+    csync();
+    stampc(12);
     if (warp == 0) {
-      int t = 0x7fffffff;
-      for (int w = 0; w < kCW; ++w) t = min(t, iv[w]);
       int tk = V - 1;
       if (t != 0x7fffffff) {
-        const int owner = t / C;
-        double base = owner == 0 ? 0.0 : scan[owner - 1];
-        for (int tt = owner * C; tt < t; ++tt) base += psum[tt] * exp((double)pmax[tt] - lse);
+        double base = red[0];
         bool done = false;
         for (; t < T && !done; ++t) {
           double p[4];
@@ -838,16 +835,16 @@ __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int k = t * kLmTile + lane * 4 + i;
-            p[i] = k < V ? exp((double)x[k] - lse) : 0.0;
+            p[i] = k < V ? exp_nonpos_call((double)x[k] - lse) : 0.0;
             ls += p[i];
           }
-          double incl = ls;
+          double in2 = ls;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
-            const double n = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += n;
+            const double n = __shfl_up_sync(0xffffffffu, in2, o);
+            if (lane >= o) in2 += n;
           }
-          double cum = base + (incl - ls);
+          double cum = base + (in2 - ls);
           int found = 0x7fffffff;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -861,7 +858,7 @@ __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
             tk = found;
             done = true;
           }
-          base += __shfl_sync(0xffffffffu, incl, 31);
+          base += __shfl_sync(0xffffffffu, in2, 31);
         }
       }
       if (lane == 0) iv[kCW] = tk;
@@ -869,19 +866,19 @@ __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
     csync();
     tok = iv[kCW];
   }
+  stampc(13);
   if (ct == 0) {
-    const int pos_row = P.plan.row_pos[r];
     const int new_len = pos_row + 1;
-    const int gen = P.ss.gen_count[s];
+    const int gen = gen0;
     int flag = 1;
-    if (tok == P.ss.terminator[s]) flag = 3;
-    else if (gen + 1 >= P.ss.max_tokens[s]) flag = 2;
+    if (tok == term) flag = 3;
+    else if (gen + 1 >= maxtok) flag = 2;
     else if (new_len + 1 > P.ss.max_seq) flag = 2;
     DevEvent e;
     e.flag = flag;
     e.token = tok;
     e.position = gen;
-    e.version = *P.version;
+    e.version = ver;
     e.logprob = (double)x[tok] - lse;
     P.ring.ev[ev] = e;
     P.ss.seq_len[s] = new_len;
@@ -895,6 +892,7 @@ __device__ void mk_sample(const MkParams& P, int s, int ct, uint8_t* scr) {
     P.next.last_row[s] = alive ? s : -1;
   }
   csync();
+  stampc(14);
 }
 
 // ------------------------------------------------------------ kernel ---
@@ -952,34 +950,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t ph = 0;
-      // Targeted L2 prefetch (SRL_MK_PF=1): when a GEMM phase starts, the
-      // k-blocks of the next GEMM phase's items that the shared-memory ring
-      // cannot hold are pulled into L2, so they stream at L2 rather than HBM
-      // latency once that phase's barrier opens.  (LM head: first item only.)
-      auto prefetch_next_gemm = [&](int p0) {
-        for (int q = p0 + 1; q < P.n_phases; ++q) {
-          const MkPhase& Q = P.phases[q];
-          if (!is_gemm(Q.kind)) continue;
-          const int kbt = Q.K / kBK;
-          int n_items = 0;
-          for (int i = first_item(c, Q.rot, GR); i < Q.n_items; i += GR) {
-            const int split = i % Q.cs;
-            const int kb0 = (split * kbt) / Q.cs, nkb = ((split + 1) * kbt) / Q.cs - kb0;
-            for (int k = (n_items == 0 ? STAGES : 0); k < nkb; ++k)
-              tma_prefetch_l2(&P.wmaps[Q.wmap], (kb0 + k) * kBK, (i / Q.cs) * kBN);
-            if (Q.kind == MK_LM && ++n_items >= 1) break;
-            ++n_items;
-          }
-          return;
-        }
-      };
-      auto load_issued = [&]() {};
       for (int p = 0; p < P.n_phases; ++p) {
         const MkPhase& F = P.phases[p];
         if (F.kind == MK_EMBED || F.kind == MK_ATTN || F.kind == MK_SAMPLE) continue;
         const CUtensorMap* tw = &P.wmaps[F.wmap];
         const CUtensorMap* tx = &P.xmaps[F.xmap];
-        if (P.pf_blocks > 0) prefetch_next_gemm(p);
         bool dep_ok = false;
         const int kb_total = F.K / kBK;
         for (int i = first_item(c, F.rot, GR); i < F.n_items; i += GR) {
@@ -993,7 +968,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             mk_wait(&empty[stage], ph ^ 1);
             mbar_arrive_expect_tx(&full[stage], kStageBytes);
             tma_load_2d_hint(smem + stage * kStageBytes, tw, &full[stage], (kb0 + k) * kBK, n0, pol);
-            load_issued();
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
           if (!dep_ok) {
@@ -1017,7 +991,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             uint8_t* a = smem + stage * kStageBytes;
             tma_load_2d_hint(a, tw, &full[stage], (kb0 + k) * kBK, n0, pol);
             tma_load_2d(a + kABytes, tx, &full[stage], (kb0 + k) * kBK, 0);
-            load_issued();
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
         }
@@ -1103,7 +1076,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           if (tr && ct == 0 && tr[10] == 0) tr[10] = clock64() - a_c0;
         }
       } else if (F.kind == MK_SAMPLE) {
-        for (int s = first_item(c, F.rot, GR); s < F.n_items; s += GR) mk_sample(P, s, ct, scratch);
+        for (int s = first_item(c, F.rot, GR); s < F.n_items; s += GR) mk_sample(P, s, ct, scratch, tr);
       } else {
         mk_rows(P, F.kind, s_rstd, ct);
         for (int i = first_item(c, F.rot, GR); i < F.n_items; i += GR) {
@@ -1137,11 +1110,14 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
               if (n < qend) { kh = n / hd / (P.nq / P.nkv); idx = n - kh * (P.nq / P.nkv) * hd; }
               else if (n < kend) { kh = (n - qend) / hd; idx = (P.nq / P.nkv) * hd + (n - qend) % hd; }
               else { kh = (n - kend) / hd; idx = (P.nq / P.nkv + 1) * hd + (n - kend) % hd; }
-              float* part = P.qkv_part + ((size_t)kh * F.cs + split) * Wr + idx;
               const size_t rstride = (size_t)P.nkv * F.cs * Wr;
+              float* ptr = P.qkv_part + ((size_t)kh * F.cs + split) * Wr + idx + (size_t)j0 * rstride;
+              const int nj = min(32, P.S - j0);
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (j0 + j < P.S) __stcg(&part[(size_t)(j0 + j) * rstride], __uint_as_float(ra[j]));
+              for (int j = 0; j < 32; ++j) {
+                if (j < nj) __stcg(ptr, __uint_as_float(ra[j]));
+                ptr += rstride;
+              }
             }
             continue;
           }
@@ -1297,6 +1273,7 @@ size_t megakernel_ws_floats(int n_items, int cs, int rows) {
 
 bool megakernel_supported(const DecoderDims& d, int slots) {
   if (slots > kTok || d.nq % d.nkv) return false;
+  if ((d.V + kLmTile - 1) / kLmTile > kSampleC * kCT) return false;  // sampler registers
   const int G = d.nq / d.nkv;
   if (d.hd == 64) return G == 2 || G == 7;
   if (d.hd == 128) return G == 6 || G == 7;

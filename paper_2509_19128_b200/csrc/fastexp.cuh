@@ -33,4 +33,7 @@ __device__ __forceinline__ double exp_nonpos(double d) {
   return d < -700.0 ? 0.0 : p * scale;
 }
 
+// Out-of-line copy for cold code (keeps the instruction footprint small).
+__device__ __noinline__ double exp_nonpos_call(double d) { return exp_nonpos(d); }
+
 }  // namespace srl
