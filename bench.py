@@ -134,7 +134,9 @@ def algorithmic_bytes(cfg, rows, ctx_sum):
     b["gate_up_gemm"] = L * (2 * I * H * 2 + rows * H * 2 + rows * I * 2)
     b["down_gemm"] = L * (H * I * 2 + rows * I * 2 + rows * H * (4 + 4 + 2))
     b["lm_head_gemm"] = V * H * 2 + rows * H * 2 + rows * V * 4
-    b["sample"] = rows * V * 4
+    # the sampler reads the LM-head epilogue's per-(row, 128-column tile)
+    # (max, fp64 sum) statistics and walks one tile of the row
+    b["sample"] = rows * (((V + 127) // 128) * 12 + 128 * 4)
     b["plan"] = rows * 16
     return b
 
@@ -315,6 +317,13 @@ def main():
     eng.profile_next_round()
     eng.advance(2)  # a pending refill prefill may take the first round; the next decode round is profiled
     prof = eng.kernel_profile()
+    fused_ms = []
+    if "decode_megakernel" in prof:  # average the one-launch round over a few more rounds
+        fused_ms.append(prof["decode_megakernel"][0])
+        for _ in range(7):
+            eng.profile_next_round()
+            eng.advance(1)
+            fused_ms.append(eng.kernel_profile()["decode_megakernel"][0])
     ctx_now = [len(eng.stream_tokens(sid)) for sid in live]
     # drain the profiled round's events so the actor stays consistent
     for sid in list(live):
@@ -366,22 +375,35 @@ def main():
         lag = {"max_lag_steps": int(tt[2]), "mean_lag_steps": tt[1] / max(tt[0], 1),
                "sequences": len(seqs), "finished_sequences": len(token_versions)}
 
-    # roofline of the dominant kernel class (profiled round)
+    # roofline of the dominant kernel (profiled rounds)
     hbm, bf16, peak_kind = load_peaks()
     abytes = algorithmic_bytes(cfg, B, sum(ctx_now))
-    cls_ms = {k: prof[k][0] for k in KERNEL_CLASSES}
-    dom = max(cls_ms, key=cls_ms.get)
-    round_ms = sum(cls_ms.values())
-    traffic = load_traffic().get(args.config, {}).get(dom)
-    nlaunch = max(prof[dom][1], 1)
-    roof = {"kernel": dom, "bound": "hbm", "achieved": abytes[dom] / (cls_ms[dom] * 1e-3) / 1e9,
-            "peak": hbm, "unit": "GB/s", "peak_kind": peak_kind,
-            "traffic": traffic, "launches_per_round": prof[dom][1],
-            "bytes_per_launch": abytes[dom] / nlaunch, "ms_per_launch": cls_ms[dom] / nlaunch}
-    roof["frac"] = roof["achieved"] / roof["peak"]
     step_bytes = sum(abytes.values())
+    cls_ms = {k: prof[k][0] for k in KERNEL_CLASSES}
+    traffic_db = load_traffic().get(args.config, {})
+    if fused_ms:
+        # the whole round is ONE persistent kernel: its algorithmic bytes are
+        # the round's, its duration the CUDA-event time of the launch
+        mk_ms = float(np.mean(fused_ms))
+        roof = {"kernel": "decode_megakernel", "bound": "hbm",
+                "achieved": step_bytes / (mk_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                "peak_kind": peak_kind, "traffic": traffic_db.get("decode_megakernel"),
+                "launches_per_round": 1, "bytes_per_launch": step_bytes, "ms_per_launch": mk_ms,
+                "ms_per_launch_samples": len(fused_ms),
+                "phase_ms_per_round": {k: round(v, 4) for k, v in cls_ms.items()}}
+        round_ms = mk_ms
+    else:
+        dom = max(cls_ms, key=cls_ms.get)
+        round_ms = sum(cls_ms.values())
+        nlaunch = max(prof[dom][1], 1)
+        roof = {"kernel": dom, "bound": "hbm", "achieved": abytes[dom] / (cls_ms[dom] * 1e-3) / 1e9,
+                "peak": hbm, "unit": "GB/s", "peak_kind": peak_kind,
+                "traffic": traffic_db.get(dom), "launches_per_round": prof[dom][1],
+                "bytes_per_launch": abytes[dom] / nlaunch, "ms_per_launch": cls_ms[dom] / nlaunch}
+    roof["frac"] = roof["achieved"] / roof["peak"]
     round_roof = {"bound": "hbm", "achieved": step_bytes / (round_ms * 1e-3) / 1e9, "peak": hbm,
-                  "unit": "GB/s", "bytes": step_bytes, "ms": round_ms}
+                  "unit": "GB/s", "bytes": step_bytes, "ms": round_ms,
+                  "bytes_by_class": {k: int(v) for k, v in abytes.items()}}
     round_roof["frac"] = round_roof["achieved"] / hbm
     roofline_tps = B / (step_bytes / (hbm * 1e9))
 
@@ -412,6 +434,7 @@ def main():
         "round_roofline": round_roof,
         "roofline_tokens_per_s": roofline_tps,
         "kernel_ms_per_round": {k: round(v, 4) for k, v in cls_ms.items()},
+        "update_gbs": pol.weights()[1] / (float(np.median(upd)) * 1e-3) / 1e9,
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -205,6 +205,11 @@ typedef struct {
   int32_t launches[SRL_KERNEL_CLASSES];
   int32_t valid;
   int32_t rows;
+  /* 1 when the round ran as the persistent megakernel: ms[] then holds the
+   * grid-wide phase durations (globaltimer stamps) per class and fused_ms the
+   * CUDA-event time of the one launch. */
+  int32_t fused;
+  double fused_ms;
 } srl_kernel_profile;
 int srl_engine_profile_next_round(srl_engine* e);
 int srl_engine_kernel_profile(const srl_engine* e, srl_kernel_profile* out);

@@ -70,7 +70,8 @@ class TrainerStatsC(C.Structure):
 
 
 class KernelProfileC(C.Structure):
-    _fields_ = [("ms", f64 * 10), ("launches", i32 * 10), ("valid", i32), ("rows", i32)]
+    _fields_ = [("ms", f64 * 10), ("launches", i32 * 10), ("valid", i32), ("rows", i32),
+                ("fused", i32), ("fused_ms", f64)]
 
 
 KERNEL_CLASSES = ["plan", "embed", "qkv_gemm", "rope_kv_append", "attention", "o_gemm",

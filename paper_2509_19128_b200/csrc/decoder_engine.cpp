@@ -246,6 +246,8 @@ DecoderBackend::~DecoderBackend() {
   if (pinned_) cudaFreeHost(pinned_);
   if (ev_start_) cudaEventDestroy(ev_start_);
   if (ev_stop_) cudaEventDestroy(ev_stop_);
+  for (cudaEvent_t& ev : ev_prof_)
+    if (ev) cudaEventDestroy(ev);
   runner_.reset();
   if (st_) cudaStreamDestroy(st_);
 }
@@ -255,6 +257,7 @@ int DecoderBackend::init(const Policy& p) {
   SRL_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   SRL_CUDA(cudaEventCreate(&ev_start_));
   SRL_CUDA(cudaEventCreate(&ev_stop_));
+  for (cudaEvent_t& ev : ev_prof_) SRL_CUDA(cudaEventCreate(&ev));
   const DecoderWeights& src = *p.dec;
   d_ = src.dims;
   S_ = std::max(1, opts_.max_streams);
@@ -434,9 +437,11 @@ int DecoderBackend::mega_round(int b, bool profile) {
     p.trace = mk_.trace;
     SRL_CUDA(cudaMemsetAsync(mk_.trace, 0, 128 * (size_t)mk_.n_phases * mk_.grid, st_));
   }
+  if (profile) SRL_CUDA(cudaEventRecord(ev_prof_[0], st_));
   const cudaError_t e = launch_megakernel(p, d_, mk_.grid, st_);
   if (e != cudaSuccess) return cuda_fail(e, "launch_megakernel");
   if (profile) {
+    SRL_CUDA(cudaEventRecord(ev_prof_[1], st_));
     SRL_CUDA(cudaMemcpyAsync(mk_.stamps_host, mk_.stamps, 8 * (size_t)(mk_.n_phases + 1),
                              cudaMemcpyDeviceToHost, st_));
     SRL_CUDA(cudaStreamSynchronize(st_));
@@ -450,6 +455,10 @@ int DecoderBackend::mega_round(int b, bool profile) {
     }
     profile_.valid = 1;
     profile_.rows = S_;
+    profile_.fused = 1;
+    float fms = 0.f;
+    SRL_CUDA(cudaEventElapsedTime(&fms, ev_prof_[0], ev_prof_[1]));
+    profile_.fused_ms = fms;
     if (mk_.trace) {  // debugging dump: kind, cs, n_items per phase then the raw stamps
       const size_t nt = 16 * (size_t)mk_.n_phases * mk_.grid;
       std::vector<unsigned long long> h(nt);

@@ -120,6 +120,7 @@ class DecoderBackend final : public Backend {
   cudaStream_t st_ = nullptr;
   cudaGraphExec_t exec_[2] = {nullptr, nullptr};
   cudaEvent_t ev_start_ = nullptr, ev_stop_ = nullptr;
+  cudaEvent_t ev_prof_[2] = {nullptr, nullptr};  // around a profiled megakernel launch
   void* dev_state_ = nullptr;
   void* pinned_ = nullptr;
   size_t pinned_bytes_ = 0;

@@ -220,7 +220,10 @@ class Engine:
     def kernel_profile(self) -> dict:
         p = _lib.KernelProfileC()
         _raise_for(_lib.lib().srl_engine_kernel_profile(self._h, C.byref(p)), "kernel_profile")
-        return {name: (p.ms[i], p.launches[i]) for i, name in enumerate(_lib.KERNEL_CLASSES)}
+        out = {name: (p.ms[i], p.launches[i]) for i, name in enumerate(_lib.KERNEL_CLASSES)}
+        if p.fused:  # the round ran as the persistent megakernel (one launch)
+            out["decode_megakernel"] = (p.fused_ms, 1)
+        return out
 
     def close(self):
         if getattr(self, "_h", None):

@@ -1,0 +1,113 @@
+#!/usr/bin/env python
+"""Probe + timeline analysis of the persistent decode megakernel.
+
+Runs the bench workload (Qwen2.5-0.5B shape, batch 64) for a few rounds,
+profiles one decode round with SRL_MK_TRACE (per-CTA, per-phase globaltimer
+stamps written by decode_megakernel) and prints, per phase kind, where the
+time goes: barrier propagation (last arrival of the previous phase -> median
+CTA start), the activation dependency seen by the TMA producer, the first
+accumulator, split-K exchange, epilogue, and the phase period.
+
+  python tools/mk_trace.py [--config qwen2.5-0.5b] [--batch 64] [--rounds 40]
+"""
+import argparse
+import os
+import struct
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+KINDS = ["embed", "qkv", "attn", "o", "gu", "down", "lm", "sample"]
+
+
+def load(path):
+    b = Path(path).read_bytes()
+    n, grid = struct.unpack_from("ii", b, 0)
+    meta = np.frombuffer(b, dtype=np.int32, count=4 * n, offset=8).reshape(n, 4)
+    tr = np.frombuffer(b, dtype=np.uint64, offset=8 + 16 * n).reshape(n, grid, 16).astype(np.int64)
+    return meta, tr
+
+
+def analyse(meta, tr):
+    n, grid, _ = tr.shape
+    t0 = tr[:, :, 0]
+    base = t0[0].min()
+    rows = []
+    prev_last = None
+    for p in range(n):
+        kind = KINDS[meta[p, 0]]
+        active = tr[p, :, 7] > 0
+        st = t0[p][active] - base
+        arr = tr[p, :, 7][active] - base
+        last = arr.max()
+        r = dict(p=p, kind=kind, cs=int(meta[p, 1]), items=int(meta[p, 2]),
+                 start_med=np.median(st), start_max=st.max(), last=last,
+                 work_med=np.median(tr[p, :, 3][active] - t0[p][active]),
+                 work_max=(tr[p, :, 3][active] - t0[p][active]).max())
+        r["bar"] = (np.median(st) - prev_last) if prev_last is not None else 0.0
+        r["period"] = last - prev_last if prev_last is not None else last
+        for k, name in [(4, "dep"), (1, "acc"), (2, "xchg"), (5, "red"), (6, "epi")]:
+            v = tr[p, :, k]
+            ok = (v > 0) & active
+            r[name] = float(np.median(v[ok] - t0[p][ok])) if ok.any() else float("nan")
+        rows.append(r)
+        prev_last = last
+    return rows
+
+
+def report(rows):
+    total = rows[-1]["last"]
+    print(f"round {total / 1e3:.1f} us over {len(rows)} phases")
+    by = {}
+    for r in rows:
+        by.setdefault(r["kind"], []).append(r)
+    print(f"{'kind':6s} {'n':>3s} {'period':>8s} {'barrier':>8s} {'work_med':>8s} {'work_max':>8s} "
+          f"{'dep':>7s} {'acc':>7s} {'xchg':>7s} {'red':>7s} {'epi':>7s} {'cs':>3s} {'items':>5s}  (us, medians)")
+    for k in KINDS:
+        if k not in by:
+            continue
+        rs = by[k]
+        f = lambda key: np.nanmedian([x[key] for x in rs]) / 1e3
+        print(f"{k:6s} {len(rs):3d} {f('period'):8.2f} {f('bar'):8.2f} {f('work_med'):8.2f} "
+              f"{f('work_max'):8.2f} {f('dep'):7.2f} {f('acc'):7.2f} {f('xchg'):7.2f} {f('red'):7.2f} "
+              f"{f('epi'):7.2f} {rs[0]['cs']:3d} {rs[0]['items']:5d}   sum period {sum(x['period'] for x in rs) / 1e3:7.1f}")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="qwen2.5-0.5b")
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--prompt", type=int, default=64)
+    ap.add_argument("--rounds", type=int, default=40)
+    ap.add_argument("--trace", default="gpurun_out/mk_trace.bin")
+    ap.add_argument("--file", help="analyse an existing trace instead of running")
+    a = ap.parse_args()
+    if a.file:
+        report(analyse(*load(a.file)))
+        return
+    os.environ["SRL_MK_TRACE"] = str(Path(a.trace).resolve())
+    Path(a.trace).parent.mkdir(parents=True, exist_ok=True)
+    from paper_2509_19128_b200.engine import Engine
+    from paper_2509_19128_b200.policy import PRESETS, DecoderPolicy
+
+    cfg = PRESETS[a.config]
+    pol = DecoderPolicy.random(cfg, seed=0, scale=0.02)
+    eng = Engine(pol, start_paused=True, max_streams=a.batch, max_seq_len=a.prompt + a.rounds + 8,
+                 rounds_per_sync=8, event_ring=64)
+    rng = np.random.default_rng(0)
+    for i in range(a.batch):
+        eng.open_stream("p", a.rounds + 4, i, -1, rng.integers(0, cfg.vocab_size, a.prompt).tolist())
+    eng.advance(a.rounds)
+    eng.profile_next_round()
+    eng.advance(1)
+    prof = eng.kernel_profile()
+    print({k: round(v[0], 4) for k, v in prof.items()})
+    eng.close()
+    report(analyse(*load(a.trace)))
+
+
+if __name__ == "__main__":
+    main()
