@@ -324,7 +324,8 @@ __device__ __forceinline__ void mk_epilogue(const MkParams& P, const MkPhase& ph
       const float2 u2 = *reinterpret_cast<const float2*>(&tile[j * kPitch + 64 + c]);
       const float g0 = g2.x * r, g1 = g2.y * r, u0 = u2.x * r, u1 = u2.y * r;
       *reinterpret_cast<__nv_bfloat162*>(&P.act[(size_t)j * P.I + (n0 >> 1) + c]) =
-          __floats2bfloat162_rn(g0 / (1.f + expf(-g0)) * u0, g1 / (1.f + expf(-g1)) * u1);
+          __floats2bfloat162_rn(__fdividef(g0, 1.f + __expf(-g0)) * u0,
+                                __fdividef(g1, 1.f + __expf(-g1)) * u1);
     }
   } else if (ph.kind == MK_LM) {
     // scale by rstd and store the logits (one float4 per thread per row), keep
@@ -979,7 +980,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             }
             fence_proxy_async_global();  // generic-proxy results -> TMA reads
             dep_ok = true;
-            if (P.trace) P.trace[((size_t)p * GR + c) * 16 + 4] = globaltimer();
+            if (P.trace) P.trace[((size_t)p * GR + c) * 16 + 4] = clock64();  // raw cycles
           }
           for (int k = 0; k < pre; ++k) {
             const int st = (s0 + k) % STAGES;
@@ -1013,9 +1014,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           mk_wait(&tempty[acc], aph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + acc * kTok;
+          unsigned long long* trm = P.trace ? P.trace + ((size_t)p * GR + c) * 16 : nullptr;
           for (int k = 0; k < nkb; ++k) {
             mk_wait(&full[stage], ph);
             tc_fence_after();
+            if (trm && k == 0 && trm[14] == 0) trm[14] = clock64();  // raw cycles
             const uint32_t a = smem_u32(smem + stage * kStageBytes);
             const uint32_t b = a + kABytes;
 #pragma unroll
@@ -1026,6 +1029,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
           mma_commit(&tfull[acc]);
+          if (trm && trm[15] == 0) trm[15] = clock64();  // raw cycles
           if (++acc == 2) { acc = 0; aph ^= 1; }
         }
       }
@@ -1044,6 +1048,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
     if (stamp) P.stamps[0] = globaltimer();
     for (int p = 0; p < P.n_phases; ++p) {
       const MkPhase& F = P.phases[p];
+      // the first item's epilogue column constant (a weight: independent of
+      // the barrier below) -- its global load latency overlaps the wait
+      unsigned short colv0 = 0;
+      const long long colv_off = (F.kind == MK_O || F.kind == MK_DOWN) ? F.colv : -1;
+      if (colv_off >= 0) {
+        const int i0 = first_item(c, F.rot, GR);
+        const int n = (i0 / F.cs) * kBN + col;
+        if (i0 < F.n_items && n < F.N) colv0 = reinterpret_cast<const unsigned short*>(P.w)[colv_off + n];
+      }
       if (p > 0) {  // results of the previous phase, grid-wide
         if (ct == 0) {
           phase_wait(P.phase_done, p - 1, target);
@@ -1081,17 +1094,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
         mk_rows(P, F.kind, s_rstd, ct);
         for (int i = first_item(c, F.rot, GR); i < F.n_items; i += GR) {
           const int tile_n = i / F.cs, split = i % F.cs;
-          float colv = 0.f;
-          if (tile_n * kBN + col < F.N) {
-            const __nv_bfloat16* w = P.w;
-            if (F.kind == MK_O) colv = bf2f(w[P.layers[F.layer].ln2 + tile_n * kBN + col]);
-            else if (F.kind == MK_DOWN)
-              colv = bf2f(w[(F.layer + 1 < P.L ? P.layers[F.layer + 1].ln1 : P.off_final_norm) +
-                            tile_n * kBN + col]);
-          }
+          unsigned short colv_bits = colv0;
+          if (i != first_item(c, F.rot, GR) && colv_off >= 0 && tile_n * kBN + col < F.N)
+            colv_bits = reinterpret_cast<const unsigned short*>(P.w)[colv_off + tile_n * kBN + col];
           mk_wait(&tfull[acc], aph);
           tc_fence_after();
-          if (tr && ct == 0 && tr[1] == 0) tr[1] = globaltimer();
+          if (tr && ct == 0 && tr[1] == 0) tr[1] = clock64() - tr[8];
           uint32_t ra[32];
           tmem_ld_32x32b_x32(tmem + acc * kTok + hf * 32 + ((uint32_t)((cw & 3) * 32) << 16), ra);
           tmem_ld_wait();
@@ -1132,6 +1140,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             for (int j = 0; j < 32; ++j)
               if (j0 + j < P.S) __stcg(&part[(j0 + j) * kBN + col], __uint_as_float(ra[j]));
             fence_proxy_async_global();
+            if (tr && ct == 0 && tr[11] == 0) tr[11] = clock64() - tr[8];
             r0 = (split * P.S) / F.cs;
             r1 = ((split + 1) * P.S) / F.cs;
             const int nr = r1 - r0;
@@ -1142,8 +1151,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
                 unsigned* tc = &P.tile_ctr[F.ctr_base + tile_n];
                 __threadfence();
                 atomicAdd(tc, 1u);
+                if (tr && tr[12] == 0) tr[12] = clock64() - tr[8];
                 wait_count(tc, ep1 * (unsigned)F.cs);
-                if (tr && tr[2] == 0) tr[2] = globaltimer();
+                if (tr && tr[2] == 0) tr[2] = clock64() - tr[8];
                 if (nr > 0) mbar_arrive_expect_tx(cbar, (uint32_t)(F.cs * nr * kBN * 4));
               }
               __syncwarp();
@@ -1168,11 +1178,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
               }
             }
           }
-          if (tr && ct == 0 && tr[5] == 0) tr[5] = globaltimer();
+          if (tr && ct == 0 && tr[5] == 0) tr[5] = clock64() - tr[8];
           csync();
+          const float colv = __uint_as_float((unsigned)colv_bits << 16);
           if (r1 > r0) mk_epilogue(P, F, tile_n, tile, s_rstd, ct, r0, r1, colv);
           csync();
-          if (tr && ct == 0 && tr[6] == 0) tr[6] = globaltimer();
+          if (tr && ct == 0 && tr[6] == 0) tr[6] = clock64() - tr[8];
         }
       }
       fence_proxy_async_global();  // later phases read these results with TMA
@@ -1180,7 +1191,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
       if (ct == 0) {
         if (tr) {
           tr[3] = globaltimer();
-          tr[9] = clock64();
+          tr[9] = clock64() - tr[8];
         }
         __threadfence();
         phase_arrive(P.phase_done, p, c);

@@ -38,6 +38,7 @@ struct MkPhase {
   int xmap;     // activation tensor-map index: 0 xg, 1 attn, 2 act
   int ctr_base; // first split-K counter of this phase
   int rot;      // item -> CTA rotation
+  long long colv;  // O / DOWN: offset of the next RMSNorm gain (epilogue column constant), else -1
 };
 
 struct MkLayer {

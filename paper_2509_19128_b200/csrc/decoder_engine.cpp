@@ -325,7 +325,11 @@ int DecoderBackend::mega_init() {
   size_t ws = (size_t)S_ * d_.nkv * splits * (d_.nq / d_.nkv) * (d_.hd + 2);
   auto add = [&](int kind, int layer, int n_items, int cs, int N, int K, int wmap, int xmap,
                  int counters) {
-    MkPhase f{kind, layer, n_items, cs, N, K, wmap, xmap, ctr, items_total % grid};
+    MkPhase f{kind, layer, n_items, cs, N, K, wmap, xmap, ctr, items_total % grid, -1};
+    const LayerOffsets* lo = buf_[0]->layout.layers;
+    if (kind == MK_O) f.colv = (long long)lo[layer].ln2;
+    if (kind == MK_DOWN)
+      f.colv = (long long)(layer + 1 < d_.L ? lo[layer + 1].ln1 : buf_[0]->layout.final_norm);
     ctr += counters;
     items_total += n_items;
     ph.push_back(f);
@@ -600,13 +604,20 @@ int DecoderBackend::run_rounds(int n, std::vector<SlotEvent>& events, double* de
   events.assign((size_t)n * S_, SlotEvent{});
   int done = 0;
   while (done < n) {
-    const int batch = std::min(n - done, R_);
+    int batch = std::min(n - done, R_);
     std::vector<std::vector<int>> prefilled_at(batch);
     bool profiled = false;
     SRL_CUDA(cudaEventRecord(ev_start_, st_));
     const int64_t c0 = round_ctr_host_;
     for (int i = 0; i < batch; ++i) {
       int st;
+      if (any_pending_ && i > 0) {
+        // a prefill round builds the running slots' decode rows from host
+        // state, which only learns this batch's tokens when its events are
+        // copied back: end the batch here, the prefill opens the next one
+        batch = i;
+        break;
+      }
       if (any_pending_) {
         if ((st = prefill_round(active_, prefilled_at[i]))) return st;
         for (int s : prefilled_at[i]) host_[s].pending = false;

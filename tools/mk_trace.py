@@ -31,6 +31,14 @@ def load(path):
     return meta, tr
 
 
+GHZ = 1.965  # SM clock under load (bench clocks: 1965 MHz)
+# per-CTA stamps inside a phase, SM cycles since the phase start (tr[8]);
+# attention items use 10-14 as cycles since the item start
+GEMM_FIELDS = [(4, "dep"), (14, "full0"), (15, "committed"), (1, "acc"), (11, "stored"), (12, "arrived"), (2, "xchg"), (5, "red"),
+               (13, "xready"), (6, "epi"), (9, "end")]
+ATTN_FIELDS = [(11, "operands"), (12, "keys"), (13, "sync"), (14, "merged"), (10, "item")]
+
+
 def analyse(meta, tr):
     n, grid, _ = tr.shape
     t0 = tr[:, :, 0]
@@ -44,15 +52,18 @@ def analyse(meta, tr):
         arr = tr[p, :, 7][active] - base
         last = arr.max()
         r = dict(p=p, kind=kind, cs=int(meta[p, 1]), items=int(meta[p, 2]),
-                 start_med=np.median(st), start_max=st.max(), last=last,
-                 work_med=np.median(tr[p, :, 3][active] - t0[p][active]),
-                 work_max=(tr[p, :, 3][active] - t0[p][active]).max())
+                 start_med=np.median(st), last=last)
         r["bar"] = (np.median(st) - prev_last) if prev_last is not None else 0.0
         r["period"] = last - prev_last if prev_last is not None else last
-        for k, name in [(4, "dep"), (1, "acc"), (2, "xchg"), (5, "red"), (6, "epi")]:
-            v = tr[p, :, k]
+        r["arrive"] = float(np.median(tr[p, :, 7][active] - tr[p, :, 3][active]))
+        fields = ATTN_FIELDS if kind == "attn" else GEMM_FIELDS
+        for k, name in fields:
+            v = tr[p, :, k].copy()
+            if k in (4, 14, 15):  # raw clock64 of the producer / MMA warps
+                v = np.where(v > 0, v - tr[p, :, 8], 0)
             ok = (v > 0) & active
-            r[name] = float(np.median(v[ok] - t0[p][ok])) if ok.any() else float("nan")
+            r[name] = float(np.median(v[ok])) / GHZ if ok.any() else float("nan")
+            r[name + "_max"] = float(v[ok].max()) / GHZ if ok.any() else float("nan")
         rows.append(r)
         prev_last = last
     return rows
@@ -60,20 +71,22 @@ def analyse(meta, tr):
 
 def report(rows):
     total = rows[-1]["last"]
-    print(f"round {total / 1e3:.1f} us over {len(rows)} phases")
+    print(f"round {total / 1e3:.1f} us over {len(rows)} phases (ns medians over layers; "
+          f"inner stamps = median over CTAs, ns since the CTA's phase start)")
     by = {}
     for r in rows:
         by.setdefault(r["kind"], []).append(r)
-    print(f"{'kind':6s} {'n':>3s} {'period':>8s} {'barrier':>8s} {'work_med':>8s} {'work_max':>8s} "
-          f"{'dep':>7s} {'acc':>7s} {'xchg':>7s} {'red':>7s} {'epi':>7s} {'cs':>3s} {'items':>5s}  (us, medians)")
     for k in KINDS:
         if k not in by:
             continue
         rs = by[k]
-        f = lambda key: np.nanmedian([x[key] for x in rs]) / 1e3
-        print(f"{k:6s} {len(rs):3d} {f('period'):8.2f} {f('bar'):8.2f} {f('work_med'):8.2f} "
-              f"{f('work_max'):8.2f} {f('dep'):7.2f} {f('acc'):7.2f} {f('xchg'):7.2f} {f('red'):7.2f} "
-              f"{f('epi'):7.2f} {rs[0]['cs']:3d} {rs[0]['items']:5d}   sum period {sum(x['period'] for x in rs) / 1e3:7.1f}")
+        med = lambda key: np.nanmedian([x.get(key, np.nan) for x in rs])
+        fields = ATTN_FIELDS if k == "attn" else GEMM_FIELDS
+        inner = " ".join(f"{name}={med(name):.0f}/{med(name + '_max'):.0f}" for _, name in fields
+                         if not np.isnan(med(name)))
+        print(f"{k:6s} n={len(rs):2d} cs={rs[0]['cs']:2d} items={rs[0]['items']:4d} "
+              f"period={med('period'):6.0f} barrier={med('bar'):5.0f} arrive={med('arrive'):4.0f} | {inner}"
+              f"  [sum period {sum(x['period'] for x in rs) / 1e3:.1f} us]")
 
 
 def main():
