@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=4)
+    ap.add_argument("--no-trainer", action="store_true", help="skip the trainer-step measurement")
+    ap.add_argument("--train-seqs", type=int, default=64, help="trajectories per trainer step")
     return ap.parse_args()
 
 
@@ -189,6 +191,62 @@ def cpu_decode_sample(cfg, batch, prompt, steps, warmup=0, seed=0):
     return batch * steps / dt, dt, os.cpu_count()
 
 
+def matmul_params(cfg):
+    """Parameters that enter a GEMM per token (all projections + LM head)."""
+    H, I, L, V = cfg.hidden, cfg.intermediate, cfg.layers, cfg.vocab_size
+    qd, qkv = cfg.q_heads * cfg.head_dim, (cfg.q_heads + 2 * cfg.kv_heads) * cfg.head_dim
+    return L * (qkv * H + H * qd + 2 * I * H + H * I) + V * H
+
+
+def trainer_measure(cfg, pol, n_seq, prompt, gen, steps=3):
+    """Trainer side of config 2: one optimizer step =
+    current-policy log-prob recompute + truncated-IS REINFORCE objective + full
+    backward + Adam over n_seq trajectories of prompt + gen tokens.  Device
+    time from the trainer's own CUDA events (srl_trainer_stats.step_ms) plus
+    the Adam kernel; tensor throughput counts 6 * matmul params per token plus
+    causal attention (fwd 4 * T^2/2 * nq * hd per layer and sequence, x3)."""
+    import torch
+
+    from paper_2509_19128_b200.trainer import Trainer
+
+    rng = np.random.default_rng(7)
+    seq = prompt + 1 + gen
+    trajs = []
+    for i in range(n_seq):
+        toks = [cfg.bos_token] + rng.integers(0, cfg.vocab_size, size=seq - 1).tolist()
+        mu = (-np.log(cfg.vocab_size) + 0.1 * rng.standard_normal(seq)).tolist()
+        a = float(rng.standard_normal())
+        trajs.append(dict(tokens=toks, loss_begin=prompt + 1, behavior_logprobs=mu,
+                          advantages=[a] * seq))
+    tr = Trainer(pol.clone(), max_tokens=n_seq * seq)
+    tr.step(trajs)  # warm-up (allocations, first launches)
+    tr.apply_adam(1e-6)
+    torch.cuda.synchronize()
+    ms, fwd = [], []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r = tr.step(trajs)
+        e0.record()
+        tr.apply_adam(1e-6)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(r.step_ms + e0.elapsed_time(e1))
+        fwd.append(r.forward_ms)
+    tokens = r.tokens
+    attn = cfg.layers * n_seq * 4 * (seq * seq / 2) * cfg.q_heads * cfg.head_dim * 3
+    flops = 6.0 * matmul_params(cfg) * tokens + attn
+    t = float(np.median(ms))
+    _, bf16, kind = load_peaks()
+    tf = flops / (t * 1e-3) / 1e12
+    out = {"workload": f"{n_seq} trajectories x {seq} tokens ({tokens} scored rows), "
+                       f"IS-REINFORCE fwd + bwd + Adam",
+           "tokens_per_s": tokens / (t * 1e-3), "step_ms": t, "forward_ms": float(np.median(fwd)),
+           "tflops": tf, "bound": "tensor", "peak_tflops": bf16, "peak_kind": kind,
+           "frac": tf / bf16 if bf16 else None, "objective": r.objective, "ess": r.ess}
+    tr.close()
+    return out
+
+
 def reference_arm(args, cfg):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -308,6 +366,8 @@ def main():
         dev_ms = (st1["decode_ms"] - st0["decode_ms"]) + upd_ms + pause
         if record is not None:
             record.append(dict(tokens=emitted, dev_ms=dev_ms, wall_ms=1000 * wall, pause_ms=pause,
+                               prefill_ms=st1["prefill_ms"] - st0["prefill_ms"],
+                               prefill_rows=st1["prefill_rows"] - st0["prefill_rows"],
                                update_ms=upd_ms, launches=st1["launches"] - st0["launches"],
                                finished=len(finished)))
 
@@ -435,8 +495,13 @@ def main():
         "roofline_tokens_per_s": roofline_tps,
         "kernel_ms_per_round": {k: round(v, 4) for k, v in cls_ms.items()},
         "update_gbs": pol.weights()[1] / (float(np.median(upd)) * 1e-3) / 1e9,
+        "prefill": {"ms_per_step": sum(r["prefill_ms"] for r in rec) / args.steps,
+                    "rows_per_step": sum(r["prefill_rows"] for r in rec) / args.steps,
+                    "note": "refill prefill rounds of finished streams (inside value's device time)"},
         "clocks": clk,
     }
+    if rank == 0 and not args.no_trainer:
+        out["trainer"] = trainer_measure(cfg, pol, args.train_seqs, args.prompt, args.gen)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tps, dt, cores = cpu_decode_sample(cfg, B, 8, args.cpu_steps, 1)
         out["cpu_baseline"] = {"value": tps, "unit": UNIT, "cores": cores, "kind": "port",

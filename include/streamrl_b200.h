@@ -190,6 +190,9 @@ typedef struct {
   double last_pause_ms;
   double max_pause_ms;
   int64_t launches;      /* kernels launched by the engine (graph nodes counted) */
+  int64_t prefill_rounds; /* rounds that prefilled newly opened streams */
+  int64_t prefill_rows;   /* token rows those rounds ran (prompts + running decode rows) */
+  double prefill_ms;      /* their device time (CUDA events), included in decode_ms */
 } srl_engine_stats;
 int srl_engine_stats_get(const srl_engine* e, srl_engine_stats* out);
 

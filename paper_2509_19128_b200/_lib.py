@@ -57,7 +57,8 @@ class TokenEventC(C.Structure):
 
 class EngineStatsC(C.Structure):
     _fields_ = [("rounds", i64), ("tokens", i64), ("updates", i64), ("decode_ms", f64),
-                ("last_pause_ms", f64), ("max_pause_ms", f64), ("launches", i64)]
+                ("last_pause_ms", f64), ("max_pause_ms", f64), ("launches", i64),
+                ("prefill_rounds", i64), ("prefill_rows", i64), ("prefill_ms", f64)]
 
 
 class TrainerOptionsC(C.Structure):

@@ -248,6 +248,8 @@ DecoderBackend::~DecoderBackend() {
   if (ev_stop_) cudaEventDestroy(ev_stop_);
   for (cudaEvent_t& ev : ev_prof_)
     if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t& ev : ev_pf_)
+    if (ev) cudaEventDestroy(ev);
   runner_.reset();
   if (st_) cudaStreamDestroy(st_);
 }
@@ -258,6 +260,7 @@ int DecoderBackend::init(const Policy& p) {
   SRL_CUDA(cudaEventCreate(&ev_start_));
   SRL_CUDA(cudaEventCreate(&ev_stop_));
   for (cudaEvent_t& ev : ev_prof_) SRL_CUDA(cudaEventCreate(&ev));
+  for (cudaEvent_t& ev : ev_pf_) SRL_CUDA(cudaEventCreate(&ev));
   const DecoderWeights& src = *p.dec;
   d_ = src.dims;
   S_ = std::max(1, opts_.max_streams);
@@ -579,6 +582,7 @@ int DecoderBackend::prefill_round(int b, std::vector<int>& prefilled) {
   }
   const int M = (int)rs.size();
   if (M > r.M_max) return fail(SRL_INVALID_ARGUMENT, "prefill exceeds the engine's row budget");
+  last_prefill_rows_ = M;
   int32_t* pin = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(pinned_) + (size_t)R_ * S_ * sizeof(DevEvent));
   std::memcpy(pin, rs.data(), 4 * M);
   std::memcpy(pin + M, rp.data(), 4 * M);
@@ -606,7 +610,7 @@ int DecoderBackend::run_rounds(int n, std::vector<SlotEvent>& events, double* de
   while (done < n) {
     int batch = std::min(n - done, R_);
     std::vector<std::vector<int>> prefilled_at(batch);
-    bool profiled = false;
+    bool profiled = false, prefilled = false;
     SRL_CUDA(cudaEventRecord(ev_start_, st_));
     const int64_t c0 = round_ctr_host_;
     for (int i = 0; i < batch; ++i) {
@@ -619,7 +623,10 @@ int DecoderBackend::run_rounds(int n, std::vector<SlotEvent>& events, double* de
         break;
       }
       if (any_pending_) {
+        SRL_CUDA(cudaEventRecord(ev_pf_[0], st_));
         if ((st = prefill_round(active_, prefilled_at[i]))) return st;
+        SRL_CUDA(cudaEventRecord(ev_pf_[1], st_));
+        prefilled = true;
         for (int s : prefilled_at[i]) host_[s].pending = false;
         any_pending_ = false;
         for (const HostSlot& h : host_)
@@ -664,6 +671,13 @@ int DecoderBackend::run_rounds(int n, std::vector<SlotEvent>& events, double* de
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ev_start_, ev_stop_);
     if (device_ms) *device_ms += ms;
+    if (prefilled) {
+      float pms = 0.f;
+      cudaEventElapsedTime(&pms, ev_pf_[0], ev_pf_[1]);
+      prefill_ms_ += pms;
+      prefill_rounds_ += 1;
+      prefill_rows_ += last_prefill_rows_;
+    }
     if (profiled) {
       timer_.collect(&profile_);
       profile_.rows = S_;

@@ -84,6 +84,11 @@ class DecoderBackend final : public Backend {
   int open_slot(int slot, const StreamSpec& spec) override;
   void close_slot(int slot) override;
   int run_rounds(int n, std::vector<SlotEvent>& events, double* device_ms) override;
+  void prefill_stats(srl_engine_stats* s) const override {
+    s->prefill_rounds = prefill_rounds_;
+    s->prefill_rows = prefill_rows_;
+    s->prefill_ms = prefill_ms_;
+  }
   int check_update(const Policy& p) override;
   int apply_update(const Policy& p, bool recompute, int version) override;
   int standby(void** ptr, size_t* bytes) override;
@@ -121,6 +126,10 @@ class DecoderBackend final : public Backend {
   cudaGraphExec_t exec_[2] = {nullptr, nullptr};
   cudaEvent_t ev_start_ = nullptr, ev_stop_ = nullptr;
   cudaEvent_t ev_prof_[2] = {nullptr, nullptr};  // around a profiled megakernel launch
+  cudaEvent_t ev_pf_[2] = {nullptr, nullptr};    // around a prefill round
+  int64_t prefill_rounds_ = 0, prefill_rows_ = 0;
+  double prefill_ms_ = 0.0;
+  int last_prefill_rows_ = 0;
   void* dev_state_ = nullptr;
   void* pinned_ = nullptr;
   size_t pinned_bytes_ = 0;

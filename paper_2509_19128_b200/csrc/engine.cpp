@@ -333,6 +333,7 @@ srl_engine_stats Engine::stats() const {
   std::lock_guard<std::mutex> lk(lock_);
   srl_engine_stats s = stats_;
   s.launches = backend_->launches();
+  backend_->prefill_stats(&s);
   return s;
 }
 

@@ -23,6 +23,7 @@
 #include <mutex>
 
 #include "gemm.cuh"
+#include "gemm_epi.cuh"
 #include "sm100.cuh"
 
 namespace srl {
@@ -53,7 +54,6 @@ struct Layout {
   static constexpr int kAlloc = kTotal + 1024;  // manual 1024-B alignment slack
 };
 
-__device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -67,21 +67,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
                   blockIdx.x) * 8 + (i)] = gtimer();                                          \
   } while (0)
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 
 template <int TOK, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -99,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   int4* s_row = reinterpret_cast<int4*>(smem + L::kRowOffset);
   float* tile = reinterpret_cast<float*>(smem);  // epilogue view, aliases the ring
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const int n_tile = blockIdx.x, split = blockIdx.y, tok_tile = blockIdx.z;
   const int n_tiles = gridDim.x;
   const int n0 = n_tile * kBlockN, t0 = tok_tile * TOK;
@@ -261,158 +246,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   }
 
-  // ---- epilogue over rows [r0, r1)
+  // ---- epilogue over rows [r0, r1) (gemm_epi.cuh)
   SRL_STAMP(4);
   griddep_wait();  // epilogue inputs (ssq, residual) come from earlier kernels
-  for (int j = r0 + threadIdx.x; j < r1; j += kThreads) {
-    float r = 1.f;
-    const int m = t0 + j;
-    if (epi.ssq_in != nullptr && m < M) {
-      float s = 0.f;
-      for (int p = 0; p < epi.ssq_in_parts; ++p) s += epi.ssq_in[(size_t)m * epi.ssq_in_parts + p];
-      r = rsqrtf(s * epi.inv_dim + epi.eps);
-    }
-    s_rstd[j] = r;
-    if (epi.kind == EPI_QKV) {  // (stamp 5 follows the row-parameter loads)  // KV-cache coordinates of this row
-      int4 rc = make_int4(-1, 0, 0, 0);
-      if (m < M) {
-        rc.x = epi.row_slot[m];
-        rc.y = epi.row_pos[m];
-        if (rc.x >= 0) {
-          rc.z = epi.block_table[(size_t)rc.x * epi.pages_per_seq + rc.y / 64];
-          rc.w = rc.y % 64;
-        }
-      }
-      s_row[j] = rc;
-    }
-  }
+  gemm_detail::epi_row_meta(epi, r0, r1, t0, M, s_rstd, s_row, threadIdx.x, kThreads);
   __syncthreads();
-
   SRL_STAMP(5);
-  const int rows = r1 - r0;
-  if (epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16) {
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
-      const int j = r0 + (idx >> 7), c = idx & 127;
-      const int m = t0 + j, n = n0 + c;
-      if (m >= M || n >= N) continue;
-      float v = tile[j * L::kPitch + c] * s_rstd[j];
-      if (epi.bias) v += bf2f(epi.bias[n]);
-      if (epi.kind == EPI_STORE_F32)
-        epi.out_f32[(size_t)m * epi.ld_out + n] = v;
-      else
-        epi.out_bf16[(size_t)m * epi.ld_bf16 + n] = __float2bfloat16(v);
-    }
-  } else if (epi.kind == EPI_ACCUM_F32) {
-    for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
-      const int j = r0 + (idx >> 7), c = idx & 127;
-      const int m = t0 + j, n = n0 + c;
-      if (m >= M || n >= N) continue;
-      epi.out_f32[(size_t)m * epi.ld_out + n] += epi.scale * tile[j * L::kPitch + c];
-    }
-  } else if (epi.kind == EPI_SWIGLU) {
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < rows * (kBlockN / 2); idx += kThreads) {
-      const int j = r0 + (idx >> 6), c = idx & 63;
-      const int m = t0 + j;
-      if (m >= M || n0 + c >= N) continue;
-      const float g = tile[j * L::kPitch + c] * s_rstd[j];
-      const float u = tile[j * L::kPitch + 64 + c] * s_rstd[j];
-      const float a = g / (1.f + expf(-g)) * u;
-      epi.out_bf16[(size_t)m * epi.ld_bf16 + (n0 >> 1) + c] = __float2bfloat16(a);
-    }
-  } else if (epi.kind == EPI_QKV) {
-    for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
-      const int j = r0 + (idx >> 7), c = idx & 127;
-      const int n = n0 + c;
-      float v = 0.f;
-      if (t0 + j < M && n < N) v = tile[j * L::kPitch + c] * s_rstd[j] + bf2f(epi.bias[n]);
-      tile[j * L::kPitch + c] = v;
-    }
-    __syncthreads();
-    const int hd = epi.hd, half = hd >> 1;
-    const int qend = epi.nq * hd, kend = (epi.nq + epi.nkv) * hd;
-    for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
-      const int j = r0 + (idx >> 7), c = idx & 127;
-      const int m = t0 + j, n = n0 + c;
-      const int4 rc = s_row[j];
-      if (m >= M || n >= N || rc.x < 0) continue;
-      const int jj = n % hd;
-      const float* row = &tile[j * L::kPitch + (c - jj)];  // this head's hd values
-      float y;
-      if (n < kend) {  // RoPE (rotate pairs (i, i + hd/2)) on q and k
-        const int i = jj < half ? jj : jj - half;
-        const float co = epi.cos_sin[(size_t)rc.y * hd + i];
-        const float si = epi.cos_sin[(size_t)rc.y * hd + half + i];
-        const float x1 = row[i], x2 = row[i + half];
-        y = jj < half ? x1 * co - x2 * si : x2 * co + x1 * si;
-      } else {
-        y = row[jj];
-      }
-      const __nv_bfloat16 b = __float2bfloat16(y);
-      if (n < qend) {
-        epi.q_out[(size_t)m * qend + n] = b;
-      } else {
-        const int kv = n < kend ? n - qend : n - kend;
-        const int kh = kv / hd;
-        const size_t at = (((size_t)rc.z * epi.nkv + kh) * 64 + rc.w) * hd + jj;
-        if (n < kend) epi.kc[at] = b;
-        else epi.vc[at] = b;
-      }
-    }
-  } else if (epi.kind == EPI_LOGITS) {
-    for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
-      const int j = r0 + (idx >> 7), c = idx & 127;
-      const int m = t0 + j, n = n0 + c;
-      float v = -INFINITY;
-      if (m < M && n < N) {
-        v = tile[j * L::kPitch + c] * s_rstd[j];
-        epi.out_f32[(size_t)m * epi.ld_out + n] = v;
-      }
-      tile[j * L::kPitch + c] = v;
-    }
-    __syncthreads();
-    for (int j = r0 + warp; j < r1; j += kThreads / 32) {
-      const float4 x = *reinterpret_cast<const float4*>(&tile[j * L::kPitch + lane * 4]);
-      const float mx = warp_max(fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
-      double s = 0.0;
-      if (mx != -INFINITY) {
-        const double md = (double)mx;
-        s = exp((double)x.x - md) + exp((double)x.y - md) + exp((double)x.z - md) +
-            exp((double)x.w - md);
-      }
-      s = warp_sum_d(s);
-      const int m = t0 + j;
-      if (lane == 0 && m < M) {
-        epi.part_max[(size_t)m * n_tiles + n_tile] = mx;
-        epi.part_sum[(size_t)m * n_tiles + n_tile] = s;
-      }
-    }
-  } else if (epi.kind == EPI_RESID) {
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < rows * kBlockN; idx += kThreads) {
-      const int j = r0 + (idx >> 7), c = idx & 127;
-      const int m = t0 + j, n = n0 + c;
-      float x = 0.f;
-      if (m < M && n < N) {
-        const size_t o = (size_t)m * N + n;
-        x = epi.resid[o] + tile[j * L::kPitch + c];
-        epi.resid[o] = x;
-        epi.xg[o] = __float2bfloat16(x * bf2f(epi.gain[n]));
-      }
-      tile[j * L::kPitch + c] = x;
-    }
-    __syncthreads();
-    for (int j = r0 + warp; j < r1; j += kThreads / 32) {
-      float s = 0.f;
-      for (int c = lane; c < kBlockN; c += 32) {
-        const float x = tile[j * L::kPitch + c];
-        s += x * x;
-      }
-      s = warp_sum(s);
-      if (lane == 0 && t0 + j < M) epi.ssq_out[(size_t)(t0 + j) * n_tiles + n_tile] = s;
-    }
-  }
+  gemm_detail::epi_apply(epi, tile, L::kPitch, r0, r1, t0, n0, n_tile, n_tiles, M, N, s_rstd, s_row,
+                         threadIdx.x, kThreads, [] { __syncthreads(); });
   __syncthreads();
   SRL_STAMP(6);
 }
@@ -509,6 +350,22 @@ cudaError_t gemm_bf16_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M
   if (M < 1 || N < 1 || K < kBlockK || K % kBlockK != 0 || splits < 1)
     return cudaErrorInvalidValue;
   if (epi.kind == EPI_SWIGLU && N % kBlockN != 0) return cudaErrorInvalidValue;
+  // many token rows: the persistent double-buffered kernel (gemm_big.cu);
+  // SRL_GEMM_BIG=0 disables it, =1 forces it for every M > 128 (A/B tests)
+  static const char* big_env = std::getenv("SRL_GEMM_BIG");
+  static const int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  int big = gemm_big_tok(M, N, K, sms);
+  if (big_env && big_env[0] == '0') big = 0;
+  if (big_env && big_env[0] == '1' && M > 128 && big == 0) big = 128;
+  static const bool log = std::getenv("SRL_GEMM_LOG") != nullptr;  // launch trace (profiling)
+  if (log) std::fprintf(stderr, "srl gemm M=%d N=%d K=%d kind=%d path=%s\n", M, N, K, epi.kind,
+                        big ? (big == 256 ? "big256" : "big128") : "splitk");
+  if (big) return gemm_big_launch(tw, tx, M, N, K, big, epi, stream);
   int cs = 1;
   while (cs * 2 <= splits && cs * 2 <= kMaxCluster && cs * 2 <= K / kBlockK) cs *= 2;
   if (gemm_tok_tile(M) == 64) return launch_impl<64, 4>(tw, tx, M, N, K, cs, ws, epi, stream);

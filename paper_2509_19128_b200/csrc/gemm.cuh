@@ -75,7 +75,14 @@ int gemm_tok_tile(int M);
 int gemm_auto_splits(int M, int N, int K, int num_sms);
 size_t gemm_workspace_floats(int M, int N, int splits);
 
+// Persistent large-M kernel (gemm_big.cu): token tile 256 or 128 when the
+// tile count fills `num_sms`, else 0 (use the split-K kernel).
+int gemm_big_tok(int M, int N, int K, int num_sms);
+cudaError_t gemm_big_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int tok,
+                            const EpiParams& epi, cudaStream_t stream);
+
 // Launch.  tw: W [N x K] (box 128 rows); tx: X [>=M x K] (box gemm_tok_tile(M) rows).
+// Dispatches to gemm_big_launch when gemm_big_tok() says so (splits ignored).
 cudaError_t gemm_bf16_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K,
                              int splits, const GemmWorkspace& ws, const EpiParams& epi,
                              cudaStream_t stream);

@@ -1,0 +1,274 @@
+// gemm_big.cu -- persistent, warp-specialised tcgen05 GEMM for many token
+// rows (prefill chunks, the trainer's forward and backward GEMMs).
+//
+// Same contract and fused epilogues as gemm.cu (swap-AB: 128 weight rows are
+// the UMMA M, TOK = 128 or 256 token rows the UMMA N), but built for
+// throughput instead of decode latency:
+//   * one CTA per SM walks output tiles n-fastest (concurrent CTAs share the
+//     activation block, the weights stay L2-resident);
+//   * warp 0 streams A (16 KB) + B (TOK x 128 B) k-blocks by TMA into a
+//     STAGES-deep ring across tile boundaries; warp 1 issues
+//     tcgen05.mma 128 x TOK x 16 into one of TWO TMEM accumulators
+//     (2 x TOK fp32 columns) and moves on to the next tile at once;
+//   * warps 4-11 drain the other accumulator and run the epilogue while the
+//     next tile's MMAs run: two groups of four warps (each group covers the
+//     128 TMEM lanes) take alternate 32-token chunks, stage them in shared
+//     memory and run gemm_epi.cuh on them.
+// No split-K: it is chosen only when the tile count fills the machine.
+#include <cstdio>
+
+#include "gemm.cuh"
+#include "gemm_epi.cuh"
+#include "sm100.cuh"
+
+namespace srl {
+using namespace sm100;
+
+namespace {
+
+constexpr int kBN = 128;  // weight rows per tile (UMMA M)
+constexpr int kBK = 64;   // k-block (128-B swizzle row)
+constexpr int kThreads = 384;
+constexpr int kChunk = 32;  // tokens per epilogue chunk
+constexpr int kPitch = kBN;  // drain writes are lane-contiguous: no padding needed
+
+template <int TOK>
+struct BigLayout {
+  static constexpr int STAGES = TOK == 256 ? 4 : 6;
+  static constexpr int kABytes = kBN * kBK * 2;
+  static constexpr int kBBytes = TOK * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kRing = STAGES * kStageBytes;
+  static constexpr int kEpi = kRing;                               // [2][kChunk][kPitch] fp32
+  static constexpr int kRstd = kEpi + 2 * kChunk * kPitch * 4;     // [2][kChunk] fp32
+  static constexpr int kRow = kRstd + 2 * kChunk * 4;              // [2][kChunk] int4
+  static constexpr int kBar = kRow + 2 * kChunk * 16;
+  static constexpr int kMisc = kBar + (2 * STAGES + 4) * 8;
+  static constexpr int kTotal = kMisc + 16;
+  static constexpr int kAlloc = kTotal + 1024;
+  static_assert(kAlloc <= 232448, "shared memory budget");
+};
+
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+}
+
+template <int TOK>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_big_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
+                    int M, int N, int K, const EpiParams epi) {
+  using L = BigLayout<TOK>;
+  constexpr int STAGES = L::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kMisc);
+
+  const int warp = threadIdx.x >> 5;
+  const int n_tiles = (N + kBN - 1) / kBN;
+  const int tok_tiles = (M + TOK - 1) / TOK;
+  const int total = n_tiles * tok_tiles;
+  const int kbt = K / kBK;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tw);
+      tma_prefetch_desc(&tx);
+    }
+    __syncwarp();
+    tmem_alloc<2 * TOK>(tmem_slot);
+  } else if (warp == 1) {
+    if (elect_one()) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(&tfull[a], 1);
+        mbar_init(&tempty[a], 256);  // every epilogue thread, after its last TMEM load
+      }
+      fence_barrier_init();
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_launch_dependents();
+
+  if (warp == 0) {
+    if (elect_one()) {  // ---- TMA producer
+      griddep_wait();   // the activations come from the previous kernel
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int n0 = (t % n_tiles) * kBN, t0 = (t / n_tiles) * TOK;
+        for (int kb = 0; kb < kbt; ++kb) {
+          mbar_wait(&empty[stage], ph ^ 1);
+          uint8_t* a = smem + stage * L::kStageBytes;
+          mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+          tma_load_2d(a, &tw, &full[stage], kb * kBK, n0);
+#pragma unroll
+          for (int h = 0; h < TOK / 128; ++h)  // the X map's box is 128 rows
+            tma_load_2d(a + L::kABytes + h * 128 * 128, &tx, &full[stage], kb * kBK, t0 + h * 128);
+          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {  // ---- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16_f32(128, TOK);
+      int stage = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * TOK;
+        for (int kb = 0; kb < kbt; ++kb) {
+          mbar_wait(&full[stage], ph);
+          tc_fence_after();
+          const uint32_t a = smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t b = a + L::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            mma_bf16_ss(d, umma_desc_k_sw128(a, kk * 32), umma_desc_k_sw128(b, kk * 32), idesc,
+                        (kb | kk) != 0);
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ---- epilogue: group g (warps 4-7 / 8-11), TMEM lane quadrant q
+    const int g = (warp - 4) >> 2, q = warp & 3;
+    const int tid = q * 32 + (threadIdx.x & 31);  // = the TMEM lane = the tile column drained
+    float* tile = reinterpret_cast<float*>(smem + L::kEpi) + g * kChunk * kPitch;
+    float* s_rstd = reinterpret_cast<float*>(smem + L::kRstd) + g * kChunk;
+    int4* s_row = reinterpret_cast<int4*>(smem + L::kRow) + g * kChunk;
+    auto sync = [g] { group_sync(g); };
+    const bool direct = epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16 || epi.kind == EPI_ACCUM_F32;
+    bool waited = false;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int n_tile = t % n_tiles, n0 = n_tile * kBN, t0 = (t / n_tiles) * TOK;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      if (!waited) {  // epilogue inputs (residual, ssq) come from earlier kernels
+        griddep_wait();
+        waited = true;
+      }
+      const int last = TOK / kChunk - 2 + g;  // this group's last chunk of the tile
+      for (int c = g; c < TOK / kChunk; c += 2) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + acc * TOK + c * kChunk + ((uint32_t)(q * 32) << 16), r);
+        tmem_ld_wait();
+        if (c == last) {  // accumulator drained by this thread
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
+        const int tc0 = t0 + c * kChunk;
+        if (tc0 >= M) continue;  // rows past M: nothing to store (uniform per group)
+        if (direct) {
+          // plain stores straight from the accumulator registers: thread =
+          // output column n, so each warp store covers 32 consecutive columns
+          const int n = n0 + tid;
+          const int lane = threadIdx.x & 31;
+          float rs = 1.f;  // rstd of token tc0 + lane, broadcast below
+          if (epi.ssq_in != nullptr && tc0 + lane < M) {
+            float sacc = 0.f;
+            for (int p = 0; p < epi.ssq_in_parts; ++p)
+              sacc += epi.ssq_in[(size_t)(tc0 + lane) * epi.ssq_in_parts + p];
+            rs = rsqrtf(sacc * epi.inv_dim + epi.eps);
+          }
+          const float bias = (epi.bias != nullptr && n < N) ? gemm_detail::epi_bf2f(epi.bias[n]) : 0.f;
+          const int jn = min(32, M - tc0);
+          if (n < N) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float rj = __shfl_sync(0xffffffffu, rs, j);
+              if (j >= jn) continue;
+              const float v = __uint_as_float(r[j]);
+              const size_t m = (size_t)(tc0 + j);
+              if (epi.kind == EPI_STORE_F32) epi.out_f32[m * epi.ld_out + n] = v * rj + bias;
+              else if (epi.kind == EPI_STORE_BF16) epi.out_bf16[m * epi.ld_bf16 + n] = __float2bfloat16(v * rj + bias);
+              else epi.out_f32[m * epi.ld_out + n] += epi.scale * v;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) (void)__shfl_sync(0xffffffffu, rs, j);
+          }
+          continue;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) tile[j * kPitch + tid] = __uint_as_float(r[j]);
+        gemm_detail::epi_row_meta(epi, 0, kChunk, tc0, M, s_rstd, s_row, tid, 128);
+        sync();
+        gemm_detail::epi_apply(epi, tile, kPitch, 0, kChunk, tc0, n0, n_tile, n_tiles, M, N, s_rstd,
+                               s_row, tid, 128, sync);
+        sync();  // the staged chunk is reused next
+      }
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_free<2 * TOK>(tmem);
+}
+
+int num_sms_cached() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <int TOK>
+cudaError_t launch_big(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K,
+                       const EpiParams& epi, cudaStream_t stream) {
+  using L = BigLayout<TOK>;
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      gemm_big_kernel<TOK>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
+  if (attr != cudaSuccess) return attr;
+  const int tiles = ((N + kBN - 1) / kBN) * ((M + TOK - 1) / TOK);
+  const int grid = tiles < num_sms_cached() ? tiles : num_sms_cached();
+  return launch_pdl(gemm_big_kernel<TOK>, dim3(grid), dim3(kThreads), (size_t)L::kAlloc, stream,
+                    dim3(1, 1, 1), tw, tx, M, N, K, epi);
+}
+
+}  // namespace
+
+// Measured on B200 (tools/gemm_bench.py, Qwen2.5 0.5B/1.5B/7B shapes,
+// M = 200..16384): the persistent kernel wins from ~36 tiles of 128 x 128 on;
+// below that, or for a long K on less than one wave of tiles (7B down
+// projection at M = 256), the cluster split-K kernel fills the machine
+// better.  256-token tiles pay off once there are two waves of them.
+int gemm_big_tok(int M, int N, int K, int num_sms) {
+  if (M <= 128) return 0;
+  const int n_tiles = (N + kBN - 1) / kBN;
+  if (n_tiles * ((M + 255) / 256) >= 2 * num_sms) return 256;
+  const int t128 = n_tiles * ((M + 127) / 128);
+  if (t128 < 36 || (K >= 8192 && t128 < num_sms)) return 0;
+  return 128;
+}
+
+cudaError_t gemm_big_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int tok,
+                            const EpiParams& epi, cudaStream_t stream) {
+  if (tok == 256) return launch_big<256>(tw, tx, M, N, K, epi, stream);
+  if (tok == 128) return launch_big<128>(tw, tx, M, N, K, epi, stream);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace srl

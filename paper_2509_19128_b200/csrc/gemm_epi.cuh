@@ -1,0 +1,196 @@
+// gemm_epi.cuh -- the fused GEMM epilogues (EpiKind), shared by the
+// one-tile-per-CTA decode GEMM (gemm.cu) and the persistent large-M GEMM
+// (gemm_big.cu).
+//
+// Both kernels stage a block of the fp32 accumulator tile in shared memory as
+// tile[j * pitch + c]: j = token row of the block (global row t0 + j), c = one
+// of the tile's 128 output columns (global column n0 + c).  `tid`/`nthr` are
+// the cooperating threads (a multiple of 32, >= 64); `sync()` is their barrier.
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "gemm.cuh"
+
+namespace srl::gemm_detail {
+
+__device__ __forceinline__ float epi_bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float epi_warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double epi_warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float epi_warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Per-row inputs of rows [r0, r1): the deferred-RMSNorm rstd and (EPI_QKV)
+// the row's KV-cache coordinates (slot, pos, page, offset in page).
+__device__ __forceinline__ void epi_row_meta(const EpiParams& epi, int r0, int r1, int t0, int M,
+                                             float* s_rstd, int4* s_row, int tid, int nthr) {
+  for (int j = r0 + tid; j < r1; j += nthr) {
+    float r = 1.f;
+    const int m = t0 + j;
+    if (epi.ssq_in != nullptr && m < M) {
+      float s = 0.f;
+      for (int p = 0; p < epi.ssq_in_parts; ++p) s += epi.ssq_in[(size_t)m * epi.ssq_in_parts + p];
+      r = rsqrtf(s * epi.inv_dim + epi.eps);
+    }
+    s_rstd[j] = r;
+    if (epi.kind == EPI_QKV) {
+      int4 rc = make_int4(-1, 0, 0, 0);
+      if (m < M) {
+        rc.x = epi.row_slot[m];
+        rc.y = epi.row_pos[m];
+        if (rc.x >= 0) {
+          rc.z = epi.block_table[(size_t)rc.x * epi.pages_per_seq + rc.y / 64];
+          rc.w = rc.y % 64;
+        }
+      }
+      s_row[j] = rc;
+    }
+  }
+}
+
+// The epilogue over rows [r0, r1) of the staged block.  n_tile / n_tiles
+// index the per-(row, 128-column tile) outputs (EPI_LOGITS, EPI_RESID ssq).
+template <class Sync>
+__device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int pitch, int r0, int r1,
+                                          int t0, int n0, int n_tile, int n_tiles, int M, int N,
+                                          const float* s_rstd, const int4* s_row, int tid, int nthr,
+                                          Sync sync) {
+  const int rows = r1 - r0;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
+  if (epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16) {
+#pragma unroll 4
+    for (int idx = tid; idx < rows * 128; idx += nthr) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
+      const int m = t0 + j, n = n0 + c;
+      if (m >= M || n >= N) continue;
+      float v = tile[j * pitch + c] * s_rstd[j];
+      if (epi.bias) v += epi_bf2f(epi.bias[n]);
+      if (epi.kind == EPI_STORE_F32)
+        epi.out_f32[(size_t)m * epi.ld_out + n] = v;
+      else
+        epi.out_bf16[(size_t)m * epi.ld_bf16 + n] = __float2bfloat16(v);
+    }
+  } else if (epi.kind == EPI_ACCUM_F32) {
+    for (int idx = tid; idx < rows * 128; idx += nthr) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
+      const int m = t0 + j, n = n0 + c;
+      if (m >= M || n >= N) continue;
+      epi.out_f32[(size_t)m * epi.ld_out + n] += epi.scale * tile[j * pitch + c];
+    }
+  } else if (epi.kind == EPI_SWIGLU) {
+#pragma unroll 4
+    for (int idx = tid; idx < rows * 64; idx += nthr) {
+      const int j = r0 + (idx >> 6), c = idx & 63;
+      const int m = t0 + j;
+      if (m >= M || n0 + c >= N) continue;
+      const float g = tile[j * pitch + c] * s_rstd[j];
+      const float u = tile[j * pitch + 64 + c] * s_rstd[j];
+      const float a = g / (1.f + expf(-g)) * u;
+      epi.out_bf16[(size_t)m * epi.ld_bf16 + (n0 >> 1) + c] = __float2bfloat16(a);
+    }
+  } else if (epi.kind == EPI_QKV) {
+    for (int idx = tid; idx < rows * 128; idx += nthr) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
+      const int n = n0 + c;
+      float v = 0.f;
+      if (t0 + j < M && n < N) v = tile[j * pitch + c] * s_rstd[j] + epi_bf2f(epi.bias[n]);
+      tile[j * pitch + c] = v;
+    }
+    sync();
+    const int hd = epi.hd, half = hd >> 1;
+    const int qend = epi.nq * hd, kend = (epi.nq + epi.nkv) * hd;
+    for (int idx = tid; idx < rows * 128; idx += nthr) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
+      const int m = t0 + j, n = n0 + c;
+      const int4 rc = s_row[j];
+      if (m >= M || n >= N || rc.x < 0) continue;
+      const int jj = n % hd;
+      const float* row = &tile[j * pitch + (c - jj)];  // this head's hd values
+      float y;
+      if (n < kend) {  // RoPE (rotate pairs (i, i + hd/2)) on q and k
+        const int i = jj < half ? jj : jj - half;
+        const float co = epi.cos_sin[(size_t)rc.y * hd + i];
+        const float si = epi.cos_sin[(size_t)rc.y * hd + half + i];
+        const float x1 = row[i], x2 = row[i + half];
+        y = jj < half ? x1 * co - x2 * si : x2 * co + x1 * si;
+      } else {
+        y = row[jj];
+      }
+      const __nv_bfloat16 b = __float2bfloat16(y);
+      if (n < qend) {
+        epi.q_out[(size_t)m * qend + n] = b;
+      } else {
+        const int kv = n < kend ? n - qend : n - kend;
+        const int kh = kv / hd;
+        const size_t at = (((size_t)rc.z * epi.nkv + kh) * 64 + rc.w) * hd + jj;
+        if (n < kend) epi.kc[at] = b;
+        else epi.vc[at] = b;
+      }
+    }
+  } else if (epi.kind == EPI_LOGITS) {
+    for (int idx = tid; idx < rows * 128; idx += nthr) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
+      const int m = t0 + j, n = n0 + c;
+      float v = -INFINITY;
+      if (m < M && n < N) {
+        v = tile[j * pitch + c] * s_rstd[j];
+        epi.out_f32[(size_t)m * epi.ld_out + n] = v;
+      }
+      tile[j * pitch + c] = v;
+    }
+    sync();
+    for (int j = r0 + warp; j < r1; j += nwarps) {
+      const float4 x = *reinterpret_cast<const float4*>(&tile[j * pitch + lane * 4]);
+      const float mx = epi_warp_max(fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
+      double s = 0.0;
+      if (mx != -INFINITY) {
+        const double md = (double)mx;
+        s = exp((double)x.x - md) + exp((double)x.y - md) + exp((double)x.z - md) +
+            exp((double)x.w - md);
+      }
+      s = epi_warp_sum_d(s);
+      const int m = t0 + j;
+      if (lane == 0 && m < M) {
+        epi.part_max[(size_t)m * n_tiles + n_tile] = mx;
+        epi.part_sum[(size_t)m * n_tiles + n_tile] = s;
+      }
+    }
+  } else if (epi.kind == EPI_RESID) {
+#pragma unroll 4
+    for (int idx = tid; idx < rows * 128; idx += nthr) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
+      const int m = t0 + j, n = n0 + c;
+      float x = 0.f;
+      if (m < M && n < N) {
+        const size_t o = (size_t)m * N + n;
+        x = epi.resid[o] + tile[j * pitch + c];
+        epi.resid[o] = x;
+        epi.xg[o] = __float2bfloat16(x * epi_bf2f(epi.gain[n]));
+      }
+      tile[j * pitch + c] = x;
+    }
+    sync();
+    for (int j = r0 + warp; j < r1; j += nwarps) {
+      float s = 0.f;
+      for (int c = lane; c < 128; c += 32) {
+        const float x = tile[j * pitch + c];
+        s += x * x;
+      }
+      s = epi_warp_sum(s);
+      if (lane == 0 && t0 + j < M) epi.ssq_out[(size_t)(t0 + j) * n_tiles + n_tile] = s;
+    }
+  }
+}
+
+}  // namespace srl::gemm_detail

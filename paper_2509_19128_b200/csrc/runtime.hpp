@@ -112,6 +112,7 @@ class Backend {
   virtual void request_profile() {}
   virtual bool kernel_profile(srl_kernel_profile* out) const { return false; }
   virtual int64_t launches() const { return launches_; }
+  virtual void prefill_stats(srl_engine_stats* s) const { (void)s; }
   virtual int prompt_index(const std::string& prompt_id) { return intern(prompt_id); }
   int intern(const std::string& s) {
     auto it = prompts_.find(s);

@@ -51,8 +51,14 @@ void launch_attention_bwd(const __nv_bfloat16* q, const __nv_bfloat16* o, const 
                           const float* lse, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                           const int32_t* row_slot, const int32_t* row_pos,
                           const int32_t* seq_start, const int32_t* seq_len,
-                          const int32_t* block_table, int pages_per_seq, int T, int nq, int nkv,
-                          int hd, float* dqkv, cudaStream_t st);
+                          const int32_t* block_table, int pages_per_seq, int T, int n_seq, int nq,
+                          int nkv, int hd, float* dqkv, cudaStream_t st);
+// The tensor-core path of the above (train_attn.cu); D = rowsum(dO * O).
+cudaError_t launch_attention_bwd_mma(const __nv_bfloat16* q, const float* d_o, const float* lse,
+                                     const float* D, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
+                                     const int32_t* seq_start, const int32_t* seq_len,
+                                     const int32_t* block_table, int pages_per_seq, int n_seq, int nq,
+                                     int nkv, int hd, float* dqkv, cudaStream_t st);
 // Undo RoPE on the q/k part of dqkv in place (rotation by -angle).
 void launch_rope_bwd(float* dqkv, const int32_t* row_pos, const float* cos_sin, int T, int nq,
                      int nkv, int hd, cudaStream_t st);

@@ -1,0 +1,378 @@
+// train_attn.cu -- causal GQA attention backward of the trainer on the tensor
+// cores (mma.sync m16n8k16 bf16 -> fp32), tiled FlashAttention-2 style.
+//
+// The trainer's forward keeps q (post-RoPE, bf16), the attention output o,
+// the per-(row, head) log-sum-exp and writes K/V into a paged cache (one
+// 64-token page per block of a sequence).  With D = rowsum(dO * O):
+//   P  = exp(scale * Q K^T - lse)          (causal)
+//   dV = P^T dO,   dP = dO V^T,   dS = P * (dP - D)
+//   dQ = scale * dS K,   dK = scale * dS^T Q
+// Two deterministic kernels (no atomics):
+//   attn_bwd_dkv_mma : CTA = (64-key block, sequence, KV head); loops over the
+//                      G query heads of the group and the causal query blocks;
+//   attn_bwd_dq_mma  : CTA = (64-query block, sequence, query head); loops
+//                      over the causal key blocks.
+// Four warps per CTA, each owning 16 rows (keys resp. queries) of the block.
+// P and dS enter the second GEMM of each pair as bf16, as in the forward.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "decoder.cuh"
+#include "train.cuh"
+
+namespace srl {
+namespace {
+
+constexpr int kBlk = 64;      // keys / queries per block (= one KV page)
+constexpr int kWarps = 4;
+constexpr int kPadT = kBlk + 8;  // transposed tiles [HD][64 + 8]
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+__device__ __forceinline__ uint32_t ld32(const __nv_bfloat16* p) {
+  return *reinterpret_cast<const uint32_t*>(p);
+}
+// A fragment (16 x 16) of a row-major bf16 tile X[row][col] with pitch P.
+__device__ __forceinline__ void frag_a(uint32_t (&a)[4], const __nv_bfloat16* X, int P, int r0, int c0,
+                                       int lane) {
+  const int r = r0 + (lane >> 2), c = c0 + (lane & 3) * 2;
+  a[0] = ld32(X + r * P + c);
+  a[1] = ld32(X + (r + 8) * P + c);
+  a[2] = ld32(X + r * P + c + 8);
+  a[3] = ld32(X + (r + 8) * P + c + 8);
+}
+// B fragment (16 x 8, B[k][n]) read from Y[n][k] (k contiguous), pitch P.
+__device__ __forceinline__ void frag_b(uint32_t& b0, uint32_t& b1, const __nv_bfloat16* Y, int P, int n0,
+                                       int k0, int lane) {
+  const __nv_bfloat16* p = Y + (n0 + (lane >> 2)) * P + k0 + (lane & 3) * 2;
+  b0 = ld32(p);
+  b1 = ld32(p + 8);
+}
+
+__device__ __forceinline__ const __nv_bfloat16* page_row(const __nv_bfloat16* c, const int32_t* bt, int pps,
+                                                         int slot, int pos, int nkv, int kh, int hd) {
+  const int page = bt[(size_t)slot * pps + pos / kPageTokens];
+  return c + (((size_t)page * nkv + kh) * kPageTokens + (pos % kPageTokens)) * hd;
+}
+
+// Stage 64 rows x HD of a bf16 source (row r -> src(r) or zeros past L) into
+// X[64][HD + 8] and, if XT, its transpose XT[HD][64 + 8].
+template <int HD, class Src>
+__device__ __forceinline__ void stage_bf16(__nv_bfloat16* X, __nv_bfloat16* XT, int valid, Src src) {
+  constexpr int P = HD + 8, V8 = HD / 8;
+  for (int e = threadIdx.x; e < kBlk * V8; e += kWarps * 32) {
+    const int r = e / V8, c = (e % V8) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < valid) v = *reinterpret_cast<const uint4*>(src(r) + c);
+    *reinterpret_cast<uint4*>(X + r * P + c) = v;
+    if (XT) {
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) XT[(c + i) * kPadT + r] = h[i];
+    }
+  }
+}
+// Same for an fp32 source (dO), rounded to bf16.
+template <int HD, class Src>
+__device__ __forceinline__ void stage_f32(__nv_bfloat16* X, __nv_bfloat16* XT, int valid, Src src) {
+  constexpr int P = HD + 8, V4 = HD / 4;
+  for (int e = threadIdx.x; e < kBlk * V4; e += kWarps * 32) {
+    const int r = e / V4, c = (e % V4) * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < valid) v = *reinterpret_cast<const float4*>(src(r) + c);
+    const __nv_bfloat16 h[4] = {__float2bfloat16(v.x), __float2bfloat16(v.y), __float2bfloat16(v.z),
+                                __float2bfloat16(v.w)};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      X[r * P + c + i] = h[i];
+      if (XT) XT[(c + i) * kPadT + r] = h[i];
+    }
+  }
+}
+
+template <int HD>
+struct BwdSmem {
+  static constexpr int P = HD + 8;
+  static constexpr size_t tile = sizeof(__nv_bfloat16) * kBlk * P;
+  static constexpr size_t tileT = sizeof(__nv_bfloat16) * HD * kPadT;
+  static constexpr size_t vec = sizeof(float) * kBlk;
+  // dkv: K, V, Q, Q^T, dO, dO^T, lse, D ; dq: Q, dO, K, K^T, V, lse, D
+  static constexpr size_t dkv = 4 * tile + 2 * tileT + 2 * vec;
+  static constexpr size_t dq = 4 * tile + tileT + 2 * vec;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kWarps * 32)
+    attn_bwd_dkv_mma(const __nv_bfloat16* __restrict__ q, const float* __restrict__ d_o,
+                     const float* __restrict__ lse, const float* __restrict__ D,
+                     const __nv_bfloat16* __restrict__ kc, const __nv_bfloat16* __restrict__ vc,
+                     const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_len,
+                     const int32_t* __restrict__ bt, int pps, int nq, int nkv, float scale,
+                     float* __restrict__ dqkv) {
+  using S = BwdSmem<HD>;
+  constexpr int P = S::P, NT = HD / 8;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem);
+  __nv_bfloat16* Vs = reinterpret_cast<__nv_bfloat16*>(smem + S::tile);
+  __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smem + 2 * S::tile);
+  __nv_bfloat16* dOs = reinterpret_cast<__nv_bfloat16*>(smem + 3 * S::tile);
+  __nv_bfloat16* Qt = reinterpret_cast<__nv_bfloat16*>(smem + 4 * S::tile);
+  __nv_bfloat16* dOt = reinterpret_cast<__nv_bfloat16*>(smem + 4 * S::tile + S::tileT);
+  float* s_lse = reinterpret_cast<float*>(smem + 4 * S::tile + 2 * S::tileT);
+  float* s_D = s_lse + kBlk;
+
+  const int slot = blockIdx.y, kh = blockIdx.z;
+  const int L = seq_len[slot], s0 = seq_start[slot];
+  const int k0 = blockIdx.x * kBlk;
+  if (k0 >= L) return;
+  const int G = nq / nkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kvalid = min(kBlk, L - k0);
+  stage_bf16<HD>(Ks, nullptr, kvalid, [&](int r) { return page_row(kc, bt, pps, slot, k0 + r, nkv, kh, HD); });
+  stage_bf16<HD>(Vs, nullptr, kvalid, [&](int r) { return page_row(vc, bt, pps, slot, k0 + r, nkv, kh, HD); });
+
+  float dk[NT][4], dv[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dk[n][i] = dv[n][i] = 0.f;
+  const int kr = warp * 16;  // this warp's 16 keys (block-local)
+  const int key_lo = k0 + kr + (lane >> 2), key_hi = key_lo + 8;
+
+  for (int g = 0; g < G; ++g) {
+    const int h = kh * G + g;
+    for (int q0 = k0; q0 < L; q0 += kBlk) {
+      const int qvalid = min(kBlk, L - q0);
+      __syncthreads();  // previous tiles consumed
+      stage_bf16<HD>(Qs, Qt, qvalid, [&](int r) { return q + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+      stage_f32<HD>(dOs, dOt, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+      for (int r = threadIdx.x; r < kBlk; r += kWarps * 32) {
+        s_lse[r] = r < qvalid ? lse[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
+        s_D[r] = r < qvalid ? D[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
+      }
+      __syncthreads();
+      // S^T = K_w Q^T and dP^T = V_w dO^T: [16 keys x 64 queries]
+      float st[8][4], dpt[8][4];
+#pragma unroll
+      for (int n = 0; n < 8; ++n)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) st[n][i] = dpt[n][i] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        uint32_t ak[4], av[4];
+        frag_a(ak, Ks, P, kr, kk * 16, lane);
+        frag_a(av, Vs, P, kr, kk * 16, lane);
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          uint32_t b0, b1;
+          frag_b(b0, b1, Qs, P, n * 8, kk * 16, lane);
+          mma16816(st[n], ak, b0, b1);
+          frag_b(b0, b1, dOs, P, n * 8, kk * 16, lane);
+          mma16816(dpt[n], av, b0, b1);
+        }
+      }
+      // P^T and dS^T (scaled), causal: query position >= key position
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int ql = n * 8 + (lane & 3) * 2 + (i & 1);
+          const int qpos = q0 + ql, kpos = i < 2 ? key_lo : key_hi;
+          const bool ok = ql < qvalid && qpos >= kpos && kpos < L;
+          const float p = ok ? __expf(st[n][i] * scale - s_lse[ql]) : 0.f;
+          st[n][i] = p;
+          dpt[n][i] = p * (dpt[n][i] - s_D[ql]) * scale;
+        }
+      }
+      // dV += P^T dO, dK += dS^T Q   (k = 64 queries in 4 steps of 16)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        uint32_t ap[4], ad[4];
+        ap[0] = pack_bf16(st[2 * ks][0], st[2 * ks][1]);
+        ap[1] = pack_bf16(st[2 * ks][2], st[2 * ks][3]);
+        ap[2] = pack_bf16(st[2 * ks + 1][0], st[2 * ks + 1][1]);
+        ap[3] = pack_bf16(st[2 * ks + 1][2], st[2 * ks + 1][3]);
+        ad[0] = pack_bf16(dpt[2 * ks][0], dpt[2 * ks][1]);
+        ad[1] = pack_bf16(dpt[2 * ks][2], dpt[2 * ks][3]);
+        ad[2] = pack_bf16(dpt[2 * ks + 1][0], dpt[2 * ks + 1][1]);
+        ad[3] = pack_bf16(dpt[2 * ks + 1][2], dpt[2 * ks + 1][3]);
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          uint32_t b0, b1;
+          frag_b(b0, b1, dOt, kPadT, n * 8, ks * 16, lane);
+          mma16816(dv[n], ap, b0, b1);
+          frag_b(b0, b1, Qt, kPadT, n * 8, ks * 16, lane);
+          mma16816(dk[n], ad, b0, b1);
+        }
+      }
+    }
+  }
+  // write dk / dv rows (fp32, pre-RoPE rotation applied by the caller)
+  const int qkv = (nq + 2 * nkv) * HD;
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int kpos = i < 2 ? key_lo : key_hi;
+      if (kpos >= L) continue;
+      const int d = n * 8 + (lane & 3) * 2 + (i & 1);
+      float* row = dqkv + (size_t)(s0 + kpos) * qkv;
+      row[nq * HD + kh * HD + d] = dk[n][i];
+      row[(nq + nkv) * HD + kh * HD + d] = dv[n][i];
+    }
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kWarps * 32)
+    attn_bwd_dq_mma(const __nv_bfloat16* __restrict__ q, const float* __restrict__ d_o,
+                    const float* __restrict__ lse, const float* __restrict__ D,
+                    const __nv_bfloat16* __restrict__ kc, const __nv_bfloat16* __restrict__ vc,
+                    const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_len,
+                    const int32_t* __restrict__ bt, int pps, int nq, int nkv, float scale,
+                    float* __restrict__ dqkv) {
+  using S = BwdSmem<HD>;
+  constexpr int P = S::P, NT = HD / 8;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smem);
+  __nv_bfloat16* dOs = reinterpret_cast<__nv_bfloat16*>(smem + S::tile);
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem + 2 * S::tile);
+  __nv_bfloat16* Vs = reinterpret_cast<__nv_bfloat16*>(smem + 3 * S::tile);
+  __nv_bfloat16* Kt = reinterpret_cast<__nv_bfloat16*>(smem + 4 * S::tile);
+  float* s_lse = reinterpret_cast<float*>(smem + 4 * S::tile + S::tileT);
+  float* s_D = s_lse + kBlk;
+
+  const int slot = blockIdx.y, h = blockIdx.z;
+  const int L = seq_len[slot], s0 = seq_start[slot];
+  const int q0 = blockIdx.x * kBlk;
+  if (q0 >= L) return;
+  const int kh = h / (nq / nkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qvalid = min(kBlk, L - q0);
+  stage_bf16<HD>(Qs, nullptr, qvalid, [&](int r) { return q + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+  stage_f32<HD>(dOs, nullptr, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+  for (int r = threadIdx.x; r < kBlk; r += kWarps * 32) {
+    s_lse[r] = r < qvalid ? lse[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
+    s_D[r] = r < qvalid ? D[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
+  }
+  const int qr = warp * 16;
+  const int ql_lo = qr + (lane >> 2), ql_hi = ql_lo + 8;
+  float dq[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dq[n][i] = 0.f;
+
+  for (int k0 = 0; k0 <= q0; k0 += kBlk) {
+    const int kvalid = min(kBlk, L - k0);
+    __syncthreads();
+    stage_bf16<HD>(Ks, Kt, kvalid, [&](int r) { return page_row(kc, bt, pps, slot, k0 + r, nkv, kh, HD); });
+    stage_bf16<HD>(Vs, nullptr, kvalid, [&](int r) { return page_row(vc, bt, pps, slot, k0 + r, nkv, kh, HD); });
+    __syncthreads();
+    float s[8][4], dp[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s[n][i] = dp[n][i] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      uint32_t aq[4], ad[4];
+      frag_a(aq, Qs, P, qr, kk * 16, lane);
+      frag_a(ad, dOs, P, qr, kk * 16, lane);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        uint32_t b0, b1;
+        frag_b(b0, b1, Ks, P, n * 8, kk * 16, lane);
+        mma16816(s[n], aq, b0, b1);
+        frag_b(b0, b1, Vs, P, n * 8, kk * 16, lane);
+        mma16816(dp[n], ad, b0, b1);
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int kl = n * 8 + (lane & 3) * 2 + (i & 1);
+        const int ql = i < 2 ? ql_lo : ql_hi;
+        const int kpos = k0 + kl, qpos = q0 + ql;
+        const bool ok = kl < kvalid && kpos <= qpos && ql < qvalid;
+        const float p = ok ? __expf(s[n][i] * scale - s_lse[ql]) : 0.f;
+        dp[n][i] = p * (dp[n][i] - s_D[ql]) * scale;
+      }
+    }
+    // dQ += dS K  (k = 64 keys in 4 steps of 16)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      uint32_t a[4];
+      a[0] = pack_bf16(dp[2 * ks][0], dp[2 * ks][1]);
+      a[1] = pack_bf16(dp[2 * ks][2], dp[2 * ks][3]);
+      a[2] = pack_bf16(dp[2 * ks + 1][0], dp[2 * ks + 1][1]);
+      a[3] = pack_bf16(dp[2 * ks + 1][2], dp[2 * ks + 1][3]);
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        uint32_t b0, b1;
+        frag_b(b0, b1, Kt, kPadT, n * 8, ks * 16, lane);
+        mma16816(dq[n], a, b0, b1);
+      }
+    }
+  }
+  const int qkv = (nq + 2 * nkv) * HD;
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int ql = i < 2 ? ql_lo : ql_hi;
+      if (ql >= qvalid) continue;
+      const int d = n * 8 + (lane & 3) * 2 + (i & 1);
+      dqkv[(size_t)(s0 + q0 + ql) * qkv + h * HD + d] = dq[n][i];
+    }
+  }
+}
+
+template <int HD>
+cudaError_t launch_t(const __nv_bfloat16* q, const float* d_o, const float* lse, const float* D,
+                     const __nv_bfloat16* kc, const __nv_bfloat16* vc, const int32_t* seq_start,
+                     const int32_t* seq_len, const int32_t* bt, int pps, int n_seq, int nq, int nkv,
+                     float scale, float* dqkv, cudaStream_t st) {
+  using S = BwdSmem<HD>;
+  static const bool attr = cudaFuncSetAttribute(attn_bwd_dkv_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)S::dkv) == cudaSuccess &&
+                           cudaFuncSetAttribute(attn_bwd_dq_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)S::dq) == cudaSuccess;
+  if (!attr) return cudaErrorInvalidValue;
+  // pages per sequence = 64-token blocks per sequence
+  attn_bwd_dkv_mma<HD><<<dim3(pps, n_seq, nkv), kWarps * 32, S::dkv, st>>>(
+      q, d_o, lse, D, kc, vc, seq_start, seq_len, bt, pps, nq, nkv, scale, dqkv);
+  attn_bwd_dq_mma<HD><<<dim3(pps, n_seq, nq), kWarps * 32, S::dq, st>>>(
+      q, d_o, lse, D, kc, vc, seq_start, seq_len, bt, pps, nq, nkv, scale, dqkv);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_attention_bwd_mma(const __nv_bfloat16* q, const float* d_o, const float* lse,
+                                     const float* D, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
+                                     const int32_t* seq_start, const int32_t* seq_len,
+                                     const int32_t* block_table, int pages_per_seq, int n_seq, int nq,
+                                     int nkv, int hd, float* dqkv, cudaStream_t st) {
+  const float scale = 1.0f / sqrtf((float)hd);
+  if (hd == 64)
+    return launch_t<64>(q, d_o, lse, D, kc, vc, seq_start, seq_len, block_table, pages_per_seq, n_seq,
+                        nq, nkv, scale, dqkv, st);
+  if (hd == 128)
+    return launch_t<128>(q, d_o, lse, D, kc, vc, seq_start, seq_len, block_table, pages_per_seq, n_seq,
+                         nq, nkv, scale, dqkv, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace srl

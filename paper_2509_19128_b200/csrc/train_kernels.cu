@@ -1,3 +1,4 @@
+#include <cstdlib>
 // train_kernels.cu -- non-GEMM kernels of the decoder trainer step (see
 // train.cuh).  Correctness-first CUDA-core implementations; every reduction
 // over rows that feeds a weight gradient uses fp32 atomics (gradients are
@@ -415,20 +416,27 @@ void launch_attention_bwd(const __nv_bfloat16* q, const __nv_bfloat16* o, const 
                           const float* lse, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                           const int32_t* row_slot, const int32_t* row_pos,
                           const int32_t* seq_start, const int32_t* seq_len,
-                          const int32_t* block_table, int pages_per_seq, int T, int nq, int nkv,
-                          int hd, float* dqkv, cudaStream_t st) {
+                          const int32_t* block_table, int pages_per_seq, int T, int n_seq, int nq,
+                          int nkv, int hd, float* dqkv, cudaStream_t st) {
   float* D = nullptr;
   cudaMallocAsync(&D, sizeof(float) * (size_t)T * nq, st);
-  const float scale = 1.0f / sqrtf((float)hd);
-  const int w1 = T * nq, w2 = T * nkv;
+  const int w1 = T * nq;
   attn_bwd_dot_kernel<<<(w1 * 32 + 255) / 256, 256, 0, st>>>(d_o, o, T, nq, hd, D);
-  attn_bwd_dq_kernel<<<(w1 * 32 + 255) / 256, 256, 0, st>>>(q, d_o, lse, D, kc, vc, row_slot, row_pos,
-                                                             block_table, pages_per_seq, T, nq, nkv,
-                                                             hd, scale, dqkv);
-  attn_bwd_dkv_kernel<<<(w2 * 32 + 255) / 256, 256, 0, st>>>(q, d_o, lse, D, kc, vc, row_slot,
-                                                              row_pos, seq_start, seq_len,
-                                                              block_table, pages_per_seq, T, nq,
-                                                              nkv, hd, scale, dqkv);
+  static const bool scalar = std::getenv("SRL_ATTN_BWD_SCALAR") != nullptr;  // A/B: the CUDA-core path
+  if (!scalar) {
+    launch_attention_bwd_mma(q, d_o, lse, D, kc, vc, seq_start, seq_len, block_table, pages_per_seq,
+                             n_seq, nq, nkv, hd, dqkv, st);
+  } else {
+    const float scale = 1.0f / sqrtf((float)hd);
+    const int w2 = T * nkv;
+    attn_bwd_dq_kernel<<<(w1 * 32 + 255) / 256, 256, 0, st>>>(q, d_o, lse, D, kc, vc, row_slot, row_pos,
+                                                               block_table, pages_per_seq, T, nq, nkv,
+                                                               hd, scale, dqkv);
+    attn_bwd_dkv_kernel<<<(w2 * 32 + 255) / 256, 256, 0, st>>>(q, d_o, lse, D, kc, vc, row_slot,
+                                                                row_pos, seq_start, seq_len,
+                                                                block_table, pages_per_seq, T, nq,
+                                                                nkv, hd, scale, dqkv);
+  }
   cudaFreeAsync(D, st);
 }
 void launch_rope_bwd(float* dqkv, const int32_t* row_pos, const float* cos_sin, int T, int nq,

@@ -72,7 +72,10 @@ int decoder_policy_logprobs(const DecoderWeights& w, const std::vector<int32_t>&
 
 // ----------------------------------------------------------- trainer ---
 namespace {
-constexpr int kLogitChunk = 512;  // rows per LM-head pass (logits chunk = 512 x V fp32)
+// rows per LM-head pass: the logits chunk is [chunk x V] fp32.  Large chunks
+// keep the LM-head GEMMs efficient and, above all, accumulate the [V x H] fp32
+// LM-head gradient (a read-modify-write of 0.5 GB at V = 152k) few times.
+constexpr int kLogitChunkMax = 4096;
 int pad64(int x) { return (x + 63) / 64 * 64; }
 }  // namespace
 
@@ -104,6 +107,7 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
   lay_ = weights_->layout;
   n_ = lay_.total;
   T_max_ = pad64(std::max(64, o.max_tokens));
+  chunk_ = std::min(kLogitChunkMax, T_max_);
   const int H = d_.H, L = d_.L, I = d_.I, qd = d_.qdim(), qkv = d_.qkv();
   // fp32 master weights, Adam moments, gradient, transposed bf16 weights
   if ((st = alloc(&master_, n_)) || (st = alloc(&grad_, n_)) || (st = alloc(&adam_m_, n_)) ||
@@ -124,11 +128,11 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
   }
   if ((st = alloc(&x_, (size_t)T_max_ * H)) || (st = alloc(&xgF_, (size_t)T_max_ * H)) ||
       (st = alloc(&rstdF_, T_max_)) || (st = alloc(&ssq_, (size_t)T_max_ * d_.ssq_parts())) ||
-      (st = alloc(&logits_, (size_t)kLogitChunk * d_.V)) ||
-      (st = alloc(&pmax_, (size_t)kLogitChunk * ((d_.V + 127) / 128))) ||
-      (st = alloc(&psum_, (size_t)kLogitChunk * ((d_.V + 127) / 128))) ||
-      (st = alloc(&dlogits_, (size_t)kLogitChunk * d_.V)) ||
-      (st = alloc(&dlogitsT_, (size_t)d_.V * kLogitChunk)) || (st = alloc(&dx_, (size_t)T_max_ * H)) ||
+      (st = alloc(&logits_, (size_t)chunk_ * d_.V)) ||
+      (st = alloc(&pmax_, (size_t)chunk_ * ((d_.V + 127) / 128))) ||
+      (st = alloc(&psum_, (size_t)chunk_ * ((d_.V + 127) / 128))) ||
+      (st = alloc(&dlogits_, (size_t)chunk_ * d_.V)) ||
+      (st = alloc(&dlogitsT_, (size_t)d_.V * chunk_)) || (st = alloc(&dx_, (size_t)T_max_ * H)) ||
       (st = alloc(&dz_, (size_t)T_max_ * std::max(H, 2 * I))) ||
       (st = alloc(&dbig_, (size_t)T_max_ * std::max({2 * I, qkv, qd}))) ||
       (st = alloc(&dbig_bf_, (size_t)T_max_ * std::max({2 * I, qkv, qd, H}))) ||
@@ -297,8 +301,8 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
 
   // ---- pass 1: log pi(target) of every row
   const int nT = (V + 127) / 128;
-  for (int c0 = 0; c0 < T; c0 += kLogitChunk) {
-    const int C = std::min(kLogitChunk, T - c0);
+  for (int c0 = 0; c0 < T; c0 += chunk_) {
+    const int C = std::min(chunk_, T - c0);
     EpiParams e;
     e.kind = EPI_LOGITS;
     e.ssq_in = ssq_ + (size_t)c0 * parts; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d_.eps;
@@ -353,8 +357,8 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
   launch_zero(dx_, (size_t)T_max_ * H, st);
   // pass 2: dlogits per chunk -> d(final xg) and dE(lm_head)
   float* g_lm = grad_ + lay_.lm_head;
-  for (int c0 = 0; c0 < T; c0 += kLogitChunk) {
-    const int C = std::min(kLogitChunk, T - c0), Cp = pad64(C);
+  for (int c0 = 0; c0 < T; c0 += chunk_) {
+    const int C = std::min(chunk_, T - c0), Cp = pad64(C);
     EpiParams e;
     e.kind = EPI_LOGITS;
     e.ssq_in = ssq_ + (size_t)c0 * parts; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d_.eps;
@@ -404,7 +408,7 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
     if ((s = gemm_accum(tA_, H, tB_, qd, Tp, grad_ + o.o_w))) return s;
     // attention + RoPE backward -> dqkv (pre-RoPE, pre-bias) fp32
     launch_attention_bwd(a.q, a.attn, dz_, a.lse, kc_ + kv_elems * l, vc_ + kv_elems * l, row_slot_,
-                         row_pos_, d_sstart, d_slen, d_bt, pps, T, d_.nq, d_.nkv, d_.hd, dbig_, st);
+                         row_pos_, d_sstart, d_slen, d_bt, pps, T, n_seq, d_.nq, d_.nkv, d_.hd, dbig_, st);
     launch_rope_bwd(dbig_, row_pos_, cos_sin_, T, d_.nq, d_.nkv, d_.hd, st);
     launch_colsum_accum(dbig_, T, qkv, grad_ + o.qkv_b, st);
     launch_f32_to_bf16(dbig_, (size_t)T * qkv, dbig_bf_, st);

@@ -57,6 +57,7 @@ class DecoderTrainer {
   float *master_ = nullptr, *grad_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;
   __nv_bfloat16* wt_ = nullptr;  // transposed weights (same offsets)
   std::vector<LayerActs> acts_;
+  int chunk_ = 512;  // LM-head rows per pass (trainer.cpp, kLogitChunkMax)
   float *x_ = nullptr, *rstdF_ = nullptr, *ssq_ = nullptr, *logits_ = nullptr, *pmax_ = nullptr;
   double* psum_ = nullptr;
   __nv_bfloat16 *xgF_ = nullptr, *dlogits_ = nullptr, *dlogitsT_ = nullptr, *dbig_bf_ = nullptr,

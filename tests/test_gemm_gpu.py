@@ -30,9 +30,13 @@ def close(a, b, tol=2e-3):
     assert err <= tol * scale, f"max err {err} vs scale {scale}"
 
 
+# the last four shapes fill the machine with tiles, so they run the persistent
+# large-M kernel (gemm_big.cu, token tile 128 or 256; ragged M and N tails)
 @pytest.mark.parametrize("M,N,K,splits", [(64, 256, 128, 1), (64, 1152, 896, 0), (64, 896, 4864, 0),
                                           (37, 384, 256, 1), (200, 512, 512, 1), (64, 300, 192, 2),
-                                          (1, 128, 64, 1), (256, 1024, 896, 0)])
+                                          (1, 128, 64, 1), (256, 1024, 896, 0),
+                                          (2000, 1280, 896, 0), (4096, 9728, 896, 0),
+                                          (3001, 9700, 128, 0), (16384, 896, 4864, 0)])
 def test_gemm_store_f32(cuda, M, N, K, splits):
     g = torch.Generator(device=cuda).manual_seed(M * 7 + N)
     w = torch.randn(N, K, device=cuda, generator=g).bfloat16()
@@ -56,8 +60,8 @@ def test_gemm_deterministic_splitk(cuda):
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
 
 
-def test_gemm_rmsnorm_scale_and_swiglu(cuda):
-    M, N, K = 64, 1024, 256
+@pytest.mark.parametrize("M,N,K", [(64, 1024, 256), (4000, 9728, 896)])
+def test_gemm_rmsnorm_scale_and_swiglu(cuda, M, N, K):
     w = torch.randn(N, K, device=cuda).bfloat16()
     x = torch.randn(M, K, device=cuda).bfloat16()
     parts = 2
@@ -73,8 +77,9 @@ def test_gemm_rmsnorm_scale_and_swiglu(cuda):
     close(out, ref, tol=1e-2)
 
 
-def test_gemm_residual_epilogue(cuda):
-    M, N, K = 64, 896, 896
+@pytest.mark.parametrize("M", [64, 5000])
+def test_gemm_residual_epilogue(cuda, M):
+    N, K = 896, 896
     w = torch.randn(N, K, device=cuda).bfloat16()
     x = torch.randn(M, K, device=cuda).bfloat16()
     resid = torch.randn(M, N, device=cuda)
