@@ -501,7 +501,10 @@ def main():
         "clocks": clk,
     }
     if rank == 0 and not args.no_trainer:
+        tclk = ClockSampler(local)
+        tclk.start()
         out["trainer"] = trainer_measure(cfg, pol, args.train_seqs, args.prompt, args.gen)
+        out["trainer"]["clocks"] = tclk.stop()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tps, dt, cores = cpu_decode_sample(cfg, B, 8, args.cpu_steps, 1)
         out["cpu_baseline"] = {"value": tps, "unit": UNIT, "cores": cores, "kind": "port",

@@ -22,6 +22,8 @@ enum EpiKind : int {
   EPI_QKV = 4,         // rstd*acc + bias, RoPE on q/k, q -> bf16 rows, k/v -> paged KV cache
   EPI_LOGITS = 5,      // out_f32 = rstd*acc; per (row, 128-col tile): max and fp64 sum exp(x - max)
   EPI_ACCUM_F32 = 6,   // out_f32[m, n] += scale * acc  (gradient accumulation)
+  EPI_DLOGITS = 7,     // x = rstd*acc; d = coef[m] * (onehot(tgt[m]) - exp(x - lse[m])) -> bf16
+                       // out_bf16[m, n] and (outT_bf16) the transpose [n, m]
 };
 
 struct EpiParams {
@@ -54,6 +56,14 @@ struct EpiParams {
   float* part_max = nullptr;            // [M x ceil(N/128)]
   double* part_sum = nullptr;           // [M x ceil(N/128)]
   float scale = 1.f;                    // EPI_ACCUM_F32
+  // EPI_LOGITS (optional): out_f32 may be null (statistics only); the logit of
+  // column tgt_row[m] is stored to tgt_out[m].  EPI_DLOGITS: see above.
+  const int32_t* tgt_row = nullptr;
+  float* tgt_out = nullptr;
+  const double* lse_in = nullptr;
+  const float* row_coef = nullptr;
+  __nv_bfloat16* outT_bf16 = nullptr;
+  int ldT = 0;
   // debug: per-CTA %globaltimer phase stamps [ctas x 8] (null = off)
   unsigned long long* stamps = nullptr;
 };

@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* s_rstd = reinterpret_cast<float*>(smem + L::kRstd) + g * kChunk;
     int4* s_row = reinterpret_cast<int4*>(smem + L::kRow) + g * kChunk;
     auto sync = [g] { group_sync(g); };
-    const bool direct = epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16 || epi.kind == EPI_ACCUM_F32;
+    const bool direct = epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16 ||
+                        epi.kind == EPI_ACCUM_F32 || epi.kind == EPI_DLOGITS;
     bool waited = false;
     int acc = 0;
     uint32_t aph = 0;
@@ -192,6 +193,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const float bias = (epi.bias != nullptr && n < N) ? gemm_detail::epi_bf2f(epi.bias[n]) : 0.f;
           const int jn = min(32, M - tc0);
+          if (epi.kind == EPI_DLOGITS) {
+            // d = coef * (onehot - softmax) of token tc0 + j at vocab column n; the
+            // transposed copy [n][tokens] is 32 contiguous bf16 per thread
+            float lse = 0.f, cf = 0.f;
+            int tg = -1;
+            if (tc0 + lane < M) {
+              lse = (float)epi.lse_in[tc0 + lane];
+              cf = epi.row_coef[tc0 + lane];
+              tg = epi.tgt_row[tc0 + lane];
+            }
+            uint32_t packed[16];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float rj = __shfl_sync(0xffffffffu, rs, j);
+              const float lj = __shfl_sync(0xffffffffu, lse, j);
+              const float cj = __shfl_sync(0xffffffffu, cf, j);
+              const int tj = __shfl_sync(0xffffffffu, tg, j);
+              const float x = __uint_as_float(r[j]) * rj;
+              const float d = j < jn ? cj * ((n == tj ? 1.f : 0.f) - __expf(x - lj)) : 0.f;
+              const __nv_bfloat16 b = __float2bfloat16(d);
+              if (j < jn && n < N) epi.out_bf16[(size_t)(tc0 + j) * epi.ld_bf16 + n] = b;
+              const uint32_t bits = (uint32_t)__bfloat16_as_ushort(b);
+              if (j & 1) packed[j >> 1] |= bits << 16;
+              else packed[j >> 1] = bits;
+            }
+            if (epi.outT_bf16 && n < N) {  // columns past M are written as 0 (padding)
+              uint4* dst = reinterpret_cast<uint4*>(epi.outT_bf16 + (size_t)n * epi.ldT + tc0);
+#pragma unroll
+              for (int v = 0; v < 4; ++v)
+                dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+            }
+            continue;
+          }
           if (n < N) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {

@@ -44,6 +44,8 @@ __device__ __forceinline__ void epi_row_meta(const EpiParams& epi, int r0, int r
       r = rsqrtf(s * epi.inv_dim + epi.eps);
     }
     s_rstd[j] = r;
+    if ((epi.kind == EPI_LOGITS || epi.kind == EPI_DLOGITS) && epi.tgt_row != nullptr)
+      s_row[j] = make_int4(m < M ? epi.tgt_row[m] : -1, 0, 0, 0);
     if (epi.kind == EPI_QKV) {
       int4 rc = make_int4(-1, 0, 0, 0);
       if (m < M) {
@@ -145,7 +147,8 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
       float v = -INFINITY;
       if (m < M && n < N) {
         v = tile[j * pitch + c] * s_rstd[j];
-        epi.out_f32[(size_t)m * epi.ld_out + n] = v;
+        if (epi.out_f32) epi.out_f32[(size_t)m * epi.ld_out + n] = v;
+        if (epi.tgt_out && n == s_row[j].x) epi.tgt_out[m] = v;
       }
       tile[j * pitch + c] = v;
     }
@@ -165,6 +168,17 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
         epi.part_max[(size_t)m * n_tiles + n_tile] = mx;
         epi.part_sum[(size_t)m * n_tiles + n_tile] = s;
       }
+    }
+  } else if (epi.kind == EPI_DLOGITS) {
+    for (int idx = tid; idx < rows * 128; idx += nthr) {
+      const int j = r0 + (idx >> 7), c = idx & 127;
+      const int m = t0 + j, n = n0 + c;
+      if (m >= M || n >= N) continue;
+      const float x = tile[j * pitch + c] * s_rstd[j];
+      const float p = __expf(x - (float)epi.lse_in[m]);
+      const __nv_bfloat16 d = __float2bfloat16(epi.row_coef[m] * ((n == s_row[j].x ? 1.f : 0.f) - p));
+      epi.out_bf16[(size_t)m * epi.ld_bf16 + n] = d;
+      if (epi.outT_bf16) epi.outT_bf16[(size_t)n * epi.ldT + m] = d;
     }
   } else if (epi.kind == EPI_RESID) {
 #pragma unroll 4

@@ -29,6 +29,9 @@ void launch_zero(float* p, size_t n, cudaStream_t st);
 // logits[r, tgt] - lse (fp64), dlogits[r, :] = coef[r] * (onehot(tgt) -
 // softmax) in bf16 -- the gradient of J = sum_r coef[r] * log pi(tgt_r) w.r.t.
 // the logits (rl_math.cpp:239-256 for one row).
+// lse and log pi(target) per row from the LM-head epilogue's tile partials.
+void launch_lse_logprob(const float* pmax, const double* psum, int V, int rows, const float* tgt_logit,
+                        double* lse, double* logprob, cudaStream_t st);
 void launch_loss_dlogits(const float* logits, const float* pmax, const double* psum, int V,
                          int rows, const int32_t* targets, const float* coef, double* logprob,
                          __nv_bfloat16* dlogits, cudaStream_t st);

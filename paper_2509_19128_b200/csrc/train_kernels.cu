@@ -131,6 +131,40 @@ __global__ void __launch_bounds__(kRowThreads)
   if (threadIdx.x == 0) logprob[r] = (double)x[tgt] - lse;
 }
 
+// Per row: lse = log-sum-exp of the LM-head logits from the per-128-column
+// (max, fp64 sum) partials (same combination as loss_dlogits_kernel) and
+// log pi(target) = logit(target) - lse.
+__global__ void __launch_bounds__(kRowThreads)
+    lse_logprob_kernel(const float* __restrict__ pmax, const double* __restrict__ psum, int V,
+                       const float* __restrict__ tgt_logit, double* __restrict__ lse_out,
+                       double* __restrict__ logprob) {
+  __shared__ float fred[33];
+  __shared__ double dred[33];
+  const int r = blockIdx.x;
+  const int T = (V + 127) / 128;
+  const float* pm = pmax + (size_t)r * T;
+  const double* ps = psum + (size_t)r * T;
+  float mx = -INFINITY;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) mx = fmaxf(mx, pm[t]);
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) fred[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? fred[threadIdx.x] : -INFINITY;
+    v = warp_max(v);
+    if (threadIdx.x == 0) fred[32] = v;
+  }
+  __syncthreads();
+  const double M = (double)fred[32];
+  double part = 0.0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) part += ps[t] * exp((double)pm[t] - M);
+  const double lse = M + log(block_sum_dd(part, dred));
+  if (threadIdx.x == 0) {
+    lse_out[r] = lse;
+    logprob[r] = (double)tgt_logit[r] - lse;
+  }
+}
+
 __global__ void __launch_bounds__(kRowThreads)
     row_rstd_kernel(const float* __restrict__ x, int H, float eps, float* __restrict__ rstd) {
   __shared__ float red[33];
@@ -393,6 +427,10 @@ void launch_bf16_to_f32(const __nv_bfloat16* src, size_t n, float* dst, cudaStre
 }
 void launch_zero(float* p, size_t n, cudaStream_t st) {
   zero_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, n);
+}
+void launch_lse_logprob(const float* pmax, const double* psum, int V, int rows, const float* tgt_logit,
+                        double* lse, double* logprob, cudaStream_t st) {
+  if (rows > 0) lse_logprob_kernel<<<rows, kRowThreads, 0, st>>>(pmax, psum, V, tgt_logit, lse, logprob);
 }
 void launch_loss_dlogits(const float* logits, const float* pmax, const double* psum, int V,
                          int rows, const int32_t* targets, const float* coef, double* logprob,

@@ -128,7 +128,6 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
   }
   if ((st = alloc(&x_, (size_t)T_max_ * H)) || (st = alloc(&xgF_, (size_t)T_max_ * H)) ||
       (st = alloc(&rstdF_, T_max_)) || (st = alloc(&ssq_, (size_t)T_max_ * d_.ssq_parts())) ||
-      (st = alloc(&logits_, (size_t)chunk_ * d_.V)) ||
       (st = alloc(&pmax_, (size_t)chunk_ * ((d_.V + 127) / 128))) ||
       (st = alloc(&psum_, (size_t)chunk_ * ((d_.V + 127) / 128))) ||
       (st = alloc(&dlogits_, (size_t)chunk_ * d_.V)) ||
@@ -141,7 +140,7 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
       (st = alloc(&ones_, T_max_)) || (st = alloc(&row_slot_, T_max_)) ||
       (st = alloc(&row_pos_, T_max_)) || (st = alloc(&row_tok_, T_max_)) ||
       (st = alloc(&row_tgt_, T_max_)) || (st = alloc(&coef_, T_max_)) ||
-      (st = alloc(&lp_, T_max_)) || (st = alloc(&cos_sin_, (size_t)d_.max_pos * d_.hd)))
+      (st = alloc(&lp_, T_max_)) || (st = alloc(&lse_, T_max_)) || (st = alloc(&tgt_logit_, T_max_)) || (st = alloc(&cos_sin_, (size_t)d_.max_pos * d_.hd)))
     return st;
   launch_rope_table(cos_sin_, d_.max_pos, d_.hd, (double)d_.theta, st_);
   std::vector<float> ones(T_max_, 1.f);
@@ -306,9 +305,11 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
     EpiParams e;
     e.kind = EPI_LOGITS;
     e.ssq_in = ssq_ + (size_t)c0 * parts; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d_.eps;
-    e.out_f32 = logits_; e.ld_out = V; e.part_max = pmax_; e.part_sum = psum_;
+    // statistics and the target's logit only: the [C x V] logits are never stored
+    e.out_f32 = nullptr; e.part_max = pmax_; e.part_sum = psum_;
+    e.tgt_row = row_tgt_ + c0; e.tgt_out = tgt_logit_ + c0;
     if ((s = gemm(xgF_ + (size_t)c0 * H, C, C, w + lay_.lm_head, V, H, e))) return s;
-    launch_loss_dlogits(logits_, pmax_, psum_, V, C, row_tgt_ + c0, ones_, lp_ + c0, dlogits_, st);
+    launch_lse_logprob(pmax_, psum_, V, C, tgt_logit_ + c0, lse_ + c0, lp_ + c0, st);
   }
   cudaEventRecord(e1, st);
   std::vector<double> lp(T);
@@ -359,20 +360,21 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
   float* g_lm = grad_ + lay_.lm_head;
   for (int c0 = 0; c0 < T; c0 += chunk_) {
     const int C = std::min(chunk_, T - c0), Cp = pad64(C);
+    // dlogits = coef (onehot - softmax) straight from the LM-head accumulator
+    // (lse of pass 1: same weights, same logits), row-major and transposed
+    if (Cp > C) SRL_CUDA(cudaMemsetAsync(dlogitsT_, 0, sizeof(__nv_bfloat16) * (size_t)V * Cp, st));
     EpiParams e;
-    e.kind = EPI_LOGITS;
+    e.kind = EPI_DLOGITS;
     e.ssq_in = ssq_ + (size_t)c0 * parts; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d_.eps;
-    e.out_f32 = logits_; e.ld_out = V; e.part_max = pmax_; e.part_sum = psum_;
+    e.lse_in = lse_ + c0; e.row_coef = coef_ + c0; e.tgt_row = row_tgt_ + c0;
+    e.out_bf16 = dlogits_; e.ld_bf16 = V; e.outT_bf16 = dlogitsT_; e.ldT = Cp;
     if ((s = gemm(xgF_ + (size_t)c0 * H, C, C, w + lay_.lm_head, V, H, e))) return s;
-    launch_loss_dlogits(logits_, pmax_, psum_, V, C, row_tgt_ + c0, coef_ + c0, lp_ + c0, dlogits_, st);
     // dzw[t, h] = sum_v dlogits[t, v] E[v, h]   (W-side operand: E^T [H x V])
     if ((s = gemm_store(dlogits_, C, wt_ + lay_.lm_head, H, V, dz_))) return s;
     launch_rmsnorm_bwd(dz_, x_ + (size_t)c0 * H, w + lay_.final_norm, rstdF_ + c0, C, H,
                        dx_ + (size_t)c0 * H, grad_ + lay_.final_norm, st);
     // dE[v, h] += sum_t dlogits[t, v] * rstd[t] xg[t, h]
-    SRL_CUDA(cudaMemsetAsync(dlogitsT_, 0, sizeof(__nv_bfloat16) * (size_t)V * Cp, st));
     SRL_CUDA(cudaMemsetAsync(tB_, 0, sizeof(__nv_bfloat16) * (size_t)H * Cp, st));
-    launch_transpose_bf16(dlogits_, C, V, dlogitsT_, Cp, st);
     launch_scale_transpose_bf16(xgF_ + (size_t)c0 * H, rstdF_ + c0, C, H, tB_, Cp, st);
     if ((s = gemm_accum(dlogitsT_, V, tB_, H, Cp, g_lm))) return s;
   }

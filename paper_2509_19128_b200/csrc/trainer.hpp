@@ -58,13 +58,15 @@ class DecoderTrainer {
   __nv_bfloat16* wt_ = nullptr;  // transposed weights (same offsets)
   std::vector<LayerActs> acts_;
   int chunk_ = 512;  // LM-head rows per pass (trainer.cpp, kLogitChunkMax)
-  float *x_ = nullptr, *rstdF_ = nullptr, *ssq_ = nullptr, *logits_ = nullptr, *pmax_ = nullptr;
+  float *x_ = nullptr, *rstdF_ = nullptr, *ssq_ = nullptr, *pmax_ = nullptr;
   double* psum_ = nullptr;
   __nv_bfloat16 *xgF_ = nullptr, *dlogits_ = nullptr, *dlogitsT_ = nullptr, *dbig_bf_ = nullptr,
                 *tA_ = nullptr, *tB_ = nullptr;
   float *dx_ = nullptr, *dz_ = nullptr, *dbig_ = nullptr, *ones_ = nullptr, *coef_ = nullptr,
         *cos_sin_ = nullptr;
   double* lp_ = nullptr;
+  double* lse_ = nullptr;       // per row, from pass 1 (reused by the pass-2 dlogits epilogue)
+  float* tgt_logit_ = nullptr;  // per row: the target's logit (pass 1)
   int32_t *row_slot_ = nullptr, *row_pos_ = nullptr, *row_tok_ = nullptr, *row_tgt_ = nullptr;
   __nv_bfloat16 *kc_ = nullptr, *vc_ = nullptr;
   size_t kv_cap_ = 0;

@@ -33,4 +33,5 @@ for s in range(a.steps):
     r = tr.step(trajs)
     tr.apply_adam(1e-6)
     torch.cuda.synchronize()
-    print(f"step {s}: {r.step_ms:.1f} ms (forward {r.forward_ms:.1f}), {r.tokens} tokens", flush=True)
+    g = tr.gradient()
+    print(f"step {s}: {r.step_ms:.1f} ms (forward {r.forward_ms:.1f}), {r.tokens} tokens, J={r.objective:.3e} ess={r.ess:.3f} |g|={g.norm().item():.3e} finite={bool(torch.isfinite(g).all())}", flush=True)
