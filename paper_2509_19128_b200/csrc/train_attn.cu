@@ -339,6 +339,172 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
 }
 
+// Forward over packed sequences: CTA = (64-query block, sequence, query head),
+// online softmax over the causal key blocks; O (bf16) and lse (natural log of
+// the scaled scores' partition sum) per (row, head), as the backward expects.
+template <int HD>
+struct FwdSmem {
+  static constexpr int P = HD + 8;
+  static constexpr size_t tile = sizeof(__nv_bfloat16) * kBlk * P;
+  static constexpr size_t tileT = sizeof(__nv_bfloat16) * HD * kPadT;
+  static constexpr size_t total = 2 * tile + tileT;  // Q, K, V^T
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kWarps * 32)
+    attn_fwd_mma(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
+                 const __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ seq_start,
+                 const int32_t* __restrict__ seq_len, const int32_t* __restrict__ bt, int pps, int nq,
+                 int nkv, float scale, __nv_bfloat16* __restrict__ out, float* __restrict__ lse_out) {
+  using S = FwdSmem<HD>;
+  constexpr int P = S::P, NT = HD / 8;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smem);
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem + S::tile);
+  __nv_bfloat16* Vt = reinterpret_cast<__nv_bfloat16*>(smem + 2 * S::tile);
+  const int slot = blockIdx.y, h = blockIdx.z;
+  const int L = seq_len[slot], s0 = seq_start[slot];
+  const int q0 = blockIdx.x * kBlk;
+  if (q0 >= L) return;
+  const int kh = h / (nq / nkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qvalid = min(kBlk, L - q0);
+  stage_bf16<HD>(Qs, nullptr, qvalid, [&](int r) { return q + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+  const int qr = warp * 16;
+  const int ql_lo = qr + (lane >> 2), ql_hi = ql_lo + 8;
+  float o[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[n][i] = 0.f;
+  float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
+
+  for (int k0 = 0; k0 <= q0; k0 += kBlk) {
+    const int kvalid = min(kBlk, L - k0);
+    __syncthreads();
+    stage_bf16<HD>(Ks, nullptr, kvalid, [&](int r) { return page_row(kc, bt, pps, slot, k0 + r, nkv, kh, HD); });
+    {  // V^T [HD][64]
+      constexpr int V8 = HD / 8;
+      for (int e = threadIdx.x; e < kBlk * V8; e += kWarps * 32) {
+        const int r = e / V8, c = (e % V8) * 8;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < kvalid) v = *reinterpret_cast<const uint4*>(page_row(vc, bt, pps, slot, k0 + r, nkv, kh, HD) + c);
+        const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) Vt[(c + i) * kPadT + r] = hv[i];
+      }
+    }
+    __syncthreads();
+    float s[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s[n][i] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      uint32_t a[4];
+      frag_a(a, Qs, P, qr, kk * 16, lane);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        uint32_t b0, b1;
+        frag_b(b0, b1, Ks, P, n * 8, kk * 16, lane);
+        mma16816(s[n], a, b0, b1);
+      }
+    }
+    // scale + causal mask, new running max per row (a row's 64 columns live
+    // on the 4 lanes of a quad)
+    float mx_lo = m_lo, mx_hi = m_hi;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int kl = n * 8 + (lane & 3) * 2 + (i & 1);
+        const int ql = i < 2 ? ql_lo : ql_hi;
+        const bool ok = kl < kvalid && k0 + kl <= q0 + ql;
+        s[n][i] = ok ? s[n][i] * scale : -INFINITY;
+        if (i < 2) mx_lo = fmaxf(mx_lo, s[n][i]);
+        else mx_hi = fmaxf(mx_hi, s[n][i]);
+      }
+    }
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+      mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, off));
+      mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, off));
+    }
+    const float c_lo = m_lo == -INFINITY ? 0.f : __expf(m_lo - mx_lo);
+    const float c_hi = m_hi == -INFINITY ? 0.f : __expf(m_hi - mx_hi);
+    m_lo = mx_lo;
+    m_hi = mx_hi;
+    float sum_lo = 0.f, sum_hi = 0.f;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float mm = i < 2 ? m_lo : m_hi;
+        const float p = s[n][i] == -INFINITY ? 0.f : __expf(s[n][i] - mm);
+        s[n][i] = p;
+        if (i < 2) sum_lo += p;
+        else sum_hi += p;
+      }
+    }
+    l_lo = l_lo * c_lo + sum_lo;  // per-lane partial sums; combined across the quad at the end
+    l_hi = l_hi * c_hi + sum_hi;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      o[n][0] *= c_lo; o[n][1] *= c_lo;
+      o[n][2] *= c_hi; o[n][3] *= c_hi;
+    }
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      uint32_t a[4];
+      a[0] = pack_bf16(s[2 * ks][0], s[2 * ks][1]);
+      a[1] = pack_bf16(s[2 * ks][2], s[2 * ks][3]);
+      a[2] = pack_bf16(s[2 * ks + 1][0], s[2 * ks + 1][1]);
+      a[3] = pack_bf16(s[2 * ks + 1][2], s[2 * ks + 1][3]);
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        uint32_t b0, b1;
+        frag_b(b0, b1, Vt, kPadT, n * 8, ks * 16, lane);
+        mma16816(o[n], a, b0, b1);
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 1; off <= 2; off <<= 1) {
+    l_lo += __shfl_xor_sync(0xffffffffu, l_lo, off);
+    l_hi += __shfl_xor_sync(0xffffffffu, l_hi, off);
+  }
+  const float inv_lo = l_lo > 0.f ? 1.f / l_lo : 0.f, inv_hi = l_hi > 0.f ? 1.f / l_hi : 0.f;
+  const int qd = nq * HD;
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    const int d = n * 8 + (lane & 3) * 2;
+    if (ql_lo < qvalid)
+      *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(s0 + q0 + ql_lo) * qd + h * HD + d) =
+          __floats2bfloat162_rn(o[n][0] * inv_lo, o[n][1] * inv_lo);
+    if (ql_hi < qvalid)
+      *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(s0 + q0 + ql_hi) * qd + h * HD + d) =
+          __floats2bfloat162_rn(o[n][2] * inv_hi, o[n][3] * inv_hi);
+  }
+  if ((lane & 3) == 0) {
+    if (ql_lo < qvalid) lse_out[(size_t)(s0 + q0 + ql_lo) * nq + h] = m_lo + logf(l_lo);
+    if (ql_hi < qvalid) lse_out[(size_t)(s0 + q0 + ql_hi) * nq + h] = m_hi + logf(l_hi);
+  }
+}
+
+template <int HD>
+cudaError_t launch_fwd_t(const __nv_bfloat16* q, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
+                         const int32_t* seq_start, const int32_t* seq_len, const int32_t* bt, int pps,
+                         int n_seq, int nq, int nkv, float scale, __nv_bfloat16* out, float* lse,
+                         cudaStream_t st) {
+  static const bool attr = cudaFuncSetAttribute(attn_fwd_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)FwdSmem<HD>::total) == cudaSuccess;
+  if (!attr) return cudaErrorInvalidValue;
+  attn_fwd_mma<HD><<<dim3(pps, n_seq, nq), kWarps * 32, FwdSmem<HD>::total, st>>>(
+      q, kc, vc, seq_start, seq_len, bt, pps, nq, nkv, scale, out, lse);
+  return cudaGetLastError();
+}
+
 template <int HD>
 cudaError_t launch_t(const __nv_bfloat16* q, const float* d_o, const float* lse, const float* D,
                      const __nv_bfloat16* kc, const __nv_bfloat16* vc, const int32_t* seq_start,
@@ -375,4 +541,20 @@ cudaError_t launch_attention_bwd_mma(const __nv_bfloat16* q, const float* d_o, c
   return cudaErrorInvalidValue;
 }
 
+}  // namespace srl
+
+namespace srl {
+cudaError_t launch_attention_fwd_mma(const __nv_bfloat16* q, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
+                                     const int32_t* seq_start, const int32_t* seq_len,
+                                     const int32_t* block_table, int pages_per_seq, int n_seq, int nq,
+                                     int nkv, int hd, __nv_bfloat16* out, float* lse, cudaStream_t st) {
+  const float scale = 1.0f / sqrtf((float)hd);
+  if (hd == 64)
+    return launch_fwd_t<64>(q, kc, vc, seq_start, seq_len, block_table, pages_per_seq, n_seq, nq, nkv,
+                            scale, out, lse, st);
+  if (hd == 128)
+    return launch_fwd_t<128>(q, kc, vc, seq_start, seq_len, block_table, pages_per_seq, n_seq, nq, nkv,
+                             scale, out, lse, st);
+  return cudaErrorInvalidValue;
+}
 }  // namespace srl

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // trainer.cpp -- trainer-side device computations of the decoder policy.
 //
 //  * decoder_policy_logprobs: per-token current-policy log-prob recompute
@@ -266,6 +267,11 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
     e.row_slot = row_slot_; e.row_pos = row_pos_; e.block_table = d_bt; e.cos_sin = cos_sin_;
     e.q_out = a.q; e.kc = kcl; e.vc = vcl;
     if ((s = gemm(a.xg1, T_max_, T, w + o.qkv_w, qkv, H, e))) return s;
+    static const bool scalar_fwd = std::getenv("SRL_ATTN_FWD_SCALAR") != nullptr;  // A/B switch
+    if (!scalar_fwd) {
+      SRL_CUDA(launch_attention_fwd_mma(a.q, kcl, vcl, d_sstart, d_slen, d_bt, pps, n_seq, d_.nq, d_.nkv,
+                                        d_.hd, a.attn, a.lse, st));
+    } else {
     RoundPlan plan{row_slot_, row_pos_, row_tok_, nullptr};
     float* attn_ws = nullptr;
     int* attn_cnt = nullptr;
@@ -279,6 +285,7 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
                      st, a.lse);
     cudaFreeAsync(attn_ws, st);
     cudaFreeAsync(attn_cnt, st);
+    }
     EpiParams r;
     r.kind = EPI_RESID; r.resid = x_; r.gain = w + o.ln2; r.xg = a.xg2; r.ssq_out = ssq_;
     if ((s = gemm(a.attn, T_max_, T, w + o.o_w, H, qd, r))) return s;
