@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2509_19128_b200.policy import TINY, DecoderPolicy
+from paper_2509_19128_b200.policy import TINY, DecoderConfig, DecoderPolicy
 from paper_2509_19128_b200.trainer import Trainer
 
 from .torch_decoder_ref import TorchDecoder
@@ -32,17 +32,23 @@ def make_trajs(rng, V, n, lens, prompts):
     return out
 
 
-@pytest.mark.parametrize("granularity", ["sequence", "per_token"])
-def test_trainer_gradient_matches_torch_fp64(cuda, granularity):
-    pol = DecoderPolicy.random(TINY, seed=11, scale=0.03)
+# head_dim 128 with 3 query heads per KV head (the 1.5B / 7B attention layout)
+# and an untied LM head: the tensor-core attention kernels' other instance
+TINY128 = DecoderConfig("tiny-hd128", 256, 256, 2, 6, 2, 128, 512, False, 0, 4096, 10000.0, 1e-6)
+
+
+@pytest.mark.parametrize("cfg,granularity", [(TINY, "sequence"), (TINY, "per_token"),
+                                             (TINY128, "sequence")])
+def test_trainer_gradient_matches_torch_fp64(cuda, cfg, granularity):
+    pol = DecoderPolicy.random(cfg, seed=11, scale=0.03)
     w16 = pol.torch_weights().cpu().view(torch.int16).numpy().view(np.uint16)
     rng = np.random.default_rng(5)
-    trajs = make_trajs(rng, TINY.vocab_size, 4, [12, 33, 20, 70], [3, 5, 1, 9])
+    trajs = make_trajs(rng, cfg.vocab_size, 4, [12, 33, 20, 70], [3, 5, 1, 9])
     tr = Trainer(pol, max_tokens=256)
     res = tr.step(trajs, clamp=5.0, granularity=granularity)
     g_dev = tr.gradient().cpu().numpy().astype(np.float64)
 
-    ref = TorchDecoder(TINY.to_dict(), w16)
+    ref = TorchDecoder(cfg.to_dict(), w16)
     J, lps = ref.is_reinforce(trajs, len(trajs), 5.0, granularity)
     g_ref = ref.flat_grad()
 
