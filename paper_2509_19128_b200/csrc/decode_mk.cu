@@ -10,6 +10,7 @@
 
 #include "decode_mk.cuh"
 #include "fastexp.cuh"
+#include "gemm_epi.cuh"
 #include "sm100.cuh"
 
 namespace srl {
@@ -39,11 +40,6 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ int ld_acquire_cta(const int* p) {
   int v;
   asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
@@ -52,7 +48,6 @@ __device__ __forceinline__ int ld_acquire_cta(const int* p) {
 __device__ __forceinline__ void st_release_cta(int* p, int v) {
   asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
-__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -122,17 +117,48 @@ __device__ __forceinline__ void mk_wait(uint64_t* bar, uint32_t parity) {
 // first item of CTA c in a phase whose items are dealt round-robin from `rot`
 __device__ __forceinline__ int first_item(int c, int rot, int G) { return c >= rot ? c - rot : c - rot + G; }
 
-// L2 prefetch of one weight tile (no shared memory, no completion).
-__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* m, int32_t c0, int32_t c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(m)),
-               "r"(c0), "r"(c1)
-               : "memory");
+// DSMEM (cluster of two CTAs): address of the same shared location in the
+// partner CTA, remote store, remote release-arrive, cluster-scope acquire wait.
+__device__ __forceinline__ uint32_t partner_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
 }
-__device__ __forceinline__ bool is_gemm(int kind) {
-  return kind == MK_QKV || kind == MK_O || kind == MK_GU || kind == MK_DOWN || kind == MK_LM;
+// mma.sync m16n8k16 (bf16 -> fp32) for the attention items: fragments of a
+// row-major bf16 tile X[row][col] (pitch in elements) and of B from Y[n][k].
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t ld_b32(const __nv_bfloat16* p) { return *reinterpret_cast<const uint32_t*>(p); }
+__device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+// (x, y) -> bf16x2 hi = RN(x, y) and lo = RN(x - hi, y - hi): hi + lo carries
+// ~16 significant bits.
+__device__ __forceinline__ void split_bf16(float x, float y, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+  const float2 hf = __bfloat1622float2(h);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = pack2_bf16(x - hf.x, y - hf.y);
+}
+// B fragment (k = 16 rows of a row-major [k][n] tile, n = 8 columns at col0)
+// through ldmatrix.trans: lanes 0-15 address rows k0 .. k0 + 15.
+__device__ __forceinline__ void ldsm_x2_trans(uint32_t& b0, uint32_t& b1, const uint8_t* tile, int pitch_bytes,
+                                              int k0, int col0, int lane) {
+  const uint8_t* p = tile + (size_t)(k0 + (lane & 15)) * pitch_bytes + col0 * 2;
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+               : "=r"(b0), "=r"(b1)
+               : "r"(smem_u32(p)));
 }
 
+__device__ __forceinline__ void fence_proxy_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -161,11 +187,6 @@ __device__ __forceinline__ double wsum_d(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ float wmax(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 __device__ __forceinline__ double uniform_draw(uint64_t seed, uint64_t n) {
   uint64_t z = seed + (n + 1) * kGolden;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -181,13 +202,15 @@ __device__ __forceinline__ double uniform_draw(uint64_t seed, uint64_t n) {
 template <int HD, int G>
 struct AttnSmem {
   static constexpr int KT = HD == 64 ? 32 : 16;  // keys per tile
-  static constexpr int ROW = HD * 2 + 16;        // padded K row (conflict-free LDS.128)
-  static constexpr int VROW = HD * 2;
-  static constexpr size_t sq = sizeof(float) * G * HD;
+  static constexpr int ROW = HD * 2 + 16;        // padded K row (conflict-free fragment loads)
+  static constexpr int VROW = HD * 2 + 16;       // padded V row (conflict-free ldmatrix.trans)
+  static constexpr int QP = HD + 8;              // bf16 q tile [16 (heads, zero-padded)][QP]
+  static constexpr size_t sq = sizeof(__nv_bfloat16) * 16 * QP > sizeof(float) * G * HD
+                                   ? sizeof(__nv_bfloat16) * 16 * QP : sizeof(float) * G * HD;
   static constexpr size_t kbuf = (size_t)KT * ROW, vbuf = (size_t)KT * VROW;
   static constexpr size_t warp_bytes = kbuf + vbuf;
   static constexpr size_t tiles = kCW * warp_bytes;
-  static constexpr size_t sp = sizeof(float) * kCW * G * 32;
+  static constexpr size_t sp = 0;  // (probabilities stay in registers: mma.sync P.V)
   static constexpr size_t sml = sizeof(float) * 2 * kCW * G;
   static constexpr size_t spage = sizeof(int) * kMaxSplitPages;
   static constexpr size_t sraw = sizeof(float) * (G + 2) * HD;  // reduced q | k | v of the row
@@ -208,7 +231,7 @@ struct MkLayout {
   static constexpr size_t scratch =
       gemm_scr > att ? (gemm_scr > smp ? gemm_scr : smp) : (att > smp ? att : smp);
   static constexpr size_t bar = ring + scratch;
-  static constexpr size_t misc = bar + (2 * STAGES + 5) * 8;
+  static constexpr size_t misc = bar + (2 * STAGES + 6) * 8;
   static constexpr size_t rstd = misc + 32;
   static constexpr size_t rows = rstd + kTok * 4;  // round-constant (slot, pos) of every row
   static constexpr size_t total = rows + kTok * 8;
@@ -223,7 +246,7 @@ __device__ void mk_rows(const MkParams& P, int kind, float* s_rstd, int ct) {
     float r = 1.f;
     if ((kind == MK_GU || kind == MK_LM) && j < P.S) {
       float s = 0.f;
-      for (int p = 0; p < P.parts; ++p) s += P.ssq[(size_t)j * P.parts + p];
+      s = gemm_detail::ssq_row_sum(P.ssq + (size_t)j * P.parts, P.parts);
       r = rsqrtf(s * P.inv_h + P.eps);
     }
     s_rstd[j] = r;
@@ -276,7 +299,7 @@ __device__ __noinline__ void mk_lm_stats(const MkParams& P, const float* tile, i
 // reduced by the attention items that consume them.
 __device__ __forceinline__ void mk_epilogue(const MkParams& P, const MkPhase& ph, int n_tile,
                                             float* tile, const float* s_rstd, int ct, int r0,
-                                            int r1, float colv) {
+                                            int r1, float colv, const float* xs) {
   const int n0 = n_tile * kBN, N = ph.N, M = r1;
   const int nr = r1 - r0;
   const int cw = ct >> 5, lane = ct & 31;
@@ -289,7 +312,7 @@ __device__ __forceinline__ void mk_epilogue(const MkParams& P, const MkPhase& ph
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int j = j0 + 2 * u;
-        xr[u] = (j < r1 && n < N) ? P.x[(size_t)j * N + n] : 0.f;
+        xr[u] = (j < r1 && n < N) ? (xs ? xs[(j - r0) * kBN + c] : P.x[(size_t)j * N + n]) : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -371,10 +394,9 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
                              unsigned long long* tr) {
   using A = AttnSmem<HD, G>;
   const long long c_start = clock64();
-  constexpr int KT = A::KT, DPL = HD / 32, V4 = HD / 8, PER = KT * V4 / 32;
+  constexpr int KT = A::KT, V4 = HD / 8, PER = KT * V4 / 32;
   constexpr int W = (G + 2) * HD;            // q heads | k | v of this kv head
   constexpr int WPT = (W + kCT - 1) / kCT;   // of them per thread
-  float(*sq)[HD] = reinterpret_cast<float(*)[HD]>(scr);
   uint8_t* tiles = scr + A::sq;
   float(*sp)[G][32] = reinterpret_cast<float(*)[G][32]>(scr + A::sq + A::tiles);
   float(*sm_m)[G] = reinterpret_cast<float(*)[G]>(scr + A::sq + A::tiles + A::sp);
@@ -384,6 +406,7 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
   __nv_bfloat16* snew = reinterpret_cast<__nv_bfloat16*>(scr + A::sq + A::tiles + A::sp + A::sml +
                                                          A::spage + A::sraw);
   float(*sm_acc)[G][HD] = reinterpret_cast<float(*)[G][HD]>(tiles);  // after the tiles are consumed
+  __nv_bfloat16* sqb = reinterpret_cast<__nv_bfloat16*>(scr);          // [16][QP] bf16 q (rows >= G zero)
   const int warp = ct >> 5, lane = ct & 31;
   const int splits = P.attn_splits, nq = P.nq, nkv = P.nkv;
   const int slot = s_rows[m].x;
@@ -400,6 +423,45 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
   const bool owner = pos >= k0 && pos < k0 + P.attn_chunk;  // this split holds the new key
   const int qend = nq * HD, kend = qend + nkv * HD;
 
+  const int pg0 = k0 / kPageTokens;
+  // K/V tiles: warp w streams tiles w, w + 8, ... into buffer slot 7 - w, so the
+  // first tiles land in the slots the QKV partial staging does not alias and
+  // their loads are issued now, under the partials' L2 round trip
+  const __nv_bfloat16* kc = P.kc + P.kv_layer_elems * layer;
+  const __nv_bfloat16* vc = P.vc + P.kv_layer_elems * layer;
+  uint8_t* kb = tiles + (kCW - 1 - warp) * A::warp_bytes;
+  uint8_t* vb = kb + A::kbuf;
+  auto load_tile = [&](int t, int page) {
+    const int key0 = k0 + t * KT;
+    const int nv = min(KT, k1 - key0);
+    const size_t base = (((size_t)page * nkv + kh) * kPageTokens + (key0 % kPageTokens)) * HD;
+    const uint4* kg = reinterpret_cast<const uint4*>(kc + base);
+    const uint4* vg = reinterpret_cast<const uint4*>(vc + base);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = lane + 32 * i, r = e / V4, c = e % V4;
+      if (r < nv) {
+        cp_async16(kb + r * A::ROW + c * 16, kg + e);
+        cp_async16(vb + r * A::VROW + c * 16, vg + e);
+      } else {  // P is 0 there, but 0 x a stale NaN pattern is NaN in the MMA
+        *reinterpret_cast<uint4*>(vb + r * A::VROW + c * 16) = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    cp_async_commit();
+  };
+  const int free_slot0 = P.pairs ? 0 : (qkv_cs * W * 4 + (int)A::warp_bytes - 1) / (int)A::warp_bytes;
+  const bool early = warp < ntiles && kCW - 1 - warp >= free_slot0;
+  if (early) load_tile(warp, P.block_table[(size_t)slot * P.pps + (k0 + warp * KT) / kPageTokens]);
+  if (P.pairs) {
+    // pair mode: the QKV phase already wrote q (bf16, post-RoPE) and the new
+    // token's K/V into the paged cache
+    const __nv_bfloat16* qrow = P.q + (size_t)m * nq * HD + (size_t)kh * G * HD;
+    for (int i = ct; i < 16 * HD; i += kCT)
+      sqb[(i / HD) * A::QP + i % HD] = i < G * HD ? qrow[i] : __float2bfloat16(0.f);
+    for (int i = ct; i < (nkeys + kPageTokens - 1) / kPageTokens; i += kCT)
+      spage[i] = P.block_table[(size_t)slot * P.pps + pg0 + i];
+    csync();
+  } else {
   // ---- (1) operands: split partials (bulk), pages, bias, rope, rstd -- all in flight
   float* stage = reinterpret_cast<float*>(tiles);  // [qkv_cs][W], free until the K/V tiles
   if (ct == 0) {  // the row's partials are contiguous: [m][kh][split][W]
@@ -407,7 +469,6 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
     mbar_arrive_expect_tx(cbar, (uint32_t)(qkv_cs * W * 4));
     bulk_g2s(stage, P.qkv_part + ((size_t)m * nkv + kh) * qkv_cs * W, qkv_cs * W * 4, cbar);
   }
-  const int pg0 = k0 / kPageTokens;
   for (int i = ct; i < (nkeys + kPageTokens - 1) / kPageTokens; i += kCT)
     spage[i] = P.block_table[(size_t)slot * P.pps + pg0 + i];
   constexpr int half = HD / 2;
@@ -433,10 +494,14 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
   }
   const int cpage = P.block_table[(size_t)slot * P.pps + pos / kPageTokens];
   float ss = 0.f;
-  for (int p = 0; p < P.parts; ++p) ss += P.ssq[(size_t)m * P.parts + p];
+  ss = gemm_detail::ssq_row_sum(P.ssq + (size_t)m * P.parts, P.parts);
   const float rstd = rsqrtf(ss * P.inv_h + P.eps);
+  for (int i = ct; i < (16 - G) * HD; i += kCT)
+    sqb[(G + i / HD) * A::QP + i % HD] = __float2bfloat16(0.f);
+  if (tr && ct == 0 && tr[1] == 0) tr[1] = clock64() - c_start;
   mk_wait(cbar, cph);
   cph ^= 1;
+  if (tr && ct == 0 && tr[2] == 0) tr[2] = clock64() - c_start;
 #pragma unroll
   for (int u = 0; u < WPT; ++u) {
     const int idx = ct + u * kCT;
@@ -448,6 +513,7 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
     }
   }
   csync();
+  if (tr && ct == 0 && tr[5] == 0) tr[5] = clock64() - c_start;
   {
     const size_t at = (((size_t)cpage * nkv + kh) * kPageTokens + (pos % kPageTokens)) * HD;
     __nv_bfloat16* kcw = P.kc + P.kv_layer_elems * layer;
@@ -467,7 +533,7 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
       }
       const __nv_bfloat16 b = __float2bfloat16(y);
       if (idx < G * HD) {
-        sq[idx / HD][jj] = bf2f(b) * P.scale;
+        sqb[(idx / HD) * A::QP + jj] = b;
       } else if (idx < (G + 1) * HD) {
         snew[jj] = b;
         if (owner) kcw[at + jj] = b;
@@ -478,42 +544,25 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
     }
   }
   csync();
+  }
 
   if (tr && ct == 0 && tr[11] == 0) tr[11] = clock64() - c_start;
-  // ---- (2) keys: each warp streams its tiles
-  const __nv_bfloat16* kc = P.kc + P.kv_layer_elems * layer;
-  const __nv_bfloat16* vc = P.vc + P.kv_layer_elems * layer;
-  uint8_t* kb = tiles + warp * A::warp_bytes;
-  uint8_t* vb = kb + A::kbuf;
-  float mrun[G], lrun[G], acc[G][DPL];
+  // ---- (2) keys: each warp streams its tiles; S = Q K^T and O += P V on the
+  // tensor cores (mma.sync m16n8k16: rows = the G query heads padded to 16)
+  constexpr int NKT = KT / 8, NDT = HD / 8;
+  float o[NDT][4];
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    mrun[g] = -INFINITY;
-    lrun[g] = 0.f;
+  for (int n = 0; n < NDT; ++n)
 #pragma unroll
-    for (int d = 0; d < DPL; ++d) acc[g][d] = 0.f;
-  }
+    for (int i = 0; i < 4; ++i) o[n][i] = 0.f;
+  float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;  // heads lane/4, lane/4 + 8
   for (int t = warp; t < ntiles; t += kCW) {
     const int key0 = k0 + t * KT;
     const int nv = min(KT, k1 - key0);
-    {
-      const int page = spage[key0 / kPageTokens - pg0];
-      const size_t base = (((size_t)page * nkv + kh) * kPageTokens + (key0 % kPageTokens)) * HD;
-      const uint4* kg = reinterpret_cast<const uint4*>(kc + base);
-      const uint4* vg = reinterpret_cast<const uint4*>(vc + base);
-#pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int e = lane + 32 * i, r = e / V4, c = e % V4;
-        if (r < nv) {
-          cp_async16(kb + r * A::ROW + c * 16, kg + e);
-          cp_async16(vb + r * A::VROW + c * 16, vg + e);
-        }
-      }
-      cp_async_commit();
-      cp_async_wait_all();
-    }
+    if (!(early && t == warp)) load_tile(t, spage[key0 / kPageTokens - pg0]);
+    cp_async_wait_all();
     __syncwarp();
-    if (owner && pos >= key0 && pos < key0 + nv) {  // the new key from shared memory
+    if (!P.pairs && owner && pos >= key0 && pos < key0 + nv) {  // the new key from shared memory
       const int r = pos - key0;
       for (int d = lane; d < HD; d += 32) {
         reinterpret_cast<__nv_bfloat16*>(kb + r * A::ROW)[d] = snew[d];
@@ -521,81 +570,105 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
       }
       __syncwarp();
     }
-    float s[G];
+    float sc[NKT][4];
 #pragma unroll
-    for (int g = 0; g < G; ++g) s[g] = 0.f;
-    if (lane < nv) {
+    for (int n = 0; n < NKT; ++n)
 #pragma unroll
-      for (int c = 0; c < V4; ++c) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(kb + lane * A::ROW + c * 16);
-        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-        float kf[8];
+      for (int i = 0; i < 4; ++i) sc[n][i] = 0.f;
+    const __nv_bfloat16* kt = reinterpret_cast<const __nv_bfloat16*>(kb);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(p2[e]);
-          kf[2 * e] = f.x;
-          kf[2 * e + 1] = f.y;
-        }
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      uint32_t a[4];
+      const __nv_bfloat16* qa = sqb + (lane >> 2) * A::QP + kk * 16 + (lane & 3) * 2;
+      a[0] = ld_b32(qa);
+      a[1] = ld_b32(qa + 8 * A::QP);
+      a[2] = ld_b32(qa + 8);
+      a[3] = ld_b32(qa + 8 * A::QP + 8);
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const float4 qa = *reinterpret_cast<const float4*>(&sq[g][c * 8]);
-          const float4 qb = *reinterpret_cast<const float4*>(&sq[g][c * 8 + 4]);
-          s[g] += qa.x * kf[0] + qa.y * kf[1] + qa.z * kf[2] + qa.w * kf[3] + qb.x * kf[4] +
-                  qb.y * kf[5] + qb.z * kf[6] + qb.w * kf[7];
-        }
+      for (int n = 0; n < NKT; ++n) {
+        const __nv_bfloat16* kp = kt + (n * 8 + (lane >> 2)) * (A::ROW / 2) + kk * 16 + (lane & 3) * 2;
+        mma16816(sc[n], a, ld_b32(kp), ld_b32(kp + 8));
       }
     }
+    float mx_lo = m_lo, mx_hi = m_hi;
 #pragma unroll
-    for (int g = 0; g < G; ++g) {  // online softmax
-      const float sv_ = lane < nv ? s[g] : -INFINITY;
-      const float mn = fmaxf(mrun[g], wmax(sv_));
-      const float corr = mrun[g] == -INFINITY ? 0.f : __expf(mrun[g] - mn);
-      const float p = lane < nv ? __expf(sv_ - mn) : 0.f;
-      lrun[g] = lrun[g] * corr + wsum(p);
-      mrun[g] = mn;
+    for (int n = 0; n < NKT; ++n)
 #pragma unroll
-      for (int d = 0; d < DPL; ++d) acc[g][d] *= corr;
-      sp[warp][g][lane] = p;
+      for (int i = 0; i < 4; ++i) {
+        const int key = n * 8 + (lane & 3) * 2 + (i & 1);
+        sc[n][i] = key < nv ? sc[n][i] * P.scale : -INFINITY;
+        if (i < 2) mx_lo = fmaxf(mx_lo, sc[n][i]);
+        else mx_hi = fmaxf(mx_hi, sc[n][i]);
+      }
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+      mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, off));
+      mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, off));
+    }
+    const float c_lo = m_lo == -INFINITY ? 0.f : __expf(m_lo - mx_lo);
+    const float c_hi = m_hi == -INFINITY ? 0.f : __expf(m_hi - mx_hi);
+    m_lo = mx_lo;
+    m_hi = mx_hi;
+    float sum_lo = 0.f, sum_hi = 0.f;
+#pragma unroll
+    for (int n = 0; n < NKT; ++n)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float mm = i < 2 ? m_lo : m_hi;
+        const float pv = sc[n][i] == -INFINITY ? 0.f : __expf(sc[n][i] - mm);
+        sc[n][i] = pv;
+        if (i < 2) sum_lo += pv;
+        else sum_hi += pv;
+      }
+    l_lo = l_lo * c_lo + sum_lo;  // per-lane partial sums (quad-reduced at the end)
+    l_hi = l_hi * c_hi + sum_hi;
+#pragma unroll
+    for (int n = 0; n < NDT; ++n) {
+      o[n][0] *= c_lo; o[n][1] *= c_lo;
+      o[n][2] *= c_hi; o[n][3] *= c_hi;
+    }
+    // P enters as hi + lo bf16 halves (two MMAs on the same V fragment): ~16
+    // mantissa bits, so P.V keeps fp32-class accuracy (the oracle's P is fp64)
+#pragma unroll
+    for (int ks = 0; ks < KT / 16; ++ks) {
+      uint32_t ah[4], al[4];
+      split_bf16(sc[2 * ks][0], sc[2 * ks][1], ah[0], al[0]);
+      split_bf16(sc[2 * ks][2], sc[2 * ks][3], ah[1], al[1]);
+      split_bf16(sc[2 * ks + 1][0], sc[2 * ks + 1][1], ah[2], al[2]);
+      split_bf16(sc[2 * ks + 1][2], sc[2 * ks + 1][3], ah[3], al[3]);
+#pragma unroll
+      for (int n = 0; n < NDT; ++n) {
+        uint32_t b0, b1;
+        ldsm_x2_trans(b0, b1, vb, A::VROW, ks * 16, n * 8, lane);
+        mma16816(o[n], ah, b0, b1);
+        mma16816(o[n], al, b0, b1);
+      }
     }
     __syncwarp();
-    for (int j = 0; j < nv; ++j) {
-      float vf[DPL];
-      const uint8_t* vrow = vb + j * A::VROW + lane * DPL * 2;
-      if constexpr (DPL == 2) {
-        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vrow));
-        vf[0] = f.x;
-        vf[1] = f.y;
-      } else {
-        const uint2 raw = *reinterpret_cast<const uint2*>(vrow);
-        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-        const float2 a = __bfloat1622float2(p2[0]), c2 = __bfloat1622float2(p2[1]);
-        vf[0] = a.x; vf[1] = a.y; vf[2] = c2.x; vf[3] = c2.y;
-      }
+  }
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float pj = sp[warp][g][j];
-#pragma unroll
-        for (int d = 0; d < DPL; ++d) acc[g][d] += pj * vf[d];
-      }
-    }
-    __syncwarp();
+  for (int off = 1; off <= 2; off <<= 1) {
+    l_lo += __shfl_xor_sync(0xffffffffu, l_lo, off);
+    l_hi += __shfl_xor_sync(0xffffffffu, l_hi, off);
   }
 
   // ---- (3) merge the warps, then the splits
   if (tr && ct == 0 && tr[12] == 0) tr[12] = clock64() - c_start;
   csync();  // sm_acc aliases the tiles
   if (tr && ct == 0 && tr[13] == 0) tr[13] = clock64() - c_start;
-  if (lane == 0) {
+  {
+    const int h_lo = lane >> 2, h_hi = h_lo + 8;
+    if ((lane & 3) == 0) {
+      if (h_lo < G) { sm_m[warp][h_lo] = m_lo; sm_l[warp][h_lo] = l_lo; }
+      if (h_hi < G) { sm_m[warp][h_hi] = m_hi; sm_l[warp][h_hi] = l_hi; }
+    }
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      sm_m[warp][g] = mrun[g];
-      sm_l[warp][g] = lrun[g];
+    for (int n = 0; n < NDT; ++n) {
+      const int d = n * 8 + (lane & 3) * 2;
+      if (h_lo < G) { sm_acc[warp][h_lo][d] = o[n][0]; sm_acc[warp][h_lo][d + 1] = o[n][1]; }
+      if (h_hi < G) { sm_acc[warp][h_hi][d] = o[n][2]; sm_acc[warp][h_hi][d + 1] = o[n][3]; }
     }
   }
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-#pragma unroll
-    for (int d = 0; d < DPL; ++d) sm_acc[warp][g][lane * DPL + d] = acc[g][d];
   csync();
   constexpr size_t rec = (size_t)G * (HD + 2);
   float* my_ws = ws + (((size_t)m * nkv + kh) * splits + split) * rec;
@@ -911,6 +984,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* cbar = tempty + 2;  // compute warps' bulk-copy barrier
+  uint64_t* xbar = cbar + 1;    // pair phases: the partner CTA's partial rows have landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Lo::misc);
   int* s_flag = reinterpret_cast<int*>(smem + Lo::misc + 4);
   int* s_seen = reinterpret_cast<int*>(smem + Lo::misc + 8);  // last phase seen complete
@@ -936,6 +1010,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
         mbar_init(&tempty[a], kCT);
       }
       mbar_init(cbar, 1);
+      mbar_init(xbar, 1);
       fence_barrier_init();
     }
     __syncwarp();
@@ -1041,6 +1116,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
     const int col = ct & (kBN - 1);      // accumulator lane (= output column) drained
     const int hf = cw >> 2;              // token half [32 hf, 32 hf + 32) drained
     uint32_t cph = 0;                    // cbar phase
+    uint32_t xph = 0;                    // xbar phase
     bool rows_ready = false;
     const bool stamp = P.stamps != nullptr && c == 0 && ct == 0;
     int acc = 0;
@@ -1097,6 +1173,35 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           unsigned short colv_bits = colv0;
           if (i != first_item(c, F.rot, GR) && colv_off >= 0 && tile_n * kBN + col < F.N)
             colv_bits = reinterpret_cast<const unsigned short*>(P.w)[colv_off + tile_n * kBN + col];
+          // pair items: register the partner's incoming bytes, and gather what
+          // the epilogue needs (it does not depend on this phase) under the MMA
+          const bool pair = P.pairs && F.cs == 2;
+          const int phalf = (P.S + 1) / 2;
+          const int pr0 = split == 0 ? 0 : phalf, pr1 = split == 0 ? phalf : P.S;
+          float* xbuf = tile + kTok * kPitch;                            // partner's rows (pitch kPitch)
+          int4* s_row4 = reinterpret_cast<int4*>(xbuf + 32 * kPitch);   // QKV row metadata
+          float* xs = reinterpret_cast<float*>(s_row4 + kTok);          // O: residual rows (pitch kBN)
+          EpiParams qe;
+          if (pair) {
+            if (ct == 0) mbar_arrive_expect_tx(xbar, (uint32_t)((pr1 - pr0) * kPitch * 4));
+            if (F.kind == MK_QKV) {
+              qe.kind = EPI_QKV;
+              qe.ssq_in = P.ssq; qe.ssq_in_parts = P.parts; qe.inv_dim = P.inv_h; qe.eps = P.eps;
+              qe.bias = P.w + P.layers[F.layer].qkv_b;
+              qe.nq = P.nq; qe.nkv = P.nkv; qe.hd = P.hd; qe.pages_per_seq = P.pps;
+              qe.row_slot = P.plan.row_slot; qe.row_pos = P.plan.row_pos; qe.block_table = P.block_table;
+              qe.cos_sin = P.cos_sin; qe.q_out = P.q;
+              qe.kc = P.kc + P.kv_layer_elems * F.layer; qe.vc = P.vc + P.kv_layer_elems * F.layer;
+              gemm_detail::epi_row_meta(qe, pr0, pr1, 0, P.S, s_rstd, s_row4, ct, kCT);
+            } else {  // O: x[pr0, pr1) x 128 columns into xs by cp.async
+              const int n0 = tile_n * kBN;
+              for (int e = ct; e < (pr1 - pr0) * (kBN / 4); e += kCT) {
+                const int j = pr0 + e / (kBN / 4), cc = (e % (kBN / 4)) * 4;
+                cp_async16(xs + (j - pr0) * kBN + cc, P.x + (size_t)j * F.N + n0 + cc);
+              }
+              cp_async_commit();
+            }
+          }
           mk_wait(&tfull[acc], aph);
           tc_fence_after();
           if (tr && ct == 0 && tr[1] == 0) tr[1] = clock64() - tr[8];
@@ -1108,7 +1213,45 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           if (++acc == 2) { acc = 0; aph ^= 1; }
           const int j0 = hf * 32;  // tokens of ra
           int r0 = 0, r1 = P.S;
-          if (F.kind == MK_QKV) {
+          if (pair) {
+            // ---- split-K over the CTA pair (cluster of 2): split s owns rows
+            // [pr0, pr1).  Both halves of the partial go to the local tile; the
+            // partner's half is shipped in ONE bulk copy into its xbuf, landing
+            // on its xbar.  Result = p0 + p1 on both sides (fp add commutes):
+            // deterministic.
+            const uint32_t other = (uint32_t)split ^ 1u;
+            r0 = pr0;
+            r1 = pr1;
+            const int o0 = split == 0 ? phalf : 0, o1 = split == 0 ? P.S : phalf;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j0 + j < P.S) tile[(j0 + j) * kPitch + col] = __uint_as_float(ra[j]);
+            fence_proxy_async_shared();
+            csync();
+            if (ct == 0 && o1 > o0) {
+              const uint32_t dst = partner_addr(xbuf, other), bar = partner_addr(xbar, other);
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                  ::"r"(dst), "r"(smem_u32(tile + o0 * kPitch)), "r"((uint32_t)((o1 - o0) * kPitch * 4)), "r"(bar)
+                  : "memory");
+            }
+            mk_wait(xbar, xph);
+            xph ^= 1;
+            if (tr && ct == 0 && tr[2] == 0) tr[2] = clock64() - tr[8];
+            for (int e = ct; e < (r1 - r0) * kBN; e += kCT) {
+              const int j = r0 + e / kBN, cc = e % kBN;
+              tile[j * kPitch + cc] += xbuf[(j - r0) * kPitch + cc];
+            }
+            if (F.kind == MK_O) cp_async_wait_all();
+            csync();
+            if (F.kind == MK_QKV) {
+              // bias, rstd, RoPE, q -> bf16 rows, k / v -> the paged cache (gemm_epi.cuh)
+              gemm_detail::epi_apply(qe, tile, kPitch, r0, r1, 0, tile_n * kBN, tile_n, (F.N + kBN - 1) / kBN,
+                                     P.S, F.N, s_rstd, s_row4, ct, kCT, [] { csync(); });
+              csync();
+              continue;
+            }
+          } else if (F.kind == MK_QKV) {
             // raw split partial [split][row][col]; the attention items reduce it
             const int n = tile_n * kBN + col;
             if (n < F.N) {  // consumer layout [row][kv head][split][q heads | k | v]
@@ -1128,8 +1271,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
               }
             }
             continue;
-          }
-          if (F.cs == 1) {
+          } else if (F.cs == 1) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) tile[(j0 + j) * kPitch + col] = __uint_as_float(ra[j]);
           } else {
@@ -1181,7 +1323,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           if (tr && ct == 0 && tr[5] == 0) tr[5] = clock64() - tr[8];
           csync();
           const float colv = __uint_as_float((unsigned)colv_bits << 16);
-          if (r1 > r0) mk_epilogue(P, F, tile_n, tile, s_rstd, ct, r0, r1, colv);
+          if (r1 > r0) mk_epilogue(P, F, tile_n, tile, s_rstd, ct, r0, r1, colv, pair ? xs : nullptr);
           csync();
           if (tr && ct == 0 && tr[6] == 0) tr[6] = clock64() - tr[8];
         }
@@ -1237,11 +1379,15 @@ cudaError_t launch_t(const MkParams& p, int grid, cudaStream_t st) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = Lo::alloc;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeCooperative;  // co-residency for the phase counters
   at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;  // pair mode: CTAs 2i, 2i+1 share DSMEM
+  at[1].val.clusterDim.x = p.pairs ? 2 : 1;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = p.pairs ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, decode_megakernel<HD, G>, p);
 }
 
@@ -1273,6 +1419,7 @@ int megakernel_qkv_splits(const DecoderDims& d, int grid) {
   int cap = 1;
   if (d.hd == 64) cap = G == 2 ? qkv_cap_t<64, 2>() : qkv_cap_t<64, 7>();
   else cap = G == 6 ? qkv_cap_t<128, 6>() : qkv_cap_t<128, 7>();
+  cap = cap / 4 > 1 ? cap / 4 : 1;  // staging <= 2 of the 8 K/V warp buffers: 6 tiles load early
   const int cs = megakernel_splits(d.qkv(), d.H, grid);
   return cs < cap ? cs : cap;
 }
@@ -1295,6 +1442,37 @@ size_t megakernel_smem_bytes(const DecoderDims& d) {
   const int G = d.nq / d.nkv;
   if (d.hd == 64) return G == 2 ? MkLayout<64, 2>::alloc : MkLayout<64, 7>::alloc;
   return G == 6 ? MkLayout<128, 6>::alloc : MkLayout<128, 7>::alloc;
+}
+
+template <int HD, int G>
+int pair_clusters_t() {
+  if (!set_smem_attr<HD, G>()) return 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = MkLayout<HD, G>::alloc;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, decode_megakernel<HD, G>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int megakernel_pair_clusters(const DecoderDims& d) {
+  const int G = d.nq / d.nkv;
+  if (d.hd == 64 && G == 2) return pair_clusters_t<64, 2>();
+  if (d.hd == 64 && G == 7) return pair_clusters_t<64, 7>();
+  if (d.hd == 128 && G == 6) return pair_clusters_t<128, 6>();
+  if (d.hd == 128 && G == 7) return pair_clusters_t<128, 7>();
+  return 0;
 }
 
 int megakernel_occupancy(const DecoderDims& d) {

@@ -81,6 +81,8 @@ struct MkParams {
   unsigned long long* stamps;   // profiling: [n_phases + 1] globaltimer (ns) or nullptr
   int dbg;                      // experiments
   int pf_blocks;                // L2 weight prefetch distance (16 KB k-blocks per CTA)
+  int pairs;                    // launched as CTA pairs (cluster 2): QKV and O reduce split-K
+                                // through DSMEM; attention reads finished q / K / V
   unsigned long long* trace;    // debugging: [n_phases][grid][8] per-CTA timestamps or nullptr
 };
 
@@ -93,6 +95,8 @@ int megakernel_qkv_splits(const DecoderDims& d, int grid);
 // Floats of split partials a phase needs.
 size_t megakernel_ws_floats(int n_items, int cs, int rows);
 size_t megakernel_smem_bytes(const DecoderDims& d);
+// Co-resident clusters of two megakernel CTAs (pair mode needs grid / 2).
+int megakernel_pair_clusters(const DecoderDims& d);
 // CTAs of the megakernel resident per SM (0: cannot launch).
 int megakernel_occupancy(const DecoderDims& d);
 cudaError_t launch_megakernel(const MkParams& p, const DecoderDims& d, int grid, cudaStream_t st);

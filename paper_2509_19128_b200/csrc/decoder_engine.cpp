@@ -323,12 +323,18 @@ int DecoderBackend::mega_init() {
   const int grid = r.sms;
   if (megakernel_occupancy(d_) < 1) return SRL_OK;  // not co-resident: multi-kernel round
   const int L = d_.L, splits = (max_seq_ + kMkAttnChunk - 1) / kMkAttnChunk;
+  // pair mode (SRL_MK_PAIRS=1): cluster of two CTAs, DSMEM split-K for QKV and
+  // O, attention reads finished q / K / V
+  const char* pe = std::getenv("SRL_MK_PAIRS");
+  // (measured slower at 0.5B / B = 64: the 32-row pair epilogues are latency-bound; off by default)
+  const bool pairs = pe && pe[0] == '1' && grid % 2 == 0 && megakernel_pair_clusters(d_) * 2 >= grid;
   std::vector<MkPhase> ph;
   int ctr = 0, items_total = 0;
   size_t ws = (size_t)S_ * d_.nkv * splits * (d_.nq / d_.nkv) * (d_.hd + 2);
   auto add = [&](int kind, int layer, int n_items, int cs, int N, int K, int wmap, int xmap,
                  int counters) {
     MkPhase f{kind, layer, n_items, cs, N, K, wmap, xmap, ctr, items_total % grid, -1};
+    if (pairs && cs == 2 && (kind == MK_QKV || kind == MK_O)) f.rot &= ~1;  // split 0 on the even CTA
     const LayerOffsets* lo = buf_[0]->layout.layers;
     if (kind == MK_O) f.colv = (long long)lo[layer].ln2;
     if (kind == MK_DOWN)
@@ -354,11 +360,15 @@ int DecoderBackend::mega_init() {
   int qkv_cs = megakernel_qkv_splits(d_, grid);
   if (const char* v = std::getenv("SRL_MK_CS_QKV")) qkv_cs = std::max(1, std::min(qkv_cs, std::atoi(v)));
   const int qkv_tiles = (d_.qkv() + 127) / 128;
+  if (pairs) qkv_cs = 2;
   add(MK_EMBED, 0, S_, 1, 0, 0, 0, 0, 0);
   for (int l = 0; l < L; ++l) {
     add(MK_QKV, l, qkv_tiles * qkv_cs, qkv_cs, d_.qkv(), d_.H, 4 * l + 0, 0, 0);
     add(MK_ATTN, l, S_ * d_.nkv * splits, qkv_cs, 0, 0, 0, 0, S_ * d_.nkv);
-    gemm(MK_O, l, d_.H, d_.qdim(), 4 * l + 1, 1);
+    if (pairs)  // the pair reduces through DSMEM: no L2 partials, no counters
+      add(MK_O, l, ((d_.H + 127) / 128) * 2, 2, d_.H, d_.qdim(), 4 * l + 1, 1, 0);
+    else
+      gemm(MK_O, l, d_.H, d_.qdim(), 4 * l + 1, 1);
     gemm(MK_GU, l, 2 * d_.I, d_.H, 4 * l + 2, 0);
     gemm(MK_DOWN, l, d_.H, d_.I, 4 * l + 3, 2);
   }
@@ -427,6 +437,7 @@ int DecoderBackend::mega_init() {
     if (const char* dbg = std::getenv("SRL_MK_DBG")) P.dbg = std::atoi(dbg);
     P.pf_blocks = 0;  // L2 weight prefetch: off (measured slower; SRL_MK_PF_KB to experiment)
     if (const char* pf = std::getenv("SRL_MK_PF_KB")) P.pf_blocks = std::max(0, std::atoi(pf) / 16);
+    P.pairs = pairs ? 1 : 0;
   }
   mk_.stamps = reinterpret_cast<unsigned long long*>(base + o_st);
   if (std::getenv("SRL_MK_TRACE")) SRL_CUDA(cudaMalloc(&mk_.trace, 128 * (size_t)n * grid));

@@ -186,9 +186,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int lane = threadIdx.x & 31;
           float rs = 1.f;  // rstd of token tc0 + lane, broadcast below
           if (epi.ssq_in != nullptr && tc0 + lane < M) {
-            float sacc = 0.f;
-            for (int p = 0; p < epi.ssq_in_parts; ++p)
-              sacc += epi.ssq_in[(size_t)(tc0 + lane) * epi.ssq_in_parts + p];
+            const float sacc = gemm_detail::ssq_row_sum(epi.ssq_in + (size_t)(tc0 + lane) * epi.ssq_in_parts,
+                                                        epi.ssq_in_parts);
             rs = rsqrtf(sacc * epi.inv_dim + epi.eps);
           }
           const float bias = (epi.bias != nullptr && n < N) ? gemm_detail::epi_bf2f(epi.bias[n]) : 0.f;

@@ -31,6 +31,22 @@ __device__ __forceinline__ float epi_warp_max(float v) {
   return v;
 }
 
+// Sum of a row's x^2 partials (one per 128 columns) in index order -- the
+// loads of a batch of 8 are issued together (a dependent load-add chain costs
+// one L2 round trip per part).
+__device__ __forceinline__ float ssq_row_sum(const float* row, int parts) {
+  float s = 0.f;
+  for (int p0 = 0; p0 < parts; p0 += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = p0 + u < parts ? row[p0 + u] : 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (p0 + u < parts) s += v[u];
+  }
+  return s;
+}
+
 // Per-row inputs of rows [r0, r1): the deferred-RMSNorm rstd and (EPI_QKV)
 // the row's KV-cache coordinates (slot, pos, page, offset in page).
 __device__ __forceinline__ void epi_row_meta(const EpiParams& epi, int r0, int r1, int t0, int M,
@@ -39,8 +55,7 @@ __device__ __forceinline__ void epi_row_meta(const EpiParams& epi, int r0, int r
     float r = 1.f;
     const int m = t0 + j;
     if (epi.ssq_in != nullptr && m < M) {
-      float s = 0.f;
-      for (int p = 0; p < epi.ssq_in_parts; ++p) s += epi.ssq_in[(size_t)m * epi.ssq_in_parts + p];
+      const float s = ssq_row_sum(epi.ssq_in + (size_t)m * epi.ssq_in_parts, epi.ssq_in_parts);
       r = rsqrtf(s * epi.inv_dim + epi.eps);
     }
     s_rstd[j] = r;
@@ -101,6 +116,59 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
       const float a = g / (1.f + expf(-g)) * u;
       epi.out_bf16[(size_t)m * epi.ld_bf16 + (n0 >> 1) + c] = __float2bfloat16(a);
     }
+  } else if (epi.kind == EPI_QKV && (nthr & 127) == 0) {
+    // thread = one column c for rows r0 + (tid >> 7) + k * (nthr / 128): the
+    // bias is loaded once, the RoPE cos/sin of 8 rows are in flight together
+    const int c = tid & 127, rstep = nthr >> 7, n = n0 + c;
+    const bool colok = n < N;
+    const float bias = colok ? epi_bf2f(epi.bias[n]) : 0.f;
+    for (int j = r0 + (tid >> 7); j < r1; j += rstep) {
+      float v = 0.f;
+      if (t0 + j < M && colok) v = tile[j * pitch + c] * s_rstd[j] + bias;
+      tile[j * pitch + c] = v;
+    }
+    sync();
+    const int hd = epi.hd, half = hd >> 1;
+    const int qend = epi.nq * hd, kend = (epi.nq + epi.nkv) * hd;
+    const int jj = n % hd, i = jj < half ? jj : jj - half;
+    const bool rot = n < kend;
+    for (int jb = r0 + (tid >> 7); jb < r1; jb += 8 * rstep) {
+      float co[8], si[8];
+      int4 rc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = jb + u * rstep;
+        rc[u] = j < r1 ? s_row[j] : make_int4(-1, 0, 0, 0);
+        co[u] = 1.f;
+        si[u] = 0.f;
+        if (rot && colok && rc[u].x >= 0 && t0 + j < M) {
+          co[u] = epi.cos_sin[(size_t)rc[u].y * hd + i];
+          si[u] = epi.cos_sin[(size_t)rc[u].y * hd + half + i];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = jb + u * rstep, m = t0 + j;
+        if (j >= r1 || m >= M || !colok || rc[u].x < 0) continue;
+        const float* row = &tile[j * pitch + (c - jj)];  // this head's hd values
+        float y;
+        if (rot) {  // RoPE (rotate pairs (i, i + hd/2)) on q and k
+          const float x1 = row[i], x2 = row[i + half];
+          y = jj < half ? x1 * co[u] - x2 * si[u] : x2 * co[u] + x1 * si[u];
+        } else {
+          y = row[jj];
+        }
+        const __nv_bfloat16 b = __float2bfloat16(y);
+        if (n < qend) {
+          epi.q_out[(size_t)m * qend + n] = b;
+        } else {
+          const int kv = n < kend ? n - qend : n - kend;
+          const size_t at = (((size_t)rc[u].z * epi.nkv + kv / hd) * 64 + rc[u].w) * hd + jj;
+          if (n < kend) epi.kc[at] = b;
+          else epi.vc[at] = b;
+        }
+      }
+    }
   } else if (epi.kind == EPI_QKV) {
     for (int idx = tid; idx < rows * 128; idx += nthr) {
       const int j = r0 + (idx >> 7), c = idx & 127;
@@ -118,9 +186,9 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
       const int4 rc = s_row[j];
       if (m >= M || n >= N || rc.x < 0) continue;
       const int jj = n % hd;
-      const float* row = &tile[j * pitch + (c - jj)];  // this head's hd values
+      const float* row = &tile[j * pitch + (c - jj)];
       float y;
-      if (n < kend) {  // RoPE (rotate pairs (i, i + hd/2)) on q and k
+      if (n < kend) {
         const int i = jj < half ? jj : jj - half;
         const float co = epi.cos_sin[(size_t)rc.y * hd + i];
         const float si = epi.cos_sin[(size_t)rc.y * hd + half + i];
@@ -134,8 +202,7 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
         epi.q_out[(size_t)m * qend + n] = b;
       } else {
         const int kv = n < kend ? n - qend : n - kend;
-        const int kh = kv / hd;
-        const size_t at = (((size_t)rc.z * epi.nkv + kh) * 64 + rc.w) * hd + jj;
+        const size_t at = (((size_t)rc.z * epi.nkv + kv / hd) * 64 + rc.w) * hd + jj;
         if (n < kend) epi.kc[at] = b;
         else epi.vc[at] = b;
       }
@@ -179,6 +246,42 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
       const __nv_bfloat16 d = __float2bfloat16(epi.row_coef[m] * ((n == s_row[j].x ? 1.f : 0.f) - p));
       epi.out_bf16[(size_t)m * epi.ld_bf16 + n] = d;
       if (epi.outT_bf16) epi.outT_bf16[(size_t)n * epi.ldT + m] = d;
+    }
+  } else if (epi.kind == EPI_RESID && (nthr & 127) == 0) {
+    // thread = one column; the residual loads of 8 rows are in flight together
+    const int c = tid & 127, rstep = nthr >> 7, n = n0 + c;
+    const bool colok = n < N;
+    const float gain = colok ? epi_bf2f(epi.gain[n]) : 0.f;
+    for (int jb = r0 + (tid >> 7); jb < r1; jb += 8 * rstep) {
+      float xr[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = jb + u * rstep;
+        xr[u] = (j < r1 && t0 + j < M && colok) ? epi.resid[(size_t)(t0 + j) * N + n] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = jb + u * rstep;
+        if (j >= r1) break;
+        float x = 0.f;
+        if (t0 + j < M && colok) {
+          const size_t o = (size_t)(t0 + j) * N + n;
+          x = xr[u] + tile[j * pitch + c];
+          epi.resid[o] = x;
+          epi.xg[o] = __float2bfloat16(x * gain);
+        }
+        tile[j * pitch + c] = x;
+      }
+    }
+    sync();
+    for (int j = r0 + warp; j < r1; j += nwarps) {
+      float s = 0.f;
+      for (int cc = lane; cc < 128; cc += 32) {
+        const float x = tile[j * pitch + cc];
+        s += x * x;
+      }
+      s = epi_warp_sum(s);
+      if (lane == 0 && t0 + j < M) epi.ssq_out[(size_t)(t0 + j) * n_tiles + n_tile] = s;
     }
   } else if (epi.kind == EPI_RESID) {
 #pragma unroll 4
