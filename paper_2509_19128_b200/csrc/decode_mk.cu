@@ -81,8 +81,12 @@ __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
 #define SRL_BAR_LANES 1
 #endif
 constexpr int kBarLanes = SRL_BAR_LANES;
+// Arrival = one release reduction (no return value to wait for; .release
+// orders this CTA's prior writes -- made CTA-visible by the preceding bar.sync
+// -- before the count, like __threadfence + atomicAdd, without the round trip).
 __device__ __forceinline__ void phase_arrive(unsigned* pd, int p, int c) {
-  atomicAdd(&pd[p * kBarLanes + (c % kBarLanes)], 1u);
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&pd[p * kBarLanes + (c % kBarLanes)]), "r"(1u)
+               : "memory");
 }
 __device__ __forceinline__ void phase_wait(const unsigned* pd, int p, unsigned target) {
   SpinGuard g;
@@ -388,7 +392,7 @@ __device__ __forceinline__ void mk_epilogue(const MkParams& P, const MkPhase& ph
 //  3. warps merged in shared memory; several splits (long contexts) merged by
 //     the last-arriving split in split order (deterministic).
 template <int HD, int G>
-__device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, int kh, int split,
+__device__ void mk_attention(const MkParams& P, int layer, long long bias_off, int qkv_cs, int m, int kh, int split,
                              uint8_t* scr, const int2* s_rows, unsigned* ctr, unsigned ep1,
                              float* ws, int ct, int* s_flag, uint64_t* cbar, uint32_t& cph,
                              unsigned long long* tr) {
@@ -401,7 +405,6 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
   float(*sp)[G][32] = reinterpret_cast<float(*)[G][32]>(scr + A::sq + A::tiles);
   float(*sm_m)[G] = reinterpret_cast<float(*)[G]>(scr + A::sq + A::tiles + A::sp);
   float(*sm_l)[G] = reinterpret_cast<float(*)[G]>(scr + A::sq + A::tiles + A::sp + sizeof(float) * kCW * G);
-  int* spage = reinterpret_cast<int*>(scr + A::sq + A::tiles + A::sp + A::sml);
   float* sraw = reinterpret_cast<float*>(scr + A::sq + A::tiles + A::sp + A::sml + A::spage);
   __nv_bfloat16* snew = reinterpret_cast<__nv_bfloat16*>(scr + A::sq + A::tiles + A::sp + A::sml +
                                                          A::spage + A::sraw);
@@ -423,7 +426,6 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
   const bool owner = pos >= k0 && pos < k0 + P.attn_chunk;  // this split holds the new key
   const int qend = nq * HD, kend = qend + nkv * HD;
 
-  const int pg0 = k0 / kPageTokens;
   // K/V tiles: warp w streams tiles w, w + 8, ... into buffer slot 7 - w, so the
   // first tiles land in the slots the QKV partial staging does not alias and
   // their loads are issued now, under the partials' L2 round trip
@@ -451,40 +453,43 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
   };
   const int free_slot0 = P.pairs ? 0 : (qkv_cs * W * 4 + (int)A::warp_bytes - 1) / (int)A::warp_bytes;
   const bool early = warp < ntiles && kCW - 1 - warp >= free_slot0;
-  if (early) load_tile(warp, P.block_table[(size_t)slot * P.pps + (k0 + warp * KT) / kPageTokens]);
   if (P.pairs) {
+    if (early) load_tile(warp, P.block_table[(size_t)slot * P.pps + (k0 + warp * KT) / kPageTokens]);
     // pair mode: the QKV phase already wrote q (bf16, post-RoPE) and the new
     // token's K/V into the paged cache
     const __nv_bfloat16* qrow = P.q + (size_t)m * nq * HD + (size_t)kh * G * HD;
     for (int i = ct; i < 16 * HD; i += kCT)
       sqb[(i / HD) * A::QP + i % HD] = i < G * HD ? qrow[i] : __float2bfloat16(0.f);
-    for (int i = ct; i < (nkeys + kPageTokens - 1) / kPageTokens; i += kCT)
-      spage[i] = P.block_table[(size_t)slot * P.pps + pg0 + i];
     csync();
   } else {
   // ---- (1) operands: split partials (bulk), pages, bias, rope, rstd -- all in flight
   float* stage = reinterpret_cast<float*>(tiles);  // [qkv_cs][W], free until the K/V tiles
   if (ct == 0) {  // the row's partials are contiguous: [m][kh][split][W]
-    fence_proxy_async_global();
+    // (the writers fenced generic -> async proxy before their phase arrival)
     mbar_arrive_expect_tx(cbar, (uint32_t)(qkv_cs * W * 4));
     bulk_g2s(stage, P.qkv_part + ((size_t)m * nkv + kh) * qkv_cs * W, qkv_cs * W * 4, cbar);
+    if (tr && tr[4] == 0) tr[4] = clock64() - c_start;
   }
-  for (int i = ct; i < (nkeys + kPageTokens - 1) / kPageTokens; i += kCT)
-    spage[i] = P.block_table[(size_t)slot * P.pps + pg0 + i];
+  // every independent load first (one L2 round trip for all of them), the
+  // consumers after: the early tile's page, the new token's page, the bias
+  // (raw bf16 bits), RoPE cos / sin, the row's x^2 partials
+  const int page_early = early ? P.block_table[(size_t)slot * P.pps + (k0 + warp * KT) / kPageTokens] : 0;
+  const int cpage = P.block_table[(size_t)slot * P.pps + pos / kPageTokens];
   constexpr int half = HD / 2;
-  const __nv_bfloat16* bias = P.w + P.layers[layer].qkv_b;
-  float bia[WPT], co[WPT], si[WPT];
+  const unsigned short* bias = reinterpret_cast<const unsigned short*>(P.w + bias_off);
+  unsigned short bbits[WPT];
+  float co[WPT], si[WPT];
 #pragma unroll
   for (int u = 0; u < WPT; ++u) {
     const int idx = ct + u * kCT;
-    bia[u] = 0.f;
+    bbits[u] = 0;
     co[u] = 1.f;
     si[u] = 0.f;
     if (idx < W) {
       const int col = idx < G * HD ? kh * G * HD + idx
                       : idx < (G + 1) * HD ? qend + kh * HD + (idx - G * HD)
                                            : kend + kh * HD + (idx - (G + 1) * HD);
-      bia[u] = bf2f(bias[col]);
+      bbits[u] = bias[col];
       if (idx < (G + 1) * HD) {
         const int jj = idx % HD, i = jj < half ? jj : jj - half;
         co[u] = P.cos_sin[(size_t)pos * HD + i];
@@ -492,9 +497,12 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
       }
     }
   }
-  const int cpage = P.block_table[(size_t)slot * P.pps + pos / kPageTokens];
-  float ss = 0.f;
-  ss = gemm_detail::ssq_row_sum(P.ssq + (size_t)m * P.parts, P.parts);
+  const float ss = gemm_detail::ssq_row_sum(P.ssq + (size_t)m * P.parts, P.parts);
+  if (tr && ct == 0 && tr[6] == 0) tr[6] = clock64() - c_start;
+  if (early) load_tile(warp, page_early);
+  float bia[WPT];
+#pragma unroll
+  for (int u = 0; u < WPT; ++u) bia[u] = __uint_as_float((unsigned)bbits[u] << 16);
   const float rstd = rsqrtf(ss * P.inv_h + P.eps);
   for (int i = ct; i < (16 - G) * HD; i += kCT)
     sqb[(G + i / HD) * A::QP + i % HD] = __float2bfloat16(0.f);
@@ -559,7 +567,7 @@ __device__ void mk_attention(const MkParams& P, int layer, int qkv_cs, int m, in
   for (int t = warp; t < ntiles; t += kCW) {
     const int key0 = k0 + t * KT;
     const int nv = min(KT, k1 - key0);
-    if (!(early && t == warp)) load_tile(t, spage[key0 / kPageTokens - pg0]);
+    if (!(early && t == warp)) load_tile(t, P.block_table[(size_t)slot * P.pps + key0 / kPageTokens]);
     cp_async_wait_all();
     __syncwarp();
     if (!P.pairs && owner && pos >= key0 && pos < key0 + nv) {  // the new key from shared memory
@@ -1160,7 +1168,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           const int split = i % P.attn_splits;
           const int rest = i / P.attn_splits;
           const long long a_c0 = clock64();
-          mk_attention<HD, G>(P, F.layer, F.cs, rest / P.nkv, rest % P.nkv, split, scratch, s_rows,
+          mk_attention<HD, G>(P, F.layer, F.colv, F.cs, rest / P.nkv, rest % P.nkv, split, scratch, s_rows,
                               P.tile_ctr + F.ctr_base, ep1, P.ws, ct, s_flag, cbar, cph, tr);
           if (tr && ct == 0 && tr[10] == 0) tr[10] = clock64() - a_c0;
         }
@@ -1335,7 +1343,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           tr[3] = globaltimer();
           tr[9] = clock64() - tr[8];
         }
-        __threadfence();
         phase_arrive(P.phase_done, p, c);
         if (tr) tr[7] = globaltimer();
       }

@@ -38,7 +38,8 @@ struct MkPhase {
   int xmap;     // activation tensor-map index: 0 xg, 1 attn, 2 act
   int ctr_base; // first split-K counter of this phase
   int rot;      // item -> CTA rotation
-  long long colv;  // O / DOWN: offset of the next RMSNorm gain (epilogue column constant), else -1
+  long long colv;  // O / DOWN: offset of the next RMSNorm gain (epilogue column constant);
+                   // ATTN: offset of the layer's qkv bias; else -1
 };
 
 struct MkLayer {

@@ -337,6 +337,7 @@ int DecoderBackend::mega_init() {
     if (pairs && cs == 2 && (kind == MK_QKV || kind == MK_O)) f.rot &= ~1;  // split 0 on the even CTA
     const LayerOffsets* lo = buf_[0]->layout.layers;
     if (kind == MK_O) f.colv = (long long)lo[layer].ln2;
+    if (kind == MK_ATTN) f.colv = (long long)lo[layer].qkv_b;
     if (kind == MK_DOWN)
       f.colv = (long long)(layer + 1 < d_.L ? lo[layer + 1].ln1 : buf_[0]->layout.final_norm);
     ctr += counters;

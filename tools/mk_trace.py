@@ -36,7 +36,7 @@ GHZ = 1.965  # SM clock under load (bench clocks: 1965 MHz)
 # attention items use 10-14 as cycles since the item start
 GEMM_FIELDS = [(4, "dep"), (14, "full0"), (15, "committed"), (1, "acc"), (11, "stored"), (12, "arrived"), (2, "xchg"), (5, "red"),
                (13, "xready"), (6, "epi"), (9, "end")]
-ATTN_FIELDS = [(1, "issued"), (2, "partials"), (5, "reduced"), (11, "operands"), (12, "keys"), (13, "sync"), (14, "merged"), (10, "item")]
+ATTN_FIELDS = [(4, "bulk"), (6, "loads"), (1, "issued"), (2, "partials"), (5, "reduced"), (11, "operands"), (12, "keys"), (13, "sync"), (14, "merged"), (10, "item")]
 
 
 def analyse(meta, tr):
@@ -59,7 +59,7 @@ def analyse(meta, tr):
         fields = ATTN_FIELDS if kind == "attn" else GEMM_FIELDS
         for k, name in fields:
             v = tr[p, :, k].copy()
-            if k in (4, 14, 15):  # raw clock64 of the producer / MMA warps
+            if k in (4, 14, 15) and kind != "attn":  # raw clock64 of the producer / MMA warps
                 v = np.where(v > 0, v - tr[p, :, 8], 0)
             ok = (v > 0) & active
             r[name] = float(np.median(v[ok])) / GHZ if ok.any() else float("nan")
