@@ -12,6 +12,7 @@
 #include <cstring>
 
 #include "decoder_engine.hpp"
+#include "train.cuh"
 
 namespace srl {
 
@@ -140,6 +141,7 @@ int DecoderRunner::init(const DecoderDims& dims, const WeightLayout& layout, int
   gws.counter_count = counters;
   if ((st2 = alloc(&gws.partials, need)) || (st2 = alloc(&gws.counters, counters))) return st2;
   attn_ws_floats = std::max(attention_ws_floats(d, S, max_seq), attention_ws_floats(d, M_max, max_seq));
+  if ((st2 = alloc(&seg, 4 * (size_t)std::max(S, 1)))) return st2;
   if ((st2 = alloc(&attn_ws, attn_ws_floats)) || (st2 = alloc(&attn_counters, (size_t)M_max * d.nkv)))
     return st2;
   SRL_CUDA(cudaStreamSynchronize(st_));
@@ -184,8 +186,18 @@ int DecoderRunner::forward(int M, const __nv_bfloat16* w, const WeightMaps& wm) 
       te();
     }
     tb(4);
-    launch_attention(q, d, plan, M, block_table, pages_per_seq, kcl, vcl, max_seq, attn_ws,
-                     attn_counters, attn_ws_floats, attn, st_);
+    if (n_seg > 0) {
+      // prompt segments on the tensor cores, the single decode rows per row
+      if (n_single > 0)
+        launch_attention(q, d, plan, n_single, block_table, pages_per_seq, kcl, vcl, max_seq, attn_ws,
+                         attn_counters, attn_ws_floats, attn, st_);
+      SRL_CUDA(launch_attention_fwd_mma(q, kcl, vcl, seg, seg + S, block_table, pages_per_seq, n_seg, d.nq,
+                                        d.nkv, d.hd, attn, nullptr, st_, seg + 2 * S, seg + 3 * S,
+                                        seg_max_rows));
+    } else {
+      launch_attention(q, d, plan, M, block_table, pages_per_seq, kcl, vcl, max_seq, attn_ws,
+                       attn_counters, attn_ws_floats, attn, st_);
+    }
     te();
     EpiParams r;
     r.kind = EPI_RESID; r.resid = x; r.gain = w + o.ln2; r.xg = xg; r.ssq_out = ssq;
@@ -595,18 +607,40 @@ int DecoderBackend::prefill_round(int b, std::vector<int>& prefilled) {
   const int M = (int)rs.size();
   if (M > r.M_max) return fail(SRL_INVALID_ARGUMENT, "prefill exceeds the engine's row budget");
   last_prefill_rows_ = M;
+  // one attention segment per prompt (rows after the running slots' decode rows)
+  std::vector<int32_t> seg(4 * (size_t)S_, 0);
+  int n_seg = 0, seg_max = 0;
+  const int n_single = S_ > 0 ? (int)std::count_if(last.begin(), last.end(), [](int v) { return v >= 0; }) -
+                                    (int)prefilled.size()
+                              : 0;
+  for (int s : prefilled) {
+    const int n = (int)host_[s].tokens.size();
+    seg[n_seg] = last[s] - n + 1;
+    seg[S_ + n_seg] = n;
+    seg[2 * S_ + n_seg] = 0;
+    seg[3 * S_ + n_seg] = s;
+    seg_max = std::max(seg_max, n);
+    ++n_seg;
+  }
   int32_t* pin = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(pinned_) + (size_t)R_ * S_ * sizeof(DevEvent));
   std::memcpy(pin, rs.data(), 4 * M);
   std::memcpy(pin + M, rp.data(), 4 * M);
   std::memcpy(pin + 2 * M, rt.data(), 4 * M);
   std::memcpy(pin + 3 * M, last.data(), 4 * S_);
+  std::memcpy(pin + 3 * M + S_, seg.data(), 16 * (size_t)S_);
+  SRL_CUDA(cudaMemcpyAsync(r.seg, pin + 3 * M + S_, 16 * (size_t)S_, cudaMemcpyHostToDevice, st_));
   SRL_CUDA(cudaMemcpyAsync(r.next.row_slot, pin, 4 * M, cudaMemcpyHostToDevice, st_));
   SRL_CUDA(cudaMemcpyAsync(r.next.row_pos, pin + M, 4 * M, cudaMemcpyHostToDevice, st_));
   SRL_CUDA(cudaMemcpyAsync(r.next.row_token, pin + 2 * M, 4 * M, cudaMemcpyHostToDevice, st_));
   SRL_CUDA(cudaMemcpyAsync(r.next.last_row, pin + 3 * M, 4 * S_, cudaMemcpyHostToDevice, st_));
   launch_plan_copy(r.plan, r.next, M, S_, round_ctr_dev_, st_);
   int st;
-  if ((st = r.forward(M, buf_[b]->w, maps_[b]))) return st;
+  r.n_seg = n_seg;
+  r.n_single = n_single;
+  r.seg_max_rows = seg_max;
+  st = r.forward(M, buf_[b]->w, maps_[b]);
+  r.n_seg = 0;
+  if (st) return st;
   launch_gather_rows(r.xg, r.ssq, r.plan.last_row, S_, d_.H, d_.ssq_parts(), r.xg_last, r.ssq_last, st_);
   if ((st = r.lm_head(S_, maps_[b], true))) return st;
   launch_sample(r.logits, r.lse_max, r.lse_sum, d_.V, S_, r.plan, r.next, ss_, ring_,

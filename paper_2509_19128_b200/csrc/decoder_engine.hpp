@@ -57,6 +57,11 @@ struct DecoderRunner {
   int* attn_counters = nullptr;
   size_t attn_ws_floats = 0;
   CUtensorMap xg_map[2], attn_map[2], act_map[2], last_map[2];
+  // Prompt / recompute segments of the next forward (tensor-core attention):
+  // rows [0, n_single) attend one query each (per-row kernel); segment y covers
+  // rows seg[y] .. + seg[S + y] at positions seg[2S + y] .. of slot seg[3S + y].
+  int32_t* seg = nullptr;         // device [4][slots]
+  int n_seg = 0, n_single = 0, seg_max_rows = 0;
   KernelTimer* timer = nullptr;  // set for a profiled round
   bool unfused_qkv = false;
   void tb(int kind) { if (timer) timer->begin(kind); }

@@ -350,11 +350,16 @@ struct FwdSmem {
   static constexpr size_t total = 2 * tile + tileT;  // Q, K, V^T
 };
 
+// Segment y: query rows seq_start[y] .. + seq_len[y] at positions pos0[y] ..
+// (0 when pos0 is null) of slot seg_slot[y] (y when null); keys 0 .. the last
+// query's position from the slot's pages.  The trainer passes whole packed
+// sequences; a prefill round passes each new prompt (and recompute chunks).
 template <int HD>
 __global__ void __launch_bounds__(kWarps * 32)
     attn_fwd_mma(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ kc,
                  const __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ seq_start,
-                 const int32_t* __restrict__ seq_len, const int32_t* __restrict__ bt, int pps, int nq,
+                 const int32_t* __restrict__ seq_len, const int32_t* __restrict__ seg_pos0,
+                 const int32_t* __restrict__ seg_slot, const int32_t* __restrict__ bt, int pps, int nq,
                  int nkv, float scale, __nv_bfloat16* __restrict__ out, float* __restrict__ lse_out) {
   using S = FwdSmem<HD>;
   constexpr int P = S::P, NT = HD / 8;
@@ -362,13 +367,15 @@ __global__ void __launch_bounds__(kWarps * 32)
   __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smem);
   __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem + S::tile);
   __nv_bfloat16* Vt = reinterpret_cast<__nv_bfloat16*>(smem + 2 * S::tile);
-  const int slot = blockIdx.y, h = blockIdx.z;
-  const int L = seq_len[slot], s0 = seq_start[slot];
-  const int q0 = blockIdx.x * kBlk;
-  if (q0 >= L) return;
+  const int y = blockIdx.y, h = blockIdx.z;
+  const int nrows = seq_len[y], s0 = seq_start[y];
+  const int slot = seg_slot ? seg_slot[y] : y, p0 = seg_pos0 ? seg_pos0[y] : 0;
+  const int q0 = blockIdx.x * kBlk;  // first query of the block (segment-local)
+  if (q0 >= nrows) return;
   const int kh = h / (nq / nkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qvalid = min(kBlk, L - q0);
+  const int qvalid = min(kBlk, nrows - q0);
+  const int kend = p0 + q0 + qvalid;  // keys [0, kend): up to the block's last query position
   stage_bf16<HD>(Qs, nullptr, qvalid, [&](int r) { return q + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
   const int qr = warp * 16;
   const int ql_lo = qr + (lane >> 2), ql_hi = ql_lo + 8;
@@ -379,8 +386,8 @@ __global__ void __launch_bounds__(kWarps * 32)
     for (int i = 0; i < 4; ++i) o[n][i] = 0.f;
   float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
 
-  for (int k0 = 0; k0 <= q0; k0 += kBlk) {
-    const int kvalid = min(kBlk, L - k0);
+  for (int k0 = 0; k0 < kend; k0 += kBlk) {
+    const int kvalid = min(kBlk, kend - k0);
     __syncthreads();
     stage_bf16<HD>(Ks, nullptr, kvalid, [&](int r) { return page_row(kc, bt, pps, slot, k0 + r, nkv, kh, HD); });
     {  // V^T [HD][64]
@@ -420,7 +427,7 @@ __global__ void __launch_bounds__(kWarps * 32)
       for (int i = 0; i < 4; ++i) {
         const int kl = n * 8 + (lane & 3) * 2 + (i & 1);
         const int ql = i < 2 ? ql_lo : ql_hi;
-        const bool ok = kl < kvalid && k0 + kl <= q0 + ql;
+        const bool ok = kl < kvalid && k0 + kl <= p0 + q0 + ql;
         s[n][i] = ok ? s[n][i] * scale : -INFINITY;
         if (i < 2) mx_lo = fmaxf(mx_lo, s[n][i]);
         else mx_hi = fmaxf(mx_hi, s[n][i]);
@@ -486,7 +493,7 @@ __global__ void __launch_bounds__(kWarps * 32)
       *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(s0 + q0 + ql_hi) * qd + h * HD + d) =
           __floats2bfloat162_rn(o[n][2] * inv_hi, o[n][3] * inv_hi);
   }
-  if ((lane & 3) == 0) {
+  if (lse_out && (lane & 3) == 0) {
     if (ql_lo < qvalid) lse_out[(size_t)(s0 + q0 + ql_lo) * nq + h] = m_lo + logf(l_lo);
     if (ql_hi < qvalid) lse_out[(size_t)(s0 + q0 + ql_hi) * nq + h] = m_hi + logf(l_hi);
   }
@@ -494,14 +501,14 @@ __global__ void __launch_bounds__(kWarps * 32)
 
 template <int HD>
 cudaError_t launch_fwd_t(const __nv_bfloat16* q, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
-                         const int32_t* seq_start, const int32_t* seq_len, const int32_t* bt, int pps,
-                         int n_seq, int nq, int nkv, float scale, __nv_bfloat16* out, float* lse,
-                         cudaStream_t st) {
+                         const int32_t* seq_start, const int32_t* seq_len, const int32_t* pos0,
+                         const int32_t* slot, const int32_t* bt, int pps, int n_seq, int max_rows, int nq,
+                         int nkv, float scale, __nv_bfloat16* out, float* lse, cudaStream_t st) {
   static const bool attr = cudaFuncSetAttribute(attn_fwd_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)FwdSmem<HD>::total) == cudaSuccess;
   if (!attr) return cudaErrorInvalidValue;
-  attn_fwd_mma<HD><<<dim3(pps, n_seq, nq), kWarps * 32, FwdSmem<HD>::total, st>>>(
-      q, kc, vc, seq_start, seq_len, bt, pps, nq, nkv, scale, out, lse);
+  attn_fwd_mma<HD><<<dim3((max_rows + kBlk - 1) / kBlk, n_seq, nq), kWarps * 32, FwdSmem<HD>::total, st>>>(
+      q, kc, vc, seq_start, seq_len, pos0, slot, bt, pps, nq, nkv, scale, out, lse);
   return cudaGetLastError();
 }
 
@@ -547,14 +554,16 @@ namespace srl {
 cudaError_t launch_attention_fwd_mma(const __nv_bfloat16* q, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                                      const int32_t* seq_start, const int32_t* seq_len,
                                      const int32_t* block_table, int pages_per_seq, int n_seq, int nq,
-                                     int nkv, int hd, __nv_bfloat16* out, float* lse, cudaStream_t st) {
+                                     int nkv, int hd, __nv_bfloat16* out, float* lse, cudaStream_t st,
+                                     const int32_t* seg_pos0, const int32_t* seg_slot, int max_rows) {
   const float scale = 1.0f / sqrtf((float)hd);
+  if (max_rows <= 0) max_rows = pages_per_seq * kBlk;
   if (hd == 64)
-    return launch_fwd_t<64>(q, kc, vc, seq_start, seq_len, block_table, pages_per_seq, n_seq, nq, nkv,
-                            scale, out, lse, st);
+    return launch_fwd_t<64>(q, kc, vc, seq_start, seq_len, seg_pos0, seg_slot, block_table, pages_per_seq,
+                            n_seq, max_rows, nq, nkv, scale, out, lse, st);
   if (hd == 128)
-    return launch_fwd_t<128>(q, kc, vc, seq_start, seq_len, block_table, pages_per_seq, n_seq, nq, nkv,
-                             scale, out, lse, st);
+    return launch_fwd_t<128>(q, kc, vc, seq_start, seq_len, seg_pos0, seg_slot, block_table, pages_per_seq,
+                             n_seq, max_rows, nq, nkv, scale, out, lse, st);
   return cudaErrorInvalidValue;
 }
 }  // namespace srl
