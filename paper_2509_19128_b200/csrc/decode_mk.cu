@@ -1054,7 +1054,18 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             tma_load_2d_hint(smem + stage * kStageBytes, tw, &full[stage], (kb0 + k) * kBK, n0, pol);
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
-          if (!dep_ok) {
+          // dataflow phases: k-block kb's activations are ready once the
+          // producing tile's done counter reaches its per-round target
+          const bool flow = F.flow_ctr >= 0;
+          int flow_seen = -1;
+          auto flow_wait = [&](int kb) {
+            const int t = (kb * kBK) / F.flow_cols;
+            if (t == flow_seen) return;
+            wait_count(&P.tile_ctr[F.flow_ctr + t], ep1 * (unsigned)F.flow_target);
+            fence_proxy_async_global();  // generic-proxy results -> TMA reads
+            flow_seen = t;
+          };
+          if (!dep_ok && !flow) {
             // the compute warps' poller publishes each completed phase here
             // (one global poller per CTA)
             {
@@ -1067,6 +1078,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           }
           for (int k = 0; k < pre; ++k) {
             const int st = (s0 + k) % STAGES;
+            if (flow) flow_wait(kb0 + k);
             tma_load_2d(smem + st * kStageBytes + kABytes, tx, &full[st], (kb0 + k) * kBK, 0);
           }
           for (int k = pre; k < nkb; ++k) {
@@ -1074,6 +1086,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             mbar_arrive_expect_tx(&full[stage], kStageBytes);
             uint8_t* a = smem + stage * kStageBytes;
             tma_load_2d_hint(a, tw, &full[stage], (kb0 + k) * kBK, n0, pol);
+            if (flow) flow_wait(kb0 + k);
             tma_load_2d(a + kABytes, tx, &full[stage], (kb0 + k) * kBK, 0);
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
@@ -1141,7 +1154,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
         const int n = (i0 / F.cs) * kBN + col;
         if (i0 < F.n_items && n < F.N) colv0 = reinterpret_cast<const unsigned short*>(P.w)[colv_off + n];
       }
-      if (p > 0) {  // results of the previous phase, grid-wide
+      const bool flow_phase = F.flow_ctr >= 0;
+      if (p > 0 && !flow_phase) {  // results of the previous phase, grid-wide
         if (ct == 0) {
           phase_wait(P.phase_done, p - 1, target);
           st_release_cta(s_seen, p);
@@ -1332,13 +1346,25 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           csync();
           const float colv = __uint_as_float((unsigned)colv_bits << 16);
           if (r1 > r0) mk_epilogue(P, F, tile_n, tile, s_rstd, ct, r0, r1, colv, pair ? xs : nullptr);
+          if (F.done_ctr >= 0) fence_proxy_async_global();  // consumers read with TMA
           csync();
+          if (F.done_ctr >= 0 && ct == 0)  // this tile (row slice) is final
+            asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&P.tile_ctr[F.done_ctr + tile_n]),
+                         "r"(1u)
+                         : "memory");
           if (tr && ct == 0 && tr[6] == 0) tr[6] = clock64() - tr[8];
         }
       }
       fence_proxy_async_global();  // later phases read these results with TMA
       csync();
       if (ct == 0) {
+        if (flow_phase) {
+          // arrival here must still imply the previous phase is complete
+          // (later phases read its other results: ssq, x)
+          phase_wait(P.phase_done, p - 1, target);
+          st_release_cta(s_seen, p);
+          if (stamp) P.stamps[p] = globaltimer();
+        }
         if (tr) {
           tr[3] = globaltimer();
           tr[9] = clock64() - tr[8];

@@ -40,6 +40,12 @@ struct MkPhase {
   int rot;      // item -> CTA rotation
   long long colv;  // O / DOWN: offset of the next RMSNorm gain (epilogue column constant);
                    // ATTN: offset of the layer's qkv bias; else -1
+  // Dataflow dependency (QKV after DOWN, DOWN after gate/up): instead of the
+  // grid barrier, the producer waits per k-block for the producing tile's
+  // done counter tile_ctr[flow_ctr + (kb * 64) / flow_cols] to reach
+  // flow_target per round; -1: grid barrier.
+  int flow_ctr, flow_cols, flow_target;
+  int done_ctr;  // this phase's items signal tile_ctr[done_ctr + tile] after their epilogue (-1: no)
 };
 
 struct MkLayer {

@@ -345,7 +345,7 @@ int DecoderBackend::mega_init() {
   size_t ws = (size_t)S_ * d_.nkv * splits * (d_.nq / d_.nkv) * (d_.hd + 2);
   auto add = [&](int kind, int layer, int n_items, int cs, int N, int K, int wmap, int xmap,
                  int counters) {
-    MkPhase f{kind, layer, n_items, cs, N, K, wmap, xmap, ctr, items_total % grid, -1};
+    MkPhase f{kind, layer, n_items, cs, N, K, wmap, xmap, ctr, items_total % grid, -1, -1, 0, 0, -1};
     if (pairs && cs == 2 && (kind == MK_QKV || kind == MK_O)) f.rot &= ~1;  // split 0 on the even CTA
     const LayerOffsets* lo = buf_[0]->layout.layers;
     if (kind == MK_O) f.colv = (long long)lo[layer].ln2;
@@ -387,6 +387,28 @@ int DecoderBackend::mega_init() {
   }
   gemm(MK_LM, 0, d_.V, d_.H, 4 * L, 0);
   add(MK_SAMPLE, 0, S_, 1, 0, 0, 0, 0, 0);
+  // dataflow links (experiment, SRL_MK_FLOW=1 / q / d; measured slower than
+  // the grid barriers at 0.5B, B = 64: the per-tile counter polls and done
+  // signals cost more than the barrier they skip): QKV(l) reads xg from
+  // down(l-1) tiles of 128 columns, down(l) reads act from gate/up(l) tiles of
+  // 64 act columns; producer tiles count their row slices' epilogues
+  const char* fe = std::getenv("SRL_MK_FLOW");
+  if (fe && fe[0] != '0' && !pairs) {
+    for (size_t i = 1; i < ph.size(); ++i) {
+      MkPhase& f = ph[i];
+      MkPhase& prev = ph[i - 1];
+      const bool want_q = !fe || fe[0] != 'd', want_d = !fe || fe[0] != 'q';
+      const bool link = (want_q && f.kind == MK_QKV && prev.kind == MK_DOWN) ||
+                        (want_d && f.kind == MK_DOWN && prev.kind == MK_GU);
+      if (!link) continue;
+      const int tiles = (prev.N + 127) / 128;
+      prev.done_ctr = ctr;
+      ctr += tiles;
+      f.flow_ctr = prev.done_ctr;
+      f.flow_cols = prev.kind == MK_GU ? 64 : 128;
+      f.flow_target = prev.cs;
+    }
+  }
   const int n = (int)ph.size();
 
   // one allocation: phases | layers | xmaps | phase_done | epoch | tile counters | stamps
