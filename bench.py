@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=4)
     ap.add_argument("--no-trainer", action="store_true", help="skip the trainer-step measurement")
+    ap.add_argument("--no-pipeline", action="store_true", help="skip the one-GPU PipelineRL loop")
     ap.add_argument("--train-seqs", type=int, default=64, help="trajectories per trainer step")
     return ap.parse_args()
 
@@ -245,6 +246,33 @@ def trainer_measure(cfg, pol, n_seq, prompt, gen, steps=3):
            "frac": tf / bf16 if bf16 else None, "objective": r.objective, "ess": r.ess}
     tr.close()
     return out
+
+
+def pipeline_measure(cfg, args, steps=6):
+    """The whole PipelineRL loop time-shared on ONE GPU (paper_2509_19128_b200/
+    pipeline.py): constant-batch generator -> actor queue -> IS-REINFORCE
+    trainer step on every train_batch finished sequences -> in-flight update.
+    Config 2 puts generator and trainer on two GPUs; here they alternate, so
+    tokens_per_s_wall is a lower bound for that configuration."""
+    from paper_2509_19128_b200.pipeline import PipelineRL
+    from paper_2509_19128_b200.policy import DecoderPolicy
+
+    pol = DecoderPolicy.random(cfg, seed=1, scale=0.02)
+    pl = PipelineRL(pol, batch=args.batch, prompt_len=args.prompt, max_tokens=args.gen,
+                    train_batch=args.batch, queue_capacity=4 * args.batch, rounds_per_poll=args.rounds,
+                    n_prompts=8, lr=1e-5, seed=0)
+    pl.run(optimizer_steps=1)  # warm-up
+    rep = pl.run(optimizer_steps=steps)
+    pl.close()
+    return {"workload": f"{cfg.name}, batch {args.batch}, train batch {args.batch} sequences of "
+                        f"{args.prompt} + {args.gen} tokens, {steps} optimizer steps",
+            "tokens_per_s_wall": rep.generated_tokens / rep.wall_s,
+            "tokens_per_s_generating": rep.generated_tokens / rep.generate_s,
+            "trainer_ms_per_step": 1e3 * rep.train_s / max(1, len(rep.steps)),
+            "max_lag_steps": max(st.max_lag_steps for st in rep.steps),
+            "mean_lag_steps": float(np.mean([st.mean_lag_steps for st in rep.steps])),
+            "pause_ms_max": max(st.pause_ms for st in rep.steps),
+            "stalls": rep.stalls, "evicted": rep.evicted}
 
 
 def reference_arm(args, cfg):
@@ -505,6 +533,8 @@ def main():
         tclk.start()
         out["trainer"] = trainer_measure(cfg, pol, args.train_seqs, args.prompt, args.gen)
         out["trainer"]["clocks"] = tclk.stop()
+    if rank == 0 and world == 1 and not args.no_pipeline:
+        out["pipeline_1gpu"] = pipeline_measure(cfg, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tps, dt, cores = cpu_decode_sample(cfg, B, 8, args.cpu_steps, 1)
         out["cpu_baseline"] = {"value": tps, "unit": UNIT, "cores": cores, "kind": "port",
