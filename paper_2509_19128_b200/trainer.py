@@ -66,6 +66,17 @@ class Trainer:
         return TrainStep(stats.objective, stats.ess, stats.clamped, stats.tokens, stats.forward_ms,
                          stats.step_ms, lps)
 
+    def step_data_parallel(self, trajectories, rank: int, world: int, group=None, **kw) -> TrainStep:
+        """One data-parallel trainer step: this rank's shard of the consumed
+        batch (weight_sync.shard), the objective normalised by the GLOBAL
+        trajectory count, then the gradient all-reduce over the trainer group
+        (weight_sync.GradientSync).  Every rank then applies the same Adam step."""
+        from .weight_sync import GradientSync, shard
+
+        res = self.step(shard(trajectories, rank, world), n_trajectories=len(trajectories), **kw)
+        GradientSync(group).allreduce_(self.gradient())
+        return res
+
     def gradient(self):
         """Zero-copy torch view (fp32, flat weight layout) of the last gradient."""
         import torch

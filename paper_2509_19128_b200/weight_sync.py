@@ -107,6 +107,31 @@ class EngineStandby:
         return res.applied, pause
 
 
+def shard(items, rank: int, world: int):
+    """The trainer data-parallel split of a consumed batch: trajectory i goes to
+    rank i % world (every rank keeps the GLOBAL trajectory count m for the 1/m
+    of the objective, rl_math.cpp:219)."""
+    return list(items)[rank::world]
+
+
+class GradientSync:
+    """Trainer data-parallel gradient all-reduce (SURVEY 8e exchange 2): one
+    in-place SUM over the trainer group per optimizer step, on the fp32
+    gradient buffer (NCCL over NVLink on the box, gloo in the CPU tests).
+    With each shard normalised by the global m, the sum is the full-batch
+    gradient."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def allreduce_(self, grad):
+        import torch.distributed as dist
+
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=self.group)
+        return grad
+
+
 def max_over_ranks(value: float, group=None) -> float:
     """Max of a per-rank timing (the contract's multi-GPU timing rule)."""
     import torch

@@ -113,3 +113,21 @@ def test_trainer_adam_moves_weights_and_feeds_the_engine(cuda):
     evs, _ = eng.collect(sid)
     assert [e.weight_version for e in evs] == [0, 0, 1, 1]
     eng.close()
+
+
+def test_trainer_data_parallel_shards_sum_to_full_batch(cuda):
+    """Two shards (rank 0 / rank 1 of a world-2 trainer group, run one after
+    the other on this GPU), each normalised by the global m: their gradients
+    sum to the full-batch gradient (the all-reduce's input contract)."""
+    pol = DecoderPolicy.random(TINY, seed=14, scale=0.03)
+    rng = np.random.default_rng(9)
+    trajs = make_trajs(rng, TINY.vocab_size, 5, [14, 22, 9, 30, 17], [2, 4, 1, 6, 3])
+    tr = Trainer(pol, max_tokens=256)
+    tr.step(trajs)
+    full = tr.gradient().cpu().numpy().astype(np.float64).copy()
+    parts = []
+    for r in range(2):
+        tr.step_data_parallel(trajs, r, 2)  # no process group: the all-reduce is the identity
+        parts.append(tr.gradient().cpu().numpy().astype(np.float64).copy())
+    rel = np.linalg.norm(parts[0] + parts[1] - full) / np.linalg.norm(full)
+    assert rel < 1e-5, rel

@@ -113,3 +113,54 @@ def test_stale_version_is_rejected_without_side_effects():
     assert eng.stage(2) is None  # version_conflict: not staged
     ok, _ = eng.commit(2)
     assert not ok and torch.equal(eng.active, before) and eng.version == 0
+
+
+def _dp_worker(rank, world, port, q):
+    """Each rank: the reference-semantics tabular IS-REINFORCE gradient of its
+    shard (global baseline, shard normalised by the global m), then the
+    trainer's gradient all-reduce; the result must equal the full-batch
+    gradient (rl_math.cpp:211-276)."""
+    import numpy as np
+
+    from oracle.oracle import Oracle
+    from paper_2509_19128_b200.weight_sync import GradientSync, shard
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc = Oracle()
+        rng = np.random.default_rng(3)
+        V = 5
+        doc = {"schema": "streamrl.policy/1", "type": "tabular", "vocab_size": V, "context_order": 1,
+               "rows": [{"prompt_id": "p", "context": [], "logits": [0.1, -0.2, 0.3, 0.0, 0.5]},
+                        {"prompt_id": "p", "context": [1], "logits": [0.0, 0.4, -0.1, 0.2, 0.1]}]}
+        trajs = []
+        for i in range(7):
+            toks = rng.integers(0, V, size=int(rng.integers(2, 6))).tolist()
+            trajs.append(dict(prompt_id="p", tokens=toks,
+                              behavior_logprobs=(-np.log(V) + 0.3 * rng.standard_normal(len(toks))).tolist(),
+                              reward=float(rng.standard_normal())))
+        full, _, base = orc.reinforce_gradient_tab(doc, trajs)
+        mine = shard(trajs, rank, world)
+        g, _, _ = orc.reinforce_gradient_tab(doc, mine, baseline=base)
+        g = torch.tensor(g * (len(mine) / len(trajs)))
+        GradientSync().allreduce_(g)
+        q.put((rank, float(np.abs(g.numpy() - full).max()), float(np.abs(full).max())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_trainer_data_parallel_gradient_allreduce_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_dp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, err, scale in res:
+        assert scale > 0 and err <= 1e-12 * scale, (rank, err, scale)
