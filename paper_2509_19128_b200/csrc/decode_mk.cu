@@ -649,7 +649,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
         uint32_t b0, b1;
         ldsm_x2_trans(b0, b1, vb, A::VROW, ks * 16, n * 8, lane);
         mma16816(o[n], ah, b0, b1);
-        mma16816(o[n], al, b0, b1);
+        if (!(P.dbg & 1)) mma16816(o[n], al, b0, b1);  // SRL_MK_DBG=1: single bf16 P (A/B)
       }
     }
     __syncwarp();

@@ -129,13 +129,17 @@ int DecoderRunner::init(const DecoderDims& dims, const WeightLayout& layout, int
   int counters = 1;
   const int shapes[5][2] = {{d.qkv(), H}, {H, d.qdim()}, {2 * d.I, H}, {H, d.I}, {d.V, H}};
   const int m_hi = std::max(M_max, this->logits_rows);
-  for (int M = 1; M <= m_hi; M = (M < 64) ? 64 : M + 64) {
-    const int tok = gemm_tok_tile(M);
+  // every row count the engine may launch: 1, 64, 128, ... and m_hi itself
+  // (a row count between two multiples of 64 can need the larger token tile)
+  for (int M = 1;; M = (M < 64) ? 64 : M + 64) {
+    const int Mc = std::min(M, m_hi);
+    const int tok = gemm_tok_tile(Mc);
     for (auto& sh : shapes) {
-      const int sp = gemm_auto_splits(M, sh[0], sh[1], sms);
-      need = std::max(need, sp > 1 ? gemm_workspace_floats(M, sh[0], sp) : 0);
-      counters = std::max(counters, ((sh[0] + 127) / 128) * ((M + tok - 1) / tok));
+      const int sp = gemm_auto_splits(Mc, sh[0], sh[1], sms);
+      need = std::max(need, sp > 1 ? gemm_workspace_floats(Mc, sh[0], sp) : 0);
+      counters = std::max(counters, ((sh[0] + 127) / 128) * ((Mc + tok - 1) / tok));
     }
+    if (M >= m_hi) break;
   }
   gws.partial_floats = need;
   gws.counter_count = counters;

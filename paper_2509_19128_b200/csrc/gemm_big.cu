@@ -49,6 +49,23 @@ struct BigLayout {
   static_assert(kAlloc <= 232448, "shared memory budget");
 };
 
+// 32 values per lane -> lane l holds the reduction over the warp's lanes of
+// value l (recursive halving: 16 + 8 + 4 + 2 + 1 shuffles).  Sum or max.
+template <bool kSum>
+__device__ __forceinline__ void butterfly_reduce(float (&v)[32], int lane) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool upper = (lane & w) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = upper ? v[i] : v[i + w];
+      const float keep = upper ? v[i + w] : v[i];
+      const float got = __shfl_xor_sync(0xffffffffu, send, w);
+      v[i] = kSum ? keep + got : fmaxf(keep, got);
+    }
+  }
+}
+
 __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
 }
@@ -155,8 +172,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* s_rstd = reinterpret_cast<float*>(smem + L::kRstd) + g * kChunk;
     int4* s_row = reinterpret_cast<int4*>(smem + L::kRow) + g * kChunk;
     auto sync = [g] { group_sync(g); };
+    // statistics-only LM head (the trainer's pass 1: no logits stored)
+    const bool stats_only = epi.kind == EPI_LOGITS && epi.out_f32 == nullptr;
     const bool direct = epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16 ||
-                        epi.kind == EPI_ACCUM_F32 || epi.kind == EPI_DLOGITS;
+                        epi.kind == EPI_ACCUM_F32 || epi.kind == EPI_DLOGITS || stats_only;
+    float* red = tile;  // stats_only: [4 warps][32 tokens] cross-warp partials (the unused staging tile)
     bool waited = false;
     int acc = 0;
     uint32_t aph = 0;
@@ -192,6 +212,51 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const float bias = (epi.bias != nullptr && n < N) ? gemm_detail::epi_bf2f(epi.bias[n]) : 0.f;
           const int jn = min(32, M - tc0);
+          if (stats_only) {
+            // per token: the target's logit, and over this tile's 128 columns
+            // the max and the sum of exp(x - max) (fp32 exp, fp64 combine).
+            // Each warp reduces its 32 columns for all 32 tokens at once with a
+            // butterfly transpose (31 shuffles, lane l ends with token l), the
+            // group's four warps combine through shared memory.
+            int tg = -1;
+            if (epi.tgt_row && tc0 + lane < M) tg = epi.tgt_row[tc0 + lane];
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float rj = __shfl_sync(0xffffffffu, rs, j);
+              const int tj = __shfl_sync(0xffffffffu, tg, j);
+              v[j] = n < N && j < jn ? __uint_as_float(r[j]) * rj : -INFINITY;
+              if (n == tj && j < jn) epi.tgt_out[tc0 + j] = v[j];
+            }
+            float mx[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) mx[j] = v[j];
+            butterfly_reduce<false>(mx, lane);  // lane l: max of token l over this warp's columns
+            const int q = tid >> 5;
+            red[q * 32 + lane] = mx[0];
+            sync();
+            float M_l = red[lane];
+#pragma unroll
+            for (int w = 1; w < 4; ++w) M_l = fmaxf(M_l, red[w * 32 + lane]);
+            float e[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float Mj = __shfl_sync(0xffffffffu, M_l, j);
+              e[j] = v[j] == -INFINITY ? 0.f : __expf(v[j] - Mj);
+            }
+            butterfly_reduce<true>(e, lane);  // lane l: this warp's sum for token l
+            sync();  // everyone has read the maxima
+            red[q * 32 + lane] = e[0];
+            sync();
+            if (q == 0 && lane < jn) {
+              const double sum = (double)red[lane] + (double)red[32 + lane] + (double)red[64 + lane] +
+                                 (double)red[96 + lane];
+              epi.part_max[(size_t)(tc0 + lane) * n_tiles + n_tile] = M_l;
+              epi.part_sum[(size_t)(tc0 + lane) * n_tiles + n_tile] = M_l == -INFINITY ? 0.0 : sum;
+            }
+            sync();  // red is reused by the next chunk
+            continue;
+          }
           if (epi.kind == EPI_DLOGITS) {
             // d = coef * (onehot - softmax) of token tc0 + j at vocab column n; the
             // transposed copy [n][tokens] is 32 contiguous bf16 per thread

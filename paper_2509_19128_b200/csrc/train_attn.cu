@@ -1,3 +1,4 @@
+#include <cstdlib>
 // train_attn.cu -- causal GQA attention backward of the trainer on the tensor
 // cores (mma.sync m16n8k16 bf16 -> fp32), tiled FlashAttention-2 style.
 //
@@ -38,6 +39,13 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&v);
+}
+// (x, y) -> bf16x2 hi = RN(x, y) and lo = RN(x - hi, y - hi)
+__device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+  const float2 hf = __bfloat1622float2(h);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = pack_bf16(x - hf.x, y - hf.y);
 }
 __device__ __forceinline__ uint32_t ld32(const __nv_bfloat16* p) {
   return *reinterpret_cast<const uint32_t*>(p);
@@ -360,7 +368,8 @@ __global__ void __launch_bounds__(kWarps * 32)
                  const __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ seq_start,
                  const int32_t* __restrict__ seq_len, const int32_t* __restrict__ seg_pos0,
                  const int32_t* __restrict__ seg_slot, const int32_t* __restrict__ bt, int pps, int nq,
-                 int nkv, float scale, __nv_bfloat16* __restrict__ out, float* __restrict__ lse_out) {
+                 int nkv, float scale, __nv_bfloat16* __restrict__ out, float* __restrict__ lse_out,
+                 int split_p) {
   using S = FwdSmem<HD>;
   constexpr int P = S::P, NT = HD / 8;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -461,18 +470,20 @@ __global__ void __launch_bounds__(kWarps * 32)
       o[n][0] *= c_lo; o[n][1] *= c_lo;
       o[n][2] *= c_hi; o[n][3] *= c_hi;
     }
+    // P enters as bf16 (optionally + its lo residual, split_p)
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
-      uint32_t a[4];
-      a[0] = pack_bf16(s[2 * ks][0], s[2 * ks][1]);
-      a[1] = pack_bf16(s[2 * ks][2], s[2 * ks][3]);
-      a[2] = pack_bf16(s[2 * ks + 1][0], s[2 * ks + 1][1]);
-      a[3] = pack_bf16(s[2 * ks + 1][2], s[2 * ks + 1][3]);
+      uint32_t ah[4], al[4];
+      split2(s[2 * ks][0], s[2 * ks][1], ah[0], al[0]);
+      split2(s[2 * ks][2], s[2 * ks][3], ah[1], al[1]);
+      split2(s[2 * ks + 1][0], s[2 * ks + 1][1], ah[2], al[2]);
+      split2(s[2 * ks + 1][2], s[2 * ks + 1][3], ah[3], al[3]);
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         uint32_t b0, b1;
         frag_b(b0, b1, Vt, kPadT, n * 8, ks * 16, lane);
-        mma16816(o[n], a, b0, b1);
+        mma16816(o[n], ah, b0, b1);
+        if (split_p) mma16816(o[n], al, b0, b1);
       }
     }
   }
@@ -506,9 +517,16 @@ cudaError_t launch_fwd_t(const __nv_bfloat16* q, const __nv_bfloat16* kc, const 
                          int nkv, float scale, __nv_bfloat16* out, float* lse, cudaStream_t st) {
   static const bool attr = cudaFuncSetAttribute(attn_fwd_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)FwdSmem<HD>::total) == cudaSuccess;
+  // P as hi + lo bf16 halves (default; vs the fp64 oracle at 0.5B the
+  // log-prob error drops from 1.65e-2 to 1.04e-2 max, as with the CUDA-core
+  // kernel); SRL_ATTN_SPLIT=0: a single bf16 P (A/B)
+  static const int split = [] {
+    const char* e = std::getenv("SRL_ATTN_SPLIT");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
   if (!attr) return cudaErrorInvalidValue;
   attn_fwd_mma<HD><<<dim3((max_rows + kBlk - 1) / kBlk, n_seq, nq), kWarps * 32, FwdSmem<HD>::total, st>>>(
-      q, kc, vc, seq_start, seq_len, pos0, slot, bt, pps, nq, nkv, scale, out, lse);
+      q, kc, vc, seq_start, seq_len, pos0, slot, bt, pps, nq, nkv, scale, out, lse, split);
   return cudaGetLastError();
 }
 

@@ -76,7 +76,7 @@ namespace {
 // rows per LM-head pass: the logits chunk is [chunk x V] fp32.  Large chunks
 // keep the LM-head GEMMs efficient and, above all, accumulate the [V x H] fp32
 // LM-head gradient (a read-modify-write of 0.5 GB at V = 152k) few times.
-constexpr int kLogitChunkMax = 4096;
+constexpr int kLogitChunkMax = 16384;
 int pad64(int x) { return (x + 63) / 64 * 64; }
 }  // namespace
 

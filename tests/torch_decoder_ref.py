@@ -42,7 +42,7 @@ class TorchDecoder:
         for name, t in self.p.items():
             o, n = self.off[name]
             if t.grad is not None:
-                g[o:o + n] += t.grad.detach().numpy().ravel()
+                g[o:o + n] += t.grad.detach().cpu().numpy().ravel()
         return g
 
     def logprobs(self, tokens):
@@ -101,7 +101,7 @@ class TorchDecoder:
         lps = []
         for t in trajs:
             lp = self.logprobs(t["tokens"])
-            lps.append(lp.detach().numpy())
+            lps.append(lp.detach().cpu().numpy())
             lb = t["loss_begin"] - 1
             mu = torch.tensor(t["behavior_logprobs"][1:], dtype=torch.float64)
             adv = torch.tensor(t["advantages"][1:], dtype=torch.float64)
