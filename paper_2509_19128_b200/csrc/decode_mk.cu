@@ -1322,7 +1322,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
               }
               __syncwarp();
               if (nr > 0 && lane < F.cs) {  // one bulk copy per lane, issued in parallel
-                fence_proxy_async_global();
+                // (each writer fenced its partial generic -> async proxy before arriving)
                 const float* src = P.ws + (size_t)tile_n * F.cs * kTileFloats + (size_t)r0 * kBN;
                 bulk_g2s(stage + (size_t)lane * nr * kBN, src + (size_t)lane * kTileFloats, nr * kBN * 4, cbar);
               }

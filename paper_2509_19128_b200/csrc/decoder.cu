@@ -152,6 +152,22 @@ __global__ void rope_append_kernel(const float* __restrict__ qkv, int nq, int nk
 constexpr int kAttnWarps = 4;
 constexpr int kAttnChunk = 32 * kAttnWarps;  // keys per split
 
+__device__ __forceinline__ void att_mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t att_ld32(const void* p) { return *reinterpret_cast<const uint32_t*>(p); }
+__device__ __forceinline__ void att_split(float x, float y, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+  const float2 hf = __bfloat1622float2(h);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(x - hf.x, y - hf.y);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
 template <int G, int HD>
 __global__ void __launch_bounds__(32 * kAttnWarps)
     attention_kernel(const __nv_bfloat16* __restrict__ q, int nq, int nkv,
@@ -160,21 +176,23 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
                      const __nv_bfloat16* __restrict__ kc, const __nv_bfloat16* __restrict__ vc,
                      float scale, float* __restrict__ ws, int* __restrict__ counters,
                      __nv_bfloat16* __restrict__ out, float* __restrict__ lse_out) {
-  constexpr int DPL = HD / 32;           // dims per lane in the PV phase
-  constexpr int ROW = HD * 2 + 16;       // padded K row in smem (bytes): conflict-free LDS.128
-  constexpr int VROW = HD * 2;           // V rows are read row-wise: no padding needed
+  // S = Q K^T and O = P V on the tensor cores (mma.sync m16n8k16): the G
+  // query heads of the KV head are the A rows (padded to 16), each warp one
+  // 32-key tile; P enters as hi + lo bf16 halves (fp32-class accuracy)
+  constexpr int ROW = HD * 2 + 16;       // padded K / V rows in smem (bytes): conflict-free
   constexpr int V4 = HD / 8;             // uint4 per K/V row
+  constexpr int QP = HD + 8;             // bf16 q tile pitch (elements)
+  constexpr int NDT = HD / 8;
   extern __shared__ __align__(16) uint8_t att_smem[];
-  using SqT = float[G][HD];
+  using SqT = __nv_bfloat16[16][QP];
   using SkT = uint8_t[kAttnWarps][32 * ROW];
-  using SvT = uint8_t[kAttnWarps][32 * VROW];
+  using SvT = uint8_t[kAttnWarps][32 * ROW];
   using SpT = float[kAttnWarps][G][32];
   using SmT = float[kAttnWarps][G];
   using SaT = float[kAttnWarps][G][HD];
   SqT& sq = *reinterpret_cast<SqT*>(att_smem);
   SkT& sk = *reinterpret_cast<SkT*>(att_smem + sizeof(SqT));
   SvT& sv = *reinterpret_cast<SvT*>(att_smem + sizeof(SqT) + sizeof(SkT));
-  SpT& sp = *reinterpret_cast<SpT*>(att_smem + sizeof(SqT) + sizeof(SkT) + sizeof(SvT));
   SmT& sm_m = *reinterpret_cast<SmT*>(att_smem + sizeof(SqT) + sizeof(SkT) + sizeof(SvT) + sizeof(SpT));
   SmT& sm_l = *reinterpret_cast<SmT*>(att_smem + sizeof(SqT) + sizeof(SkT) + sizeof(SvT) + sizeof(SpT) + sizeof(SmT));
   SaT& sm_acc = *reinterpret_cast<SaT*>(att_smem + sizeof(SqT));  // aliases sk after the tiles
@@ -189,18 +207,15 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
   const int k_begin = split * kAttnChunk;
   if (k_begin >= ctx && splits == 1) return;
 
-  for (int i = threadIdx.x; i < G * HD; i += blockDim.x)
-    sq[i / HD][i % HD] = __bfloat162float(q[(size_t)m * nq * HD + (kh * G) * HD + i]) * scale;
-  __syncthreads();
+  for (int i = threadIdx.x; i < 16 * HD; i += blockDim.x)
+    sq[i / HD][i % HD] = i < G * HD ? q[(size_t)m * nq * HD + (kh * G) * HD + i] : __float2bfloat16(0.f);
 
-  float mrun[G], lrun[G], acc[G][DPL];
+  float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;  // heads lane/4, lane/4 + 8
+  float o[NDT][4];
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    mrun[g] = -INFINITY;
-    lrun[g] = 0.f;
+  for (int n = 0; n < NDT; ++n)
 #pragma unroll
-    for (int d = 0; d < DPL; ++d) acc[g][d] = 0.f;
-  }
+    for (int i = 0; i < 4; ++i) o[n][i] = 0.f;
 
   const int t0 = k_begin + warp * 32;
   const int nvalid = max(0, min(32, ctx - t0));
@@ -214,89 +229,103 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
 #pragma unroll
     for (int i = 0; i < V4; ++i) {  // 32 rows x V4 uint4, lane-strided: coalesced
       const int e = lane + 32 * i, r = e / V4;
+      kr[i] = make_uint4(0u, 0u, 0u, 0u);
+      vr[i] = make_uint4(0u, 0u, 0u, 0u);  // rows past the context stay 0 (0 x NaN is NaN)
       if (r < nvalid) { kr[i] = __ldg(kg + e); vr[i] = __ldg(vg + e); }
     }
 #pragma unroll
     for (int i = 0; i < V4; ++i) {
       const int e = lane + 32 * i, r = e / V4, c = e % V4;
-      if (r < nvalid) {
-        *reinterpret_cast<uint4*>(&sk[warp][r * ROW + c * 16]) = kr[i];
-        *reinterpret_cast<uint4*>(&sv[warp][r * VROW + c * 16]) = vr[i];
+      *reinterpret_cast<uint4*>(&sk[warp][r * ROW + c * 16]) = kr[i];
+      *reinterpret_cast<uint4*>(&sv[warp][r * ROW + c * 16]) = vr[i];
+    }
+  }
+  __syncthreads();  // q tile and the warps' K/V tiles
+  if (nvalid > 0) {
+    float sc[4][4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sc[n][i] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      uint32_t a[4];
+      const __nv_bfloat16* qa = &sq[lane >> 2][kk * 16 + (lane & 3) * 2];
+      a[0] = att_ld32(qa);
+      a[1] = att_ld32(qa + 8 * QP);
+      a[2] = att_ld32(qa + 8);
+      a[3] = att_ld32(qa + 8 * QP + 8);
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        const uint8_t* kp = &sk[warp][(n * 8 + (lane >> 2)) * ROW + (kk * 16 + (lane & 3) * 2) * 2];
+        att_mma16816(sc[n], a, att_ld32(kp), att_ld32(kp + 16));
       }
     }
-    __syncwarp();
-    // scores: lane = key
-    float s[G];
+    float mx_lo = -INFINITY, mx_hi = -INFINITY;
 #pragma unroll
-    for (int g = 0; g < G; ++g) s[g] = 0.f;
-    if (lane < nvalid) {
+    for (int n = 0; n < 4; ++n)
 #pragma unroll
-      for (int c = 0; c < V4; ++c) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(&sk[warp][lane * ROW + c * 16]);
-        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-        float kf[8];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(p2[e]);
-          kf[2 * e] = f.x;
-          kf[2 * e + 1] = f.y;
-        }
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const float4 qa = *reinterpret_cast<const float4*>(&sq[g][c * 8]);
-          const float4 qb = *reinterpret_cast<const float4*>(&sq[g][c * 8 + 4]);
-          s[g] += qa.x * kf[0] + qa.y * kf[1] + qa.z * kf[2] + qa.w * kf[3] + qb.x * kf[4] +
-                  qb.y * kf[5] + qb.z * kf[6] + qb.w * kf[7];
-        }
-      }
-    }
-    // online softmax per head over this tile
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float sv_ = lane < nvalid ? s[g] : -INFINITY;
-      const float mx = warp_max(sv_);
-      const float p = lane < nvalid ? __expf(sv_ - mx) : 0.f;
-      mrun[g] = mx;
-      lrun[g] = warp_sum(p);
-      sp[warp][g][lane] = p;
-    }
-    __syncwarp();
-    // P.V: lane = dims
-    for (int j = 0; j < nvalid; ++j) {
-      float vf[DPL];
-      const uint8_t* vrow = &sv[warp][j * VROW + lane * DPL * 2];
-      if constexpr (DPL == 2) {
-        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vrow));
-        vf[0] = f.x;
-        vf[1] = f.y;
-      } else {
-        const uint2 raw = *reinterpret_cast<const uint2*>(vrow);
-        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-        const float2 a = __bfloat1622float2(p2[0]), b = __bfloat1622float2(p2[1]);
-        vf[0] = a.x; vf[1] = a.y; vf[2] = b.x; vf[3] = b.y;
+      for (int i = 0; i < 4; ++i) {
+        const int key = n * 8 + (lane & 3) * 2 + (i & 1);
+        sc[n][i] = key < nvalid ? sc[n][i] * scale : -INFINITY;
+        if (i < 2) mx_lo = fmaxf(mx_lo, sc[n][i]);
+        else mx_hi = fmaxf(mx_hi, sc[n][i]);
       }
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float pj = sp[warp][g][j];
+    for (int off = 1; off <= 2; off <<= 1) {
+      mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, off));
+      mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, off));
+    }
+    m_lo = mx_lo;
+    m_hi = mx_hi;
 #pragma unroll
-        for (int d = 0; d < DPL; ++d) acc[g][d] += pj * vf[d];
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float pv = sc[n][i] == -INFINITY ? 0.f : __expf(sc[n][i] - (i < 2 ? m_lo : m_hi));
+        sc[n][i] = pv;
+        if (i < 2) l_lo += pv;
+        else l_hi += pv;
+      }
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+      l_lo += __shfl_xor_sync(0xffffffffu, l_lo, off);
+      l_hi += __shfl_xor_sync(0xffffffffu, l_hi, off);
+    }
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      uint32_t ah[4], al[4];
+      att_split(sc[2 * ks][0], sc[2 * ks][1], ah[0], al[0]);
+      att_split(sc[2 * ks][2], sc[2 * ks][3], ah[1], al[1]);
+      att_split(sc[2 * ks + 1][0], sc[2 * ks + 1][1], ah[2], al[2]);
+      att_split(sc[2 * ks + 1][2], sc[2 * ks + 1][3], ah[3], al[3]);
+#pragma unroll
+      for (int n = 0; n < NDT; ++n) {
+        uint32_t b0, b1;
+        const uint8_t* vp = &sv[warp][(ks * 16 + (lane & 15)) * ROW + n * 16];
+        asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                     : "=r"(b0), "=r"(b1)
+                     : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(vp))));
+        att_mma16816(o[n], ah, b0, b1);
+        att_mma16816(o[n], al, b0, b1);
       }
     }
   }
-
   // combine the warps of this CTA (sm_acc aliases the K tiles: wait for all warps)
   __syncthreads();
-  if (lane == 0) {
+  {
+    const int h_lo = lane >> 2, h_hi = h_lo + 8;
+    if ((lane & 3) == 0) {
+      if (h_lo < G) { sm_m[warp][h_lo] = m_lo; sm_l[warp][h_lo] = l_lo; }
+      if (h_hi < G) { sm_m[warp][h_hi] = m_hi; sm_l[warp][h_hi] = l_hi; }
+    }
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      sm_m[warp][g] = mrun[g];
-      sm_l[warp][g] = lrun[g];
+    for (int n = 0; n < NDT; ++n) {
+      const int d = n * 8 + (lane & 3) * 2;
+      if (h_lo < G) { sm_acc[warp][h_lo][d] = o[n][0]; sm_acc[warp][h_lo][d + 1] = o[n][1]; }
+      if (h_hi < G) { sm_acc[warp][h_hi][d] = o[n][2]; sm_acc[warp][h_hi][d + 1] = o[n][3]; }
     }
   }
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-#pragma unroll
-    for (int d = 0; d < DPL; ++d) sm_acc[warp][g][lane * DPL + d] = acc[g][d];
   __syncthreads();
 
   constexpr size_t rec = (size_t)G * (HD + 2);
@@ -834,9 +863,9 @@ size_t attention_ws_floats(const DecoderDims& d, int M, int max_ctx) {
 
 template <int G, int HD>
 constexpr size_t attention_smem() {
-  return sizeof(float) * G * HD + (size_t)kAttnWarps * 32 * (HD * 2 + 16) +
-         (size_t)kAttnWarps * 32 * HD * 2 + sizeof(float) * kAttnWarps * G * 32 +
-         2 * sizeof(float) * kAttnWarps * G;
+  // bf16 q tile [16][HD + 8], K and V tiles (padded rows), (legacy P area), m, l
+  return sizeof(__nv_bfloat16) * 16 * (HD + 8) + 2 * (size_t)kAttnWarps * 32 * (HD * 2 + 16) +
+         sizeof(float) * kAttnWarps * G * 32 + 2 * sizeof(float) * kAttnWarps * G;
 }
 
 template <int G, int HD>

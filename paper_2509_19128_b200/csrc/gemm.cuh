@@ -63,6 +63,7 @@ struct EpiParams {
   const double* lse_in = nullptr;
   const float* row_coef = nullptr;
   __nv_bfloat16* outT_bf16 = nullptr;
+  __nv_bfloat16* out2_bf16 = nullptr;   // EPI_SWIGLU: also the rstd-scaled gate | up [M x N] (bf16)
   int ldT = 0;
   // debug: per-CTA %globaltimer phase stamps [ctas x 8] (null = off)
   unsigned long long* stamps = nullptr;

@@ -115,6 +115,10 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
       const float u = tile[j * pitch + 64 + c] * s_rstd[j];
       const float a = g / (1.f + expf(-g)) * u;
       epi.out_bf16[(size_t)m * epi.ld_bf16 + (n0 >> 1) + c] = __float2bfloat16(a);
+      if (epi.out2_bf16) {
+        epi.out2_bf16[(size_t)m * N + n0 + c] = __float2bfloat16(g);
+        epi.out2_bf16[(size_t)m * N + n0 + 64 + c] = __float2bfloat16(u);
+      }
     }
   } else if (epi.kind == EPI_QKV && (nthr & 127) == 0) {
     // thread = one column c for rows r0 + (tid >> 7) + k * (nthr / 128): the

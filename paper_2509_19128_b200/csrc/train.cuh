@@ -45,7 +45,7 @@ void launch_rmsnorm_bwd(const float* dzw, const float* x, const __nv_bfloat16* g
 void launch_row_rstd(const float* x, int T, int H, float eps, float* rstd, cudaStream_t st);
 
 // SwiGLU backward (interleaved 64-col gate|up blocks): dgu = d[silu(g) u].
-void launch_swiglu_bwd(const float* dact, const float* gu, int T, int I, __nv_bfloat16* dgu,
+void launch_swiglu_bwd(const float* dact, const __nv_bfloat16* gu, int T, int I, __nv_bfloat16* dgu,
                        float* dgu_f32, cudaStream_t st);
 
 // Attention backward (causal, paged K/V as in the forward).  dq/dk/dv are

@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kRowThreads)
   }
 }
 
-__global__ void swiglu_bwd_kernel(const float* __restrict__ dact, const float* __restrict__ gu,
+__global__ void swiglu_bwd_kernel(const float* __restrict__ dact, const __nv_bfloat16* __restrict__ gu,
                                   int T, int I, __nv_bfloat16* __restrict__ dgu,
                                   float* __restrict__ dgu_f32) {
   const size_t n = (size_t)T * I;
@@ -208,7 +208,7 @@ __global__ void swiglu_bwd_kernel(const float* __restrict__ dact, const float* _
     const int j = (int)(e % I);
     const int blk = j >> 6, c = j & 63;
     const size_t gi = t * 2 * I + (size_t)blk * 128 + c, ui = gi + 64;
-    const float gv = gu[gi], uv = gu[ui], da = dact[e];
+    const float gv = __bfloat162float(gu[gi]), uv = __bfloat162float(gu[ui]), da = dact[e];
     const float sg = 1.f / (1.f + expf(-gv));
     const float silu = gv * sg;
     const float dg = da * uv * (sg * (1.f + gv * (1.f - sg)));
@@ -446,7 +446,7 @@ void launch_rmsnorm_bwd(const float* dzw, const float* x, const __nv_bfloat16* g
 void launch_row_rstd(const float* x, int T, int H, float eps, float* rstd, cudaStream_t st) {
   if (T > 0) row_rstd_kernel<<<T, kRowThreads, 0, st>>>(x, H, eps, rstd);
 }
-void launch_swiglu_bwd(const float* dact, const float* gu, int T, int I, __nv_bfloat16* dgu,
+void launch_swiglu_bwd(const float* dact, const __nv_bfloat16* gu, int T, int I, __nv_bfloat16* dgu,
                        float* dgu_f32, cudaStream_t st) {
   swiglu_bwd_kernel<<<grid_for((size_t)T * I, 256), 256, 0, st>>>(dact, gu, T, I, dgu, dgu_f32);
 }

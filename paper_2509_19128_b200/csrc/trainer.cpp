@@ -291,12 +291,11 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
     if ((s = gemm(a.attn, T_max_, T, w + o.o_w, H, qd, r))) return s;
     SRL_CUDA(cudaMemcpyAsync(a.x_mid, x_, sizeof(float) * T * H, cudaMemcpyDeviceToDevice, st));
     launch_row_rstd(a.x_mid, T, H, d_.eps, a.rstd2, st);
-    EpiParams g;
-    g.kind = EPI_STORE_F32;
+    EpiParams g;  // SwiGLU fused: act for the down GEMM, gate | up kept (bf16) for the backward
+    g.kind = EPI_SWIGLU;
     g.ssq_in = ssq_; g.ssq_in_parts = parts; g.inv_dim = inv_h; g.eps = d_.eps;
-    g.out_f32 = a.gu; g.ld_out = 2 * I;
+    g.out_bf16 = a.act; g.ld_bf16 = I; g.out2_bf16 = a.gu;
     if ((s = gemm(a.xg2, T_max_, T, w + o.gate_up_w, 2 * I, H, g))) return s;
-    launch_swiglu_fwd(a.gu, T, I, a.act, st);
     EpiParams r2;
     r2.kind = EPI_RESID; r2.resid = x_; r2.ssq_out = ssq_;
     r2.xg = l + 1 < L ? acts_[l + 1].xg1 : xgF_;

@@ -34,9 +34,9 @@ class DecoderTrainer {
 
  private:
   struct LayerActs {
-    float *x_in = nullptr, *rstd1 = nullptr, *lse = nullptr, *x_mid = nullptr, *rstd2 = nullptr,
-          *gu = nullptr;
-    __nv_bfloat16 *xg1 = nullptr, *q = nullptr, *attn = nullptr, *xg2 = nullptr, *act = nullptr;
+    float *x_in = nullptr, *rstd1 = nullptr, *lse = nullptr, *x_mid = nullptr, *rstd2 = nullptr;
+    __nv_bfloat16 *xg1 = nullptr, *q = nullptr, *attn = nullptr, *xg2 = nullptr, *act = nullptr,
+                  *gu = nullptr;  // rstd-scaled gate | up pre-activations (bf16, 64-row interleave)
   };
   template <typename T>
   int alloc(T** p, size_t n);
