@@ -248,6 +248,30 @@ def trainer_measure(cfg, pol, n_seq, prompt, gen, steps=3):
     return out
 
 
+def recompute_pause_measure(cfg, pol, payload_policy, args, rounds=128):
+    """The same in-flight update with the engine in recompute mode
+    (engine.cpp:107-113): at the swap every live stream's KV cache is rebuilt
+    from its full prefix under the new weights (chunked prefill, tensor-core
+    attention segments) -- the pause PipelineRL avoids by keeping the stale
+    cache.  B streams of prompt + `rounds` generated tokens."""
+    from paper_2509_19128_b200.engine import Engine
+
+    eng = Engine(pol, recompute_state=True, start_paused=True, max_streams=args.batch,
+                 max_seq_len=args.prompt + rounds + 8, rounds_per_sync=32,
+                 prefill_budget=args.batch * (args.prompt + 1))
+    rng = np.random.default_rng(5)
+    for i in range(args.batch):
+        eng.open_stream("p", rounds + 4, i, -1, rng.integers(0, cfg.vocab_size, size=args.prompt).tolist())
+    eng.advance(rounds)
+    ctx = sum(len(eng.stream_tokens(f"s{i}")) for i in range(args.batch))
+    res = eng.apply_weight_update(1, payload_policy)
+    assert res.applied
+    pause = eng.stats()["last_pause_ms"]
+    eng.close()
+    return {"ms": pause, "rebuilt_tokens": ctx,
+            "note": f"{args.batch} streams, recompute mode: full-prefix KV rebuild at the swap"}
+
+
 def pipeline_measure(cfg, args, steps=6):
     """The whole PipelineRL loop time-shared on ONE GPU (paper_2509_19128_b200/
     pipeline.py): constant-batch generator -> actor queue -> IS-REINFORCE
@@ -534,6 +558,7 @@ def main():
         out["trainer"] = trainer_measure(cfg, pol, args.train_seqs, args.prompt, args.gen)
         out["trainer"]["clocks"] = tclk.stop()
     if rank == 0 and world == 1 and not args.no_pipeline:
+        out["pause_ms_recompute_mode"] = recompute_pause_measure(cfg, pol, payloads[0], args)
         out["pipeline_1gpu"] = pipeline_measure(cfg, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tps, dt, cores = cpu_decode_sample(cfg, B, 8, args.cpu_steps, 1)

@@ -796,40 +796,59 @@ int DecoderBackend::swap_and_recompute(bool recompute, int version) {
 // chunk only attends to already-rewritten keys.
 int DecoderBackend::recompute_kv() {
   DecoderRunner& r = *runner_;
-  int max_fed = 0;
+  int max_fed = 0, n_live = 0;
   for (const HostSlot& h : host_)
-    if (h.live && !h.pending) max_fed = std::max(max_fed, h.fed);
-  std::vector<int32_t> rs, rp, rt;
-  auto flush = [&]() -> int {
+    if (h.live && !h.pending) {
+      max_fed = std::max(max_fed, h.fed);
+      ++n_live;
+    }
+  if (n_live == 0) return SRL_OK;
+  // chunks of positions [c0, c1), rows slot-major inside a chunk: each live
+  // slot's rows form one attention segment (first row, count, first position,
+  // slot) for the tensor-core kernel; keys before c0 were rewritten by the
+  // previous chunks, keys in [c0, p] by this chunk's QKV epilogue
+  const int span = std::max(1, r.M_max / n_live);
+  std::vector<int32_t> rs, rp, rt, seg(4 * (size_t)S_);
+  for (int c0 = 0; c0 < max_fed; c0 += span) {
+    const int c1 = std::min(max_fed, c0 + span);
+    rs.clear(); rp.clear(); rt.clear();
+    int n_seg = 0, seg_max = 0;
+    for (int s = 0; s < S_; ++s) {
+      const HostSlot& h = host_[s];
+      if (!h.live || h.pending || c0 >= h.fed) continue;
+      const int e = std::min(c1, h.fed);
+      seg[n_seg] = (int)rs.size();
+      seg[S_ + n_seg] = e - c0;
+      seg[2 * S_ + n_seg] = c0;
+      seg[3 * S_ + n_seg] = s;
+      seg_max = std::max(seg_max, e - c0);
+      ++n_seg;
+      for (int p = c0; p < e; ++p) {
+        rs.push_back(s);
+        rp.push_back(p);
+        rt.push_back(h.tokens[p]);
+      }
+    }
     const int M = (int)rs.size();
-    if (M == 0) return SRL_OK;
+    if (M == 0) continue;
     int32_t* pin = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(pinned_) + (size_t)R_ * S_ * sizeof(DevEvent));
     std::memcpy(pin, rs.data(), 4 * M);
     std::memcpy(pin + M, rp.data(), 4 * M);
     std::memcpy(pin + 2 * M, rt.data(), 4 * M);
+    std::memcpy(pin + 3 * M + S_, seg.data(), 16 * (size_t)S_);
     SRL_CUDA(cudaMemcpyAsync(r.plan.row_slot, pin, 4 * M, cudaMemcpyHostToDevice, st_));
     SRL_CUDA(cudaMemcpyAsync(r.plan.row_pos, pin + M, 4 * M, cudaMemcpyHostToDevice, st_));
     SRL_CUDA(cudaMemcpyAsync(r.plan.row_token, pin + 2 * M, 4 * M, cudaMemcpyHostToDevice, st_));
+    SRL_CUDA(cudaMemcpyAsync(r.seg, pin + 3 * M + S_, 16 * (size_t)S_, cudaMemcpyHostToDevice, st_));
+    r.n_seg = n_seg;
+    r.n_single = 0;
+    r.seg_max_rows = seg_max;
     const int st = r.forward(M, buf_[active_]->w, maps_[active_]);
+    r.n_seg = 0;
     if (st != SRL_OK) return st;
-    SRL_CUDA(cudaStreamSynchronize(st_));
-    rs.clear(); rp.clear(); rt.clear();
-    return SRL_OK;
-  };
-  for (int p = 0; p < max_fed; ++p) {
-    for (int s = 0; s < S_; ++s) {
-      const HostSlot& h = host_[s];
-      if (!h.live || h.pending || p >= h.fed) continue;
-      if ((int)rs.size() == r.M_max) {
-        const int st = flush();
-        if (st != SRL_OK) return st;
-      }
-      rs.push_back(s);
-      rp.push_back(p);
-      rt.push_back(h.tokens[p]);
-    }
+    SRL_CUDA(cudaStreamSynchronize(st_));  // the pinned staging is reused by the next chunk
   }
-  return flush();
+  return SRL_OK;
 }
 
 int DecoderBackend::apply_update(const Policy& p, bool recompute, int version) {
