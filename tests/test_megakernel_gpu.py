@@ -87,3 +87,45 @@ def test_megakernel_matches_multikernel_round(cuda, monkeypatch):
             agree += 1
             lp_close([x.logprob], [y.logprob], 2e-3)
     assert agree >= 0.9 * 64 * 6
+
+
+def test_megakernel_terminator_and_refill(cuda):
+    """Terminator handling inside the megakernel's sampler (engine.cpp:146-149,
+    docs/protocol.md:33-34): with the terminator set to a token a stream
+    samples mid-way (found by a first run without one), the same seeded
+    stream replays the same prefix, emits the terminator and ends there;
+    a freed slot is refilled by a new stream that decodes its own prompt."""
+    from paper_2509_19128_b200.policy import TINY
+
+    pol = DecoderPolicy.random(TINY, seed=4, scale=0.5)
+
+    def run(term):
+        eng = Engine(pol, start_paused=True, max_streams=4, max_seq_len=96)
+        sids = [eng.open_stream("p", 40, 500 + i, term, [1, 2, 3]) for i in range(4)]
+        eng.profile_next_round()
+        eng.advance(44)
+        assert "decode_megakernel" in eng.kernel_profile()
+        out = [eng.collect(sid) for sid in sids]
+        return eng, out
+
+    eng, free = run(-1)
+    eng.close()
+    toks0 = [e.token for e in free[0][0]]
+    term = toks0[10]
+    first = toks0.index(term)
+    eng, out = run(term)
+    evs, reason = out[0]
+    assert reason == "terminator" and [e.token for e in evs] == toks0[:first + 1]
+    for (evs, reason), (fevs, _) in zip(out, free):
+        ft = [e.token for e in fevs]
+        if term in ft:
+            k = ft.index(term)
+            assert reason == "terminator" and [e.token for e in evs] == ft[:k + 1]
+        else:
+            assert reason == "length" and [e.token for e in evs] == ft
+    sid = eng.open_stream("q", 5, 99, -1, [9, 9])
+    eng.advance(8)
+    evs, reason = eng.collect(sid)
+    assert reason == "length" and len(evs) == 5
+    assert eng.stream_tokens(sid)[:3] == [TINY.bos_token, 9, 9]
+    eng.close()
