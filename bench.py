@@ -552,7 +552,7 @@ def main():
                     "note": "refill prefill rounds of finished streams (inside value's device time)"},
         "clocks": clk,
     }
-    if rank == 0 and not args.no_trainer:
+    if rank == 0 and world == 1 and not args.no_trainer:
         tclk = ClockSampler(local)
         tclk.start()
         out["trainer"] = trainer_measure(cfg, pol, args.train_seqs, args.prompt, args.gen)

@@ -917,6 +917,24 @@ void launch_attention(const __nv_bfloat16* q, const DecoderDims& d, const RoundP
                               vc, scale, ws, counters, out, lse_out);
 }
 
+// Slot bookkeeping written by a one-thread kernel (values travel as kernel
+// parameters: no pinned staging to keep alive, no stream synchronisation).
+__global__ void slot_set_kernel(SlotState ss, int slot, int live, int reset, int max_tokens, int terminator,
+                                unsigned long long seed) {
+  ss.live[slot] = live;
+  if (reset) {
+    ss.seq_len[slot] = 0;
+    ss.gen_count[slot] = 0;
+    ss.max_tokens[slot] = max_tokens;
+    ss.terminator[slot] = terminator;
+    ss.seed[slot] = seed;
+  }
+}
+void launch_slot_set(const SlotState& ss, int slot, int live, int reset, int max_tokens, int terminator,
+                     uint64_t seed, cudaStream_t st) {
+  slot_set_kernel<<<1, 1, 0, st>>>(ss, slot, live, reset, max_tokens, terminator, (unsigned long long)seed);
+}
+
 void launch_gather_rows(const __nv_bfloat16* xg, const float* ssq, const int32_t* last_row,
                         int slots, int H, int parts, __nv_bfloat16* xg_out, float* ssq_out,
                         cudaStream_t st) {

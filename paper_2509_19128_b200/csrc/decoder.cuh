@@ -97,6 +97,8 @@ void launch_attention(const __nv_bfloat16* q, const DecoderDims& d, const RoundP
 size_t attention_ws_floats(const DecoderDims& d, int M, int max_ctx);
 
 // Gather the last row of each emitting slot (decode rounds use identity).
+void launch_slot_set(const SlotState& ss, int slot, int live, int reset, int max_tokens, int terminator,
+                     uint64_t seed, cudaStream_t st);
 void launch_gather_rows(const __nv_bfloat16* xg, const float* ssq, const int32_t* last_row,
                         int slots, int H, int parts, __nv_bfloat16* xg_out, float* ssq_out,
                         cudaStream_t st);

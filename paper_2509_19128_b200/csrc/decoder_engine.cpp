@@ -260,6 +260,7 @@ DecoderBackend::~DecoderBackend() {
     if (exec_[b]) cudaGraphExecDestroy(exec_[b]);
   if (dev_state_) cudaFree(dev_state_);
   if (pinned_) cudaFreeHost(pinned_);
+  if (slot_stage_) cudaFreeHost(slot_stage_);
   if (ev_start_) cudaEventDestroy(ev_start_);
   if (ev_stop_) cudaEventDestroy(ev_stop_);
   for (cudaEvent_t& ev : ev_prof_)
@@ -320,6 +321,7 @@ int DecoderBackend::init(const Policy& p) {
   pinned_bytes_ = (size_t)R_ * S_ * sizeof(DevEvent) + (size_t)(runner_->M_max * 3 + S_ + 64) * 4 +
                   (size_t)S_ * 64;
   SRL_CUDA(cudaMallocHost(&pinned_, pinned_bytes_));
+  SRL_CUDA(cudaMallocHost(&slot_stage_, 4 * (size_t)S_ * max_seq_));
   host_.assign(S_, HostSlot{});
   // next plan: every slot dead
   std::vector<int32_t> neg(std::max(runner_->M_max, S_), -1);
@@ -546,20 +548,14 @@ int DecoderBackend::open_slot(int slot, const StreamSpec& spec) {
   h.tokens.push_back(d_.bos);
   h.tokens.insert(h.tokens.end(), spec.prompt.begin(), spec.prompt.end());
   h.fed = 0;
-  // device slot state (pinned staging; synchronous so the staging can be reused)
-  int32_t* pi = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(pinned_) + pinned_bytes_ - 64);
-  uint64_t* pu = reinterpret_cast<uint64_t*>(pi + 8);
-  pi[0] = 1; pi[1] = 0; pi[2] = 0; pi[3] = spec.max_tokens; pi[4] = spec.terminator;
-  pu[0] = spec.seed;
-  SRL_CUDA(cudaMemcpyAsync(ss_.live + slot, pi + 0, 4, cudaMemcpyHostToDevice, st_));
-  SRL_CUDA(cudaMemcpyAsync(ss_.seq_len + slot, pi + 1, 4, cudaMemcpyHostToDevice, st_));
-  SRL_CUDA(cudaMemcpyAsync(ss_.gen_count + slot, pi + 2, 4, cudaMemcpyHostToDevice, st_));
-  SRL_CUDA(cudaMemcpyAsync(ss_.max_tokens + slot, pi + 3, 4, cudaMemcpyHostToDevice, st_));
-  SRL_CUDA(cudaMemcpyAsync(ss_.terminator + slot, pi + 4, 4, cudaMemcpyHostToDevice, st_));
-  SRL_CUDA(cudaMemcpyAsync(ss_.seed + slot, pu, 8, cudaMemcpyHostToDevice, st_));
-  SRL_CUDA(cudaMemcpyAsync(ss_.history + (size_t)slot * max_seq_, h.tokens.data(),
-                           4 * h.tokens.size(), cudaMemcpyHostToDevice, st_));
-  SRL_CUDA(cudaStreamSynchronize(st_));
+  // device slot state: one tiny kernel for the scalars, the prefix from this
+  // slot's own pinned staging row (alive until the slot is reopened, which
+  // happens only after the stream's rounds ran): no stream synchronisation
+  launch_slot_set(ss_, slot, 1, 1, spec.max_tokens, spec.terminator, spec.seed, st_);
+  int32_t* stage = slot_stage_ + (size_t)slot * max_seq_;
+  std::memcpy(stage, h.tokens.data(), 4 * h.tokens.size());
+  SRL_CUDA(cudaMemcpyAsync(ss_.history + (size_t)slot * max_seq_, stage, 4 * h.tokens.size(),
+                           cudaMemcpyHostToDevice, st_));
   any_pending_ = true;
   return SRL_OK;
 }
@@ -567,10 +563,7 @@ int DecoderBackend::open_slot(int slot, const StreamSpec& spec) {
 void DecoderBackend::close_slot(int slot) {
   host_[slot].live = false;
   host_[slot].pending = false;
-  int32_t* pi = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(pinned_) + pinned_bytes_ - 64);
-  pi[0] = 0;
-  cudaMemcpyAsync(ss_.live + slot, pi, 4, cudaMemcpyHostToDevice, st_);
-  cudaStreamSynchronize(st_);
+  launch_slot_set(ss_, slot, 0, 0, 0, -1, 0, st_);  // stream-ordered before the next round
 }
 
 int DecoderBackend::decode_round_eager(int b) {

@@ -132,6 +132,7 @@ class DecoderBackend final : public Backend {
   cudaEvent_t ev_start_ = nullptr, ev_stop_ = nullptr;
   cudaEvent_t ev_prof_[2] = {nullptr, nullptr};  // around a profiled megakernel launch
   cudaEvent_t ev_pf_[2] = {nullptr, nullptr};    // around a prefill round
+  int32_t* slot_stage_ = nullptr;  // pinned [slots x max_seq] prompt staging (open_slot)
   int64_t prefill_rounds_ = 0, prefill_rows_ = 0;
   double prefill_ms_ = 0.0;
   int last_prefill_rows_ = 0;
