@@ -295,6 +295,17 @@ int srl_kernel_gemm_bf16(const void* w, const void* x, int32_t M, int32_t N, int
                          void* out, float* resid, const void* gain, void* xg, float* ssq_out,
                          void* stream);
 
+/* tcgen05 GEMM with an MN-major W operand (the trainer's weight gradients
+ * and input gradients without transposes): out[m, n] (+)= scale * sum_k
+ * X(m, k) w[k, n]; w is [k_rows x N] row-major bf16; X is x[k, m] ([k_rows x
+ * M], x_kmajor = 0) or x[m, k] ([M x k_rows], x_kmajor = 1, k_rows % 64 == 0).
+ * K = k_rows rounded up to 64 (rows past k_rows read as zero).  accumulate
+ * != 0 adds into out (fp32 [M x N]); splits <= 0 plans the K slicing, which
+ * stays deterministic (ordered slices). */
+int srl_kernel_gemm_mn(const void* w, const void* x, int32_t M, int32_t N, int32_t k_rows,
+                       int32_t x_kmajor, int32_t splits, int32_t accumulate, float scale, float* out,
+                       void* stream);
+
 /* The decode sampler on raw fp32 logits rows (device pointers): row r uses
  * draw #draw_index[r] of SplitMix64(seeds[r]) (rng.hpp:18-28) and the
  * inverse CDF of exp(log_softmax) in fp64 (rng.hpp:61-69, engine.cpp:130-138);

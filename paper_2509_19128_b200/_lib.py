@@ -84,6 +84,7 @@ I = C.c_int
 SIGNATURES: dict[str, tuple] = {
     "srl_status_string": (cp, [I]),
     "srl_last_error": (cp, []),
+    "srl_kernel_gemm_mn": (I, [vp, vp, i32, i32, i32, i32, i32, i32, f32, vp, vp]),
     "srl_kernel_gemm_bf16": (I, [vp, vp, i32, i32, i32, i32, i32, vp, vp, i32, f32, f32,
                                  vp, vp, vp, vp, vp, vp]),
     "srl_policy_tabular_create": (I, [i32, i32, vp, i32, P(cp), vp, vp, vp, P(vp)]),

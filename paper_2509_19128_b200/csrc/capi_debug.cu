@@ -70,6 +70,35 @@ extern "C" int srl_kernel_gemm_bf16(const void* w, const void* x, int32_t M, int
   return cuda_status(gemm_bf16_launch(tw, tx, M, N, K, splits, ws, epi, st));
 }
 
+extern "C" int srl_kernel_gemm_mn(const void* w, const void* x, int32_t M, int32_t N, int32_t k_rows,
+                                  int32_t x_kmajor, int32_t splits, int32_t accumulate, float scale,
+                                  float* out, void* stream) {
+  if (!w || !x || !out || M < 1 || N < 1 || k_rows < 1 || N % 8) return SRL_INVALID_ARGUMENT;
+  if (x_kmajor ? k_rows % 64 != 0 : M % 8 != 0) return SRL_INVALID_ARGUMENT;
+  const int K = (k_rows + 63) / 64 * 64;
+  const CUtensorMap tw = make_tmap_bf16(w, (uint64_t)k_rows, (uint64_t)N, 64);
+  const CUtensorMap tx = x_kmajor ? make_tmap_bf16(x, (uint64_t)M, (uint64_t)K, 128)
+                                  : make_tmap_bf16(x, (uint64_t)k_rows, (uint64_t)M, 64);
+  int planned = 1;
+  const int tok = gemm_mn_plan(M, N, K, num_sms(), &planned);
+  if (splits <= 0) splits = planned;
+  static int* g_flags = nullptr;  // split-K ordering counters (self-resetting)
+  constexpr int kFlags = 1 << 16;
+  if (g_flags == nullptr) {
+    if (cudaMalloc(&g_flags, kFlags * sizeof(int)) != cudaSuccess) return SRL_OUT_OF_MEMORY;
+    if (cudaMemset(g_flags, 0, kFlags * sizeof(int)) != cudaSuccess) return SRL_CUDA_ERROR;
+  }
+  if ((size_t)((N + 127) / 128) * ((M + tok - 1) / tok) > (size_t)kFlags) return SRL_INVALID_ARGUMENT;
+  EpiParams epi;
+  epi.kind = accumulate ? EPI_ACCUM_F32 : EPI_STORE_F32;
+  epi.out_f32 = out;
+  epi.ld_out = N;
+  epi.scale = scale;
+  epi.tile_flags = g_flags;
+  if (!accumulate && splits > 1) return SRL_INVALID_ARGUMENT;
+  return cuda_status(gemm_mn_launch(tw, tx, M, N, K, tok, splits, !x_kmajor, epi, static_cast<cudaStream_t>(stream)));
+}
+
 extern "C" int srl_kernel_sample_logits(const float* logits, int32_t vocab, int32_t rows,
                                         const uint64_t* seeds, const int32_t* draw_index,
                                         int32_t greedy, int32_t* tokens_out, double* logprobs_out,

@@ -65,6 +65,7 @@ struct EpiParams {
   __nv_bfloat16* outT_bf16 = nullptr;
   __nv_bfloat16* out2_bf16 = nullptr;   // EPI_SWIGLU: also the rstd-scaled gate | up [M x N] (bf16)
   int ldT = 0;
+  int* tile_flags = nullptr;            // gemm_mn_launch split-K ordering (>= tiles ints, zeroed once)
   // debug: per-CTA %globaltimer phase stamps [ctas x 8] (null = off)
   unsigned long long* stamps = nullptr;
 };
@@ -91,6 +92,16 @@ size_t gemm_workspace_floats(int M, int N, int splits);
 int gemm_big_tok(int M, int N, int K, int num_sms);
 cudaError_t gemm_big_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int tok,
                             const EpiParams& epi, cudaStream_t stream);
+
+// W operand MN-major: tw maps W as [K x N] with 64 x 64 boxes
+// (make_tmap_bf16(p, K_rows, N, 64)); rows past the map's K read as zero, so
+// K may be rounded up to 64.  x_mn: X is MN-major too ([K x M], 64 x 64
+// boxes), else K-major [M x K] with a box of `tok` rows.  C[m, n] = sum_k
+// X(m, k) W[k, n] through EPI_STORE_F32 / EPI_ACCUM_F32 (no rstd / bias);
+// splits > 1 (ordered K slices) needs EPI_ACCUM_F32 and epi.tile_flags.
+int gemm_mn_plan(int M, int N, int K, int num_sms, int* splits);
+cudaError_t gemm_mn_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int tok,
+                           int splits, bool x_mn, const EpiParams& epi, cudaStream_t stream);
 
 // Launch.  tw: W [N x K] (box 128 rows); tx: X [>=M x K] (box gemm_tok_tile(M) rows).
 // Dispatches to gemm_big_launch when gemm_big_tok() says so (splits ignored).

@@ -70,10 +70,17 @@ __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
 }
 
-template <int TOK>
+// AMN / BMN: the W / X operand is MN-major (given as [K x N] / [K x M]
+// row-major, e.g. the trainer's dW = dY^T X with the token axis as K, or
+// dX = dY W with W's rows as K): 64 x 64 TMA boxes, UMMA descriptors with
+// the 64-element MN groups 8 KB apart.  `splits` > 1 cuts K into
+// ordered slices whose EPI_ACCUM epilogues add into the output one after the
+// other (per-tile counters in epi.tile_flags, self-resetting): deterministic
+// split-K for the small-output, long-K weight gradients.
+template <int TOK, bool AMN, bool BMN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_big_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
-                    int M, int N, int K, const EpiParams epi) {
+                    int M, int N, int K, int splits, const EpiParams epi) {
   using L = BigLayout<TOK>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -88,7 +95,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int n_tiles = (N + kBN - 1) / kBN;
   const int tok_tiles = (M + TOK - 1) / TOK;
-  const int total = n_tiles * tok_tiles;
+  const int tiles = n_tiles * tok_tiles;
+  const int total = tiles * splits;
   const int kbt = K / kBK;
 
   if (warp == 0) {
@@ -124,15 +132,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int n0 = (t % n_tiles) * kBN, t0 = (t / n_tiles) * TOK;
-        for (int kb = 0; kb < kbt; ++kb) {
+        const int tile = t % tiles, sp = t / tiles;
+        const int n0 = (tile % n_tiles) * kBN, t0 = (tile / n_tiles) * TOK;
+        for (int kb = sp * kbt / splits; kb < (sp + 1) * kbt / splits; ++kb) {
           mbar_wait(&empty[stage], ph ^ 1);
           uint8_t* a = smem + stage * L::kStageBytes;
           mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
-          tma_load_2d(a, &tw, &full[stage], kb * kBK, n0);
+          if constexpr (AMN) {  // 64 x 64 boxes: [k rows][64 MN columns], 8 KB each
+            tma_load_2d(a, &tw, &full[stage], n0, kb * kBK);
+            tma_load_2d(a + 8192, &tw, &full[stage], n0 + 64, kb * kBK);
+          } else {
+            tma_load_2d(a, &tw, &full[stage], kb * kBK, n0);
+          }
+          if constexpr (BMN) {
 #pragma unroll
-          for (int h = 0; h < TOK / 128; ++h)  // the X map's box is 128 rows
-            tma_load_2d(a + L::kABytes + h * 128 * 128, &tx, &full[stage], kb * kBK, t0 + h * 128);
+            for (int h = 0; h < TOK / 64; ++h)
+              tma_load_2d(a + L::kABytes + h * 8192, &tx, &full[stage], t0 + h * 64, kb * kBK);
+          } else {
+#pragma unroll
+            for (int h = 0; h < TOK / 128; ++h)  // the X map's box is 128 rows
+              tma_load_2d(a + L::kABytes + h * 128 * 128, &tx, &full[stage], kb * kBK, t0 + h * 128);
+          }
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
         }
       }
@@ -140,22 +160,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (elect_one()) {  // ---- MMA issuer
-      constexpr uint32_t idesc = idesc_bf16_f32(128, TOK);
+      constexpr uint32_t idesc = idesc_bf16_f32(128, TOK) | (AMN ? idesc_a_mn_major : 0u) |
+                                 (BMN ? idesc_b_mn_major : 0u);
       int stage = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * TOK;
-        for (int kb = 0; kb < kbt; ++kb) {
+        const int sp = t / tiles, kb0 = sp * kbt / splits;
+        for (int kb = kb0; kb < (sp + 1) * kbt / splits; ++kb) {
           mbar_wait(&full[stage], ph);
           tc_fence_after();
           const uint32_t a = smem_u32(smem + stage * L::kStageBytes);
           const uint32_t b = a + L::kABytes;
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk)
-            mma_bf16_ss(d, umma_desc_k_sw128(a, kk * 32), umma_desc_k_sw128(b, kk * 32), idesc,
-                        (kb | kk) != 0);
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            // MN-major: 16 k rows = two 1-KB swizzle atoms; K-major: 32 B inside the atom
+            const uint64_t da = AMN ? umma_desc_mn_sw128(a + kk * 2048, 8192) : umma_desc_k_sw128(a, kk * 32);
+            const uint64_t db = BMN ? umma_desc_mn_sw128(b + kk * 2048, 8192) : umma_desc_k_sw128(b, kk * 32);
+            mma_bf16_ss(d, da, db, idesc, (kb != kb0) || kk != 0);
+          }
           mma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
         }
@@ -181,12 +206,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const int n_tile = t % n_tiles, n0 = n_tile * kBN, t0 = (t / n_tiles) * TOK;
+      const int otile = t % tiles, sp = t / tiles;
+      const int n_tile = otile % n_tiles, n0 = n_tile * kBN, t0 = (otile / n_tiles) * TOK;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       if (!waited) {  // epilogue inputs (residual, ssq) come from earlier kernels
         griddep_wait();
         waited = true;
+      }
+      if (splits > 1 && sp > 0) {  // K slice sp adds after slices 0..sp-1 (both groups each)
+        if (tid == 0) {
+          while (ld_acquire_gpu(epi.tile_flags + otile) < 2 * sp) __nanosleep(64);
+        }
+        sync();
       }
       const int last = TOK / kChunk - 2 + g;  // this group's last chunk of the tile
       for (int c = g; c < TOK / kChunk; c += 2) {
@@ -315,6 +347,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                s_row, tid, 128, sync);
         sync();  // the staged chunk is reused next
       }
+      if (splits > 1) {
+        __threadfence();
+        sync();
+        if (tid == 0 && atomicAdd(epi.tile_flags + otile, 1) == 2 * splits - 1)
+          atomicExch(epi.tile_flags + otile, 0);  // last slice: reset for the next launch
+      }
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
   }
@@ -333,17 +371,17 @@ int num_sms_cached() {
   return n;
 }
 
-template <int TOK>
-cudaError_t launch_big(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K,
+template <int TOK, bool AMN, bool BMN>
+cudaError_t launch_big(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int splits,
                        const EpiParams& epi, cudaStream_t stream) {
   using L = BigLayout<TOK>;
   static const cudaError_t attr = cudaFuncSetAttribute(
-      gemm_big_kernel<TOK>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
+      gemm_big_kernel<TOK, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
   if (attr != cudaSuccess) return attr;
-  const int tiles = ((N + kBN - 1) / kBN) * ((M + TOK - 1) / TOK);
+  const int tiles = ((N + kBN - 1) / kBN) * ((M + TOK - 1) / TOK) * splits;
   const int grid = tiles < num_sms_cached() ? tiles : num_sms_cached();
-  return launch_pdl(gemm_big_kernel<TOK>, dim3(grid), dim3(kThreads), (size_t)L::kAlloc, stream,
-                    dim3(1, 1, 1), tw, tx, M, N, K, epi);
+  return launch_pdl(gemm_big_kernel<TOK, AMN, BMN>, dim3(grid), dim3(kThreads), (size_t)L::kAlloc, stream,
+                    dim3(1, 1, 1), tw, tx, M, N, K, splits, epi);
 }
 
 }  // namespace
@@ -364,8 +402,40 @@ int gemm_big_tok(int M, int N, int K, int num_sms) {
 
 cudaError_t gemm_big_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int tok,
                             const EpiParams& epi, cudaStream_t stream) {
-  if (tok == 256) return launch_big<256>(tw, tx, M, N, K, epi, stream);
-  if (tok == 128) return launch_big<128>(tw, tx, M, N, K, epi, stream);
+  if (tok == 256) return launch_big<256, false, false>(tw, tx, M, N, K, 1, epi, stream);
+  if (tok == 128) return launch_big<128, false, false>(tw, tx, M, N, K, 1, epi, stream);
+  return cudaErrorInvalidValue;
+}
+
+// MN-major plan: 256-token tiles when they give two waves, else 128; long-K
+// outputs of less than half a wave get K slices (>= 8 k-blocks each) up to
+// about one wave.
+int gemm_mn_plan(int M, int N, int K, int num_sms, int* splits) {
+  const int n_tiles = (N + kBN - 1) / kBN;
+  const int tok = n_tiles * ((M + 255) / 256) >= 2 * num_sms ? 256 : 128;
+  const int tiles = n_tiles * ((M + tok - 1) / tok);
+  int s = 1;
+  if (2 * tiles <= num_sms)
+    while ((s + 1) * tiles <= num_sms && (K / kBK) / (s + 1) >= 8) ++s;
+  *splits = s;
+  return tok;
+}
+
+cudaError_t gemm_mn_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int tok,
+                           int splits, bool x_mn, const EpiParams& epi, cudaStream_t stream) {
+  if (M < 1 || N < 1 || K < kBK || K % kBK != 0 || splits < 1 || splits > K / kBK)
+    return cudaErrorInvalidValue;
+  const bool direct = epi.kind == EPI_ACCUM_F32 || epi.kind == EPI_STORE_F32;
+  if (!direct || (splits > 1 && (epi.kind != EPI_ACCUM_F32 || epi.tile_flags == nullptr)) ||
+      epi.ssq_in != nullptr || epi.bias != nullptr)
+    return cudaErrorInvalidValue;
+  if (x_mn) {
+    if (tok == 256) return launch_big<256, true, true>(tw, tx, M, N, K, splits, epi, stream);
+    if (tok == 128) return launch_big<128, true, true>(tw, tx, M, N, K, splits, epi, stream);
+  } else {
+    if (tok == 256) return launch_big<256, true, false>(tw, tx, M, N, K, splits, epi, stream);
+    if (tok == 128) return launch_big<128, true, false>(tw, tx, M, N, K, splits, epi, stream);
+  }
   return cudaErrorInvalidValue;
 }
 

@@ -157,6 +157,25 @@ SRL_DEVICE uint64_t umma_desc_k_sw128(uint32_t smem_addr, uint32_t byte_off) {
          (2ull << 61) /* SWIZZLE_128B */;
 }
 
+// UMMA descriptor for an MN-major, 128B-swizzled operand as TMA writes a
+// [k rows x 64 elements] box: 8-row (1 KB) swizzle atoms along K, 64-element
+// MN groups `mn_group_bytes` apart (the LBO of the swizzled MN-major layout).
+// Advance along K by whole atoms (2048 B per UMMA_K = 16 rows).
+SRL_DEVICE uint64_t umma_desc_mn_sw128(uint32_t smem_addr, uint32_t mn_group_bytes) {
+  const uint64_t start = (smem_addr >> 4) & 0x3FFFull;
+  const uint64_t lbo = (mn_group_bytes >> 4) & 0x3FFFull;
+  const uint64_t sbo = (1024ull >> 4);
+  return start | (lbo << 16) | (sbo << 32) | (1ull << 46) | (2ull << 61);
+}
+SRL_DEVICE int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// a_major / b_major bits of the instruction descriptor (operand MN-major).
+constexpr uint32_t idesc_a_mn_major = 1u << 15;
+constexpr uint32_t idesc_b_mn_major = 1u << 16;
+
 // Instruction descriptor: bf16 x bf16 -> fp32, both operands K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
   return (1u << 4)           // D format f32

@@ -19,6 +19,9 @@ void launch_transpose_f32_bf16(const float* src, int rows, int cols, __nv_bfloat
 // dst[r, :] = bf16(scale[r] * src[r, :]) then transposed (xn^T for weight gradients).
 void launch_scale_transpose_bf16(const __nv_bfloat16* src, const float* row_scale, int rows,
                                  int cols, __nv_bfloat16* dst, int ld_dst, cudaStream_t st);
+// dst[r, :] = bf16(scale[r] * src[r, :]) (xn for the MN-major weight gradients); cols % 8 == 0.
+void launch_scale_rows_bf16(const __nv_bfloat16* src, const float* row_scale, int rows, int cols,
+                            __nv_bfloat16* dst, cudaStream_t st);
 // act[t, j] = bf16(silu(g) * u) from the interleaved fp32 gate|up pre-activations.
 void launch_swiglu_fwd(const float* gu, int T, int I, __nv_bfloat16* act, cudaStream_t st);
 void launch_f32_to_bf16(const float* src, size_t n, __nv_bfloat16* dst, cudaStream_t st);

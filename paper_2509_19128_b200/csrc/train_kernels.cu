@@ -87,6 +87,20 @@ __global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ s, size_t n
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     d[i] = __bfloat162float(s[i]);
 }
+// dst[r, :] = bf16(scale[r] * src[r, :]), 8 columns per thread (cols % 8 == 0)
+__global__ void scale_rows_kernel(const __nv_bfloat16* __restrict__ src, const float* __restrict__ scale,
+                                  int rows, int cols, __nv_bfloat16* __restrict__ dst) {
+  const int c8 = cols / 8;
+  const size_t n = (size_t)rows * c8;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float sc = scale[i / c8];
+    uint4 v = reinterpret_cast<const uint4*>(src)[i];
+    __nv_bfloat16* b = reinterpret_cast<__nv_bfloat16*>(&v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b[j] = __float2bfloat16(sc * __bfloat162float(b[j]));
+    reinterpret_cast<uint4*>(dst)[i] = v;
+  }
+}
 __global__ void zero_kernel(float* p, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     p[i] = 0.f;
@@ -421,6 +435,10 @@ void launch_swiglu_fwd(const float* gu, int T, int I, __nv_bfloat16* act, cudaSt
 }
 void launch_f32_to_bf16(const float* src, size_t n, __nv_bfloat16* dst, cudaStream_t st) {
   f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(src, n, dst);
+}
+void launch_scale_rows_bf16(const __nv_bfloat16* src, const float* row_scale, int rows, int cols,
+                            __nv_bfloat16* dst, cudaStream_t st) {
+  scale_rows_kernel<<<grid_for((size_t)rows * (cols / 8), 256), 256, 0, st>>>(src, row_scale, rows, cols, dst);
 }
 void launch_bf16_to_f32(const __nv_bfloat16* src, size_t n, float* dst, cudaStream_t st) {
   bf16_to_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(src, n, dst);

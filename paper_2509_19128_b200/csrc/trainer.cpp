@@ -77,6 +77,7 @@ namespace {
 // keep the LM-head GEMMs efficient and, above all, accumulate the [V x H] fp32
 // LM-head gradient (a read-modify-write of 0.5 GB at V = 152k) few times.
 constexpr int kLogitChunkMax = 16384;
+constexpr int kTileFlags = 4096;
 int pad64(int x) { return (x + 63) / 64 * 64; }
 }  // namespace
 
@@ -110,10 +111,11 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
   T_max_ = pad64(std::max(64, o.max_tokens));
   chunk_ = std::min(kLogitChunkMax, T_max_);
   const int H = d_.H, L = d_.L, I = d_.I, qd = d_.qdim(), qkv = d_.qkv();
-  // fp32 master weights, Adam moments, gradient, transposed bf16 weights
+  // fp32 master weights, Adam moments, gradient
   if ((st = alloc(&master_, n_)) || (st = alloc(&grad_, n_)) || (st = alloc(&adam_m_, n_)) ||
-      (st = alloc(&adam_v_, n_)) || (st = alloc(&wt_, n_)))
+      (st = alloc(&adam_v_, n_)) || (st = alloc(&tile_flags_, kTileFlags)))
     return st;
+  SRL_CUDA(cudaMemsetAsync(tile_flags_, 0, sizeof(int) * kTileFlags, st_));
   launch_bf16_to_f32(weights_->w, n_, master_, st_);
   // saved activations
   acts_.resize(L);
@@ -131,13 +133,11 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
       (st = alloc(&rstdF_, T_max_)) || (st = alloc(&ssq_, (size_t)T_max_ * d_.ssq_parts())) ||
       (st = alloc(&pmax_, (size_t)chunk_ * ((d_.V + 127) / 128))) ||
       (st = alloc(&psum_, (size_t)chunk_ * ((d_.V + 127) / 128))) ||
-      (st = alloc(&dlogits_, (size_t)chunk_ * d_.V)) ||
-      (st = alloc(&dlogitsT_, (size_t)d_.V * chunk_)) || (st = alloc(&dx_, (size_t)T_max_ * H)) ||
+      (st = alloc(&dlogits_, (size_t)chunk_ * d_.V)) || (st = alloc(&dx_, (size_t)T_max_ * H)) ||
       (st = alloc(&dz_, (size_t)T_max_ * std::max(H, 2 * I))) ||
       (st = alloc(&dbig_, (size_t)T_max_ * std::max({2 * I, qkv, qd}))) ||
       (st = alloc(&dbig_bf_, (size_t)T_max_ * std::max({2 * I, qkv, qd, H}))) ||
-      (st = alloc(&tA_, (size_t)std::max({2 * I, qkv, qd, H, I}) * T_max_)) ||
-      (st = alloc(&tB_, (size_t)std::max({2 * I, qkv, qd, H, I}) * T_max_)) ||
+      (st = alloc(&xn_, (size_t)T_max_ * H)) ||
       (st = alloc(&ones_, T_max_)) || (st = alloc(&row_slot_, T_max_)) ||
       (st = alloc(&row_pos_, T_max_)) || (st = alloc(&row_tok_, T_max_)) ||
       (st = alloc(&row_tgt_, T_max_)) || (st = alloc(&coef_, T_max_)) ||
@@ -191,20 +191,30 @@ int DecoderTrainer::gemm_accum(const __nv_bfloat16* X, int M, const __nv_bfloat1
   return gemm(X, M, M, W, N, K, e);
 }
 
-// W^T of every matrix (K-major operands for dX = dY W).
-void DecoderTrainer::transpose_weights() {
-  const __nv_bfloat16* w = weights_->w;
-  auto tr = [&](size_t off, int rows, int cols) {
-    launch_transpose_bf16(w + off, rows, cols, wt_ + off, rows, st_);
-  };
-  for (int l = 0; l < d_.L; ++l) {
-    const LayerOffsets& o = lay_.layers[l];
-    tr(o.qkv_w, d_.qkv(), d_.H);
-    tr(o.o_w, d_.H, d_.qdim());
-    tr(o.gate_up_w, 2 * d_.I, d_.H);
-    tr(o.down_w, d_.H, d_.I);
+// C[m, n] (+)= sum_k X(m, k) W[k, n] with W MN-major ([k_rows x N] row-major:
+// an activation with tokens as K, or a weight matrix used as dX = dY W) and X
+// MN-major [k_rows x M] or K-major [M x k_rows] -- no transposed copies.
+int DecoderTrainer::gemm_mn(const __nv_bfloat16* X, bool x_kmajor, int M, const __nv_bfloat16* W, int N,
+                            int k_rows, float* out, bool accumulate) {
+  const int K = pad64(k_rows);
+  const CUtensorMap tw = make_tmap_bf16(W, (uint64_t)k_rows, (uint64_t)N, 64);
+  const CUtensorMap tx = x_kmajor ? make_tmap_bf16(X, (uint64_t)M, (uint64_t)k_rows, 128)
+                                  : make_tmap_bf16(X, (uint64_t)k_rows, (uint64_t)M, 64);
+  int splits = 1;
+  const int tok = gemm_mn_plan(M, N, K, sms_, &splits);
+  if ((size_t)((N + 127) / 128) * ((M + tok - 1) / tok) > (size_t)kTileFlags) splits = 1;
+  if (splits > 1 && !accumulate) {  // ordered K slices add into a zeroed output
+    SRL_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)M * N, st_));
+    accumulate = true;
   }
-  tr(lay_.lm_head, d_.V, d_.H);
+  EpiParams e;
+  e.kind = accumulate ? EPI_ACCUM_F32 : EPI_STORE_F32;
+  e.out_f32 = out;
+  e.ld_out = N;
+  e.tile_flags = tile_flags_;
+  const cudaError_t err = gemm_mn_launch(tw, tx, M, N, K, tok, splits, !x_kmajor, e, st_);
+  if (err != cudaSuccess) return cuda_fail(err, "trainer gemm_mn");
+  return SRL_OK;
 }
 
 int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
@@ -360,72 +370,57 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
 
   // ---- backward
   launch_zero(grad_, n_, st);
-  transpose_weights();
   launch_zero(dx_, (size_t)T_max_ * H, st);
+  // Every backward GEMM reads its operands in place: weight gradients take
+  // both operands MN-major (tokens as K), input gradients take W MN-major.
   // pass 2: dlogits per chunk -> d(final xg) and dE(lm_head)
   float* g_lm = grad_ + lay_.lm_head;
   for (int c0 = 0; c0 < T; c0 += chunk_) {
-    const int C = std::min(chunk_, T - c0), Cp = pad64(C);
+    const int C = std::min(chunk_, T - c0);
     // dlogits = coef (onehot - softmax) straight from the LM-head accumulator
-    // (lse of pass 1: same weights, same logits), row-major and transposed
-    if (Cp > C) SRL_CUDA(cudaMemsetAsync(dlogitsT_, 0, sizeof(__nv_bfloat16) * (size_t)V * Cp, st));
+    // (lse of pass 1: same weights, same logits)
     EpiParams e;
     e.kind = EPI_DLOGITS;
     e.ssq_in = ssq_ + (size_t)c0 * parts; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d_.eps;
     e.lse_in = lse_ + c0; e.row_coef = coef_ + c0; e.tgt_row = row_tgt_ + c0;
-    e.out_bf16 = dlogits_; e.ld_bf16 = V; e.outT_bf16 = dlogitsT_; e.ldT = Cp;
+    e.out_bf16 = dlogits_; e.ld_bf16 = V;
     if ((s = gemm(xgF_ + (size_t)c0 * H, C, C, w + lay_.lm_head, V, H, e))) return s;
-    // dzw[t, h] = sum_v dlogits[t, v] E[v, h]   (W-side operand: E^T [H x V])
-    if ((s = gemm_store(dlogits_, C, wt_ + lay_.lm_head, H, V, dz_))) return s;
+    // dzw[t, h] = sum_v dlogits[t, v] E[v, h]
+    if ((s = gemm_mn(dlogits_, true, C, w + lay_.lm_head, H, V, dz_, false))) return s;
     launch_rmsnorm_bwd(dz_, x_ + (size_t)c0 * H, w + lay_.final_norm, rstdF_ + c0, C, H,
                        dx_ + (size_t)c0 * H, grad_ + lay_.final_norm, st);
     // dE[v, h] += sum_t dlogits[t, v] * rstd[t] xg[t, h]
-    SRL_CUDA(cudaMemsetAsync(tB_, 0, sizeof(__nv_bfloat16) * (size_t)H * Cp, st));
-    launch_scale_transpose_bf16(xgF_ + (size_t)c0 * H, rstdF_ + c0, C, H, tB_, Cp, st);
-    if ((s = gemm_accum(dlogitsT_, V, tB_, H, Cp, g_lm))) return s;
+    launch_scale_rows_bf16(xgF_ + (size_t)c0 * H, rstdF_ + c0, C, H, xn_, st);
+    if ((s = gemm_mn(dlogits_, false, V, xn_, H, C, g_lm, true))) return s;
   }
   // layers in reverse; dx_ holds dJ/dx_out of the layer being processed
   for (int l = L - 1; l >= 0; --l) {
     LayerActs& a = acts_[l];
     const LayerOffsets& o = lay_.layers[l];
     // down: x_out = x_mid + act W_down^T
-    launch_f32_to_bf16(dx_, (size_t)T * H, dbig_bf_, st);                      // dY bf16 [T x H]
-    if ((s = gemm_store(dbig_bf_, T, wt_ + o.down_w, I, H, dz_))) return s;   // dact [T x I]
-    SRL_CUDA(cudaMemsetAsync(tA_, 0, sizeof(__nv_bfloat16) * (size_t)H * Tp, st));
-    SRL_CUDA(cudaMemsetAsync(tB_, 0, sizeof(__nv_bfloat16) * (size_t)I * Tp, st));
-    launch_transpose_f32_bf16(dx_, T, H, tA_, Tp, st);                        // dY^T [H x Tp]
-    launch_transpose_bf16(a.act, T, I, tB_, Tp, st);                           // act^T [I x Tp]
-    if ((s = gemm_accum(tA_, H, tB_, I, Tp, grad_ + o.down_w))) return s;     // dW_down [H x I]
+    launch_f32_to_bf16(dx_, (size_t)T * H, dbig_bf_, st);                       // dY bf16 [T x H]
+    if ((s = gemm_mn(dbig_bf_, true, T, w + o.down_w, I, H, dz_, false))) return s;       // dact [T x I]
+    if ((s = gemm_mn(dbig_bf_, false, H, a.act, I, T, grad_ + o.down_w, true))) return s;  // dW_down [H x I]
     // SwiGLU
-    launch_swiglu_bwd(dz_, a.gu, T, I, dbig_bf_, nullptr, st);                 // dgu bf16 [T x 2I]
+    launch_swiglu_bwd(dz_, a.gu, T, I, dbig_bf_, nullptr, st);                  // dgu bf16 [T x 2I]
     // gate_up: gu = rstd2 * (xg2 W_gu^T)
-    if ((s = gemm_store(dbig_bf_, T, wt_ + o.gate_up_w, H, 2 * I, dz_))) return s;  // dzw [T x H]
-    SRL_CUDA(cudaMemsetAsync(tA_, 0, sizeof(__nv_bfloat16) * (size_t)2 * I * Tp, st));
-    SRL_CUDA(cudaMemsetAsync(tB_, 0, sizeof(__nv_bfloat16) * (size_t)H * Tp, st));
-    launch_transpose_bf16(dbig_bf_, T, 2 * I, tA_, Tp, st);                    // dgu^T
-    launch_scale_transpose_bf16(a.xg2, a.rstd2, T, H, tB_, Tp, st);            // xn2^T
-    if ((s = gemm_accum(tA_, 2 * I, tB_, H, Tp, grad_ + o.gate_up_w))) return s;
+    if ((s = gemm_mn(dbig_bf_, true, T, w + o.gate_up_w, H, 2 * I, dz_, false))) return s;  // dzw [T x H]
+    launch_scale_rows_bf16(a.xg2, a.rstd2, T, H, xn_, st);                      // xn2 [T x H]
+    if ((s = gemm_mn(dbig_bf_, false, 2 * I, xn_, H, T, grad_ + o.gate_up_w, true))) return s;
     launch_rmsnorm_bwd(dz_, a.x_mid, w + o.ln2, a.rstd2, T, H, dx_, grad_ + o.ln2, st);
     // O: x_mid = x_in + attn W_o^T   (dx_ now = dJ/dx_mid)
     launch_f32_to_bf16(dx_, (size_t)T * H, dbig_bf_, st);
-    if ((s = gemm_store(dbig_bf_, T, wt_ + o.o_w, qd, H, dz_))) return s;     // dO [T x qd]
-    SRL_CUDA(cudaMemsetAsync(tA_, 0, sizeof(__nv_bfloat16) * (size_t)H * Tp, st));
-    SRL_CUDA(cudaMemsetAsync(tB_, 0, sizeof(__nv_bfloat16) * (size_t)qd * Tp, st));
-    launch_transpose_f32_bf16(dx_, T, H, tA_, Tp, st);
-    launch_transpose_bf16(a.attn, T, qd, tB_, Tp, st);
-    if ((s = gemm_accum(tA_, H, tB_, qd, Tp, grad_ + o.o_w))) return s;
+    if ((s = gemm_mn(dbig_bf_, true, T, w + o.o_w, qd, H, dz_, false))) return s;          // dO [T x qd]
+    if ((s = gemm_mn(dbig_bf_, false, H, a.attn, qd, T, grad_ + o.o_w, true))) return s;   // dW_o [H x qd]
     // attention + RoPE backward -> dqkv (pre-RoPE, pre-bias) fp32
     launch_attention_bwd(a.q, a.attn, dz_, a.lse, kc_ + kv_elems * l, vc_ + kv_elems * l, row_slot_,
                          row_pos_, d_sstart, d_slen, d_bt, pps, T, n_seq, d_.nq, d_.nkv, d_.hd, dbig_, st);
     launch_rope_bwd(dbig_, row_pos_, cos_sin_, T, d_.nq, d_.nkv, d_.hd, st);
     launch_colsum_accum(dbig_, T, qkv, grad_ + o.qkv_b, st);
     launch_f32_to_bf16(dbig_, (size_t)T * qkv, dbig_bf_, st);
-    if ((s = gemm_store(dbig_bf_, T, wt_ + o.qkv_w, H, qkv, dz_))) return s;  // dzw [T x H]
-    SRL_CUDA(cudaMemsetAsync(tA_, 0, sizeof(__nv_bfloat16) * (size_t)qkv * Tp, st));
-    SRL_CUDA(cudaMemsetAsync(tB_, 0, sizeof(__nv_bfloat16) * (size_t)H * Tp, st));
-    launch_transpose_bf16(dbig_bf_, T, qkv, tA_, Tp, st);
-    launch_scale_transpose_bf16(a.xg1, a.rstd1, T, H, tB_, Tp, st);
-    if ((s = gemm_accum(tA_, qkv, tB_, H, Tp, grad_ + o.qkv_w))) return s;
+    if ((s = gemm_mn(dbig_bf_, true, T, w + o.qkv_w, H, qkv, dz_, false))) return s;     // dzw [T x H]
+    launch_scale_rows_bf16(a.xg1, a.rstd1, T, H, xn_, st);
+    if ((s = gemm_mn(dbig_bf_, false, qkv, xn_, H, T, grad_ + o.qkv_w, true))) return s;
     launch_rmsnorm_bwd(dz_, a.x_in, w + o.ln1, a.rstd1, T, H, dx_, grad_ + o.ln1, st);
   }
   launch_embed_bwd(dx_, row_tok_, T, H, grad_ + lay_.embed, st);

@@ -44,7 +44,8 @@ class DecoderTrainer {
            const EpiParams& e);
   int gemm_store(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, float* out);
   int gemm_accum(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, float* out);
-  void transpose_weights();
+  int gemm_mn(const __nv_bfloat16* X, bool x_kmajor, int M, const __nv_bfloat16* W, int N, int k_rows,
+              float* out, bool accumulate);
 
   srl_trainer_options opts_{};
   DecoderDims d_{};
@@ -55,13 +56,12 @@ class DecoderTrainer {
   cudaStream_t st_ = nullptr;
   std::vector<void*> allocs_;
   float *master_ = nullptr, *grad_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;
-  __nv_bfloat16* wt_ = nullptr;  // transposed weights (same offsets)
+  int* tile_flags_ = nullptr;  // ordered split-K counters of gemm_mn (self-resetting)
   std::vector<LayerActs> acts_;
   int chunk_ = 512;  // LM-head rows per pass (trainer.cpp, kLogitChunkMax)
   float *x_ = nullptr, *rstdF_ = nullptr, *ssq_ = nullptr, *pmax_ = nullptr;
   double* psum_ = nullptr;
-  __nv_bfloat16 *xgF_ = nullptr, *dlogits_ = nullptr, *dlogitsT_ = nullptr, *dbig_bf_ = nullptr,
-                *tA_ = nullptr, *tB_ = nullptr;
+  __nv_bfloat16 *xgF_ = nullptr, *dlogits_ = nullptr, *dbig_bf_ = nullptr, *xn_ = nullptr;
   float *dx_ = nullptr, *dz_ = nullptr, *dbig_ = nullptr, *ones_ = nullptr, *coef_ = nullptr,
         *cos_sin_ = nullptr;
   double* lp_ = nullptr;
