@@ -23,6 +23,7 @@ enum EpiKind : int {
   EPI_LOGITS = 5,      // out_f32 = rstd*acc; per (row, 128-col tile): max and fp64 sum exp(x - max)
   EPI_ACCUM_F32 = 6,   // out_f32[m, n] += scale * acc  (gradient accumulation)
   EPI_DLOGITS = 7,     // x = rstd*acc; d = coef[m] * (onehot(tgt[m]) - exp(x - lse[m])) -> bf16
+  EPI_SWIGLU_BWD = 8,  // acc = dact[m, j]: dgu (bf16, gate | up 64-col interleave of gu_in) = SwiGLU'
                        // out_bf16[m, n] and (outT_bf16) the transpose [n, m]
 };
 
@@ -64,6 +65,7 @@ struct EpiParams {
   const float* row_coef = nullptr;
   __nv_bfloat16* outT_bf16 = nullptr;
   __nv_bfloat16* out2_bf16 = nullptr;   // EPI_SWIGLU: also the rstd-scaled gate | up [M x N] (bf16)
+  const __nv_bfloat16* gu_in = nullptr; // EPI_SWIGLU_BWD: gate | up pre-activations [M x 2N]
   int ldT = 0;
   int* tile_flags = nullptr;            // gemm_mn_launch split-K ordering (>= tiles ints, zeroed once)
   // debug: per-CTA %globaltimer phase stamps [ctas x 8] (null = off)
@@ -97,7 +99,7 @@ cudaError_t gemm_big_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M,
 // (make_tmap_bf16(p, K_rows, N, 64)); rows past the map's K read as zero, so
 // K may be rounded up to 64.  x_mn: X is MN-major too ([K x M], 64 x 64
 // boxes), else K-major [M x K] with a box of `tok` rows.  C[m, n] = sum_k
-// X(m, k) W[k, n] through EPI_STORE_F32 / EPI_ACCUM_F32 (no rstd / bias);
+// X(m, k) W[k, n] through EPI_STORE_F32 / EPI_ACCUM_F32 / EPI_SWIGLU_BWD (no rstd / bias);
 // splits > 1 (ordered K slices) needs EPI_ACCUM_F32 and epi.tile_flags.
 int gemm_mn_plan(int M, int N, int K, int num_sms, int* splits);
 cudaError_t gemm_mn_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int tok,

@@ -66,6 +66,12 @@ __device__ __forceinline__ void butterfly_reduce(float (&v)[32], int lane) {
   }
 }
 
+// The direct SwiGLU epilogue stores bf16 pairs: needs whole 128-column tiles
+// and an even act row stride.
+__device__ __forceinline__ bool direct_swiglu_ok(const EpiParams& epi, int N) {
+  return N % 128 == 0 && (epi.ld_bf16 & 1) == 0;
+}
+
 __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
 }
@@ -200,7 +206,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // statistics-only LM head (the trainer's pass 1: no logits stored)
     const bool stats_only = epi.kind == EPI_LOGITS && epi.out_f32 == nullptr;
     const bool direct = epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16 ||
-                        epi.kind == EPI_ACCUM_F32 || epi.kind == EPI_DLOGITS || stats_only;
+                        epi.kind == EPI_ACCUM_F32 || epi.kind == EPI_DLOGITS ||
+                        epi.kind == EPI_SWIGLU_BWD || epi.kind == EPI_RESID ||
+                        (epi.kind == EPI_QKV && 128 % epi.hd == 0) ||
+                        (epi.kind == EPI_SWIGLU && direct_swiglu_ok(epi, N)) || stats_only;
     float* red = tile;  // stats_only: [4 warps][32 tokens] cross-warp partials (the unused staging tile)
     bool waited = false;
     int acc = 0;
@@ -322,6 +331,158 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             continue;
           }
+          if (epi.kind == EPI_RESID) {
+            // resid += acc, xg = bf16(resid * gain); the 32 residual loads in
+            // flight together, the per-token x^2 sum over the tile's 128 columns
+            // by a butterfly transpose (lane l: token l) + the group's 4 warps
+            const bool colok = n < N;
+            const float gain = colok ? gemm_detail::epi_bf2f(epi.gain[n]) : 0.f;
+            float xr[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              xr[j] = (colok && j < jn) ? epi.resid[(size_t)(tc0 + j) * N + n] : 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float x = 0.f;
+              if (colok && j < jn) {
+                const size_t o = (size_t)(tc0 + j) * N + n;
+                x = xr[j] + __uint_as_float(r[j]);
+                epi.resid[o] = x;
+                epi.xg[o] = __float2bfloat16(x * gain);
+              }
+              xr[j] = x * x;
+            }
+            butterfly_reduce<true>(xr, lane);
+            const int q = tid >> 5;
+            red[q * 32 + lane] = xr[0];
+            sync();
+            if (q == 0 && lane < jn)
+              epi.ssq_out[(size_t)(tc0 + lane) * n_tiles + n_tile] =
+                  ((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane];
+            sync();  // red is reused by the next chunk
+            continue;
+          }
+          if (epi.kind == EPI_QKV) {
+            // v = rstd acc + bias staged (RoPE pairs live in other warps); the
+            // row's slot / position / page held by lane j and broadcast; the
+            // cos / sin of 8 tokens in flight together
+            const bool colok = n < N;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float rj = __shfl_sync(0xffffffffu, rs, j);
+              tile[j * kPitch + tid] = (colok && j < jn) ? __uint_as_float(r[j]) * rj + bias : 0.f;
+            }
+            int4 rc = make_int4(-1, 0, 0, 0);
+            if (lane < jn) {
+              rc.x = epi.row_slot[tc0 + lane];
+              rc.y = epi.row_pos[tc0 + lane];
+            }
+            if (rc.x >= 0) {
+              rc.z = epi.block_table[(size_t)rc.x * epi.pages_per_seq + rc.y / 64];
+              rc.w = rc.y % 64;
+            }
+            sync();
+            const int hd = epi.hd, half = hd >> 1;
+            const int qend = epi.nq * hd, kend = (epi.nq + epi.nkv) * hd;
+            const int jj = n % hd, i = jj < half ? jj : jj - half, hb = tid - jj;
+            const bool rot = n < kend;
+#pragma unroll
+            for (int jb = 0; jb < 32; jb += 8) {
+              float co[8], si[8];
+              int4 rr[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                rr[u].x = __shfl_sync(0xffffffffu, rc.x, jb + u);
+                rr[u].y = __shfl_sync(0xffffffffu, rc.y, jb + u);
+                rr[u].z = __shfl_sync(0xffffffffu, rc.z, jb + u);
+                rr[u].w = __shfl_sync(0xffffffffu, rc.w, jb + u);
+                co[u] = 1.f;
+                si[u] = 0.f;
+                if (rot && colok && rr[u].x >= 0) {
+                  co[u] = epi.cos_sin[(size_t)rr[u].y * hd + i];
+                  si[u] = epi.cos_sin[(size_t)rr[u].y * hd + half + i];
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int j = jb + u, m = tc0 + j;
+                if (!colok || rr[u].x < 0) continue;  // also rows past M (slot -1)
+                const float* row = &tile[j * kPitch + hb];
+                float y;
+                if (rot) {
+                  const float x1 = row[i], x2 = row[i + half];
+                  y = jj < half ? x1 * co[u] - x2 * si[u] : x2 * co[u] + x1 * si[u];
+                } else {
+                  y = row[jj];
+                }
+                const __nv_bfloat16 b = __float2bfloat16(y);
+                if (n < qend) {
+                  epi.q_out[(size_t)m * qend + n] = b;
+                } else {
+                  const int kv = n < kend ? n - qend : n - kend;
+                  const size_t at = (((size_t)rr[u].z * epi.nkv + kv / hd) * 64 + rr[u].w) * hd + jj;
+                  if (n < kend) epi.kc[at] = b;
+                  else epi.vc[at] = b;
+                }
+              }
+            }
+            sync();  // the staged chunk is reused next
+            continue;
+          }
+          if (epi.kind == EPI_SWIGLU) {
+            // tile = 64 gate | 64 up columns: stage rstd-scaled values, then
+            // thread (column pair, 8 tokens) forms act = silu(g) u, bf16x2 stores
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float rj = __shfl_sync(0xffffffffu, rs, j);
+              const float v = __uint_as_float(r[j]) * rj;
+              tile[j * kPitch + tid] = v;
+              if (epi.out2_bf16 && j < jn) epi.out2_bf16[(size_t)(tc0 + j) * N + n] = __float2bfloat16(v);
+            }
+            sync();
+            const int cp = 2 * (tid & 31), jb = (tid >> 5) * 8;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int j = jb + u;
+              if (j >= jn) break;
+              const float2 gg = *reinterpret_cast<const float2*>(&tile[j * kPitch + cp]);
+              const float2 uu = *reinterpret_cast<const float2*>(&tile[j * kPitch + 64 + cp]);
+              const float a0 = gg.x / (1.f + expf(-gg.x)) * uu.x;
+              const float a1 = gg.y / (1.f + expf(-gg.y)) * uu.y;
+              *reinterpret_cast<__nv_bfloat162*>(epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + (n0 >> 1) + cp) =
+                  __floats2bfloat162_rn(a0, a1);
+            }
+            sync();  // the staged chunk is reused next
+            continue;
+          }
+          if (epi.kind == EPI_SWIGLU_BWD) {
+            // column n = act index j of 64-block b: gate at 128 b + (j & 63), up 64 after
+            if (n < N) {
+              const size_t gcol = (size_t)(n >> 6) * 128 + (n & 63);
+              // all 64 gate / up loads in flight before the first store
+              uint16_t gb[32], ub[32];
+              const uint16_t* gu = reinterpret_cast<const uint16_t*>(epi.gu_in);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const size_t row = (size_t)(tc0 + (j < jn ? j : 0)) * epi.ld_bf16;
+                gb[j] = __ldg(gu + row + gcol);
+                ub[j] = __ldg(gu + row + gcol + 64);
+              }
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (j >= jn) continue;
+                const size_t row = (size_t)(tc0 + j) * epi.ld_bf16;
+                const float gv = __bfloat162float(__ushort_as_bfloat16(gb[j]));
+                const float uv = __bfloat162float(__ushort_as_bfloat16(ub[j]));
+                const float da = __uint_as_float(r[j]);
+                const float sg = 1.f / (1.f + expf(-gv));  // as swiglu_bwd_kernel
+                const float silu = gv * sg;
+                epi.out_bf16[row + gcol] = __float2bfloat16(da * uv * (sg * (1.f + gv * (1.f - sg))));
+                epi.out_bf16[row + gcol + 64] = __float2bfloat16(da * silu);
+              }
+            }
+            continue;
+          }
           if (n < N) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -425,7 +586,7 @@ cudaError_t gemm_mn_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, 
                            int splits, bool x_mn, const EpiParams& epi, cudaStream_t stream) {
   if (M < 1 || N < 1 || K < kBK || K % kBK != 0 || splits < 1 || splits > K / kBK)
     return cudaErrorInvalidValue;
-  const bool direct = epi.kind == EPI_ACCUM_F32 || epi.kind == EPI_STORE_F32;
+  const bool direct = epi.kind == EPI_ACCUM_F32 || epi.kind == EPI_STORE_F32 || epi.kind == EPI_SWIGLU_BWD;
   if (!direct || (splits > 1 && (epi.kind != EPI_ACCUM_F32 || epi.tile_flags == nullptr)) ||
       epi.ssq_in != nullptr || epi.bias != nullptr)
     return cudaErrorInvalidValue;

@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstdlib>
 // train_kernels.cu -- non-GEMM kernels of the decoder trainer step (see
 // train.cuh).  Correctness-first CUDA-core implementations; every reduction
@@ -179,37 +180,68 @@ __global__ void __launch_bounds__(kRowThreads)
   }
 }
 
-__global__ void __launch_bounds__(kRowThreads)
-    row_rstd_kernel(const float* __restrict__ x, int H, float eps, float* __restrict__ rstd) {
-  __shared__ float red[33];
-  const int r = blockIdx.x;
-  float s = 0.f;
-  for (int k = threadIdx.x; k < H; k += blockDim.x) {
-    const float v = x[(size_t)r * H + k];
-    s += v * v;
+// One warp per row, float4 loads (H % 4 == 0).
+__global__ void row_rstd_kernel(const float* __restrict__ x, int T, int H, float eps,
+                                float* __restrict__ rstd) {
+  const int lane = threadIdx.x & 31;
+  const int H4 = H / 4;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < T; r += gridDim.x * (blockDim.x >> 5)) {
+    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)r * H);
+    float s = 0.f;
+    for (int k = lane; k < H4; k += 32) {
+      const float4 v = xr[k];
+      s += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) rstd[r] = rsqrtf(s / (float)H + eps);
   }
-  s = block_sum(s, red);
-  if (threadIdx.x == 0) rstd[r] = rsqrtf(s / (float)H + eps);
 }
 
-__global__ void __launch_bounds__(kRowThreads)
-    rmsnorm_bwd_kernel(const float* __restrict__ dzw, const float* __restrict__ x,
-                       const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd, int H,
-                       float* __restrict__ dx, float* __restrict__ dg) {
-  __shared__ float red[33];
-  const int r = blockIdx.x;
-  const float rs = rstd[r];
-  float dr = 0.f;
-  for (int k = threadIdx.x; k < H; k += blockDim.x)
-    dr += dzw[(size_t)r * H + k] * x[(size_t)r * H + k] * __bfloat162float(g[k]);
-  dr = block_sum(dr, red);
-  const float coef = -rs * rs * rs / (float)H * dr;
-  for (int k = threadIdx.x; k < H; k += blockDim.x) {
-    const size_t o = (size_t)r * H + k;
-    const float du = rs * dzw[o];
-    dx[o] += du * __bfloat162float(g[k]) + coef * x[o];
-    atomicAdd(&dg[k], du * x[o]);
+// dx += rstd (g * dzw) - rstd^3 / H * (sum_k dzw x g) x, dg += sum_rows rstd dzw x.
+// One warp per row (float4, H % 4 == 0); the gain gradient is summed per block
+// in shared memory and added to dg once per block.
+__global__ void rmsnorm_bwd_kernel(const float* __restrict__ dzw, const float* __restrict__ x,
+                                   const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd,
+                                   int T, int H, float* __restrict__ dx, float* __restrict__ dg) {
+  extern __shared__ float s_dg[];
+  for (int k = threadIdx.x; k < H; k += blockDim.x) s_dg[k] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int H4 = H / 4;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < T; r += gridDim.x * (blockDim.x >> 5)) {
+    const float4* dz4 = reinterpret_cast<const float4*>(dzw + (size_t)r * H);
+    const float4* x4 = reinterpret_cast<const float4*>(x + (size_t)r * H);
+    float4* dx4 = reinterpret_cast<float4*>(dx + (size_t)r * H);
+    const float rs = rstd[r];
+    float dr = 0.f;
+    for (int k = lane; k < H4; k += 32) {
+      const float4 d = dz4[k], v = x4[k];
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(g + 4 * k);
+      const float2 ga = __bfloat1622float2(g2[0]), gb = __bfloat1622float2(g2[1]);
+      dr += d.x * v.x * ga.x + d.y * v.y * ga.y + d.z * v.z * gb.x + d.w * v.w * gb.y;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dr += __shfl_xor_sync(0xffffffffu, dr, o);
+    const float coef = -rs * rs * rs / (float)H * dr;
+    for (int k = lane; k < H4; k += 32) {
+      const float4 d = dz4[k], v = x4[k];
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(g + 4 * k);
+      const float2 ga = __bfloat1622float2(g2[0]), gb = __bfloat1622float2(g2[1]);
+      float4 o = dx4[k];
+      o.x += rs * d.x * ga.x + coef * v.x;
+      o.y += rs * d.y * ga.y + coef * v.y;
+      o.z += rs * d.z * gb.x + coef * v.z;
+      o.w += rs * d.w * gb.y + coef * v.w;
+      dx4[k] = o;
+      atomicAdd(&s_dg[4 * k], rs * d.x * v.x);
+      atomicAdd(&s_dg[4 * k + 1], rs * d.y * v.y);
+      atomicAdd(&s_dg[4 * k + 2], rs * d.z * v.z);
+      atomicAdd(&s_dg[4 * k + 3], rs * d.w * v.w);
+    }
   }
+  __syncthreads();
+  for (int k = threadIdx.x; k < H; k += blockDim.x) atomicAdd(&dg[k], s_dg[k]);
 }
 
 __global__ void swiglu_bwd_kernel(const float* __restrict__ dact, const __nv_bfloat16* __restrict__ gu,
@@ -408,6 +440,16 @@ __global__ void adam_kernel(float* __restrict__ master, __nv_bfloat16* __restric
   }
 }
 
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
 int grid_for(size_t n, int threads) {
   size_t b = (n + threads - 1) / threads;
   return (int)(b > 8192 ? 8192 : (b < 1 ? 1 : b));
@@ -459,10 +501,12 @@ void launch_loss_dlogits(const float* logits, const float* pmax, const double* p
 }
 void launch_rmsnorm_bwd(const float* dzw, const float* x, const __nv_bfloat16* g,
                         const float* rstd, int T, int H, float* dx, float* dg, cudaStream_t st) {
-  if (T > 0) rmsnorm_bwd_kernel<<<T, kRowThreads, 0, st>>>(dzw, x, g, rstd, H, dx, dg);
+  if (T < 1) return;
+  const int blocks = std::min((T + 7) / 8, 2 * num_sms());
+  rmsnorm_bwd_kernel<<<blocks, 256, sizeof(float) * H, st>>>(dzw, x, g, rstd, T, H, dx, dg);
 }
 void launch_row_rstd(const float* x, int T, int H, float eps, float* rstd, cudaStream_t st) {
-  if (T > 0) row_rstd_kernel<<<T, kRowThreads, 0, st>>>(x, H, eps, rstd);
+  if (T > 0) row_rstd_kernel<<<(T + 7) / 8, 256, 0, st>>>(x, T, H, eps, rstd);
 }
 void launch_swiglu_bwd(const float* dact, const __nv_bfloat16* gu, int T, int I, __nv_bfloat16* dgu,
                        float* dgu_f32, cudaStream_t st) {

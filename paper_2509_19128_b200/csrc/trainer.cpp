@@ -137,7 +137,7 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
       (st = alloc(&dz_, (size_t)T_max_ * std::max(H, 2 * I))) ||
       (st = alloc(&dbig_, (size_t)T_max_ * std::max({2 * I, qkv, qd}))) ||
       (st = alloc(&dbig_bf_, (size_t)T_max_ * std::max({2 * I, qkv, qd, H}))) ||
-      (st = alloc(&xn_, (size_t)T_max_ * H)) ||
+      (st = alloc(&xn_, (size_t)T_max_ * H)) || (st = alloc(&dgu_, (size_t)T_max_ * 2 * I)) ||
       (st = alloc(&ones_, T_max_)) || (st = alloc(&row_slot_, T_max_)) ||
       (st = alloc(&row_pos_, T_max_)) || (st = alloc(&row_tok_, T_max_)) ||
       (st = alloc(&row_tgt_, T_max_)) || (st = alloc(&coef_, T_max_)) ||
@@ -194,6 +194,31 @@ int DecoderTrainer::gemm_accum(const __nv_bfloat16* X, int M, const __nv_bfloat1
 // C[m, n] (+)= sum_k X(m, k) W[k, n] with W MN-major ([k_rows x N] row-major:
 // an activation with tokens as K, or a weight matrix used as dX = dY W) and X
 // MN-major [k_rows x M] or K-major [M x k_rows] -- no transposed copies.
+// dgu = SwiGLU'(gu) applied to dact = dY W (W MN-major [k_rows x I]): fused
+// into the GEMM epilogue when the plan needs no K slices, else through dz_.
+int DecoderTrainer::gemm_swiglu_bwd(const __nv_bfloat16* dY, int M, const __nv_bfloat16* W, int I, int k_rows,
+                                    const __nv_bfloat16* gu, __nv_bfloat16* dgu) {
+  const int K = pad64(k_rows);
+  int splits = 1;
+  const int tok = gemm_mn_plan(M, I, K, sms_, &splits);
+  if (splits > 1) {
+    int s = gemm_mn(dY, true, M, W, I, k_rows, dz_, false);
+    if (s) return s;
+    launch_swiglu_bwd(dz_, gu, M, I, dgu, nullptr, st_);
+    return SRL_OK;
+  }
+  const CUtensorMap tw = make_tmap_bf16(W, (uint64_t)k_rows, (uint64_t)I, 64);
+  const CUtensorMap tx = make_tmap_bf16(dY, (uint64_t)M, (uint64_t)k_rows, 128);
+  EpiParams e;
+  e.kind = EPI_SWIGLU_BWD;
+  e.gu_in = gu;
+  e.out_bf16 = dgu;
+  e.ld_bf16 = 2 * I;
+  const cudaError_t err = gemm_mn_launch(tw, tx, M, I, K, tok, 1, false, e, st_);
+  if (err != cudaSuccess) return cuda_fail(err, "trainer gemm_swiglu_bwd");
+  return SRL_OK;
+}
+
 int DecoderTrainer::gemm_mn(const __nv_bfloat16* X, bool x_kmajor, int M, const __nv_bfloat16* W, int N,
                             int k_rows, float* out, bool accumulate) {
   const int K = pad64(k_rows);
@@ -399,14 +424,13 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
     const LayerOffsets& o = lay_.layers[l];
     // down: x_out = x_mid + act W_down^T
     launch_f32_to_bf16(dx_, (size_t)T * H, dbig_bf_, st);                       // dY bf16 [T x H]
-    if ((s = gemm_mn(dbig_bf_, true, T, w + o.down_w, I, H, dz_, false))) return s;       // dact [T x I]
     if ((s = gemm_mn(dbig_bf_, false, H, a.act, I, T, grad_ + o.down_w, true))) return s;  // dW_down [H x I]
-    // SwiGLU
-    launch_swiglu_bwd(dz_, a.gu, T, I, dbig_bf_, nullptr, st);                  // dgu bf16 [T x 2I]
+    // dact [T x I] = dY W_down, SwiGLU backward in its epilogue -> dgu bf16 [T x 2I]
+    if ((s = gemm_swiglu_bwd(dbig_bf_, T, w + o.down_w, I, H, a.gu, dgu_))) return s;
     // gate_up: gu = rstd2 * (xg2 W_gu^T)
-    if ((s = gemm_mn(dbig_bf_, true, T, w + o.gate_up_w, H, 2 * I, dz_, false))) return s;  // dzw [T x H]
+    if ((s = gemm_mn(dgu_, true, T, w + o.gate_up_w, H, 2 * I, dz_, false))) return s;  // dzw [T x H]
     launch_scale_rows_bf16(a.xg2, a.rstd2, T, H, xn_, st);                      // xn2 [T x H]
-    if ((s = gemm_mn(dbig_bf_, false, 2 * I, xn_, H, T, grad_ + o.gate_up_w, true))) return s;
+    if ((s = gemm_mn(dgu_, false, 2 * I, xn_, H, T, grad_ + o.gate_up_w, true))) return s;
     launch_rmsnorm_bwd(dz_, a.x_mid, w + o.ln2, a.rstd2, T, H, dx_, grad_ + o.ln2, st);
     // O: x_mid = x_in + attn W_o^T   (dx_ now = dJ/dx_mid)
     launch_f32_to_bf16(dx_, (size_t)T * H, dbig_bf_, st);

@@ -46,6 +46,8 @@ class DecoderTrainer {
   int gemm_accum(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, float* out);
   int gemm_mn(const __nv_bfloat16* X, bool x_kmajor, int M, const __nv_bfloat16* W, int N, int k_rows,
               float* out, bool accumulate);
+  int gemm_swiglu_bwd(const __nv_bfloat16* dY, int M, const __nv_bfloat16* W, int I, int k_rows,
+                      const __nv_bfloat16* gu, __nv_bfloat16* dgu);
 
   srl_trainer_options opts_{};
   DecoderDims d_{};
@@ -61,7 +63,8 @@ class DecoderTrainer {
   int chunk_ = 512;  // LM-head rows per pass (trainer.cpp, kLogitChunkMax)
   float *x_ = nullptr, *rstdF_ = nullptr, *ssq_ = nullptr, *pmax_ = nullptr;
   double* psum_ = nullptr;
-  __nv_bfloat16 *xgF_ = nullptr, *dlogits_ = nullptr, *dbig_bf_ = nullptr, *xn_ = nullptr;
+  __nv_bfloat16 *xgF_ = nullptr, *dlogits_ = nullptr, *dbig_bf_ = nullptr, *xn_ = nullptr,
+                *dgu_ = nullptr;
   float *dx_ = nullptr, *dz_ = nullptr, *dbig_ = nullptr, *ones_ = nullptr, *coef_ = nullptr,
         *cos_sin_ = nullptr;
   double* lp_ = nullptr;
