@@ -15,536 +15,42 @@
 //     128 TMEM lanes) take alternate 32-token chunks, stage them in shared
 //     memory and run gemm_epi.cuh on them.
 // No split-K: it is chosen only when the tile count fills the machine.
-#include <cstdio>
-
-#include "gemm.cuh"
-#include "gemm_epi.cuh"
-#include "sm100.cuh"
+#include "gemm_big_impl.cuh"
 
 namespace srl {
-using namespace sm100;
+using bigk::launch_big;
 
 namespace {
-
-constexpr int kBN = 128;  // weight rows per tile (UMMA M)
-constexpr int kBK = 64;   // k-block (128-B swizzle row)
-constexpr int kThreads = 384;
-constexpr int kChunk = 32;  // tokens per epilogue chunk
-constexpr int kPitch = kBN;  // drain writes are lane-contiguous: no padding needed
-
-template <int TOK>
-struct BigLayout {
-  static constexpr int STAGES = TOK == 256 ? 4 : 6;
-  static constexpr int kABytes = kBN * kBK * 2;
-  static constexpr int kBBytes = TOK * kBK * 2;
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kRing = STAGES * kStageBytes;
-  static constexpr int kEpi = kRing;                               // [2][kChunk][kPitch] fp32
-  static constexpr int kRstd = kEpi + 2 * kChunk * kPitch * 4;     // [2][kChunk] fp32
-  static constexpr int kRow = kRstd + 2 * kChunk * 4;              // [2][kChunk] int4
-  static constexpr int kBar = kRow + 2 * kChunk * 16;
-  static constexpr int kMisc = kBar + (2 * STAGES + 4) * 8;
-  static constexpr int kTotal = kMisc + 16;
-  static constexpr int kAlloc = kTotal + 1024;
-  static_assert(kAlloc <= 232448, "shared memory budget");
-};
-
-// 32 values per lane -> lane l holds the reduction over the warp's lanes of
-// value l (recursive halving: 16 + 8 + 4 + 2 + 1 shuffles).  Sum or max.
-template <bool kSum>
-__device__ __forceinline__ void butterfly_reduce(float (&v)[32], int lane) {
-#pragma unroll
-  for (int w = 16; w >= 1; w >>= 1) {
-    const bool upper = (lane & w) != 0;
-#pragma unroll
-    for (int i = 0; i < w; ++i) {
-      const float send = upper ? v[i] : v[i + w];
-      const float keep = upper ? v[i + w] : v[i];
-      const float got = __shfl_xor_sync(0xffffffffu, send, w);
-      v[i] = kSum ? keep + got : fmaxf(keep, got);
-    }
-  }
-}
-
-// The direct SwiGLU epilogue stores bf16 pairs: needs whole 128-column tiles
-// and an even act row stride.
-__device__ __forceinline__ bool direct_swiglu_ok(const EpiParams& epi, int N) {
-  return N % 128 == 0 && (epi.ld_bf16 & 1) == 0;
-}
-
-__device__ __forceinline__ void group_sync(int g) {
-  asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
-}
-
-// AMN / BMN: the W / X operand is MN-major (given as [K x N] / [K x M]
-// row-major, e.g. the trainer's dW = dY^T X with the token axis as K, or
-// dX = dY W with W's rows as K): 64 x 64 TMA boxes, UMMA descriptors with
-// the 64-element MN groups 8 KB apart.  `splits` > 1 cuts K into
-// ordered slices whose EPI_ACCUM epilogues add into the output one after the
-// other (per-tile counters in epi.tile_flags, self-resetting): deterministic
-// split-K for the small-output, long-K weight gradients.
 template <int TOK, bool AMN, bool BMN>
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_big_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
-                    int M, int N, int K, int splits, const EpiParams epi) {
-  using L = BigLayout<TOK>;
-  constexpr int STAGES = L::STAGES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kMisc);
-
-  const int warp = threadIdx.x >> 5;
-  const int n_tiles = (N + kBN - 1) / kBN;
-  const int tok_tiles = (M + TOK - 1) / TOK;
-  const int tiles = n_tiles * tok_tiles;
-  const int total = tiles * splits;
-  const int kbt = K / kBK;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      tma_prefetch_desc(&tw);
-      tma_prefetch_desc(&tx);
+cudaError_t by_kind(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int splits,
+                    const EpiParams& epi, cudaStream_t stream) {
+  if constexpr (!AMN) {
+    switch (epi.kind) {
+      case 0: return launch_big<TOK, false, false, 0>(tw, tx, M, N, K, splits, epi, stream);
+      case 1: return launch_big<TOK, false, false, 1>(tw, tx, M, N, K, splits, epi, stream);
+      case 2: return launch_big<TOK, false, false, 2>(tw, tx, M, N, K, splits, epi, stream);
+      case 3: return launch_big<TOK, false, false, 3>(tw, tx, M, N, K, splits, epi, stream);
+      case 4: return launch_big<TOK, false, false, 4>(tw, tx, M, N, K, splits, epi, stream);
+      case 5: return launch_big<TOK, false, false, 5>(tw, tx, M, N, K, splits, epi, stream);
+      case 6: return launch_big<TOK, false, false, 6>(tw, tx, M, N, K, splits, epi, stream);
+      case 7: return launch_big<TOK, false, false, 7>(tw, tx, M, N, K, splits, epi, stream);
+      default: return cudaErrorInvalidValue;
     }
-    __syncwarp();
-    tmem_alloc<2 * TOK>(tmem_slot);
-  } else if (warp == 1) {
-    if (elect_one()) {
-      for (int s = 0; s < STAGES; ++s) {
-        mbar_init(&full[s], 1);
-        mbar_init(&empty[s], 1);
-      }
-      for (int a = 0; a < 2; ++a) {
-        mbar_init(&tfull[a], 1);
-        mbar_init(&tempty[a], 256);  // every epilogue thread, after its last TMEM load
-      }
-      fence_barrier_init();
+  } else if constexpr (BMN) {
+    switch (epi.kind) {
+      case 0: return launch_big<TOK, true, true, 0>(tw, tx, M, N, K, splits, epi, stream);
+      case 6: return launch_big<TOK, true, true, 6>(tw, tx, M, N, K, splits, epi, stream);
+      default: return cudaErrorInvalidValue;
     }
-    __syncwarp();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  griddep_launch_dependents();
-
-  if (warp == 0) {
-    if (elect_one()) {  // ---- TMA producer
-      griddep_wait();   // the activations come from the previous kernel
-      int stage = 0;
-      uint32_t ph = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int tile = t % tiles, sp = t / tiles;
-        const int n0 = (tile % n_tiles) * kBN, t0 = (tile / n_tiles) * TOK;
-        for (int kb = sp * kbt / splits; kb < (sp + 1) * kbt / splits; ++kb) {
-          mbar_wait(&empty[stage], ph ^ 1);
-          uint8_t* a = smem + stage * L::kStageBytes;
-          mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
-          if constexpr (AMN) {  // 64 x 64 boxes: [k rows][64 MN columns], 8 KB each
-            tma_load_2d(a, &tw, &full[stage], n0, kb * kBK);
-            tma_load_2d(a + 8192, &tw, &full[stage], n0 + 64, kb * kBK);
-          } else {
-            tma_load_2d(a, &tw, &full[stage], kb * kBK, n0);
-          }
-          if constexpr (BMN) {
-#pragma unroll
-            for (int h = 0; h < TOK / 64; ++h)
-              tma_load_2d(a + L::kABytes + h * 8192, &tx, &full[stage], t0 + h * 64, kb * kBK);
-          } else {
-#pragma unroll
-            for (int h = 0; h < TOK / 128; ++h)  // the X map's box is 128 rows
-              tma_load_2d(a + L::kABytes + h * 128 * 128, &tx, &full[stage], kb * kBK, t0 + h * 128);
-          }
-          if (++stage == STAGES) { stage = 0; ph ^= 1; }
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    if (elect_one()) {  // ---- MMA issuer
-      constexpr uint32_t idesc = idesc_bf16_f32(128, TOK) | (AMN ? idesc_a_mn_major : 0u) |
-                                 (BMN ? idesc_b_mn_major : 0u);
-      int stage = 0, acc = 0;
-      uint32_t ph = 0, aph = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        mbar_wait(&tempty[acc], aph ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + acc * TOK;
-        const int sp = t / tiles, kb0 = sp * kbt / splits;
-        for (int kb = kb0; kb < (sp + 1) * kbt / splits; ++kb) {
-          mbar_wait(&full[stage], ph);
-          tc_fence_after();
-          const uint32_t a = smem_u32(smem + stage * L::kStageBytes);
-          const uint32_t b = a + L::kABytes;
-#pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk) {
-            // MN-major: 16 k rows = two 1-KB swizzle atoms; K-major: 32 B inside the atom
-            const uint64_t da = AMN ? umma_desc_mn_sw128(a + kk * 2048, 8192) : umma_desc_k_sw128(a, kk * 32);
-            const uint64_t db = BMN ? umma_desc_mn_sw128(b + kk * 2048, 8192) : umma_desc_k_sw128(b, kk * 32);
-            mma_bf16_ss(d, da, db, idesc, (kb != kb0) || kk != 0);
-          }
-          mma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; ph ^= 1; }
-        }
-        mma_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; aph ^= 1; }
-      }
-    }
-    __syncwarp();
-  } else if (warp >= 4) {
-    // ---- epilogue: group g (warps 4-7 / 8-11), TMEM lane quadrant q
-    const int g = (warp - 4) >> 2, q = warp & 3;
-    const int tid = q * 32 + (threadIdx.x & 31);  // = the TMEM lane = the tile column drained
-    float* tile = reinterpret_cast<float*>(smem + L::kEpi) + g * kChunk * kPitch;
-    float* s_rstd = reinterpret_cast<float*>(smem + L::kRstd) + g * kChunk;
-    int4* s_row = reinterpret_cast<int4*>(smem + L::kRow) + g * kChunk;
-    auto sync = [g] { group_sync(g); };
-    // statistics-only LM head (the trainer's pass 1: no logits stored)
-    const bool stats_only = epi.kind == EPI_LOGITS && epi.out_f32 == nullptr;
-    const bool direct = epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16 ||
-                        epi.kind == EPI_ACCUM_F32 || epi.kind == EPI_DLOGITS ||
-                        epi.kind == EPI_SWIGLU_BWD || epi.kind == EPI_RESID ||
-                        (epi.kind == EPI_QKV && 128 % epi.hd == 0) ||
-                        (epi.kind == EPI_SWIGLU && direct_swiglu_ok(epi, N)) || stats_only;
-    float* red = tile;  // stats_only: [4 warps][32 tokens] cross-warp partials (the unused staging tile)
-    bool waited = false;
-    int acc = 0;
-    uint32_t aph = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const int otile = t % tiles, sp = t / tiles;
-      const int n_tile = otile % n_tiles, n0 = n_tile * kBN, t0 = (otile / n_tiles) * TOK;
-      mbar_wait(&tfull[acc], aph);
-      tc_fence_after();
-      if (!waited) {  // epilogue inputs (residual, ssq) come from earlier kernels
-        griddep_wait();
-        waited = true;
-      }
-      if (splits > 1 && sp > 0) {  // K slice sp adds after slices 0..sp-1 (both groups each)
-        if (tid == 0) {
-          while (ld_acquire_gpu(epi.tile_flags + otile) < 2 * sp) __nanosleep(64);
-        }
-        sync();
-      }
-      const int last = TOK / kChunk - 2 + g;  // this group's last chunk of the tile
-      for (int c = g; c < TOK / kChunk; c += 2) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem + acc * TOK + c * kChunk + ((uint32_t)(q * 32) << 16), r);
-        tmem_ld_wait();
-        if (c == last) {  // accumulator drained by this thread
-          tc_fence_before();
-          mbar_arrive(&tempty[acc]);
-        }
-        const int tc0 = t0 + c * kChunk;
-        if (tc0 >= M) continue;  // rows past M: nothing to store (uniform per group)
-        if (direct) {
-          // plain stores straight from the accumulator registers: thread =
-          // output column n, so each warp store covers 32 consecutive columns
-          const int n = n0 + tid;
-          const int lane = threadIdx.x & 31;
-          float rs = 1.f;  // rstd of token tc0 + lane, broadcast below
-          if (epi.ssq_in != nullptr && tc0 + lane < M) {
-            const float sacc = gemm_detail::ssq_row_sum(epi.ssq_in + (size_t)(tc0 + lane) * epi.ssq_in_parts,
-                                                        epi.ssq_in_parts);
-            rs = rsqrtf(sacc * epi.inv_dim + epi.eps);
-          }
-          const float bias = (epi.bias != nullptr && n < N) ? gemm_detail::epi_bf2f(epi.bias[n]) : 0.f;
-          const int jn = min(32, M - tc0);
-          if (stats_only) {
-            // per token: the target's logit, and over this tile's 128 columns
-            // the max and the sum of exp(x - max) (fp32 exp, fp64 combine).
-            // Each warp reduces its 32 columns for all 32 tokens at once with a
-            // butterfly transpose (31 shuffles, lane l ends with token l), the
-            // group's four warps combine through shared memory.
-            int tg = -1;
-            if (epi.tgt_row && tc0 + lane < M) tg = epi.tgt_row[tc0 + lane];
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float rj = __shfl_sync(0xffffffffu, rs, j);
-              const int tj = __shfl_sync(0xffffffffu, tg, j);
-              v[j] = n < N && j < jn ? __uint_as_float(r[j]) * rj : -INFINITY;
-              if (n == tj && j < jn) epi.tgt_out[tc0 + j] = v[j];
-            }
-            float mx[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) mx[j] = v[j];
-            butterfly_reduce<false>(mx, lane);  // lane l: max of token l over this warp's columns
-            const int q = tid >> 5;
-            red[q * 32 + lane] = mx[0];
-            sync();
-            float M_l = red[lane];
-#pragma unroll
-            for (int w = 1; w < 4; ++w) M_l = fmaxf(M_l, red[w * 32 + lane]);
-            float e[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float Mj = __shfl_sync(0xffffffffu, M_l, j);
-              e[j] = v[j] == -INFINITY ? 0.f : __expf(v[j] - Mj);
-            }
-            butterfly_reduce<true>(e, lane);  // lane l: this warp's sum for token l
-            sync();  // everyone has read the maxima
-            red[q * 32 + lane] = e[0];
-            sync();
-            if (q == 0 && lane < jn) {
-              const double sum = (double)red[lane] + (double)red[32 + lane] + (double)red[64 + lane] +
-                                 (double)red[96 + lane];
-              epi.part_max[(size_t)(tc0 + lane) * n_tiles + n_tile] = M_l;
-              epi.part_sum[(size_t)(tc0 + lane) * n_tiles + n_tile] = M_l == -INFINITY ? 0.0 : sum;
-            }
-            sync();  // red is reused by the next chunk
-            continue;
-          }
-          if (epi.kind == EPI_DLOGITS) {
-            // d = coef * (onehot - softmax) of token tc0 + j at vocab column n; the
-            // transposed copy [n][tokens] is 32 contiguous bf16 per thread
-            float lse = 0.f, cf = 0.f;
-            int tg = -1;
-            if (tc0 + lane < M) {
-              lse = (float)epi.lse_in[tc0 + lane];
-              cf = epi.row_coef[tc0 + lane];
-              tg = epi.tgt_row[tc0 + lane];
-            }
-            uint32_t packed[16];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float rj = __shfl_sync(0xffffffffu, rs, j);
-              const float lj = __shfl_sync(0xffffffffu, lse, j);
-              const float cj = __shfl_sync(0xffffffffu, cf, j);
-              const int tj = __shfl_sync(0xffffffffu, tg, j);
-              const float x = __uint_as_float(r[j]) * rj;
-              const float d = j < jn ? cj * ((n == tj ? 1.f : 0.f) - __expf(x - lj)) : 0.f;
-              const __nv_bfloat16 b = __float2bfloat16(d);
-              if (j < jn && n < N) epi.out_bf16[(size_t)(tc0 + j) * epi.ld_bf16 + n] = b;
-              const uint32_t bits = (uint32_t)__bfloat16_as_ushort(b);
-              if (j & 1) packed[j >> 1] |= bits << 16;
-              else packed[j >> 1] = bits;
-            }
-            if (epi.outT_bf16 && n < N) {  // columns past M are written as 0 (padding)
-              uint4* dst = reinterpret_cast<uint4*>(epi.outT_bf16 + (size_t)n * epi.ldT + tc0);
-#pragma unroll
-              for (int v = 0; v < 4; ++v)
-                dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
-            }
-            continue;
-          }
-          if (epi.kind == EPI_RESID) {
-            // resid += acc, xg = bf16(resid * gain); the 32 residual loads in
-            // flight together, the per-token x^2 sum over the tile's 128 columns
-            // by a butterfly transpose (lane l: token l) + the group's 4 warps
-            const bool colok = n < N;
-            const float gain = colok ? gemm_detail::epi_bf2f(epi.gain[n]) : 0.f;
-            float xr[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              xr[j] = (colok && j < jn) ? epi.resid[(size_t)(tc0 + j) * N + n] : 0.f;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              float x = 0.f;
-              if (colok && j < jn) {
-                const size_t o = (size_t)(tc0 + j) * N + n;
-                x = xr[j] + __uint_as_float(r[j]);
-                epi.resid[o] = x;
-                epi.xg[o] = __float2bfloat16(x * gain);
-              }
-              xr[j] = x * x;
-            }
-            butterfly_reduce<true>(xr, lane);
-            const int q = tid >> 5;
-            red[q * 32 + lane] = xr[0];
-            sync();
-            if (q == 0 && lane < jn)
-              epi.ssq_out[(size_t)(tc0 + lane) * n_tiles + n_tile] =
-                  ((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane];
-            sync();  // red is reused by the next chunk
-            continue;
-          }
-          if (epi.kind == EPI_QKV) {
-            // v = rstd acc + bias staged (RoPE pairs live in other warps); the
-            // row's slot / position / page held by lane j and broadcast; the
-            // cos / sin of 8 tokens in flight together
-            const bool colok = n < N;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float rj = __shfl_sync(0xffffffffu, rs, j);
-              tile[j * kPitch + tid] = (colok && j < jn) ? __uint_as_float(r[j]) * rj + bias : 0.f;
-            }
-            int4 rc = make_int4(-1, 0, 0, 0);
-            if (lane < jn) {
-              rc.x = epi.row_slot[tc0 + lane];
-              rc.y = epi.row_pos[tc0 + lane];
-            }
-            if (rc.x >= 0) {
-              rc.z = epi.block_table[(size_t)rc.x * epi.pages_per_seq + rc.y / 64];
-              rc.w = rc.y % 64;
-            }
-            sync();
-            const int hd = epi.hd, half = hd >> 1;
-            const int qend = epi.nq * hd, kend = (epi.nq + epi.nkv) * hd;
-            const int jj = n % hd, i = jj < half ? jj : jj - half, hb = tid - jj;
-            const bool rot = n < kend;
-#pragma unroll
-            for (int jb = 0; jb < 32; jb += 8) {
-              float co[8], si[8];
-              int4 rr[8];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                rr[u].x = __shfl_sync(0xffffffffu, rc.x, jb + u);
-                rr[u].y = __shfl_sync(0xffffffffu, rc.y, jb + u);
-                rr[u].z = __shfl_sync(0xffffffffu, rc.z, jb + u);
-                rr[u].w = __shfl_sync(0xffffffffu, rc.w, jb + u);
-                co[u] = 1.f;
-                si[u] = 0.f;
-                if (rot && colok && rr[u].x >= 0) {
-                  co[u] = epi.cos_sin[(size_t)rr[u].y * hd + i];
-                  si[u] = epi.cos_sin[(size_t)rr[u].y * hd + half + i];
-                }
-              }
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const int j = jb + u, m = tc0 + j;
-                if (!colok || rr[u].x < 0) continue;  // also rows past M (slot -1)
-                const float* row = &tile[j * kPitch + hb];
-                float y;
-                if (rot) {
-                  const float x1 = row[i], x2 = row[i + half];
-                  y = jj < half ? x1 * co[u] - x2 * si[u] : x2 * co[u] + x1 * si[u];
-                } else {
-                  y = row[jj];
-                }
-                const __nv_bfloat16 b = __float2bfloat16(y);
-                if (n < qend) {
-                  epi.q_out[(size_t)m * qend + n] = b;
-                } else {
-                  const int kv = n < kend ? n - qend : n - kend;
-                  const size_t at = (((size_t)rr[u].z * epi.nkv + kv / hd) * 64 + rr[u].w) * hd + jj;
-                  if (n < kend) epi.kc[at] = b;
-                  else epi.vc[at] = b;
-                }
-              }
-            }
-            sync();  // the staged chunk is reused next
-            continue;
-          }
-          if (epi.kind == EPI_SWIGLU) {
-            // tile = 64 gate | 64 up columns: stage rstd-scaled values, then
-            // thread (column pair, 8 tokens) forms act = silu(g) u, bf16x2 stores
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float rj = __shfl_sync(0xffffffffu, rs, j);
-              const float v = __uint_as_float(r[j]) * rj;
-              tile[j * kPitch + tid] = v;
-              if (epi.out2_bf16 && j < jn) epi.out2_bf16[(size_t)(tc0 + j) * N + n] = __float2bfloat16(v);
-            }
-            sync();
-            const int cp = 2 * (tid & 31), jb = (tid >> 5) * 8;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int j = jb + u;
-              if (j >= jn) break;
-              const float2 gg = *reinterpret_cast<const float2*>(&tile[j * kPitch + cp]);
-              const float2 uu = *reinterpret_cast<const float2*>(&tile[j * kPitch + 64 + cp]);
-              const float a0 = gg.x / (1.f + expf(-gg.x)) * uu.x;
-              const float a1 = gg.y / (1.f + expf(-gg.y)) * uu.y;
-              *reinterpret_cast<__nv_bfloat162*>(epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + (n0 >> 1) + cp) =
-                  __floats2bfloat162_rn(a0, a1);
-            }
-            sync();  // the staged chunk is reused next
-            continue;
-          }
-          if (epi.kind == EPI_SWIGLU_BWD) {
-            // column n = act index j of 64-block b: gate at 128 b + (j & 63), up 64 after
-            if (n < N) {
-              const size_t gcol = (size_t)(n >> 6) * 128 + (n & 63);
-              // all 64 gate / up loads in flight before the first store
-              uint16_t gb[32], ub[32];
-              const uint16_t* gu = reinterpret_cast<const uint16_t*>(epi.gu_in);
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const size_t row = (size_t)(tc0 + (j < jn ? j : 0)) * epi.ld_bf16;
-                gb[j] = __ldg(gu + row + gcol);
-                ub[j] = __ldg(gu + row + gcol + 64);
-              }
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                if (j >= jn) continue;
-                const size_t row = (size_t)(tc0 + j) * epi.ld_bf16;
-                const float gv = __bfloat162float(__ushort_as_bfloat16(gb[j]));
-                const float uv = __bfloat162float(__ushort_as_bfloat16(ub[j]));
-                const float da = __uint_as_float(r[j]);
-                const float sg = 1.f / (1.f + expf(-gv));  // as swiglu_bwd_kernel
-                const float silu = gv * sg;
-                epi.out_bf16[row + gcol] = __float2bfloat16(da * uv * (sg * (1.f + gv * (1.f - sg))));
-                epi.out_bf16[row + gcol + 64] = __float2bfloat16(da * silu);
-              }
-            }
-            continue;
-          }
-          if (n < N) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float rj = __shfl_sync(0xffffffffu, rs, j);
-              if (j >= jn) continue;
-              const float v = __uint_as_float(r[j]);
-              const size_t m = (size_t)(tc0 + j);
-              if (epi.kind == EPI_STORE_F32) epi.out_f32[m * epi.ld_out + n] = v * rj + bias;
-              else if (epi.kind == EPI_STORE_BF16) epi.out_bf16[m * epi.ld_bf16 + n] = __float2bfloat16(v * rj + bias);
-              else epi.out_f32[m * epi.ld_out + n] += epi.scale * v;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) (void)__shfl_sync(0xffffffffu, rs, j);
-          }
-          continue;
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) tile[j * kPitch + tid] = __uint_as_float(r[j]);
-        gemm_detail::epi_row_meta(epi, 0, kChunk, tc0, M, s_rstd, s_row, tid, 128);
-        sync();
-        gemm_detail::epi_apply(epi, tile, kPitch, 0, kChunk, tc0, n0, n_tile, n_tiles, M, N, s_rstd,
-                               s_row, tid, 128, sync);
-        sync();  // the staged chunk is reused next
-      }
-      if (splits > 1) {
-        __threadfence();
-        sync();
-        if (tid == 0 && atomicAdd(epi.tile_flags + otile, 1) == 2 * splits - 1)
-          atomicExch(epi.tile_flags + otile, 0);  // last slice: reset for the next launch
-      }
-      if (++acc == 2) { acc = 0; aph ^= 1; }
+  } else {
+    switch (epi.kind) {
+      case 0: return launch_big<TOK, true, false, 0>(tw, tx, M, N, K, splits, epi, stream);
+      case 6: return launch_big<TOK, true, false, 6>(tw, tx, M, N, K, splits, epi, stream);
+      case 8: return launch_big<TOK, true, false, 8>(tw, tx, M, N, K, splits, epi, stream);
+      default: return cudaErrorInvalidValue;
     }
   }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_free<2 * TOK>(tmem);
 }
-
-int num_sms_cached() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
-}
-
-template <int TOK, bool AMN, bool BMN>
-cudaError_t launch_big(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int splits,
-                       const EpiParams& epi, cudaStream_t stream) {
-  using L = BigLayout<TOK>;
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      gemm_big_kernel<TOK, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
-  if (attr != cudaSuccess) return attr;
-  const int tiles = ((N + kBN - 1) / kBN) * ((M + TOK - 1) / TOK) * splits;
-  const int grid = tiles < num_sms_cached() ? tiles : num_sms_cached();
-  return launch_pdl(gemm_big_kernel<TOK, AMN, BMN>, dim3(grid), dim3(kThreads), (size_t)L::kAlloc, stream,
-                    dim3(1, 1, 1), tw, tx, M, N, K, splits, epi);
-}
-
 }  // namespace
 
 // Measured on B200 (tools/gemm_bench.py, Qwen2.5 0.5B/1.5B/7B shapes,
@@ -554,7 +60,7 @@ cudaError_t launch_big(const CUtensorMap& tw, const CUtensorMap& tx, int M, int 
 // better.  256-token tiles pay off once there are two waves of them.
 int gemm_big_tok(int M, int N, int K, int num_sms) {
   if (M <= 128) return 0;
-  const int n_tiles = (N + kBN - 1) / kBN;
+  const int n_tiles = (N + bigk::kBN - 1) / bigk::kBN;
   if (n_tiles * ((M + 255) / 256) >= 2 * num_sms) return 256;
   const int t128 = n_tiles * ((M + 127) / 128);
   if (t128 < 36 || (K >= 8192 && t128 < num_sms)) return 0;
@@ -563,8 +69,8 @@ int gemm_big_tok(int M, int N, int K, int num_sms) {
 
 cudaError_t gemm_big_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int tok,
                             const EpiParams& epi, cudaStream_t stream) {
-  if (tok == 256) return launch_big<256, false, false>(tw, tx, M, N, K, 1, epi, stream);
-  if (tok == 128) return launch_big<128, false, false>(tw, tx, M, N, K, 1, epi, stream);
+  if (tok == 256) return by_kind<256, false, false>(tw, tx, M, N, K, 1, epi, stream);
+  if (tok == 128) return by_kind<128, false, false>(tw, tx, M, N, K, 1, epi, stream);
   return cudaErrorInvalidValue;
 }
 
@@ -572,30 +78,30 @@ cudaError_t gemm_big_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M,
 // outputs of less than half a wave get K slices (>= 8 k-blocks each) up to
 // about one wave.
 int gemm_mn_plan(int M, int N, int K, int num_sms, int* splits) {
-  const int n_tiles = (N + kBN - 1) / kBN;
+  const int n_tiles = (N + bigk::kBN - 1) / bigk::kBN;
   const int tok = n_tiles * ((M + 255) / 256) >= 2 * num_sms ? 256 : 128;
   const int tiles = n_tiles * ((M + tok - 1) / tok);
   int s = 1;
   if (2 * tiles <= num_sms)
-    while ((s + 1) * tiles <= num_sms && (K / kBK) / (s + 1) >= 8) ++s;
+    while ((s + 1) * tiles <= num_sms && (K / bigk::kBK) / (s + 1) >= 8) ++s;
   *splits = s;
   return tok;
 }
 
 cudaError_t gemm_mn_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int tok,
                            int splits, bool x_mn, const EpiParams& epi, cudaStream_t stream) {
-  if (M < 1 || N < 1 || K < kBK || K % kBK != 0 || splits < 1 || splits > K / kBK)
+  if (M < 1 || N < 1 || K < bigk::kBK || K % bigk::kBK != 0 || splits < 1 || splits > K / bigk::kBK)
     return cudaErrorInvalidValue;
   const bool direct = epi.kind == EPI_ACCUM_F32 || epi.kind == EPI_STORE_F32 || epi.kind == EPI_SWIGLU_BWD;
   if (!direct || (splits > 1 && (epi.kind != EPI_ACCUM_F32 || epi.tile_flags == nullptr)) ||
       epi.ssq_in != nullptr || epi.bias != nullptr)
     return cudaErrorInvalidValue;
   if (x_mn) {
-    if (tok == 256) return launch_big<256, true, true>(tw, tx, M, N, K, splits, epi, stream);
-    if (tok == 128) return launch_big<128, true, true>(tw, tx, M, N, K, splits, epi, stream);
+    if (tok == 256) return by_kind<256, true, true>(tw, tx, M, N, K, splits, epi, stream);
+    if (tok == 128) return by_kind<128, true, true>(tw, tx, M, N, K, splits, epi, stream);
   } else {
-    if (tok == 256) return launch_big<256, true, false>(tw, tx, M, N, K, splits, epi, stream);
-    if (tok == 128) return launch_big<128, true, false>(tw, tx, M, N, K, splits, epi, stream);
+    if (tok == 256) return by_kind<256, true, false>(tw, tx, M, N, K, splits, epi, stream);
+    if (tok == 128) return by_kind<128, true, false>(tw, tx, M, N, K, splits, epi, stream);
   }
   return cudaErrorInvalidValue;
 }

@@ -1,0 +1,598 @@
+// gemm_big_impl.cuh -- the persistent tcgen05 GEMM kernel template
+// (gemm_big.cu describes it).  Specialised per epilogue kind EK so each
+// instance carries only its own epilogue (a kernel holding every variant
+// stalled on instruction-cache misses); instantiated in gemm_big_i*.cu.
+#pragma once
+#include <cstdio>
+
+#include "gemm.cuh"
+#include "gemm_epi.cuh"
+#include "sm100.cuh"
+
+namespace srl {
+namespace bigk {
+using namespace sm100;
+
+
+constexpr int kBN = 128;  // weight rows per tile (UMMA M)
+constexpr int kBK = 64;   // k-block (128-B swizzle row)
+constexpr int kThreads = 384;
+constexpr int kChunk = 32;  // tokens per epilogue chunk
+constexpr int kQb = 8;      // EPI_QKV: tokens whose cos / sin loads are in flight together
+constexpr int kPitch = kBN;  // drain writes are lane-contiguous: no padding needed
+
+template <int TOK>
+struct BigLayout {
+  static constexpr int STAGES = TOK == 256 ? 4 : 6;
+  static constexpr int kABytes = kBN * kBK * 2;
+  static constexpr int kBBytes = TOK * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kRing = STAGES * kStageBytes;
+  static constexpr int kEpi = kRing;                               // [2][kChunk][kPitch] fp32
+  static constexpr int kRstd = kEpi + 2 * kChunk * kPitch * 4;     // [2][kChunk] fp32
+  static constexpr int kRow = kRstd + 2 * kChunk * 4;              // [2][kChunk] int4
+  static constexpr int kBar = kRow + 2 * kChunk * 16;
+  static constexpr int kMisc = kBar + (2 * STAGES + 4) * 8;
+  static constexpr int kTotal = kMisc + 16;
+  static constexpr int kAlloc = kTotal + 1024;
+  static_assert(kAlloc <= 232448, "shared memory budget");
+};
+
+// 32 values per lane -> lane l holds the reduction over the warp's lanes of
+// value l (recursive halving: 16 + 8 + 4 + 2 + 1 shuffles).  Sum or max.
+template <bool kSum>
+__device__ __forceinline__ void butterfly_reduce(float (&v)[32], int lane) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool upper = (lane & w) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = upper ? v[i] : v[i + w];
+      const float keep = upper ? v[i + w] : v[i];
+      const float got = __shfl_xor_sync(0xffffffffu, send, w);
+      v[i] = kSum ? keep + got : fmaxf(keep, got);
+    }
+  }
+}
+
+// The direct SwiGLU epilogue stores bf16 pairs: needs whole 128-column tiles
+// and an even act row stride.
+__device__ __forceinline__ bool direct_swiglu_ok(const EpiParams& epi, int N) {
+  return N % 128 == 0 && (epi.ld_bf16 & 1) == 0;
+}
+
+// debug timeline (epi.stamps, [ctas x 8] %globaltimer): 0 start, 1 setup done,
+// 2 first TMA issued, 3 first k-block landed, 4 last MMA committed,
+// 5 first accumulator ready (epilogue), 6 epilogue done (group 0), 7 exit
+__device__ __forceinline__ void big_stamp(const EpiParams& epi, int i) {
+  if (epi.stamps != nullptr) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    epi.stamps[(size_t)blockIdx.x * 8 + i] = t;
+  }
+}
+
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+}
+
+// AMN / BMN: the W / X operand is MN-major (given as [K x N] / [K x M]
+// row-major, e.g. the trainer's dW = dY^T X with the token axis as K, or
+// dX = dY W with W's rows as K): 64 x 64 TMA boxes, UMMA descriptors with
+// the 64-element MN groups 8 KB apart.  `splits` > 1 cuts K into
+// ordered slices whose EPI_ACCUM epilogues add into the output one after the
+// other (per-tile counters in epi.tile_flags, self-resetting): deterministic
+// split-K for the small-output, long-K weight gradients.
+template <int TOK, bool AMN, bool BMN, int EK>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_big_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
+                    int M, int N, int K, int splits, const EpiParams epi) {
+  using L = BigLayout<TOK>;
+  const int kind = gemm_detail::epi_kind<EK>(epi);
+  constexpr int STAGES = L::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kMisc);
+
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) big_stamp(epi, 0);
+  const int n_tiles = (N + kBN - 1) / kBN;
+  const int tok_tiles = (M + TOK - 1) / TOK;
+  const int tiles = n_tiles * tok_tiles;
+  const int total = tiles * splits;
+  const int kbt = K / kBK;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&tw);
+      tma_prefetch_desc(&tx);
+    }
+    __syncwarp();
+    tmem_alloc<2 * TOK>(tmem_slot);
+  } else if (warp == 1) {
+    if (elect_one()) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(&tfull[a], 1);
+        mbar_init(&tempty[a], 256);  // every epilogue thread, after its last TMEM load
+      }
+      fence_barrier_init();
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_launch_dependents();
+  if (threadIdx.x == 0) big_stamp(epi, 1);
+
+  if (warp == 0) {
+    if (elect_one()) {  // ---- TMA producer
+      griddep_wait();   // the activations come from the previous kernel
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int tile = t % tiles, sp = t / tiles;
+        const int n0 = (tile % n_tiles) * kBN, t0 = (tile / n_tiles) * TOK;
+        for (int kb = sp * kbt / splits; kb < (sp + 1) * kbt / splits; ++kb) {
+          mbar_wait(&empty[stage], ph ^ 1);
+          uint8_t* a = smem + stage * L::kStageBytes;
+          mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+          if (kb == 0 && t == (int)blockIdx.x) big_stamp(epi, 2);
+          if constexpr (AMN) {  // 64 x 64 boxes: [k rows][64 MN columns], 8 KB each
+            tma_load_2d(a, &tw, &full[stage], n0, kb * kBK);
+            tma_load_2d(a + 8192, &tw, &full[stage], n0 + 64, kb * kBK);
+          } else {
+            tma_load_2d(a, &tw, &full[stage], kb * kBK, n0);
+          }
+          if constexpr (BMN) {
+#pragma unroll
+            for (int h = 0; h < TOK / 64; ++h)
+              tma_load_2d(a + L::kABytes + h * 8192, &tx, &full[stage], t0 + h * 64, kb * kBK);
+          } else {
+#pragma unroll
+            for (int h = 0; h < TOK / 128; ++h)  // the X map's box is 128 rows
+              tma_load_2d(a + L::kABytes + h * 128 * 128, &tx, &full[stage], kb * kBK, t0 + h * 128);
+          }
+          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {  // ---- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16_f32(128, TOK) | (AMN ? idesc_a_mn_major : 0u) |
+                                 (BMN ? idesc_b_mn_major : 0u);
+      int stage = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * TOK;
+        const int sp = t / tiles, kb0 = sp * kbt / splits;
+        for (int kb = kb0; kb < (sp + 1) * kbt / splits; ++kb) {
+          mbar_wait(&full[stage], ph);
+          tc_fence_after();
+          if (kb == kb0 && t == (int)blockIdx.x) big_stamp(epi, 3);
+          const uint32_t a = smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t b = a + L::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            // MN-major: 16 k rows = two 1-KB swizzle atoms; K-major: 32 B inside the atom
+            const uint64_t da = AMN ? umma_desc_mn_sw128(a + kk * 2048, 8192) : umma_desc_k_sw128(a, kk * 32);
+            const uint64_t db = BMN ? umma_desc_mn_sw128(b + kk * 2048, 8192) : umma_desc_k_sw128(b, kk * 32);
+            mma_bf16_ss(d, da, db, idesc, (kb != kb0) || kk != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+        big_stamp(epi, 4);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ---- epilogue: group g (warps 4-7 / 8-11), TMEM lane quadrant q
+    const int g = (warp - 4) >> 2, q = warp & 3;
+    const int tid = q * 32 + (threadIdx.x & 31);  // = the TMEM lane = the tile column drained
+    float* tile = reinterpret_cast<float*>(smem + L::kEpi) + g * kChunk * kPitch;
+    float* s_rstd = reinterpret_cast<float*>(smem + L::kRstd) + g * kChunk;
+    int4* s_row = reinterpret_cast<int4*>(smem + L::kRow) + g * kChunk;
+    auto sync = [g] { group_sync(g); };
+    // statistics-only LM head (the trainer's pass 1: no logits stored)
+    const bool stats_only = kind == EPI_LOGITS && epi.out_f32 == nullptr;
+    const bool direct = kind == EPI_STORE_F32 || kind == EPI_STORE_BF16 ||
+                        kind == EPI_ACCUM_F32 || kind == EPI_DLOGITS ||
+                        kind == EPI_SWIGLU_BWD || kind == EPI_RESID ||
+                        (kind == EPI_QKV && 128 % epi.hd == 0) ||
+                        (kind == EPI_SWIGLU && direct_swiglu_ok(epi, N)) || stats_only;
+    float* red = tile;  // stats_only: [4 warps][32 tokens] cross-warp partials (the unused staging tile)
+    bool waited = false;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int otile = t % tiles, sp = t / tiles;
+      const int n_tile = otile % n_tiles, n0 = n_tile * kBN, t0 = (otile / n_tiles) * TOK;
+      if (!waited) {  // epilogue inputs (residual, ssq) come from earlier kernels
+        griddep_wait();
+        waited = true;
+      }
+      // Row inputs of this group's chunks (independent of the accumulator),
+      // loaded while the tile's MMAs run: lane l holds token (chunk row) l's
+      // deferred-RMSNorm rstd and (EPI_QKV) slot / position / page / offset.
+      constexpr int kCpg = TOK / (2 * kChunk);  // chunks per group
+      float pre_rs[kCpg];
+      int2 pre_rc[kCpg];  // (position or -1, page)
+      if (direct) {
+        const int lane = threadIdx.x & 31;
+        float ssum[kCpg];
+#pragma unroll
+        for (int ci = 0; ci < kCpg; ++ci) {
+          const int m = t0 + (g + 2 * ci) * kChunk + lane;
+          ssum[ci] = -1.f;
+          pre_rc[ci] = make_int2(-1, -1);  // .y = slot until the page is known
+          if (m < M) {
+            if (epi.ssq_in != nullptr)
+              ssum[ci] = gemm_detail::ssq_row_sum(epi.ssq_in + (size_t)m * epi.ssq_in_parts, epi.ssq_in_parts);
+            if (kind == EPI_QKV) {
+              pre_rc[ci].y = epi.row_slot[m];
+              pre_rc[ci].x = epi.row_pos[m];
+            }
+          }
+        }
+#pragma unroll
+        for (int ci = 0; ci < kCpg; ++ci) {
+          pre_rs[ci] = ssum[ci] >= 0.f ? rsqrtf(ssum[ci] * epi.inv_dim + epi.eps) : 1.f;
+          if (pre_rc[ci].y >= 0)
+            pre_rc[ci].y = epi.block_table[(size_t)pre_rc[ci].y * epi.pages_per_seq + pre_rc[ci].x / 64];
+          else
+            pre_rc[ci].x = -1;
+        }
+      }
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      if (tid == 0 && g == 0 && t == (int)blockIdx.x) big_stamp(epi, 5);
+      if (splits > 1 && sp > 0) {  // K slice sp adds after slices 0..sp-1 (both groups each)
+        if (tid == 0) {
+          while (ld_acquire_gpu(epi.tile_flags + otile) < 2 * sp) __nanosleep(64);
+        }
+        sync();
+      }
+      const int last = TOK / kChunk - 2 + g;  // this group's last chunk of the tile
+      for (int c = g; c < TOK / kChunk; c += 2) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + acc * TOK + c * kChunk + ((uint32_t)(q * 32) << 16), r);
+        tmem_ld_wait();
+        if (c == last) {  // accumulator drained by this thread
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
+        const int tc0 = t0 + c * kChunk;
+        if (tc0 >= M) continue;  // rows past M: nothing to store (uniform per group)
+        if (direct) {
+          // plain stores straight from the accumulator registers: thread =
+          // output column n, so each warp store covers 32 consecutive columns
+          const int n = n0 + tid;
+          const int lane = threadIdx.x & 31;
+          // rstd of token tc0 + lane (prefetched), broadcast below
+          const int ci = (c - g) >> 1;
+          float rs = pre_rs[0];
+          int2 rc = pre_rc[0];
+#pragma unroll
+          for (int k = 1; k < kCpg; ++k)
+            if (ci == k) { rs = pre_rs[k]; rc = pre_rc[k]; }
+          const float bias = (epi.bias != nullptr && n < N) ? gemm_detail::epi_bf2f(epi.bias[n]) : 0.f;
+          const int jn = min(32, M - tc0);
+          if (stats_only) {
+            // per token: the target's logit, and over this tile's 128 columns
+            // the max and the sum of exp(x - max) (fp32 exp, fp64 combine).
+            // Each warp reduces its 32 columns for all 32 tokens at once with a
+            // butterfly transpose (31 shuffles, lane l ends with token l), the
+            // group's four warps combine through shared memory.
+            int tg = -1;
+            if (epi.tgt_row && tc0 + lane < M) tg = epi.tgt_row[tc0 + lane];
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float rj = __shfl_sync(0xffffffffu, rs, j);
+              const int tj = __shfl_sync(0xffffffffu, tg, j);
+              v[j] = n < N && j < jn ? __uint_as_float(r[j]) * rj : -INFINITY;
+              if (n == tj && j < jn) epi.tgt_out[tc0 + j] = v[j];
+            }
+            float mx[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) mx[j] = v[j];
+            butterfly_reduce<false>(mx, lane);  // lane l: max of token l over this warp's columns
+            const int q = tid >> 5;
+            red[q * 32 + lane] = mx[0];
+            sync();
+            float M_l = red[lane];
+#pragma unroll
+            for (int w = 1; w < 4; ++w) M_l = fmaxf(M_l, red[w * 32 + lane]);
+            float e[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float Mj = __shfl_sync(0xffffffffu, M_l, j);
+              e[j] = v[j] == -INFINITY ? 0.f : __expf(v[j] - Mj);
+            }
+            butterfly_reduce<true>(e, lane);  // lane l: this warp's sum for token l
+            sync();  // everyone has read the maxima
+            red[q * 32 + lane] = e[0];
+            sync();
+            if (q == 0 && lane < jn) {
+              const double sum = (double)red[lane] + (double)red[32 + lane] + (double)red[64 + lane] +
+                                 (double)red[96 + lane];
+              epi.part_max[(size_t)(tc0 + lane) * n_tiles + n_tile] = M_l;
+              epi.part_sum[(size_t)(tc0 + lane) * n_tiles + n_tile] = M_l == -INFINITY ? 0.0 : sum;
+            }
+            sync();  // red is reused by the next chunk
+            continue;
+          }
+          if (kind == EPI_DLOGITS) {
+            // d = coef * (onehot - softmax) of token tc0 + j at vocab column n; the
+            // transposed copy [n][tokens] is 32 contiguous bf16 per thread
+            float lse = 0.f, cf = 0.f;
+            int tg = -1;
+            if (tc0 + lane < M) {
+              lse = (float)epi.lse_in[tc0 + lane];
+              cf = epi.row_coef[tc0 + lane];
+              tg = epi.tgt_row[tc0 + lane];
+            }
+            uint32_t packed[16];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float rj = __shfl_sync(0xffffffffu, rs, j);
+              const float lj = __shfl_sync(0xffffffffu, lse, j);
+              const float cj = __shfl_sync(0xffffffffu, cf, j);
+              const int tj = __shfl_sync(0xffffffffu, tg, j);
+              const float x = __uint_as_float(r[j]) * rj;
+              const float d = j < jn ? cj * ((n == tj ? 1.f : 0.f) - __expf(x - lj)) : 0.f;
+              const __nv_bfloat16 b = __float2bfloat16(d);
+              if (j < jn && n < N) epi.out_bf16[(size_t)(tc0 + j) * epi.ld_bf16 + n] = b;
+              const uint32_t bits = (uint32_t)__bfloat16_as_ushort(b);
+              if (j & 1) packed[j >> 1] |= bits << 16;
+              else packed[j >> 1] = bits;
+            }
+            if (epi.outT_bf16 && n < N) {  // columns past M are written as 0 (padding)
+              uint4* dst = reinterpret_cast<uint4*>(epi.outT_bf16 + (size_t)n * epi.ldT + tc0);
+#pragma unroll
+              for (int v = 0; v < 4; ++v)
+                dst[v] = make_uint4(packed[4 * v], packed[4 * v + 1], packed[4 * v + 2], packed[4 * v + 3]);
+            }
+            continue;
+          }
+          if (kind == EPI_RESID) {
+            // resid += acc, xg = bf16(resid * gain); the 32 residual loads in
+            // flight together, the per-token x^2 sum over the tile's 128 columns
+            // by a butterfly transpose (lane l: token l) + the group's 4 warps
+            const bool colok = n < N;
+            const float gain = colok ? gemm_detail::epi_bf2f(epi.gain[n]) : 0.f;
+            float xr[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              xr[j] = (colok && j < jn) ? epi.resid[(size_t)(tc0 + j) * N + n] : 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float x = 0.f;
+              if (colok && j < jn) {
+                const size_t o = (size_t)(tc0 + j) * N + n;
+                x = xr[j] + __uint_as_float(r[j]);
+                epi.resid[o] = x;
+                epi.xg[o] = __float2bfloat16(x * gain);
+              }
+              xr[j] = x * x;
+            }
+            butterfly_reduce<true>(xr, lane);
+            const int q = tid >> 5;
+            red[q * 32 + lane] = xr[0];
+            sync();
+            if (q == 0 && lane < jn)
+              epi.ssq_out[(size_t)(tc0 + lane) * n_tiles + n_tile] =
+                  ((red[lane] + red[32 + lane]) + red[64 + lane]) + red[96 + lane];
+            sync();  // red is reused by the next chunk
+            continue;
+          }
+          if (kind == EPI_QKV) {
+            // v = rstd acc + bias staged (RoPE pairs live in other warps); the
+            // row's slot / position / page held by lane j and broadcast; the
+            // cos / sin of 8 tokens in flight together
+            const bool colok = n < N;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float rj = __shfl_sync(0xffffffffu, rs, j);
+              tile[j * kPitch + tid] = (colok && j < jn) ? __uint_as_float(r[j]) * rj + bias : 0.f;
+            }
+            sync();
+            const int hd = epi.hd, half = hd >> 1;
+            const int qend = epi.nq * hd, kend = (epi.nq + epi.nkv) * hd;
+            const int jj = n % hd, i = jj < half ? jj : jj - half, hb = tid - jj;
+            const bool rot = n < kend;
+#pragma unroll
+            for (int jb = 0; jb < 32; jb += kQb) {
+              float co[kQb], si[kQb];
+#pragma unroll
+              for (int u = 0; u < kQb; ++u) {
+                const int ps = __shfl_sync(0xffffffffu, rc.x, jb + u);
+                co[u] = 1.f;
+                si[u] = 0.f;
+                if (rot && colok && ps >= 0) {
+                  co[u] = epi.cos_sin[(size_t)ps * hd + i];
+                  si[u] = epi.cos_sin[(size_t)ps * hd + half + i];
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < kQb; ++u) {
+                const int j = jb + u, m = tc0 + j;
+                const int ps = __shfl_sync(0xffffffffu, rc.x, j);
+                const int page = __shfl_sync(0xffffffffu, rc.y, j);
+                if (!colok || ps < 0) continue;  // also rows past M and free slots
+                const float* row = &tile[j * kPitch + hb];
+                float y;
+                if (rot) {
+                  const float x1 = row[i], x2 = row[i + half];
+                  y = jj < half ? x1 * co[u] - x2 * si[u] : x2 * co[u] + x1 * si[u];
+                } else {
+                  y = row[jj];
+                }
+                const __nv_bfloat16 b = __float2bfloat16(y);
+                if (n < qend) {
+                  epi.q_out[(size_t)m * qend + n] = b;
+                } else {
+                  const int kv = n < kend ? n - qend : n - kend;
+                  const size_t at = (((size_t)page * epi.nkv + kv / hd) * 64 + ps % 64) * hd + jj;
+                  if (n < kend) epi.kc[at] = b;
+                  else epi.vc[at] = b;
+                }
+              }
+            }
+            sync();  // the staged chunk is reused next
+            continue;
+          }
+          if (kind == EPI_SWIGLU) {
+            // tile = 64 gate | 64 up columns: stage rstd-scaled values, then
+            // thread (column pair, 8 tokens) forms act = silu(g) u, bf16x2 stores
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float rj = __shfl_sync(0xffffffffu, rs, j);
+              const float v = __uint_as_float(r[j]) * rj;
+              tile[j * kPitch + tid] = v;
+              if (epi.out2_bf16 && j < jn) epi.out2_bf16[(size_t)(tc0 + j) * N + n] = __float2bfloat16(v);
+            }
+            sync();
+            const int cp = 2 * (tid & 31), jb = (tid >> 5) * 8;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int j = jb + u;
+              if (j >= jn) break;
+              const float2 gg = *reinterpret_cast<const float2*>(&tile[j * kPitch + cp]);
+              const float2 uu = *reinterpret_cast<const float2*>(&tile[j * kPitch + 64 + cp]);
+              const float a0 = gg.x / (1.f + expf(-gg.x)) * uu.x;
+              const float a1 = gg.y / (1.f + expf(-gg.y)) * uu.y;
+              *reinterpret_cast<__nv_bfloat162*>(epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + (n0 >> 1) + cp) =
+                  __floats2bfloat162_rn(a0, a1);
+            }
+            sync();  // the staged chunk is reused next
+            continue;
+          }
+          if (kind == EPI_SWIGLU_BWD) {
+            // column n = act index j of 64-block b: gate at 128 b + (j & 63), up 64 after
+            if (n < N) {
+              const size_t gcol = (size_t)(n >> 6) * 128 + (n & 63);
+              // all 64 gate / up loads in flight before the first store
+              uint16_t gb[32], ub[32];
+              const uint16_t* gu = reinterpret_cast<const uint16_t*>(epi.gu_in);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const size_t row = (size_t)(tc0 + (j < jn ? j : 0)) * epi.ld_bf16;
+                gb[j] = __ldg(gu + row + gcol);
+                ub[j] = __ldg(gu + row + gcol + 64);
+              }
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (j >= jn) continue;
+                const size_t row = (size_t)(tc0 + j) * epi.ld_bf16;
+                const float gv = __bfloat162float(__ushort_as_bfloat16(gb[j]));
+                const float uv = __bfloat162float(__ushort_as_bfloat16(ub[j]));
+                const float da = __uint_as_float(r[j]);
+                const float sg = 1.f / (1.f + expf(-gv));  // as swiglu_bwd_kernel
+                const float silu = gv * sg;
+                epi.out_bf16[row + gcol] = __float2bfloat16(da * uv * (sg * (1.f + gv * (1.f - sg))));
+                epi.out_bf16[row + gcol + 64] = __float2bfloat16(da * silu);
+              }
+            }
+            continue;
+          }
+          if (n < N) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float rj = __shfl_sync(0xffffffffu, rs, j);
+              if (j >= jn) continue;
+              const float v = __uint_as_float(r[j]);
+              const size_t m = (size_t)(tc0 + j);
+              if (kind == EPI_STORE_F32) epi.out_f32[m * epi.ld_out + n] = v * rj + bias;
+              else if (kind == EPI_STORE_BF16) epi.out_bf16[m * epi.ld_bf16 + n] = __float2bfloat16(v * rj + bias);
+              else epi.out_f32[m * epi.ld_out + n] += epi.scale * v;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) (void)__shfl_sync(0xffffffffu, rs, j);
+          }
+          continue;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) tile[j * kPitch + tid] = __uint_as_float(r[j]);
+        gemm_detail::epi_row_meta<EK>(epi, 0, kChunk, tc0, M, s_rstd, s_row, tid, 128);
+        sync();
+        gemm_detail::epi_apply<EK>(epi, tile, kPitch, 0, kChunk, tc0, n0, n_tile, n_tiles, M, N, s_rstd,
+                               s_row, tid, 128, sync);
+        sync();  // the staged chunk is reused next
+      }
+      if (splits > 1) {
+        __threadfence();
+        sync();
+        if (tid == 0 && atomicAdd(epi.tile_flags + otile, 1) == 2 * splits - 1)
+          atomicExch(epi.tile_flags + otile, 0);  // last slice: reset for the next launch
+      }
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+  if (warp == 4 && (threadIdx.x & 31) == 0) big_stamp(epi, 6);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_free<2 * TOK>(tmem);
+  if (threadIdx.x == 0) big_stamp(epi, 7);
+}
+
+inline int num_sms_cached() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <int TOK, bool AMN, bool BMN, int EK>
+cudaError_t launch_big(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int splits,
+                       const EpiParams& epi, cudaStream_t stream) {
+  using L = BigLayout<TOK>;
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      gemm_big_kernel<TOK, AMN, BMN, EK>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
+  if (attr != cudaSuccess) return attr;
+  const int tiles = ((N + kBN - 1) / kBN) * ((M + TOK - 1) / TOK) * splits;
+  const int grid = tiles < num_sms_cached() ? tiles : num_sms_cached();
+  return launch_pdl(gemm_big_kernel<TOK, AMN, BMN, EK>, dim3(grid), dim3(kThreads), (size_t)L::kAlloc, stream,
+                    dim3(1, 1, 1), tw, tx, M, N, K, splits, epi);
+}
+
+
+// Explicit instantiations live in gemm_big_i*.cu (parallel compilation).
+#define SRL_BIG_LAUNCH_ARGS                                                                  \
+  const CUtensorMap&, const CUtensorMap&, int, int, int, int, const EpiParams&, cudaStream_t
+#define SRL_BIG_EXTERN(TOK, AMN, BMN, EK) \
+  extern template cudaError_t launch_big<TOK, AMN, BMN, EK>(SRL_BIG_LAUNCH_ARGS);
+#define SRL_BIG_INSTANTIATE(TOK, AMN, BMN, EK) \
+  template cudaError_t launch_big<TOK, AMN, BMN, EK>(SRL_BIG_LAUNCH_ARGS);
+#define SRL_BIG_ALL(X)                                                                      \
+  X(256, false, false, 0) X(256, false, false, 1) X(256, false, false, 2) X(256, false, false, 3) \
+  X(256, false, false, 4) X(256, false, false, 5) X(256, false, false, 6) X(256, false, false, 7) \
+  X(128, false, false, 0) X(128, false, false, 1) X(128, false, false, 2) X(128, false, false, 3) \
+  X(128, false, false, 4) X(128, false, false, 5) X(128, false, false, 6) X(128, false, false, 7) \
+  X(256, true, true, 0) X(256, true, true, 6) X(128, true, true, 0) X(128, true, true, 6)        \
+  X(256, true, false, 0) X(256, true, false, 6) X(256, true, false, 8)                          \
+  X(128, true, false, 0) X(128, true, false, 6) X(128, true, false, 8)
+SRL_BIG_ALL(SRL_BIG_EXTERN)
+
+}  // namespace bigk
+}  // namespace srl

@@ -47,10 +47,17 @@ __device__ __forceinline__ float ssq_row_sum(const float* row, int parts) {
   return s;
 }
 
+// The epilogue kind: a compile-time constant when the kernel is specialised
+// (EK >= 0; dead variants drop out of the instruction stream), else runtime.
+template <int EK>
+__device__ __forceinline__ int epi_kind(const EpiParams& e) { return EK >= 0 ? EK : e.kind; }
+
 // Per-row inputs of rows [r0, r1): the deferred-RMSNorm rstd and (EPI_QKV)
 // the row's KV-cache coordinates (slot, pos, page, offset in page).
+template <int EK = -1>
 __device__ __forceinline__ void epi_row_meta(const EpiParams& epi, int r0, int r1, int t0, int M,
                                              float* s_rstd, int4* s_row, int tid, int nthr) {
+  const int kind = epi_kind<EK>(epi);
   for (int j = r0 + tid; j < r1; j += nthr) {
     float r = 1.f;
     const int m = t0 + j;
@@ -59,9 +66,9 @@ __device__ __forceinline__ void epi_row_meta(const EpiParams& epi, int r0, int r
       r = rsqrtf(s * epi.inv_dim + epi.eps);
     }
     s_rstd[j] = r;
-    if ((epi.kind == EPI_LOGITS || epi.kind == EPI_DLOGITS) && epi.tgt_row != nullptr)
+    if ((kind == EPI_LOGITS || kind == EPI_DLOGITS) && epi.tgt_row != nullptr)
       s_row[j] = make_int4(m < M ? epi.tgt_row[m] : -1, 0, 0, 0);
-    if (epi.kind == EPI_QKV) {
+    if (kind == EPI_QKV) {
       int4 rc = make_int4(-1, 0, 0, 0);
       if (m < M) {
         rc.x = epi.row_slot[m];
@@ -78,14 +85,15 @@ __device__ __forceinline__ void epi_row_meta(const EpiParams& epi, int r0, int r
 
 // The epilogue over rows [r0, r1) of the staged block.  n_tile / n_tiles
 // index the per-(row, 128-column tile) outputs (EPI_LOGITS, EPI_RESID ssq).
-template <class Sync>
+template <int EK = -1, class Sync>
 __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int pitch, int r0, int r1,
                                           int t0, int n0, int n_tile, int n_tiles, int M, int N,
                                           const float* s_rstd, const int4* s_row, int tid, int nthr,
                                           Sync sync) {
   const int rows = r1 - r0;
   const int warp = tid >> 5, lane = tid & 31, nwarps = nthr >> 5;
-  if (epi.kind == EPI_STORE_F32 || epi.kind == EPI_STORE_BF16) {
+  const int kind = epi_kind<EK>(epi);
+  if (kind == EPI_STORE_F32 || kind == EPI_STORE_BF16) {
 #pragma unroll 4
     for (int idx = tid; idx < rows * 128; idx += nthr) {
       const int j = r0 + (idx >> 7), c = idx & 127;
@@ -93,19 +101,19 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
       if (m >= M || n >= N) continue;
       float v = tile[j * pitch + c] * s_rstd[j];
       if (epi.bias) v += epi_bf2f(epi.bias[n]);
-      if (epi.kind == EPI_STORE_F32)
+      if (kind == EPI_STORE_F32)
         epi.out_f32[(size_t)m * epi.ld_out + n] = v;
       else
         epi.out_bf16[(size_t)m * epi.ld_bf16 + n] = __float2bfloat16(v);
     }
-  } else if (epi.kind == EPI_ACCUM_F32) {
+  } else if (kind == EPI_ACCUM_F32) {
     for (int idx = tid; idx < rows * 128; idx += nthr) {
       const int j = r0 + (idx >> 7), c = idx & 127;
       const int m = t0 + j, n = n0 + c;
       if (m >= M || n >= N) continue;
       epi.out_f32[(size_t)m * epi.ld_out + n] += epi.scale * tile[j * pitch + c];
     }
-  } else if (epi.kind == EPI_SWIGLU) {
+  } else if (kind == EPI_SWIGLU) {
 #pragma unroll 4
     for (int idx = tid; idx < rows * 64; idx += nthr) {
       const int j = r0 + (idx >> 6), c = idx & 63;
@@ -120,7 +128,7 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
         epi.out2_bf16[(size_t)m * N + n0 + 64 + c] = __float2bfloat16(u);
       }
     }
-  } else if (epi.kind == EPI_QKV && (nthr & 127) == 0) {
+  } else if (kind == EPI_QKV && (nthr & 127) == 0) {
     // thread = one column c for rows r0 + (tid >> 7) + k * (nthr / 128): the
     // bias is loaded once, the RoPE cos/sin of 8 rows are in flight together
     const int c = tid & 127, rstep = nthr >> 7, n = n0 + c;
@@ -173,7 +181,7 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
         }
       }
     }
-  } else if (epi.kind == EPI_QKV) {
+  } else if (kind == EPI_QKV) {
     for (int idx = tid; idx < rows * 128; idx += nthr) {
       const int j = r0 + (idx >> 7), c = idx & 127;
       const int n = n0 + c;
@@ -211,7 +219,7 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
         else epi.vc[at] = b;
       }
     }
-  } else if (epi.kind == EPI_LOGITS) {
+  } else if (kind == EPI_LOGITS) {
     for (int idx = tid; idx < rows * 128; idx += nthr) {
       const int j = r0 + (idx >> 7), c = idx & 127;
       const int m = t0 + j, n = n0 + c;
@@ -240,7 +248,7 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
         epi.part_sum[(size_t)m * n_tiles + n_tile] = s;
       }
     }
-  } else if (epi.kind == EPI_DLOGITS) {
+  } else if (kind == EPI_DLOGITS) {
     for (int idx = tid; idx < rows * 128; idx += nthr) {
       const int j = r0 + (idx >> 7), c = idx & 127;
       const int m = t0 + j, n = n0 + c;
@@ -251,7 +259,7 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
       epi.out_bf16[(size_t)m * epi.ld_bf16 + n] = d;
       if (epi.outT_bf16) epi.outT_bf16[(size_t)n * epi.ldT + m] = d;
     }
-  } else if (epi.kind == EPI_RESID && (nthr & 127) == 0) {
+  } else if (kind == EPI_RESID && (nthr & 127) == 0) {
     // thread = one column; the residual loads of 8 rows are in flight together
     const int c = tid & 127, rstep = nthr >> 7, n = n0 + c;
     const bool colok = n < N;
@@ -287,7 +295,7 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
       s = epi_warp_sum(s);
       if (lane == 0 && t0 + j < M) epi.ssq_out[(size_t)(t0 + j) * n_tiles + n_tile] = s;
     }
-  } else if (epi.kind == EPI_RESID) {
+  } else if (kind == EPI_RESID) {
 #pragma unroll 4
     for (int idx = tid; idx < rows * 128; idx += nthr) {
       const int j = r0 + (idx >> 7), c = idx & 127;
