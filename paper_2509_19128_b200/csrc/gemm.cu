@@ -68,7 +68,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 
 
-template <int TOK, int STAGES>
+template <int TOK, int STAGES, int EK>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
                      int M, int N, int K, int cs, float* __restrict__ ws, const EpiParams epi) {
@@ -215,17 +215,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float4* base = reinterpret_cast<const float4*>(ws + tile_id * (TOK * kBlockN)) +
                          (size_t)r0 * (kBlockN / 4);
     const size_t split_stride4 = tiles_total * (TOK * kBlockN) / 4;
-    for (int q0 = 0; q0 < cs; q0 += 4) {
-      float4 v[4][kMaxPer];
+    constexpr int kQ = TOK == 128 ? 2 : 4;  // partials in flight (register budget)
+    for (int q0 = 0; q0 < cs; q0 += kQ) {
+      float4 v[kQ][kMaxPer];
 #pragma unroll
-      for (int dq = 0; dq < 4; ++dq)
+      for (int dq = 0; dq < kQ; ++dq)
 #pragma unroll
         for (int k = 0; k < kMaxPer; ++k) {
           const int i = threadIdx.x + k * kThreads;
           if (q0 + dq < cs && i < n4) v[dq][k] = __ldcg(base + (size_t)(q0 + dq) * split_stride4 + i);
         }
 #pragma unroll
-      for (int dq = 0; dq < 4; ++dq)
+      for (int dq = 0; dq < kQ; ++dq)
 #pragma unroll
         for (int k = 0; k < kMaxPer; ++k) {
           const int i = threadIdx.x + k * kThreads;
@@ -249,23 +250,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ---- epilogue over rows [r0, r1) (gemm_epi.cuh)
   SRL_STAMP(4);
   griddep_wait();  // epilogue inputs (ssq, residual) come from earlier kernels
-  gemm_detail::epi_row_meta(epi, r0, r1, t0, M, s_rstd, s_row, threadIdx.x, kThreads);
+  gemm_detail::epi_row_meta<EK>(epi, r0, r1, t0, M, s_rstd, s_row, threadIdx.x, kThreads);
   __syncthreads();
   SRL_STAMP(5);
-  gemm_detail::epi_apply(epi, tile, L::kPitch, r0, r1, t0, n0, n_tile, n_tiles, M, N, s_rstd, s_row,
+  gemm_detail::epi_apply<EK>(epi, tile, L::kPitch, r0, r1, t0, n0, n_tile, n_tiles, M, N, s_rstd, s_row,
                          threadIdx.x, kThreads, [] { __syncthreads(); });
   __syncthreads();
   SRL_STAMP(6);
 }
 
-template <int TOK, int STAGES>
+// One instance per epilogue kind (only its own epilogue in the instruction stream).
+template <int TOK, int STAGES, int EK>
 cudaError_t launch_impl(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int cs,
                         const GemmWorkspace& ws, const EpiParams& epi, cudaStream_t stream) {
   using L = Layout<TOK, STAGES>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_bf16_kernel<TOK, STAGES>,
+    attr_err = cudaFuncSetAttribute(gemm_bf16_kernel<TOK, STAGES, EK>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
   });
   if (attr_err != cudaSuccess) return attr_err;
@@ -275,8 +277,24 @@ cudaError_t launch_impl(const CUtensorMap& tw, const CUtensorMap& tx, int M, int
     const size_t need = (size_t)cs * n_tiles * tok_tiles * TOK * kBlockN;
     if (ws.partials == nullptr || need > ws.partial_floats) return cudaErrorInvalidValue;
   }
-  return launch_pdl(gemm_bf16_kernel<TOK, STAGES>, dim3(n_tiles, cs, tok_tiles), dim3(kThreads),
+  return launch_pdl(gemm_bf16_kernel<TOK, STAGES, EK>, dim3(n_tiles, cs, tok_tiles), dim3(kThreads),
                     (size_t)L::kAlloc, stream, dim3(1, cs, 1), tw, tx, M, N, K, cs, ws.partials, epi);
+}
+
+template <int TOK>
+cudaError_t launch_kind(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, int K, int cs,
+                        const GemmWorkspace& ws, const EpiParams& epi, cudaStream_t stream) {
+  switch (epi.kind) {
+    case 0: return launch_impl<TOK, 4, 0>(tw, tx, M, N, K, cs, ws, epi, stream);
+    case 1: return launch_impl<TOK, 4, 1>(tw, tx, M, N, K, cs, ws, epi, stream);
+    case 2: return launch_impl<TOK, 4, 2>(tw, tx, M, N, K, cs, ws, epi, stream);
+    case 3: return launch_impl<TOK, 4, 3>(tw, tx, M, N, K, cs, ws, epi, stream);
+    case 4: return launch_impl<TOK, 4, 4>(tw, tx, M, N, K, cs, ws, epi, stream);
+    case 5: return launch_impl<TOK, 4, 5>(tw, tx, M, N, K, cs, ws, epi, stream);
+    case 6: return launch_impl<TOK, 4, 6>(tw, tx, M, N, K, cs, ws, epi, stream);
+    case 7: return launch_impl<TOK, 4, 7>(tw, tx, M, N, K, cs, ws, epi, stream);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -368,8 +386,8 @@ cudaError_t gemm_bf16_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M
   if (big) return gemm_big_launch(tw, tx, M, N, K, big, epi, stream);
   int cs = 1;
   while (cs * 2 <= splits && cs * 2 <= kMaxCluster && cs * 2 <= K / kBlockK) cs *= 2;
-  if (gemm_tok_tile(M) == 64) return launch_impl<64, 4>(tw, tx, M, N, K, cs, ws, epi, stream);
-  return launch_impl<128, 4>(tw, tx, M, N, K, cs, ws, epi, stream);
+  if (gemm_tok_tile(M) == 64) return launch_kind<64>(tw, tx, M, N, K, cs, ws, epi, stream);
+  return launch_kind<128>(tw, tx, M, N, K, cs, ws, epi, stream);
 }
 
 }  // namespace srl

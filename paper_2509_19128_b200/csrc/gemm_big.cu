@@ -53,17 +53,18 @@ cudaError_t by_kind(const CUtensorMap& tw, const CUtensorMap& tx, int M, int N, 
 }
 }  // namespace
 
-// Measured on B200 (tools/gemm_bench.py, Qwen2.5 0.5B/1.5B/7B shapes,
-// M = 200..16384): the persistent kernel wins from ~36 tiles of 128 x 128 on;
-// below that, or for a long K on less than one wave of tiles (7B down
-// projection at M = 256), the cluster split-K kernel fills the machine
-// better.  256-token tiles pay off once there are two waves of them.
+// Measured on B200 (tools/gemm_bench.py --graph, Qwen2.5 0.5B/1.5B/7B
+// shapes, M = 200..20480): with per-kind instances the persistent kernel
+// beats the cluster split-K kernel from M = 200 on for every 0.5B shape but
+// a long K on very few tiles (down projection at M = 200: 14 tiles), and the
+// 7B down projection on less than a wave.  256-token tiles pay off once
+// there are two waves of them.
 int gemm_big_tok(int M, int N, int K, int num_sms) {
-  if (M <= 128) return 0;
+  if (M <= 64) return 0;
   const int n_tiles = (N + bigk::kBN - 1) / bigk::kBN;
   if (n_tiles * ((M + 255) / 256) >= 2 * num_sms) return 256;
   const int t128 = n_tiles * ((M + 127) / 128);
-  if (t128 < 36 || (K >= 8192 && t128 < num_sms)) return 0;
+  if ((K >= 2048 && t128 < 16) || (K >= 8192 && t128 < num_sms)) return 0;
   return 128;
 }
 
