@@ -369,7 +369,7 @@ cudaError_t gemm_bf16_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M
     return cudaErrorInvalidValue;
   if (epi.kind == EPI_SWIGLU && N % kBlockN != 0) return cudaErrorInvalidValue;
   // many token rows: the persistent double-buffered kernel (gemm_big.cu);
-  // SRL_GEMM_BIG=0 disables it, =1 forces it for every M > 128 (A/B tests)
+  // SRL_GEMM_BIG=0 disables it, =1 forces it for every M > 64 (A/B tests)
   static const char* big_env = std::getenv("SRL_GEMM_BIG");
   static const int sms = [] {
     int dev = 0, v = 148;
@@ -379,7 +379,7 @@ cudaError_t gemm_bf16_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M
   }();
   int big = gemm_big_tok(M, N, K, sms);
   if (big_env && big_env[0] == '0') big = 0;
-  if (big_env && big_env[0] == '1' && M > 128 && big == 0) big = 128;
+  if (big_env && big_env[0] == '1' && M > 64 && big == 0) big = 128;
   static const bool log = std::getenv("SRL_GEMM_LOG") != nullptr;  // launch trace (profiling)
   if (log) std::fprintf(stderr, "srl gemm M=%d N=%d K=%d kind=%d path=%s\n", M, N, K, epi.kind,
                         big ? (big == 256 ? "big256" : "big128") : "splitk");
