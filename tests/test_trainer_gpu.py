@@ -132,8 +132,13 @@ def test_trainer_data_parallel_shards_sum_to_full_batch(cuda):
     for r in range(2):
         tr.step_data_parallel(trajs, r, 2)  # no process group: the all-reduce is the identity
         parts.append(tr.gradient().cpu().numpy().astype(np.float64).copy())
+    # The full batch (92 rows) and the shards take different GEMM kernels (the
+    # persistent one from 65 rows on, the split-K one below): fp32 summation
+    # order differs, bf16-rounded activations flip by an ulp here and there,
+    # measured 6e-4.  A wrong normalisation (local instead of global m) is
+    # off by O(1).
     rel = np.linalg.norm(parts[0] + parts[1] - full) / np.linalg.norm(full)
-    assert rel < 1e-5, rel
+    assert rel < 5e-3, rel
 
 
 def test_trainer_qwen05b_large_batch_paths(cuda):
