@@ -94,6 +94,9 @@ cudaError_t gemm_mn_launch(const CUtensorMap& tw, const CUtensorMap& tx, int M, 
   if (M < 1 || N < 1 || K < bigk::kBK || K % bigk::kBK != 0 || splits < 1 || splits > K / bigk::kBK)
     return cudaErrorInvalidValue;
   const bool direct = epi.kind == EPI_ACCUM_F32 || epi.kind == EPI_STORE_F32 || epi.kind == EPI_SWIGLU_BWD;
+  if (epi.kind == EPI_SWIGLU_BWD &&  // 16-byte rows of the dgu tile
+      (N % 64 != 0 || epi.ld_bf16 % 8 != 0 || (reinterpret_cast<uintptr_t>(epi.out_bf16) & 15) != 0))
+    return cudaErrorInvalidValue;
   if (!direct || (splits > 1 && (epi.kind != EPI_ACCUM_F32 || epi.tile_flags == nullptr)) ||
       epi.ssq_in != nullptr || epi.bias != nullptr)
     return cudaErrorInvalidValue;

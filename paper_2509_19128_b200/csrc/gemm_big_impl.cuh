@@ -55,10 +55,11 @@ __device__ __forceinline__ void butterfly_reduce(float (&v)[32], int lane) {
   }
 }
 
-// The direct SwiGLU epilogue stores bf16 pairs: needs whole 128-column tiles
-// and an even act row stride.
+// The direct SwiGLU epilogue stores 16-byte vectors: whole 128-column tiles,
+// 16-byte aligned rows.
 __device__ __forceinline__ bool direct_swiglu_ok(const EpiParams& epi, int N) {
-  return N % 128 == 0 && (epi.ld_bf16 & 1) == 0;
+  return N % 128 == 0 && (epi.ld_bf16 & 7) == 0 && (reinterpret_cast<uintptr_t>(epi.out_bf16) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(epi.out2_bf16) & 15) == 0;
 }
 
 // debug timeline (epi.stamps, [ctas x 8] %globaltimer): 0 start, 1 setup done,
@@ -70,6 +71,11 @@ __device__ __forceinline__ void big_stamp(const EpiParams& epi, int i) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     epi.stamps[(size_t)blockIdx.x * 8 + i] = t;
   }
+}
+
+__device__ __forceinline__ uint32_t bf2_bits(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
 
 __device__ __forceinline__ void group_sync(int g) {
@@ -348,6 +354,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               cf = epi.row_coef[tc0 + lane];
               tg = epi.tgt_row[tc0 + lane];
             }
+            const bool vec = epi.outT_bf16 == nullptr && (epi.ld_bf16 & 7) == 0 && (N & 7) == 0 &&
+                             (reinterpret_cast<uintptr_t>(epi.out_bf16) & 15) == 0;
+            uint16_t* st16 = reinterpret_cast<uint16_t*>(tile);  // [32 tokens][128] bf16 staging
             uint32_t packed[16];
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -358,12 +367,26 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float x = __uint_as_float(r[j]) * rj;
               const float d = j < jn ? cj * ((n == tj ? 1.f : 0.f) - __expf(x - lj)) : 0.f;
               const __nv_bfloat16 b = __float2bfloat16(d);
-              if (j < jn && n < N) epi.out_bf16[(size_t)(tc0 + j) * epi.ld_bf16 + n] = b;
               const uint32_t bits = (uint32_t)__bfloat16_as_ushort(b);
-              if (j & 1) packed[j >> 1] |= bits << 16;
-              else packed[j >> 1] = bits;
+              if (vec) {
+                st16[j * 128 + tid] = (uint16_t)bits;
+              } else {
+                if (j < jn && n < N) epi.out_bf16[(size_t)(tc0 + j) * epi.ld_bf16 + n] = b;
+                if (j & 1) packed[j >> 1] |= bits << 16;
+                else packed[j >> 1] = bits;
+              }
             }
-            if (epi.outT_bf16 && n < N) {  // columns past M are written as 0 (padding)
+            if (vec) {  // 16-byte rows of 8 columns, 4 per thread
+              sync();
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int idx = tid + 128 * k, j = idx >> 4, c8 = (idx & 15) * 8;
+                if (j < jn && n0 + c8 < N)
+                  *reinterpret_cast<uint4*>(epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + n0 + c8) =
+                      *reinterpret_cast<const uint4*>(&st16[j * 128 + c8]);
+              }
+              sync();  // the staging area is reused next
+            } else if (epi.outT_bf16 && n < N) {  // columns past M are written as 0 (padding)
               uint4* dst = reinterpret_cast<uint4*>(epi.outT_bf16 + (size_t)n * epi.ldT + tc0);
 #pragma unroll
               for (int v = 0; v < 4; ++v)
@@ -459,57 +482,83 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           if (kind == EPI_SWIGLU) {
-            // tile = 64 gate | 64 up columns: stage rstd-scaled values, then
-            // thread (column pair, 8 tokens) forms act = silu(g) u, bf16x2 stores
+            // tile = 64 gate | 64 up columns: stage the rstd-scaled values, then
+            // 16-byte stores: the bf16 gate|up copy (8 columns x 1 token per
+            // thread-step) and act = silu(g) u (8 act columns x 1 token)
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const float rj = __shfl_sync(0xffffffffu, rs, j);
-              const float v = __uint_as_float(r[j]) * rj;
-              tile[j * kPitch + tid] = v;
-              if (epi.out2_bf16 && j < jn) epi.out2_bf16[(size_t)(tc0 + j) * N + n] = __float2bfloat16(v);
+              tile[j * kPitch + tid] = __uint_as_float(r[j]) * rj;
             }
             sync();
-            const int cp = 2 * (tid & 31), jb = (tid >> 5) * 8;
+            if (epi.out2_bf16) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int j = jb + u;
-              if (j >= jn) break;
-              const float2 gg = *reinterpret_cast<const float2*>(&tile[j * kPitch + cp]);
-              const float2 uu = *reinterpret_cast<const float2*>(&tile[j * kPitch + 64 + cp]);
-              const float a0 = gg.x / (1.f + expf(-gg.x)) * uu.x;
-              const float a1 = gg.y / (1.f + expf(-gg.y)) * uu.y;
-              *reinterpret_cast<__nv_bfloat162*>(epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + (n0 >> 1) + cp) =
-                  __floats2bfloat162_rn(a0, a1);
+              for (int k = 0; k < 4; ++k) {
+                const int idx = tid + 128 * k, j = idx >> 4, c8 = (idx & 15) * 8;
+                if (j >= jn) continue;
+                const float4 x0 = *reinterpret_cast<const float4*>(&tile[j * kPitch + c8]);
+                const float4 x1 = *reinterpret_cast<const float4*>(&tile[j * kPitch + c8 + 4]);
+                uint4 o;
+                o.x = bf2_bits(x0.x, x0.y); o.y = bf2_bits(x0.z, x0.w);
+                o.z = bf2_bits(x1.x, x1.y); o.w = bf2_bits(x1.z, x1.w);
+                *reinterpret_cast<uint4*>(epi.out2_bf16 + (size_t)(tc0 + j) * N + n0 + c8) = o;
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int idx = tid + 128 * k, j = idx >> 3, c8 = (idx & 7) * 8;
+              if (j >= jn) continue;
+              float g[8], u[8];
+              *reinterpret_cast<float4*>(&g[0]) = *reinterpret_cast<const float4*>(&tile[j * kPitch + c8]);
+              *reinterpret_cast<float4*>(&g[4]) = *reinterpret_cast<const float4*>(&tile[j * kPitch + c8 + 4]);
+              *reinterpret_cast<float4*>(&u[0]) = *reinterpret_cast<const float4*>(&tile[j * kPitch + 64 + c8]);
+              *reinterpret_cast<float4*>(&u[4]) = *reinterpret_cast<const float4*>(&tile[j * kPitch + 64 + c8 + 4]);
+              float a[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) a[e] = g[e] / (1.f + expf(-g[e])) * u[e];
+              uint4 o;
+              o.x = bf2_bits(a[0], a[1]); o.y = bf2_bits(a[2], a[3]);
+              o.z = bf2_bits(a[4], a[5]); o.w = bf2_bits(a[6], a[7]);
+              *reinterpret_cast<uint4*>(epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + (n0 >> 1) + c8) = o;
             }
             sync();  // the staged chunk is reused next
             continue;
           }
           if (kind == EPI_SWIGLU_BWD) {
-            // column n = act index j of 64-block b: gate at 128 b + (j & 63), up 64 after
-            if (n < N) {
-              const size_t gcol = (size_t)(n >> 6) * 128 + (n & 63);
-              // all 64 gate / up loads in flight before the first store
-              uint16_t gb[32], ub[32];
-              const uint16_t* gu = reinterpret_cast<const uint16_t*>(epi.gu_in);
+            // column n = act index of 64-block b: gate at 128 b + (n & 63), up 64
+            // after; the tile's 256 dgu columns of a token are contiguous
+            // (2 n0 ..), staged as bf16 and written as 16-byte rows
+            const int lc = (tid >> 6) * 128 + (tid & 63);  // tile-local gate column
+            uint16_t* st16 = reinterpret_cast<uint16_t*>(tile);  // [32][256]
+            const size_t gcol = (size_t)2 * n0 + lc;
+            // all 64 gate / up loads in flight before the first store
+            uint16_t gb[32], ub[32];
+            const uint16_t* gu = reinterpret_cast<const uint16_t*>(epi.gu_in);
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const size_t row = (size_t)(tc0 + (j < jn ? j : 0)) * epi.ld_bf16;
-                gb[j] = __ldg(gu + row + gcol);
-                ub[j] = __ldg(gu + row + gcol + 64);
-              }
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                if (j >= jn) continue;
-                const size_t row = (size_t)(tc0 + j) * epi.ld_bf16;
-                const float gv = __bfloat162float(__ushort_as_bfloat16(gb[j]));
-                const float uv = __bfloat162float(__ushort_as_bfloat16(ub[j]));
-                const float da = __uint_as_float(r[j]);
-                const float sg = 1.f / (1.f + expf(-gv));  // as swiglu_bwd_kernel
-                const float silu = gv * sg;
-                epi.out_bf16[row + gcol] = __float2bfloat16(da * uv * (sg * (1.f + gv * (1.f - sg))));
-                epi.out_bf16[row + gcol + 64] = __float2bfloat16(da * silu);
-              }
+            for (int j = 0; j < 32; ++j) {
+              const size_t row = (size_t)(tc0 + (j < jn ? j : 0)) * epi.ld_bf16;
+              gb[j] = n < N ? __ldg(gu + row + gcol) : (uint16_t)0;
+              ub[j] = n < N ? __ldg(gu + row + gcol + 64) : (uint16_t)0;
             }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float gv = __bfloat162float(__ushort_as_bfloat16(gb[j]));
+              const float uv = __bfloat162float(__ushort_as_bfloat16(ub[j]));
+              const float da = __uint_as_float(r[j]);
+              const float sg = 1.f / (1.f + expf(-gv));  // as swiglu_bwd_kernel
+              const float silu = gv * sg;
+              st16[j * 256 + lc] = __bfloat16_as_ushort(__float2bfloat16(da * uv * (sg * (1.f + gv * (1.f - sg)))));
+              st16[j * 256 + lc + 64] = __bfloat16_as_ushort(__float2bfloat16(da * silu));
+            }
+            sync();
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int idx = tid + 128 * k, j = idx >> 5, c8 = (idx & 31) * 8;
+              if (j < jn && n0 + (c8 >> 1) < N)
+                *reinterpret_cast<uint4*>(epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + 2 * n0 + c8) =
+                    *reinterpret_cast<const uint4*>(&st16[j * 256 + c8]);
+            }
+            sync();  // the staging area is reused next
             continue;
           }
           if (n < N) {
