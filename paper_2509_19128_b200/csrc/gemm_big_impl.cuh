@@ -561,6 +561,60 @@ __global__ void __launch_bounds__(kThreads, 1)
             sync();  // the staging area is reused next
             continue;
           }
+          {
+            // store / accumulate through a staged fp32 chunk: 16-byte rows, the
+            // accumulate's loads all in flight before its stores
+            const bool bf = kind == EPI_STORE_BF16;
+            const int ld = bf ? epi.ld_bf16 : epi.ld_out;
+            const void* base = bf ? static_cast<const void*>(epi.out_bf16) : static_cast<const void*>(epi.out_f32);
+            const bool vec = (N & 7) == 0 && (ld & 7) == 0 && (reinterpret_cast<uintptr_t>(base) & 15) == 0;
+            if (vec) {
+              const bool acc_kind = kind == EPI_ACCUM_F32;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const float rj = __shfl_sync(0xffffffffu, rs, j);
+                const float v = __uint_as_float(r[j]);
+                tile[j * kPitch + tid] = acc_kind ? epi.scale * v : v * rj + bias;
+              }
+              sync();
+              if (bf) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const int idx = tid + 128 * k, j = idx >> 4, c8 = (idx & 15) * 8;
+                  if (j >= jn || n0 + c8 >= N) continue;
+                  const float4 x0 = *reinterpret_cast<const float4*>(&tile[j * kPitch + c8]);
+                  const float4 x1 = *reinterpret_cast<const float4*>(&tile[j * kPitch + c8 + 4]);
+                  uint4 o;
+                  o.x = bf2_bits(x0.x, x0.y); o.y = bf2_bits(x0.z, x0.w);
+                  o.z = bf2_bits(x1.x, x1.y); o.w = bf2_bits(x1.z, x1.w);
+                  *reinterpret_cast<uint4*>(epi.out_bf16 + (size_t)(tc0 + j) * ld + n0 + c8) = o;
+                }
+              } else {
+                float4 cur[8];
+                if (acc_kind) {
+#pragma unroll
+                  for (int k = 0; k < 8; ++k) {
+                    const int idx = tid + 128 * k, j = idx >> 5, c4 = (idx & 31) * 4;
+                    cur[k] = (j < jn && n0 + c4 < N)
+                                 ? *reinterpret_cast<const float4*>(epi.out_f32 + (size_t)(tc0 + j) * ld + n0 + c4)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+                  }
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                  const int idx = tid + 128 * k, j = idx >> 5, c4 = (idx & 31) * 4;
+                  if (j >= jn || n0 + c4 >= N) continue;
+                  float4 v = *reinterpret_cast<const float4*>(&tile[j * kPitch + c4]);
+                  if (acc_kind) {
+                    v.x += cur[k].x; v.y += cur[k].y; v.z += cur[k].z; v.w += cur[k].w;
+                  }
+                  *reinterpret_cast<float4*>(epi.out_f32 + (size_t)(tc0 + j) * ld + n0 + c4) = v;
+                }
+              }
+              sync();  // the staged chunk is reused next
+              continue;
+            }
+          }
           if (n < N) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
