@@ -18,7 +18,6 @@ constexpr int kBN = 128;  // weight rows per tile (UMMA M)
 constexpr int kBK = 64;   // k-block (128-B swizzle row)
 constexpr int kThreads = 384;
 constexpr int kChunk = 32;  // tokens per epilogue chunk
-constexpr int kQb = 8;      // EPI_QKV: tokens whose cos / sin loads are in flight together
 constexpr int kPitch = kBN;  // drain writes are lane-contiguous: no padding needed
 
 template <int TOK>
@@ -220,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool direct = kind == EPI_STORE_F32 || kind == EPI_STORE_BF16 ||
                         kind == EPI_ACCUM_F32 || kind == EPI_DLOGITS ||
                         kind == EPI_SWIGLU_BWD || kind == EPI_RESID ||
-                        (kind == EPI_QKV && 128 % epi.hd == 0) ||
+                        (kind == EPI_QKV && 128 % epi.hd == 0 && epi.hd % 8 == 0 && N % 8 == 0) ||
                         (kind == EPI_SWIGLU && direct_swiglu_ok(epi, N)) || stats_only;
     float* red = tile;  // stats_only: [4 warps][32 tokens] cross-warp partials (the unused staging tile)
     bool waited = false;
@@ -426,59 +425,61 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           if (kind == EPI_QKV) {
-            // v = rstd acc + bias staged (RoPE pairs live in other warps); the
-            // row's slot / position / page held by lane j and broadcast; the
-            // cos / sin of 8 tokens in flight together
+            // v = rstd acc + bias staged (RoPE pairs live in other warps) with
+            // each token's (position, page); then thread-steps of 8 consecutive
+            // columns of one token: cos / sin as two float4 each, one 16-byte
+            // store into q or the K / V page
             const bool colok = n < N;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const float rj = __shfl_sync(0xffffffffu, rs, j);
               tile[j * kPitch + tid] = (colok && j < jn) ? __uint_as_float(r[j]) * rj + bias : 0.f;
             }
+            if (tid < 32) s_row[tid] = make_int4(rc.x, rc.y, 0, 0);
             sync();
             const int hd = epi.hd, half = hd >> 1;
             const int qend = epi.nq * hd, kend = (epi.nq + epi.nkv) * hd;
-            const int jj = n % hd, i = jj < half ? jj : jj - half, hb = tid - jj;
-            const bool rot = n < kend;
 #pragma unroll
-            for (int jb = 0; jb < 32; jb += kQb) {
-              float co[kQb], si[kQb];
+            for (int k = 0; k < 4; ++k) {
+              const int idx = tid + 128 * k, j = idx >> 4, c8 = (idx & 15) * 8, nn = n0 + c8;
+              if (j >= jn || nn >= N) continue;
+              const int4 rr = s_row[j];
+              const int ps = rr.x;
+              if (ps < 0) continue;  // free slot / padding row
+              const int jj = nn % hd, hb = c8 - jj;
+              const float* row = &tile[j * kPitch + hb];
+              float y[8];
+              if (nn < kend) {  // RoPE on q and k: pairs (i, i + hd/2)
+                const int i0 = jj < half ? jj : jj - half;
+                const float4* cs = reinterpret_cast<const float4*>(epi.cos_sin + (size_t)ps * hd);
+                float co[8], si[8];
+                *reinterpret_cast<float4*>(&co[0]) = cs[i0 / 4];
+                *reinterpret_cast<float4*>(&co[4]) = cs[i0 / 4 + 1];
+                *reinterpret_cast<float4*>(&si[0]) = cs[(half + i0) / 4];
+                *reinterpret_cast<float4*>(&si[4]) = cs[(half + i0) / 4 + 1];
 #pragma unroll
-              for (int u = 0; u < kQb; ++u) {
-                const int ps = __shfl_sync(0xffffffffu, rc.x, jb + u);
-                co[u] = 1.f;
-                si[u] = 0.f;
-                if (rot && colok && ps >= 0) {
-                  co[u] = epi.cos_sin[(size_t)ps * hd + i];
-                  si[u] = epi.cos_sin[(size_t)ps * hd + half + i];
+                for (int e = 0; e < 8; ++e) {
+                  const float x1 = row[i0 + e], x2 = row[i0 + e + half];
+                  y[e] = jj < half ? x1 * co[e] - x2 * si[e] : x2 * co[e] + x1 * si[e];
                 }
+              } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) y[e] = row[jj + e];
               }
-#pragma unroll
-              for (int u = 0; u < kQb; ++u) {
-                const int j = jb + u, m = tc0 + j;
-                const int ps = __shfl_sync(0xffffffffu, rc.x, j);
-                const int page = __shfl_sync(0xffffffffu, rc.y, j);
-                if (!colok || ps < 0) continue;  // also rows past M and free slots
-                const float* row = &tile[j * kPitch + hb];
-                float y;
-                if (rot) {
-                  const float x1 = row[i], x2 = row[i + half];
-                  y = jj < half ? x1 * co[u] - x2 * si[u] : x2 * co[u] + x1 * si[u];
-                } else {
-                  y = row[jj];
-                }
-                const __nv_bfloat16 b = __float2bfloat16(y);
-                if (n < qend) {
-                  epi.q_out[(size_t)m * qend + n] = b;
-                } else {
-                  const int kv = n < kend ? n - qend : n - kend;
-                  const size_t at = (((size_t)page * epi.nkv + kv / hd) * 64 + ps % 64) * hd + jj;
-                  if (n < kend) epi.kc[at] = b;
-                  else epi.vc[at] = b;
-                }
+              uint4 o;
+              o.x = bf2_bits(y[0], y[1]); o.y = bf2_bits(y[2], y[3]);
+              o.z = bf2_bits(y[4], y[5]); o.w = bf2_bits(y[6], y[7]);
+              __nv_bfloat16* dst;
+              if (nn < qend) {
+                dst = epi.q_out + (size_t)(tc0 + j) * qend + nn;
+              } else {
+                const int kv = nn < kend ? nn - qend : nn - kend;
+                const size_t at = (((size_t)rr.y * epi.nkv + kv / hd) * 64 + ps % 64) * hd + jj;
+                dst = (nn < kend ? epi.kc : epi.vc) + at;
               }
+              *reinterpret_cast<uint4*>(dst) = o;
             }
-            sync();  // the staged chunk is reused next
+            sync();  // the staged chunk and s_row are reused next
             continue;
           }
           if (kind == EPI_SWIGLU) {
