@@ -272,6 +272,10 @@ def recompute_pause_measure(cfg, pol, payload_policy, args, rounds=128):
             "note": f"{args.batch} streams, recompute mode: full-prefix KV rebuild at the swap"}
 
 
+HOSTPROF = os.environ.get("SRL_BENCH_HOSTPROF") == "1"
+HOSTPROF_ACC = {"advance": 0.0, "publish": 0.0, "drain": 0.0, "refill": 0.0}
+
+
 def pipeline_measure(cfg, args, steps=6):
     """The whole PipelineRL loop time-shared on ONE GPU (paper_2509_19128_b200/
     pipeline.py): constant-batch generator -> actor queue -> IS-REINFORCE
@@ -388,6 +392,7 @@ def main():
         st0 = eng.stats()
         t_wall = time.perf_counter()
         emitted = eng.advance(R)
+        t_adv = time.perf_counter()
         # in-flight update: trainer rank 0's weights -> every standby buffer
         # (ncclBroadcast for N > 1, a device copy at N = 1) -> swap at the next
         # token boundary; the streams continue on their stale KV cache
@@ -400,6 +405,7 @@ def main():
                                                    engine=standby)
             e1.record(s)
         s.synchronize()
+        t_pub = time.perf_counter()
         assert applied, "weight update rejected"
         # actor side: drain events, refill finished streams (constant batch)
         finished = []
@@ -409,10 +415,17 @@ def main():
             live[sid].extend(e.weight_version for e in evs)
             if not more or reason != "running":
                 finished.append(sid)
+        t_drain = time.perf_counter()
         for sid in finished:
             token_versions.append(live.pop(sid))
             open_one(0, args.gen)
         wall = time.perf_counter() - t_wall
+        if HOSTPROF and record is not None:  # SRL_BENCH_HOSTPROF=1: host split of the e2e step
+            hp = HOSTPROF_ACC
+            hp["advance"] += t_adv - t_wall
+            hp["publish"] += t_pub - t_adv
+            hp["drain"] += t_drain - t_pub
+            hp["refill"] += time.perf_counter() - t_drain
         st1 = eng.stats()
         upd_ms = e0.elapsed_time(e1)
         dev_ms = (st1["decode_ms"] - st0["decode_ms"]) + upd_ms + pause
@@ -521,6 +534,9 @@ def main():
 
     value = total_tokens / (dev_ms_max * 1e-3)
     e2e = total_tokens / (wall_ms_max * 1e-3)
+    if HOSTPROF:
+        print("host ms/step", {k: round(1e3 * v / args.steps, 3) for k, v in HOSTPROF_ACC.items()},
+              "device ms/step", round(dev_ms / args.steps, 3), file=sys.stderr)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
