@@ -409,8 +409,8 @@ def main():
         assert applied, "weight update rejected"
         # actor side: drain events, refill finished streams (constant batch)
         finished = []
-        for sid in list(live):
-            evs, reason, more = eng.wait_events(sid)
+        drained = eng.wait_events_many(list(live))
+        for sid, (evs, reason, more) in drained.items():
             d2h_bytes += 24 * len(evs)
             live[sid].extend(e.weight_version for e in evs)
             if not more or reason != "running":

@@ -151,6 +151,12 @@ int srl_engine_open_stream(srl_engine* e, const char* prompt_id, int32_t max_tok
  * up to cap events; *more = the reference's return value. */
 int srl_engine_wait_events(srl_engine* e, int64_t stream, srl_token_event* buf, int32_t cap,
                            int32_t* n_out, int32_t* finish_reason, int32_t* more);
+/* One wait_events per listed stream in one call (the actor's per-step drain):
+ * stream i's events follow stream i-1's in buf, counts[i] of them (cap shared;
+ * a stream whose events do not fit gets more[i] = 1 and keeps the rest). */
+int srl_engine_wait_events_many(srl_engine* e, const int64_t* streams, int32_t n_streams,
+                                srl_token_event* buf, int32_t cap, int32_t* counts,
+                                int32_t* finish_reasons, int32_t* more);
 /* apply_weight_update (engine.cpp:79-117).  Returns SRL_VERSION_CONFLICT /
  * SRL_INVALID_POLICY / SRL_POLICY_MISMATCH without side effects. */
 int srl_engine_apply_weight_update(srl_engine* e, int32_t new_version, const srl_policy* policy,

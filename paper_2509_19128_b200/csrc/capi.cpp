@@ -281,6 +281,33 @@ extern "C" int srl_engine_wait_events(srl_engine* e, int64_t stream, srl_token_e
   });
 }
 
+extern "C" int srl_engine_wait_events_many(srl_engine* e, const int64_t* streams, int32_t n_streams,
+                                           srl_token_event* buf, int32_t cap, int32_t* counts,
+                                           int32_t* finish_reasons, int32_t* more) {
+  return guarded([&] {
+    if (!e || !streams || n_streams < 0 || !buf || cap < 1 || !counts || !finish_reasons || !more)
+      return fail(SRL_INVALID_ARGUMENT, "wait_events_many: bad arguments");
+    int32_t used = 0;
+    std::vector<srl_token_event> out;
+    for (int32_t i = 0; i < n_streams; ++i) {
+      int reason = 0, m = 0;
+      out.clear();
+      if (used < cap) {
+        const int st = e->e->wait_events(streams[i], out, cap - used, &reason, &m);
+        if (st != SRL_OK) return st;
+      } else {
+        m = 1;  // no room left: the stream keeps its events for the next call
+      }
+      std::copy(out.begin(), out.end(), buf + used);
+      counts[i] = (int32_t)out.size();
+      used += counts[i];
+      finish_reasons[i] = reason;
+      more[i] = m;
+    }
+    return (int)SRL_OK;
+  });
+}
+
 extern "C" int srl_engine_apply_weight_update(srl_engine* e, int32_t new_version,
                                               const srl_policy* policy, int32_t* version_out) {
   return guarded([&] {

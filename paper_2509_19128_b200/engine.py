@@ -122,6 +122,30 @@ class Engine:
                 break
         return events, FINISH[reason.value], bool(more.value)
 
+    def wait_events_many(self, stream_ids):
+        """wait_events for each listed stream in ONE native call (the actor's
+        per-step drain): {stream_id: (events, finish_reason, more)}.  A stream
+        whose events did not fit in the buffer reports more=True."""
+        ids = np.array([self._sid(s) for s in stream_ids], dtype=np.int64)
+        k = len(ids)
+        counts = np.zeros(k, dtype=np.int32)
+        reasons = np.zeros(k, dtype=np.int32)
+        more = np.zeros(k, dtype=np.int32)
+        st = _lib.lib().srl_engine_wait_events_many(self._h, ids.ctypes.data, k, self._evbuf, len(self._evbuf),
+                                                    counts.ctypes.data, reasons.ctypes.data, more.ctypes.data)
+        _raise_for(st, "wait_events_many")
+        total = int(counts.sum())
+        a = self._evarr[:total]
+        pos, tok, lp, ver = (a["position"].tolist(), a["token"].tolist(), a["logprob"].tolist(),
+                             a["weight_version"].tolist())
+        out = {}
+        o = 0
+        for sid, c, r, m in zip(stream_ids, counts.tolist(), reasons.tolist(), more.tolist()):
+            out[sid] = (list(map(TokenEvent, repeat(sid, c), pos[o:o + c], tok[o:o + c], lp[o:o + c],
+                                 ver[o:o + c])), FINISH[r], bool(m))
+            o += c
+        return out
+
     def collect(self, stream_id: str):
         """Drain a stream to completion: (events, finish_reason)."""
         out = []

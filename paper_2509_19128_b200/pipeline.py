@@ -163,8 +163,9 @@ class PipelineRL:
         self.engine.advance(self.rounds_per_poll)
         self.round += self.rounds_per_poll
         finished = []
+        drained = self.engine.wait_events_many(list(self.live))
         for sid, seq in list(self.live.items()):
-            evs, reason, more = self.engine.wait_events(sid)
+            evs, reason, more = drained[sid]
             for e in evs:
                 seq.tokens.append(e.token)
                 seq.behavior_logprobs.append(e.logprob)

@@ -189,3 +189,28 @@ def test_policy_logprobs_toy(cuda, orc):
     assert np.allclose(got, exp, rtol=LP_REL, atol=0)
     with pytest.raises(ValueError):
         rlmath.policy_logprobs(policy_from_dict(g["v0"]), "demo", [6])
+
+
+def test_wait_events_many_matches_per_stream_drain(cuda):
+    """The batched drain (one native call for many streams) returns what
+    per-stream wait_events returns on an identical engine, including a stream
+    that finished and one whose events stay behind for the next call."""
+    g = GOLDEN["demo_scenario"]
+
+    def run(batched):
+        eng = Engine(policy_from_dict(g["v0"]), start_paused=True, max_streams=4, max_seq_len=64)
+        sids = [eng.open_stream("demo", n, 7 + i) for i, n in enumerate([3, 9, 9])]
+        got = []
+        for _ in range(3):
+            eng.advance(4)
+            if batched:
+                d = eng.wait_events_many(sids)
+                got.append([(d[s][0], d[s][1], d[s][2]) for s in sids])
+            else:
+                got.append([eng.wait_events(s) for s in sids])
+        eng.close()
+        return got
+
+    a, b = run(True), run(False)
+    assert [[(evs, r, m) for evs, r, m in step] for step in a] == [[tuple(x) for x in step] for step in b]
+    assert a[0][0][1] == "length" and len(a[0][1][0]) == 4
