@@ -409,10 +409,10 @@ def main():
         assert applied, "weight update rejected"
         # actor side: drain events, refill finished streams (constant batch)
         finished = []
-        drained = eng.wait_events_many(list(live))
+        drained = eng.wait_events_many(list(live), columns=True)
         for sid, (evs, reason, more) in drained.items():
             d2h_bytes += 24 * len(evs)
-            live[sid].extend(e.weight_version for e in evs)
+            live[sid].extend(evs.weight_version.tolist())
             if not more or reason != "running":
                 finished.append(sid)
         t_drain = time.perf_counter()

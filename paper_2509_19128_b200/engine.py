@@ -39,6 +39,19 @@ class TokenEvent:
     weight_version: int
 
 
+@dataclass(slots=True)
+class EventColumns:
+    """A stream's drained events as columns (wait_events_many(columns=True))."""
+
+    position: np.ndarray
+    token: np.ndarray
+    logprob: np.ndarray
+    weight_version: np.ndarray
+
+    def __len__(self):
+        return len(self.token)
+
+
 @dataclass
 class UpdateResult:
     """UpdateResult (engine.hpp:34-38)."""
@@ -122,10 +135,12 @@ class Engine:
                 break
         return events, FINISH[reason.value], bool(more.value)
 
-    def wait_events_many(self, stream_ids):
+    def wait_events_many(self, stream_ids, columns: bool = False):
         """wait_events for each listed stream in ONE native call (the actor's
         per-step drain): {stream_id: (events, finish_reason, more)}.  A stream
-        whose events did not fit in the buffer reports more=True."""
+        whose events did not fit in the buffer reports more=True.  columns=True
+        returns each stream's events as an EventColumns of numpy arrays instead
+        of TokenEvent objects (no per-event Python object)."""
         ids = np.array([self._sid(s) for s in stream_ids], dtype=np.int64)
         k = len(ids)
         counts = np.zeros(k, dtype=np.int32)
@@ -136,6 +151,15 @@ class Engine:
         _raise_for(st, "wait_events_many")
         total = int(counts.sum())
         a = self._evarr[:total]
+        if columns:
+            out = {}
+            o = 0
+            for sid, c, r, m in zip(stream_ids, counts.tolist(), reasons.tolist(), more.tolist()):
+                b = a[o:o + c]
+                out[sid] = (EventColumns(b["position"].copy(), b["token"].copy(), b["logprob"].copy(),
+                                         b["weight_version"].copy()), FINISH[r], bool(m))
+                o += c
+            return out
         pos, tok, lp, ver = (a["position"].tolist(), a["token"].tolist(), a["logprob"].tolist(),
                              a["weight_version"].tolist())
         out = {}

@@ -214,3 +214,14 @@ def test_wait_events_many_matches_per_stream_drain(cuda):
     a, b = run(True), run(False)
     assert [[(evs, r, m) for evs, r, m in step] for step in a] == [[tuple(x) for x in step] for step in b]
     assert a[0][0][1] == "length" and len(a[0][1][0]) == 4
+    # the columnar form carries the same fields
+    eng = Engine(policy_from_dict(g["v0"]), start_paused=True, max_streams=4, max_seq_len=64)
+    sids = [eng.open_stream("demo", n, 7 + i) for i, n in enumerate([3, 9, 9])]
+    eng.advance(4)
+    cols = eng.wait_events_many(sids, columns=True)
+    for s, (evs, r, m) in zip(sids, a[0]):
+        c, rc, mc = cols[s]
+        assert (rc, mc) == (r, m) and c.token.tolist() == [e.token for e in evs]
+        assert c.logprob.tolist() == [e.logprob for e in evs] and c.position.tolist() == [e.position for e in evs]
+        assert c.weight_version.tolist() == [e.weight_version for e in evs]
+    eng.close()
