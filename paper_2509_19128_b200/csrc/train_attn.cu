@@ -77,14 +77,20 @@ __device__ __forceinline__ const __nv_bfloat16* page_row(const __nv_bfloat16* c,
 // X[64][HD + 8] and, if XT, its transpose XT[HD][64 + 8].
 template <int HD, class Src>
 __device__ __forceinline__ void stage_bf16(__nv_bfloat16* X, __nv_bfloat16* XT, int valid, Src src) {
-  constexpr int P = HD + 8, V8 = HD / 8;
-  for (int e = threadIdx.x; e < kBlk * V8; e += kWarps * 32) {
-    const int r = e / V8, c = (e % V8) * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < valid) v = *reinterpret_cast<const uint4*>(src(r) + c);
-    *reinterpret_cast<uint4*>(X + r * P + c) = v;
+  constexpr int P = HD + 8, V8 = HD / 8, NV = kBlk * V8 / (kWarps * 32);
+  // every load of the tile in flight before the first shared-memory store
+  uint4 v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int e = threadIdx.x + k * kWarps * 32, r = e / V8, c = (e % V8) * 8;
+    v[k] = r < valid ? *reinterpret_cast<const uint4*>(src(r) + c) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int e = threadIdx.x + k * kWarps * 32, r = e / V8, c = (e % V8) * 8;
+    *reinterpret_cast<uint4*>(X + r * P + c) = v[k];
     if (XT) {
-      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v);
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v[k]);
 #pragma unroll
       for (int i = 0; i < 8; ++i) XT[(c + i) * kPadT + r] = h[i];
     }
@@ -93,13 +99,18 @@ __device__ __forceinline__ void stage_bf16(__nv_bfloat16* X, __nv_bfloat16* XT, 
 // Same for an fp32 source (dO), rounded to bf16.
 template <int HD, class Src>
 __device__ __forceinline__ void stage_f32(__nv_bfloat16* X, __nv_bfloat16* XT, int valid, Src src) {
-  constexpr int P = HD + 8, V4 = HD / 4;
-  for (int e = threadIdx.x; e < kBlk * V4; e += kWarps * 32) {
-    const int r = e / V4, c = (e % V4) * 4;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < valid) v = *reinterpret_cast<const float4*>(src(r) + c);
-    const __nv_bfloat16 h[4] = {__float2bfloat16(v.x), __float2bfloat16(v.y), __float2bfloat16(v.z),
-                                __float2bfloat16(v.w)};
+  constexpr int P = HD + 8, V4 = HD / 4, NV = kBlk * V4 / (kWarps * 32);
+  float4 v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int e = threadIdx.x + k * kWarps * 32, r = e / V4, c = (e % V4) * 4;
+    v[k] = r < valid ? *reinterpret_cast<const float4*>(src(r) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int e = threadIdx.x + k * kWarps * 32, r = e / V4, c = (e % V4) * 4;
+    const __nv_bfloat16 h[4] = {__float2bfloat16(v[k].x), __float2bfloat16(v[k].y), __float2bfloat16(v[k].z),
+                                __float2bfloat16(v[k].w)};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       X[r * P + c + i] = h[i];
@@ -400,12 +411,18 @@ __global__ void __launch_bounds__(kWarps * 32)
     __syncthreads();
     stage_bf16<HD>(Ks, nullptr, kvalid, [&](int r) { return page_row(kc, bt, pps, slot, k0 + r, nkv, kh, HD); });
     {  // V^T [HD][64]
-      constexpr int V8 = HD / 8;
-      for (int e = threadIdx.x; e < kBlk * V8; e += kWarps * 32) {
-        const int r = e / V8, c = (e % V8) * 8;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (r < kvalid) v = *reinterpret_cast<const uint4*>(page_row(vc, bt, pps, slot, k0 + r, nkv, kh, HD) + c);
-        const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&v);
+      constexpr int V8 = HD / 8, NV = kBlk * V8 / (kWarps * 32);
+      uint4 v[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int e = threadIdx.x + k * kWarps * 32, r = e / V8, c = (e % V8) * 8;
+        v[k] = r < kvalid ? *reinterpret_cast<const uint4*>(page_row(vc, bt, pps, slot, k0 + r, nkv, kh, HD) + c)
+                          : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int e = threadIdx.x + k * kWarps * 32, r = e / V8, c = (e % V8) * 8;
+        const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&v[k]);
 #pragma unroll
         for (int i = 0; i < 8; ++i) Vt[(c + i) * kPadT + r] = hv[i];
       }
