@@ -75,18 +75,28 @@ __device__ __forceinline__ const __nv_bfloat16* page_row(const __nv_bfloat16* c,
 
 // Stage 64 rows x HD of a bf16 source (row r -> src(r) or zeros past L) into
 // X[64][HD + 8] and, if XT, its transpose XT[HD][64 + 8].
+template <int HD>
+constexpr int kNvB = kBlk * (HD / 8) / (kWarps * 32);  // uint4 per thread of a bf16 tile
+template <int HD>
+constexpr int kNvF = kBlk * (HD / 4) / (kWarps * 32);  // float4 per thread of an fp32 tile
+
+// Load a 64 x HD bf16 tile (row r -> src(r), zeros past `valid`) into registers
+// -- every load in flight together -- and store it into X[64][HD + 8] and,
+// if XT, its transpose XT[HD][64 + 8].
 template <int HD, class Src>
-__device__ __forceinline__ void stage_bf16(__nv_bfloat16* X, __nv_bfloat16* XT, int valid, Src src) {
-  constexpr int P = HD + 8, V8 = HD / 8, NV = kBlk * V8 / (kWarps * 32);
-  // every load of the tile in flight before the first shared-memory store
-  uint4 v[NV];
+__device__ __forceinline__ void load_bf16(uint4 (&v)[kNvB<HD>], int valid, Src src) {
+  constexpr int V8 = HD / 8;
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
+  for (int k = 0; k < kNvB<HD>; ++k) {
     const int e = threadIdx.x + k * kWarps * 32, r = e / V8, c = (e % V8) * 8;
     v[k] = r < valid ? *reinterpret_cast<const uint4*>(src(r) + c) : make_uint4(0, 0, 0, 0);
   }
+}
+template <int HD>
+__device__ __forceinline__ void store_bf16(__nv_bfloat16* X, __nv_bfloat16* XT, const uint4 (&v)[kNvB<HD>]) {
+  constexpr int P = HD + 8, V8 = HD / 8;
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
+  for (int k = 0; k < kNvB<HD>; ++k) {
     const int e = threadIdx.x + k * kWarps * 32, r = e / V8, c = (e % V8) * 8;
     *reinterpret_cast<uint4*>(X + r * P + c) = v[k];
     if (XT) {
@@ -96,18 +106,27 @@ __device__ __forceinline__ void stage_bf16(__nv_bfloat16* X, __nv_bfloat16* XT, 
     }
   }
 }
+template <int HD, class Src>
+__device__ __forceinline__ void stage_bf16(__nv_bfloat16* X, __nv_bfloat16* XT, int valid, Src src) {
+  uint4 v[kNvB<HD>];
+  load_bf16<HD>(v, valid, src);
+  store_bf16<HD>(X, XT, v);
+}
 // Same for an fp32 source (dO), rounded to bf16.
 template <int HD, class Src>
-__device__ __forceinline__ void stage_f32(__nv_bfloat16* X, __nv_bfloat16* XT, int valid, Src src) {
-  constexpr int P = HD + 8, V4 = HD / 4, NV = kBlk * V4 / (kWarps * 32);
-  float4 v[NV];
+__device__ __forceinline__ void load_f32(float4 (&v)[kNvF<HD>], int valid, Src src) {
+  constexpr int V4 = HD / 4;
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
+  for (int k = 0; k < kNvF<HD>; ++k) {
     const int e = threadIdx.x + k * kWarps * 32, r = e / V4, c = (e % V4) * 4;
     v[k] = r < valid ? *reinterpret_cast<const float4*>(src(r) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+}
+template <int HD>
+__device__ __forceinline__ void store_f32(__nv_bfloat16* X, __nv_bfloat16* XT, const float4 (&v)[kNvF<HD>]) {
+  constexpr int P = HD + 8, V4 = HD / 4;
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
+  for (int k = 0; k < kNvF<HD>; ++k) {
     const int e = threadIdx.x + k * kWarps * 32, r = e / V4, c = (e % V4) * 4;
     const __nv_bfloat16 h[4] = {__float2bfloat16(v[k].x), __float2bfloat16(v[k].y), __float2bfloat16(v[k].z),
                                 __float2bfloat16(v[k].w)};
@@ -117,6 +136,12 @@ __device__ __forceinline__ void stage_f32(__nv_bfloat16* X, __nv_bfloat16* XT, i
       if (XT) XT[(c + i) * kPadT + r] = h[i];
     }
   }
+}
+template <int HD, class Src>
+__device__ __forceinline__ void stage_f32(__nv_bfloat16* X, __nv_bfloat16* XT, int valid, Src src) {
+  float4 v[kNvF<HD>];
+  load_f32<HD>(v, valid, src);
+  store_f32<HD>(X, XT, v);
 }
 
 template <int HD>
@@ -168,18 +193,50 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int kr = warp * 16;  // this warp's 16 keys (block-local)
   const int key_lo = k0 + kr + (lane >> 2), key_hi = key_lo + 8;
 
+  // (query head g, query block q0) tiles in order; with HD = 64 the next
+  // tile's loads are issued before this tile's MMAs (registers: Q 16, dO 32)
+  constexpr bool kPipe = HD == 64;
+  uint4 pq[kPipe ? kNvB<HD> : 1];
+  float4 pd[kPipe ? kNvF<HD> : 1];
+  float pl = 0.f, pD = 0.f;
+  static_assert(kWarps * 32 >= kBlk, "one lse / D row per thread");
+  auto fetch = [&](int g, int q0) {
+    if constexpr (kPipe) {
+      const int h = kh * G + g, qvalid = min(kBlk, L - q0);
+      load_bf16<HD>(pq, qvalid, [&](int r) { return q + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+      load_f32<HD>(pd, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+      const int r = threadIdx.x;
+      pl = r < qvalid ? lse[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
+      pD = r < qvalid ? D[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
+    }
+  };
+  fetch(0, k0);
   for (int g = 0; g < G; ++g) {
     const int h = kh * G + g;
     for (int q0 = k0; q0 < L; q0 += kBlk) {
       const int qvalid = min(kBlk, L - q0);
       __syncthreads();  // previous tiles consumed
-      stage_bf16<HD>(Qs, Qt, qvalid, [&](int r) { return q + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
-      stage_f32<HD>(dOs, dOt, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
-      for (int r = threadIdx.x; r < kBlk; r += kWarps * 32) {
-        s_lse[r] = r < qvalid ? lse[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
-        s_D[r] = r < qvalid ? D[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
+      if constexpr (kPipe) {
+        store_bf16<HD>(Qs, Qt, pq);
+        store_f32<HD>(dOs, dOt, pd);
+        if (threadIdx.x < kBlk) {
+          s_lse[threadIdx.x] = pl;
+          s_D[threadIdx.x] = pD;
+        }
+      } else {
+        stage_bf16<HD>(Qs, Qt, qvalid, [&](int r) { return q + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+        stage_f32<HD>(dOs, dOt, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+        for (int r = threadIdx.x; r < kBlk; r += kWarps * 32) {
+          s_lse[r] = r < qvalid ? lse[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
+          s_D[r] = r < qvalid ? D[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
+        }
       }
       __syncthreads();
+      if constexpr (kPipe) {  // the next tile's loads fly during this tile's MMAs
+        int g2 = g, q2 = q0 + kBlk;
+        if (q2 >= L) { ++g2; q2 = k0; }
+        if (g2 < G) fetch(g2, q2);
+      }
       // S^T = K_w Q^T and dP^T = V_w dO^T: [16 keys x 64 queries]
       float st[8][4], dpt[8][4];
 #pragma unroll
