@@ -104,6 +104,13 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
   dev_ = w.device;
   SRL_CUDA(cudaSetDevice(dev_));
   SRL_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  {  // the step's stream-ordered scratch (block tables, attention partials) stays
+     // mapped between steps instead of returning to the driver at every sync
+    cudaMemPool_t pool;
+    uint64_t keep = UINT64_MAX;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev_) == cudaSuccess)
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   int st;
   if ((st = clone_decoder(w, weights_))) return st;
   lay_ = weights_->layout;
