@@ -348,8 +348,12 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
 
   // ---- pass 1: log pi(target) of every row
   const int nT = (V + 127) / 128;
-  for (int c0 = 0; c0 < T; c0 += chunk_) {
-    const int C = std::min(chunk_, T - c0);
+  // LM-head row chunks of equal size (<= chunk_, a multiple of 256): a short
+  // tail chunk ran at half the rate of a full one
+  const int n_chunks = (T + chunk_ - 1) / chunk_;
+  const int cb = std::min(chunk_, ((T + n_chunks - 1) / n_chunks + 255) / 256 * 256);
+  for (int c0 = 0; c0 < T; c0 += cb) {
+    const int C = std::min(cb, T - c0);
     EpiParams e;
     e.kind = EPI_LOGITS;
     e.ssq_in = ssq_ + (size_t)c0 * parts; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d_.eps;
@@ -407,8 +411,8 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
   // both operands MN-major (tokens as K), input gradients take W MN-major.
   // pass 2: dlogits per chunk -> d(final xg) and dE(lm_head)
   float* g_lm = grad_ + lay_.lm_head;
-  for (int c0 = 0; c0 < T; c0 += chunk_) {
-    const int C = std::min(chunk_, T - c0);
+  for (int c0 = 0; c0 < T; c0 += cb) {
+    const int C = std::min(cb, T - c0);
     // dlogits = coef (onehot - softmax) straight from the LM-head accumulator
     // (lse of pass 1: same weights, same logits)
     EpiParams e;
