@@ -69,6 +69,9 @@ KernelTimer::~KernelTimer() {
 // ------------------------------------------------------------- runner ---
 DecoderRunner::~DecoderRunner() {
   for (void* p : allocs_) cudaFree(p);
+  if (fork_) cudaEventDestroy(fork_);
+  if (join_) cudaEventDestroy(join_);
+  if (side_) cudaStreamDestroy(side_);
 }
 
 int DecoderRunner::init(const DecoderDims& dims, const WeightLayout& layout, int slots, int max_seq,
@@ -84,6 +87,9 @@ int DecoderRunner::init(const DecoderDims& dims, const WeightLayout& layout, int
   dev = device;
   st_ = st;
   sms = sm_count(device);
+  SRL_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  SRL_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+  SRL_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
   unfused_qkv = std::getenv("SRL_UNFUSED_QKV") != nullptr;  // A/B switch: separate RoPE kernel
   const int H = d.H, parts = d.ssq_parts();
   auto alloc = [&](auto** p, size_t n) -> int {
@@ -191,13 +197,22 @@ int DecoderRunner::forward(int M, const __nv_bfloat16* w, const WeightMaps& wm) 
     }
     tb(4);
     if (n_seg > 0) {
-      // prompt segments on the tensor cores, the single decode rows per row
-      if (n_single > 0)
+      // prompt segments on the tensor cores, the single decode rows per row --
+      // on a side stream, concurrently (disjoint output rows; both small)
+      const bool side = n_single > 0 && timer == nullptr;
+      if (n_single > 0) {
+        if (side) {
+          SRL_CUDA(cudaEventRecord(fork_, st_));
+          SRL_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
+        }
         launch_attention(q, d, plan, n_single, block_table, pages_per_seq, kcl, vcl, max_seq, attn_ws,
-                         attn_counters, attn_ws_floats, attn, st_);
+                         attn_counters, attn_ws_floats, attn, side ? side_ : st_);
+        if (side) SRL_CUDA(cudaEventRecord(join_, side_));
+      }
       SRL_CUDA(launch_attention_fwd_mma(q, kcl, vcl, seg, seg + S, block_table, pages_per_seq, n_seg, d.nq,
                                         d.nkv, d.hd, attn, nullptr, st_, seg + 2 * S, seg + 3 * S,
                                         seg_max_rows));
+      if (side) SRL_CUDA(cudaStreamWaitEvent(st_, join_, 0));
     } else {
       launch_attention(q, d, plan, M, block_table, pages_per_seq, kcl, vcl, max_seq, attn_ws,
                        attn_counters, attn_ws_floats, attn, st_);

@@ -77,6 +77,9 @@ struct DecoderRunner {
 
  private:
   cudaStream_t st_ = nullptr;
+  // a prefill round's single-row attention runs beside the segment attention
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t fork_ = nullptr, join_ = nullptr;
   std::vector<void*> allocs_;
 };
 
