@@ -160,6 +160,18 @@ int DecoderRunner::init(const DecoderDims& dims, const WeightLayout& layout, int
 
 int DecoderRunner::gemm(const CUtensorMap& tw, const CUtensorMap* tx, int M, int N, int K,
                         const EpiParams& e) {
+  static const bool lm_big = [] {
+    const char* v = std::getenv("SRL_LM_BIG");
+    return !(v && v[0] == '0');
+  }();
+  if (lm_big && M <= 64 && e.kind == EPI_LOGITS && (N + 127) / 128 >= 4 * sms) {
+    // the LM head of <= 64 rows (a prefill round's slots, the multi-kernel
+    // decode): the persistent kernel streams the vocabulary tiles through its
+    // ring (the split-K kernel pays a pipeline fill per 128-row tile)
+    const cudaError_t err = gemm_big_launch(tw, tx[1], M, N, K, 128, e, st_);
+    if (err != cudaSuccess) return cuda_fail(err, "gemm_big_launch (lm head)");
+    return SRL_OK;
+  }
   const int splits = gemm_auto_splits(M, N, K, sms);
   const CUtensorMap& x_map = tx[gemm_tok_tile(M) == 64 ? 0 : 1];
   const cudaError_t err = gemm_bf16_launch(tw, x_map, M, N, K, splits, gws, e, st_);
