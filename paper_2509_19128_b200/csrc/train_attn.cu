@@ -349,12 +349,31 @@ __global__ void __launch_bounds__(kWarps * 32)
 #pragma unroll
     for (int i = 0; i < 4; ++i) dq[n][i] = 0.f;
 
+  // with HD = 64 the next key block's K / V loads fly during this block's MMAs
+  constexpr bool kPipe = HD == 64;
+  uint4 pk[kPipe ? kNvB<HD> : 1], pv[kPipe ? kNvB<HD> : 1];
+  auto fetch = [&](int k0) {
+    if constexpr (kPipe) {
+      const int kvalid = min(kBlk, L - k0);
+      load_bf16<HD>(pk, kvalid, [&](int r) { return page_row(kc, bt, pps, slot, k0 + r, nkv, kh, HD); });
+      load_bf16<HD>(pv, kvalid, [&](int r) { return page_row(vc, bt, pps, slot, k0 + r, nkv, kh, HD); });
+    }
+  };
+  fetch(0);
   for (int k0 = 0; k0 <= q0; k0 += kBlk) {
     const int kvalid = min(kBlk, L - k0);
     __syncthreads();
-    stage_bf16<HD>(Ks, Kt, kvalid, [&](int r) { return page_row(kc, bt, pps, slot, k0 + r, nkv, kh, HD); });
-    stage_bf16<HD>(Vs, nullptr, kvalid, [&](int r) { return page_row(vc, bt, pps, slot, k0 + r, nkv, kh, HD); });
+    if constexpr (kPipe) {
+      store_bf16<HD>(Ks, Kt, pk);
+      store_bf16<HD>(Vs, nullptr, pv);
+    } else {
+      stage_bf16<HD>(Ks, Kt, kvalid, [&](int r) { return page_row(kc, bt, pps, slot, k0 + r, nkv, kh, HD); });
+      stage_bf16<HD>(Vs, nullptr, kvalid, [&](int r) { return page_row(vc, bt, pps, slot, k0 + r, nkv, kh, HD); });
+    }
     __syncthreads();
+    if constexpr (kPipe) {
+      if (k0 + kBlk <= q0) fetch(k0 + kBlk);
+    }
     float s[8][4], dp[8][4];
 #pragma unroll
     for (int n = 0; n < 8; ++n)
