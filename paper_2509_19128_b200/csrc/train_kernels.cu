@@ -244,6 +244,81 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ dzw, const float* _
   for (int k = threadIdx.x; k < H; k += blockDim.x) atomicAdd(&dg[k], s_dg[k]);
 }
 
+// The same for H <= 32 * 4 * NV: a lane keeps its columns' dz, x, gain and the
+// gain-gradient partials in registers (one pass over the row, one shared
+// atomic per column per warp instead of one per element).
+template <int NV>
+__global__ void __launch_bounds__(256)
+    rmsnorm_bwd_reg_kernel(const float* __restrict__ dzw, const float* __restrict__ x,
+                           const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd, int T,
+                           int H, float* __restrict__ dx, float* __restrict__ dg) {
+  extern __shared__ float s_dg[];
+  for (int k = threadIdx.x; k < H; k += blockDim.x) s_dg[k] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int H4 = H / 4;
+  float4 gv[NV], acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int k = lane + 32 * i;
+    acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    gv[i] = acc[i];
+    if (k < H4) {
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(g + 4 * k);
+      const float2 ga = __bfloat1622float2(g2[0]), gb = __bfloat1622float2(g2[1]);
+      gv[i] = make_float4(ga.x, ga.y, gb.x, gb.y);
+    }
+  }
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < T; r += gridDim.x * (blockDim.x >> 5)) {
+    const float4* dz4 = reinterpret_cast<const float4*>(dzw + (size_t)r * H);
+    const float4* x4 = reinterpret_cast<const float4*>(x + (size_t)r * H);
+    float4* dx4 = reinterpret_cast<float4*>(dx + (size_t)r * H);
+    const float rs = rstd[r];
+    float4 d[NV], v[NV], o[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int k = lane + 32 * i;
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      d[i] = k < H4 ? dz4[k] : z;
+      v[i] = k < H4 ? x4[k] : z;
+      o[i] = k < H4 ? dx4[k] : z;
+    }
+    float dr = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      dr += d[i].x * v[i].x * gv[i].x + d[i].y * v[i].y * gv[i].y + d[i].z * v[i].z * gv[i].z +
+            d[i].w * v[i].w * gv[i].w;
+#pragma unroll
+    for (int s = 16; s; s >>= 1) dr += __shfl_xor_sync(0xffffffffu, dr, s);
+    const float coef = -rs * rs * rs / (float)H * dr;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int k = lane + 32 * i;
+      if (k >= H4) continue;
+      o[i].x += rs * d[i].x * gv[i].x + coef * v[i].x;
+      o[i].y += rs * d[i].y * gv[i].y + coef * v[i].y;
+      o[i].z += rs * d[i].z * gv[i].z + coef * v[i].z;
+      o[i].w += rs * d[i].w * gv[i].w + coef * v[i].w;
+      dx4[k] = o[i];
+      acc[i].x += rs * d[i].x * v[i].x;
+      acc[i].y += rs * d[i].y * v[i].y;
+      acc[i].z += rs * d[i].z * v[i].z;
+      acc[i].w += rs * d[i].w * v[i].w;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int k = lane + 32 * i;
+    if (k >= H4) continue;
+    atomicAdd(&s_dg[4 * k], acc[i].x);
+    atomicAdd(&s_dg[4 * k + 1], acc[i].y);
+    atomicAdd(&s_dg[4 * k + 2], acc[i].z);
+    atomicAdd(&s_dg[4 * k + 3], acc[i].w);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < H; k += blockDim.x) atomicAdd(&dg[k], s_dg[k]);
+}
+
 __global__ void swiglu_bwd_kernel(const float* __restrict__ dact, const __nv_bfloat16* __restrict__ gu,
                                   int T, int I, __nv_bfloat16* __restrict__ dgu,
                                   float* __restrict__ dgu_f32) {
@@ -503,7 +578,18 @@ void launch_rmsnorm_bwd(const float* dzw, const float* x, const __nv_bfloat16* g
                         const float* rstd, int T, int H, float* dx, float* dg, cudaStream_t st) {
   if (T < 1) return;
   const int blocks = std::min((T + 7) / 8, 2 * num_sms());
-  rmsnorm_bwd_kernel<<<blocks, 256, sizeof(float) * H, st>>>(dzw, x, g, rstd, T, H, dx, dg);
+  const size_t sm = sizeof(float) * H;
+  switch ((H / 4 + 31) / 32) {  // float4 columns per lane
+    case 1: rmsnorm_bwd_reg_kernel<1><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
+    case 2: rmsnorm_bwd_reg_kernel<2><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
+    case 3: rmsnorm_bwd_reg_kernel<3><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
+    case 4: rmsnorm_bwd_reg_kernel<4><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
+    case 5: rmsnorm_bwd_reg_kernel<5><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
+    case 6: rmsnorm_bwd_reg_kernel<6><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
+    case 7: rmsnorm_bwd_reg_kernel<7><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
+    case 8: rmsnorm_bwd_reg_kernel<8><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
+    default: rmsnorm_bwd_kernel<<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg);
+  }
 }
 void launch_row_rstd(const float* x, int T, int H, float eps, float* rstd, cudaStream_t st) {
   if (T > 0) row_rstd_kernel<<<(T + 7) / 8, 256, 0, st>>>(x, T, H, eps, rstd);
