@@ -28,21 +28,6 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// block reduce (any blockDim multiple of 32, <= 1024)
-__device__ float block_sum(float v, float* red) {
-  v = warp_sum(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  float t = threadIdx.x < (blockDim.x >> 5) ? red[l] : 0.f;
-  if (w == 0) {
-    t = warp_sum(t);
-    if (l == 0) red[32] = t;
-  }
-  __syncthreads();
-  return red[32];
-}
 __device__ double block_sum_dd(double v, double* red) {
   v = warp_sum_d(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -83,6 +68,14 @@ __global__ void transpose_kernel(const In* __restrict__ src, const float* __rest
 __global__ void f32_to_bf16_kernel(const float* __restrict__ s, size_t n, __nv_bfloat16* __restrict__ d) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     d[i] = __float2bfloat16(s[i]);
+}
+// 4 elements per step (16-byte loads, 8-byte stores; n % 4 == 0, aligned)
+__global__ void f32_to_bf16_x4_kernel(const float4* __restrict__ s, size_t n4, uint2* __restrict__ d) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 v = s[i];
+    const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    d[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+  }
 }
 __global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ s, size_t n, float* __restrict__ d) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -367,6 +360,27 @@ __global__ void attn_bwd_dot_kernel(const float* __restrict__ d_o, const __nv_bf
   s = warp_sum(s);
   if (lane == 0) D[warp] = s;
 }
+// D = rowsum(dO * O) per (row, head) with L = hd / 8 lanes per pair, 8 elements
+// per lane (two float4 of dO, one 16-byte load of O); hd in {32, 64, 128, 256}
+template <int L>
+__global__ void attn_bwd_dot_v_kernel(const float* __restrict__ d_o, const __nv_bfloat16* __restrict__ o,
+                                      int pairs, int hd, float* __restrict__ D) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x, p = t / L, j = t % L;
+  float s = 0.f;
+  if (p < pairs) {
+    const size_t base = (size_t)p * hd + j * 8;
+    const float4 a = *reinterpret_cast<const float4*>(d_o + base);
+    const float4 b = *reinterpret_cast<const float4*>(d_o + base + 4);
+    const uint4 ov = *reinterpret_cast<const uint4*>(o + base);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&ov);
+    const float2 o0 = __bfloat1622float2(h[0]), o1 = __bfloat1622float2(h[1]), o2 = __bfloat1622float2(h[2]),
+                 o3 = __bfloat1622float2(h[3]);
+    s = a.x * o0.x + a.y * o0.y + a.z * o1.x + a.w * o1.y + b.x * o2.x + b.y * o2.y + b.z * o3.x + b.w * o3.y;
+  }
+#pragma unroll
+  for (int w = L / 2; w; w >>= 1) s += __shfl_xor_sync(0xffffffffu, s, w);
+  if (p < pairs && j == 0) D[p] = s;
+}
 
 __device__ __forceinline__ const __nv_bfloat16* kv_row(const __nv_bfloat16* c, const int32_t* bt,
                                                        int pps, int slot, int pos, int nkv, int kh,
@@ -487,8 +501,14 @@ __global__ void colsum_kernel(const float* __restrict__ src, int rows, int cols,
   if (c >= cols) return;
   const int chunk = (rows + gridDim.y - 1) / gridDim.y;
   const int r0 = blockIdx.y * chunk, r1 = min(rows, r0 + chunk);
-  float s = 0.f;
-  for (int r = r0; r < r1; ++r) s += src[(size_t)r * cols + c];
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 loads in flight
+  int r = r0;
+  for (; r + 8 <= r1; r += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] += src[(size_t)(r + u) * cols + c];
+  }
+  for (; r < r1; ++r) a[0] += src[(size_t)r * cols + c];
+  const float s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   atomicAdd(&out[c], s);
 }
 
@@ -551,6 +571,12 @@ void launch_swiglu_fwd(const float* gu, int T, int I, __nv_bfloat16* act, cudaSt
   swiglu_fwd_kernel<<<grid_for((size_t)T * I, 256), 256, 0, st>>>(gu, T, I, act);
 }
 void launch_f32_to_bf16(const float* src, size_t n, __nv_bfloat16* dst, cudaStream_t st) {
+  if (n % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+    const size_t n4 = n / 4;
+    f32_to_bf16_x4_kernel<<<(int)std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * 16), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(src), n4, reinterpret_cast<uint2*>(dst));
+    return;
+  }
   f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(src, n, dst);
 }
 void launch_scale_rows_bf16(const __nv_bfloat16* src, const float* row_scale, int rows, int cols,
@@ -607,7 +633,12 @@ void launch_attention_bwd(const __nv_bfloat16* q, const __nv_bfloat16* o, const 
   float* D = nullptr;
   cudaMallocAsync(&D, sizeof(float) * (size_t)T * nq, st);
   const int w1 = T * nq;
-  attn_bwd_dot_kernel<<<(w1 * 32 + 255) / 256, 256, 0, st>>>(d_o, o, T, nq, hd, D);
+  if (hd == 64)
+    attn_bwd_dot_v_kernel<8><<<(w1 * 8 + 255) / 256, 256, 0, st>>>(d_o, o, w1, hd, D);
+  else if (hd == 128)
+    attn_bwd_dot_v_kernel<16><<<(w1 * 16 + 255) / 256, 256, 0, st>>>(d_o, o, w1, hd, D);
+  else
+    attn_bwd_dot_kernel<<<(w1 * 32 + 255) / 256, 256, 0, st>>>(d_o, o, T, nq, hd, D);
   static const bool scalar = std::getenv("SRL_ATTN_BWD_SCALAR") != nullptr;  // A/B: the CUDA-core path
   if (!scalar) {
     launch_attention_bwd_mma(q, d_o, lse, D, kc, vc, seq_start, seq_len, block_table, pages_per_seq,
