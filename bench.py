@@ -2,28 +2,41 @@
 """PipelineRL generator hot path on B200: generated tokens/s with in-flight
 weight updates, weight-update pause, token lag.
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on; its
-generator side fits one GPU): Qwen2.5-0.5B-shaped random-init bf16 policy,
-constant generation batch 64 (Algorithm 2: finished streams are refilled with
-new synthetic prompts at once), one in-flight weight update per optimizer
-step.  One bench step = one optimizer-step period: R decode rounds of the
-whole batch, then the update (the trainer's fresh weights land in the standby
-buffer -- ncclBroadcast from rank 0 for N > 1, a device copy at N = 1 -- and
-are swapped in at the next token boundary; streams continue on their stale
-KV cache).
+Workload (N = 1): BASELINE.json's largest single-GPU configuration -- the
+1-GPU point of configs[4]'s scaling sweep on the Qwen2.5-1.5B shape, with
+configs[2]'s 8k-token synthetic reasoning rollouts: random-init bf16 weights,
+constant generation batch 64 (Algorithm 2: a finished stream is replaced by a
+new synthetic prompt at once), rollouts of up to 8192 generated tokens.  The
+batch starts in the steady state of such a generator: stream i is a rollout
+already (i + 0.5)/64 of the way through (its prefix is prefilled before the
+timed region), so contexts are spread uniformly over 64..8256 tokens.  One
+bench step = one optimizer-step period: R decode rounds of the whole batch
+while the trainer's fresh weights stream into the standby buffer on a side
+stream, then the swap at the next token boundary (the streams continue on
+their stale KV cache).
 
-  value         tokens / device time (CUDA events on the engine stream + the
-                update copy/broadcast + the swap pause), max over ranks
-  e2e           the same through the public API (Engine.advance / wait_events
-                / open_stream / begin/commit_weight_update), wall clock: every
-                step includes the H2D prompts of refilled streams and the D2H
-                token events, plus the host-side event collection
-  roofline      the dominant kernel class of a decode round, timed with CUDA
-                events around each launch of a profiled round
-  cpu_baseline  the CPU oracle port of the same decoder (oracle/, numpy fp32,
-                all host cores) on a bounded sample of the workload
+  value         tokens / device time (CUDA events on the engine stream, plus
+                the swap pause and any transfer time not hidden under decode)
+  e2e           the same through the public API (Engine.advance /
+                begin/commit_weight_update / wait_events_many / open_stream),
+                host wall clock: every step includes the H2D prompts of
+                refilled streams and the D2H token events
+  pause         swap_ms = the decode loop blocked by the pointer swap;
+                decode_stall_ms = (step time with the update in flight) -
+                (step time without an update): what the update costs decode
+  lag           per consumed sequence (sim.cpp:63-104): version at consumption
+                minus the version that emitted each token
+  roofline      the decode megakernel (one launch per round), CUDA events
+  cpu_baseline  the CPU port of the same decode round (oracle/decoder_cpu.py,
+                numpy fp32 on all host cores) on the same streams and contexts
 
-Inputs: weights (0.99 GB) are larger than L2 (126 MB) and stream every round.
+N > 1 (torchrun, or --gpus N which relaunches itself under torchrun): the
+partitioned PipelineRL of paper_2509_19128_b200/pipeline_dist.py -- trainer
+ranks (data-parallel, gradient all-reduce) and generator ranks (weight
+broadcast into their standby buffers), 1+1 / 2+2 / 4+4 / 6+2 (--trainers).
+
+Inputs: weights (3.09 GB) and KV caches (~7.6 GB) are larger than L2
+(126 MB) and stream every round.
 """
 from __future__ import annotations
 
@@ -47,24 +60,30 @@ KERNEL_CLASSES = ["plan", "embed", "qkv_gemm", "rope_kv_append", "attention", "o
                   "gate_up_gemm", "down_gemm", "lm_head_gemm", "sample"]
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="qwen2.5-0.5b")
+    ap.add_argument("--config", default="qwen2.5-1.5b")
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--prompt", type=int, default=64)
-    ap.add_argument("--gen", type=int, default=256, help="max_tokens per stream")
+    ap.add_argument("--gen", type=int, default=8192, help="max generated tokens per rollout")
     ap.add_argument("--rounds", type=int, default=32, help="decode rounds per optimizer step")
+    ap.add_argument("--no-steady", action="store_true",
+                    help="start every stream at its prompt instead of the steady-state spread")
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=4)
     ap.add_argument("--no-trainer", action="store_true", help="skip the trainer-step measurement")
     ap.add_argument("--no-pipeline", action="store_true", help="skip the one-GPU PipelineRL loop")
+    ap.add_argument("--no-extra", action="store_true", help="skip the 0.5B / 7B generator lines")
+    ap.add_argument("--extra", default="qwen2.5-0.5b:64:256,qwen2.5-7b:256:1024",
+                    help="extra generator configs name:batch:gen (N = 1)")
     ap.add_argument("--train-seqs", type=int, default=64, help="trajectories per trainer step")
-    return ap.parse_args()
+    ap.add_argument("--train-gen", type=int, default=256, help="generated tokens per trainer trajectory")
+    ap.add_argument("--trainers", type=int, default=None, help="trainer ranks of the partition (N > 1)")
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -72,6 +91,19 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: one process per GPU."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 # --------------------------------------------------------------- clocks ---
@@ -95,6 +127,7 @@ class ClockSampler:
             self.thread.start()
         except FileNotFoundError:
             self.proc = None
+        return self
 
     def _read(self):
         for line in self.proc.stdout:
@@ -159,39 +192,6 @@ def load_traffic():
     return {}
 
 
-# -------------------------------------------------------- CPU baseline ---
-def cpu_decode_sample(cfg, batch, prompt, steps, warmup=0, seed=0):
-    """The oracle port (oracle/decoder_oracle.py, numpy fp32, BLAS on all host
-    cores) decoding `steps` rounds of `batch` streams after a short prefill.
-    Returns (tokens/s, seconds, cores)."""
-    from oracle.decoder_oracle import DecoderOracle, layout
-
-    _, total = layout(cfg.to_dict())
-    rng = np.random.default_rng(seed)
-    w = (rng.standard_normal(total, dtype=np.float32) * 0.02).view(np.uint32)
-    w = (w >> 16).astype(np.uint16)
-    off, _ = layout(cfg.to_dict())
-    for name, (o, n) in off.items():  # unit norm gains like the device init
-        if name.endswith("ln1") or name.endswith("ln2") or name == "final_norm":
-            w[o:o + n] = 0x3F80
-    m = DecoderOracle(cfg.to_dict(), w, np.float32)
-    caches = [m.new_cache() for _ in range(batch)]
-    prompts = rng.integers(0, cfg.vocab_size, size=(batch, prompt))
-    toks = np.full(batch, cfg.bos_token)
-    for p in range(prompt + 1):
-        logits = m.step(caches, toks, np.full(batch, p))
-        toks = prompts[:, p] if p < prompt else logits.argmax(-1)
-    for _ in range(warmup):
-        logits = m.step(caches, toks, np.full(batch, len(caches[0]["tokens"])))
-        toks = logits.argmax(-1)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        logits = m.step(caches, toks, np.full(batch, len(caches[0]["tokens"])))
-        toks = logits.argmax(-1)
-    dt = time.perf_counter() - t0
-    return batch * steps / dt, dt, os.cpu_count()
-
-
 def matmul_params(cfg):
     """Parameters that enter a GEMM per token (all projections + LM head)."""
     H, I, L, V = cfg.hidden, cfg.intermediate, cfg.layers, cfg.vocab_size
@@ -199,13 +199,31 @@ def matmul_params(cfg):
     return L * (qkv * H + H * qd + 2 * I * H + H * I) + V * H
 
 
+def pipeline_max_lag_steps(gen_batch, inference_count, max_len, mean_len, train_batch):
+    """g_max = ceil(H * I * L / (mean L * B)) (throughput.cpp:260-269)."""
+    import math
+
+    return int(math.ceil(gen_batch * inference_count * max_len / (mean_len * train_batch)))
+
+
+def steady_contexts(B, prompt, gen):
+    """Stream i of a steady-state constant-batch generator is (i + 0.5)/B of
+    the way through its rollout: (prefix tokens after the prompt, tokens left)."""
+    out = []
+    for i in range(B):
+        done = int((i + 0.5) * gen / B)
+        out.append((done, gen - done))
+    return out
+
+
+# ---------------------------------------------------------- trainer side ---
 def trainer_measure(cfg, pol, n_seq, prompt, gen, steps=3):
-    """Trainer side of config 2: one optimizer step =
-    current-policy log-prob recompute + truncated-IS REINFORCE objective + full
-    backward + Adam over n_seq trajectories of prompt + gen tokens.  Device
-    time from the trainer's own CUDA events (srl_trainer_stats.step_ms) plus
-    the Adam kernel; tensor throughput counts 6 * matmul params per token plus
-    causal attention (fwd 4 * T^2/2 * nq * hd per layer and sequence, x3)."""
+    """Trainer side: one optimizer step = current-policy
+    log-prob recompute + truncated-IS REINFORCE objective + full backward +
+    Adam over n_seq trajectories of prompt + gen tokens.  Device time from the
+    trainer's own CUDA events (srl_trainer_stats.step_ms) plus the Adam
+    kernel; tensor throughput counts 6 * matmul params per token plus causal
+    attention (fwd 4 * T^2/2 * nq * hd per layer and sequence, x3)."""
     import torch
 
     from paper_2509_19128_b200.trainer import Trainer
@@ -239,7 +257,7 @@ def trainer_measure(cfg, pol, n_seq, prompt, gen, steps=3):
     t = float(np.median(ms))
     _, bf16, kind = load_peaks()
     tf = flops / (t * 1e-3) / 1e12
-    out = {"workload": f"{n_seq} trajectories x {seq} tokens ({tokens} scored rows), "
+    out = {"workload": f"{cfg.name}: {n_seq} trajectories x {seq} tokens ({tokens} scored rows), "
                        f"IS-REINFORCE fwd + bwd + Adam",
            "tokens_per_s": tokens / (t * 1e-3), "step_ms": t, "forward_ms": float(np.median(fwd)),
            "tflops": tf, "bound": "tensor", "peak_tflops": bf16, "peak_kind": kind,
@@ -248,7 +266,7 @@ def trainer_measure(cfg, pol, n_seq, prompt, gen, steps=3):
     return out
 
 
-def recompute_pause_measure(cfg, pol, payload_policy, args, rounds=128):
+def recompute_pause_measure(cfg, pol, payload_policy, B, prompt, rounds=128):
     """The same in-flight update with the engine in recompute mode
     (engine.cpp:107-113): at the swap every live stream's KV cache is rebuilt
     from its full prefix under the new weights (chunked prefill, tensor-core
@@ -256,337 +274,442 @@ def recompute_pause_measure(cfg, pol, payload_policy, args, rounds=128):
     cache.  B streams of prompt + `rounds` generated tokens."""
     from paper_2509_19128_b200.engine import Engine
 
-    eng = Engine(pol, recompute_state=True, start_paused=True, max_streams=args.batch,
-                 max_seq_len=args.prompt + rounds + 8, rounds_per_sync=32,
-                 prefill_budget=args.batch * (args.prompt + 1))
+    eng = Engine(pol, recompute_state=True, start_paused=True, max_streams=B,
+                 max_seq_len=prompt + rounds + 8, rounds_per_sync=32,
+                 prefill_budget=B * (prompt + 1))
     rng = np.random.default_rng(5)
-    for i in range(args.batch):
-        eng.open_stream("p", rounds + 4, i, -1, rng.integers(0, cfg.vocab_size, size=args.prompt).tolist())
+    for i in range(B):
+        eng.open_stream("p", rounds + 4, i, -1, rng.integers(0, cfg.vocab_size, size=prompt).tolist())
     eng.advance(rounds)
-    ctx = sum(len(eng.stream_tokens(f"s{i}")) for i in range(args.batch))
+    ctx = sum(len(eng.stream_tokens(f"s{i}")) for i in range(B))
     res = eng.apply_weight_update(1, payload_policy)
     assert res.applied
     pause = eng.stats()["last_pause_ms"]
     eng.close()
     return {"ms": pause, "rebuilt_tokens": ctx,
-            "note": f"{args.batch} streams, recompute mode: full-prefix KV rebuild at the swap"}
+            "note": f"{B} streams, recompute mode: full-prefix KV rebuild at the swap"}
 
 
-HOSTPROF = os.environ.get("SRL_BENCH_HOSTPROF") == "1"
-HOSTPROF_ACC = {"advance": 0.0, "publish": 0.0, "drain": 0.0, "refill": 0.0}
-
-
-def pipeline_measure(cfg, args, steps=6):
+def pipeline_measure(cfg, B, prompt, gen, rounds, steps=6):
     """The whole PipelineRL loop time-shared on ONE GPU (paper_2509_19128_b200/
     pipeline.py): constant-batch generator -> actor queue -> IS-REINFORCE
     trainer step on every train_batch finished sequences -> in-flight update.
-    Config 2 puts generator and trainer on two GPUs; here they alternate, so
-    tokens_per_s_wall is a lower bound for that configuration."""
+    Per consumed batch: the lag statistics of make_step_record (sim.cpp:63-104)
+    and the analytic bound g_max (throughput.cpp:260-269) for this loop."""
     from paper_2509_19128_b200.pipeline import PipelineRL
     from paper_2509_19128_b200.policy import DecoderPolicy
 
     pol = DecoderPolicy.random(cfg, seed=1, scale=0.02)
-    pl = PipelineRL(pol, batch=args.batch, prompt_len=args.prompt, max_tokens=args.gen,
-                    train_batch=args.batch, queue_capacity=4 * args.batch, rounds_per_poll=args.rounds,
-                    n_prompts=8, lr=1e-5, seed=0)
+    pl = PipelineRL(pol, batch=B, prompt_len=prompt, max_tokens=gen, train_batch=B,
+                    queue_capacity=4 * B, rounds_per_poll=rounds, n_prompts=8, lr=1e-5, seed=0)
     pl.run(optimizer_steps=1)  # warm-up
     rep = pl.run(optimizer_steps=steps)
     pl.close()
-    return {"workload": f"{cfg.name}, batch {args.batch}, train batch {args.batch} sequences of "
-                        f"{args.prompt} + {args.gen} tokens, {steps} optimizer steps",
+    mean_len = float(np.mean([st.mean_length for st in rep.steps]))
+    return {"workload": f"{cfg.name}, batch {B}, train batch {B} sequences of "
+                        f"{prompt} + {gen} tokens, {steps} optimizer steps",
             "tokens_per_s_wall": rep.generated_tokens / rep.wall_s,
             "tokens_per_s_generating": rep.generated_tokens / rep.generate_s,
             "trainer_ms_per_step": 1e3 * rep.train_s / max(1, len(rep.steps)),
             "max_lag_steps": max(st.max_lag_steps for st in rep.steps),
             "mean_lag_steps": float(np.mean([st.mean_lag_steps for st in rep.steps])),
+            "sample_max_lag": max(st.sample_max_lag for st in rep.steps),
+            "g_max_analytic": pipeline_max_lag_steps(B, 1, gen, mean_len, B),
             "pause_ms_max": max(st.pause_ms for st in rep.steps),
             "stalls": rep.stalls, "evicted": rep.evicted}
 
 
-def reference_arm(args, cfg):
-    world, rank, _ = dist_env()
-    if rank != 0:
-        return
-    # each step = one decode round of the whole batch on the CPU port
-    batch = args.batch
-    prompt = min(args.prompt, 16)
-    tps, dt, cores = cpu_decode_sample(cfg, batch, prompt, args.steps, args.warmup)
-    line = {
-        "impl": "reference", "metric": METRIC, "value": tps, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic prompts, random-init weights",
-        "config": {"workload": f"{cfg.name} decode, batch {batch}, CPU oracle port",
-                   "global_batch": batch, "seq_len": prompt + 1 + args.steps,
-                   "parallelism": "cpu"},
-        "cpu_baseline": {"value": tps, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{batch} streams x {args.steps} decode rounds after a "
-                                   f"{prompt}-token prefill (reference has no decoder; "
-                                   f"oracle/decoder_oracle.py, numpy fp32)"},
-        "e2e": {"value": tps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-# --------------------------------------------------------------- ours ---
+# ------------------------------------------------------- generator side ---
 class _Raw:
     def __init__(self, ptr, nbytes):
         self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
                                          "data": (ptr, False), "version": 3}
 
 
-def main():
-    args = parse()
-    from paper_2509_19128_b200.policy import PRESETS
-
-    cfg = PRESETS[args.config]
-    if args.impl == "reference":
-        return reference_arm(args, cfg)
-
+def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use_graphs=True,
+                      device=0, n_payloads=2, profile=True, lag=True):
+    """One generator GPU: constant batch B, an in-flight update every R rounds
+    whose transfer into the standby buffer overlaps the decode rounds (a side
+    stream), swap at the token boundary after them.  Returns the measurement
+    dict (value / e2e / pause / stall / lag / roofline) and the policy."""
     import torch
-    import torch.distributed as dist
 
     from paper_2509_19128_b200 import _lib
     from paper_2509_19128_b200.engine import Engine
     from paper_2509_19128_b200.policy import DecoderPolicy
-    from paper_2509_19128_b200.weight_sync import EngineStandby, WeightChannel, max_over_ranks
 
-    world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-
-    # policy v0 and two alternating "trainer" payloads (random init, then drift)
-    pol = DecoderPolicy.random(cfg, seed=0, scale=0.02, device=local)
-    payloads = [pol.clone().perturb(1000 + i, 0.002) for i in range(2)]
-    B, R = args.batch, args.rounds
-    max_seq = args.prompt + 1 + args.gen + 1
+    dev = torch.device("cuda", device)
+    pol = DecoderPolicy.random(cfg, seed=0, scale=0.02, device=device)
+    payloads = [pol.clone().perturb(1000 + i, 0.002) for i in range(n_payloads)]
+    max_seq = prompt + 1 + gen + 1
     eng = Engine(pol, start_paused=True, max_streams=B, max_seq_len=max_seq,
-                 rounds_per_sync=R, event_ring=max(64, R), use_graphs=not args.no_graphs,
-                 device=local, prefill_budget=B * (args.prompt + 1))
-    rng = np.random.default_rng(1234 + rank)
+                 rounds_per_sync=R, event_ring=max(64, R), use_graphs=use_graphs, device=device,
+                 prefill_budget=max(B * (prompt + 1), max_seq))
+    rng = np.random.default_rng(1234 + device)
     live = {}
-    h2d_bytes = 0
-    d2h_bytes = 0
+    h2d = [0]
+    d2h = [0]
 
-    def open_one(i, max_tokens):
-        nonlocal h2d_bytes
-        pr = rng.integers(0, cfg.vocab_size, size=args.prompt).tolist()
-        sid = eng.open_stream("synthetic", max_tokens, int(rng.integers(0, 2**63)), -1, pr)
-        h2d_bytes += 4 * len(pr) + 24
+    def open_one(done=0, left=gen):
+        pr = rng.integers(0, cfg.vocab_size, size=prompt + done).tolist()
+        sid = eng.open_stream("synthetic", left, int(rng.integers(0, 2**63)), -1, pr)
+        h2d[0] += 4 * len(pr) + 24
         live[sid] = []
         return sid
 
-    # staggered initial lengths so finishes (and refills) spread over steps
-    for i in range(B):
-        open_one(i, max(8, args.gen - (i * args.gen) // B))
+    if steady:
+        for done, left in steady_contexts(B, prompt, gen):
+            open_one(done, left)
+    else:  # staggered lengths so finishes (and refills) spread over steps
+        for i in range(B):
+            open_one(0, max(8, gen - (i * gen) // B))
+    # seat every stream (prefill of the steady-state prefixes) before timing:
+    # a stream has been prefilled once it emitted its first token
+    waiting = set(live)
+    while waiting:
+        eng.advance(4)
+        for sid, (evs, reason, more) in eng.wait_events_many(list(live), columns=True).items():
+            live[sid].extend(evs.weight_version.tolist())
+            if len(evs) or reason != "running":
+                waiting.discard(sid)
+    side = torch.cuda.Stream(device=dev)
+    consumed = []       # (version at consumption, token versions) per finished sequence
+    version = [0]
 
-    token_versions = []  # finished sequences (for lag stats)
-    s = torch.cuda.Stream(device=dev)
-    chan = WeightChannel(src=0)
-    standby = EngineStandby(eng, dev)
-
-    def step(record):
-        nonlocal d2h_bytes
+    def step(record, update=True):
         st0 = eng.stats()
         t_wall = time.perf_counter()
+        copy_ms = 0.0
+        if update:
+            # the trainer's weights stream into the standby buffer on a side
+            # stream while the decode rounds run; the swap waits for the copy
+            nxt = version[0] + 1
+            ptr, n = eng.begin_weight_update(nxt)
+            src, _ = payloads[nxt % len(payloads)].weights()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(side):
+                e0.record(side)
+                torch.as_tensor(_Raw(ptr, n), device=dev).copy_(torch.as_tensor(_Raw(src, n), device=dev))
+                e1.record(side)
         emitted = eng.advance(R)
-        t_adv = time.perf_counter()
-        # in-flight update: trainer rank 0's weights -> every standby buffer
-        # (ncclBroadcast for N > 1, a device copy at N = 1) -> swap at the next
-        # token boundary; the streams continue on their stale KV cache
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        src, n = payloads[(chan.version + 1) % 2].weights()
-        payload = torch.as_tensor(_Raw(src, n), device=dev)
-        with torch.cuda.stream(s):
-            e0.record(s)
-            applied, _, pause = chan.publish(rank, None, payload if rank == 0 else None,
-                                                   engine=standby)
-            e1.record(s)
-        s.synchronize()
-        t_pub = time.perf_counter()
-        assert applied, "weight update rejected"
+        pause = 0.0
+        if update:
+            side.synchronize()
+            res, pause = eng.commit_weight_update(nxt)
+            assert res.applied, "weight update rejected"
+            version[0] = nxt
+            copy_ms = e0.elapsed_time(e1)
         # actor side: drain events, refill finished streams (constant batch)
         finished = []
         drained = eng.wait_events_many(list(live), columns=True)
         for sid, (evs, reason, more) in drained.items():
-            d2h_bytes += 24 * len(evs)
+            d2h[0] += 24 * len(evs)
             live[sid].extend(evs.weight_version.tolist())
             if not more or reason != "running":
                 finished.append(sid)
-        t_drain = time.perf_counter()
         for sid in finished:
-            token_versions.append(live.pop(sid))
-            open_one(0, args.gen)
+            consumed.append((version[0], live.pop(sid)))
+            open_one()
         wall = time.perf_counter() - t_wall
-        if HOSTPROF and record is not None:  # SRL_BENCH_HOSTPROF=1: host split of the e2e step
-            hp = HOSTPROF_ACC
-            hp["advance"] += t_adv - t_wall
-            hp["publish"] += t_pub - t_adv
-            hp["drain"] += t_drain - t_pub
-            hp["refill"] += time.perf_counter() - t_drain
         st1 = eng.stats()
-        upd_ms = e0.elapsed_time(e1)
-        dev_ms = (st1["decode_ms"] - st0["decode_ms"]) + upd_ms + pause
+        dec = st1["decode_ms"] - st0["decode_ms"]
+        dev_ms = dec + pause + max(0.0, copy_ms - dec)
         if record is not None:
-            record.append(dict(tokens=emitted, dev_ms=dev_ms, wall_ms=1000 * wall, pause_ms=pause,
+            record.append(dict(tokens=emitted, dev_ms=dev_ms, decode_ms=dec, wall_ms=1000 * wall,
+                               pause_ms=pause, copy_ms=copy_ms,
                                prefill_ms=st1["prefill_ms"] - st0["prefill_ms"],
                                prefill_rows=st1["prefill_rows"] - st0["prefill_rows"],
-                               update_ms=upd_ms, launches=st1["launches"] - st0["launches"],
-                               finished=len(finished)))
+                               launches=st1["launches"] - st0["launches"], finished=len(finished)))
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step(None)
-    # one profiled round (outside the timed region): per-kernel-class CUDA events
-    eng.profile_next_round()
-    eng.advance(2)  # a pending refill prefill may take the first round; the next decode round is profiled
-    prof = eng.kernel_profile()
-    fused_ms = []
-    if "decode_megakernel" in prof:  # average the one-launch round over a few more rounds
-        fused_ms.append(prof["decode_megakernel"][0])
-        for _ in range(7):
-            eng.profile_next_round()
-            eng.advance(1)
-            fused_ms.append(eng.kernel_profile()["decode_megakernel"][0])
+    prof, fused_ms = {}, []
+    if profile:  # profiled rounds (outside the timed region): per-class CUDA events
+        eng.profile_next_round()
+        eng.advance(2)  # a pending refill prefill may take the first round
+        prof = eng.kernel_profile()
+        if "decode_megakernel" in prof:  # the one-launch round, averaged over 8 rounds
+            fused_ms.append(prof["decode_megakernel"][0])
+            for _ in range(7):
+                eng.profile_next_round()
+                eng.advance(1)
+                fused_ms.append(eng.kernel_profile()["decode_megakernel"][0])
     ctx_now = [len(eng.stream_tokens(sid)) for sid in live]
-    # drain the profiled round's events so the actor stays consistent
-    for sid in list(live):
-        evs, reason, more = eng.wait_events(sid)
-        live[sid].extend(e.weight_version for e in evs)
+    for sid, (evs, reason, more) in eng.wait_events_many(list(live), columns=True).items():
+        live[sid].extend(evs.weight_version.tolist())
 
-    clocks = ClockSampler(local)
-    h2d0, d2h0 = h2d_bytes, d2h_bytes
-    if world > 1:
-        dist.barrier()
+    clocks = ClockSampler(device).start()
+    h2d0, d2h0 = h2d[0], d2h[0]
     torch.cuda.synchronize()
-    clocks.start()
     rec = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         step(rec)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     clk = clocks.stop()
+    # the same steps without an update in flight: the decode stall the update causes
+    rec_nu = []
+    for _ in range(max(3, steps // 2)):
+        step(rec_nu, update=False)
 
     tokens = sum(r["tokens"] for r in rec)
     dev_ms = sum(r["dev_ms"] for r in rec)
     wall_ms = sum(r["wall_ms"] for r in rec)
-    launches = sum(r["launches"] for r in rec)
-    pauses = [r["pause_ms"] for r in rec]
-    upd = [r["update_ms"] for r in rec]
-    dev_ms_max = max_over_ranks(dev_ms)
-    wall_ms_max = max_over_ranks(wall_ms)
-    total_tokens = float(tokens)
-    if world > 1:
-        t = torch.tensor([float(tokens)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        total_tokens = t.item()
-
-    # lag bookkeeping of the sequences consumed so far (device lag kernel)
-    lag = {"max_lag_steps": None}
-    seqs = token_versions + [v for v in live.values() if v]
-    if seqs:
-        vers = torch.tensor(np.concatenate([np.asarray(v, dtype=np.int32) for v in seqs]), device=dev)
-        offs = torch.tensor(np.concatenate([[0], np.cumsum([len(v) for v in seqs])]),
-                            dtype=torch.int64, device=dev)
-        hist = torch.zeros(4096, dtype=torch.int64, device=dev)
-        sums = torch.zeros(len(seqs), dtype=torch.int64, device=dev)
-        tot = torch.zeros(4, dtype=torch.int64, device=dev)
-        _lib.call("srl_lag_stats", vers.data_ptr(), offs.data_ptr(), len(seqs), chan.version,
-                  hist.data_ptr(), 4096, sums.data_ptr(), tot.data_ptr(), None)
-        torch.cuda.synchronize()
-        tt = tot.cpu().tolist()
-        lag = {"max_lag_steps": int(tt[2]), "mean_lag_steps": tt[1] / max(tt[0], 1),
-               "sequences": len(seqs), "finished_sequences": len(token_versions)}
-
+    out = {
+        "tokens": tokens, "dev_ms": dev_ms, "wall_ms": wall_ms,
+        "launches": sum(r["launches"] for r in rec),
+        "h2d_bytes_per_step": (h2d[0] - h2d0) // steps, "d2h_bytes_per_step": (d2h[0] - d2h0) // steps,
+        "clocks": clk, "ctx_now": ctx_now, "max_seq": max_seq,
+    }
+    per_upd = float(np.mean([r["decode_ms"] + r["pause_ms"] + max(0.0, r["copy_ms"] - r["decode_ms"])
+                             for r in rec]))
+    per_nu = float(np.mean([r["decode_ms"] for r in rec_nu]))
+    nbytes = pol.weights()[1]
+    out["pause"] = {
+        "swap_ms": {"median": float(np.median([r["pause_ms"] for r in rec])),
+                    "max": float(np.max([r["pause_ms"] for r in rec]))},
+        "decode_stall_ms": per_upd - per_nu,
+        "step_ms_with_update": per_upd, "step_ms_without_update": per_nu,
+        "transfer_ms": float(np.median([r["copy_ms"] for r in rec])),
+        "transfer_gbs": nbytes / (float(np.median([r["copy_ms"] for r in rec])) * 1e-3) / 1e9,
+        "payload_bytes": nbytes,
+        "transfer": "device copy into the standby buffer on a side stream, overlapped with "
+                    "the decode rounds (N = 1: the trainer shares the GPU)",
+    }
+    if lag and consumed:
+        # lag of every consumed sequence (sim.cpp:63-104), on the device
+        mx, tot, cnt = 0, 0, 0
+        for vb in sorted({vb for vb, _ in consumed}):
+            idx = [i for i, (b, _) in enumerate(consumed) if b == vb]
+            sub = [consumed[i][1] for i in idx]
+            sv = torch.tensor(np.concatenate([np.asarray(v, np.int32) for v in sub]), device=dev)
+            so = torch.tensor(np.concatenate([[0], np.cumsum([len(v) for v in sub])]),
+                              dtype=torch.int64, device=dev)
+            hist = torch.zeros(8192, dtype=torch.int64, device=dev)
+            sums = torch.zeros(len(sub), dtype=torch.int64, device=dev)
+            t4 = torch.zeros(4, dtype=torch.int64, device=dev)
+            _lib.call("srl_lag_stats", sv.data_ptr(), so.data_ptr(), len(sub), vb, hist.data_ptr(),
+                      8192, sums.data_ptr(), t4.data_ptr(), None)
+            t = t4.cpu().tolist()
+            cnt += t[0]
+            tot += t[1]
+            mx = max(mx, t[2])
+        out["lag"] = {"consumed_sequences": len(consumed), "tokens": cnt, "max_lag_steps": mx,
+                      "mean_lag_steps": tot / max(cnt, 1),
+                      "updates_per_rollout": int(np.ceil(gen / R)),
+                      "definition": "each finished sequence consumed at the drain that saw it "
+                                    "finish; lag = version then - version that emitted the token "
+                                    "(sim.cpp:74); one update every rounds_per_step rounds"}
     # roofline of the dominant kernel (profiled rounds)
-    hbm, bf16, peak_kind = load_peaks()
+    hbm, _, peak_kind = load_peaks()
     abytes = algorithmic_bytes(cfg, B, sum(ctx_now))
     step_bytes = sum(abytes.values())
-    cls_ms = {k: prof[k][0] for k in KERNEL_CLASSES}
-    traffic_db = load_traffic().get(args.config, {})
+    cls_ms = {k: prof[k][0] for k in KERNEL_CLASSES} if prof else {}
+    traffic = load_traffic().get(f"{cfg.name}:{B}:{gen}", {})
     if fused_ms:
-        # the whole round is ONE persistent kernel: its algorithmic bytes are
-        # the round's, its duration the CUDA-event time of the launch
         mk_ms = float(np.mean(fused_ms))
         roof = {"kernel": "decode_megakernel", "bound": "hbm",
                 "achieved": step_bytes / (mk_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                "peak_kind": peak_kind, "traffic": traffic_db.get("decode_megakernel"),
+                "peak_kind": peak_kind, "traffic": traffic.get("decode_megakernel"),
                 "launches_per_round": 1, "bytes_per_launch": step_bytes, "ms_per_launch": mk_ms,
                 "ms_per_launch_samples": len(fused_ms),
                 "phase_ms_per_round": {k: round(v, 4) for k, v in cls_ms.items()}}
         round_ms = mk_ms
-    else:
+    elif cls_ms:
         dom = max(cls_ms, key=cls_ms.get)
         round_ms = sum(cls_ms.values())
         nlaunch = max(prof[dom][1], 1)
         roof = {"kernel": dom, "bound": "hbm", "achieved": abytes[dom] / (cls_ms[dom] * 1e-3) / 1e9,
                 "peak": hbm, "unit": "GB/s", "peak_kind": peak_kind,
-                "traffic": traffic_db.get(dom), "launches_per_round": prof[dom][1],
+                "traffic": traffic.get(dom), "launches_per_round": prof[dom][1],
                 "bytes_per_launch": abytes[dom] / nlaunch, "ms_per_launch": cls_ms[dom] / nlaunch}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    round_roof = {"bound": "hbm", "achieved": step_bytes / (round_ms * 1e-3) / 1e9, "peak": hbm,
-                  "unit": "GB/s", "bytes": step_bytes, "ms": round_ms,
-                  "bytes_by_class": {k: int(v) for k, v in abytes.items()}}
-    round_roof["frac"] = round_roof["achieved"] / hbm
-    roofline_tps = B / (step_bytes / (hbm * 1e9))
+    else:
+        roof, round_ms = None, None
+    if roof:
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        out["roofline"] = roof
+        out["round_roofline"] = {"bound": "hbm", "achieved": step_bytes / (round_ms * 1e-3) / 1e9,
+                                 "peak": hbm, "unit": "GB/s", "bytes": step_bytes, "ms": round_ms,
+                                 "ctx_sum": int(sum(ctx_now)),
+                                 "bytes_by_class": {k: int(v) for k, v in abytes.items()},
+                                 "frac": step_bytes / (round_ms * 1e-3) / 1e9 / hbm}
+        out["roofline_tokens_per_s"] = B / (step_bytes / (hbm * 1e9))
+        out["kernel_ms_per_round"] = {k: round(v, 4) for k, v in cls_ms.items()}
+    out["prefill"] = {"ms_per_step": sum(r["prefill_ms"] for r in rec) / steps,
+                      "rows_per_step": sum(r["prefill_rows"] for r in rec) / steps,
+                      "note": "refill prefill rounds of finished streams (inside value's device time)"}
+    eng.close()
+    return out, pol
 
-    value = total_tokens / (dev_ms_max * 1e-3)
-    e2e = total_tokens / (wall_ms_max * 1e-3)
-    if HOSTPROF:
-        print("host ms/step", {k: round(1e3 * v / args.steps, 3) for k, v in HOSTPROF_ACC.items()},
-              "device ms/step", round(dev_ms / args.steps, 3), file=sys.stderr)
+
+def cpu_sample(cfg, contexts, rounds=2):
+    """The CPU port (oracle/decoder_cpu.py) on the same streams and contexts."""
+    from oracle.decoder_cpu import time_rounds
+
+    tps, dt, cores = time_rounds(cfg.to_dict(), contexts, rounds)
+    return {"value": tps, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{len(contexts)} streams x {rounds} decode rounds at the measured contexts "
+                      f"(mean {np.mean(contexts):.0f} tokens), oracle/decoder_cpu.py numpy fp32 "
+                      f"on all host cores ({dt:.1f} s); the reference has no decoder"}
+
+
+# ------------------------------------------------------ reference arm ---
+def reference_arm(args, cfg):
+    """The CPU path on the host cores, same config as our arm: each step is one
+    decode round of the same B streams at the same steady-state contexts
+    (oracle/decoder_cpu.py: the reference has no transformer, so this is the
+    builder's port).  Next to it, the REFERENCE ITSELF (oracle/_ref, compiled
+    from /root/reference on the build machine): its Engine on the toy
+    recurrent policy, one instance per core, and its update pause
+    (policy_to_json + crc32 + policy_from_json + apply_weight_update)."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.decoder_cpu import CpuDecoder
+
+    B = args.batch
+    ctx = [1 + args.prompt + d for d, _ in steady_contexts(B, args.prompt, args.gen)] \
+        if not args.no_steady else [1 + args.prompt] * B
+    dec = CpuDecoder(cfg.to_dict())
+    dec.add_streams(ctx, max(ctx) + args.steps + args.warmup + 1)
+    toks = np.zeros(B, dtype=np.int64)
+    for _ in range(args.warmup):
+        toks = dec.round(toks)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        toks = dec.round(toks)
+    dt = time.perf_counter() - t0
+    tps = B * args.steps / dt
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tps, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic prompts, random-init weights",
+        "config": {"workload": f"{cfg.name} generator, constant batch {B}, rollouts of up to "
+                               f"{args.gen} tokens (steady-state contexts), CPU",
+                   "model": cfg.name, "global_batch": B, "seq_len": 1 + args.prompt + args.gen + 1,
+                   "parallelism": "cpu", "same_config": True,
+                   "sample": "each step = one decode round of the same B streams at the same "
+                             "contexts as the device run (no update: the CPU time per token is "
+                             "dominated by the round)"},
+        "cpu_baseline": {"value": tps, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{B} streams x {args.steps} decode rounds, mean context "
+                                   f"{np.mean(ctx):.0f} tokens, oracle/decoder_cpu.py numpy fp32"},
+        "e2e": {"value": tps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    try:  # the reference itself, on the configuration it can run
+        from oracle.oracle import Ref
+
+        ref = Ref()
+        doc = ref.random_recurrent_policy(256, 128, 0.6, 1)
+        nxt = ref.drift_checkpoints(doc, 1, 0.05, 2)[-1]
+        tok, sec = ref.engine_throughput_parallel(doc, cores, 64, 200)
+        tok1, sec1 = ref.engine_throughput(doc, 64, 200)
+        line["reference_engine_toy"] = {
+            "value": tok / sec, "unit": UNIT, "cores": cores, "kind": "reference",
+            "one_core": tok1 / sec1,
+            "sample": f"{cores} x reference proto::Engine (RecurrentToyPolicy V=256 D=128), 64 "
+                      f"streams x 200 tokens each, one instance per core (oracle/_ref)"}
+        line["reference_pause_toy"] = {
+            "stale": ref.update_pause(doc, nxt, 64, 128, False),
+            "recompute": ref.update_pause(doc, nxt, 64, 128, True),
+            "note": "reference update path for the toy policy (V=256, D=128): policy_to_json + "
+                    "crc32 + policy_from_json + apply_weight_update with 64 live streams"}
+    except Exception as e:  # noqa: BLE001 -- oracle/_ref is only built where /root/reference exists
+        line["reference_engine_toy"] = {"unavailable": f"{type(e).__name__}: {e}"}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- ours ---
+def main():
+    args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+    from paper_2509_19128_b200.policy import PRESETS
+
+    cfg = PRESETS[args.config]
+    if args.impl == "reference":
+        return reference_arm(args, cfg)
+    world, rank, local = dist_env()
+    if world > 1:
+        from paper_2509_19128_b200.pipeline_dist import bench_partitioned
+
+        line = bench_partitioned(args, cfg)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    B, R = args.batch, args.rounds
+    g, pol = generator_measure(cfg, B=B, prompt=args.prompt, gen=args.gen, R=R, steps=args.steps,
+                               warmup=args.warmup, steady=not args.no_steady,
+                               use_graphs=not args.no_graphs, device=local)
+    value = g["tokens"] / (g["dev_ms"] * 1e-3)
+    e2e = g["tokens"] / (g["wall_ms"] * 1e-3)
     out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": g["dev_ms"] / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic prompts, random-init weights",
-        "config": {"workload": f"{cfg.name} generator, constant batch {B}, in-flight update "
-                               f"every {R} decode rounds (one optimizer step)",
-                   "model": cfg.name, "global_batch": B * world, "seq_len": max_seq,
+        "config": {"workload": f"{cfg.name} generator, constant batch {B}, rollouts of up to "
+                               f"{args.gen} tokens" + ("" if args.no_steady else
+                                                       " (steady-state contexts)")
+                               + f", in-flight update every {R} decode rounds",
+                   "model": cfg.name, "global_batch": B, "seq_len": g["max_seq"],
                    "prompt": args.prompt, "max_tokens": args.gen, "rounds_per_step": R,
-                   "parallelism": f"generator replicas x{world} (update broadcast from rank 0)"
-                                  if world > 1 else "1 generator (update = device copy)",
+                   "parallelism": "1 GPU: generator (update = device copy into the standby buffer)",
                    "cuda_graphs": not args.no_graphs,
-                   "l2": "inputs larger than L2 (0.99 GB weights streamed every round)"},
-        "e2e": {"value": e2e, "unit": UNIT,
-                "h2d_bytes_per_step": (h2d_bytes - h2d0) // args.steps,
-                "d2h_bytes_per_step": (d2h_bytes - d2h0) // args.steps},
-        "gpu_launches": launches,
-        "pause_ms": {"median": float(np.median(pauses)), "max": float(np.max(pauses))},
-        "update_copy_ms": {"median": float(np.median(upd)), "max": float(np.max(upd)),
-                           "payload_bytes": pol.weights()[1]},
-        "lag": lag,
-        "roofline": roof,
-        "round_roofline": round_roof,
-        "roofline_tokens_per_s": roofline_tps,
-        "kernel_ms_per_round": {k: round(v, 4) for k, v in cls_ms.items()},
-        "update_gbs": pol.weights()[1] / (float(np.median(upd)) * 1e-3) / 1e9,
-        "prefill": {"ms_per_step": sum(r["prefill_ms"] for r in rec) / args.steps,
-                    "rows_per_step": sum(r["prefill_rows"] for r in rec) / args.steps,
-                    "note": "refill prefill rounds of finished streams (inside value's device time)"},
-        "clocks": clk,
+                   "l2": "inputs larger than L2 (weights + KV caches streamed every round)"},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": g["h2d_bytes_per_step"],
+                "d2h_bytes_per_step": g["d2h_bytes_per_step"]},
+        "gpu_launches": g["launches"],
+        "pause_ms": g["pause"]["swap_ms"],
+        "pause": g["pause"],
+        "lag": g.get("lag"),
+        "roofline": g.get("roofline"),
+        "round_roofline": g.get("round_roofline"),
+        "roofline_tokens_per_s": g.get("roofline_tokens_per_s"),
+        "kernel_ms_per_round": g.get("kernel_ms_per_round"),
+        "prefill": g["prefill"],
+        "clocks": g["clocks"],
     }
-    if rank == 0 and world == 1 and not args.no_trainer:
-        tclk = ClockSampler(local)
-        tclk.start()
-        out["trainer"] = trainer_measure(cfg, pol, args.train_seqs, args.prompt, args.gen)
+    ctx_now = g["ctx_now"]
+    if not args.no_trainer:
+        tclk = ClockSampler(local).start()
+        out["trainer"] = trainer_measure(cfg, pol, args.train_seqs, args.prompt, args.train_gen)
         out["trainer"]["clocks"] = tclk.stop()
-    if rank == 0 and world == 1 and not args.no_pipeline:
-        out["pause_ms_recompute_mode"] = recompute_pause_measure(cfg, pol, payloads[0], args)
-        out["pipeline_1gpu"] = pipeline_measure(cfg, args)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        tps, dt, cores = cpu_decode_sample(cfg, B, 8, args.cpu_steps, 1)
-        out["cpu_baseline"] = {"value": tps, "unit": UNIT, "cores": cores, "kind": "port",
-                               "sample": f"{B} streams x {args.cpu_steps} decode rounds after an "
-                                         f"8-token prefill, oracle/decoder_oracle.py numpy fp32 "
-                                         f"({dt:.1f} s)"}
-    eng.close()
-    if rank == 0:
-        print(json.dumps(out), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    if not args.no_pipeline:
+        payload = pol.clone().perturb(99, 0.002)
+        out["pause_ms_recompute_mode"] = recompute_pause_measure(cfg, pol, payload, B, args.prompt)
+        del payload
+        out["pipeline_1gpu"] = pipeline_measure(cfg, B, args.prompt, args.train_gen, R)
+    del pol
+    if not args.no_extra:
+        out["extra_configs"] = {}
+        for spec in filter(None, args.extra.split(",")):
+            name, b, gen = spec.split(":")
+            c = PRESETS[name]
+            try:
+                e, p = generator_measure(c, B=int(b), prompt=args.prompt, gen=int(gen), R=R,
+                                         steps=max(3, args.steps // 2), warmup=2, steady=True,
+                                         use_graphs=not args.no_graphs, device=local, n_payloads=1)
+                del p
+                out["extra_configs"][f"{name}:{b}:{gen}"] = {
+                    "value": e["tokens"] / (e["dev_ms"] * 1e-3), "e2e": e["tokens"] / (e["wall_ms"] * 1e-3),
+                    "ms_per_step": e["dev_ms"] / max(3, args.steps // 2),
+                    "pause": e["pause"], "roofline": e.get("roofline"),
+                    "round_roofline": {k: v for k, v in (e.get("round_roofline") or {}).items()
+                                       if k != "bytes_by_class"},
+                    "roofline_tokens_per_s": e.get("roofline_tokens_per_s"),
+                    "lag": e.get("lag"), "clocks": e["clocks"]}
+            except Exception as ex:  # noqa: BLE001 -- an extra line must not sink the headline
+                out["extra_configs"][f"{name}:{b}:{gen}"] = {"error": f"{type(ex).__name__}: {ex}"}
+            torch.cuda.empty_cache()
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_sample(cfg, ctx_now)
+    print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":

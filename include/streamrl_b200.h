@@ -96,6 +96,8 @@ int srl_policy_decoder_from_buffer(const srl_decoder_config* cfg, const void* we
 size_t srl_decoder_weight_bytes(const srl_decoder_config* cfg);
 /* Device pointer + size of a decoder policy's flat weights (owned by it). */
 int srl_policy_decoder_weights(const srl_policy* p, void** device_ptr, size_t* nbytes);
+/* CUDA device index the decoder policy's weights live on. */
+int srl_policy_decoder_device(const srl_policy* p, int32_t* device);
 /* Element offset (bf16 elements) of a named tensor: "embed", "final_norm",
  * "lm_head", or "<layer>.<ln1|qkv_w|qkv_b|o_w|ln2|gate_up_w|down_w>". */
 int srl_policy_decoder_offset(const srl_policy* p, const char* name, size_t* offset);
@@ -170,6 +172,9 @@ int srl_engine_begin_weight_update(srl_engine* e, int32_t new_version, void** st
 int srl_engine_commit_weight_update(srl_engine* e, int32_t new_version, int32_t* version_out,
                                     double* pause_ms);
 int srl_engine_abort_weight_update(srl_engine* e);
+/* Size of the weight payload an update of this engine carries (the standby
+ * buffer's size), without staging anything. */
+int srl_engine_standby_bytes(srl_engine* e, size_t* nbytes);
 /* advance (engine.cpp:174-187): paused engines only (SRL_LOGIC_ERROR). */
 int srl_engine_advance(srl_engine* e, int32_t rounds, int64_t* emitted);
 int srl_engine_pause(srl_engine* e);
@@ -244,7 +249,7 @@ int srl_ess(const double* weights, int32_t n, double* out);
 typedef struct srl_trainer srl_trainer;
 typedef struct {
   int32_t max_tokens;  /* packed rows per step (sum of sequence lengths - 1) */
-  int32_t device;
+  int32_t device;      /* the trainer's device (weights are peer-copied there); < 0 = the policy's */
 } srl_trainer_options;
 typedef struct {
   double objective;    /* J at the current weights */

@@ -380,6 +380,10 @@ class Ref:
         L.ref_engine_lockstep.argtypes = [C.c_char_p]
         L.ref_engine_throughput.argtypes = [C.c_char_p, C.c_int, C.c_int, u64, C.POINTER(i64),
                                             C.POINTER(f64)]
+        L.ref_engine_throughput_parallel.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, u64,
+                                                     C.POINTER(i64), C.POINTER(f64)]
+        L.ref_update_pause.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, vp,
+                                       C.POINTER(i64)]
         L.ref_run_pipeline.argtypes = [C.c_char_p]
         L.ref_run_conventional.argtypes = [C.c_char_p]
         L.ref_crc32.restype = C.c_uint
@@ -463,6 +467,27 @@ class Ref:
                                         C.byref(tok), C.byref(sec)):
             raise RuntimeError("engine_throughput failed")
         return tok.value, sec.value
+
+    def engine_throughput_parallel(self, doc, n_threads, n_streams, max_tokens, seed=1):
+        """n_threads independent reference Engines at once (one per core):
+        (aggregate tokens, wall seconds of the slowest)."""
+        tok, sec = i64(), f64()
+        if self.L.ref_engine_throughput_parallel(json.dumps(doc).encode(), n_threads, n_streams,
+                                                 max_tokens, seed, C.byref(tok), C.byref(sec)):
+            raise RuntimeError("engine_throughput_parallel failed")
+        return tok.value, sec.value
+
+    def update_pause(self, doc, new_doc, n_streams, rounds, recompute=False):
+        """The reference's weight-update pause: {serialize, crc32, parse, apply}
+        milliseconds and the JSON payload bytes."""
+        out = np.zeros(4)
+        nb = i64()
+        st = self.L.ref_update_pause(json.dumps(doc).encode(), json.dumps(new_doc).encode(),
+                                     n_streams, rounds, int(recompute), out.ctypes.data, C.byref(nb))
+        if st:
+            raise RuntimeError(f"update_pause failed ({st})")
+        return dict(zip(("serialize_ms", "crc32_ms", "parse_ms", "apply_ms"), out.tolist()),
+                    payload_bytes=nb.value)
 
     def run_pipeline(self, cfg):
         return self._s(self.L.ref_run_pipeline(json.dumps(cfg).encode()))

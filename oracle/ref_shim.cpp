@@ -8,6 +8,7 @@
 // All structured data crosses the boundary as JSON text (the reference's own
 // policy / trajectory document formats); strings returned by ref_* are
 // malloc'd and released with ref_free.
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -231,6 +232,78 @@ int ref_engine_throughput(const char* policy_json, int n_streams, int max_tokens
     const auto t1 = std::chrono::steady_clock::now();
     *seconds = std::chrono::duration<double>(t1 - t0).count();
     engine.stop();
+    return 0;
+  } catch (const std::exception&) { return 1; }
+}
+
+// The same probe on every host core at once: n_threads independent Engines
+// (one scheduler thread each, SURVEY 8d "one instance per core"), each with
+// n_streams streams; returns the aggregate tokens and the wall seconds of
+// the slowest instance.
+int ref_engine_throughput_parallel(const char* policy_json, int n_threads, int n_streams,
+                                   int max_tokens, unsigned long long seed, long long* tokens,
+                                   double* seconds) {
+  try {
+    const auto pol = rlmath::policy_from_json(policy_json);
+    std::vector<long long> tok(n_threads, 0);
+    std::vector<double> sec(n_threads, 0.0);
+    std::vector<std::thread> th;
+    for (int t = 0; t < n_threads; ++t)
+      th.emplace_back([&, t] {
+        proto::Engine engine({pol, false, true});
+        for (int i = 0; i < n_streams; ++i)
+          engine.open_stream("p", max_tokens, rng::derive_stream(seed + t, i), -1);
+        const auto t0 = std::chrono::steady_clock::now();
+        tok[t] = engine.advance(max_tokens);
+        sec[t] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        engine.stop();
+      });
+    for (auto& x : th) x.join();
+    *tokens = 0;
+    *seconds = 0.0;
+    for (int t = 0; t < n_threads; ++t) {
+      *tokens += tok[t];
+      *seconds = std::max(*seconds, sec[t]);
+    }
+    return 0;
+  } catch (const std::exception&) { return 1; }
+}
+
+// The reference's in-flight update pause for one payload (protocol.cpp:147-190
+// handler path + engine.cpp:79-117): the trainer serialises the policy
+// (policy_to_json), the client checksums the body (crc32), the server parses
+// it (policy_from_json) and applies it under the round lock with n_streams
+// live streams after `rounds` rounds (stale or recompute state).
+// out_ms = {serialize, crc32, parse, apply}; *payload_bytes = JSON body size.
+int ref_update_pause(const char* policy_json, const char* new_policy_json, int n_streams,
+                     int rounds, int recompute, double* out_ms, long long* payload_bytes) {
+  try {
+    using clk = std::chrono::steady_clock;
+    auto ms = [](clk::time_point a, clk::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    proto::Engine engine({rlmath::policy_from_json(policy_json), recompute != 0, true});
+    for (int i = 0; i < n_streams; ++i)
+      engine.open_stream("p", rounds + 16, rng::derive_stream(7, i), -1);
+    engine.advance(rounds);
+    const auto next = rlmath::policy_from_json(new_policy_json);
+    const auto t0 = clk::now();
+    const std::string body = rlmath::policy_to_json(next);
+    const auto t1 = clk::now();
+    volatile std::uint32_t crc = proto::crc32(body);
+    (void)crc;
+    const auto t2 = clk::now();
+    auto parsed = rlmath::policy_from_json(body);
+    const auto t3 = clk::now();
+    const auto r = engine.apply_weight_update(1, std::move(parsed));
+    const auto t4 = clk::now();
+    engine.stop();
+    if (!r.applied) return 2;
+    out_ms[0] = ms(t0, t1);
+    out_ms[1] = ms(t1, t2);
+    out_ms[2] = ms(t2, t3);
+    out_ms[3] = ms(t3, t4);
+    *payload_bytes = (long long)body.size();
     return 0;
   } catch (const std::exception&) { return 1; }
 }

@@ -93,6 +93,7 @@ SIGNATURES: dict[str, tuple] = {
     "srl_policy_decoder_from_buffer": (I, [P(DecoderConfigC), vp, sz, i32, i32, P(vp)]),
     "srl_decoder_weight_bytes": (sz, [P(DecoderConfigC)]),
     "srl_policy_decoder_weights": (I, [vp, P(vp), P(sz)]),
+    "srl_policy_decoder_device": (I, [vp, P(i32)]),
     "srl_policy_decoder_offset": (I, [vp, cp, P(sz)]),
     "srl_policy_decoder_perturb": (I, [vp, u64, f64]),
     "srl_policy_type": (I, [vp]),
@@ -108,6 +109,7 @@ SIGNATURES: dict[str, tuple] = {
     "srl_engine_begin_weight_update": (I, [vp, i32, P(vp), P(sz)]),
     "srl_engine_commit_weight_update": (I, [vp, i32, P(i32), P(f64)]),
     "srl_engine_abort_weight_update": (I, [vp]),
+    "srl_engine_standby_bytes": (I, [vp, P(sz)]),
     "srl_engine_advance": (I, [vp, i32, P(i64)]),
     "srl_engine_pause": (I, [vp]),
     "srl_engine_resume": (I, [vp]),

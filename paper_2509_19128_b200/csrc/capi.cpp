@@ -171,6 +171,13 @@ extern "C" int srl_policy_decoder_from_buffer(const srl_decoder_config* cfg, con
   });
 }
 
+extern "C" int srl_policy_decoder_device(const srl_policy* p, int32_t* device) {
+  if (!p || !device || p->p.type != SRL_POLICY_DECODER || !p->p.dec)
+    return fail(SRL_INVALID_ARGUMENT, "not a decoder policy");
+  *device = p->p.dec->device;
+  return SRL_OK;
+}
+
 extern "C" int srl_policy_decoder_weights(const srl_policy* p, void** device_ptr, size_t* nbytes) {
   if (!p || p->p.type != SRL_POLICY_DECODER || !p->p.dec) return fail(SRL_INVALID_ARGUMENT, "not a decoder policy");
   if (device_ptr) *device_ptr = p->p.dec->w;
@@ -332,6 +339,11 @@ extern "C" int srl_engine_commit_weight_update(srl_engine* e, int32_t new_versio
   const int st = e->e->commit_weight_update(new_version, &v, pause_ms);
   if (version_out) *version_out = v;
   return st;
+}
+
+extern "C" int srl_engine_standby_bytes(srl_engine* e, size_t* nbytes) {
+  if (!e || !nbytes) return fail(SRL_INVALID_ARGUMENT, "standby_bytes");
+  return e->e->standby_bytes(nbytes);
 }
 
 extern "C" int srl_engine_abort_weight_update(srl_engine* e) {
@@ -550,6 +562,8 @@ extern "C" int srl_trainer_create(const srl_policy* p, const srl_trainer_options
     o.max_tokens = 4096;
     o.device = p->p.dec->device;
     if (opts) o = *opts;
+    if (o.device < 0) o.device = p->p.dec->device;
+    if ((st = require_device(o.device))) return st;
     auto h = std::make_unique<srl_trainer>();
     h->t = std::make_unique<DecoderTrainer>();
     if ((st = h->t->init(*p->p.dec, o))) return st;

@@ -313,7 +313,7 @@ int DecoderBackend::init(const Policy& p) {
   prefill_budget_ = std::max(opts_.prefill_budget, 1);
   int st;
   for (int b = 0; b < 2; ++b) {
-    if ((st = clone_decoder(src, buf_[b]))) return st;
+    if ((st = clone_decoder(src, buf_[b], opts_.device))) return st;
     maps_[b] = build_weight_maps(d_, buf_[b]->layout, buf_[b]->w);
   }
   runner_ = std::make_unique<DecoderRunner>();
@@ -564,10 +564,16 @@ int DecoderBackend::mega_round(int b, bool profile) {
   return SRL_OK;
 }
 
-int DecoderBackend::open_slot(int slot, const StreamSpec& spec) {
-  const int n_prefix = 1 + (int)spec.prompt.size();
+int DecoderBackend::check_stream(const StreamSpec& spec) const {
+  const int64_t n_prefix = 1 + (int64_t)spec.prompt.size();
   if (n_prefix + spec.max_tokens > max_seq_)
     return fail(SRL_INVALID_ARGUMENT, "open_stream: bos + prompt + max_tokens exceeds max_seq_len");
+  return SRL_OK;
+}
+
+int DecoderBackend::open_slot(int slot, const StreamSpec& spec) {
+  const int n_prefix = 1 + (int)spec.prompt.size();
+  if (const int st = check_stream(spec)) return st;
   HostSlot& h = host_[slot];
   h = HostSlot{};
   h.live = true;
@@ -799,15 +805,24 @@ int DecoderBackend::check_update(const Policy& p) {
 }
 
 int DecoderBackend::swap_and_recompute(bool recompute, int version) {
-  active_ ^= 1;
   int32_t* pi = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(pinned_) + pinned_bytes_ - 64);
+  const int old_version = version - 1;  // versions are strictly sequential (engine.cpp:82-87)
+  active_ ^= 1;
   pi[5] = version;
   SRL_CUDA(cudaMemcpyAsync(version_dev_, pi + 5, 4, cudaMemcpyHostToDevice, st_));
-  if (recompute) {
-    const int st = recompute_kv();
-    if (st != SRL_OK) return st;
+  int st = recompute ? recompute_kv() : SRL_OK;
+  if (st == SRL_OK && cudaStreamSynchronize(st_) != cudaSuccess) st = SRL_CUDA_ERROR;
+  if (st != SRL_OK) {
+    // a rejected update leaves the engine serving the old weights at the old
+    // version (engine.cpp:79-117): swap back, restore the version stamp and,
+    // in recompute mode, rebuild the live caches under the old weights
+    active_ ^= 1;
+    pi[5] = old_version;
+    cudaMemcpyAsync(version_dev_, pi + 5, 4, cudaMemcpyHostToDevice, st_);
+    if (recompute) recompute_kv();
+    cudaStreamSynchronize(st_);
+    return st;
   }
-  SRL_CUDA(cudaStreamSynchronize(st_));
   return SRL_OK;
 }
 

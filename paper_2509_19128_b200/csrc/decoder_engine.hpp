@@ -99,6 +99,7 @@ class DecoderBackend final : public Backend {
   }
   int check_update(const Policy& p) override;
   int apply_update(const Policy& p, bool recompute, int version) override;
+  int check_stream(const StreamSpec& spec) const override;
   int standby(void** ptr, size_t* bytes) override;
   int commit_standby(bool recompute, int version) override;
   int slot_history(int slot, std::vector<int32_t>& out) override;

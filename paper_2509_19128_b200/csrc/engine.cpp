@@ -53,6 +53,10 @@ int Engine::open_stream(const std::string& prompt_id, int max_tokens, uint64_t s
         return fail(SRL_INVALID_ARGUMENT, "open_stream: prompt token out of vocab");
       }
   }
+  if (const int st = backend_->check_stream(s->spec)) {
+    --next_stream_;
+    return st;
+  }
   *id = s->id;
   pending_.push_back(s.get());
   streams_.push_back(std::move(s));
@@ -123,6 +127,12 @@ int Engine::apply_weight_update(int new_version, const Policy& policy, int* vers
   return SRL_OK;
 }
 
+int Engine::standby_bytes(size_t* bytes) {
+  std::lock_guard<std::mutex> lk(lock_);
+  void* p = nullptr;
+  return backend_->standby(&p, bytes);
+}
+
 int Engine::begin_weight_update(int new_version, void** ptr, size_t* bytes) {
   std::lock_guard<std::mutex> lk(lock_);
   if (new_version != version_ + 1) return fail(SRL_VERSION_CONFLICT, "version_conflict");
@@ -141,7 +151,10 @@ int Engine::commit_weight_update(int new_version, int* version_out, double* paus
     return fail(SRL_VERSION_CONFLICT, "version_conflict");
   const auto t1 = std::chrono::steady_clock::now();
   const int st = backend_->commit_standby(recompute_, new_version);
-  if (st != SRL_OK) return st;
+  if (st != SRL_OK) {  // the backend swapped back: version and weights unchanged
+    staged_version_ = -1;
+    return st;
+  }
   const auto t2 = std::chrono::steady_clock::now();
   staged_version_ = -1;
   version_ = new_version;

@@ -110,10 +110,14 @@ int create_decoder(const srl_decoder_config& cfg, int device, std::shared_ptr<De
   return SRL_OK;
 }
 
-int clone_decoder(const DecoderWeights& src, std::shared_ptr<DecoderWeights>& out) {
-  const int st = create_decoder(src.cfg, src.device, out);
+int clone_decoder(const DecoderWeights& src, std::shared_ptr<DecoderWeights>& out, int device) {
+  if (device < 0) device = src.device;
+  const int st = create_decoder(src.cfg, device, out);
   if (st != SRL_OK) return st;
-  SRL_CUDA(cudaMemcpy(out->w, src.w, src.bytes, cudaMemcpyDeviceToDevice));
+  if (device == src.device)
+    SRL_CUDA(cudaMemcpy(out->w, src.w, src.bytes, cudaMemcpyDeviceToDevice));
+  else
+    SRL_CUDA(cudaMemcpyPeer(out->w, device, src.w, src.device, src.bytes));
   return SRL_OK;
 }
 

@@ -71,7 +71,9 @@ struct Policy {
 };
 
 // Make a deep copy of a decoder weight buffer on the same device.
-int clone_decoder(const DecoderWeights& src, std::shared_ptr<DecoderWeights>& out);
+// device < 0: the source's device; otherwise the copy lands on `device`
+// (a peer copy when it differs from the source's).
+int clone_decoder(const DecoderWeights& src, std::shared_ptr<DecoderWeights>& out, int device = -1);
 int create_decoder(const srl_decoder_config& cfg, int device, std::shared_ptr<DecoderWeights>& out);
 bool same_decoder_shape(const srl_decoder_config& a, const srl_decoder_config& b);
 
@@ -98,6 +100,9 @@ class Backend {
   virtual ~Backend() = default;
   virtual int slots() const = 0;
   virtual int open_slot(int slot, const StreamSpec& spec) = 0;
+  // open-time validation (the reference's invalid_argument at open_stream):
+  // a stream the backend could never seat is refused before it is queued
+  virtual int check_stream(const StreamSpec& spec) const { (void)spec; return SRL_OK; }
   virtual void close_slot(int slot) = 0;
   // Launch n rounds, wait, and return n x slots events (row-major by round).
   virtual int run_rounds(int n, std::vector<SlotEvent>& events, double* device_ms) = 0;
@@ -141,6 +146,7 @@ class Engine {
   int wait_events(int64_t id, std::vector<srl_token_event>& out, int cap, int* reason, int* more);
   int apply_weight_update(int new_version, const Policy& policy, int* version_out);
   int begin_weight_update(int new_version, void** ptr, size_t* bytes);
+  int standby_bytes(size_t* bytes);
   int commit_weight_update(int new_version, int* version_out, double* pause_ms);
   int abort_weight_update();
   int advance(int rounds, int64_t* emitted);

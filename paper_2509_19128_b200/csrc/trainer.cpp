@@ -101,7 +101,7 @@ int DecoderTrainer::alloc(T** p, size_t n) {
 int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) {
   opts_ = o;
   d_ = w.dims;
-  dev_ = w.device;
+  dev_ = o.device >= 0 ? o.device : w.device;  // the trainer lives on opts.device
   SRL_CUDA(cudaSetDevice(dev_));
   SRL_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   {  // the step's stream-ordered scratch (block tables, attention partials) stays
@@ -112,7 +112,7 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
   int st;
-  if ((st = clone_decoder(w, weights_))) return st;
+  if ((st = clone_decoder(w, weights_, dev_))) return st;
   lay_ = weights_->layout;
   n_ = lay_.total;
   T_max_ = pad64(std::max(64, o.max_tokens));

@@ -11,6 +11,7 @@ ValueError (invalid_argument) on negative rounds.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass
 from itertools import repeat
 
@@ -94,10 +95,20 @@ class Engine:
         _raise_for(st, "srl_engine_create")
         self._h = h
         self._recompute = recompute_state
-        self._evbuf = (_lib.TokenEventC * 4096)()
-        # a numpy view of the same buffer: events leave as four column lists
-        # (the per-field ctypes reads cost ~1 us per event)
-        self._evarr = np.frombuffer(self._evbuf, dtype=_EVENT_DTYPE)
+        # one event buffer per calling thread: the native wait releases the GIL,
+        # so handler threads of the HTTP server (server.py) draining different
+        # streams at once must not share it
+        self._tls = threading.local()
+
+    def _buffers(self):
+        """(ctypes event buffer, numpy view of it) of the calling thread; events
+        leave through the view as column lists (per-field ctypes reads cost
+        ~1 us per event)."""
+        t = self._tls
+        if not hasattr(t, "evbuf"):
+            t.evbuf = (_lib.TokenEventC * 4096)()
+            t.evarr = np.frombuffer(t.evbuf, dtype=_EVENT_DTYPE)
+        return t.evbuf, t.evarr
 
     # engine.cpp:46-61
     def open_stream(self, prompt_id: str, max_tokens: int, seed: int, terminator_token: int = -1,
@@ -121,17 +132,18 @@ class Engine:
     def wait_events(self, stream_id: str):
         """Blocks until >= 1 event or finish; returns (events, finish_reason, more)."""
         sid = self._sid(stream_id)
+        evbuf, evarr = self._buffers()
         events = []
         n, reason, more = C.c_int32(), C.c_int32(), C.c_int32()
         while True:
-            st = _lib.lib().srl_engine_wait_events(self._h, sid, self._evbuf, len(self._evbuf),
+            st = _lib.lib().srl_engine_wait_events(self._h, sid, evbuf, len(evbuf),
                                                    C.byref(n), C.byref(reason), C.byref(more))
             _raise_for(st, "wait_events")
             if n.value:
-                a = self._evarr[:n.value]
+                a = evarr[:n.value]
                 events.extend(map(TokenEvent, repeat(stream_id, n.value), a["position"].tolist(),
                                   a["token"].tolist(), a["logprob"].tolist(), a["weight_version"].tolist()))
-            if n.value < len(self._evbuf):
+            if n.value < len(evbuf):
                 break
         return events, FINISH[reason.value], bool(more.value)
 
@@ -146,11 +158,12 @@ class Engine:
         counts = np.zeros(k, dtype=np.int32)
         reasons = np.zeros(k, dtype=np.int32)
         more = np.zeros(k, dtype=np.int32)
-        st = _lib.lib().srl_engine_wait_events_many(self._h, ids.ctypes.data, k, self._evbuf, len(self._evbuf),
+        evbuf, evarr = self._buffers()
+        st = _lib.lib().srl_engine_wait_events_many(self._h, ids.ctypes.data, k, evbuf, len(evbuf),
                                                     counts.ctypes.data, reasons.ctypes.data, more.ctypes.data)
         _raise_for(st, "wait_events_many")
         total = int(counts.sum())
-        a = self._evarr[:total]
+        a = evarr[:total]
         if columns:
             out = {}
             o = 0
@@ -206,6 +219,12 @@ class Engine:
             return UpdateResult(False, v.value, "version_conflict"), 0.0
         _raise_for(st, "commit_weight_update")
         return UpdateResult(True, v.value, ""), ms.value
+
+    def standby_bytes(self) -> int:
+        """Payload size of a weight update (the standby buffer), nothing staged."""
+        n = C.c_size_t()
+        _raise_for(_lib.lib().srl_engine_standby_bytes(self._h, C.byref(n)), "standby_bytes")
+        return n.value
 
     def abort_weight_update(self):
         _raise_for(_lib.lib().srl_engine_abort_weight_update(self._h), "abort")

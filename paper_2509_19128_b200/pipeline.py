@@ -93,6 +93,7 @@ class StepReport:
     pause_ms: float
     train_ms: float
     post_warmup: bool
+    mean_length: float = 0.0   # mean generated length of the consumed batch
 
 
 @dataclass
@@ -232,7 +233,8 @@ class PipelineRL:
         return StepReport(step, self.round, version_before, float(np.mean([s.reward for s in batch])),
                           res.objective, res.ess, res.clamped, res.tokens, int(t[2]),
                           t[1] / max(t[0], 1), h, int(sample_lag), pause, res.step_ms,
-                          all(s.versions and s.versions[0] >= 1 for s in batch))  # sim.cpp:106-110
+                          all(s.versions and s.versions[0] >= 1 for s in batch),  # sim.cpp:106-110
+                          float(np.mean([len(s.tokens) for s in batch])))
 
     # --------------------------------------------------------------- loop ---
     def run(self, optimizer_steps: int, max_rounds: int = 1_000_000) -> PipelineReport:

@@ -138,9 +138,18 @@ class DecoderPolicy:
         _lib.call("srl_policy_decoder_perturb", self._h, seed, magnitude)
         return self
 
-    def clone(self):
+    @property
+    def device(self) -> int:
+        """CUDA device index of the weights."""
+        d = C.c_int32()
+        _lib.call("srl_policy_decoder_device", self._h, C.byref(d))
+        return d.value
+
+    def clone(self, device: int | None = None):
+        """A copy on `device` (default: this policy's device)."""
         p, n = self.weights()
-        return DecoderPolicy.from_buffer(self.config, p, n, True)
+        return DecoderPolicy.from_buffer(self.config, p, n, True,
+                                         self.device if device is None else device)
 
     def torch_weights(self):
         """Zero-copy torch view (uint16 -> bf16) of the flat weight buffer."""
@@ -151,7 +160,7 @@ class DecoderPolicy:
         class _Arr:
             __cuda_array_interface__ = {"shape": (n // 2,), "typestr": "<u2", "data": (p, False),
                                         "version": 3}
-        return torch.as_tensor(_Arr(), device="cuda").view(torch.bfloat16)
+        return torch.as_tensor(_Arr(), device=f"cuda:{self.device}").view(torch.bfloat16)
 
     def __del__(self):
         try:

@@ -34,11 +34,12 @@ class TrainStep:
 
 
 class Trainer:
-    def __init__(self, policy: DecoderPolicy, max_tokens: int = 4096, device: int = 0):
+    def __init__(self, policy: DecoderPolicy, max_tokens: int = 4096, device: int | None = None):
         if not isinstance(policy, DecoderPolicy):
             raise TypeError("Trainer needs a DecoderPolicy")
         self.config = policy.config
-        opts = _lib.TrainerOptionsC(max_tokens, device)
+        self.device = policy.device if device is None else device
+        opts = _lib.TrainerOptionsC(max_tokens, self.device)
         h = C.c_void_p()
         _lib.call("srl_trainer_create", policy.handle, C.byref(opts), C.byref(h))
         self._h = h
@@ -87,7 +88,7 @@ class Trainer:
         class _Arr:
             __cuda_array_interface__ = {"shape": (n.value,), "typestr": "<f4",
                                         "data": (p.value, False), "version": 3}
-        return torch.as_tensor(_Arr(), device="cuda")
+        return torch.as_tensor(_Arr(), device=f"cuda:{self.device}")
 
     def apply_adam(self, lr: float, betas=(0.9, 0.999), eps: float = 1e-8):
         _lib.call("srl_trainer_apply_adam", self._h, lr, betas[0], betas[1], eps)
@@ -100,7 +101,7 @@ class Trainer:
 
     def policy(self) -> DecoderPolicy:
         p, n = self.weights()
-        return DecoderPolicy.from_buffer(self.config, p, n, True)
+        return DecoderPolicy.from_buffer(self.config, p, n, True, self.device)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -129,6 +129,13 @@ class GradientSync:
 
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
             dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=self.group)
+            if grad.is_cuda:
+                import torch
+
+                # NCCL orders the collective on torch's current stream only; the
+                # trainer's kernels (Adam, the next step's gradient zeroing) run
+                # on the trainer's own stream and must see the reduced gradient
+                torch.cuda.current_stream(grad.device).synchronize()
         return grad
 
 
