@@ -278,6 +278,47 @@ int srl_trainer_apply_adam(srl_trainer* t, double lr, double beta1, double beta2
 /* bf16 flat weights (device) -- the payload broadcast to the generators. */
 int srl_trainer_weights(srl_trainer* t, void** device_ptr, size_t* nbytes);
 
+/* ------------------------------------------------------- comm (NCCL) --- */
+/* The weight-transfer channel and the trainer's gradient all-reduce over
+ * NCCL on NVLink / NVSwitch, drivable from C++ (csrc/comm.cpp).  Replaces the
+ * reference's group weight push -- init_process_group (protocol.cpp:378-395,
+ * engine.cpp:276-291) and request_group_weight_update (protocol.cpp:397-406:
+ * the policy JSON POSTed to each member in turn) -- with one broadcast of the
+ * flat bf16 buffer from the trainer root into every generator's standby
+ * buffer, overlapped with decode, then the swap at a token boundary.
+ * NCCL is loaded at run time; without it every call returns SRL_NCCL_ERROR.
+ * A generator/trainer partition uses two communicators: the trainer group
+ * (gradient all-reduce) and the broadcast group (trainer root + generators),
+ * each from its own unique id (srl_comm_unique_id on the group's first rank,
+ * distributed out of band). */
+typedef struct srl_comm srl_comm;
+int srl_comm_unique_id(uint8_t* id_out /* 128 bytes */);
+int srl_comm_init(const uint8_t* id, int32_t world, int32_t rank, int32_t device, srl_comm** out);
+void srl_comm_destroy(srl_comm* c);
+int srl_comm_size(const srl_comm* c, int32_t* world, int32_t* rank);
+/* In-place broadcast of a device buffer from root (synchronous). */
+int srl_comm_broadcast_bytes(srl_comm* c, int32_t root, void* device_buf, size_t nbytes);
+/* Root: broadcast the trainer's bf16 weights (ordered after its queued work;
+ * its next Adam step waits for the send).  Asynchronous: srl_comm_wait. */
+int srl_comm_send_weights(srl_comm* c, srl_trainer* t);
+/* Generator: stage new_version and enqueue the receive into the engine's
+ * standby buffer on the transfer stream; returns at once (decode continues).
+ * *staged = 0 when the engine rejected the version (version_conflict): the
+ * rank still receives (into scratch) so the collective completes on every
+ * rank, and keeps serving at its old version. */
+int srl_comm_recv_weights_begin(srl_comm* c, int32_t root, srl_engine* e, int32_t new_version,
+                                int32_t* staged);
+/* Generator: wait for the transfer, then commit (swap at the next token
+ * boundary).  transfer_ms = device time of the broadcast; pause_ms = time
+ * the decode loop was blocked by the swap. */
+int srl_comm_recv_weights_finish(srl_comm* c, srl_engine* e, int32_t new_version, int32_t* applied,
+                                 int32_t* version_out, double* transfer_ms, double* pause_ms);
+/* Wait for the in-flight broadcast (root side); transfer_ms as above. */
+int srl_comm_wait(srl_comm* c, double* transfer_ms);
+/* Trainer group: in-place SUM of the fp32 gradient, on the trainer's stream
+ * between its backward and its Adam step. */
+int srl_comm_allreduce_gradient(srl_comm* c, srl_trainer* t);
+
 /* ---------------------------------------------------------------- lag --- */
 /* Per consumed batch lag statistics on the device (sim.cpp:63-110):
  * lag = version_before - token_version; hist must hold hist_cap counters.

@@ -11,10 +11,13 @@ after a switch (rl_math.cpp:64-73, engine.cpp:103-113).
 It rounds to bf16 at exactly the points the device path does (normalised
 activations, q/k/v, attention output, SwiGLU output) and accumulates every
 dot product in fp64, so GPU-vs-oracle differences come only from fp32
-accumulation order.  Parity for the transformer layers is NOT pinned by the
-reference (there is none); it is pinned by central finite differences of
-the backward pass (tests/test_decoder_oracle.py) and by the teacher-forced
-parity tests against the device path.
+accumulation order.  The reference has no transformer to pin it against;
+tests/test_decoder_oracle.py pins it to an independent implementation
+instead: with the rounding points off (exact=True) it equals transformers'
+Qwen2ForCausalLM (5.5.0, float64) to 1e-9 on random Qwen2-shaped weights in
+this layout, and central finite differences of its IS-REINFORCE objective
+equal the fp64 autograd gradient that the device trainer is checked against
+(tests/torch_decoder_ref.py), the recipe of test_rl_math.cpp:57-90.
 """
 from __future__ import annotations
 
@@ -68,9 +71,15 @@ def layout(cfg):
 class DecoderOracle:
     """fp64-accumulating decoder forward with a per-stream KV cache."""
 
-    def __init__(self, cfg: dict, weights_u16: np.ndarray, dtype=np.float64):
+    def __init__(self, cfg: dict, weights_u16: np.ndarray, dtype=np.float64, exact: bool = False):
+        """exact=True drops the device's bf16 rounding points and fp32 storage
+        of activations (every value fp64): the plain Qwen2 forward, the form
+        pinned against transformers' Qwen2ForCausalLM (tests/test_decoder_oracle.py)."""
         self.cfg = cfg
-        self.dtype = dtype
+        self.dtype = np.float64 if exact else dtype
+        self.exact = exact
+        self._f = np.float64 if exact else np.float32
+        self._rnd = (lambda a: np.asarray(a, dtype=np.float64)) if exact else bf16_round
         self.off, total = layout(cfg)
         w = np.asarray(weights_u16)
         if w.size < total:
@@ -86,10 +95,17 @@ class DecoderOracle:
                            f"{l}.o_w": (H, nq * hd), f"{l}.ln2": (H,),
                            f"{l}.gate_up_w": (2 * I, H), f"{l}.down_w": (H, I)})
         for name, (o, n) in self.off.items():
-            self.w[name] = bf16_bits_to_f32(w[o:o + n]).reshape(shapes[name]).astype(dtype)
+            vals = w[o:o + n] if w.dtype == np.float64 else bf16_bits_to_f32(w[o:o + n])
+            self.w[name] = vals.reshape(shapes[name]).astype(self.dtype)
         half = hd // 2
         self.inv_freq = cfg["rope_theta"] ** (-2.0 * np.arange(half) / hd)
-        self.scale = np.float32(1.0 / math.sqrt(hd))
+        self.scale = self._f(1.0 / math.sqrt(hd))
+
+    @classmethod
+    def from_flat64(cls, cfg: dict, flat64: np.ndarray):
+        """Exact-mode oracle over arbitrary fp64 weight values in the flat
+        layout (finite-difference probes perturb single weights)."""
+        return cls(cfg, np.asarray(flat64, dtype=np.float64), exact=True)
 
     # ------------------------------------------------------------ pieces
     def _rstd(self, x):
@@ -97,18 +113,18 @@ class DecoderOracle:
         return 1.0 / np.sqrt(ssq / self.cfg["hidden"] + self.cfg["rms_eps"])
 
     def _xg(self, x, gain):
-        return bf16_round(x.astype(np.float32) * gain.astype(np.float32)).astype(self.dtype)
+        return self._rnd(x.astype(self._f) * gain.astype(self._f)).astype(self.dtype)
 
     def _rope(self, x, pos):
         """x: [..., hd] fp32 values at integer position pos (scalar or [rows])."""
         hd = self.cfg["head_dim"]
         half = hd // 2
         ang = np.asarray(pos, dtype=np.float64)[..., None] * self.inv_freq
-        c = np.cos(ang).astype(np.float32)
-        s = np.sin(ang).astype(np.float32)
+        c = np.cos(ang).astype(self._f)
+        s = np.sin(ang).astype(self._f)
         while c.ndim < x.ndim:
             c, s = c[..., None, :], s[..., None, :]
-        x1, x2 = x[..., :half].astype(np.float32), x[..., half:].astype(np.float32)
+        x1, x2 = x[..., :half].astype(self._f), x[..., half:].astype(self._f)
         return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
 
     def new_cache(self):
@@ -124,18 +140,18 @@ class DecoderOracle:
         G = nq // nkv
         tokens = np.asarray(tokens)
         rows = len(tokens)
-        x = w["embed"][tokens].astype(np.float32)  # fp32 residual stream
+        x = w["embed"][tokens].astype(self._f)  # fp32 residual stream
         xg = self._xg(x, w["0.ln1"])
         rstd = self._rstd(x)
         for l in range(cfg["layers"]):
             qkv = (xg @ w[f"{l}.qkv_w"].T) * rstd[:, None] + w[f"{l}.qkv_b"]
-            qkv = qkv.astype(np.float32)
+            qkv = qkv.astype(self._f)
             q = qkv[:, :nq * hd].reshape(rows, nq, hd)
             k = qkv[:, nq * hd:(nq + nkv) * hd].reshape(rows, nkv, hd)
             v = qkv[:, (nq + nkv) * hd:].reshape(rows, nkv, hd)
-            q = bf16_round(self._rope(q, positions))
-            k = bf16_round(self._rope(k, positions))
-            v = bf16_round(v)
+            q = self._rnd(self._rope(q, positions))
+            k = self._rnd(self._rope(k, positions))
+            v = self._rnd(v)
             attn = np.zeros((rows, nq, hd), dtype=np.float64)
             for r in range(rows):
                 c = caches[r]
@@ -143,22 +159,22 @@ class DecoderOracle:
                 c["v"][l].append(v[r])
                 K = np.stack(c["k"][l]).astype(np.float64)  # [T, nkv, hd]
                 Vv = np.stack(c["v"][l]).astype(np.float64)
-                qs = (q[r].astype(np.float32) * self.scale).astype(np.float64)  # [nq, hd]
+                qs = (q[r].astype(self._f) * self.scale).astype(np.float64)  # [nq, hd]
                 for h in range(nq):
                     kh = h // G
                     s = K[:, kh, :] @ qs[h]
                     p = np.exp(s - s.max())
                     attn[r, h] = (p @ Vv[:, kh, :]) / p.sum()
-            attn = bf16_round(attn.reshape(rows, nq * hd)).astype(self.dtype)
-            x = (x + attn @ w[f"{l}.o_w"].T).astype(np.float32)
+            attn = self._rnd(attn.reshape(rows, nq * hd)).astype(self.dtype)
+            x = (x + attn @ w[f"{l}.o_w"].T).astype(self._f)
             xg = self._xg(x, w[f"{l}.ln2"])
             rstd = self._rstd(x)
             gu = (xg @ w[f"{l}.gate_up_w"].T) * rstd[:, None]
             gu = gu.reshape(rows, I // 64, 2, 64)
             g, u = gu[:, :, 0, :].reshape(rows, I), gu[:, :, 1, :].reshape(rows, I)
-            g32, u32 = g.astype(np.float32), u.astype(np.float32)
-            act = bf16_round(g32 / (np.float32(1) + np.exp(-g32)) * u32).astype(self.dtype)
-            x = (x + act @ w[f"{l}.down_w"].T).astype(np.float32)
+            g32, u32 = g.astype(self._f), u.astype(self._f)
+            act = self._rnd(g32 / (self._f(1) + np.exp(-g32)) * u32).astype(self.dtype)
+            x = (x + act @ w[f"{l}.down_w"].T).astype(self._f)
             nxt = w[f"{l + 1}.ln1"] if l + 1 < cfg["layers"] else w["final_norm"]
             xg = self._xg(x, nxt)
             rstd = self._rstd(x)

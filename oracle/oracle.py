@@ -386,6 +386,8 @@ class Ref:
                                        C.POINTER(i64)]
         L.ref_run_pipeline.argtypes = [C.c_char_p]
         L.ref_run_conventional.argtypes = [C.c_char_p]
+        L.ref_pipeline_max_lag_steps.restype = C.c_longlong
+        L.ref_pipeline_max_lag_steps.argtypes = [C.c_longlong, C.c_longlong, f64, f64, C.c_longlong]
         L.ref_crc32.restype = C.c_uint
         L.ref_crc32.argtypes = [C.c_char_p, C.c_size_t]
         L.ref_process_group_id.argtypes = [C.c_char_p]
@@ -488,6 +490,12 @@ class Ref:
             raise RuntimeError(f"update_pause failed ({st})")
         return dict(zip(("serialize_ms", "crc32_ms", "parse_ms", "apply_ms"), out.tolist()),
                     payload_bytes=nb.value)
+
+    def pipeline_max_lag_steps(self, H, I, L, mean_len, B):
+        v = self.L.ref_pipeline_max_lag_steps(H, I, L, mean_len, B)
+        if v < 0:
+            raise ValueError("pipeline_max_lag_steps: invalid arguments")
+        return v
 
     def run_pipeline(self, cfg):
         return self._s(self.L.ref_run_pipeline(json.dumps(cfg).encode()))

@@ -22,6 +22,7 @@
 #include "streamrl/engine.hpp"
 #include "streamrl/rl_math.hpp"
 #include "streamrl/sim.hpp"
+#include "streamrl/throughput.hpp"
 #include "streamrl/trajectory.hpp"
 
 using nlohmann::json;
@@ -320,6 +321,14 @@ char* ref_run_conventional(const char* sim_config_json) {
     const auto cfg = sim::SimConfig::from_json(sim_config_json);
     return dup(sim::run_conventional(cfg).to_json());
   } catch (const std::exception& e) { return error_json(e); }
+}
+
+long long ref_pipeline_max_lag_steps(long long gen_batch, long long inference_count, double max_len,
+                                     double mean_len, long long train_batch) {
+  try {
+    return throughput::pipeline_max_lag_steps(gen_batch, inference_count, max_len, mean_len,
+                                              train_batch);
+  } catch (const std::exception&) { return -1; }
 }
 
 unsigned int ref_crc32(const char* bytes, size_t n) {

@@ -138,6 +138,16 @@ SIGNATURES: dict[str, tuple] = {
     "srl_trainer_apply_adam": (I, [vp, f64, f64, f64, f64]),
     "srl_trainer_weights": (I, [vp, P(vp), P(sz)]),
     "srl_engine_kernel_profile": (I, [vp, P(KernelProfileC)]),
+    "srl_comm_unique_id": (I, [vp]),
+    "srl_comm_init": (I, [vp, i32, i32, i32, P(vp)]),
+    "srl_comm_destroy": (None, [vp]),
+    "srl_comm_size": (I, [vp, P(i32), P(i32)]),
+    "srl_comm_broadcast_bytes": (I, [vp, i32, vp, sz]),
+    "srl_comm_send_weights": (I, [vp, vp]),
+    "srl_comm_recv_weights_begin": (I, [vp, i32, vp, i32, P(i32)]),
+    "srl_comm_recv_weights_finish": (I, [vp, vp, i32, P(i32), P(i32), P(f64), P(f64)]),
+    "srl_comm_wait": (I, [vp, P(f64)]),
+    "srl_comm_allreduce_gradient": (I, [vp, vp]),
 }
 
 

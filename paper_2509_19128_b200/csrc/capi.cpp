@@ -8,19 +8,8 @@
 #include <string>
 #include <vector>
 
+#include "capi_handles.hpp"
 #include "decoder_engine.hpp"
-#include "runtime.hpp"
-#include "trainer.hpp"
-
-struct srl_policy {
-  srl::Policy p;
-};
-struct srl_engine {
-  std::unique_ptr<srl::Engine> e;
-};
-struct srl_trainer {
-  std::unique_ptr<srl::DecoderTrainer> t;
-};
 
 namespace srl {
 int toy_policy_logprobs(const Policy& p, const std::string& prompt_id,

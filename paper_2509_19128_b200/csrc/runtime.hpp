@@ -157,6 +157,7 @@ class Engine {
   int64_t total_streams() const;
   int64_t rounds_done() const;
   bool recompute_state_mode() const { return recompute_; }
+  int device() const { return opts_.device; }
   void set_process_group(std::string id, std::vector<std::string> members);
   std::optional<std::string> process_group_id() const;
   void stop();

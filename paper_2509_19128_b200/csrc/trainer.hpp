@@ -28,6 +28,8 @@ class DecoderTrainer {
   int step(const TrainBatch& b, srl_trainer_stats* stats);
   int apply_adam(float lr, float beta1, float beta2, float eps);
   float* gradient() const { return grad_; }
+  cudaStream_t stream() const { return st_; }
+  int device() const { return dev_; }
   size_t elements() const { return n_; }
   DecoderWeights& weights() { return *weights_; }
   const std::vector<double>& last_logprobs() const { return lp_host_; }

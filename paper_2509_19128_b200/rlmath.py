@@ -113,3 +113,16 @@ def fit_baseline(trajectories) -> BaselineTable:
             s, n = cells.get((t.prompt_id, p), (0.0, 0))
             cells[(t.prompt_id, p)] = (s + t.reward, n + 1)
     return BaselineTable({k: s / n for k, (s, n) in cells.items()})
+
+
+def pipeline_max_lag_steps(gen_batch: int, inference_count: int, max_len: float, mean_len: float,
+                           train_batch: int) -> int:
+    """g_max = ceil(H * I * L / (mean L * B)) (throughput.cpp:260-269): the
+    analytic maximum token lag, in optimizer steps, of a pipeline with I
+    generators of constant batch H and a trainer consuming B sequences per
+    step -- the cross-check for the lag the loop measures (test_sim.cpp:233-242)."""
+    import math
+
+    if gen_batch < 1 or inference_count < 1 or train_batch < 1 or not max_len > 0 or not mean_len > 0:
+        raise ValueError("pipeline_max_lag_steps: invalid arguments")
+    return int(math.ceil(float(gen_batch) * float(inference_count) * max_len / (mean_len * float(train_batch))))

@@ -18,8 +18,11 @@ def bf16_st(x):
 
 
 class TorchDecoder:
-    def __init__(self, cfg: dict, flat_u16: np.ndarray):
+    def __init__(self, cfg: dict, flat_u16: np.ndarray, exact: bool = False):
+        """exact=True: no bf16 rounding points, fp64 RoPE tables and scale
+        (pinned against transformers' Qwen2 in tests/test_decoder_oracle.py)."""
         self.cfg = cfg
+        self.exact = exact
         self.off, self.total = layout(cfg)
         H, I = cfg["hidden"], cfg["intermediate"]
         nq, nkv, hd = cfg["q_heads"], cfg["kv_heads"], cfg["head_dim"]
@@ -58,8 +61,12 @@ class TorchDecoder:
         pos = torch.arange(T, dtype=torch.float64)
         inv = c["rope_theta"] ** (-2.0 * torch.arange(half, dtype=torch.float64) / hd)
         ang = pos[:, None] * inv
-        cos = ang.cos().to(torch.float32).to(torch.float64)
-        sin = ang.sin().to(torch.float32).to(torch.float64)
+        if self.exact:
+            cos, sin = ang.cos(), ang.sin()
+        else:
+            cos = ang.cos().to(torch.float32).to(torch.float64)
+            sin = ang.sin().to(torch.float32).to(torch.float64)
+        bf16 = (lambda z: z) if self.exact else bf16_st
 
         def rope(z):  # [T, heads, hd]
             z1, z2 = z[..., :half], z[..., half:]
@@ -70,27 +77,27 @@ class TorchDecoder:
             return 1.0 / torch.sqrt((z * z).mean(-1) + c["rms_eps"])
 
         mask = torch.ones(T, T, dtype=torch.bool).tril()
-        scale = float(np.float32(1.0 / math.sqrt(hd)))
+        scale = 1.0 / math.sqrt(hd) if self.exact else float(np.float32(1.0 / math.sqrt(hd)))
         for l in range(c["layers"]):
-            u = bf16_st(x * p[f"{l}.ln1"])
+            u = bf16(x * p[f"{l}.ln1"])
             qkv = rstd(x)[:, None] * (u @ p[f"{l}.qkv_w"].T) + p[f"{l}.qkv_b"]
-            q = bf16_st(rope(qkv[:, :nq * hd].reshape(T, nq, hd)))
-            k = bf16_st(rope(qkv[:, nq * hd:(nq + nkv) * hd].reshape(T, nkv, hd)))
-            v = bf16_st(qkv[:, (nq + nkv) * hd:].reshape(T, nkv, hd))
+            q = bf16(rope(qkv[:, :nq * hd].reshape(T, nq, hd)))
+            k = bf16(rope(qkv[:, nq * hd:(nq + nkv) * hd].reshape(T, nkv, hd)))
+            v = bf16(qkv[:, (nq + nkv) * hd:].reshape(T, nkv, hd))
             k = k.repeat_interleave(G, dim=1)
             v = v.repeat_interleave(G, dim=1)
             s = torch.einsum("thd,shd->hts", q * scale, k)
             s = s.masked_fill(~mask, float("-inf"))
             a = torch.softmax(s, -1)
-            o = bf16_st(torch.einsum("hts,shd->thd", a, v).reshape(T, nq * hd))
+            o = bf16(torch.einsum("hts,shd->thd", a, v).reshape(T, nq * hd))
             x = x + o @ p[f"{l}.o_w"].T
-            u2 = bf16_st(x * p[f"{l}.ln2"])
+            u2 = bf16(x * p[f"{l}.ln2"])
             gu = rstd(x)[:, None] * (u2 @ p[f"{l}.gate_up_w"].T)
             gu = gu.reshape(T, I // 64, 2, 64)
             g, up = gu[:, :, 0, :].reshape(T, I), gu[:, :, 1, :].reshape(T, I)
-            act = bf16_st(torch.nn.functional.silu(g) * up)
+            act = bf16(torch.nn.functional.silu(g) * up)
             x = x + act @ p[f"{l}.down_w"].T
-        uF = bf16_st(x * p["final_norm"])
+        uF = bf16(x * p["final_norm"])
         W = p["embed"] if c["tie_embeddings"] else p["lm_head"]
         logits = rstd(x)[:, None] * (uF @ W.T)
         return torch.log_softmax(logits, -1)[torch.arange(T), tgt]
