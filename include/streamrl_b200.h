@@ -239,6 +239,23 @@ int srl_truncated_is_weight(double pi_logprob_sum, double mu_logprob_sum, double
                             double* out);
 /* ess (rl_math.cpp:152-163): SRL_ESS_UNDEFINED when all weights are zero. */
 int srl_ess(const double* weights, int32_t n, double* out);
+/* is_reinforce_gradient / reinforce_gradient for a TabularPolicy
+ * (rl_math.cpp:211-276, GradientTable rl_math.hpp:39-46) on the device.
+ * Trajectories packed: tokens[offsets[n_traj]], prompt_ids[n_traj],
+ * behavior_logprobs packed like tokens, rewards[n_traj]; baseline packed like
+ * tokens (b(prompt, t) -- the caller's BaselineTable::at lookups, which throw
+ * on a missing cell in the reference).  use_is = 0: reinforce_gradient (clamp
+ * and granularity ignored); granularity 0 = Sequence, 1 = PerToken.
+ * Output: grad_rows [(n_rows + 1) x V] -- the policy's rows in ContextKey
+ * order (std::map order, as srl_policy_tabular_create stores them), then the
+ * default row -- and row_touched[n_rows + 1]: 1 where the
+ * reference would have created the row (a non-zero contribution landed). */
+int srl_tabular_is_reinforce_gradient(const srl_policy* p, int32_t n_traj, const char* const* prompt_ids,
+                                      const int32_t* tokens, const int64_t* offsets,
+                                      const double* behavior_logprobs, const double* rewards,
+                                      const double* baseline, int32_t use_is, double clamp,
+                                      int32_t granularity, double* grad_rows, int32_t* row_touched);
+
 
 /* ------------------------------------------------ decoder trainer step --- */
 /* IS-REINFORCE for the decoder policy: the reference's
@@ -250,6 +267,10 @@ typedef struct srl_trainer srl_trainer;
 typedef struct {
   int32_t max_tokens;  /* packed rows per step (sum of sequence lengths - 1) */
   int32_t device;      /* the trainer's device (weights are peer-copied there); < 0 = the policy's */
+  int32_t fast_bf16;   /* 0 (default): precise -- activations and backward operands carried as
+                          bf16 hi + lo pairs (fp32-class, the 1e-3 parity bar); 1: single bf16
+                          operands (faster, ~1e-2 gradient agreement) */
+  int32_t logit_chunk; /* LM-head rows per pass (0 = 16384) */
 } srl_trainer_options;
 typedef struct {
   double objective;    /* J at the current weights */

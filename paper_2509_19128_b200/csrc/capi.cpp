@@ -16,6 +16,10 @@ int toy_policy_logprobs(const Policy& p, const std::string& prompt_id,
                         const std::vector<int32_t>& tokens, std::vector<double>& out, int device);
 int decoder_policy_logprobs(const DecoderWeights& w, const std::vector<int32_t>& tokens,
                             std::vector<double>& out);
+int tabular_is_reinforce_gradient(const Policy& p, int n_traj, const char* const* prompt_ids,
+                                  const int32_t* tokens, const int64_t* offsets, const double* mu,
+                                  const double* rewards, const double* baseline, bool use_is, double clamp,
+                                  int granularity, double* grad_out, int32_t* touched_out, int device);
 }  // namespace srl
 
 using namespace srl;
@@ -461,6 +465,30 @@ extern "C" int srl_truncated_is_weight(double pi_sum, double mu_sum, double clam
     return fail(SRL_INVALID_ARGUMENT, "truncated_is_weight: non-finite log-probability");
   *out = std::min(clamp, std::exp(pi_sum - mu_sum));
   return SRL_OK;
+}
+
+// is_reinforce_gradient for TabularPolicy (rl_math.cpp:211-276), tabular_grad.cu
+extern "C" int srl_tabular_is_reinforce_gradient(const srl_policy* p, int32_t n_traj,
+                                                 const char* const* prompt_ids, const int32_t* tokens,
+                                                 const int64_t* offsets, const double* behavior_logprobs,
+                                                 const double* rewards, const double* baseline, int32_t use_is,
+                                                 double clamp, int32_t granularity, double* grad_rows,
+                                                 int32_t* row_touched) {
+  return guarded([&] {
+    if (!p || !offsets || !rewards || !baseline || !grad_rows || !row_touched || !prompt_ids ||
+        (use_is && !behavior_logprobs) || (granularity != 0 && granularity != 1))
+      return fail(SRL_INVALID_ARGUMENT, "tabular_is_reinforce_gradient: bad arguments");
+    if (p->p.type != SRL_POLICY_TABULAR) return fail(SRL_INVALID_ARGUMENT, "gradient: needs a tabular policy");
+    std::string why;
+    if (p->p.validate(&why) != SRL_OK) return fail(SRL_INVALID_POLICY, why);
+    int st;
+    if ((st = require_device(0))) return st;
+    std::vector<double> zeros;
+    if (!use_is) zeros.assign((size_t)std::max<int64_t>(0, offsets[std::max(0, n_traj)]), 0.0);
+    return tabular_is_reinforce_gradient(p->p, n_traj, prompt_ids, tokens, offsets,
+                                         use_is ? behavior_logprobs : zeros.data(), rewards, baseline,
+                                         use_is != 0, clamp, granularity, grad_rows, row_touched, 0);
+  });
 }
 
 // ess (rl_math.cpp:152-163)

@@ -68,6 +68,24 @@ struct EpiParams {
   const __nv_bfloat16* gu_in = nullptr; // EPI_SWIGLU_BWD: gate | up pre-activations [M x 2N]
   int ldT = 0;
   int* tile_flags = nullptr;            // gemm_mn_launch split-K ordering (>= tiles ints, zeroed once)
+  // Split operands (gemm_big only; the trainer's precise mode carries a value
+  // as two bf16 halves hi + lo = fp32 to ~2^-17).  The K loop is the
+  // concatenation of up to 3 segments of seg_kb k-blocks each (K = segments *
+  // seg_kb * 64); segment s reads X and W shifted by x_off[s] / w_off[s]
+  // elements -- along K for a K-major operand, along MN for an MN-major one.
+  // (hi + lo) W = [hi | lo] . [W ; W]: 2 segments, x_off = {0, lo}, w_off = 0;
+  // (dh + dl)^T (uh + ul) ~ dh uh + dh ul + dl uh: 3 segments.
+  int seg_kb = 0;                       // 0: one plain segment
+  int x_off0 = 0, x_off1 = 0, x_off2 = 0;
+  int w_off0 = 0, w_off1 = 0, w_off2 = 0;
+  // Split bf16 outputs (EPI_RESID xg, EPI_SWIGLU act, EPI_DLOGITS, EPI_SWIGLU_BWD):
+  // hi at column c, lo = bf16(v - hi) at column c + lo_off (0: hi only).
+  // EPI_RESID's xg row stride is N + lo_off.
+  int lo_off = 0;
+  float* out2_f32 = nullptr;            // EPI_SWIGLU: fp32 rstd-scaled gate | up [M x N]
+  const float* gu_in_f32 = nullptr;     // EPI_SWIGLU_BWD: fp32 gate | up (instead of gu_in)
+  const float* row_scale = nullptr;     // EPI_SWIGLU_BWD: dgu[m, :] *= row_scale[m]
+  int fold_rstd = 0;                    // EPI_DLOGITS: d *= rstd[m] (the LM head's rstd folded in)
   // debug: per-CTA %globaltimer phase stamps [ctas x 8] (null = off)
   unsigned long long* stamps = nullptr;
 };

@@ -153,20 +153,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* a = smem + stage * L::kStageBytes;
           mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
           if (kb == 0 && t == (int)blockIdx.x) big_stamp(epi, 2);
+          // split operands: segment sg of the K concatenation (see EpiParams)
+          int kl = kb, xo = 0, wo = 0;
+          if (epi.seg_kb > 0) {
+            const int sg = kb / epi.seg_kb;
+            kl = kb - sg * epi.seg_kb;
+            xo = sg == 0 ? epi.x_off0 : sg == 1 ? epi.x_off1 : epi.x_off2;
+            wo = sg == 0 ? epi.w_off0 : sg == 1 ? epi.w_off1 : epi.w_off2;
+          }
           if constexpr (AMN) {  // 64 x 64 boxes: [k rows][64 MN columns], 8 KB each
-            tma_load_2d(a, &tw, &full[stage], n0, kb * kBK);
-            tma_load_2d(a + 8192, &tw, &full[stage], n0 + 64, kb * kBK);
+            tma_load_2d(a, &tw, &full[stage], n0 + wo, kl * kBK);
+            tma_load_2d(a + 8192, &tw, &full[stage], n0 + 64 + wo, kl * kBK);
           } else {
-            tma_load_2d(a, &tw, &full[stage], kb * kBK, n0);
+            tma_load_2d(a, &tw, &full[stage], kl * kBK + wo, n0);
           }
           if constexpr (BMN) {
 #pragma unroll
             for (int h = 0; h < TOK / 64; ++h)
-              tma_load_2d(a + L::kABytes + h * 8192, &tx, &full[stage], t0 + h * 64, kb * kBK);
+              tma_load_2d(a + L::kABytes + h * 8192, &tx, &full[stage], t0 + h * 64 + xo, kl * kBK);
           } else {
 #pragma unroll
             for (int h = 0; h < TOK / 128; ++h)  // the X map's box is 128 rows
-              tma_load_2d(a + L::kABytes + h * 128 * 128, &tx, &full[stage], kb * kBK, t0 + h * 128);
+              tma_load_2d(a + L::kABytes + h * 128 * 128, &tx, &full[stage], kl * kBK + xo, t0 + h * 128);
           }
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
         }
@@ -354,8 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               tg = epi.tgt_row[tc0 + lane];
             }
             const bool vec = epi.outT_bf16 == nullptr && (epi.ld_bf16 & 7) == 0 && (N & 7) == 0 &&
-                             (reinterpret_cast<uintptr_t>(epi.out_bf16) & 15) == 0;
-            uint16_t* st16 = reinterpret_cast<uint16_t*>(tile);  // [32 tokens][128] bf16 staging
+                             (reinterpret_cast<uintptr_t>(epi.out_bf16) & 15) == 0 &&
+                             (epi.lo_off & 7) == 0;
+            // [32 tokens][128] bf16 staging, the lo halves (split output) after it
+            uint16_t* st16 = reinterpret_cast<uint16_t*>(tile);
             uint32_t packed[16];
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -364,12 +374,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float cj = __shfl_sync(0xffffffffu, cf, j);
               const int tj = __shfl_sync(0xffffffffu, tg, j);
               const float x = __uint_as_float(r[j]) * rj;
-              const float d = j < jn ? cj * ((n == tj ? 1.f : 0.f) - __expf(x - lj)) : 0.f;
+              float d = j < jn ? cj * ((n == tj ? 1.f : 0.f) - __expf(x - lj)) : 0.f;
+              if (epi.fold_rstd) d *= rj;
               const __nv_bfloat16 b = __float2bfloat16(d);
               const uint32_t bits = (uint32_t)__bfloat16_as_ushort(b);
+              const __nv_bfloat16 bl = __float2bfloat16(d - __bfloat162float(b));
               if (vec) {
                 st16[j * 128 + tid] = (uint16_t)bits;
+                if (epi.lo_off) st16[4096 + j * 128 + tid] = __bfloat16_as_ushort(bl);
               } else {
+                if (epi.lo_off && j < jn && n < N) epi.out_bf16[(size_t)(tc0 + j) * epi.ld_bf16 + n + epi.lo_off] = bl;
                 if (j < jn && n < N) epi.out_bf16[(size_t)(tc0 + j) * epi.ld_bf16 + n] = b;
                 if (j & 1) packed[j >> 1] |= bits << 16;
                 else packed[j >> 1] = bits;
@@ -380,9 +394,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 const int idx = tid + 128 * k, j = idx >> 4, c8 = (idx & 15) * 8;
-                if (j < jn && n0 + c8 < N)
-                  *reinterpret_cast<uint4*>(epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + n0 + c8) =
-                      *reinterpret_cast<const uint4*>(&st16[j * 128 + c8]);
+                if (j < jn && n0 + c8 < N) {
+                  __nv_bfloat16* dst = epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + n0 + c8;
+                  *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(&st16[j * 128 + c8]);
+                  if (epi.lo_off)
+                    *reinterpret_cast<uint4*>(dst + epi.lo_off) =
+                        *reinterpret_cast<const uint4*>(&st16[4096 + j * 128 + c8]);
+                }
               }
               sync();  // the staging area is reused next
             } else if (epi.outT_bf16 && n < N) {  // columns past M are written as 0 (padding)
@@ -410,7 +428,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const size_t o = (size_t)(tc0 + j) * N + n;
                 x = xr[j] + __uint_as_float(r[j]);
                 epi.resid[o] = x;
-                epi.xg[o] = __float2bfloat16(x * gain);
+                const float xgv = x * gain;
+                const __nv_bfloat16 hi = __float2bfloat16(xgv);
+                if (epi.lo_off == 0) {
+                  epi.xg[o] = hi;
+                } else {  // split: row stride N + lo_off, lo = the rounding residual
+                  const size_t os = (size_t)(tc0 + j) * (N + epi.lo_off) + n;
+                  epi.xg[os] = hi;
+                  epi.xg[os + epi.lo_off] = __float2bfloat16(xgv - __bfloat162float(hi));
+                }
               }
               xr[j] = x * x;
             }
@@ -492,6 +518,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               tile[j * kPitch + tid] = __uint_as_float(r[j]) * rj;
             }
             sync();
+            if (epi.out2_f32) {  // fp32 gate | up copy (precise backward)
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const int idx = tid + 128 * k, j = idx >> 5, c4 = (idx & 31) * 4;
+                if (j >= jn) continue;
+                *reinterpret_cast<float4*>(epi.out2_f32 + (size_t)(tc0 + j) * N + n0 + c4) =
+                    *reinterpret_cast<const float4*>(&tile[j * kPitch + c4]);
+              }
+            }
             if (epi.out2_bf16) {
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
@@ -520,7 +555,21 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint4 o;
               o.x = bf2_bits(a[0], a[1]); o.y = bf2_bits(a[2], a[3]);
               o.z = bf2_bits(a[4], a[5]); o.w = bf2_bits(a[6], a[7]);
-              *reinterpret_cast<uint4*>(epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + (n0 >> 1) + c8) = o;
+              __nv_bfloat16* dst = epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + (n0 >> 1) + c8;
+              *reinterpret_cast<uint4*>(dst) = o;
+              if (epi.lo_off) {
+                const uint32_t hw[4] = {o.x, o.y, o.z, o.w};
+                float lo[8];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  lo[2 * e] = a[2 * e] - __uint_as_float(hw[e] << 16);
+                  lo[2 * e + 1] = a[2 * e + 1] - __uint_as_float(hw[e] & 0xffff0000u);
+                }
+                uint4 ol;
+                ol.x = bf2_bits(lo[0], lo[1]); ol.y = bf2_bits(lo[2], lo[3]);
+                ol.z = bf2_bits(lo[4], lo[5]); ol.w = bf2_bits(lo[6], lo[7]);
+                *reinterpret_cast<uint4*>(dst + epi.lo_off) = ol;
+              }
             }
             sync();  // the staged chunk is reused next
             continue;
@@ -533,33 +582,57 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint16_t* st16 = reinterpret_cast<uint16_t*>(tile);  // [32][256]
             const size_t gcol = (size_t)2 * n0 + lc;
             // all 64 gate / up loads in flight before the first store
-            uint16_t gb[32], ub[32];
-            const uint16_t* gu = reinterpret_cast<const uint16_t*>(epi.gu_in);
+            float gf[32], uf[32];
+            if (epi.gu_in_f32) {  // precise: fp32 gate | up, row stride 2N
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const size_t row = (size_t)(tc0 + (j < jn ? j : 0)) * epi.ld_bf16;
-              gb[j] = n < N ? __ldg(gu + row + gcol) : (uint16_t)0;
-              ub[j] = n < N ? __ldg(gu + row + gcol + 64) : (uint16_t)0;
+              for (int j = 0; j < 32; ++j) {
+                const size_t row = (size_t)(tc0 + (j < jn ? j : 0)) * (2 * (size_t)N);
+                gf[j] = n < N ? __ldg(epi.gu_in_f32 + row + gcol) : 0.f;
+                uf[j] = n < N ? __ldg(epi.gu_in_f32 + row + gcol + 64) : 0.f;
+              }
+            } else {
+              const uint16_t* gu = reinterpret_cast<const uint16_t*>(epi.gu_in);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const size_t row = (size_t)(tc0 + (j < jn ? j : 0)) * epi.ld_bf16;
+                gf[j] = n < N ? __bfloat162float(__ushort_as_bfloat16(__ldg(gu + row + gcol))) : 0.f;
+                uf[j] = n < N ? __bfloat162float(__ushort_as_bfloat16(__ldg(gu + row + gcol + 64))) : 0.f;
+              }
             }
+            float rsc = 1.f;
+            if (epi.row_scale != nullptr && tc0 + lane < M) rsc = epi.row_scale[tc0 + lane];
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const float gv = __bfloat162float(__ushort_as_bfloat16(gb[j]));
-              const float uv = __bfloat162float(__ushort_as_bfloat16(ub[j]));
-              const float da = __uint_as_float(r[j]);
+              const float gv = gf[j], uv = uf[j];
+              const float da = __uint_as_float(r[j]) * __shfl_sync(0xffffffffu, rsc, j);
               const float sg = 1.f / (1.f + expf(-gv));  // as swiglu_bwd_kernel
               const float silu = gv * sg;
-              st16[j * 256 + lc] = __bfloat16_as_ushort(__float2bfloat16(da * uv * (sg * (1.f + gv * (1.f - sg)))));
-              st16[j * 256 + lc + 64] = __bfloat16_as_ushort(__float2bfloat16(da * silu));
+              gf[j] = da * uv * (sg * (1.f + gv * (1.f - sg)));  // d gate
+              uf[j] = da * silu;                                  // d up
             }
-            sync();
+            // hi halves, then (split output) the lo halves through the same staging
+            for (int part = 0; part < (epi.lo_off ? 2 : 1); ++part) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const int idx = tid + 128 * k, j = idx >> 5, c8 = (idx & 31) * 8;
-              if (j < jn && n0 + (c8 >> 1) < N)
-                *reinterpret_cast<uint4*>(epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + 2 * n0 + c8) =
-                    *reinterpret_cast<const uint4*>(&st16[j * 256 + c8]);
+              for (int j = 0; j < 32; ++j) {
+                __nv_bfloat16 hg = __float2bfloat16(gf[j]), hu = __float2bfloat16(uf[j]);
+                if (part) {
+                  hg = __float2bfloat16(gf[j] - __bfloat162float(hg));
+                  hu = __float2bfloat16(uf[j] - __bfloat162float(hu));
+                }
+                st16[j * 256 + lc] = __bfloat16_as_ushort(hg);
+                st16[j * 256 + lc + 64] = __bfloat16_as_ushort(hu);
+              }
+              sync();
+              const int off = part ? epi.lo_off : 0;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const int idx = tid + 128 * k, j = idx >> 5, c8 = (idx & 31) * 8;
+                if (j < jn && n0 + (c8 >> 1) < N)
+                  *reinterpret_cast<uint4*>(epi.out_bf16 + (size_t)(tc0 + j) * epi.ld_bf16 + 2 * n0 + c8 + off) =
+                      *reinterpret_cast<const uint4*>(&st16[j * 256 + c8]);
+              }
+              sync();  // the staging area is reused next
             }
-            sync();  // the staging area is reused next
             continue;
           }
           {

@@ -42,8 +42,16 @@ void launch_loss_dlogits(const float* logits, const float* pmax, const double* p
 // RMSNorm backward for y = rstd(x) * (x . g) W^T with dzw = dy W:
 //   du = rstd * dzw ; drstd = sum_k dzw * x_k g_k
 //   dx += du . g - rstd^3 / H * drstd * x ;  dg += sum_rows du . x
+// prescaled: dzw already carries the row's rstd (dzw' = rstd * dy W, the
+// trainer's precise mode folds rstd into dy): du = dzw'.
 void launch_rmsnorm_bwd(const float* dzw, const float* x, const __nv_bfloat16* g,
-                        const float* rstd, int T, int H, float* dx, float* dg, cudaStream_t st);
+                        const float* rstd, int T, int H, float* dx, float* dg, cudaStream_t st,
+                        bool prescaled = false);
+// Split bf16 pair of v = src[r, c] * row_scale[r] * col_gain[c] (either may be
+// null): dst row r = [hi (cols) | lo (cols)], hi = bf16(v), lo = bf16(v - hi).
+// cols % 4 == 0.
+void launch_split_bf16(const float* src, int rows, int cols, const float* row_scale,
+                       const __nv_bfloat16* col_gain, __nv_bfloat16* dst, cudaStream_t st);
 // rstd[t] = 1/sqrt(mean(x^2) + eps)
 void launch_row_rstd(const float* x, int T, int H, float eps, float* rstd, cudaStream_t st);
 
@@ -58,7 +66,7 @@ void launch_attention_bwd(const __nv_bfloat16* q, const __nv_bfloat16* o, const 
                           const int32_t* row_slot, const int32_t* row_pos,
                           const int32_t* seq_start, const int32_t* seq_len,
                           const int32_t* block_table, int pages_per_seq, int T, int n_seq, int nq,
-                          int nkv, int hd, float* dqkv, cudaStream_t st);
+                          int nkv, int hd, float* dqkv, cudaStream_t st, bool split = false);
 // Causal attention forward over packed sequences on the tensor cores
 // (train_attn.cu): O [T x nq*hd] bf16 and lse [T x nq] (scaled scores).
 cudaError_t launch_attention_fwd_mma(const __nv_bfloat16* q, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
@@ -66,13 +74,13 @@ cudaError_t launch_attention_fwd_mma(const __nv_bfloat16* q, const __nv_bfloat16
                                      const int32_t* block_table, int pages_per_seq, int n_seq, int nq,
                                      int nkv, int hd, __nv_bfloat16* out, float* lse, cudaStream_t st,
                                      const int32_t* seg_pos0 = nullptr, const int32_t* seg_slot = nullptr,
-                                     int max_rows = 0);
+                                     int max_rows = 0, int out_lo = 0);
 // The tensor-core path of the above (train_attn.cu); D = rowsum(dO * O).
 cudaError_t launch_attention_bwd_mma(const __nv_bfloat16* q, const float* d_o, const float* lse,
                                      const float* D, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                                      const int32_t* seq_start, const int32_t* seq_len,
                                      const int32_t* block_table, int pages_per_seq, int n_seq, int nq,
-                                     int nkv, int hd, float* dqkv, cudaStream_t st);
+                                     int nkv, int hd, float* dqkv, cudaStream_t st, bool split = false);
 // Undo RoPE on the q/k part of dqkv in place (rotation by -angle).
 void launch_rope_bwd(float* dqkv, const int32_t* row_pos, const float* cos_sin, int T, int nq,
                      int nkv, int hd, cudaStream_t st);

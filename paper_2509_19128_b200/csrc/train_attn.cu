@@ -137,6 +137,28 @@ __device__ __forceinline__ void store_f32(__nv_bfloat16* X, __nv_bfloat16* XT, c
     }
   }
 }
+// Split: hi = bf16(v) into X / XT, lo = bf16(v - hi) into Xl / XlT.
+template <int HD>
+__device__ __forceinline__ void store_f32_split(__nv_bfloat16* X, __nv_bfloat16* XT, __nv_bfloat16* Xl,
+                                                __nv_bfloat16* XlT, const float4 (&v)[kNvF<HD>]) {
+  constexpr int P = HD + 8, V4 = HD / 4;
+#pragma unroll
+  for (int k = 0; k < kNvF<HD>; ++k) {
+    const int e = threadIdx.x + k * kWarps * 32, r = e / V4, c = (e % V4) * 4;
+    const float f[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat16 h = __float2bfloat16(f[i]);
+      const __nv_bfloat16 l = __float2bfloat16(f[i] - __bfloat162float(h));
+      X[r * P + c + i] = h;
+      Xl[r * P + c + i] = l;
+      if (XT) {
+        XT[(c + i) * kPadT + r] = h;
+        XlT[(c + i) * kPadT + r] = l;
+      }
+    }
+  }
+}
 template <int HD, class Src>
 __device__ __forceinline__ void stage_f32(__nv_bfloat16* X, __nv_bfloat16* XT, int valid, Src src) {
   float4 v[kNvF<HD>];
@@ -151,11 +173,16 @@ struct BwdSmem {
   static constexpr size_t tileT = sizeof(__nv_bfloat16) * HD * kPadT;
   static constexpr size_t vec = sizeof(float) * kBlk;
   // dkv: K, V, Q, Q^T, dO, dO^T, lse, D ; dq: Q, dO, K, K^T, V, lse, D
+  // (+ split: the lo halves of dO, and dO^T for dkv, after them)
   static constexpr size_t dkv = 4 * tile + 2 * tileT + 2 * vec;
   static constexpr size_t dq = 4 * tile + tileT + 2 * vec;
+  static constexpr size_t dkv_split = dkv + tile + tileT;
+  static constexpr size_t dq_split = dq + tile;
 };
 
-template <int HD>
+// SPLIT (the trainer's precise mode): dO, P and dS enter the MMAs as bf16
+// hi + lo halves (P dO ~ Ph dOh + Ph dOl + Pl dOh), fp32-class products.
+template <int HD, bool SPLIT>
 __global__ void __launch_bounds__(kWarps * 32)
     attn_bwd_dkv_mma(const __nv_bfloat16* __restrict__ q, const float* __restrict__ d_o,
                      const float* __restrict__ lse, const float* __restrict__ D,
@@ -174,6 +201,8 @@ __global__ void __launch_bounds__(kWarps * 32)
   __nv_bfloat16* dOt = reinterpret_cast<__nv_bfloat16*>(smem + 4 * S::tile + S::tileT);
   float* s_lse = reinterpret_cast<float*>(smem + 4 * S::tile + 2 * S::tileT);
   float* s_D = s_lse + kBlk;
+  __nv_bfloat16* dOl = reinterpret_cast<__nv_bfloat16*>(smem + S::dkv);
+  __nv_bfloat16* dOlt = reinterpret_cast<__nv_bfloat16*>(smem + S::dkv + S::tile);
 
   const int slot = blockIdx.y, kh = blockIdx.z;
   const int L = seq_len[slot], s0 = seq_start[slot];
@@ -218,14 +247,21 @@ __global__ void __launch_bounds__(kWarps * 32)
       __syncthreads();  // previous tiles consumed
       if constexpr (kPipe) {
         store_bf16<HD>(Qs, Qt, pq);
-        store_f32<HD>(dOs, dOt, pd);
+        if constexpr (SPLIT) store_f32_split<HD>(dOs, dOt, dOl, dOlt, pd);
+        else store_f32<HD>(dOs, dOt, pd);
         if (threadIdx.x < kBlk) {
           s_lse[threadIdx.x] = pl;
           s_D[threadIdx.x] = pD;
         }
       } else {
         stage_bf16<HD>(Qs, Qt, qvalid, [&](int r) { return q + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
-        stage_f32<HD>(dOs, dOt, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+        if constexpr (SPLIT) {
+          float4 v[kNvF<HD>];
+          load_f32<HD>(v, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+          store_f32_split<HD>(dOs, dOt, dOl, dOlt, v);
+        } else {
+          stage_f32<HD>(dOs, dOt, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+        }
         for (int r = threadIdx.x; r < kBlk; r += kWarps * 32) {
           s_lse[r] = r < qvalid ? lse[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
           s_D[r] = r < qvalid ? D[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
@@ -255,6 +291,10 @@ __global__ void __launch_bounds__(kWarps * 32)
           mma16816(st[n], ak, b0, b1);
           frag_b(b0, b1, dOs, P, n * 8, kk * 16, lane);
           mma16816(dpt[n], av, b0, b1);
+          if constexpr (SPLIT) {
+            frag_b(b0, b1, dOl, P, n * 8, kk * 16, lane);
+            mma16816(dpt[n], av, b0, b1);
+          }
         }
       }
       // P^T and dS^T (scaled), causal: query position >= key position
@@ -273,22 +313,39 @@ __global__ void __launch_bounds__(kWarps * 32)
       // dV += P^T dO, dK += dS^T Q   (k = 64 queries in 4 steps of 16)
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
-        uint32_t ap[4], ad[4];
-        ap[0] = pack_bf16(st[2 * ks][0], st[2 * ks][1]);
-        ap[1] = pack_bf16(st[2 * ks][2], st[2 * ks][3]);
-        ap[2] = pack_bf16(st[2 * ks + 1][0], st[2 * ks + 1][1]);
-        ap[3] = pack_bf16(st[2 * ks + 1][2], st[2 * ks + 1][3]);
-        ad[0] = pack_bf16(dpt[2 * ks][0], dpt[2 * ks][1]);
-        ad[1] = pack_bf16(dpt[2 * ks][2], dpt[2 * ks][3]);
-        ad[2] = pack_bf16(dpt[2 * ks + 1][0], dpt[2 * ks + 1][1]);
-        ad[3] = pack_bf16(dpt[2 * ks + 1][2], dpt[2 * ks + 1][3]);
+        uint32_t ap[4], ad[4], apl[4], adl[4];
+        if constexpr (SPLIT) {
+          split2(st[2 * ks][0], st[2 * ks][1], ap[0], apl[0]);
+          split2(st[2 * ks][2], st[2 * ks][3], ap[1], apl[1]);
+          split2(st[2 * ks + 1][0], st[2 * ks + 1][1], ap[2], apl[2]);
+          split2(st[2 * ks + 1][2], st[2 * ks + 1][3], ap[3], apl[3]);
+          split2(dpt[2 * ks][0], dpt[2 * ks][1], ad[0], adl[0]);
+          split2(dpt[2 * ks][2], dpt[2 * ks][3], ad[1], adl[1]);
+          split2(dpt[2 * ks + 1][0], dpt[2 * ks + 1][1], ad[2], adl[2]);
+          split2(dpt[2 * ks + 1][2], dpt[2 * ks + 1][3], ad[3], adl[3]);
+        } else {
+          ap[0] = pack_bf16(st[2 * ks][0], st[2 * ks][1]);
+          ap[1] = pack_bf16(st[2 * ks][2], st[2 * ks][3]);
+          ap[2] = pack_bf16(st[2 * ks + 1][0], st[2 * ks + 1][1]);
+          ap[3] = pack_bf16(st[2 * ks + 1][2], st[2 * ks + 1][3]);
+          ad[0] = pack_bf16(dpt[2 * ks][0], dpt[2 * ks][1]);
+          ad[1] = pack_bf16(dpt[2 * ks][2], dpt[2 * ks][3]);
+          ad[2] = pack_bf16(dpt[2 * ks + 1][0], dpt[2 * ks + 1][1]);
+          ad[3] = pack_bf16(dpt[2 * ks + 1][2], dpt[2 * ks + 1][3]);
+        }
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           uint32_t b0, b1;
           frag_b(b0, b1, dOt, kPadT, n * 8, ks * 16, lane);
           mma16816(dv[n], ap, b0, b1);
+          if constexpr (SPLIT) {
+            mma16816(dv[n], apl, b0, b1);
+            frag_b(b0, b1, dOlt, kPadT, n * 8, ks * 16, lane);
+            mma16816(dv[n], ap, b0, b1);
+          }
           frag_b(b0, b1, Qt, kPadT, n * 8, ks * 16, lane);
           mma16816(dk[n], ad, b0, b1);
+          if constexpr (SPLIT) mma16816(dk[n], adl, b0, b1);
         }
       }
     }
@@ -309,7 +366,7 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
 }
 
-template <int HD>
+template <int HD, bool SPLIT>
 __global__ void __launch_bounds__(kWarps * 32)
     attn_bwd_dq_mma(const __nv_bfloat16* __restrict__ q, const float* __restrict__ d_o,
                     const float* __restrict__ lse, const float* __restrict__ D,
@@ -327,6 +384,7 @@ __global__ void __launch_bounds__(kWarps * 32)
   __nv_bfloat16* Kt = reinterpret_cast<__nv_bfloat16*>(smem + 4 * S::tile);
   float* s_lse = reinterpret_cast<float*>(smem + 4 * S::tile + S::tileT);
   float* s_D = s_lse + kBlk;
+  __nv_bfloat16* dOl = reinterpret_cast<__nv_bfloat16*>(smem + S::dq);
 
   const int slot = blockIdx.y, h = blockIdx.z;
   const int L = seq_len[slot], s0 = seq_start[slot];
@@ -336,7 +394,13 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qvalid = min(kBlk, L - q0);
   stage_bf16<HD>(Qs, nullptr, qvalid, [&](int r) { return q + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
-  stage_f32<HD>(dOs, nullptr, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+  if constexpr (SPLIT) {
+    float4 v[kNvF<HD>];
+    load_f32<HD>(v, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+    store_f32_split<HD>(dOs, nullptr, dOl, nullptr, v);
+  } else {
+    stage_f32<HD>(dOs, nullptr, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+  }
   for (int r = threadIdx.x; r < kBlk; r += kWarps * 32) {
     s_lse[r] = r < qvalid ? lse[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
     s_D[r] = r < qvalid ? D[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
@@ -381,9 +445,10 @@ __global__ void __launch_bounds__(kWarps * 32)
       for (int i = 0; i < 4; ++i) s[n][i] = dp[n][i] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk) {
-      uint32_t aq[4], ad[4];
+      uint32_t aq[4], ad[4], adl[4];
       frag_a(aq, Qs, P, qr, kk * 16, lane);
       frag_a(ad, dOs, P, qr, kk * 16, lane);
+      if constexpr (SPLIT) frag_a(adl, dOl, P, qr, kk * 16, lane);
 #pragma unroll
       for (int n = 0; n < 8; ++n) {
         uint32_t b0, b1;
@@ -391,6 +456,7 @@ __global__ void __launch_bounds__(kWarps * 32)
         mma16816(s[n], aq, b0, b1);
         frag_b(b0, b1, Vs, P, n * 8, kk * 16, lane);
         mma16816(dp[n], ad, b0, b1);
+        if constexpr (SPLIT) mma16816(dp[n], adl, b0, b1);
       }
     }
 #pragma unroll
@@ -408,16 +474,24 @@ __global__ void __launch_bounds__(kWarps * 32)
     // dQ += dS K  (k = 64 keys in 4 steps of 16)
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
-      uint32_t a[4];
-      a[0] = pack_bf16(dp[2 * ks][0], dp[2 * ks][1]);
-      a[1] = pack_bf16(dp[2 * ks][2], dp[2 * ks][3]);
-      a[2] = pack_bf16(dp[2 * ks + 1][0], dp[2 * ks + 1][1]);
-      a[3] = pack_bf16(dp[2 * ks + 1][2], dp[2 * ks + 1][3]);
+      uint32_t a[4], al[4];
+      if constexpr (SPLIT) {
+        split2(dp[2 * ks][0], dp[2 * ks][1], a[0], al[0]);
+        split2(dp[2 * ks][2], dp[2 * ks][3], a[1], al[1]);
+        split2(dp[2 * ks + 1][0], dp[2 * ks + 1][1], a[2], al[2]);
+        split2(dp[2 * ks + 1][2], dp[2 * ks + 1][3], a[3], al[3]);
+      } else {
+        a[0] = pack_bf16(dp[2 * ks][0], dp[2 * ks][1]);
+        a[1] = pack_bf16(dp[2 * ks][2], dp[2 * ks][3]);
+        a[2] = pack_bf16(dp[2 * ks + 1][0], dp[2 * ks + 1][1]);
+        a[3] = pack_bf16(dp[2 * ks + 1][2], dp[2 * ks + 1][3]);
+      }
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         uint32_t b0, b1;
         frag_b(b0, b1, Kt, kPadT, n * 8, ks * 16, lane);
         mma16816(dq[n], a, b0, b1);
+        if constexpr (SPLIT) mma16816(dq[n], al, b0, b1);
       }
     }
   }
@@ -456,7 +530,7 @@ __global__ void __launch_bounds__(kWarps * 32)
                  const int32_t* __restrict__ seq_len, const int32_t* __restrict__ seg_pos0,
                  const int32_t* __restrict__ seg_slot, const int32_t* __restrict__ bt, int pps, int nq,
                  int nkv, float scale, __nv_bfloat16* __restrict__ out, float* __restrict__ lse_out,
-                 int split_p) {
+                 int split_p, int out_lo) {
   using S = FwdSmem<HD>;
   constexpr int P = S::P, NT = HD / 8;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -586,16 +660,25 @@ __global__ void __launch_bounds__(kWarps * 32)
     l_hi += __shfl_xor_sync(0xffffffffu, l_hi, off);
   }
   const float inv_lo = l_lo > 0.f ? 1.f / l_lo : 0.f, inv_hi = l_hi > 0.f ? 1.f / l_hi : 0.f;
-  const int qd = nq * HD;
+  // out row stride nq HD + out_lo; split (out_lo > 0): lo = bf16(o - hi) at + out_lo
+  const int ldo = nq * HD + out_lo;
 #pragma unroll
   for (int n = 0; n < NT; ++n) {
     const int d = n * 8 + (lane & 3) * 2;
-    if (ql_lo < qvalid)
-      *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(s0 + q0 + ql_lo) * qd + h * HD + d) =
-          __floats2bfloat162_rn(o[n][0] * inv_lo, o[n][1] * inv_lo);
-    if (ql_hi < qvalid)
-      *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(s0 + q0 + ql_hi) * qd + h * HD + d) =
-          __floats2bfloat162_rn(o[n][2] * inv_hi, o[n][3] * inv_hi);
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int ql = hh ? ql_hi : ql_lo;
+      if (ql >= qvalid) continue;
+      const float inv = hh ? inv_hi : inv_lo;
+      const float v0 = o[n][2 * hh] * inv, v1 = o[n][2 * hh + 1] * inv;
+      __nv_bfloat16* dst = out + (size_t)(s0 + q0 + ql) * ldo + h * HD + d;
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
+      *reinterpret_cast<__nv_bfloat162*>(dst) = hi;
+      if (out_lo) {
+        const float2 hf = __bfloat1622float2(hi);
+        *reinterpret_cast<__nv_bfloat162*>(dst + out_lo) = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
+      }
+    }
   }
   if (lse_out && (lane & 3) == 0) {
     if (ql_lo < qvalid) lse_out[(size_t)(s0 + q0 + ql_lo) * nq + h] = m_lo + logf(l_lo);
@@ -607,7 +690,7 @@ template <int HD>
 cudaError_t launch_fwd_t(const __nv_bfloat16* q, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                          const int32_t* seq_start, const int32_t* seq_len, const int32_t* pos0,
                          const int32_t* slot, const int32_t* bt, int pps, int n_seq, int max_rows, int nq,
-                         int nkv, float scale, __nv_bfloat16* out, float* lse, cudaStream_t st) {
+                         int nkv, float scale, __nv_bfloat16* out, float* lse, int out_lo, cudaStream_t st) {
   static const bool attr = cudaFuncSetAttribute(attn_fwd_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)FwdSmem<HD>::total) == cudaSuccess;
   // P as hi + lo bf16 halves (default; vs the fp64 oracle at 0.5B the
@@ -619,25 +702,27 @@ cudaError_t launch_fwd_t(const __nv_bfloat16* q, const __nv_bfloat16* kc, const 
   }();
   if (!attr) return cudaErrorInvalidValue;
   attn_fwd_mma<HD><<<dim3((max_rows + kBlk - 1) / kBlk, n_seq, nq), kWarps * 32, FwdSmem<HD>::total, st>>>(
-      q, kc, vc, seq_start, seq_len, pos0, slot, bt, pps, nq, nkv, scale, out, lse, split);
+      q, kc, vc, seq_start, seq_len, pos0, slot, bt, pps, nq, nkv, scale, out, lse, split, out_lo);
   return cudaGetLastError();
 }
 
-template <int HD>
+template <int HD, bool SPLIT>
 cudaError_t launch_t(const __nv_bfloat16* q, const float* d_o, const float* lse, const float* D,
                      const __nv_bfloat16* kc, const __nv_bfloat16* vc, const int32_t* seq_start,
                      const int32_t* seq_len, const int32_t* bt, int pps, int n_seq, int nq, int nkv,
                      float scale, float* dqkv, cudaStream_t st) {
   using S = BwdSmem<HD>;
-  static const bool attr = cudaFuncSetAttribute(attn_bwd_dkv_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)S::dkv) == cudaSuccess &&
-                           cudaFuncSetAttribute(attn_bwd_dq_mma<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)S::dq) == cudaSuccess;
+  constexpr size_t sk = SPLIT ? S::dkv_split : S::dkv, sq = SPLIT ? S::dq_split : S::dq;
+  static const bool attr =
+      cudaFuncSetAttribute(attn_bwd_dkv_mma<HD, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sk) ==
+          cudaSuccess &&
+      cudaFuncSetAttribute(attn_bwd_dq_mma<HD, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq) ==
+          cudaSuccess;
   if (!attr) return cudaErrorInvalidValue;
   // pages per sequence = 64-token blocks per sequence
-  attn_bwd_dkv_mma<HD><<<dim3(pps, n_seq, nkv), kWarps * 32, S::dkv, st>>>(
+  attn_bwd_dkv_mma<HD, SPLIT><<<dim3(pps, n_seq, nkv), kWarps * 32, sk, st>>>(
       q, d_o, lse, D, kc, vc, seq_start, seq_len, bt, pps, nq, nkv, scale, dqkv);
-  attn_bwd_dq_mma<HD><<<dim3(pps, n_seq, nq), kWarps * 32, S::dq, st>>>(
+  attn_bwd_dq_mma<HD, SPLIT><<<dim3(pps, n_seq, nq), kWarps * 32, sq, st>>>(
       q, d_o, lse, D, kc, vc, seq_start, seq_len, bt, pps, nq, nkv, scale, dqkv);
   return cudaGetLastError();
 }
@@ -648,14 +733,12 @@ cudaError_t launch_attention_bwd_mma(const __nv_bfloat16* q, const float* d_o, c
                                      const float* D, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
                                      const int32_t* seq_start, const int32_t* seq_len,
                                      const int32_t* block_table, int pages_per_seq, int n_seq, int nq,
-                                     int nkv, int hd, float* dqkv, cudaStream_t st) {
+                                     int nkv, int hd, float* dqkv, cudaStream_t st, bool split) {
   const float scale = 1.0f / sqrtf((float)hd);
-  if (hd == 64)
-    return launch_t<64>(q, d_o, lse, D, kc, vc, seq_start, seq_len, block_table, pages_per_seq, n_seq,
-                        nq, nkv, scale, dqkv, st);
-  if (hd == 128)
-    return launch_t<128>(q, d_o, lse, D, kc, vc, seq_start, seq_len, block_table, pages_per_seq, n_seq,
-                         nq, nkv, scale, dqkv, st);
+#define SRL_BWD_ARGS q, d_o, lse, D, kc, vc, seq_start, seq_len, block_table, pages_per_seq, n_seq, nq, nkv, scale, dqkv, st
+  if (hd == 64) return split ? launch_t<64, true>(SRL_BWD_ARGS) : launch_t<64, false>(SRL_BWD_ARGS);
+  if (hd == 128) return split ? launch_t<128, true>(SRL_BWD_ARGS) : launch_t<128, false>(SRL_BWD_ARGS);
+#undef SRL_BWD_ARGS
   return cudaErrorInvalidValue;
 }
 
@@ -666,15 +749,16 @@ cudaError_t launch_attention_fwd_mma(const __nv_bfloat16* q, const __nv_bfloat16
                                      const int32_t* seq_start, const int32_t* seq_len,
                                      const int32_t* block_table, int pages_per_seq, int n_seq, int nq,
                                      int nkv, int hd, __nv_bfloat16* out, float* lse, cudaStream_t st,
-                                     const int32_t* seg_pos0, const int32_t* seg_slot, int max_rows) {
+                                     const int32_t* seg_pos0, const int32_t* seg_slot, int max_rows,
+                                     int out_lo) {
   const float scale = 1.0f / sqrtf((float)hd);
   if (max_rows <= 0) max_rows = pages_per_seq * kBlk;
   if (hd == 64)
     return launch_fwd_t<64>(q, kc, vc, seq_start, seq_len, seg_pos0, seg_slot, block_table, pages_per_seq,
-                            n_seq, max_rows, nq, nkv, scale, out, lse, st);
+                            n_seq, max_rows, nq, nkv, scale, out, lse, out_lo, st);
   if (hd == 128)
     return launch_fwd_t<128>(q, kc, vc, seq_start, seq_len, seg_pos0, seg_slot, block_table, pages_per_seq,
-                             n_seq, max_rows, nq, nkv, scale, out, lse, st);
+                             n_seq, max_rows, nq, nkv, scale, out, lse, out_lo, st);
   return cudaErrorInvalidValue;
 }
 }  // namespace srl

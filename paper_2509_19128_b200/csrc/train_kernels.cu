@@ -196,7 +196,7 @@ __global__ void row_rstd_kernel(const float* __restrict__ x, int T, int H, float
 // in shared memory and added to dg once per block.
 __global__ void rmsnorm_bwd_kernel(const float* __restrict__ dzw, const float* __restrict__ x,
                                    const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd,
-                                   int T, int H, float* __restrict__ dx, float* __restrict__ dg) {
+                                   int T, int H, float* __restrict__ dx, float* __restrict__ dg, int pre) {
   extern __shared__ float s_dg[];
   for (int k = threadIdx.x; k < H; k += blockDim.x) s_dg[k] = 0.f;
   __syncthreads();
@@ -206,7 +206,8 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ dzw, const float* _
     const float4* dz4 = reinterpret_cast<const float4*>(dzw + (size_t)r * H);
     const float4* x4 = reinterpret_cast<const float4*>(x + (size_t)r * H);
     float4* dx4 = reinterpret_cast<float4*>(dx + (size_t)r * H);
-    const float rs = rstd[r];
+    const float rstd_r = rstd[r];
+    const float rs = pre ? 1.f : rstd_r;  // prescaled dzw carries rstd already
     float dr = 0.f;
     for (int k = lane; k < H4; k += 32) {
       const float4 d = dz4[k], v = x4[k];
@@ -216,7 +217,7 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ dzw, const float* _
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) dr += __shfl_xor_sync(0xffffffffu, dr, o);
-    const float coef = -rs * rs * rs / (float)H * dr;
+    const float coef = -rstd_r * rstd_r * rs / (float)H * dr;
     for (int k = lane; k < H4; k += 32) {
       const float4 d = dz4[k], v = x4[k];
       const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(g + 4 * k);
@@ -244,7 +245,7 @@ template <int NV>
 __global__ void __launch_bounds__(256)
     rmsnorm_bwd_reg_kernel(const float* __restrict__ dzw, const float* __restrict__ x,
                            const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd, int T,
-                           int H, float* __restrict__ dx, float* __restrict__ dg) {
+                           int H, float* __restrict__ dx, float* __restrict__ dg, int pre) {
   extern __shared__ float s_dg[];
   for (int k = threadIdx.x; k < H; k += blockDim.x) s_dg[k] = 0.f;
   __syncthreads();
@@ -266,7 +267,8 @@ __global__ void __launch_bounds__(256)
     const float4* dz4 = reinterpret_cast<const float4*>(dzw + (size_t)r * H);
     const float4* x4 = reinterpret_cast<const float4*>(x + (size_t)r * H);
     float4* dx4 = reinterpret_cast<float4*>(dx + (size_t)r * H);
-    const float rs = rstd[r];
+    const float rstd_r = rstd[r];
+    const float rs = pre ? 1.f : rstd_r;
     float4 d[NV], v[NV], o[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(256)
             d[i].w * v[i].w * gv[i].w;
 #pragma unroll
     for (int s = 16; s; s >>= 1) dr += __shfl_xor_sync(0xffffffffu, dr, s);
-    const float coef = -rs * rs * rs / (float)H * dr;
+    const float coef = -rstd_r * rstd_r * rs / (float)H * dr;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int k = lane + 32 * i;
@@ -360,22 +362,56 @@ __global__ void attn_bwd_dot_kernel(const float* __restrict__ d_o, const __nv_bf
   s = warp_sum(s);
   if (lane == 0) D[warp] = s;
 }
+// Split bf16 pair (hi | lo per row) of src * row_scale * col_gain, 4 columns per thread.
+__global__ void split_bf16_kernel(const float* __restrict__ src, int rows, int cols,
+                                  const float* __restrict__ row_scale, const __nv_bfloat16* __restrict__ col_gain,
+                                  __nv_bfloat16* __restrict__ dst) {
+  const int c4 = cols / 4;
+  const size_t n4 = (size_t)rows * c4;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / c4), c = (int)(i % c4) * 4;
+    float4 v = reinterpret_cast<const float4*>(src)[i];
+    if (row_scale) {
+      const float s = row_scale[r];
+      v.x *= s; v.y *= s; v.z *= s; v.w *= s;
+    }
+    if (col_gain) {
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(col_gain + c);
+      const float2 ga = __bfloat1622float2(g2[0]), gb = __bfloat1622float2(g2[1]);
+      v.x *= ga.x; v.y *= ga.y; v.z *= gb.x; v.w *= gb.y;
+    }
+    const __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y), h1 = __floats2bfloat162_rn(v.z, v.w);
+    const float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
+    const __nv_bfloat162 l0 = __floats2bfloat162_rn(v.x - f0.x, v.y - f0.y);
+    const __nv_bfloat162 l1 = __floats2bfloat162_rn(v.z - f1.x, v.w - f1.y);
+    __nv_bfloat16* row = dst + (size_t)r * 2 * cols + c;
+    *reinterpret_cast<__nv_bfloat162*>(row) = h0;
+    *reinterpret_cast<__nv_bfloat162*>(row + 2) = h1;
+    *reinterpret_cast<__nv_bfloat162*>(row + cols) = l0;
+    *reinterpret_cast<__nv_bfloat162*>(row + cols + 2) = l1;
+  }
+}
+
 // D = rowsum(dO * O) per (row, head) with L = hd / 8 lanes per pair, 8 elements
 // per lane (two float4 of dO, one 16-byte load of O); hd in {32, 64, 128, 256}
+// o_lo > 0: O is split, rows [hi (nq hd) | lo] (stride nq hd + o_lo), D uses hi + lo.
 template <int L>
 __global__ void attn_bwd_dot_v_kernel(const float* __restrict__ d_o, const __nv_bfloat16* __restrict__ o,
-                                      int pairs, int hd, float* __restrict__ D) {
+                                      int pairs, int hd, float* __restrict__ D, int nq, int o_lo) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x, p = t / L, j = t % L;
   float s = 0.f;
   if (p < pairs) {
     const size_t base = (size_t)p * hd + j * 8;
+    const size_t obase = o_lo ? (size_t)(p / nq) * (nq * hd + o_lo) + (size_t)(p % nq) * hd + j * 8 : base;
     const float4 a = *reinterpret_cast<const float4*>(d_o + base);
     const float4 b = *reinterpret_cast<const float4*>(d_o + base + 4);
-    const uint4 ov = *reinterpret_cast<const uint4*>(o + base);
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&ov);
-    const float2 o0 = __bfloat1622float2(h[0]), o1 = __bfloat1622float2(h[1]), o2 = __bfloat1622float2(h[2]),
-                 o3 = __bfloat1622float2(h[3]);
-    s = a.x * o0.x + a.y * o0.y + a.z * o1.x + a.w * o1.y + b.x * o2.x + b.y * o2.y + b.z * o3.x + b.w * o3.y;
+    for (int part = 0; part < (o_lo ? 2 : 1); ++part) {
+      const uint4 ov = *reinterpret_cast<const uint4*>(o + obase + (part ? o_lo : 0));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&ov);
+      const float2 o0 = __bfloat1622float2(h[0]), o1 = __bfloat1622float2(h[1]), o2 = __bfloat1622float2(h[2]),
+                   o3 = __bfloat1622float2(h[3]);
+      s += a.x * o0.x + a.y * o0.y + a.z * o1.x + a.w * o1.y + b.x * o2.x + b.y * o2.y + b.z * o3.x + b.w * o3.y;
+    }
   }
 #pragma unroll
   for (int w = L / 2; w; w >>= 1) s += __shfl_xor_sync(0xffffffffu, s, w);
@@ -627,21 +663,30 @@ void launch_loss_dlogits(const float* logits, const float* pmax, const double* p
                                                       dlogits);
 }
 void launch_rmsnorm_bwd(const float* dzw, const float* x, const __nv_bfloat16* g,
-                        const float* rstd, int T, int H, float* dx, float* dg, cudaStream_t st) {
+                        const float* rstd, int T, int H, float* dx, float* dg, cudaStream_t st,
+                        bool prescaled) {
+  const int pre = prescaled ? 1 : 0;
   if (T < 1) return;
   const int blocks = std::min((T + 7) / 8, 2 * num_sms());
   const size_t sm = sizeof(float) * H;
   switch ((H / 4 + 31) / 32) {  // float4 columns per lane
-    case 1: rmsnorm_bwd_reg_kernel<1><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
-    case 2: rmsnorm_bwd_reg_kernel<2><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
-    case 3: rmsnorm_bwd_reg_kernel<3><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
-    case 4: rmsnorm_bwd_reg_kernel<4><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
-    case 5: rmsnorm_bwd_reg_kernel<5><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
-    case 6: rmsnorm_bwd_reg_kernel<6><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
-    case 7: rmsnorm_bwd_reg_kernel<7><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
-    case 8: rmsnorm_bwd_reg_kernel<8><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg); return;
-    default: rmsnorm_bwd_kernel<<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg);
+    case 1: rmsnorm_bwd_reg_kernel<1><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
+    case 2: rmsnorm_bwd_reg_kernel<2><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
+    case 3: rmsnorm_bwd_reg_kernel<3><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
+    case 4: rmsnorm_bwd_reg_kernel<4><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
+    case 5: rmsnorm_bwd_reg_kernel<5><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
+    case 6: rmsnorm_bwd_reg_kernel<6><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
+    case 7: rmsnorm_bwd_reg_kernel<7><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
+    case 8: rmsnorm_bwd_reg_kernel<8><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
+    default: rmsnorm_bwd_kernel<<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre);
   }
+}
+void launch_split_bf16(const float* src, int rows, int cols, const float* row_scale,
+                       const __nv_bfloat16* col_gain, __nv_bfloat16* dst, cudaStream_t st) {
+  const size_t n4 = (size_t)rows * cols / 4;
+  if (n4 == 0) return;
+  split_bf16_kernel<<<(int)std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * 16), 256, 0, st>>>(
+      src, rows, cols, row_scale, col_gain, dst);
 }
 void launch_row_rstd(const float* x, int T, int H, float eps, float* rstd, cudaStream_t st) {
   if (T > 0) row_rstd_kernel<<<(T + 7) / 8, 256, 0, st>>>(x, T, H, eps, rstd);
@@ -655,20 +700,21 @@ void launch_attention_bwd(const __nv_bfloat16* q, const __nv_bfloat16* o, const 
                           const int32_t* row_slot, const int32_t* row_pos,
                           const int32_t* seq_start, const int32_t* seq_len,
                           const int32_t* block_table, int pages_per_seq, int T, int n_seq, int nq,
-                          int nkv, int hd, float* dqkv, cudaStream_t st) {
+                          int nkv, int hd, float* dqkv, cudaStream_t st, bool split) {
   float* D = nullptr;
   cudaMallocAsync(&D, sizeof(float) * (size_t)T * nq, st);
   const int w1 = T * nq;
+  const int o_lo = split ? nq * hd : 0;  // split: O rows are [hi | lo]
   if (hd == 64)
-    attn_bwd_dot_v_kernel<8><<<(w1 * 8 + 255) / 256, 256, 0, st>>>(d_o, o, w1, hd, D);
+    attn_bwd_dot_v_kernel<8><<<(w1 * 8 + 255) / 256, 256, 0, st>>>(d_o, o, w1, hd, D, nq, o_lo);
   else if (hd == 128)
-    attn_bwd_dot_v_kernel<16><<<(w1 * 16 + 255) / 256, 256, 0, st>>>(d_o, o, w1, hd, D);
+    attn_bwd_dot_v_kernel<16><<<(w1 * 16 + 255) / 256, 256, 0, st>>>(d_o, o, w1, hd, D, nq, o_lo);
   else
     attn_bwd_dot_kernel<<<(w1 * 32 + 255) / 256, 256, 0, st>>>(d_o, o, T, nq, hd, D);
   static const bool scalar = std::getenv("SRL_ATTN_BWD_SCALAR") != nullptr;  // A/B: the CUDA-core path
-  if (!scalar) {
+  if (!scalar || split) {
     launch_attention_bwd_mma(q, d_o, lse, D, kc, vc, seq_start, seq_len, block_table, pages_per_seq,
-                             n_seq, nq, nkv, hd, dqkv, st);
+                             n_seq, nq, nkv, hd, dqkv, st, split);
   } else {
     const float scale = 1.0f / sqrtf((float)hd);
     const int w2 = T * nkv;

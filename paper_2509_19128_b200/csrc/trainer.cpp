@@ -116,7 +116,11 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
   lay_ = weights_->layout;
   n_ = lay_.total;
   T_max_ = pad64(std::max(64, o.max_tokens));
-  chunk_ = std::min(kLogitChunkMax, T_max_);
+  chunk_ = std::min(o.logit_chunk > 0 ? pad64(o.logit_chunk) : kLogitChunkMax, T_max_);
+  precise_ = o.fast_bf16 == 0;
+  sp_ = precise_ ? 2 : 1;
+  if (precise_ && (d_.H % 64 || d_.I % 64 || d_.qdim() % 64 || d_.qkv() % 64 || d_.V % 64))
+    return fail(SRL_INVALID_ARGUMENT, "trainer: precise mode needs every width a multiple of 64");
   const int H = d_.H, L = d_.L, I = d_.I, qd = d_.qdim(), qkv = d_.qkv();
   // fp32 master weights, Adam moments, gradient
   if ((st = alloc(&master_, n_)) || (st = alloc(&grad_, n_)) || (st = alloc(&adam_m_, n_)) ||
@@ -128,23 +132,25 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
   acts_.resize(L);
   for (int l = 0; l < L; ++l) {
     LayerActs& a = acts_[l];
-    if ((st = alloc(&a.x_in, (size_t)T_max_ * H)) || (st = alloc(&a.xg1, (size_t)T_max_ * H)) ||
+    // split (precise) activations are [hi | lo] rows: sp_ x the width
+    if ((st = alloc(&a.x_in, (size_t)T_max_ * H)) || (st = alloc(&a.xg1, (size_t)T_max_ * H * sp_)) ||
         (st = alloc(&a.rstd1, T_max_)) || (st = alloc(&a.q, (size_t)T_max_ * qd)) ||
-        (st = alloc(&a.attn, (size_t)T_max_ * qd)) || (st = alloc(&a.lse, (size_t)T_max_ * d_.nq)) ||
-        (st = alloc(&a.x_mid, (size_t)T_max_ * H)) || (st = alloc(&a.xg2, (size_t)T_max_ * H)) ||
-        (st = alloc(&a.rstd2, T_max_)) || (st = alloc(&a.gu, (size_t)T_max_ * 2 * I)) ||
-        (st = alloc(&a.act, (size_t)T_max_ * I)))
+        (st = alloc(&a.attn, (size_t)T_max_ * qd * sp_)) || (st = alloc(&a.lse, (size_t)T_max_ * d_.nq)) ||
+        (st = alloc(&a.x_mid, (size_t)T_max_ * H)) || (st = alloc(&a.xg2, (size_t)T_max_ * H * sp_)) ||
+        (st = alloc(&a.rstd2, T_max_)) || (st = alloc(&a.act, (size_t)T_max_ * I * sp_)))
+      return st;
+    if (precise_ ? (st = alloc(&a.gu32, (size_t)T_max_ * 2 * I)) : (st = alloc(&a.gu, (size_t)T_max_ * 2 * I)))
       return st;
   }
-  if ((st = alloc(&x_, (size_t)T_max_ * H)) || (st = alloc(&xgF_, (size_t)T_max_ * H)) ||
+  if ((st = alloc(&x_, (size_t)T_max_ * H)) || (st = alloc(&xgF_, (size_t)T_max_ * H * sp_)) ||
       (st = alloc(&rstdF_, T_max_)) || (st = alloc(&ssq_, (size_t)T_max_ * d_.ssq_parts())) ||
       (st = alloc(&pmax_, (size_t)chunk_ * ((d_.V + 127) / 128))) ||
       (st = alloc(&psum_, (size_t)chunk_ * ((d_.V + 127) / 128))) ||
-      (st = alloc(&dlogits_, (size_t)chunk_ * d_.V)) || (st = alloc(&dx_, (size_t)T_max_ * H)) ||
+      (st = alloc(&dlogits_, (size_t)chunk_ * d_.V * sp_)) || (st = alloc(&dx_, (size_t)T_max_ * H)) ||
       (st = alloc(&dz_, (size_t)T_max_ * std::max(H, 2 * I))) ||
       (st = alloc(&dbig_, (size_t)T_max_ * std::max({2 * I, qkv, qd}))) ||
-      (st = alloc(&dbig_bf_, (size_t)T_max_ * std::max({2 * I, qkv, qd, H}))) ||
-      (st = alloc(&xn_, (size_t)T_max_ * H)) || (st = alloc(&dgu_, (size_t)T_max_ * 2 * I)) ||
+      (st = alloc(&dbig_bf_, (size_t)T_max_ * std::max({2 * I, qkv, qd, H}) * sp_)) ||
+      (st = alloc(&xn_, (size_t)T_max_ * H)) || (st = alloc(&dgu_, (size_t)T_max_ * 2 * I * sp_)) ||
       (st = alloc(&ones_, T_max_)) || (st = alloc(&row_slot_, T_max_)) ||
       (st = alloc(&row_pos_, T_max_)) || (st = alloc(&row_tok_, T_max_)) ||
       (st = alloc(&row_tgt_, T_max_)) || (st = alloc(&coef_, T_max_)) ||
@@ -159,9 +165,30 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
   return SRL_OK;
 }
 
-// C[m, n] (epilogue) = sum_k X[m, k] * W[n, k]; X, W bf16 K-major.
+void DecoderTrainer::apply_seg(EpiParams& e, const Seg* seg, int K) {
+  if (seg == nullptr || seg->n <= 1) return;
+  e.seg_kb = K / 64;
+  e.x_off0 = seg->x_off[0]; e.x_off1 = seg->x_off[1]; e.x_off2 = seg->x_off[2];
+  e.w_off0 = seg->w_off[0]; e.w_off1 = seg->w_off[1]; e.w_off2 = seg->w_off[2];
+}
+
+// C[m, n] (epilogue) = sum_k X[m, k] * W[n, k]; X, W bf16 K-major.  Precise
+// mode: X rows are [hi (K) | lo (K)] and the persistent kernel runs the two
+// K segments (hi W + lo W) into one accumulator.
 int DecoderTrainer::gemm(const __nv_bfloat16* X, int x_rows_alloc, int M, const __nv_bfloat16* W,
                          int N, int K, const EpiParams& e) {
+  if (precise_) {
+    const CUtensorMap tx = make_tmap_bf16(X, (uint64_t)std::max(x_rows_alloc, M), (uint64_t)(2 * K), 128);
+    const CUtensorMap tw = make_tmap_bf16(W, (uint64_t)N, (uint64_t)K, 128);
+    EpiParams es = e;
+    const Seg sg = seg_x(K);
+    apply_seg(es, &sg, K);
+    int tok = gemm_big_tok(M, N, 2 * K, sms_);
+    if (tok == 0) tok = 128;
+    const cudaError_t err = gemm_big_launch(tw, tx, M, N, 2 * K, tok, es, st_);
+    if (err != cudaSuccess) return cuda_fail(err, "trainer gemm (split)");
+    return SRL_OK;
+  }
   const int tok = gemm_tok_tile(M);
   const CUtensorMap tx = make_tmap_bf16(X, (uint64_t)std::max(x_rows_alloc, M), (uint64_t)K, (uint32_t)tok);
   const CUtensorMap tw = make_tmap_bf16(W, (uint64_t)N, (uint64_t)K, 128);
@@ -204,8 +231,28 @@ int DecoderTrainer::gemm_accum(const __nv_bfloat16* X, int M, const __nv_bfloat1
 // dgu = SwiGLU'(gu) applied to dact = dY W (W MN-major [k_rows x I]): fused
 // into the GEMM epilogue when the plan needs no K slices, else through dz_.
 int DecoderTrainer::gemm_swiglu_bwd(const __nv_bfloat16* dY, int M, const __nv_bfloat16* W, int I, int k_rows,
-                                    const __nv_bfloat16* gu, __nv_bfloat16* dgu) {
+                                    const __nv_bfloat16* gu, __nv_bfloat16* dgu, const LayerActs* a) {
   const int K = pad64(k_rows);
+  if (precise_) {
+    // dact = (dYh + dYl) W_down, SwiGLU backward on the fp32 gate | up with
+    // rstd2 folded in, dgu' written as [hi (2I) | lo (2I)] rows
+    const Seg sg = seg_x(k_rows);
+    const CUtensorMap tw = make_tmap_bf16(W, (uint64_t)k_rows, (uint64_t)I, 64);
+    const CUtensorMap tx = make_tmap_bf16(dY, (uint64_t)M, (uint64_t)(2 * k_rows), 128);
+    int splits = 1;
+    const int tok = gemm_mn_plan(M, I, 2 * K, sms_, &splits);
+    EpiParams e;
+    e.kind = EPI_SWIGLU_BWD;
+    e.gu_in_f32 = a->gu32;
+    e.row_scale = a->rstd2;
+    e.out_bf16 = dgu;
+    e.ld_bf16 = 4 * I;
+    e.lo_off = 2 * I;
+    apply_seg(e, &sg, K);
+    const cudaError_t err = gemm_mn_launch(tw, tx, M, I, 2 * K, tok, 1, false, e, st_);
+    if (err != cudaSuccess) return cuda_fail(err, "trainer gemm_swiglu_bwd (split)");
+    return SRL_OK;
+  }
   int splits = 1;
   const int tok = gemm_mn_plan(M, I, K, sms_, &splits);
   if (splits > 1) {
@@ -227,13 +274,18 @@ int DecoderTrainer::gemm_swiglu_bwd(const __nv_bfloat16* dY, int M, const __nv_b
 }
 
 int DecoderTrainer::gemm_mn(const __nv_bfloat16* X, bool x_kmajor, int M, const __nv_bfloat16* W, int N,
-                            int k_rows, float* out, bool accumulate) {
+                            int k_rows, float* out, bool accumulate, const Seg* seg) {
   const int K = pad64(k_rows);
-  const CUtensorMap tw = make_tmap_bf16(W, (uint64_t)k_rows, (uint64_t)N, 64);
-  const CUtensorMap tx = x_kmajor ? make_tmap_bf16(X, (uint64_t)M, (uint64_t)k_rows, 128)
-                                  : make_tmap_bf16(X, (uint64_t)k_rows, (uint64_t)M, 64);
+  const int nseg = seg ? seg->n : 1;
+  if (nseg > 1 && x_kmajor && k_rows % 64 != 0)
+    return fail(SRL_INVALID_ARGUMENT, "trainer gemm_mn: split K-major operand needs K % 64 == 0");
+  const uint64_t wc = seg && seg->w_cols ? seg->w_cols : N;
+  const uint64_t xc = seg && seg->x_cols ? seg->x_cols : (x_kmajor ? k_rows : M);
+  const CUtensorMap tw = make_tmap_bf16(W, (uint64_t)k_rows, wc, 64);
+  const CUtensorMap tx = x_kmajor ? make_tmap_bf16(X, (uint64_t)M, xc, 128)
+                                  : make_tmap_bf16(X, (uint64_t)k_rows, xc, 64);
   int splits = 1;
-  const int tok = gemm_mn_plan(M, N, K, sms_, &splits);
+  const int tok = gemm_mn_plan(M, N, K * nseg, sms_, &splits);
   if ((size_t)((N + 127) / 128) * ((M + tok - 1) / tok) > (size_t)kTileFlags) splits = 1;
   if (splits > 1 && !accumulate) {  // ordered K slices add into a zeroed output
     SRL_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)M * N, st_));
@@ -244,7 +296,8 @@ int DecoderTrainer::gemm_mn(const __nv_bfloat16* X, bool x_kmajor, int M, const 
   e.out_f32 = out;
   e.ld_out = N;
   e.tile_flags = tile_flags_;
-  const cudaError_t err = gemm_mn_launch(tw, tx, M, N, K, tok, splits, !x_kmajor, e, st_);
+  apply_seg(e, seg, K);
+  const cudaError_t err = gemm_mn_launch(tw, tx, M, N, K * nseg, tok, splits, !x_kmajor, e, st_);
   if (err != cudaSuccess) return cuda_fail(err, "trainer gemm_mn");
   return SRL_OK;
 }
@@ -293,7 +346,13 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
   cudaEventRecord(e0, st);
 
   // ---- forward with saved activations
-  launch_embed(w + lay_.embed, w + lay_.layers[0].ln1, row_tok_, T, H, V, x_, acts_[0].xg1, ssq_, st);
+  const bool P = precise_;
+  if (P) {  // xg1 of layer 0 as the split pair of x * ln1 (the embed kernel's bf16 xg is scratch)
+    launch_embed(w + lay_.embed, w + lay_.layers[0].ln1, row_tok_, T, H, V, x_, xn_, ssq_, st);
+    launch_split_bf16(x_, T, H, nullptr, w + lay_.layers[0].ln1, acts_[0].xg1, st);
+  } else {
+    launch_embed(w + lay_.embed, w + lay_.layers[0].ln1, row_tok_, T, H, V, x_, acts_[0].xg1, ssq_, st);
+  }
   for (int l = 0; l < L; ++l) {
     LayerActs& a = acts_[l];
     const LayerOffsets& o = lay_.layers[l];
@@ -310,9 +369,9 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
     e.q_out = a.q; e.kc = kcl; e.vc = vcl;
     if ((s = gemm(a.xg1, T_max_, T, w + o.qkv_w, qkv, H, e))) return s;
     static const bool scalar_fwd = std::getenv("SRL_ATTN_FWD_SCALAR") != nullptr;  // A/B switch
-    if (!scalar_fwd) {
+    if (!scalar_fwd || P) {
       SRL_CUDA(launch_attention_fwd_mma(a.q, kcl, vcl, d_sstart, d_slen, d_bt, pps, n_seq, d_.nq, d_.nkv,
-                                        d_.hd, a.attn, a.lse, st));
+                                        d_.hd, a.attn, a.lse, st, nullptr, nullptr, 0, P ? qd : 0));
     } else {
     RoundPlan plan{row_slot_, row_pos_, row_tok_, nullptr};
     float* attn_ws = nullptr;
@@ -330,16 +389,18 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
     }
     EpiParams r;
     r.kind = EPI_RESID; r.resid = x_; r.gain = w + o.ln2; r.xg = a.xg2; r.ssq_out = ssq_;
+    r.lo_off = P ? H : 0;
     if ((s = gemm(a.attn, T_max_, T, w + o.o_w, H, qd, r))) return s;
     SRL_CUDA(cudaMemcpyAsync(a.x_mid, x_, sizeof(float) * T * H, cudaMemcpyDeviceToDevice, st));
     launch_row_rstd(a.x_mid, T, H, d_.eps, a.rstd2, st);
     EpiParams g;  // SwiGLU fused: act for the down GEMM, gate | up kept (bf16) for the backward
     g.kind = EPI_SWIGLU;
     g.ssq_in = ssq_; g.ssq_in_parts = parts; g.inv_dim = inv_h; g.eps = d_.eps;
-    g.out_bf16 = a.act; g.ld_bf16 = I; g.out2_bf16 = a.gu;
+    g.out_bf16 = a.act; g.ld_bf16 = I * sp_; g.lo_off = P ? I : 0;
+    g.out2_bf16 = a.gu; g.out2_f32 = a.gu32;
     if ((s = gemm(a.xg2, T_max_, T, w + o.gate_up_w, 2 * I, H, g))) return s;
     EpiParams r2;
-    r2.kind = EPI_RESID; r2.resid = x_; r2.ssq_out = ssq_;
+    r2.kind = EPI_RESID; r2.resid = x_; r2.ssq_out = ssq_; r2.lo_off = P ? H : 0;
     r2.xg = l + 1 < L ? acts_[l + 1].xg1 : xgF_;
     r2.gain = w + (l + 1 < L ? lay_.layers[l + 1].ln1 : lay_.final_norm);
     if ((s = gemm(a.act, T_max_, T, w + o.down_w, H, I, r2))) return s;
@@ -360,7 +421,7 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
     // statistics and the target's logit only: the [C x V] logits are never stored
     e.out_f32 = nullptr; e.part_max = pmax_; e.part_sum = psum_;
     e.tgt_row = row_tgt_ + c0; e.tgt_out = tgt_logit_ + c0;
-    if ((s = gemm(xgF_ + (size_t)c0 * H, C, C, w + lay_.lm_head, V, H, e))) return s;
+    if ((s = gemm(xgF_ + (size_t)c0 * H * sp_, C, C, w + lay_.lm_head, V, H, e))) return s;
     launch_lse_logprob(pmax_, psum_, V, C, tgt_logit_ + c0, lse_ + c0, lp_ + c0, st);
   }
   cudaEventRecord(e1, st);
@@ -419,8 +480,22 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
     e.kind = EPI_DLOGITS;
     e.ssq_in = ssq_ + (size_t)c0 * parts; e.ssq_in_parts = parts; e.inv_dim = inv_h; e.eps = d_.eps;
     e.lse_in = lse_ + c0; e.row_coef = coef_ + c0; e.tgt_row = row_tgt_ + c0;
-    e.out_bf16 = dlogits_; e.ld_bf16 = V;
-    if ((s = gemm(xgF_ + (size_t)c0 * H, C, C, w + lay_.lm_head, V, H, e))) return s;
+    e.out_bf16 = dlogits_; e.ld_bf16 = V * sp_;
+    if (P) {  // dlogits' = rstd * dlogits as [hi | lo] rows
+      e.fold_rstd = 1;
+      e.lo_off = V;
+    }
+    if ((s = gemm(xgF_ + (size_t)c0 * H * sp_, C, C, w + lay_.lm_head, V, H, e))) return s;
+    if (P) {
+      const Seg sx = seg_x(V), sxw = seg_xw(V, H);
+      // dzw'[t, h] = sum_v dlogits'[t, v] E[v, h]  (rstd already in)
+      if ((s = gemm_mn(dlogits_, true, C, w + lay_.lm_head, H, V, dz_, false, &sx))) return s;
+      launch_rmsnorm_bwd(dz_, x_ + (size_t)c0 * H, w + lay_.final_norm, rstdF_ + c0, C, H,
+                         dx_ + (size_t)c0 * H, grad_ + lay_.final_norm, st, true);
+      // dE[v, h] += sum_t dlogits'[t, v] * u[t, h], u = x * final_norm (split)
+      if ((s = gemm_mn(dlogits_, false, V, xgF_ + (size_t)c0 * H * 2, H, C, g_lm, true, &sxw))) return s;
+      continue;
+    }
     // dzw[t, h] = sum_v dlogits[t, v] E[v, h]
     if ((s = gemm_mn(dlogits_, true, C, w + lay_.lm_head, H, V, dz_, false))) return s;
     launch_rmsnorm_bwd(dz_, x_ + (size_t)c0 * H, w + lay_.final_norm, rstdF_ + c0, C, H,
@@ -430,7 +505,37 @@ int DecoderTrainer::step(const TrainBatch& b, srl_trainer_stats* stats) {
     if ((s = gemm_mn(dlogits_, false, V, xn_, H, C, g_lm, true))) return s;
   }
   // layers in reverse; dx_ holds dJ/dx_out of the layer being processed
-  for (int l = L - 1; l >= 0; --l) {
+  for (int l = L - 1; l >= 0 && P; --l) {
+    // precise mode: every GEMM operand that is not a weight is a [hi | lo] pair;
+    // rstd is folded into the dY of the normalised GEMMs (QKV, gate/up), whose
+    // weight gradients then read the split u = x * gain directly
+    LayerActs& a = acts_[l];
+    const LayerOffsets& o = lay_.layers[l];
+    const Seg sH = seg_x(H), s2I = seg_x(2 * I), sQKV = seg_x(qkv);
+    const Seg dWd = seg_xw(H, I), dWgu = seg_xw(2 * I, H), dWo = seg_xw(H, qd), dWqkv = seg_xw(qkv, H);
+    // down: x_out = x_mid + act W_down^T
+    launch_split_bf16(dx_, T, H, nullptr, nullptr, dbig_bf_, st);                 // dY [T x 2H]
+    if ((s = gemm_mn(dbig_bf_, false, H, a.act, I, T, grad_ + o.down_w, true, &dWd))) return s;
+    if ((s = gemm_swiglu_bwd(dbig_bf_, T, w + o.down_w, I, H, nullptr, dgu_, &a))) return s;  // dgu' [T x 4I]
+    // gate_up: gu = rstd2 * (u2 W_gu^T), rstd2 folded into dgu'
+    if ((s = gemm_mn(dgu_, true, T, w + o.gate_up_w, H, 2 * I, dz_, false, &s2I))) return s;
+    if ((s = gemm_mn(dgu_, false, 2 * I, a.xg2, H, T, grad_ + o.gate_up_w, true, &dWgu))) return s;
+    launch_rmsnorm_bwd(dz_, a.x_mid, w + o.ln2, a.rstd2, T, H, dx_, grad_ + o.ln2, st, true);
+    // O: x_mid = x_in + attn W_o^T
+    launch_split_bf16(dx_, T, H, nullptr, nullptr, dbig_bf_, st);
+    if ((s = gemm_mn(dbig_bf_, true, T, w + o.o_w, qd, H, dz_, false, &sH))) return s;          // dO [T x qd]
+    if ((s = gemm_mn(dbig_bf_, false, H, a.attn, qd, T, grad_ + o.o_w, true, &dWo))) return s;
+    launch_attention_bwd(a.q, a.attn, dz_, a.lse, kc_ + kv_elems * l, vc_ + kv_elems * l, row_slot_,
+                         row_pos_, d_sstart, d_slen, d_bt, pps, T, n_seq, d_.nq, d_.nkv, d_.hd, dbig_, st,
+                         true);
+    launch_rope_bwd(dbig_, row_pos_, cos_sin_, T, d_.nq, d_.nkv, d_.hd, st);
+    launch_colsum_accum(dbig_, T, qkv, grad_ + o.qkv_b, st);
+    launch_split_bf16(dbig_, T, qkv, a.rstd1, nullptr, dbig_bf_, st);            // dqkv' = rstd1 dqkv
+    if ((s = gemm_mn(dbig_bf_, true, T, w + o.qkv_w, H, qkv, dz_, false, &sQKV))) return s;
+    if ((s = gemm_mn(dbig_bf_, false, qkv, a.xg1, H, T, grad_ + o.qkv_w, true, &dWqkv))) return s;
+    launch_rmsnorm_bwd(dz_, a.x_in, w + o.ln1, a.rstd1, T, H, dx_, grad_ + o.ln1, st, true);
+  }
+  for (int l = L - 1; l >= 0 && !P; --l) {
     LayerActs& a = acts_[l];
     const LayerOffsets& o = lay_.layers[l];
     // down: x_out = x_mid + act W_down^T

@@ -39,7 +39,29 @@ class DecoderTrainer {
     float *x_in = nullptr, *rstd1 = nullptr, *lse = nullptr, *x_mid = nullptr, *rstd2 = nullptr;
     __nv_bfloat16 *xg1 = nullptr, *q = nullptr, *attn = nullptr, *xg2 = nullptr, *act = nullptr,
                   *gu = nullptr;  // rstd-scaled gate | up pre-activations (bf16, 64-row interleave)
+    float* gu32 = nullptr;        // the same in fp32 (precise mode)
   };
+  // Split operands of the precise mode (EpiParams::seg_kb): up to 3 segments
+  // of the K concatenation with per-segment X / W offsets, and the column
+  // counts of the X / W buffers (0: the logical width).
+  struct Seg {
+    int n = 1;
+    int x_off[3] = {0, 0, 0}, w_off[3] = {0, 0, 0};
+    int x_cols = 0, w_cols = 0;
+  };
+  // (hi + lo) . W: X rows [hi (w) | lo (w)], W exact
+  static Seg seg_x(int w) {
+    Seg s;
+    s.n = 2; s.x_off[1] = w; s.x_cols = 2 * w;
+    return s;
+  }
+  // (dh + dl)^T (uh + ul) ~ dh uh + dh ul + dl uh: X rows [dh | dl] (width xw),
+  // W rows [uh | ul] (width ww), both MN-major
+  static Seg seg_xw(int xw, int ww) {
+    Seg s;
+    s.n = 3; s.x_off[2] = xw; s.w_off[1] = ww; s.x_cols = 2 * xw; s.w_cols = 2 * ww;
+    return s;
+  }
   template <typename T>
   int alloc(T** p, size_t n);
   int gemm(const __nv_bfloat16* X, int x_rows_alloc, int M, const __nv_bfloat16* W, int N, int K,
@@ -47,9 +69,10 @@ class DecoderTrainer {
   int gemm_store(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, float* out);
   int gemm_accum(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, float* out);
   int gemm_mn(const __nv_bfloat16* X, bool x_kmajor, int M, const __nv_bfloat16* W, int N, int k_rows,
-              float* out, bool accumulate);
+              float* out, bool accumulate, const Seg* seg = nullptr);
   int gemm_swiglu_bwd(const __nv_bfloat16* dY, int M, const __nv_bfloat16* W, int I, int k_rows,
-                      const __nv_bfloat16* gu, __nv_bfloat16* dgu);
+                      const __nv_bfloat16* gu, __nv_bfloat16* dgu, const LayerActs* a = nullptr);
+  static void apply_seg(EpiParams& e, const Seg* seg, int K);
 
   srl_trainer_options opts_{};
   DecoderDims d_{};
@@ -57,6 +80,8 @@ class DecoderTrainer {
   std::shared_ptr<DecoderWeights> weights_;
   size_t n_ = 0;
   int dev_ = 0, T_max_ = 64, sms_ = 148, adam_t_ = 0;
+  bool precise_ = true;  // split (hi + lo) activations and backward operands
+  int sp_ = 2;           // 2 when precise (split buffers are twice as wide), else 1
   cudaStream_t st_ = nullptr;
   std::vector<void*> allocs_;
   float *master_ = nullptr, *grad_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr;

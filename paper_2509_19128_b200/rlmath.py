@@ -115,6 +115,67 @@ def fit_baseline(trajectories) -> BaselineTable:
     return BaselineTable({k: s / n for k, (s, n) in cells.items()})
 
 
+@dataclass
+class GradientTable:
+    """GradientTable (rl_math.hpp:39-46): rows keyed by (prompt_id, context
+    tuple); contributions through the fallback row land in default_row."""
+
+    rows: dict = field(default_factory=dict)
+    default_row: np.ndarray | None = None
+
+    def max_abs(self) -> float:
+        m = 0.0
+        for r in self.rows.values():
+            m = max(m, float(np.abs(r).max(initial=0.0)))
+        if self.default_row is not None:
+            m = max(m, float(np.abs(self.default_row).max(initial=0.0)))
+        return m
+
+
+def _tabular_gradient(policy, trajectories, baseline, clamp, use_is, granularity):
+    from .policy import TabularPolicy
+
+    if not isinstance(policy, TabularPolicy):
+        raise TypeError("is_reinforce_gradient needs a TabularPolicy")
+    if not trajectories:
+        raise ValueError("reinforce_gradient: no trajectories")
+    for t in trajectories:
+        t.validate()
+    toks = np.concatenate([np.asarray(t.tokens, dtype=np.int32) for t in trajectories])
+    offs = np.concatenate([[0], np.cumsum([t.length() for t in trajectories])]).astype(np.int64)
+    mu = np.concatenate([np.asarray(t.behavior_logprobs, dtype=np.float64) for t in trajectories])
+    rew = np.array([t.reward for t in trajectories], dtype=np.float64)
+    base = np.array([baseline.at(t.prompt_id, p) for t in trajectories for p in range(t.length())],
+                    dtype=np.float64)  # BaselineTable::at throws on a missing cell
+    ids = (C.c_char_p * len(trajectories))(*[t.prompt_id.encode() for t in trajectories])
+    keys = sorted(k for k, _ in policy.rows())  # std::map<ContextKey> order
+    V = policy.vocab_size
+    grad = np.zeros((len(keys) + 1, V))
+    touched = np.zeros(len(keys) + 1, dtype=np.int32)
+    with NativePolicy(policy) as h:
+        st = _lib.lib().srl_tabular_is_reinforce_gradient(
+            h, len(trajectories), ids, toks.ctypes.data, offs.ctypes.data, mu.ctypes.data,
+            rew.ctypes.data, base.ctypes.data, 1 if use_is else 0, float(clamp),
+            1 if granularity in (1, "per_token") else 0, grad.ctypes.data, touched.ctypes.data)
+    _check(st, "is_reinforce_gradient")
+    out = GradientTable({k: grad[i] for i, k in enumerate(keys) if touched[i]},
+                        grad[-1] if touched[-1] else None)
+    return out
+
+
+def reinforce_gradient(policy, trajectories, baseline) -> GradientTable:
+    """reinforce_gradient (rl_math.cpp:264-269) for a TabularPolicy, on the device."""
+    return _tabular_gradient(policy, trajectories, baseline, 1.0, False, 0)
+
+
+def is_reinforce_gradient(policy, trajectories, baseline, clamp: float,
+                          granularity="sequence") -> GradientTable:
+    """is_reinforce_gradient (rl_math.cpp:271-276) for a TabularPolicy, on the
+    device: (1/m) w (R - b_t) (onehot(y_t) - softmax(row)), stop-gradient on
+    the truncated IS weight w (per sequence by default, or per token)."""
+    return _tabular_gradient(policy, trajectories, baseline, clamp, True, granularity)
+
+
 def pipeline_max_lag_steps(gen_batch: int, inference_count: int, max_len: float, mean_len: float,
                            train_batch: int) -> int:
     """g_max = ceil(H * I * L / (mean L * B)) (throughput.cpp:260-269): the

@@ -34,12 +34,18 @@ class TrainStep:
 
 
 class Trainer:
-    def __init__(self, policy: DecoderPolicy, max_tokens: int = 4096, device: int | None = None):
+    def __init__(self, policy: DecoderPolicy, max_tokens: int = 4096, device: int | None = None,
+                 precise: bool = True, logit_chunk: int = 0):
+        """precise (default): activations and backward operands as bf16 hi + lo
+        pairs -- the 1e-3 parity mode; precise=False: single bf16 operands
+        (faster, ~1e-2 gradient agreement).  logit_chunk: LM-head rows per pass
+        (0 = 16384)."""
         if not isinstance(policy, DecoderPolicy):
             raise TypeError("Trainer needs a DecoderPolicy")
         self.config = policy.config
         self.device = policy.device if device is None else device
-        opts = _lib.TrainerOptionsC(max_tokens, self.device)
+        self.precise = precise
+        opts = _lib.TrainerOptionsC(max_tokens, self.device, 0 if precise else 1, logit_chunk)
         h = C.c_void_p()
         _lib.call("srl_trainer_create", policy.handle, C.byref(opts), C.byref(h))
         self._h = h

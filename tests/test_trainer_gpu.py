@@ -2,10 +2,15 @@
 torch_decoder_ref.py) of the same decoder and of the IS-REINFORCE objective
 of rl_math.cpp:211-276.
 
-Tolerances: log-probs and the objective within 1e-3 relative; the gradient
-within 2e-2 relative L2 error and cosine > 0.9995 per tensor group -- the
-device backward runs its GEMMs on bf16 operands (dY, activations), which
-bounds the agreement with an fp64 reference at the bf16 resolution (2^-8)."""
+Precise mode (the default): every activation and backward operand is a
+bf16 hi + lo pair (fp32-class); only q / k / v are bf16, as in the reference
+restatement (rounding="kv").  Bars: log-probs, the objective J and the
+gradient (relative L2 and per tensor) within 1e-3 relative -- north_star's
+bar.  tools/grad_precision_study.py shows why single bf16 operands cannot
+meet it: each of the six backward rounding points alone costs ~1e-3.
+
+Fast mode (precise=False, single bf16 operands): log-probs 1e-3, J 3e-3,
+gradient 2e-2 relative L2 / cosine > 0.9995 per tensor group."""
 import numpy as np
 import pytest
 import torch
@@ -37,14 +42,46 @@ def make_trajs(rng, V, n, lens, prompts):
 TINY128 = DecoderConfig("tiny-hd128", 256, 256, 2, 6, 2, 128, 512, False, 0, 4096, 10000.0, 1e-6)
 
 
-@pytest.mark.parametrize("cfg,granularity", [(TINY, "sequence"), (TINY, "per_token"),
-                                             (TINY128, "sequence")])
-def test_trainer_gradient_matches_torch_fp64(cuda, cfg, granularity):
+def check_precise(res, g_dev, lps, J, g_ref, off, bar=1e-3):
+    for got, exp in zip(res.logprobs, lps):
+        np.testing.assert_allclose(got[1:], exp, rtol=bar, atol=1e-5)
+    assert abs(res.objective - J) <= bar * max(1e-3, abs(J)), (res.objective, J)
+    rel = np.linalg.norm(g_dev - g_ref) / np.linalg.norm(g_ref)
+    assert rel < bar, rel
+    for name, (o, n) in off.items():
+        a, b = g_dev[o:o + n], g_ref[o:o + n]
+        nb = np.linalg.norm(b)
+        if nb > 1e-6 * np.linalg.norm(g_ref):
+            assert np.linalg.norm(a - b) / nb < 10 * bar, (name, np.linalg.norm(a - b) / nb)
+    return rel
+
+
+@pytest.mark.parametrize("cfg,granularity,chunk", [(TINY, "sequence", 0), (TINY, "per_token", 0),
+                                                   (TINY128, "sequence", 0), (TINY, "sequence", 64),
+                                                   (TINY128, "per_token", 64)])
+def test_trainer_precise_gradient_within_1e3(cuda, cfg, granularity, chunk):
+    """chunk = 64: the LM head runs in 64-row passes (three chunk boundaries in
+    the 131-row batch), the path the bench's 20480-row step takes at 16384."""
     pol = DecoderPolicy.random(cfg, seed=11, scale=0.03)
     w16 = pol.torch_weights().cpu().view(torch.int16).numpy().view(np.uint16)
     rng = np.random.default_rng(5)
     trajs = make_trajs(rng, cfg.vocab_size, 4, [12, 33, 20, 70], [3, 5, 1, 9])
-    tr = Trainer(pol, max_tokens=256)
+    tr = Trainer(pol, max_tokens=256, logit_chunk=chunk)
+    res = tr.step(trajs, clamp=5.0, granularity=granularity)
+    g_dev = tr.gradient().cpu().numpy().astype(np.float64)
+    ref = TorchDecoder(cfg.to_dict(), w16, rounding="kv")
+    J, lps = ref.is_reinforce(trajs, len(trajs), 5.0, granularity)
+    check_precise(res, g_dev, lps, J, ref.flat_grad(), ref.off)
+
+
+@pytest.mark.parametrize("cfg,granularity", [(TINY, "sequence"), (TINY, "per_token"),
+                                             (TINY128, "sequence")])
+def test_trainer_fast_bf16_gradient_matches_torch_fp64(cuda, cfg, granularity):
+    pol = DecoderPolicy.random(cfg, seed=11, scale=0.03)
+    w16 = pol.torch_weights().cpu().view(torch.int16).numpy().view(np.uint16)
+    rng = np.random.default_rng(5)
+    trajs = make_trajs(rng, cfg.vocab_size, 4, [12, 33, 20, 70], [3, 5, 1, 9])
+    tr = Trainer(pol, max_tokens=256, precise=False)
     res = tr.step(trajs, clamp=5.0, granularity=granularity)
     g_dev = tr.gradient().cpu().numpy().astype(np.float64)
 
@@ -87,8 +124,8 @@ def test_trainer_on_policy_weights_are_one_and_clamp(cuda):
     cl = tr.step(trajs, clamp=5.0)
     assert cl.clamped == 3
     g5 = tr.gradient().cpu().numpy()
-    # exactly 5x up to the bf16 rounding of dlogits (coef * (onehot - p) is stored in bf16)
-    assert np.linalg.norm(g5 - 5.0 * g1) / np.linalg.norm(5.0 * g1) < 1e-2
+    # exactly 5x up to the rounding of the split dlogits (test_rl_math.cpp:273-287)
+    assert np.linalg.norm(g5 - 5.0 * g1) / np.linalg.norm(5.0 * g1) < 1e-4
 
 
 def test_trainer_adam_moves_weights_and_feeds_the_engine(cuda):
@@ -132,24 +169,24 @@ def test_trainer_data_parallel_shards_sum_to_full_batch(cuda):
     for r in range(2):
         tr.step_data_parallel(trajs, r, 2)  # no process group: the all-reduce is the identity
         parts.append(tr.gradient().cpu().numpy().astype(np.float64).copy())
-    # The full batch (92 rows) and the shards take different GEMM kernels (the
-    # persistent one from 65 rows on, the split-K one below): fp32 summation
-    # order differs, bf16-rounded activations flip by an ulp here and there,
-    # measured 6e-4.  A wrong normalisation (local instead of global m) is
-    # off by O(1).
+    # fp32 summation order differs between the full batch and the shards
+    # (tile shapes, split factors); the precise trainer's operands carry no
+    # bf16 rounding flips, so the sum agrees to fp32 accumulation noise.  A
+    # wrong normalisation (local instead of global m) is off by O(1).
     rel = np.linalg.norm(parts[0] + parts[1] - full) / np.linalg.norm(full)
-    assert rel < 5e-3, rel
+    assert rel < 1e-4, rel
 
 
-def test_trainer_qwen05b_large_batch_paths(cuda):
+@pytest.mark.parametrize("precise", [True, False])
+def test_trainer_qwen05b_large_batch_paths(cuda, precise):
     """Qwen2.5-0.5B shape (V = 151936) with 192 rows: the LM head runs on the
     persistent GEMM's direct epilogues (statistics-only pass 1, dlogits pass 2),
     which the tiny shapes never reach.  Log-probs vs the fp64 oracle (1e-3
     relative); the gradient vs the float64 autograd restatement (run on the
-    GPU in fp64) and vs the sum of per-sequence steps (64 rows each: the
-    split-K GEMM's staged epilogues), at the tiny test's bars: measured 0.93%
-    relative L2 / cosine 0.99996 for both paths -- the bf16 backward operands
-    through 24 layers."""
+    GPU in fp64) and vs the sum of per-sequence steps.  Precise mode: 1e-3
+    (rounding="kv" reference).  Fast mode: the fast bars (measured 0.93%
+    relative L2 / cosine 0.99996 -- the bf16 backward operands through 24
+    layers)."""
     from oracle.decoder_oracle import DecoderOracle
 
     from paper_2509_19128_b200.policy import QWEN25_05B
@@ -163,15 +200,16 @@ def test_trainer_qwen05b_large_batch_paths(cuda):
         # c exactly, so the gradient comparisons see the GEMM / attention paths
         # and not exp(lp - mu) amplifying bf16-level log-prob differences
         t["behavior_logprobs"] = [-100.0] * len(t["tokens"])
-    tr = Trainer(pol, max_tokens=256)
+    tr = Trainer(pol, max_tokens=256, precise=precise)
     res = tr.step(trajs, granularity="per_token")
     full = tr.gradient().cpu().numpy().astype(np.float64).copy()
     w16 = pol.torch_weights().cpu().view(torch.int16).numpy().view(np.uint16)
-    orc = DecoderOracle(QWEN25_05B.to_dict(), w16, np.float64)
-    for t, got in zip(trajs, res.logprobs):
-        exp = np.asarray(orc.sequence_logprobs(t["tokens"][1:]))  # the oracle prepends bos itself
-        err = np.abs(np.asarray(got[1:]) - exp)
-        assert np.all(err <= np.maximum(2e-3, 1e-3 * np.abs(exp))), err.max()
+    if not precise:
+        orc = DecoderOracle(QWEN25_05B.to_dict(), w16, np.float64)
+        for t, got in zip(trajs, res.logprobs):
+            exp = np.asarray(orc.sequence_logprobs(t["tokens"][1:]))  # the oracle prepends bos itself
+            err = np.abs(np.asarray(got[1:]) - exp)
+            assert np.all(err <= np.maximum(2e-3, 1e-3 * np.abs(exp))), err.max()
     parts = np.zeros_like(full)
     for t in trajs:
         tr.step([t], n_trajectories=len(trajs), granularity="per_token")
@@ -179,13 +217,49 @@ def test_trainer_qwen05b_large_batch_paths(cuda):
     prev = torch.get_default_device()
     torch.set_default_device(cuda)
     try:
-        ref = TorchDecoder(QWEN25_05B.to_dict(), w16)
-        ref.is_reinforce(trajs, len(trajs), 5.0, "per_token")
+        ref = TorchDecoder(QWEN25_05B.to_dict(), w16, rounding="kv" if precise else "device")
+        J, lps = ref.is_reinforce(trajs, len(trajs), 5.0, "per_token")
         g_ref = ref.flat_grad()
     finally:
         torch.set_default_device(prev)
     n = np.linalg.norm(g_ref)
+    if precise:
+        check_precise(res, full, lps, J, g_ref, ref.off)
+        assert np.linalg.norm(parts - g_ref) / n < 1e-3
+        assert np.linalg.norm(full - parts) / np.linalg.norm(parts) < 1e-4
+        return
     for g in (full, parts):
         assert np.linalg.norm(g - g_ref) / n < 2e-2
         assert g @ g_ref / (np.linalg.norm(g) * n) > 0.9995
     assert np.linalg.norm(full - parts) / np.linalg.norm(parts) < 2e-2
+
+
+def test_trainer_bench_shape_two_chunks_is_linear(cuda):
+    """The bench's trainer step (0.5B, 64 trajectories x 320 rows = 20480
+    rows: two 10240-row LM-head passes) against the same trajectories in four
+    16-trajectory steps (5120 rows, one pass each) normalised by the global m:
+    the gradient is linear in the trajectories, so the sum of the shards must
+    equal the full step -- a size-independent check of the chunk-boundary
+    path at the full shape (precise mode: 1e-4), and every log-prob of the
+    full step must equal the shards' (same weights, same rows)."""
+    from paper_2509_19128_b200.policy import QWEN25_05B
+
+    pol = DecoderPolicy.random(QWEN25_05B, seed=16, scale=0.02)
+    rng = np.random.default_rng(11)
+    n, L = 64, 321
+    trajs = make_trajs(rng, QWEN25_05B.vocab_size, n, [L] * n, [65] * n)
+    for t in trajs:
+        t["tokens"][0] = QWEN25_05B.bos_token
+        t["behavior_logprobs"] = [-100.0] * L
+    tr = Trainer(pol, max_tokens=n * (L - 1))
+    full_res = tr.step(trajs)
+    full = tr.gradient().cpu().numpy().astype(np.float64).copy()
+    parts = np.zeros_like(full)
+    part_lps = []
+    for k in range(4):
+        r = tr.step(trajs[16 * k:16 * (k + 1)], n_trajectories=n)
+        part_lps += r.logprobs
+        parts += tr.gradient().cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(full - parts) / np.linalg.norm(parts) < 1e-4
+    for a, b in zip(full_res.logprobs, part_lps):
+        np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6)

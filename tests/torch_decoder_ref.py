@@ -18,11 +18,17 @@ def bf16_st(x):
 
 
 class TorchDecoder:
-    def __init__(self, cfg: dict, flat_u16: np.ndarray, exact: bool = False):
+    def __init__(self, cfg: dict, flat_u16: np.ndarray, exact: bool = False, rounding: str = "device"):
         """exact=True: no bf16 rounding points, fp64 RoPE tables and scale
-        (pinned against transformers' Qwen2 in tests/test_decoder_oracle.py)."""
+        (pinned against transformers' Qwen2 in tests/test_decoder_oracle.py).
+        rounding (exact=False): "device" = every bf16 rounding point of the
+        generator / fast trainer (normalised inputs, q/k/v, attention output,
+        SwiGLU output); "kv" = the precise trainer's, which carries every
+        activation as a bf16 hi + lo pair and rounds only q, k, v (the paged
+        K/V cache and the query operand are bf16)."""
         self.cfg = cfg
         self.exact = exact
+        self.rounding = rounding
         self.off, self.total = layout(cfg)
         H, I = cfg["hidden"], cfg["intermediate"]
         nq, nkv, hd = cfg["q_heads"], cfg["kv_heads"], cfg["head_dim"]
@@ -66,7 +72,8 @@ class TorchDecoder:
         else:
             cos = ang.cos().to(torch.float32).to(torch.float64)
             sin = ang.sin().to(torch.float32).to(torch.float64)
-        bf16 = (lambda z: z) if self.exact else bf16_st
+        bf16 = (lambda z: z) if (self.exact or self.rounding == "kv") else bf16_st
+        bf16_qkv = (lambda z: z) if self.exact else bf16_st
 
         def rope(z):  # [T, heads, hd]
             z1, z2 = z[..., :half], z[..., half:]
@@ -81,9 +88,9 @@ class TorchDecoder:
         for l in range(c["layers"]):
             u = bf16(x * p[f"{l}.ln1"])
             qkv = rstd(x)[:, None] * (u @ p[f"{l}.qkv_w"].T) + p[f"{l}.qkv_b"]
-            q = bf16(rope(qkv[:, :nq * hd].reshape(T, nq, hd)))
-            k = bf16(rope(qkv[:, nq * hd:(nq + nkv) * hd].reshape(T, nkv, hd)))
-            v = bf16(qkv[:, (nq + nkv) * hd:].reshape(T, nkv, hd))
+            q = bf16_qkv(rope(qkv[:, :nq * hd].reshape(T, nq, hd)))
+            k = bf16_qkv(rope(qkv[:, nq * hd:(nq + nkv) * hd].reshape(T, nkv, hd)))
+            v = bf16_qkv(qkv[:, (nq + nkv) * hd:].reshape(T, nkv, hd))
             k = k.repeat_interleave(G, dim=1)
             v = v.repeat_interleave(G, dim=1)
             s = torch.einsum("thd,shd->hts", q * scale, k)
