@@ -86,6 +86,14 @@ def parse(argv=None):
     return ap.parse_args(argv)
 
 
+_T0 = time.perf_counter()
+
+
+def log(msg):
+    """Phase progress on stderr (the JSON line stays alone on stdout)."""
+    print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -217,7 +225,7 @@ def steady_contexts(B, prompt, gen):
 
 
 # ---------------------------------------------------------- trainer side ---
-def trainer_measure(cfg, pol, n_seq, prompt, gen, steps=3):
+def trainer_measure(cfg, pol, n_seq, prompt, gen, steps=3, precise=True):
     """Trainer side: one optimizer step = current-policy
     log-prob recompute + truncated-IS REINFORCE objective + full backward +
     Adam over n_seq trajectories of prompt + gen tokens.  Device time from the
@@ -237,7 +245,7 @@ def trainer_measure(cfg, pol, n_seq, prompt, gen, steps=3):
         a = float(rng.standard_normal())
         trajs.append(dict(tokens=toks, loss_begin=prompt + 1, behavior_logprobs=mu,
                           advantages=[a] * seq))
-    tr = Trainer(pol.clone(), max_tokens=n_seq * seq)
+    tr = Trainer(pol.clone(), max_tokens=n_seq * seq, precise=precise)
     tr.step(trajs)  # warm-up (allocations, first launches)
     tr.apply_adam(1e-6)
     torch.cuda.synchronize()
@@ -257,8 +265,12 @@ def trainer_measure(cfg, pol, n_seq, prompt, gen, steps=3):
     t = float(np.median(ms))
     _, bf16, kind = load_peaks()
     tf = flops / (t * 1e-3) / 1e12
+    mode = ("precise: activations and backward operands as bf16 hi + lo pairs (1e-3 parity mode)"
+            if precise else "fast: single bf16 operands")
     out = {"workload": f"{cfg.name}: {n_seq} trajectories x {seq} tokens ({tokens} scored rows), "
-                       f"IS-REINFORCE fwd + bwd + Adam",
+                       f"IS-REINFORCE fwd + bwd + Adam", "mode": mode,
+           "flops_counted": "model flops (6 x matmul params per token + causal attention); the "
+                            "precise mode's extra split-operand MMAs are not counted",
            "tokens_per_s": tokens / (t * 1e-3), "step_ms": t, "forward_ms": float(np.median(fwd)),
            "tflops": tf, "bound": "tensor", "peak_tflops": bf16, "peak_kind": kind,
            "frac": tf / bf16 if bf16 else None, "objective": r.objective, "ess": r.ess}
@@ -357,6 +369,7 @@ def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use
         live[sid] = []
         return sid
 
+    log(f"generator {cfg.name} B={B}: opening streams")
     if steady:
         for done, left in steady_contexts(B, prompt, gen):
             open_one(done, left)
@@ -372,6 +385,7 @@ def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use
             live[sid].extend(evs.weight_version.tolist())
             if len(evs) or reason != "running":
                 waiting.discard(sid)
+    log("generator: streams seated (prefill done)")
     side = torch.cuda.Stream(device=dev)
     consumed = []       # (version at consumption, token versions) per finished sequence
     version = [0]
@@ -423,6 +437,7 @@ def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use
 
     for _ in range(warmup):
         step(None)
+    log("generator: warm-up done")
     prof, fused_ms = {}, []
     if profile:  # profiled rounds (outside the timed region): per-class CUDA events
         eng.profile_next_round()
@@ -446,6 +461,7 @@ def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use
         step(rec)
     torch.cuda.synchronize()
     clk = clocks.stop()
+    log("generator: timed steps done")
     # the same steps without an update in flight: the decode stall the update causes
     rec_nu = []
     for _ in range(max(3, steps // 2)):
@@ -677,13 +693,19 @@ def main():
     }
     ctx_now = g["ctx_now"]
     if not args.no_trainer:
+        log("trainer")
         tclk = ClockSampler(local).start()
         out["trainer"] = trainer_measure(cfg, pol, args.train_seqs, args.prompt, args.train_gen)
         out["trainer"]["clocks"] = tclk.stop()
+        log("trainer (fast bf16 mode)")
+        out["trainer_fast"] = trainer_measure(cfg, pol, args.train_seqs, args.prompt, args.train_gen,
+                                              precise=False)
     if not args.no_pipeline:
+        log("recompute-mode pause")
         payload = pol.clone().perturb(99, 0.002)
         out["pause_ms_recompute_mode"] = recompute_pause_measure(cfg, pol, payload, B, args.prompt)
         del payload
+        log("pipeline_1gpu")
         out["pipeline_1gpu"] = pipeline_measure(cfg, B, args.prompt, args.train_gen, R)
     del pol
     if not args.no_extra:
@@ -691,6 +713,7 @@ def main():
         for spec in filter(None, args.extra.split(",")):
             name, b, gen = spec.split(":")
             c = PRESETS[name]
+            log(f"extra config {spec}")
             try:
                 e, p = generator_measure(c, B=int(b), prompt=args.prompt, gen=int(gen), R=R,
                                          steps=max(3, args.steps // 2), warmup=2, steady=True,
@@ -708,7 +731,9 @@ def main():
                 out["extra_configs"][f"{name}:{b}:{gen}"] = {"error": f"{type(ex).__name__}: {ex}"}
             torch.cuda.empty_cache()
     if not args.no_cpu_baseline:
+        log("cpu baseline")
         out["cpu_baseline"] = cpu_sample(cfg, ctx_now)
+    log("done")
     print(json.dumps(out), flush=True)
 
 

@@ -363,7 +363,8 @@ class Ref:
         for name in ("ref_random_recurrent_policy", "ref_random_tabular_policy",
                      "ref_drift_checkpoints", "ref_mixed_policy_sample", "ref_fit_baseline",
                      "ref_is_reinforce_gradient", "ref_engine_lockstep", "ref_run_pipeline",
-                     "ref_run_conventional", "ref_process_group_id", "ref_kl_per_position"):
+                     "ref_run_conventional", "ref_process_group_id", "ref_kl_per_position",
+                     "ref_search_configs"):
             getattr(L, name).restype = vp
         L.ref_free.argtypes = [vp]
         L.ref_random_recurrent_policy.argtypes = [C.c_int, C.c_int, f64, u64]
@@ -508,6 +509,11 @@ class Ref:
 
     def process_group_id(self, members):
         return self._s(self.L.ref_process_group_id(json.dumps(members).encode()), parse=False)
+
+    def search_configs(self, spec: dict):
+        """throughput::search_configs (throughput.cpp:288-330) of the reference."""
+        self.L.ref_search_configs.argtypes = [C.c_char_p]
+        return self._s(self.L.ref_search_configs(json.dumps(spec).encode()))
 
     def kl_per_position(self, behavior_docs, schedule_max_len, max_lag, recompute, target_doc,
                         prompt_id, prefixes):

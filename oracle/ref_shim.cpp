@@ -358,4 +358,28 @@ char* ref_kl_per_position(const char* behavior_ckpts_json, int schedule_max_len,
   } catch (const std::exception& e) { return error_json(e); }
 }
 
+// search_configs (throughput.cpp:288-330) on a JSON spec:
+// {n, train_batch, curve: [[h, u], ...], padding_window, tau,
+//  lengths: {kind: "uniform" | "constant" | "empirical", max_len, values}, cap, use_padding}
+char* ref_search_configs(const char* spec_json) {
+  try {
+    const json s = json::parse(spec_json);
+    throughput::UtilizationCurve curve;
+    for (const auto& pt : s.at("curve")) curve.samples.push_back({pt[0].get<double>(), pt[1].get<double>()});
+    curve.padding_window = s.value("padding_window", 64);
+    const json& l = s.at("lengths");
+    const std::string kind = l.at("kind");
+    const auto lengths = kind == "uniform"    ? throughput::LengthDistribution::uniform(l.at("max_len"))
+                         : kind == "constant" ? throughput::LengthDistribution::constant(l.at("max_len"))
+                                              : throughput::LengthDistribution::empirical(
+                                                    l.at("values").get<std::vector<int>>());
+    const auto r = throughput::search_configs(s.at("n"), s.at("train_batch"), curve, s.at("tau"), lengths,
+                                              s.at("cap"), s.value("use_padding", false));
+    return dup(json{{"feasible", r.feasible}, {"gen_batch", r.gen_batch}, {"inference_count", r.inference_count},
+                    {"r_gen", r.report.r_gen}, {"r_train", r.report.r_train}, {"r_total", r.report.r_total},
+                    {"max_lag", r.report.max_lag}}
+                   .dump());
+  } catch (const std::exception& e) { return error_json(e); }
+}
+
 }  // extern "C"

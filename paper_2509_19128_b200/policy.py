@@ -160,7 +160,11 @@ class DecoderPolicy:
         class _Arr:
             __cuda_array_interface__ = {"shape": (n // 2,), "typestr": "<u2", "data": (p, False),
                                         "version": 3}
-        return torch.as_tensor(_Arr(), device=f"cuda:{self.device}").view(torch.bfloat16)
+
+            def __init__(self, owner):
+                self.owner = owner  # the tensor keeps _Arr alive, _Arr keeps the buffer's owner alive
+
+        return torch.as_tensor(_Arr(self), device=f"cuda:{self.device}").view(torch.bfloat16)
 
     def __del__(self):
         try:

@@ -129,3 +129,43 @@ def test_megakernel_terminator_and_refill(cuda):
     assert reason == "length" and len(evs) == 5
     assert eng.stream_tokens(sid)[:3] == [TINY.bos_token, 9, 9]
     eng.close()
+
+
+def test_multikernel_round_batch256_7b_width_matches_oracle(cuda):
+    """Config 4's generator shape (Qwen2.5-7B widths: hidden 3584, 28 / 4
+    heads, hd 128, intermediate 18944, V = 152064, untied LM head) at its
+    constant batch of 256 streams -- beyond the megakernel's 64 rows, so the
+    round runs as the multi-kernel path (persistent GEMMs, single-query
+    attention, sampler).  Two layers instead of 28 keep the fp32 oracle
+    check of 8 of the 256 streams (ragged prompts, sampled decoding) cheap;
+    every per-layer kernel and the LM head run at the 7B shapes."""
+    from paper_2509_19128_b200.policy import DecoderConfig
+
+    cfg = DecoderConfig("qwen2.5-7b-2l", 152064, 3584, 2, 28, 4, 128, 18944, False, 151643, 4096)
+    pol = DecoderPolicy.random(cfg, seed=17, scale=0.02)
+    rng = np.random.default_rng(12)
+    lens = rng.integers(0, 40, size=256)
+    lens[5] = 0
+    lens[77] = 70
+    prompts = [rng.integers(0, cfg.vocab_size, size=int(n)).tolist() for n in lens]
+    steps = 4
+    eng = Engine(pol, start_paused=True, max_streams=256, max_seq_len=96)
+    sids = [eng.open_stream("p", steps, 7000 + i, -1, pr) for i, pr in enumerate(prompts)]
+    eng.advance(2)
+    eng.profile_next_round()
+    eng.advance(steps + 4)
+    prof = eng.kernel_profile()
+    assert "decode_megakernel" not in prof and prof, "a 256-row round must take the multi-kernel path"
+    out = {}
+    for i in (0, 5, 77, 100, 128, 199, 254, 255):
+        evs, reason = eng.collect(sids[i])
+        assert reason == "length" and [e.position for e in evs] == list(range(steps))
+        out[i] = evs
+    eng.close()
+    m = oracle_for(pol, np.float32)
+    for i, evs in out.items():
+        cache = m.new_cache()
+        logits = m.prefill(cache, [cfg.bos_token] + prompts[i])[-1].astype(np.float64)
+        for e in evs:
+            lp_close([e.logprob], [DecoderOracle.log_softmax(logits)[e.token]])
+            logits = m.step([cache], [e.token], [len(cache["tokens"])])[0].astype(np.float64)
