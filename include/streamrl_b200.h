@@ -257,6 +257,19 @@ int srl_tabular_is_reinforce_gradient(const srl_policy* p, int32_t n_traj, const
                                       int32_t granularity, double* grad_rows, int32_t* row_touched);
 
 
+/* kl_per_position (rl_math.cpp:336-372) for the decoder policy, on the device:
+ * mean exact KL(behaviour || target) per position over teacher-forced
+ * prefixes (packed tokens[offsets[n_prefix]]).  Behaviour = the checkpoint
+ * chain switching at switch_points (MixedPolicySchedule::switch_points,
+ * rl_math.cpp:286-310; n_switch = 0 for a single policy), its KV cache stale
+ * across a switch (PipelineRL) or rebuilt under the new checkpoint
+ * (recompute_state = 1), as the engine serves it.  kl_out[cap] receives
+ * max prefix length values. */
+int srl_decoder_kl_per_position(const srl_policy* const* checkpoints, int32_t n_checkpoints,
+                                const int32_t* switch_points, int32_t n_switch, int32_t recompute_state,
+                                const srl_policy* target, const int32_t* tokens, const int64_t* offsets,
+                                int32_t n_prefix, double* kl_out, int32_t cap);
+
 /* ------------------------------------------------ decoder trainer step --- */
 /* IS-REINFORCE for the decoder policy: the reference's
  * is_reinforce_gradient (rl_math.cpp:211-276) generalised from tabular logits

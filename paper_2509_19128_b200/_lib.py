@@ -126,6 +126,7 @@ SIGNATURES: dict[str, tuple] = {
     "srl_policy_logprobs": (I, [vp, cp, vp, i32, vp]),
     "srl_truncated_is_weight": (I, [f64, f64, f64, P(f64)]),
     "srl_ess": (I, [vp, i32, P(f64)]),
+    "srl_decoder_kl_per_position": (I, [vp, i32, vp, i32, i32, vp, vp, vp, i32, vp, i32]),
     "srl_tabular_is_reinforce_gradient": (I, [vp, i32, P(cp), vp, vp, vp, vp, vp, i32, f64, i32, vp, vp]),
     "srl_lag_stats": (I, [vp, vp, i32, i32, vp, i32, vp, vp, vp]),
     "srl_crc32": (C.c_uint32, [vp, sz]),

@@ -16,6 +16,9 @@ int toy_policy_logprobs(const Policy& p, const std::string& prompt_id,
                         const std::vector<int32_t>& tokens, std::vector<double>& out, int device);
 int decoder_policy_logprobs(const DecoderWeights& w, const std::vector<int32_t>& tokens,
                             std::vector<double>& out);
+int decoder_kl_per_position(const std::vector<const DecoderWeights*>& ck, const std::vector<int>& switch_points,
+                            bool recompute, const DecoderWeights& target,
+                            const std::vector<std::vector<int32_t>>& prefixes, std::vector<double>& out);
 int tabular_is_reinforce_gradient(const Policy& p, int n_traj, const char* const* prompt_ids,
                                   const int32_t* tokens, const int64_t* offsets, const double* mu,
                                   const double* rewards, const double* baseline, bool use_is, double clamp,
@@ -488,6 +491,41 @@ extern "C" int srl_tabular_is_reinforce_gradient(const srl_policy* p, int32_t n_
     return tabular_is_reinforce_gradient(p->p, n_traj, prompt_ids, tokens, offsets,
                                          use_is ? behavior_logprobs : zeros.data(), rewards, baseline,
                                          use_is != 0, clamp, granularity, grad_rows, row_touched, 0);
+  });
+}
+
+// kl_per_position for the decoder policy (rl_math.cpp:336-372), kl.cpp
+extern "C" int srl_decoder_kl_per_position(const srl_policy* const* checkpoints, int32_t n_checkpoints,
+                                           const int32_t* switch_points, int32_t n_switch,
+                                           int32_t recompute_state, const srl_policy* target,
+                                           const int32_t* tokens, const int64_t* offsets, int32_t n_prefix,
+                                           double* kl_out, int32_t cap) {
+  return guarded([&] {
+    if (!checkpoints || n_checkpoints < 1 || !target || n_prefix < 0 || (n_prefix > 0 && (!tokens || !offsets)) ||
+        !kl_out || (n_switch > 0 && !switch_points))
+      return fail(SRL_INVALID_ARGUMENT, "kl: bad arguments");
+    if (target->p.type != SRL_POLICY_DECODER) return fail(SRL_INVALID_ARGUMENT, "kl: needs decoder policies");
+    std::vector<const DecoderWeights*> ck;
+    for (int i = 0; i < n_checkpoints; ++i) {
+      if (!checkpoints[i] || checkpoints[i]->p.type != SRL_POLICY_DECODER)
+        return fail(SRL_INVALID_ARGUMENT, "kl: needs decoder policies");
+      ck.push_back(checkpoints[i]->p.dec.get());
+    }
+    int st;
+    if ((st = require_device(target->p.dec->device))) return st;
+    std::vector<std::vector<int32_t>> pre;
+    size_t longest = 0;
+    for (int q = 0; q < n_prefix; ++q) {
+      pre.emplace_back(tokens + offsets[q], tokens + offsets[q + 1]);
+      longest = std::max(longest, pre.back().size());
+    }
+    if ((int64_t)longest > cap) return fail(SRL_INVALID_ARGUMENT, "kl: output capacity below the longest prefix");
+    std::vector<double> out;
+    if ((st = decoder_kl_per_position(ck, std::vector<int>(switch_points, switch_points + std::max(0, n_switch)),
+                                      recompute_state != 0, *target->p.dec, pre, out)))
+      return st;
+    std::copy(out.begin(), out.end(), kl_out);
+    return (int)SRL_OK;
   });
 }
 

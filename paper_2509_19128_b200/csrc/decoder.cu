@@ -686,6 +686,49 @@ __global__ void __launch_bounds__(kSampleThreads)
   if (tid == 0) out[row] = (double)x[targets[row]] - lse;
 }
 
+// Exact categorical KL(p || q) per row from two logits rows (numeric.hpp:34-46:
+// terms with p = 0 skipped, +inf where q has no support, clamped at 0); fp64
+// log-sum-exp of both rows, fp64 accumulation.
+__global__ void __launch_bounds__(kSampleThreads)
+    row_kl_kernel(const float* __restrict__ lp, const float* __restrict__ lq, int V, double* __restrict__ out) {
+  __shared__ double red[33];
+  __shared__ float fred[32];
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const float* x = lp + (size_t)row * V;
+  const float* y = lq + (size_t)row * V;
+  double lse[2];
+  for (int side = 0; side < 2; ++side) {
+    const float* z = side ? y : x;
+    float mx = -INFINITY;
+    for (int k = tid; k < V; k += kSampleThreads) mx = fmaxf(mx, z[k]);
+    mx = warp_max(mx);
+    if ((tid & 31) == 0) fred[tid >> 5] = mx;
+    __syncthreads();
+    if (tid < 32) {
+      float v = warp_max(tid < (kSampleThreads >> 5) ? fred[tid] : -INFINITY);
+      if (tid == 0) fred[0] = v;
+    }
+    __syncthreads();
+    const double M = (double)fred[0];
+    __syncthreads();
+    double part = 0.0;
+    for (int k = tid; k < V; k += kSampleThreads) part += exp((double)z[k] - M);
+    lse[side] = M + log(block_sum_d(part, red));
+  }
+  double part = 0.0;
+  int inf = 0;
+  for (int k = tid; k < V; k += kSampleThreads) {
+    const double a = (double)x[k] - lse[0], b = (double)y[k] - lse[1];
+    const double p = exp(a);
+    if (p == 0.0) continue;
+    if (!isfinite(b)) inf = 1;
+    part += p * (a - b);
+  }
+  const int any_inf = __syncthreads_or(inf);
+  const double kl = block_sum_d(part, red);
+  if (tid == 0) out[row] = any_inf ? INFINITY : fmax(kl, 0.0);
+}
+
 __global__ void __launch_bounds__(kSampleThreads)
     sample_logits_kernel(const float* __restrict__ logits, const float* __restrict__ pmax,
                          const double* __restrict__ psum, int V, const uint64_t* __restrict__ seeds,
@@ -952,6 +995,10 @@ void launch_sample(const float* logits, const float* pmax, const double* psum, i
 void launch_row_logprobs(const float* logits, int V, int rows, const int32_t* targets, double* out,
                          cudaStream_t st) {
   if (rows > 0) row_logprobs_kernel<<<rows, kSampleThreads, 0, st>>>(logits, V, targets, out);
+}
+
+void launch_row_kl(const float* logits_p, const float* logits_q, int V, int rows, double* out, cudaStream_t st) {
+  if (rows > 0) row_kl_kernel<<<rows, kSampleThreads, 0, st>>>(logits_p, logits_q, V, out);
 }
 
 void launch_sample_logits(const float* logits, int V, int rows, const uint64_t* seeds,

@@ -115,6 +115,8 @@ void launch_sample_logits(const float* logits, int V, int rows, const uint64_t* 
                           const int32_t* draw, int greedy, int32_t* tok, double* lp, cudaStream_t st);
 
 // out[r] = logits[r, targets[r]] - logsumexp(logits[r, :]) in fp64.
+// KL(softmax(p row) || softmax(q row)) per row, fp64 (numeric.hpp:34-46).
+void launch_row_kl(const float* logits_p, const float* logits_q, int V, int rows, double* out, cudaStream_t st);
 void launch_row_logprobs(const float* logits, int V, int rows, const int32_t* targets, double* out,
                          cudaStream_t st);
 

@@ -176,6 +176,50 @@ def is_reinforce_gradient(policy, trajectories, baseline, clamp: float,
     return _tabular_gradient(policy, trajectories, baseline, clamp, True, granularity)
 
 
+def mixed_schedule(max_len: int, max_lag: int) -> list:
+    """MixedPolicySchedule::make switch points (rl_math.cpp:286-301): the first
+    segment 2L/g long (the warm-up bubble), then every L/g tokens."""
+    if max_len < 1:
+        raise ValueError("schedule: max_len must be positive")
+    if max_lag < 1:
+        raise ValueError("schedule: max_lag must be positive")
+    first, step = (2 * max_len) // max_lag, max_len // max_lag
+    pts, t = [], first
+    while t < max_len and len(pts) < max_lag:
+        pts.append(t)
+        if step == 0:
+            break
+        t += step
+    return pts
+
+
+def kl_per_position(checkpoints, switch_points, recompute_state: bool, target, prefixes) -> np.ndarray:
+    """kl_per_position (rl_math.cpp:336-372) for decoder policies, on the
+    device: mean exact KL(behaviour || target) per position over the token
+    prefixes; the behaviour switches checkpoint at switch_points with a stale
+    (PipelineRL) or recomputed KV cache.  One checkpoint and no switch points =
+    BehaviorSpec::single."""
+    from .policy import DecoderPolicy
+
+    cks = list(checkpoints)
+    if not cks:
+        raise ValueError("kl: empty behavior spec")
+    if not all(isinstance(p, DecoderPolicy) for p in cks + [target]):
+        raise TypeError("kl_per_position: decoder policies (tabular / recurrent: the reference's own)")
+    toks = np.concatenate([np.asarray(p, dtype=np.int32) for p in prefixes]) if prefixes else \
+        np.zeros(1, dtype=np.int32)
+    offs = np.concatenate([[0], np.cumsum([len(p) for p in prefixes])]).astype(np.int64)
+    n = max((len(p) for p in prefixes), default=0)
+    out = np.zeros(max(n, 1))
+    hs = (C.c_void_p * len(cks))(*[p.handle.value if hasattr(p.handle, "value") else p.handle for p in cks])
+    sw = np.asarray(switch_points, dtype=np.int32)
+    st = _lib.lib().srl_decoder_kl_per_position(hs, len(cks), sw.ctypes.data if len(sw) else None, len(sw),
+                                               int(recompute_state), target.handle, toks.ctypes.data,
+                                               offs.ctypes.data, len(prefixes), out.ctypes.data, len(out))
+    _check(st, "kl_per_position")
+    return out[:n]
+
+
 def pipeline_max_lag_steps(gen_batch: int, inference_count: int, max_len: float, mean_len: float,
                            train_batch: int) -> int:
     """g_max = ceil(H * I * L / (mean L * B)) (throughput.cpp:260-269): the
