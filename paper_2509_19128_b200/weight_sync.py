@@ -62,11 +62,27 @@ class WeightChannel:
         and committed after.  Returns (applied, version, pause_ms)."""
         import torch.distributed as dist
 
+        from ._lib import SrlError
+
         nxt = self.version + 1
+        rejected = False
         if engine is not None:
-            view = engine.stage(nxt)
+            try:
+                view = engine.stage(nxt)
+            except (ValueError, SrlError):
+                # version_conflict (or an update already staged): this rank keeps
+                # serving its current weights, but it must still join the
+                # collective -- the other ranks are already in it -- so it
+                # receives into a scratch buffer and commits nothing
+                view, rejected = None, True
             if view is not None:
                 standby_view = view
+        if rejected:
+            import torch
+
+            n = engine.standby_bytes() if hasattr(engine, "standby_bytes") else standby_view.numel()
+            standby_view = torch.empty(n, dtype=torch.uint8, device=standby_view.device
+                                       if standby_view is not None else "cpu")
         if rank == self.src and payload is not None and payload.data_ptr() != standby_view.data_ptr():
             standby_view.copy_(payload)
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
@@ -77,8 +93,8 @@ class WeightChannel:
             # the swap must not race the transfer: the engine reads the standby
             # buffer on its own stream right after commit
             torch.cuda.current_stream().synchronize()
-        applied, pause = True, 0.0
-        if engine is not None:
+        applied, pause = not rejected, 0.0
+        if engine is not None and not rejected:
             applied, pause = engine.commit(nxt)
         if applied:
             self.version = nxt
@@ -105,6 +121,9 @@ class EngineStandby:
     def commit(self, version):
         res, pause = self.engine.commit_weight_update(version)
         return res.applied, pause
+
+    def standby_bytes(self):
+        return self.engine.standby_bytes()
 
 
 def shard(items, rank: int, world: int):

@@ -75,7 +75,7 @@ class FakeEngine:
 
     def stage(self, version):
         if version != self.version + 1 or self.staged is not None:
-            return None
+            raise ValueError("version_conflict")  # as EngineStandby.stage
         self.staged = version
         return self.standby.view(torch.uint8)
 

@@ -32,8 +32,8 @@ class FakeEngine:
         self.staged = None
 
     def stage(self, v):
-        if v != self.version + 1:
-            return None
+        if v != self.version + 1:  # as EngineStandby.stage / begin_weight_update
+            raise ValueError("version_conflict")
         self.staged = v
         return self.standby
 
@@ -110,9 +110,51 @@ def test_partitions_of_the_box():
 def test_stale_version_is_rejected_without_side_effects():
     eng = FakeEngine(8)
     before = eng.active.clone()
-    assert eng.stage(2) is None  # version_conflict: not staged
+    with pytest.raises(ValueError):
+        eng.stage(2)  # version_conflict: not staged
     ok, _ = eng.commit(2)
     assert not ok and torch.equal(eng.active, before) and eng.version == 0
+
+
+def _conflict_worker(rank, world, port, q):
+    """The generator is one version ahead of the channel: it rejects the first
+    update (version_conflict) but still joins the broadcast -- the trainer
+    does not hang -- keeps its weights, and accepts the next one."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 1024
+        eng = FakeEngine(n)
+        eng.version = 1
+        eng.active.fill_(42)
+        ch = WeightChannel(src=0)
+        out = []
+        for step in range(2):
+            payload = torch.full((n,), 10 + step, dtype=torch.uint8) if rank == 0 else None
+            if rank == 1 and step == 1:
+                ch.version = 1  # the generator's channel catches up with its engine
+            applied, v, _ = ch.publish(rank, torch.empty(n, dtype=torch.uint8) if rank == 0 else eng.standby,
+                                       payload, engine=eng if rank == 1 else None)
+            out.append((applied, v, int(eng.active[0])))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rejecting_generator_still_joins_the_broadcast():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_conflict_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert out[1][0] == (False, 0, 42)      # rejected: weights untouched, version unchanged
+    assert out[1][1] == (True, 2, 11)       # the next update lands
 
 
 def _dp_worker(rank, world, port, q):
