@@ -381,7 +381,7 @@ def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use
     waiting = set(live)
     while waiting:
         eng.advance(4)
-        for sid, (evs, reason, more) in eng.wait_events_many(list(live), columns=True).items():
+        for sid, (evs, reason, more) in eng.wait_events_many(list(live), columns=True, block=False).items():
             live[sid].extend(evs.weight_version.tolist())
             if len(evs) or reason != "running":
                 waiting.discard(sid)
@@ -415,7 +415,7 @@ def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use
             copy_ms = e0.elapsed_time(e1)
         # actor side: drain events, refill finished streams (constant batch)
         finished = []
-        drained = eng.wait_events_many(list(live), columns=True)
+        drained = eng.wait_events_many(list(live), columns=True, block=False)
         for sid, (evs, reason, more) in drained.items():
             d2h[0] += 24 * len(evs)
             live[sid].extend(evs.weight_version.tolist())
@@ -450,7 +450,7 @@ def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use
                 eng.advance(1)
                 fused_ms.append(eng.kernel_profile()["decode_megakernel"][0])
     ctx_now = [len(eng.stream_tokens(sid)) for sid in live]
-    for sid, (evs, reason, more) in eng.wait_events_many(list(live), columns=True).items():
+    for sid, (evs, reason, more) in eng.wait_events_many(list(live), columns=True, block=False).items():
         live[sid].extend(evs.weight_version.tolist())
 
     clocks = ClockSampler(device).start()

@@ -159,6 +159,12 @@ int srl_engine_wait_events(srl_engine* e, int64_t stream, srl_token_event* buf, 
 int srl_engine_wait_events_many(srl_engine* e, const int64_t* streams, int32_t n_streams,
                                 srl_token_event* buf, int32_t cap, int32_t* counts,
                                 int32_t* finish_reasons, int32_t* more);
+/* The same without blocking: each stream returns whatever is queued (possibly
+ * nothing; more = 1 while it is running) -- an actor polling a paused
+ * engine whose streams may not have emitted yet. */
+int srl_engine_poll_events_many(srl_engine* e, const int64_t* streams, int32_t n_streams,
+                                srl_token_event* buf, int32_t cap, int32_t* counts,
+                                int32_t* finish_reasons, int32_t* more);
 /* apply_weight_update (engine.cpp:79-117).  Returns SRL_VERSION_CONFLICT /
  * SRL_INVALID_POLICY / SRL_POLICY_MISMATCH without side effects. */
 int srl_engine_apply_weight_update(srl_engine* e, int32_t new_version, const srl_policy* policy,

@@ -105,6 +105,7 @@ SIGNATURES: dict[str, tuple] = {
     "srl_engine_open_stream": (I, [vp, cp, i32, u64, i32, vp, i32, P(i64)]),
     "srl_engine_wait_events": (I, [vp, i64, P(TokenEventC), i32, P(i32), P(i32), P(i32)]),
     "srl_engine_wait_events_many": (I, [vp, vp, i32, P(TokenEventC), i32, vp, vp, vp]),
+    "srl_engine_poll_events_many": (I, [vp, vp, i32, P(TokenEventC), i32, vp, vp, vp]),
     "srl_engine_apply_weight_update": (I, [vp, i32, vp, P(i32)]),
     "srl_engine_begin_weight_update": (I, [vp, i32, P(vp), P(sz)]),
     "srl_engine_commit_weight_update": (I, [vp, i32, P(i32), P(f64)]),

@@ -284,9 +284,9 @@ extern "C" int srl_engine_wait_events(srl_engine* e, int64_t stream, srl_token_e
   });
 }
 
-extern "C" int srl_engine_wait_events_many(srl_engine* e, const int64_t* streams, int32_t n_streams,
-                                           srl_token_event* buf, int32_t cap, int32_t* counts,
-                                           int32_t* finish_reasons, int32_t* more) {
+namespace {
+int events_many(srl_engine* e, const int64_t* streams, int32_t n_streams, srl_token_event* buf, int32_t cap,
+                int32_t* counts, int32_t* finish_reasons, int32_t* more, bool block) {
   return guarded([&] {
     if (!e || !streams || n_streams < 0 || !buf || cap < 1 || !counts || !finish_reasons || !more)
       return fail(SRL_INVALID_ARGUMENT, "wait_events_many: bad arguments");
@@ -296,7 +296,7 @@ extern "C" int srl_engine_wait_events_many(srl_engine* e, const int64_t* streams
       int reason = 0, m = 0;
       out.clear();
       if (used < cap) {
-        const int st = e->e->wait_events(streams[i], out, cap - used, &reason, &m);
+        const int st = e->e->wait_events(streams[i], out, cap - used, &reason, &m, block);
         if (st != SRL_OK) return st;
       } else {
         m = 1;  // no room left: the stream keeps its events for the next call
@@ -309,6 +309,19 @@ extern "C" int srl_engine_wait_events_many(srl_engine* e, const int64_t* streams
     }
     return (int)SRL_OK;
   });
+}
+}  // namespace
+
+extern "C" int srl_engine_wait_events_many(srl_engine* e, const int64_t* streams, int32_t n_streams,
+                                           srl_token_event* buf, int32_t cap, int32_t* counts,
+                                           int32_t* finish_reasons, int32_t* more) {
+  return events_many(e, streams, n_streams, buf, cap, counts, finish_reasons, more, true);
+}
+
+extern "C" int srl_engine_poll_events_many(srl_engine* e, const int64_t* streams, int32_t n_streams,
+                                           srl_token_event* buf, int32_t cap, int32_t* counts,
+                                           int32_t* finish_reasons, int32_t* more) {
+  return events_many(e, streams, n_streams, buf, cap, counts, finish_reasons, more, false);
 }
 
 extern "C" int srl_engine_apply_weight_update(srl_engine* e, int32_t new_version,

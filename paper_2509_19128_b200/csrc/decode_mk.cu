@@ -179,6 +179,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 __device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
 __device__ __forceinline__ float wsum(float v) {
@@ -425,6 +426,39 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   const int ntiles = (nkeys + KT - 1) / KT;
   const bool owner = pos >= k0 && pos < k0 + P.attn_chunk;  // this split holds the new key
   const int qend = nq * HD, kend = qend + nkv * HD;
+  constexpr size_t rec = (size_t)G * (HD + 2);
+  // split arrival; the last split to arrive merges the used ones in split order
+  auto arrive_and_merge = [&]() {
+    csync();
+    if (ct == 0) {
+      __threadfence();
+      *s_flag = (atomicAdd(&ctr[m * nkv + kh], 1u) + 1u == ep1 * (unsigned)splits);
+    }
+    csync();
+    if (*s_flag) {
+      __threadfence();
+      const float* base = ws + ((size_t)m * nkv + kh) * splits * rec;
+      const int used = min(splits, (ctx + P.attn_chunk - 1) / P.attn_chunk);
+      for (int i = ct; i < G * HD; i += kCT) {
+        const int g = i / HD, d = i % HD;
+        float M = -INFINITY;
+        for (int q = 0; q < used; ++q) M = fmaxf(M, __ldcg(&base[q * rec + g * (HD + 2)]));
+        float L = 0.f, Acc = 0.f;
+        for (int q = 0; q < used; ++q) {
+          const float ms = __ldcg(&base[q * rec + g * (HD + 2)]);
+          const float a = (ms == -INFINITY) ? 0.f : __expf(ms - M);
+          L += __ldcg(&base[q * rec + g * (HD + 2) + 1]) * a;
+          Acc += __ldcg(&base[q * rec + g * (HD + 2) + 2 + d]) * a;
+        }
+        P.attn[(size_t)m * nq * HD + (kh * G + g) * HD + d] = __float2bfloat16(L > 0.f ? Acc / L : 0.f);
+      }
+    }
+    csync();
+  };
+  if (nkeys == 0) {  // a split past the context: no q / K / V work, only its arrival
+    arrive_and_merge();
+    return;
+  }
 
   // K/V tiles: warp w streams tiles w, w + 8, ... into buffer slot 7 - w, so the
   // first tiles land in the slots the QKV partial staging does not alias and
@@ -433,24 +467,40 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   const __nv_bfloat16* vc = P.vc + P.kv_layer_elems * layer;
   uint8_t* kb = tiles + (kCW - 1 - warp) * A::warp_bytes;
   uint8_t* vb = kb + A::kbuf;
-  auto load_tile = [&](int t, int page) {
+  // K and V of a tile travel as two cp.async groups, so the next tile's K
+  // streams in while this tile's softmax and P.V run, and its V while the
+  // next S = Q K^T runs (the same two buffers per warp, no extra smem)
+  auto tile_base = [&](int t, int page) {
     const int key0 = k0 + t * KT;
-    const int nv = min(KT, k1 - key0);
-    const size_t base = (((size_t)page * nkv + kh) * kPageTokens + (key0 % kPageTokens)) * HD;
-    const uint4* kg = reinterpret_cast<const uint4*>(kc + base);
-    const uint4* vg = reinterpret_cast<const uint4*>(vc + base);
+    return (((size_t)page * nkv + kh) * kPageTokens + (key0 % kPageTokens)) * HD;
+  };
+  auto load_k = [&](int t, int page) {
+    const int nv = min(KT, k1 - (k0 + t * KT));
+    const uint4* kg = reinterpret_cast<const uint4*>(kc + tile_base(t, page));
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int e = lane + 32 * i, r = e / V4, c = e % V4;
-      if (r < nv) {
-        cp_async16(kb + r * A::ROW + c * 16, kg + e);
-        cp_async16(vb + r * A::VROW + c * 16, vg + e);
-      } else {  // P is 0 there, but 0 x a stale NaN pattern is NaN in the MMA
-        *reinterpret_cast<uint4*>(vb + r * A::VROW + c * 16) = make_uint4(0u, 0u, 0u, 0u);
-      }
+      if (r < nv) cp_async16(kb + r * A::ROW + c * 16, kg + e);
     }
     cp_async_commit();
   };
+  auto load_v = [&](int t, int page) {
+    const int nv = min(KT, k1 - (k0 + t * KT));
+    const uint4* vg = reinterpret_cast<const uint4*>(vc + tile_base(t, page));
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = lane + 32 * i, r = e / V4, c = e % V4;
+      if (r < nv) cp_async16(vb + r * A::VROW + c * 16, vg + e);
+      else  // P is 0 there, but 0 x a stale NaN pattern is NaN in the MMA
+        *reinterpret_cast<uint4*>(vb + r * A::VROW + c * 16) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    cp_async_commit();
+  };
+  auto load_tile = [&](int t, int page) {
+    load_k(t, page);
+    load_v(t, page);
+  };
+  auto tile_page = [&](int t) { return P.block_table[(size_t)slot * P.pps + (k0 + t * KT) / kPageTokens]; };
   const int free_slot0 = P.pairs ? 0 : (qkv_cs * W * 4 + (int)A::warp_bytes - 1) / (int)A::warp_bytes;
   const bool early = warp < ntiles && kCW - 1 - warp >= free_slot0;
   if (P.pairs) {
@@ -564,18 +614,18 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
 #pragma unroll
     for (int i = 0; i < 4; ++i) o[n][i] = 0.f;
   float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;  // heads lane/4, lane/4 + 8
+  if (warp < ntiles && !early) load_tile(warp, tile_page(warp));
   for (int t = warp; t < ntiles; t += kCW) {
     const int key0 = k0 + t * KT;
     const int nv = min(KT, k1 - key0);
-    if (!(early && t == warp)) load_tile(t, P.block_table[(size_t)slot * P.pps + key0 / kPageTokens]);
-    cp_async_wait_all();
+    const bool has_next = t + kCW < ntiles;
+    const int next_page = has_next ? tile_page(t + kCW) : 0;  // lookup latency under this tile
+    const bool new_key = !P.pairs && owner && pos >= key0 && pos < key0 + nv;
+    cp_async_wait_1();  // pending: K(t), V(t) -> K(t) landed
     __syncwarp();
-    if (!P.pairs && owner && pos >= key0 && pos < key0 + nv) {  // the new key from shared memory
+    if (new_key) {  // the new key from shared memory
       const int r = pos - key0;
-      for (int d = lane; d < HD; d += 32) {
-        reinterpret_cast<__nv_bfloat16*>(kb + r * A::ROW)[d] = snew[d];
-        reinterpret_cast<__nv_bfloat16*>(vb + r * A::VROW)[d] = snew[HD + d];
-      }
+      for (int d = lane; d < HD; d += 32) reinterpret_cast<__nv_bfloat16*>(kb + r * A::ROW)[d] = snew[d];
       __syncwarp();
     }
     float sc[NKT][4];
@@ -598,6 +648,8 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
         mma16816(sc[n], a, ld_b32(kp), ld_b32(kp + 8));
       }
     }
+    __syncwarp();  // every lane is done with K(t)
+    if (has_next) load_k(t + kCW, next_page);
     float mx_lo = m_lo, mx_hi = m_hi;
 #pragma unroll
     for (int n = 0; n < NKT; ++n)
@@ -635,6 +687,15 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
       o[n][0] *= c_lo; o[n][1] *= c_lo;
       o[n][2] *= c_hi; o[n][3] *= c_hi;
     }
+    // pending: V(t) [, K(t + 8)] -> V(t) landed
+    if (has_next) cp_async_wait_1();
+    else cp_async_wait_all();
+    __syncwarp();
+    if (new_key) {
+      const int r = pos - key0;
+      for (int d = lane; d < HD; d += 32) reinterpret_cast<__nv_bfloat16*>(vb + r * A::VROW)[d] = snew[HD + d];
+      __syncwarp();
+    }
     // P enters as hi + lo bf16 halves (two MMAs on the same V fragment): ~16
     // mantissa bits, so P.V keeps fp32-class accuracy (the oracle's P is fp64)
 #pragma unroll
@@ -652,7 +713,8 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
         if (!(P.dbg & 1)) mma16816(o[n], al, b0, b1);  // SRL_MK_DBG=1: single bf16 P (A/B)
       }
     }
-    __syncwarp();
+    __syncwarp();  // every lane is done with V(t)
+    if (has_next) load_v(t + kCW, next_page);
   }
 #pragma unroll
   for (int off = 1; off <= 2; off <<= 1) {
@@ -678,7 +740,6 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
     }
   }
   csync();
-  constexpr size_t rec = (size_t)G * (HD + 2);
   float* my_ws = ws + (((size_t)m * nkv + kh) * splits + split) * rec;
   for (int i = ct; i < G * HD; i += kCT) {
     const int g = i / HD, d = i % HD;
@@ -707,31 +768,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
     if (tr && ct == 0 && tr[14] == 0) tr[14] = clock64() - c_start;
     return;
   }
-  csync();
-  if (ct == 0) {
-    __threadfence();
-    *s_flag = (atomicAdd(&ctr[m * nkv + kh], 1u) + 1u == ep1 * (unsigned)splits);
-  }
-  csync();
-  if (*s_flag) {
-    __threadfence();
-    const float* base = ws + ((size_t)m * nkv + kh) * splits * rec;
-    const int used = min(splits, (ctx + P.attn_chunk - 1) / P.attn_chunk);
-    for (int i = ct; i < G * HD; i += kCT) {
-      const int g = i / HD, d = i % HD;
-      float M = -INFINITY;
-      for (int q = 0; q < used; ++q) M = fmaxf(M, __ldcg(&base[q * rec + g * (HD + 2)]));
-      float L = 0.f, Acc = 0.f;
-      for (int q = 0; q < used; ++q) {
-        const float ms = __ldcg(&base[q * rec + g * (HD + 2)]);
-        const float a = (ms == -INFINITY) ? 0.f : __expf(ms - M);
-        L += __ldcg(&base[q * rec + g * (HD + 2) + 1]) * a;
-        Acc += __ldcg(&base[q * rec + g * (HD + 2) + 2 + d]) * a;
-      }
-      P.attn[(size_t)m * nq * HD + (kh * G + g) * HD + d] = __float2bfloat16(L > 0.f ? Acc / L : 0.f);
-    }
-  }
-  csync();
+  arrive_and_merge();
 }
 
 // plan copy + embedding + first RMSNorm statistics for row m.  red: one

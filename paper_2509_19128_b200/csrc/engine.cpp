@@ -88,11 +88,11 @@ void Engine::assign_slots_locked() {
 
 // engine.cpp:63-77
 int Engine::wait_events(int64_t id, std::vector<srl_token_event>& out, int cap, int* reason,
-                        int* more) {
+                        int* more, bool block) {
   std::unique_lock<std::mutex> lk(lock_);
   Stream* s = find(id);
   if (s == nullptr) return fail(SRL_UNKNOWN_STREAM, "unknown stream id s" + std::to_string(id));
-  cv_.wait(lk, [&] { return !s->outbox.empty() || s->finish != SRL_FINISH_RUNNING; });
+  if (block) cv_.wait(lk, [&] { return !s->outbox.empty() || s->finish != SRL_FINISH_RUNNING; });
   while (!s->outbox.empty() && (int)out.size() < cap) {
     out.push_back(s->outbox.front());
     s->outbox.pop_front();

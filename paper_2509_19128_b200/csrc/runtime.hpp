@@ -143,7 +143,9 @@ class Engine {
   ~Engine();
   int open_stream(const std::string& prompt_id, int max_tokens, uint64_t seed, int32_t terminator,
                   const std::vector<int32_t>& prompt, int64_t* id);
-  int wait_events(int64_t id, std::vector<srl_token_event>& out, int cap, int* reason, int* more);
+  // block = false: return at once with whatever is queued (srl_engine_poll_events_many)
+  int wait_events(int64_t id, std::vector<srl_token_event>& out, int cap, int* reason, int* more,
+                  bool block = true);
   int apply_weight_update(int new_version, const Policy& policy, int* version_out);
   int begin_weight_update(int new_version, void** ptr, size_t* bytes);
   int standby_bytes(size_t* bytes);

@@ -147,20 +147,23 @@ class Engine:
                 break
         return events, FINISH[reason.value], bool(more.value)
 
-    def wait_events_many(self, stream_ids, columns: bool = False):
+    def wait_events_many(self, stream_ids, columns: bool = False, block: bool = True):
         """wait_events for each listed stream in ONE native call (the actor's
         per-step drain): {stream_id: (events, finish_reason, more)}.  A stream
         whose events did not fit in the buffer reports more=True.  columns=True
         returns each stream's events as an EventColumns of numpy arrays instead
-        of TokenEvent objects (no per-event Python object)."""
+        of TokenEvent objects (no per-event Python object).  block=False: poll
+        (srl_engine_poll_events_many) -- a stream with nothing queued returns
+        no events instead of waiting."""
         ids = np.array([self._sid(s) for s in stream_ids], dtype=np.int64)
         k = len(ids)
         counts = np.zeros(k, dtype=np.int32)
         reasons = np.zeros(k, dtype=np.int32)
         more = np.zeros(k, dtype=np.int32)
         evbuf, evarr = self._buffers()
-        st = _lib.lib().srl_engine_wait_events_many(self._h, ids.ctypes.data, k, evbuf, len(evbuf),
-                                                    counts.ctypes.data, reasons.ctypes.data, more.ctypes.data)
+        fn = _lib.lib().srl_engine_wait_events_many if block else _lib.lib().srl_engine_poll_events_many
+        st = fn(self._h, ids.ctypes.data, k, evbuf, len(evbuf), counts.ctypes.data, reasons.ctypes.data,
+                more.ctypes.data)
         _raise_for(st, "wait_events_many")
         total = int(counts.sum())
         a = evarr[:total]

@@ -154,7 +154,12 @@ class TorchTransport:
     def recv_begin(self, engine, version: int) -> bool:
         import torch
 
-        view = engine.stage(version)
+        from ._lib import SrlError
+
+        try:
+            view = engine.stage(version)
+        except (ValueError, SrlError):  # version_conflict / busy: keep serving, still join the broadcast
+            view = None
         self._staged = view is not None
         buf = view if view is not None else torch.empty(engine.standby_bytes(), dtype=torch.uint8)
         self._t0 = time.perf_counter()

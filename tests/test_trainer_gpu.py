@@ -43,16 +43,22 @@ TINY128 = DecoderConfig("tiny-hd128", 256, 256, 2, 6, 2, 128, 512, False, 0, 409
 
 
 def check_precise(res, g_dev, lps, J, g_ref, off, bar=1e-3):
-    for got, exp in zip(res.logprobs, lps):
-        np.testing.assert_allclose(got[1:], exp, rtol=bar, atol=1e-5)
-    assert abs(res.objective - J) <= bar * max(1e-3, abs(J)), (res.objective, J)
+    lp_err = max(float(np.max(np.abs(np.asarray(got[1:]) - exp) / np.maximum(np.abs(exp), 1e-2)))
+                 for got, exp in zip(res.logprobs, lps))
     rel = np.linalg.norm(g_dev - g_ref) / np.linalg.norm(g_ref)
-    assert rel < bar, rel
+    per = {}
     for name, (o, n) in off.items():
         a, b = g_dev[o:o + n], g_ref[o:o + n]
         nb = np.linalg.norm(b)
         if nb > 1e-6 * np.linalg.norm(g_ref):
-            assert np.linalg.norm(a - b) / nb < 10 * bar, (name, np.linalg.norm(a - b) / nb)
+            per[name] = float(np.linalg.norm(a - b) / nb)
+    worst = sorted(per.items(), key=lambda kv: -kv[1])[:6]
+    diag = f"logprob rel {lp_err:.2e}, J {res.objective} vs {J}, grad relL2 {rel:.2e}, worst {worst}"
+    print(diag)
+    assert lp_err < bar, diag
+    assert abs(res.objective - J) <= bar * max(1e-3, abs(J)), diag
+    assert rel < bar, diag
+    assert all(v < 10 * bar for v in per.values()), diag
     return rel
 
 
@@ -224,6 +230,16 @@ def test_trainer_qwen05b_large_batch_paths(cuda, precise):
         torch.set_default_device(prev)
     n = np.linalg.norm(g_ref)
     if precise:
+        # the reference's own fp32-accumulation spread on the same batch (diagnostic)
+        torch.set_default_device(cuda)
+        try:
+            r32 = TorchDecoder(QWEN25_05B.to_dict(), w16, rounding="kv", dtype=torch.float32)
+            r32.is_reinforce(trajs, len(trajs), 5.0, "per_token")
+            g32 = r32.flat_grad()
+        finally:
+            torch.set_default_device(prev)
+        print(f"0.5B reference fp32-vs-fp64 gradient spread {np.linalg.norm(g32 - g_ref) / n:.2e}, "
+              f"device vs fp64 {np.linalg.norm(full - g_ref) / n:.2e}")
         check_precise(res, full, lps, J, g_ref, ref.off)
         assert np.linalg.norm(parts - g_ref) / n < 1e-3
         assert np.linalg.norm(full - parts) / np.linalg.norm(parts) < 1e-4

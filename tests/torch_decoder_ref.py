@@ -18,7 +18,8 @@ def bf16_st(x):
 
 
 class TorchDecoder:
-    def __init__(self, cfg: dict, flat_u16: np.ndarray, exact: bool = False, rounding: str = "device"):
+    def __init__(self, cfg: dict, flat_u16: np.ndarray, exact: bool = False, rounding: str = "device",
+                 dtype=torch.float64):
         """exact=True: no bf16 rounding points, fp64 RoPE tables and scale
         (pinned against transformers' Qwen2 in tests/test_decoder_oracle.py).
         rounding (exact=False): "device" = every bf16 rounding point of the
@@ -29,6 +30,7 @@ class TorchDecoder:
         self.cfg = cfg
         self.exact = exact
         self.rounding = rounding
+        self.dtype = dtype  # float32: the same restatement at fp32 accumulation (self-spread)
         self.off, self.total = layout(cfg)
         H, I = cfg["hidden"], cfg["intermediate"]
         nq, nkv, hd = cfg["q_heads"], cfg["kv_heads"], cfg["head_dim"]
@@ -44,7 +46,7 @@ class TorchDecoder:
         for name, shape in shapes.items():
             o, n = self.off[name]
             t = torch.tensor(bf16_bits_to_f32(flat_u16[o:o + n]).astype(np.float64)).reshape(shape)
-            self.p[name] = t.requires_grad_(True)
+            self.p[name] = t.to(dtype).requires_grad_(True)
 
     def flat_grad(self):
         g = np.zeros(self.total)
@@ -72,6 +74,7 @@ class TorchDecoder:
         else:
             cos = ang.cos().to(torch.float32).to(torch.float64)
             sin = ang.sin().to(torch.float32).to(torch.float64)
+        cos, sin = cos.to(self.dtype), sin.to(self.dtype)
         bf16 = (lambda z: z) if (self.exact or self.rounding == "kv") else bf16_st
         bf16_qkv = (lambda z: z) if self.exact else bf16_st
 
@@ -111,14 +114,14 @@ class TorchDecoder:
 
     def is_reinforce(self, trajs, m, clamp, granularity):
         """J and its gradient (into .grad); weights stop-gradient."""
-        J = torch.zeros((), dtype=torch.float64)
+        J = torch.zeros((), dtype=self.dtype)
         lps = []
         for t in trajs:
             lp = self.logprobs(t["tokens"])
             lps.append(lp.detach().cpu().numpy())
             lb = t["loss_begin"] - 1
-            mu = torch.tensor(t["behavior_logprobs"][1:], dtype=torch.float64)
-            adv = torch.tensor(t["advantages"][1:], dtype=torch.float64)
+            mu = torch.tensor(t["behavior_logprobs"][1:], dtype=self.dtype)
+            adv = torch.tensor(t["advantages"][1:], dtype=self.dtype)
             sl = slice(lb, None)
             if granularity == "sequence":
                 w = torch.clamp(torch.exp(lp[sl].sum() - mu[sl].sum()), max=clamp).detach()
