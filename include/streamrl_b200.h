@@ -402,6 +402,17 @@ int srl_kernel_gemm_mn(const void* w, const void* x, int32_t M, int32_t N, int32
  * draw #draw_index[r] of SplitMix64(seeds[r]) (rng.hpp:18-28) and the
  * inverse CDF of exp(log_softmax) in fp64 (rng.hpp:61-69, engine.cpp:130-138);
  * greedy = argmax, lowest index on ties.  Writes token and log-prob. */
+/* Single-query paged GQA attention of the multi-kernel round (decoder.cu
+ * attention_kernel): q [rows x nq x hd], caches [pages][nkv][64][hd] (bf16),
+ * block_table [slots x pages_per_seq], keys 0..row_pos[r] of slot row_slot[r];
+ * out [rows x nq x hd] bf16.  hd 64 or 128. */
+int srl_kernel_attention_decode(const void* q, const void* kc, const void* vc, const int32_t* block_table,
+                                int32_t pages_per_seq, const int32_t* row_slot, const int32_t* row_pos,
+                                int32_t rows, int32_t nq, int32_t nkv, int32_t hd, int32_t max_ctx, void* out,
+                                void* stream);
+/* Device-to-device copy on the copy engines (no SM: runs beside the decode
+ * megakernel), e.g. a one-GPU update into the standby buffer. */
+int srl_device_copy_async(void* dst, const void* src, size_t nbytes, void* stream);
 int srl_kernel_sample_logits(const float* logits, int32_t vocab, int32_t rows,
                              const uint64_t* seeds, const int32_t* draw_index, int32_t greedy,
                              int32_t* tokens_out, double* logprobs_out, void* stream);

@@ -109,3 +109,44 @@ extern "C" int srl_kernel_sample_logits(const float* logits, int32_t vocab, int3
                        static_cast<cudaStream_t>(stream));
   return cuda_status(cudaGetLastError());
 }
+
+// Single-query paged GQA attention (the multi-kernel round's attention_kernel,
+// decoder.cu) on caller buffers: q [rows x nq x hd] bf16, K / V caches
+// [pages][nkv][64][hd] bf16, block_table [slots x pages_per_seq], per row its
+// slot and position (keys 0..pos).  out [rows x nq x hd] bf16.
+extern "C" int srl_kernel_attention_decode(const void* q, const void* kc, const void* vc,
+                                           const int32_t* block_table, int32_t pages_per_seq,
+                                           const int32_t* row_slot, const int32_t* row_pos, int32_t rows,
+                                           int32_t nq, int32_t nkv, int32_t hd, int32_t max_ctx, void* out,
+                                           void* stream) {
+  if (!q || !kc || !vc || !block_table || !row_slot || !row_pos || !out || rows < 1 || nkv < 1 ||
+      nq % nkv != 0 || (hd != 64 && hd != 128) || max_ctx < 1)
+    return SRL_INVALID_ARGUMENT;
+  DecoderDims d{};
+  d.nq = nq;
+  d.nkv = nkv;
+  d.hd = hd;
+  RoundPlan plan{const_cast<int32_t*>(row_slot), const_cast<int32_t*>(row_pos), nullptr, nullptr};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t wsf = attention_ws_floats(d, rows, max_ctx);
+  float* ws = nullptr;
+  int* ctr = nullptr;
+  if (cudaMallocAsync(&ws, sizeof(float) * wsf, st) != cudaSuccess ||
+      cudaMallocAsync(&ctr, sizeof(int) * (size_t)rows * nkv, st) != cudaSuccess)
+    return SRL_CUDA_ERROR;
+  cudaMemsetAsync(ctr, 0, sizeof(int) * (size_t)rows * nkv, st);
+  launch_attention(static_cast<const __nv_bfloat16*>(q), d, plan, rows, block_table, pages_per_seq,
+                   static_cast<const __nv_bfloat16*>(kc), static_cast<const __nv_bfloat16*>(vc), max_ctx, ws,
+                   ctr, wsf, static_cast<__nv_bfloat16*>(out), st);
+  cudaFreeAsync(ws, st);
+  cudaFreeAsync(ctr, st);
+  return cuda_status(cudaGetLastError());
+}
+
+// Device-to-device copy on the copy engines (cudaMemcpyAsync), e.g. a
+// one-GPU weight update into the standby buffer: unlike a copy kernel it
+// needs no SM, so it runs beside the persistent decode megakernel.
+extern "C" int srl_device_copy_async(void* dst, const void* src, size_t nbytes, void* stream) {
+  if ((!dst || !src) && nbytes) return SRL_INVALID_ARGUMENT;
+  return cuda_status(cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+}

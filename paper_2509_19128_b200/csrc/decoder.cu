@@ -150,7 +150,16 @@ __global__ void rope_append_kernel(const float* __restrict__ qkv, int nq, int nk
 // P.V with lane = head dims.  Split partials are combined by the last CTA of
 // the (row, head) in split order (deterministic).
 constexpr int kAttnWarps = 4;
-constexpr int kAttnChunk = 32 * kAttnWarps;  // keys per split
+constexpr int kAttnTilesPerWarp = 4;                           // 32-key tiles per warp per split
+constexpr int kAttnChunk = 32 * kAttnWarps * kAttnTilesPerWarp;  // keys per split
+__device__ __forceinline__ void att_cp16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void att_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void att_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void att_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void att_mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -217,31 +226,49 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
 #pragma unroll
     for (int i = 0; i < 4; ++i) o[n][i] = 0.f;
 
-  const int t0 = k_begin + warp * 32;
-  const int nvalid = max(0, min(32, ctx - t0));
-  if (nvalid > 0) {
-    // tile keys [t0, t0+32) lie in one page (t0 % 32 == 0, 64-token pages)
+  // keys [k_begin, k_end) in 32-key tiles, warp w takes tiles w, w + 4, ...; K and
+  // V of a tile are two cp.async groups: the next tile's K streams in under this
+  // tile's softmax and P.V, its V under the next Q K^T (online softmax per warp)
+  const int k_end = min(ctx, k_begin + kAttnChunk);
+  const int ntiles = k_end > k_begin ? (k_end - k_begin + 31) / 32 : 0;
+  uint8_t* kb = sk[warp];
+  uint8_t* vb = sv[warp];
+  auto tile_src = [&](int t, const __nv_bfloat16* c) {
+    const int t0 = k_begin + t * 32;  // 32 keys inside one 64-token page
     const int page = block_table[(size_t)slot * pages_per_seq + t0 / kPageTokens];
-    const size_t base = (((size_t)page * nkv + kh) * kPageTokens + (t0 % kPageTokens)) * HD;
-    const uint4* kg = reinterpret_cast<const uint4*>(kc + base);
-    const uint4* vg = reinterpret_cast<const uint4*>(vc + base);
-    uint4 kr[V4], vr[V4];
-#pragma unroll
-    for (int i = 0; i < V4; ++i) {  // 32 rows x V4 uint4, lane-strided: coalesced
-      const int e = lane + 32 * i, r = e / V4;
-      kr[i] = make_uint4(0u, 0u, 0u, 0u);
-      vr[i] = make_uint4(0u, 0u, 0u, 0u);  // rows past the context stay 0 (0 x NaN is NaN)
-      if (r < nvalid) { kr[i] = __ldg(kg + e); vr[i] = __ldg(vg + e); }
-    }
+    return reinterpret_cast<const uint4*>(c + (((size_t)page * nkv + kh) * kPageTokens + (t0 % kPageTokens)) * HD);
+  };
+  auto load_k = [&](int t) {
+    const int nv = min(32, k_end - (k_begin + t * 32));
+    const uint4* g = tile_src(t, kc);
 #pragma unroll
     for (int i = 0; i < V4; ++i) {
       const int e = lane + 32 * i, r = e / V4, c = e % V4;
-      *reinterpret_cast<uint4*>(&sk[warp][r * ROW + c * 16]) = kr[i];
-      *reinterpret_cast<uint4*>(&sv[warp][r * ROW + c * 16]) = vr[i];
+      if (r < nv) att_cp16(kb + r * ROW + c * 16, g + e);
     }
+    att_commit();
+  };
+  auto load_v = [&](int t) {
+    const int nv = min(32, k_end - (k_begin + t * 32));
+    const uint4* g = tile_src(t, vc);
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      const int e = lane + 32 * i, r = e / V4, c = e % V4;
+      if (r < nv) att_cp16(vb + r * ROW + c * 16, g + e);
+      else *reinterpret_cast<uint4*>(vb + r * ROW + c * 16) = make_uint4(0u, 0u, 0u, 0u);  // 0 x NaN is NaN
+    }
+    att_commit();
+  };
+  if (warp < ntiles) {
+    load_k(warp);
+    load_v(warp);
   }
-  __syncthreads();  // q tile and the warps' K/V tiles
-  if (nvalid > 0) {
+  __syncthreads();  // the q tile
+  for (int t = warp; t < ntiles; t += kAttnWarps) {
+    const int nvalid = min(32, k_end - (k_begin + t * 32));
+    const bool has_next = t + kAttnWarps < ntiles;
+    att_wait1();  // K(t) landed (V(t) may still be in flight)
+    __syncwarp();
     float sc[4][4];
 #pragma unroll
     for (int n = 0; n < 4; ++n)
@@ -257,11 +284,13 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
       a[3] = att_ld32(qa + 8 * QP + 8);
 #pragma unroll
       for (int n = 0; n < 4; ++n) {
-        const uint8_t* kp = &sk[warp][(n * 8 + (lane >> 2)) * ROW + (kk * 16 + (lane & 3) * 2) * 2];
+        const uint8_t* kp = kb + (n * 8 + (lane >> 2)) * ROW + (kk * 16 + (lane & 3) * 2) * 2;
         att_mma16816(sc[n], a, att_ld32(kp), att_ld32(kp + 16));
       }
     }
-    float mx_lo = -INFINITY, mx_hi = -INFINITY;
+    __syncwarp();
+    if (has_next) load_k(t + kAttnWarps);
+    float mx_lo = m_lo, mx_hi = m_hi;
 #pragma unroll
     for (int n = 0; n < 4; ++n)
 #pragma unroll
@@ -276,22 +305,35 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
       mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, off));
       mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, off));
     }
+    const float c_lo = m_lo == -INFINITY ? 0.f : __expf(m_lo - mx_lo);
+    const float c_hi = m_hi == -INFINITY ? 0.f : __expf(m_hi - mx_hi);
     m_lo = mx_lo;
     m_hi = mx_hi;
+    float sum_lo = 0.f, sum_hi = 0.f;
 #pragma unroll
     for (int n = 0; n < 4; ++n)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float pv = sc[n][i] == -INFINITY ? 0.f : __expf(sc[n][i] - (i < 2 ? m_lo : m_hi));
         sc[n][i] = pv;
-        if (i < 2) l_lo += pv;
-        else l_hi += pv;
+        if (i < 2) sum_lo += pv;
+        else sum_hi += pv;
       }
 #pragma unroll
     for (int off = 1; off <= 2; off <<= 1) {
-      l_lo += __shfl_xor_sync(0xffffffffu, l_lo, off);
-      l_hi += __shfl_xor_sync(0xffffffffu, l_hi, off);
+      sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, off);
+      sum_hi += __shfl_xor_sync(0xffffffffu, sum_hi, off);
     }
+    l_lo = l_lo * c_lo + sum_lo;
+    l_hi = l_hi * c_hi + sum_hi;
+#pragma unroll
+    for (int n = 0; n < NDT; ++n) {
+      o[n][0] *= c_lo; o[n][1] *= c_lo;
+      o[n][2] *= c_hi; o[n][3] *= c_hi;
+    }
+    if (has_next) att_wait1();  // V(t) landed (K(t + 4) may still be in flight)
+    else att_wait0();
+    __syncwarp();
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
       uint32_t ah[4], al[4];
@@ -302,7 +344,7 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
 #pragma unroll
       for (int n = 0; n < NDT; ++n) {
         uint32_t b0, b1;
-        const uint8_t* vp = &sv[warp][(ks * 16 + (lane & 15)) * ROW + n * 16];
+        const uint8_t* vp = vb + (ks * 16 + (lane & 15)) * ROW + n * 16;
         asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
                      : "=r"(b0), "=r"(b1)
                      : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(vp))));
@@ -310,6 +352,8 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
         att_mma16816(o[n], al, b0, b1);
       }
     }
+    __syncwarp();
+    if (has_next) load_v(t + kAttnWarps);
   }
   // combine the warps of this CTA (sm_acc aliases the K tiles: wait for all warps)
   __syncthreads();

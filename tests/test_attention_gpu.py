@@ -1,0 +1,48 @@
+"""The multi-kernel round's single-query paged GQA attention
+(decoder.cu attention_kernel, srl_kernel_attention_decode) against a plain
+PyTorch fp32 reference of the same op on random bf16 q / K / V: contexts
+inside one 32-key tile, across tiles, across the 512-key splits (the merged
+split partials), page boundaries, GQA group sizes of the 0.5B (7), 1.5B (6)
+and 7B (7, hd 128) shapes.  Bar: 2e-3 relative to the output scale (the
+output is bf16; P enters the P.V product as hi + lo bf16 halves)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2509_19128_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("nq,nkv,hd", [(14, 2, 64), (12, 2, 128), (28, 4, 128)])
+def test_attention_decode_matches_torch(cuda, nq, nkv, hd):
+    g = torch.Generator(device="cuda").manual_seed(nq * hd)
+    ctxs = [1, 5, 31, 32, 33, 64, 65, 511, 512, 513, 1100, 2047, 4100]
+    rows = len(ctxs)
+    pps = (max(ctxs) + 63) // 64
+    # pages of slot r are a permutation (paged, not contiguous)
+    perm = torch.randperm(rows * pps, generator=g, device="cuda").to(torch.int32)
+    bt = perm.view(rows, pps).contiguous()
+    kc = (torch.randn(rows * pps, nkv, 64, hd, generator=g, device="cuda") * 0.5).to(torch.bfloat16)
+    vc = torch.randn(rows * pps, nkv, 64, hd, generator=g, device="cuda").to(torch.bfloat16)
+    q = torch.randn(rows, nq, hd, generator=g, device="cuda").to(torch.bfloat16)
+    slot = torch.arange(rows, dtype=torch.int32, device="cuda")
+    pos = torch.tensor([c - 1 for c in ctxs], dtype=torch.int32, device="cuda")
+    out = torch.empty(rows, nq, hd, dtype=torch.bfloat16, device="cuda")
+    _lib.call("srl_kernel_attention_decode", q.data_ptr(), kc.data_ptr(), vc.data_ptr(), bt.data_ptr(), pps,
+              slot.data_ptr(), pos.data_ptr(), rows, nq, nkv, hd, max(ctxs), out.data_ptr(), None)
+    torch.cuda.synchronize()
+    G = nq // nkv
+    scale = 1.0 / math.sqrt(hd)
+    for r, c in enumerate(ctxs):
+        pages = bt[r, :(c + 63) // 64].long()
+        K = kc[pages].float().permute(1, 0, 2, 3).reshape(nkv, -1, hd)[:, :c]  # [nkv, c, hd]
+        V = vc[pages].float().permute(1, 0, 2, 3).reshape(nkv, -1, hd)[:, :c]
+        qh = q[r].float().view(nkv, G, hd)
+        s = torch.einsum("kgd,kcd->kgc", qh, K) * scale
+        p = torch.softmax(s, -1)
+        ref = torch.einsum("kgc,kcd->kgd", p, V).reshape(nq, hd)
+        err = (out[r].float() - ref).abs().max().item()
+        assert err <= 2e-3 * max(1.0, ref.abs().max().item()), (c, err)

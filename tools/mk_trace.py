@@ -56,6 +56,7 @@ def analyse(meta, tr):
         r["bar"] = (np.median(st) - prev_last) if prev_last is not None else 0.0
         r["period"] = last - prev_last if prev_last is not None else last
         r["arrive"] = float(np.median(tr[p, :, 7][active] - tr[p, :, 3][active]))
+        r["spans"] = (tr[p, :, 7][active] - t0[p][active]).astype(np.float64)
         fields = ATTN_FIELDS if kind == "attn" else GEMM_FIELDS
         for k, name in fields:
             v = tr[p, :, k].copy()
@@ -84,6 +85,10 @@ def report(rows):
         fields = ATTN_FIELDS if k == "attn" else GEMM_FIELDS
         inner = " ".join(f"{name}={med(name):.0f}/{med(name + '_max'):.0f}" for _, name in fields
                          if not np.isnan(med(name)))
+        if k == "attn":  # per-CTA busy time in the phase: the work balance across SMs
+            spans = np.concatenate([x["spans"] for x in rs]) / 1e3
+            print(f"attn   per-CTA phase span (us): min {spans.min():.1f} median {np.median(spans):.1f} "
+                  f"p90 {np.percentile(spans, 90):.1f} max {spans.max():.1f}")
         print(f"{k:6s} n={len(rs):2d} cs={rs[0]['cs']:2d} items={rs[0]['items']:4d} "
               f"period={med('period'):6.0f} barrier={med('bar'):5.0f} arrive={med('arrive'):4.0f} | {inner}"
               f"  [sum period {sum(x['period'] for x in rs) / 1e3:.1f} us]")
@@ -95,6 +100,8 @@ def main():
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--prompt", type=int, default=64)
     ap.add_argument("--rounds", type=int, default=40)
+    ap.add_argument("--steady-gen", type=int, default=0,
+                    help="bench-like steady state: stream i already (i + 0.5)/B through a rollout of this length")
     ap.add_argument("--trace", default="gpurun_out/mk_trace.bin")
     ap.add_argument("--file", help="analyse an existing trace instead of running")
     a = ap.parse_args()
@@ -108,11 +115,13 @@ def main():
 
     cfg = PRESETS[a.config]
     pol = DecoderPolicy.random(cfg, seed=0, scale=0.02)
-    eng = Engine(pol, start_paused=True, max_streams=a.batch, max_seq_len=a.prompt + a.rounds + 8,
-                 rounds_per_sync=8, event_ring=64)
+    extra = [int((i + 0.5) * a.steady_gen / a.batch) for i in range(a.batch)] if a.steady_gen else [0] * a.batch
+    max_seq = a.prompt + max(extra) + a.rounds + 8
+    eng = Engine(pol, start_paused=True, max_streams=a.batch, max_seq_len=max_seq,
+                 rounds_per_sync=8, event_ring=64, prefill_budget=max(a.batch * (a.prompt + 1), max_seq))
     rng = np.random.default_rng(0)
     for i in range(a.batch):
-        eng.open_stream("p", a.rounds + 4, i, -1, rng.integers(0, cfg.vocab_size, a.prompt).tolist())
+        eng.open_stream("p", a.rounds + 4, i, -1, rng.integers(0, cfg.vocab_size, a.prompt + extra[i]).tolist())
     eng.advance(a.rounds)
     eng.profile_next_round()
     eng.advance(1)
