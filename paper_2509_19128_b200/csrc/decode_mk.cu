@@ -1225,9 +1225,23 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           csync();
           rows_ready = true;
         }
-        for (int i = first_item(c, F.rot, GR); i < F.n_items; i += GR) {
-          const int split = i % P.attn_splits;
-          const int rest = i / P.attn_splits;
+        // items are taken from a work queue (one counter per attention phase,
+        // after its split counters): item cost follows the row's context, so a
+        // static deal left CTAs idle at the phase barrier.  Every CTA makes
+        // exactly one failing grab, so a launch adds n_items + grid to the
+        // counter and (epoch x that) is this launch's base.  Split-major order:
+        // the full 1024-key splits first, partial and empty ones last.
+        unsigned* queue = P.tile_ctr + F.ctr_base + P.S * P.nkv;
+        const unsigned qbase = (ep1 - 1u) * (unsigned)(F.n_items + GR);
+        const int rowheads = P.S * P.nkv;
+        while (true) {
+          if (ct == 0) *s_flag = (int)(atomicAdd(queue, 1u) - qbase);
+          csync();
+          const int i = *s_flag;
+          csync();  // s_flag is reused inside the item
+          if (i >= F.n_items) break;
+          const int split = i / rowheads;
+          const int rest = i % rowheads;
           const long long a_c0 = clock64();
           mk_attention<HD, G>(P, F.layer, F.colv, F.cs, rest / P.nkv, rest % P.nkv, split, scratch, s_rows,
                               P.tile_ctr + F.ctr_base, ep1, P.ws, ct, s_flag, cbar, cph, tr);

@@ -410,7 +410,7 @@ int DecoderBackend::mega_init() {
   add(MK_EMBED, 0, S_, 1, 0, 0, 0, 0, 0);
   for (int l = 0; l < L; ++l) {
     add(MK_QKV, l, qkv_tiles * qkv_cs, qkv_cs, d_.qkv(), d_.H, 4 * l + 0, 0, 0);
-    add(MK_ATTN, l, S_ * d_.nkv * splits, qkv_cs, 0, 0, 0, 0, S_ * d_.nkv);
+    add(MK_ATTN, l, S_ * d_.nkv * splits, qkv_cs, 0, 0, 0, 0, S_ * d_.nkv + 1);  // + the work queue
     if (pairs)  // the pair reduces through DSMEM: no L2 partials, no counters
       add(MK_O, l, ((d_.H + 127) / 128) * 2, 2, d_.H, d_.qdim(), 4 * l + 1, 1, 0);
     else

@@ -3,8 +3,9 @@
 PyTorch fp32 reference of the same op on random bf16 q / K / V: contexts
 inside one 32-key tile, across tiles, across the 512-key splits (the merged
 split partials), page boundaries, GQA group sizes of the 0.5B (7), 1.5B (6)
-and 7B (7, hd 128) shapes.  Bar: 2e-3 relative to the output scale (the
-output is bf16; P enters the P.V product as hi + lo bf16 halves)."""
+and 7B (7, hd 128) shapes.  Bar: 5e-3 relative to the output scale -- the
+output is bf16 (half an ulp is 2^-9 of the value); P enters the P.V product
+as hi + lo bf16 halves, so the fp32 result itself is far closer."""
 import math
 
 import numpy as np
@@ -45,4 +46,5 @@ def test_attention_decode_matches_torch(cuda, nq, nkv, hd):
         p = torch.softmax(s, -1)
         ref = torch.einsum("kgc,kcd->kgd", p, V).reshape(nq, hd)
         err = (out[r].float() - ref).abs().max().item()
-        assert err <= 2e-3 * max(1.0, ref.abs().max().item()), (c, err)
+        # the output is bf16: half an ulp is 2^-9 relative, up to 3.9e-3 for values in [1, 2)
+        assert err <= 5e-3 * max(1.0, ref.abs().max().item()), (c, err)

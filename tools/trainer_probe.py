@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """One trainer step (IS-REINFORCE fwd + bwd + Adam) at a Qwen2.5 shape, for
 profiling: python tools/trainer_probe.py [--config qwen2.5-0.5b] [--seqs 64]
-[--len 321] [--steps 2]"""
+[--len 321] [--steps 2] [--fast]"""
 import argparse
 import sys
 from pathlib import Path
@@ -19,6 +19,7 @@ ap.add_argument("--config", default="qwen2.5-0.5b")
 ap.add_argument("--seqs", type=int, default=64)
 ap.add_argument("--len", type=int, default=321)
 ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--fast", action="store_true", help="single bf16 operands instead of the precise mode")
 a = ap.parse_args()
 cfg = PRESETS[a.config]
 pol = DecoderPolicy.random(cfg, seed=0, scale=0.02)
@@ -28,7 +29,7 @@ for i in range(a.seqs):
     toks = [cfg.bos_token] + rng.integers(0, cfg.vocab_size, size=a.len - 1).tolist()
     trajs.append(dict(tokens=toks, loss_begin=65, behavior_logprobs=[-12.0] * a.len,
                       advantages=[float(rng.standard_normal())] * a.len))
-tr = Trainer(pol, max_tokens=a.seqs * a.len)
+tr = Trainer(pol, max_tokens=a.seqs * a.len, precise=not a.fast)
 for s in range(a.steps):
     r = tr.step(trajs)
     tr.apply_adam(1e-6)
