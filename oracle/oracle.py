@@ -364,7 +364,7 @@ class Ref:
                      "ref_drift_checkpoints", "ref_mixed_policy_sample", "ref_fit_baseline",
                      "ref_is_reinforce_gradient", "ref_engine_lockstep", "ref_run_pipeline",
                      "ref_run_conventional", "ref_process_group_id", "ref_kl_per_position",
-                     "ref_search_configs"):
+                     "ref_search_configs", "ref_policy_wire"):
             getattr(L, name).restype = vp
         L.ref_free.argtypes = [vp]
         L.ref_random_recurrent_policy.argtypes = [C.c_int, C.c_int, f64, u64]
@@ -509,6 +509,11 @@ class Ref:
 
     def process_group_id(self, members):
         return self._s(self.L.ref_process_group_id(json.dumps(members).encode()), parse=False)
+
+    def policy_wire(self, doc: dict):
+        """The reference client's checksummed bytes of a policy document and their CRC-32."""
+        self.L.ref_policy_wire.argtypes = [C.c_char_p]
+        return self._s(self.L.ref_policy_wire(json.dumps(doc).encode()))
 
     def search_configs(self, spec: dict):
         """throughput::search_configs (throughput.cpp:288-330) of the reference."""

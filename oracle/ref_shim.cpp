@@ -358,6 +358,17 @@ char* ref_kl_per_position(const char* behavior_ckpts_json, int schedule_max_len,
   } catch (const std::exception& e) { return error_json(e); }
 }
 
+// The bytes EngineClient::request_weight_update checksums (protocol.cpp:340-356):
+// json::parse(policy_to_json(policy)).dump() of the policy the document
+// describes, and their crc32.
+char* ref_policy_wire(const char* policy_json) {
+  try {
+    const auto pol = rlmath::policy_from_json(policy_json);
+    const std::string bytes = json::parse(rlmath::policy_to_json(pol)).dump();
+    return dup(json{{"bytes", bytes}, {"crc32", proto::crc32(bytes)}}.dump());
+  } catch (const std::exception& e) { return error_json(e); }
+}
+
 // search_configs (throughput.cpp:288-330) on a JSON spec:
 // {n, train_batch, curve: [[h, u], ...], padding_window, tau,
 //  lengths: {kind: "uniform" | "constant" | "empirical", max_len, values}, cap, use_padding}

@@ -367,7 +367,13 @@ int DecoderBackend::mega_init() {
   DecoderRunner& r = *runner_;
   const int grid = r.sms;
   if (megakernel_occupancy(d_) < 1) return SRL_OK;  // not co-resident: multi-kernel round
-  const int L = d_.L, splits = (max_seq_ + kMkAttnChunk - 1) / kMkAttnChunk;
+  // keys per attention item (SRL_MK_ATTN_CHUNK: 64..2048, a multiple of 64)
+  static const int attn_chunk = [] {
+    const char* v = std::getenv("SRL_MK_ATTN_CHUNK");
+    const int c = v ? std::atoi(v) : kMkAttnChunk;
+    return std::max(64, std::min(2048, c / 64 * 64));
+  }();
+  const int L = d_.L, splits = (max_seq_ + attn_chunk - 1) / attn_chunk;
   // pair mode (SRL_MK_PAIRS=1): cluster of two CTAs, DSMEM split-K for QKV and
   // O, attention reads finished q / K / V
   const char* pe = std::getenv("SRL_MK_PAIRS");
@@ -480,7 +486,7 @@ int DecoderBackend::mega_init() {
     P = MkParams{};
     P.S = S_; P.H = d_.H; P.I = d_.I; P.V = d_.V; P.L = L; P.nq = d_.nq; P.nkv = d_.nkv;
     P.hd = d_.hd; P.qkv = d_.qkv(); P.parts = d_.ssq_parts(); P.pps = r.pages_per_seq;
-    P.attn_splits = splits; P.attn_chunk = kMkAttnChunk; P.greedy = opts_.greedy;
+    P.attn_splits = splits; P.attn_chunk = attn_chunk; P.greedy = opts_.greedy;
     P.eps = d_.eps; P.inv_h = 1.0f / (float)d_.H; P.scale = 1.0f / sqrtf((float)d_.hd);
     P.w = buf_[b]->w;
     P.wmaps = mk_.wmaps[b];
