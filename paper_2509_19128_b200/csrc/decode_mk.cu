@@ -31,7 +31,7 @@ constexpr int kPitch = kBN + 4;
 constexpr int kTileFloats = kTok * kBN;
 constexpr int kLmTile = 128;
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
-constexpr int kMaxSplitPages = 32;  // attention split <= 2048 keys
+constexpr int kMaxSplitPages = 128;  // attention split <= 8192 keys
 constexpr int kMaxCs = 16;          // split-K factor cap (reduce staging)
 #ifndef SRL_MK_KT128
 #define SRL_MK_KT128 16

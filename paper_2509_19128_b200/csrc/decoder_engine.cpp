@@ -367,11 +367,13 @@ int DecoderBackend::mega_init() {
   DecoderRunner& r = *runner_;
   const int grid = r.sms;
   if (megakernel_occupancy(d_) < 1) return SRL_OK;  // not co-resident: multi-kernel round
-  // keys per attention item (SRL_MK_ATTN_CHUNK: 64..2048, a multiple of 64)
+  // keys per attention item (SRL_MK_ATTN_CHUNK: 64..8192, a multiple of 64).  A
+  // 1.5B round at steady-state 8k contexts: 512 -> 4.59 ms, 1024 -> 3.75, 2048 ->
+  // 3.45 (the item's q / k / v prologue and split merge amortised over more keys)
   static const int attn_chunk = [] {
     const char* v = std::getenv("SRL_MK_ATTN_CHUNK");
     const int c = v ? std::atoi(v) : kMkAttnChunk;
-    return std::max(64, std::min(2048, c / 64 * 64));
+    return std::max(64, std::min(8192, c / 64 * 64));
   }();
   const int L = d_.L, splits = (max_seq_ + attn_chunk - 1) / attn_chunk;
   // pair mode (SRL_MK_PAIRS=1): cluster of two CTAs, DSMEM split-K for QKV and
