@@ -210,19 +210,8 @@ __device__ __forceinline__ double uniform_draw(uint64_t seed, uint64_t n) {
 // Attention item scratch: q, per-warp K/V tiles (cp.async), probabilities,
 // per-warp softmax state, the row's reduced q|k|v; the QKV split partials are
 // staged in the tile area first and the warp accumulators alias it last.
-// Attention groups per CTA: at hd 128 the 8 compute warps run as two groups
-// of 4 on two items at once, so one group's q / k / v prologue and split
-// merge (latency-bound) overlap the other group's key streaming
-// (SRL_MK_ATTN_GROUPS128=1: one group of 8).
-#ifndef SRL_MK_ATTN_GROUPS128
-#define SRL_MK_ATTN_GROUPS128 2
-#endif
-template <int HD>
-constexpr int attn_groups() { return HD == 128 ? SRL_MK_ATTN_GROUPS128 : 1; }
-
-template <int HD, int G, int NG = attn_groups<HD>()>
+template <int HD, int G>
 struct AttnSmem {
-  static constexpr int GW = kCW / NG;  // warps per group
   // keys per warp tile.  hd 128: 16-key tiles beside a 5-stage weight ring; 32-key
   // tiles need a 3-stage ring (SRL_MK_KT128=32 SRL_MK_STAGES128=3) -- measured at
   // 1.5B / 8k contexts: attention unchanged (4.05 vs 3.99 ms per round), the GEMM
@@ -235,15 +224,14 @@ struct AttnSmem {
                                    ? sizeof(__nv_bfloat16) * 16 * QP : sizeof(float) * G * HD;
   static constexpr size_t kbuf = (size_t)KT * ROW, vbuf = (size_t)KT * VROW;
   static constexpr size_t warp_bytes = kbuf + vbuf;
-  static constexpr size_t tiles = GW * warp_bytes;
+  static constexpr size_t tiles = kCW * warp_bytes;
   static constexpr size_t sp = 0;  // (probabilities stay in registers: mma.sync P.V)
-  static constexpr size_t sml = sizeof(float) * 2 * GW * G;
+  static constexpr size_t sml = sizeof(float) * 2 * kCW * G;
   static constexpr size_t spage = sizeof(int) * kMaxSplitPages;
   static constexpr size_t sraw = sizeof(float) * (G + 2) * HD;  // reduced q | k | v of the row
   static constexpr size_t snew = sizeof(__nv_bfloat16) * 2 * HD;  // the new token's k, v
-  static constexpr size_t group = (sq + tiles + sp + sml + spage + sraw + snew + 127) / 128 * 128;
-  static constexpr size_t total = NG * group;  // one region per group
-  static_assert(sizeof(float) * GW * G * HD <= tiles, "accumulators alias the tiles");
+  static constexpr size_t total = sq + tiles + sp + sml + spage + sraw + snew;
+  static_assert(sizeof(float) * kCW * G * HD <= tiles, "accumulators alias the tiles");
 };
 
 template <int HD, int G>
@@ -258,7 +246,7 @@ struct MkLayout {
   static constexpr size_t scratch =
       gemm_scr > att ? (gemm_scr > smp ? gemm_scr : smp) : (att > smp ? att : smp);
   static constexpr size_t bar = ring + scratch;
-  static constexpr size_t misc = bar + (2 * STAGES + 7) * 8;
+  static constexpr size_t misc = bar + (2 * STAGES + 6) * 8;
   static constexpr size_t rstd = misc + 32;
   static constexpr size_t rows = rstd + kTok * 4;  // round-constant (slot, pos) of every row
   static constexpr size_t total = rows + kTok * 8;
@@ -416,27 +404,18 @@ __device__ __forceinline__ void mk_epilogue(const MkParams& P, const MkPhase& ph
 //     the last-arriving split in split order (deterministic).
 template <int HD, int G>
 __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, int qkv_cs, int m, int kh, int split,
-                             uint8_t* scr_cta, const int2* s_rows, unsigned* ctr, unsigned ep1,
-                             float* ws, int ct_cta, int* s_flag, uint64_t* cbar, uint32_t& cph,
+                             uint8_t* scr, const int2* s_rows, unsigned* ctr, unsigned ep1,
+                             float* ws, int ct, int* s_flag, uint64_t* cbar, uint32_t& cph,
                              unsigned long long* tr) {
   using A = AttnSmem<HD, G>;
-  constexpr int NG = attn_groups<HD>(), GT = kCT / NG, GW = kCW / NG;
-  // this thread's group: its own smem region, barrier, flag and item
-  const int grp = NG == 1 ? 0 : ct_cta / GT;
-  const int ct = ct_cta - grp * GT;  // thread index within the group
-  uint8_t* scr = scr_cta + grp * A::group;
-  auto gsync = [grp]() {
-    if constexpr (NG == 1) csync();
-    else asm volatile("bar.sync %0, %1;" ::"r"(2 + grp), "r"(GT) : "memory");
-  };
   const long long c_start = clock64();
   constexpr int KT = A::KT, V4 = HD / 8, PER = KT * V4 / 32;
   constexpr int W = (G + 2) * HD;            // q heads | k | v of this kv head
-  constexpr int WPT = (W + GT - 1) / GT;   // of them per thread
+  constexpr int WPT = (W + kCT - 1) / kCT;   // of them per thread
   uint8_t* tiles = scr + A::sq;
   float(*sp)[G][32] = reinterpret_cast<float(*)[G][32]>(scr + A::sq + A::tiles);
   float(*sm_m)[G] = reinterpret_cast<float(*)[G]>(scr + A::sq + A::tiles + A::sp);
-  float(*sm_l)[G] = reinterpret_cast<float(*)[G]>(scr + A::sq + A::tiles + A::sp + sizeof(float) * GW * G);
+  float(*sm_l)[G] = reinterpret_cast<float(*)[G]>(scr + A::sq + A::tiles + A::sp + sizeof(float) * kCW * G);
   float* sraw = reinterpret_cast<float*>(scr + A::sq + A::tiles + A::sp + A::sml + A::spage);
   __nv_bfloat16* snew = reinterpret_cast<__nv_bfloat16*>(scr + A::sq + A::tiles + A::sp + A::sml +
                                                          A::spage + A::sraw);
@@ -460,17 +439,17 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   constexpr size_t rec = (size_t)G * (HD + 2);
   // split arrival; the last split to arrive merges the used ones in split order
   auto arrive_and_merge = [&]() {
-    gsync();
+    csync();
     if (ct == 0) {
       __threadfence();
       *s_flag = (atomicAdd(&ctr[m * nkv + kh], 1u) + 1u == ep1 * (unsigned)splits);
     }
-    gsync();
+    csync();
     if (*s_flag) {
       __threadfence();
       const float* base = ws + ((size_t)m * nkv + kh) * splits * rec;
       const int used = min(splits, (ctx + P.attn_chunk - 1) / P.attn_chunk);
-      for (int i = ct; i < G * HD; i += GT) {
+      for (int i = ct; i < G * HD; i += kCT) {
         const int g = i / HD, d = i % HD;
         float M = -INFINITY;
         for (int q = 0; q < used; ++q) M = fmaxf(M, __ldcg(&base[q * rec + g * (HD + 2)]));
@@ -484,7 +463,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
         P.attn[(size_t)m * nq * HD + (kh * G + g) * HD + d] = __float2bfloat16(L > 0.f ? Acc / L : 0.f);
       }
     }
-    gsync();
+    csync();
   };
   if (nkeys == 0) {  // a split past the context: no q / K / V work, only its arrival
     arrive_and_merge();
@@ -496,7 +475,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   // their loads are issued now, under the partials' L2 round trip
   const __nv_bfloat16* kc = P.kc + P.kv_layer_elems * layer;
   const __nv_bfloat16* vc = P.vc + P.kv_layer_elems * layer;
-  uint8_t* kb = tiles + (GW - 1 - warp) * A::warp_bytes;
+  uint8_t* kb = tiles + (kCW - 1 - warp) * A::warp_bytes;
   uint8_t* vb = kb + A::kbuf;
   // K and V of a tile travel as two cp.async groups, so the next tile's K
   // streams in while this tile's softmax and P.V run, and its V while the
@@ -533,15 +512,15 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   };
   auto tile_page = [&](int t) { return P.block_table[(size_t)slot * P.pps + (k0 + t * KT) / kPageTokens]; };
   const int free_slot0 = P.pairs ? 0 : (qkv_cs * W * 4 + (int)A::warp_bytes - 1) / (int)A::warp_bytes;
-  const bool early = warp < ntiles && GW - 1 - warp >= free_slot0;
+  const bool early = warp < ntiles && kCW - 1 - warp >= free_slot0;
   if (P.pairs) {
     if (early) load_tile(warp, P.block_table[(size_t)slot * P.pps + (k0 + warp * KT) / kPageTokens]);
     // pair mode: the QKV phase already wrote q (bf16, post-RoPE) and the new
     // token's K/V into the paged cache
     const __nv_bfloat16* qrow = P.q + (size_t)m * nq * HD + (size_t)kh * G * HD;
-    for (int i = ct; i < 16 * HD; i += GT)
+    for (int i = ct; i < 16 * HD; i += kCT)
       sqb[(i / HD) * A::QP + i % HD] = i < G * HD ? qrow[i] : __float2bfloat16(0.f);
-    gsync();
+    csync();
   } else {
   // ---- (1) operands: split partials (bulk), pages, bias, rope, rstd -- all in flight
   float* stage = reinterpret_cast<float*>(tiles);  // [qkv_cs][W], free until the K/V tiles
@@ -562,7 +541,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   float co[WPT], si[WPT];
 #pragma unroll
   for (int u = 0; u < WPT; ++u) {
-    const int idx = ct + u * GT;
+    const int idx = ct + u * kCT;
     bbits[u] = 0;
     co[u] = 1.f;
     si[u] = 0.f;
@@ -585,7 +564,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
 #pragma unroll
   for (int u = 0; u < WPT; ++u) bia[u] = __uint_as_float((unsigned)bbits[u] << 16);
   const float rstd = rsqrtf(ss * P.inv_h + P.eps);
-  for (int i = ct; i < (16 - G) * HD; i += GT)
+  for (int i = ct; i < (16 - G) * HD; i += kCT)
     sqb[(G + i / HD) * A::QP + i % HD] = __float2bfloat16(0.f);
   if (tr && ct == 0 && tr[1] == 0) tr[1] = clock64() - c_start;
   mk_wait(cbar, cph);
@@ -593,7 +572,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   if (tr && ct == 0 && tr[2] == 0) tr[2] = clock64() - c_start;
 #pragma unroll
   for (int u = 0; u < WPT; ++u) {
-    const int idx = ct + u * GT;
+    const int idx = ct + u * kCT;
     if (idx < W) {
       float v = 0.f;
 #pragma unroll 1
@@ -601,7 +580,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
       sraw[idx] = v * rstd + bia[u];
     }
   }
-  gsync();
+  csync();
   if (tr && ct == 0 && tr[5] == 0) tr[5] = clock64() - c_start;
   {
     const size_t at = (((size_t)cpage * nkv + kh) * kPageTokens + (pos % kPageTokens)) * HD;
@@ -609,7 +588,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
     __nv_bfloat16* vcw = P.vc + P.kv_layer_elems * layer;
 #pragma unroll
     for (int u = 0; u < WPT; ++u) {
-      const int idx = ct + u * GT;
+      const int idx = ct + u * kCT;
       if (idx >= W) continue;
       const int jj = idx % HD, base = idx - jj;
       float y;
@@ -632,7 +611,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
       }
     }
   }
-  gsync();
+  csync();
   }
 
   if (tr && ct == 0 && tr[11] == 0) tr[11] = clock64() - c_start;
@@ -646,11 +625,11 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
     for (int i = 0; i < 4; ++i) o[n][i] = 0.f;
   float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;  // heads lane/4, lane/4 + 8
   if (warp < ntiles && !early) load_tile(warp, tile_page(warp));
-  for (int t = warp; t < ntiles; t += GW) {
+  for (int t = warp; t < ntiles; t += kCW) {
     const int key0 = k0 + t * KT;
     const int nv = min(KT, k1 - key0);
-    const bool has_next = t + GW < ntiles;
-    const int next_page = has_next ? tile_page(t + GW) : 0;  // lookup latency under this tile
+    const bool has_next = t + kCW < ntiles;
+    const int next_page = has_next ? tile_page(t + kCW) : 0;  // lookup latency under this tile
     const bool new_key = !P.pairs && owner && pos >= key0 && pos < key0 + nv;
     cp_async_wait_1();  // pending: K(t), V(t) -> K(t) landed
     __syncwarp();
@@ -680,7 +659,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
       }
     }
     __syncwarp();  // every lane is done with K(t)
-    if (has_next) load_k(t + GW, next_page);
+    if (has_next) load_k(t + kCW, next_page);
     float mx_lo = m_lo, mx_hi = m_hi;
 #pragma unroll
     for (int n = 0; n < NKT; ++n)
@@ -745,7 +724,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
       }
     }
     __syncwarp();  // every lane is done with V(t)
-    if (has_next) load_v(t + GW, next_page);
+    if (has_next) load_v(t + kCW, next_page);
   }
 #pragma unroll
   for (int off = 1; off <= 2; off <<= 1) {
@@ -755,7 +734,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
 
   // ---- (3) merge the warps, then the splits
   if (tr && ct == 0 && tr[12] == 0) tr[12] = clock64() - c_start;
-  gsync();  // sm_acc aliases the tiles
+  csync();  // sm_acc aliases the tiles
   if (tr && ct == 0 && tr[13] == 0) tr[13] = clock64() - c_start;
   {
     const int h_lo = lane >> 2, h_hi = h_lo + 8;
@@ -770,16 +749,16 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
       if (h_hi < G) { sm_acc[warp][h_hi][d] = o[n][2]; sm_acc[warp][h_hi][d + 1] = o[n][3]; }
     }
   }
-  gsync();
+  csync();
   float* my_ws = ws + (((size_t)m * nkv + kh) * splits + split) * rec;
-  for (int i = ct; i < G * HD; i += GT) {
+  for (int i = ct; i < G * HD; i += kCT) {
     const int g = i / HD, d = i % HD;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < GW; ++w) M = fmaxf(M, sm_m[w][g]);
+    for (int w = 0; w < kCW; ++w) M = fmaxf(M, sm_m[w][g]);
     float L = 0.f, Acc = 0.f;
 #pragma unroll
-    for (int w = 0; w < GW; ++w) {
+    for (int w = 0; w < kCW; ++w) {
       const float a = (sm_m[w][g] == -INFINITY) ? 0.f : __expf(sm_m[w][g] - M);
       L += sm_l[w][g] * a;
       Acc += sm_acc[w][g][d] * a;
@@ -795,7 +774,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
     }
   }
   if (splits == 1) {
-    gsync();
+    csync();
     if (tr && ct == 0 && tr[14] == 0) tr[14] = clock64() - c_start;
     return;
   }
@@ -1061,7 +1040,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
   uint64_t* tempty = tfull + 2;
   uint64_t* cbar = tempty + 2;  // compute warps' bulk-copy barrier
   uint64_t* xbar = cbar + 1;    // pair phases: the partner CTA's partial rows have landed
-  uint64_t* cbar2 = cbar + 2;   // attention group 1's bulk-copy barrier
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Lo::misc);
   int* s_flag = reinterpret_cast<int*>(smem + Lo::misc + 4);
   int* s_seen = reinterpret_cast<int*>(smem + Lo::misc + 8);  // last phase seen complete
@@ -1088,7 +1066,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
       }
       mbar_init(cbar, 1);
       mbar_init(xbar, 1);
-      mbar_init(cbar2, 1);
       fence_barrier_init();
     }
     __syncwarp();
@@ -1207,7 +1184,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
     const int col = ct & (kBN - 1);      // accumulator lane (= output column) drained
     const int hf = cw >> 2;              // token half [32 hf, 32 hf + 32) drained
     uint32_t cph = 0;                    // cbar phase
-    uint32_t cph2 = 0;                   // cbar2 phase (attention group 1)
     uint32_t xph = 0;                    // xbar phase
     bool rows_ready = false;
     const bool stamp = P.stamps != nullptr && c == 0 && ct == 0;
@@ -1255,35 +1231,22 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
         // exactly one failing grab, so a launch adds n_items + grid to the
         // counter and (epoch x that) is this launch's base.  Split-major order:
         // the full 1024-key splits first, partial and empty ones last.
-        // With two attention groups each group takes its own items (its own
-        // flag, bulk-copy barrier and parity); a group makes one failing grab.
-        constexpr int NG = attn_groups<HD>(), GT = kCT / NG;
-        const int grp = NG == 1 ? 0 : ct / GT, gt = ct - grp * GT;
-        int* g_flag = grp == 0 ? s_flag : s_flag + 2;  // misc + 12 (s_seen is misc + 8)
-        uint64_t* g_cbar = grp == 0 ? cbar : cbar2;
-        uint32_t& g_cph = grp == 0 ? cph : cph2;
-        unsigned long long* g_tr = grp == 0 ? tr : nullptr;
         unsigned* queue = P.tile_ctr + F.ctr_base + P.S * P.nkv;
-        const unsigned qbase = (ep1 - 1u) * (unsigned)(F.n_items + NG * GR);
+        const unsigned qbase = (ep1 - 1u) * (unsigned)(F.n_items + GR);
         const int rowheads = P.S * P.nkv;
-        auto gsync = [grp]() {
-          if constexpr (NG == 1) csync();
-          else asm volatile("bar.sync %0, %1;" ::"r"(2 + grp), "r"(GT) : "memory");
-        };
         while (true) {
-          if (gt == 0) *g_flag = (int)(atomicAdd(queue, 1u) - qbase);
-          gsync();
-          const int i = *g_flag;
-          gsync();  // the flag is reused inside the item
+          if (ct == 0) *s_flag = (int)(atomicAdd(queue, 1u) - qbase);
+          csync();
+          const int i = *s_flag;
+          csync();  // s_flag is reused inside the item
           if (i >= F.n_items) break;
           const int split = i / rowheads;
           const int rest = i % rowheads;
           const long long a_c0 = clock64();
           mk_attention<HD, G>(P, F.layer, F.colv, F.cs, rest / P.nkv, rest % P.nkv, split, scratch, s_rows,
-                              P.tile_ctr + F.ctr_base, ep1, P.ws, ct, g_flag, g_cbar, g_cph, g_tr);
-          if (g_tr && gt == 0 && g_tr[10] == 0) g_tr[10] = clock64() - a_c0;
+                              P.tile_ctr + F.ctr_base, ep1, P.ws, ct, s_flag, cbar, cph, tr);
+          if (tr && ct == 0 && tr[10] == 0) tr[10] = clock64() - a_c0;
         }
-        csync();  // both groups done before the phase's arrival
       } else if (F.kind == MK_SAMPLE) {
         for (int s = first_item(c, F.rot, GR); s < F.n_items; s += GR) mk_sample(P, s, ct, scratch, tr);
       } else {
@@ -1524,7 +1487,7 @@ cudaError_t launch_t(const MkParams& p, int grid, cudaStream_t st) {
 
 template <int HD, int G>
 int qkv_cap_t() {
-  return (int)(AttnSmem<HD, G>::tiles / ((size_t)(G + 2) * HD * 4));  // one group's tile area
+  return (int)(AttnSmem<HD, G>::tiles / ((size_t)(G + 2) * HD * 4));
 }
 
 }  // namespace
