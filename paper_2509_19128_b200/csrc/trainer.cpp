@@ -10,10 +10,13 @@
 //      IS weights: w = min(c, exp(sum lp - sum mu)) per sequence, or per token
 //      coef_t = (1/m) * w * A_t  (m = number of trajectories, stop-gradient on w)
 //      pass 2: LM head again per row chunk -> dlogits = coef (onehot - softmax)
-//      backward through the layers (tcgen05 GEMMs on transposed operands for
-//      dX = dY W and dW = dY^T X, CUDA-core RMSNorm / SwiGLU / RoPE /
-//      attention backward) into one fp32 gradient buffer laid out like the
-//      weights -- the ascent direction of J, as in the reference.
+//      backward through the layers (tcgen05 GEMMs reading MN-major operands in
+//      place for dX = dY W and dW = dY^T X, the SwiGLU backward fused into the
+//      dact GEMM's epilogue, tensor-core (mma.sync) attention backward, per-row
+//      RMSNorm / RoPE backward) into one fp32 gradient buffer laid out like
+//      the weights -- the ascent direction of J, as in the reference.
+//  * precise mode (default): every activation and backward operand a bf16
+//    hi + lo pair (K-segmented GEMMs, split epilogues); fast mode: single bf16.
 //  * Adam on fp32 master weights writes the bf16 weights that the generator
 //    receives (ncclBroadcast payload).
 #include <algorithm>
