@@ -123,6 +123,9 @@ typedef struct {
   int32_t device;
   int32_t event_ring;      /* device event ring depth in rounds (>= rounds_per_sync) */
   int32_t prefill_budget;  /* max prompt tokens prefilled per round */
+  int32_t precise;         /* decoder: 1 = activations between the GEMMs as bf16 hi + lo pairs
+                              (only q / k / v and the K/V cache bf16; the multi-kernel round) --
+                              log-probs within 1e-3 of the fp64 oracle at every shape */
 } srl_engine_options;
 
 /* TokenEvent (engine.hpp:22-28); stream id "s<N>" is numeric N here. */

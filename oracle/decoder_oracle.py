@@ -71,15 +71,23 @@ def layout(cfg):
 class DecoderOracle:
     """fp64-accumulating decoder forward with a per-stream KV cache."""
 
-    def __init__(self, cfg: dict, weights_u16: np.ndarray, dtype=np.float64, exact: bool = False):
+    def __init__(self, cfg: dict, weights_u16: np.ndarray, dtype=np.float64, exact: bool = False,
+                 rounding: str = "device"):
         """exact=True drops the device's bf16 rounding points and fp32 storage
         of activations (every value fp64): the plain Qwen2 forward, the form
-        pinned against transformers' Qwen2ForCausalLM (tests/test_decoder_oracle.py)."""
+        pinned against transformers' Qwen2ForCausalLM (tests/test_decoder_oracle.py).
+        rounding="kv": the precise engine's rounding points only -- q, k, v
+        (the bf16 K/V cache and query operand); the normalised inputs, the
+        attention output and the SwiGLU output stay fp32 (the device carries
+        them as bf16 hi + lo pairs)."""
         self.cfg = cfg
         self.dtype = np.float64 if exact else dtype
         self.exact = exact
         self._f = np.float64 if exact else np.float32
         self._rnd = (lambda a: np.asarray(a, dtype=np.float64)) if exact else bf16_round
+        # rounding points of the activations between the GEMMs
+        self._rnd_act = (lambda a: np.asarray(a, dtype=np.float32)) if (rounding == "kv" and not exact) \
+            else self._rnd
         self.off, total = layout(cfg)
         w = np.asarray(weights_u16)
         if w.size < total:
@@ -113,7 +121,7 @@ class DecoderOracle:
         return 1.0 / np.sqrt(ssq / self.cfg["hidden"] + self.cfg["rms_eps"])
 
     def _xg(self, x, gain):
-        return self._rnd(x.astype(self._f) * gain.astype(self._f)).astype(self.dtype)
+        return self._rnd_act(x.astype(self._f) * gain.astype(self._f)).astype(self.dtype)
 
     def _rope(self, x, pos):
         """x: [..., hd] fp32 values at integer position pos (scalar or [rows])."""
@@ -165,7 +173,7 @@ class DecoderOracle:
                     s = K[:, kh, :] @ qs[h]
                     p = np.exp(s - s.max())
                     attn[r, h] = (p @ Vv[:, kh, :]) / p.sum()
-            attn = self._rnd(attn.reshape(rows, nq * hd)).astype(self.dtype)
+            attn = self._rnd_act(attn.reshape(rows, nq * hd)).astype(self.dtype)
             x = (x + attn @ w[f"{l}.o_w"].T).astype(self._f)
             xg = self._xg(x, w[f"{l}.ln2"])
             rstd = self._rstd(x)
@@ -173,7 +181,7 @@ class DecoderOracle:
             gu = gu.reshape(rows, I // 64, 2, 64)
             g, u = gu[:, :, 0, :].reshape(rows, I), gu[:, :, 1, :].reshape(rows, I)
             g32, u32 = g.astype(self._f), u.astype(self._f)
-            act = self._rnd(g32 / (self._f(1) + np.exp(-g32)) * u32).astype(self.dtype)
+            act = self._rnd_act(g32 / (self._f(1) + np.exp(-g32)) * u32).astype(self.dtype)
             x = (x + act @ w[f"{l}.down_w"].T).astype(self._f)
             nxt = w[f"{l + 1}.ln1"] if l + 1 < cfg["layers"] else w["final_norm"]
             xg = self._xg(x, nxt)

@@ -47,7 +47,7 @@ class DecoderConfigC(C.Structure):
 class EngineOptionsC(C.Structure):
     _fields_ = [("max_streams", i32), ("max_seq_len", i32), ("greedy", i32),
                 ("rounds_per_sync", i32), ("use_graphs", i32), ("device", i32),
-                ("event_ring", i32), ("prefill_budget", i32)]
+                ("event_ring", i32), ("prefill_budget", i32), ("precise", i32)]
 
 
 class TokenEventC(C.Structure):

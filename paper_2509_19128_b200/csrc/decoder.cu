@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
                      const int32_t* __restrict__ block_table, int pages_per_seq,
                      const __nv_bfloat16* __restrict__ kc, const __nv_bfloat16* __restrict__ vc,
                      float scale, float* __restrict__ ws, int* __restrict__ counters,
-                     __nv_bfloat16* __restrict__ out, float* __restrict__ lse_out) {
+                     __nv_bfloat16* __restrict__ out, float* __restrict__ lse_out, int out_lo) {
   // S = Q K^T and O = P V on the tensor cores (mma.sync m16n8k16): the G
   // query heads of the KV head are the A rows (padded to 16), each warp one
   // 32-key tile; P enters as hi + lo bf16 halves (fp32-class accuracy)
@@ -373,6 +373,13 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
   __syncthreads();
 
   constexpr size_t rec = (size_t)G * (HD + 2);
+  // out row stride nq HD + out_lo; split (out_lo > 0): lo = bf16(o - hi) at + out_lo
+  auto put_out = [&](int g, int d, float v) {
+    const size_t at = (size_t)m * (nq * HD + out_lo) + (kh * G + g) * HD + d;
+    const __nv_bfloat16 h = __float2bfloat16(v);
+    out[at] = h;
+    if (out_lo) out[at + out_lo] = __float2bfloat16(v - __bfloat162float(h));
+  };
   float* my_ws = ws + (((size_t)m * nkv + kh) * splits + split) * rec;
   for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
     const int g = i / HD, d = i % HD;
@@ -387,7 +394,7 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
       A += sm_acc[w][g][d] * a;
     }
     if (splits == 1) {
-      out[(size_t)m * nq * HD + (kh * G + g) * HD + d] = __float2bfloat16(L > 0.f ? A / L : 0.f);
+      put_out(g, d, L > 0.f ? A / L : 0.f);
       if (lse_out != nullptr && d == 0) lse_out[(size_t)m * nq + kh * G + g] = M + logf(L);
     } else {
       my_ws[g * (HD + 2) + 2 + d] = A;
@@ -418,7 +425,7 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
       L += __ldcg(&base[sp2 * rec + g * (HD + 2) + 1]) * a;
       A += __ldcg(&base[sp2 * rec + g * (HD + 2) + 2 + d]) * a;
     }
-    out[(size_t)m * nq * HD + (kh * G + g) * HD + d] = __float2bfloat16(L > 0.f ? A / L : 0.f);
+    put_out(g, d, L > 0.f ? A / L : 0.f);
     if (lse_out != nullptr && d == 0) lse_out[(size_t)m * nq + kh * G + g] = M + logf(L);
   }
   if (threadIdx.x == 0) counters[cidx] = 0;
@@ -959,7 +966,7 @@ template <int G, int HD>
 void attention_launch_t(dim3 grid, cudaStream_t st, const __nv_bfloat16* q, int nq, int nkv,
                         const RoundPlan& plan, const int32_t* bt, int pps, const __nv_bfloat16* kc,
                         const __nv_bfloat16* vc, float scale, float* ws, int* counters,
-                        __nv_bfloat16* out, float* lse_out) {
+                        __nv_bfloat16* out, float* lse_out, int out_lo) {
   constexpr size_t smem = attention_smem<G, HD>();
   static bool once = [] {
     cudaFuncSetAttribute(attention_kernel<G, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -969,17 +976,17 @@ void attention_launch_t(dim3 grid, cudaStream_t st, const __nv_bfloat16* q, int 
   (void)once;
   launch_pdl(attention_kernel<G, HD>, grid, dim3(32 * kAttnWarps), smem, st, dim3(1, 1, 1), q, nq,
              nkv, (const int32_t*)plan.row_slot, (const int32_t*)plan.row_pos, bt, pps, kc, vc,
-             scale, ws, counters, out, lse_out);
+             scale, ws, counters, out, lse_out, out_lo);
 }
 
 template <int HD>
 void attention_dispatch_g(int G, dim3 grid, cudaStream_t st, const __nv_bfloat16* q, int nq,
                           int nkv, const RoundPlan& plan, const int32_t* bt, int pps,
                           const __nv_bfloat16* kc, const __nv_bfloat16* vc, float scale, float* ws,
-                          int* counters, __nv_bfloat16* out, float* lse_out) {
+                          int* counters, __nv_bfloat16* out, float* lse_out, int out_lo) {
   switch (G) {
 #define SRL_ATTN_G(g) \
-  case g: attention_launch_t<g, HD>(grid, st, q, nq, nkv, plan, bt, pps, kc, vc, scale, ws, counters, out, lse_out); break;
+  case g: attention_launch_t<g, HD>(grid, st, q, nq, nkv, plan, bt, pps, kc, vc, scale, ws, counters, out, lse_out, out_lo); break;
     SRL_ATTN_G(1) SRL_ATTN_G(2) SRL_ATTN_G(3) SRL_ATTN_G(4)
     SRL_ATTN_G(5) SRL_ATTN_G(6) SRL_ATTN_G(7) SRL_ATTN_G(8)
 #undef SRL_ATTN_G
@@ -990,7 +997,7 @@ void attention_dispatch_g(int G, dim3 grid, cudaStream_t st, const __nv_bfloat16
 void launch_attention(const __nv_bfloat16* q, const DecoderDims& d, const RoundPlan& plan, int M,
                       const int32_t* block_table, int pages_per_seq, const __nv_bfloat16* kc,
                       const __nv_bfloat16* vc, int max_ctx, float* ws, int* counters,
-                      size_t ws_floats, __nv_bfloat16* out, cudaStream_t st, float* lse_out) {
+                      size_t ws_floats, __nv_bfloat16* out, cudaStream_t st, float* lse_out, int out_lo) {
   const int splits = attention_splits(d, M, max_ctx);
   (void)ws_floats;
   dim3 grid(M, d.nkv, splits);
@@ -998,10 +1005,10 @@ void launch_attention(const __nv_bfloat16* q, const DecoderDims& d, const RoundP
   const int G = d.nq / d.nkv;
   if (d.hd == 64)
     attention_dispatch_g<64>(G, grid, st, q, d.nq, d.nkv, plan, block_table, pages_per_seq, kc,
-                             vc, scale, ws, counters, out, lse_out);
+                             vc, scale, ws, counters, out, lse_out, out_lo);
   else
     attention_dispatch_g<128>(G, grid, st, q, d.nq, d.nkv, plan, block_table, pages_per_seq, kc,
-                              vc, scale, ws, counters, out, lse_out);
+                              vc, scale, ws, counters, out, lse_out, out_lo);
 }
 
 // Slot bookkeeping written by a one-thread kernel (values travel as kernel

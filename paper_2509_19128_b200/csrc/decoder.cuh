@@ -93,7 +93,8 @@ void launch_attention(const __nv_bfloat16* q, const DecoderDims& d, const RoundP
                       const int32_t* block_table, int pages_per_seq, const __nv_bfloat16* kc,
                       const __nv_bfloat16* vc, int max_ctx, float* ws, int* counters,
                       size_t ws_floats, __nv_bfloat16* out, cudaStream_t st,
-                      float* lse_out = nullptr /* [M x nq] natural-log LSE, for backward */);
+                      float* lse_out = nullptr /* [M x nq] natural-log LSE, for backward */,
+                      int out_lo = 0 /* > 0: out rows are [hi | lo] split pairs, lo at + out_lo */);
 size_t attention_ws_floats(const DecoderDims& d, int M, int max_ctx);
 
 // Gather the last row of each emitting slot (decode rounds use identity).

@@ -75,8 +75,12 @@ DecoderRunner::~DecoderRunner() {
 }
 
 int DecoderRunner::init(const DecoderDims& dims, const WeightLayout& layout, int slots, int max_seq,
-                        int m_max, int logits_rows, int device, cudaStream_t st) {
+                        int m_max, int logits_rows, int device, cudaStream_t st, bool precise_mode) {
   d = dims;
+  precise = precise_mode;
+  sp = precise ? 2 : 1;
+  if (precise && (d.H % 64 || d.I % 64 || d.qdim() % 64))
+    return fail(SRL_INVALID_ARGUMENT, "precise engine: every GEMM width a multiple of 64");
   lay = layout;  // offsets only (layers array owned by the weights object)
   S = slots;
   max_seq = max_seq;
@@ -101,11 +105,11 @@ int DecoderRunner::init(const DecoderDims& dims, const WeightLayout& layout, int
   int st2;
   const size_t n_pages = (size_t)S * pages_per_seq;
   kv_layer_elems = n_pages * d.nkv * kPageTokens * d.hd;
-  if ((st2 = alloc(&x, (size_t)M_max * H)) || (st2 = alloc(&xg, (size_t)M_max * H)) ||
+  if ((st2 = alloc(&x, (size_t)M_max * H)) || (st2 = alloc(&xg, (size_t)M_max * H * sp)) ||
       (st2 = alloc(&ssq, (size_t)M_max * parts)) || (st2 = alloc(&qkv, (size_t)M_max * d.qkv())) ||
-      (st2 = alloc(&q, (size_t)M_max * d.qdim())) || (st2 = alloc(&attn, (size_t)M_max * d.qdim())) ||
-      (st2 = alloc(&act, (size_t)M_max * d.I)) ||
-      (st2 = alloc(&xg_last, (size_t)this->logits_rows * H)) ||
+      (st2 = alloc(&q, (size_t)M_max * d.qdim())) || (st2 = alloc(&attn, (size_t)M_max * d.qdim() * sp)) ||
+      (st2 = alloc(&act, (size_t)M_max * d.I * sp)) ||
+      (st2 = alloc(&xg_last, (size_t)this->logits_rows * H * sp)) ||
       (st2 = alloc(&ssq_last, (size_t)this->logits_rows * parts)) ||
       (st2 = alloc(&logits, (size_t)this->logits_rows * d.V)) ||
       (st2 = alloc(&lse_max, (size_t)this->logits_rows * ((d.V + 127) / 128))) ||
@@ -125,10 +129,10 @@ int DecoderRunner::init(const DecoderDims& dims, const WeightLayout& layout, int
   // activation TMA maps (box 64 and box 128 rows)
   for (int b = 0; b < 2; ++b) {
     const uint32_t box = b == 0 ? 64 : 128;
-    xg_map[b] = make_tmap_bf16(xg, M_max, H, box);
-    attn_map[b] = make_tmap_bf16(attn, M_max, d.qdim(), box);
-    act_map[b] = make_tmap_bf16(act, M_max, d.I, box);
-    last_map[b] = make_tmap_bf16(xg_last, this->logits_rows, H, box);
+    xg_map[b] = make_tmap_bf16(xg, M_max, (uint64_t)H * sp, box);
+    attn_map[b] = make_tmap_bf16(attn, M_max, (uint64_t)d.qdim() * sp, box);
+    act_map[b] = make_tmap_bf16(act, M_max, (uint64_t)d.I * sp, box);
+    last_map[b] = make_tmap_bf16(xg_last, this->logits_rows, (uint64_t)H * sp, box);
   }
   // GEMM workspace: the largest split-K need over every row count we may launch
   size_t need = 0;
@@ -160,6 +164,16 @@ int DecoderRunner::init(const DecoderDims& dims, const WeightLayout& layout, int
 
 int DecoderRunner::gemm(const CUtensorMap& tw, const CUtensorMap* tx, int M, int N, int K,
                         const EpiParams& e) {
+  if (precise) {  // X rows [hi (K) | lo (K)]: two K segments into one accumulator (persistent kernel)
+    EpiParams es = e;
+    es.seg_kb = K / 64;
+    es.x_off1 = K;
+    int tok = gemm_big_tok(M, N, 2 * K, sms);
+    if (tok == 0) tok = 128;
+    const cudaError_t err = gemm_big_launch(tw, tx[1], M, N, 2 * K, tok, es, st_);
+    if (err != cudaSuccess) return cuda_fail(err, "gemm_big_launch (precise)");
+    return SRL_OK;
+  }
   static const bool lm_big = [] {
     const char* v = std::getenv("SRL_LM_BIG");
     return !(v && v[0] == '0');
@@ -184,6 +198,7 @@ int DecoderRunner::forward(int M, const __nv_bfloat16* w, const WeightMaps& wm) 
   const float inv_h = 1.0f / (float)H;
   tb(1);
   launch_embed(w + lay.embed, w + lay.layers[0].ln1, plan.row_token, M, H, d.V, x, xg, ssq, st_);
+  if (precise) launch_split_bf16(x, M, H, nullptr, w + lay.layers[0].ln1, xg, st_);  // xg = split(x * ln1)
   te();
   int st;
   for (int l = 0; l < d.L; ++l) {
@@ -218,32 +233,34 @@ int DecoderRunner::forward(int M, const __nv_bfloat16* w, const WeightMaps& wm) 
           SRL_CUDA(cudaStreamWaitEvent(side_, fork_, 0));
         }
         launch_attention(q, d, plan, n_single, block_table, pages_per_seq, kcl, vcl, max_seq, attn_ws,
-                         attn_counters, attn_ws_floats, attn, side ? side_ : st_);
+                         attn_counters, attn_ws_floats, attn, side ? side_ : st_, nullptr,
+                         precise ? d.qdim() : 0);
         if (side) SRL_CUDA(cudaEventRecord(join_, side_));
       }
       SRL_CUDA(launch_attention_fwd_mma(q, kcl, vcl, seg, seg + S, block_table, pages_per_seq, n_seg, d.nq,
                                         d.nkv, d.hd, attn, nullptr, st_, seg + 2 * S, seg + 3 * S,
-                                        seg_max_rows));
+                                        seg_max_rows, precise ? d.qdim() : 0));
       if (side) SRL_CUDA(cudaStreamWaitEvent(st_, join_, 0));
     } else {
       launch_attention(q, d, plan, M, block_table, pages_per_seq, kcl, vcl, max_seq, attn_ws,
-                       attn_counters, attn_ws_floats, attn, st_);
+                       attn_counters, attn_ws_floats, attn, st_, nullptr, precise ? d.qdim() : 0);
     }
     te();
     EpiParams r;
     r.kind = EPI_RESID; r.resid = x; r.gain = w + o.ln2; r.xg = xg; r.ssq_out = ssq;
+    r.lo_off = precise ? H : 0;
     tb(5);
     if ((st = gemm(wm.o[l], attn_map, M, H, d.qdim(), r))) return st;
     te();
     EpiParams g;
     g.kind = EPI_SWIGLU;
     g.ssq_in = ssq; g.ssq_in_parts = parts; g.inv_dim = inv_h; g.eps = d.eps;
-    g.out_bf16 = act; g.ld_bf16 = d.I;
+    g.out_bf16 = act; g.ld_bf16 = d.I * sp; g.lo_off = precise ? d.I : 0;
     tb(6);
     if ((st = gemm(wm.gate_up[l], xg_map, M, 2 * d.I, H, g))) return st;
     te();
     EpiParams r2;
-    r2.kind = EPI_RESID; r2.resid = x; r2.xg = xg; r2.ssq_out = ssq;
+    r2.kind = EPI_RESID; r2.resid = x; r2.xg = xg; r2.ssq_out = ssq; r2.lo_off = precise ? H : 0;
     r2.gain = w + (l + 1 < d.L ? lay.layers[l + 1].ln1 : lay.final_norm);
     tb(7);
     if ((st = gemm(wm.down[l], act_map, M, H, d.I, r2))) return st;
@@ -318,7 +335,7 @@ int DecoderBackend::init(const Policy& p) {
   }
   runner_ = std::make_unique<DecoderRunner>();
   if ((st = runner_->init(d_, buf_[0]->layout, S_, max_seq_, S_ + prefill_budget_, S_,
-                          opts_.device, st_)))
+                          opts_.device, st_, opts_.precise != 0)))
     return st;
   // slot state + ring + counters in one allocation
   const size_t ints = (size_t)S_ * 6 + 4;
@@ -367,6 +384,7 @@ int DecoderBackend::mega_init() {
   DecoderRunner& r = *runner_;
   const int grid = r.sms;
   if (megakernel_occupancy(d_) < 1) return SRL_OK;  // not co-resident: multi-kernel round
+  if (opts_.precise) return SRL_OK;                  // precise engine: the multi-kernel round
   // keys per attention item (SRL_MK_ATTN_CHUNK: 64..8192, a multiple of 64).  A
   // 1.5B round at steady-state 8k contexts: 512 -> 4.59 ms, 1024 -> 3.75, 2048 ->
   // 3.45 (the item's q / k / v prologue and split merge amortised over more keys)
@@ -701,7 +719,7 @@ int DecoderBackend::prefill_round(int b, std::vector<int>& prefilled) {
   st = r.forward(M, buf_[b]->w, maps_[b]);
   r.n_seg = 0;
   if (st) return st;
-  launch_gather_rows(r.xg, r.ssq, r.plan.last_row, S_, d_.H, d_.ssq_parts(), r.xg_last, r.ssq_last, st_);
+  launch_gather_rows(r.xg, r.ssq, r.plan.last_row, S_, d_.H * r.sp, d_.ssq_parts(), r.xg_last, r.ssq_last, st_);
   if ((st = r.lm_head(S_, maps_[b], true))) return st;
   launch_sample(r.logits, r.lse_max, r.lse_sum, d_.V, S_, r.plan, r.next, ss_, ring_,
                 round_ctr_dev_, version_dev_, opts_.greedy, st_);

@@ -64,12 +64,14 @@ struct DecoderRunner {
   int n_seg = 0, n_single = 0, seg_max_rows = 0;
   KernelTimer* timer = nullptr;  // set for a profiled round
   bool unfused_qkv = false;
+  bool precise = false;  // split (hi + lo) activations between the GEMMs
+  int sp = 1;            // 2 when precise: the split buffers are twice as wide
   void tb(int kind) { if (timer) timer->begin(kind); }
   void te() { if (timer) timer->end(); }
 
   ~DecoderRunner();
   int init(const DecoderDims& dims, const WeightLayout& layout, int slots, int max_seq, int m_max,
-           int logits_rows, int device, cudaStream_t st);
+           int logits_rows, int device, cudaStream_t st, bool precise_mode = false);
   int forward(int M, const __nv_bfloat16* w, const WeightMaps& wm);
   int lm_head(int rows, const WeightMaps& wm, bool gathered);
   int gemm(const CUtensorMap& tw, const CUtensorMap* tx, int M, int N, int K, const EpiParams& e);

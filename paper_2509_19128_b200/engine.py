@@ -81,11 +81,15 @@ class Engine:
     def __init__(self, policy, recompute_state: bool = False, start_paused: bool = False, *,
                  max_streams: int = 64, max_seq_len: int = 1024, greedy: bool = False,
                  rounds_per_sync: int = 8, use_graphs: bool = True, device: int = 0,
-                 event_ring: int = 64, prefill_budget: int = 4096):
+                 event_ring: int = 64, prefill_budget: int = 4096, precise: bool = False):
+        """precise (decoder policies): the activations between the GEMMs as bf16
+        hi + lo pairs on the multi-kernel round -- only q / k / v and the K/V
+        cache are bf16 -- for log-probs at the fp64 oracle's 1e-3 at every shape
+        (the default bf16 round sits at the bf16-flip floor)."""
         self._policy_ref = policy  # decoder weights are copied; keep the source alive anyway
         opts = _lib.EngineOptionsC(max_streams, max_seq_len, int(greedy), rounds_per_sync,
                                    int(use_graphs), device, max(event_ring, rounds_per_sync),
-                                   prefill_budget)
+                                   prefill_budget, int(precise))
         h = C.c_void_p()
         with NativePolicy(policy) as ph:
             st = _lib.lib().srl_engine_create(ph, int(recompute_state), int(start_paused),
