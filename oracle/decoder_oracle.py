@@ -190,6 +190,59 @@ class DecoderOracle:
             caches[r]["tokens"].append(int(tokens[r]))
         return (xg @ w["lm_head"].T) * rstd[:, None]
 
+    def prefill_fast(self, cache, tokens, chunk: int = 256):
+        """prefill() for one stream with the rows of each chunk batched (BLAS-3
+        instead of one matrix-vector product per token): the same operations,
+        dtypes and rounding points as step(), causal attention over the cache;
+        only the fp64 summation order of the products differs.  Returns the
+        logits of the last position."""
+        cfg, w = self.cfg, self.w
+        I = cfg["intermediate"]
+        nq, nkv, hd = cfg["q_heads"], cfg["kv_heads"], cfg["head_dim"]
+        G = nq // nkv
+        last = None
+        for c0 in range(0, len(tokens), chunk):
+            toks = np.asarray(tokens[c0:c0 + chunk])
+            rows = len(toks)
+            p0 = len(cache["tokens"])
+            pos = np.arange(p0, p0 + rows)
+            x = w["embed"][toks].astype(self._f)
+            xg = self._xg(x, w["0.ln1"])
+            rstd = self._rstd(x)
+            for l in range(cfg["layers"]):
+                qkv = ((xg @ w[f"{l}.qkv_w"].T) * rstd[:, None] + w[f"{l}.qkv_b"]).astype(self._f)
+                q = self._rnd(self._rope(qkv[:, :nq * hd].reshape(rows, nq, hd), pos))
+                k = self._rnd(self._rope(qkv[:, nq * hd:(nq + nkv) * hd].reshape(rows, nkv, hd), pos))
+                v = self._rnd(qkv[:, (nq + nkv) * hd:].reshape(rows, nkv, hd))
+                cache["k"][l].extend(list(k))
+                cache["v"][l].extend(list(v))
+                K = np.stack(cache["k"][l]).astype(np.float64)  # [T, nkv, hd]
+                Vv = np.stack(cache["v"][l]).astype(np.float64)
+                qs = (q.astype(self._f) * self.scale).astype(np.float64)  # [rows, nq, hd]
+                mask = np.arange(K.shape[0])[None, :] > pos[:, None]
+                attn = np.zeros((rows, nq, hd), dtype=np.float64)
+                for h in range(nq):
+                    kh = h // G
+                    sc = qs[:, h, :] @ K[:, kh, :].T  # [rows, T]
+                    sc = np.where(mask, -np.inf, sc)
+                    pr = np.exp(sc - sc.max(-1, keepdims=True))
+                    attn[:, h] = (pr @ Vv[:, kh, :]) / pr.sum(-1, keepdims=True)
+                attn = self._rnd_act(attn.reshape(rows, nq * hd)).astype(self.dtype)
+                x = (x + attn @ w[f"{l}.o_w"].T).astype(self._f)
+                xg = self._xg(x, w[f"{l}.ln2"])
+                rstd = self._rstd(x)
+                gu = ((xg @ w[f"{l}.gate_up_w"].T) * rstd[:, None]).reshape(rows, I // 64, 2, 64)
+                g32 = gu[:, :, 0, :].reshape(rows, I).astype(self._f)
+                u32 = gu[:, :, 1, :].reshape(rows, I).astype(self._f)
+                act = self._rnd_act(g32 / (self._f(1) + np.exp(-g32)) * u32).astype(self.dtype)
+                x = (x + act @ w[f"{l}.down_w"].T).astype(self._f)
+                nxt = w[f"{l + 1}.ln1"] if l + 1 < cfg["layers"] else w["final_norm"]
+                xg = self._xg(x, nxt)
+                rstd = self._rstd(x)
+            cache["tokens"].extend(int(t) for t in toks)
+            last = (xg[-1:] @ w["lm_head"].T) * rstd[-1:, None]
+        return last[0] if last is not None else None
+
     def prefill(self, cache, tokens):
         """Feed a whole prefix into one cache; returns logits of every position."""
         out = []
