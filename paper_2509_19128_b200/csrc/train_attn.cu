@@ -47,6 +47,15 @@ __device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t&
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = pack_bf16(x - hf.x, y - hf.y);
 }
+// B fragment (16 x 8, B[k][n]) from a row-major tile X[k][n] (n contiguous), pitch P
+// elements: ldmatrix .trans -- the transposed copy of the tile is not needed.
+__device__ __forceinline__ void frag_b_trans(uint32_t& b0, uint32_t& b1, const __nv_bfloat16* X, int P, int k0,
+                                             int n0, int lane) {
+  const __nv_bfloat16* p = X + (size_t)(k0 + (lane & 15)) * P + n0;
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+               : "=r"(b0), "=r"(b1)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+}
 __device__ __forceinline__ uint32_t ld32(const __nv_bfloat16* p) {
   return *reinterpret_cast<const uint32_t*>(p);
 }
@@ -172,11 +181,12 @@ struct BwdSmem {
   static constexpr size_t tile = sizeof(__nv_bfloat16) * kBlk * P;
   static constexpr size_t tileT = sizeof(__nv_bfloat16) * HD * kPadT;
   static constexpr size_t vec = sizeof(float) * kBlk;
-  // dkv: K, V, Q, Q^T, dO, dO^T, lse, D ; dq: Q, dO, K, K^T, V, lse, D
-  // (+ split: the lo halves of dO, and dO^T for dkv, after them)
-  static constexpr size_t dkv = 4 * tile + 2 * tileT + 2 * vec;
-  static constexpr size_t dq = 4 * tile + tileT + 2 * vec;
-  static constexpr size_t dkv_split = dkv + tile + tileT;
+  // dkv: K, V, Q, dO, lse, D ; dq: Q, dO, K, V, lse, D (+ split: the lo half of dO).
+  // The products that need a transposed operand read it with ldmatrix .trans,
+  // so no transposed tiles: two CTAs per SM at hd 128 even in split mode.
+  static constexpr size_t dkv = 4 * tile + 2 * vec;
+  static constexpr size_t dq = 4 * tile + 2 * vec;
+  static constexpr size_t dkv_split = dkv + tile;
   static constexpr size_t dq_split = dq + tile;
 };
 
@@ -197,12 +207,9 @@ __global__ void __launch_bounds__(kWarps * 32)
   __nv_bfloat16* Vs = reinterpret_cast<__nv_bfloat16*>(smem + S::tile);
   __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smem + 2 * S::tile);
   __nv_bfloat16* dOs = reinterpret_cast<__nv_bfloat16*>(smem + 3 * S::tile);
-  __nv_bfloat16* Qt = reinterpret_cast<__nv_bfloat16*>(smem + 4 * S::tile);
-  __nv_bfloat16* dOt = reinterpret_cast<__nv_bfloat16*>(smem + 4 * S::tile + S::tileT);
-  float* s_lse = reinterpret_cast<float*>(smem + 4 * S::tile + 2 * S::tileT);
+  float* s_lse = reinterpret_cast<float*>(smem + 4 * S::tile);
   float* s_D = s_lse + kBlk;
   __nv_bfloat16* dOl = reinterpret_cast<__nv_bfloat16*>(smem + S::dkv);
-  __nv_bfloat16* dOlt = reinterpret_cast<__nv_bfloat16*>(smem + S::dkv + S::tile);
 
   const int slot = blockIdx.y, kh = blockIdx.z;
   const int L = seq_len[slot], s0 = seq_start[slot];
@@ -246,21 +253,21 @@ __global__ void __launch_bounds__(kWarps * 32)
       const int qvalid = min(kBlk, L - q0);
       __syncthreads();  // previous tiles consumed
       if constexpr (kPipe) {
-        store_bf16<HD>(Qs, Qt, pq);
-        if constexpr (SPLIT) store_f32_split<HD>(dOs, dOt, dOl, dOlt, pd);
-        else store_f32<HD>(dOs, dOt, pd);
+        store_bf16<HD>(Qs, nullptr, pq);
+        if constexpr (SPLIT) store_f32_split<HD>(dOs, nullptr, dOl, nullptr, pd);
+        else store_f32<HD>(dOs, nullptr, pd);
         if (threadIdx.x < kBlk) {
           s_lse[threadIdx.x] = pl;
           s_D[threadIdx.x] = pD;
         }
       } else {
-        stage_bf16<HD>(Qs, Qt, qvalid, [&](int r) { return q + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+        stage_bf16<HD>(Qs, nullptr, qvalid, [&](int r) { return q + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
         if constexpr (SPLIT) {
           float4 v[kNvF<HD>];
           load_f32<HD>(v, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
-          store_f32_split<HD>(dOs, dOt, dOl, dOlt, v);
+          store_f32_split<HD>(dOs, nullptr, dOl, nullptr, v);
         } else {
-          stage_f32<HD>(dOs, dOt, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+          stage_f32<HD>(dOs, nullptr, qvalid, [&](int r) { return d_o + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
         }
         for (int r = threadIdx.x; r < kBlk; r += kWarps * 32) {
           s_lse[r] = r < qvalid ? lse[(size_t)(s0 + q0 + r) * nq + h] : 0.f;
@@ -336,14 +343,14 @@ __global__ void __launch_bounds__(kWarps * 32)
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           uint32_t b0, b1;
-          frag_b(b0, b1, dOt, kPadT, n * 8, ks * 16, lane);
+          frag_b_trans(b0, b1, dOs, P, ks * 16, n * 8, lane);
           mma16816(dv[n], ap, b0, b1);
           if constexpr (SPLIT) {
             mma16816(dv[n], apl, b0, b1);
-            frag_b(b0, b1, dOlt, kPadT, n * 8, ks * 16, lane);
+            frag_b_trans(b0, b1, dOl, P, ks * 16, n * 8, lane);
             mma16816(dv[n], ap, b0, b1);
           }
-          frag_b(b0, b1, Qt, kPadT, n * 8, ks * 16, lane);
+          frag_b_trans(b0, b1, Qs, P, ks * 16, n * 8, lane);
           mma16816(dk[n], ad, b0, b1);
           if constexpr (SPLIT) mma16816(dk[n], adl, b0, b1);
         }
@@ -381,8 +388,7 @@ __global__ void __launch_bounds__(kWarps * 32)
   __nv_bfloat16* dOs = reinterpret_cast<__nv_bfloat16*>(smem + S::tile);
   __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem + 2 * S::tile);
   __nv_bfloat16* Vs = reinterpret_cast<__nv_bfloat16*>(smem + 3 * S::tile);
-  __nv_bfloat16* Kt = reinterpret_cast<__nv_bfloat16*>(smem + 4 * S::tile);
-  float* s_lse = reinterpret_cast<float*>(smem + 4 * S::tile + S::tileT);
+  float* s_lse = reinterpret_cast<float*>(smem + 4 * S::tile);
   float* s_D = s_lse + kBlk;
   __nv_bfloat16* dOl = reinterpret_cast<__nv_bfloat16*>(smem + S::dq);
 
@@ -428,10 +434,10 @@ __global__ void __launch_bounds__(kWarps * 32)
     const int kvalid = min(kBlk, L - k0);
     __syncthreads();
     if constexpr (kPipe) {
-      store_bf16<HD>(Ks, Kt, pk);
+      store_bf16<HD>(Ks, nullptr, pk);
       store_bf16<HD>(Vs, nullptr, pv);
     } else {
-      stage_bf16<HD>(Ks, Kt, kvalid, [&](int r) { return page_row(kc, bt, pps, slot, k0 + r, nkv, kh, HD); });
+      stage_bf16<HD>(Ks, nullptr, kvalid, [&](int r) { return page_row(kc, bt, pps, slot, k0 + r, nkv, kh, HD); });
       stage_bf16<HD>(Vs, nullptr, kvalid, [&](int r) { return page_row(vc, bt, pps, slot, k0 + r, nkv, kh, HD); });
     }
     __syncthreads();
@@ -489,7 +495,7 @@ __global__ void __launch_bounds__(kWarps * 32)
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         uint32_t b0, b1;
-        frag_b(b0, b1, Kt, kPadT, n * 8, ks * 16, lane);
+        frag_b_trans(b0, b1, Ks, P, ks * 16, n * 8, lane);
         mma16816(dq[n], a, b0, b1);
         if constexpr (SPLIT) mma16816(dq[n], al, b0, b1);
       }
