@@ -78,8 +78,8 @@ def parse(argv=None):
     ap.add_argument("--no-trainer", action="store_true", help="skip the trainer-step measurement")
     ap.add_argument("--no-pipeline", action="store_true", help="skip the one-GPU PipelineRL loop")
     ap.add_argument("--no-extra", action="store_true", help="skip the 0.5B / 7B generator lines")
-    ap.add_argument("--extra", default="qwen2.5-0.5b:64:256,qwen2.5-7b:256:1024",
-                    help="extra generator configs name:batch:gen (N = 1)")
+    ap.add_argument("--extra", default="qwen2.5-0.5b:64:256,qwen2.5-7b:256:1024,qwen2.5-1.5b:64:8192:precise",
+                    help="extra generator configs name:batch:gen[:precise] (N = 1)")
     ap.add_argument("--train-seqs", type=int, default=64, help="trajectories per trainer step")
     ap.add_argument("--train-gen", type=int, default=256, help="generated tokens per trainer trajectory")
     ap.add_argument("--trainers", type=int, default=None, help="trainer ranks of the partition (N > 1)")
@@ -339,7 +339,7 @@ class _Raw:
 
 
 def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use_graphs=True,
-                      device=0, n_payloads=2, profile=True, lag=True):
+                      device=0, n_payloads=2, profile=True, lag=True, precise=False):
     """One generator GPU: constant batch B, an in-flight update every R rounds
     whose transfer into the standby buffer overlaps the decode rounds (a side
     stream), swap at the token boundary after them.  Returns the measurement
@@ -356,7 +356,7 @@ def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use
     max_seq = prompt + 1 + gen + 1
     eng = Engine(pol, start_paused=True, max_streams=B, max_seq_len=max_seq,
                  rounds_per_sync=R, event_ring=max(64, R), use_graphs=use_graphs, device=device,
-                 prefill_budget=max(B * (prompt + 1), max_seq))
+                 prefill_budget=max(B * (prompt + 1), max_seq), precise=precise)
     rng = np.random.default_rng(1234 + device)
     live = {}
     h2d = [0]
@@ -712,15 +712,20 @@ def main():
     if not args.no_extra:
         out["extra_configs"] = {}
         for spec in filter(None, args.extra.split(",")):
-            name, b, gen = spec.split(":")
+            name, b, gen, *mode = spec.split(":")
+            precise = bool(mode) and mode[0] == "precise"
             c = PRESETS[name]
             log(f"extra config {spec}")
             try:
                 e, p = generator_measure(c, B=int(b), prompt=args.prompt, gen=int(gen), R=R,
                                          steps=max(3, args.steps // 2), warmup=2, steady=True,
-                                         use_graphs=not args.no_graphs, device=local, n_payloads=1)
+                                         use_graphs=not args.no_graphs, device=local, n_payloads=1,
+                                         precise=precise)
                 del p
-                out["extra_configs"][f"{name}:{b}:{gen}"] = {
+                out["extra_configs"][spec] = {
+                    "note": ("precise engine: activations between the GEMMs as bf16 hi + lo pairs "
+                             "(multi-kernel round), log-probs within 1e-3 of the fp64 oracle")
+                            if precise else None,
                     "value": e["tokens"] / (e["dev_ms"] * 1e-3), "e2e": e["tokens"] / (e["wall_ms"] * 1e-3),
                     "ms_per_step": e["dev_ms"] / max(3, args.steps // 2),
                     "pause": e["pause"], "roofline": e.get("roofline"),
@@ -729,7 +734,10 @@ def main():
                     "roofline_tokens_per_s": e.get("roofline_tokens_per_s"),
                     "lag": e.get("lag"), "clocks": e["clocks"]}
             except Exception as ex:  # noqa: BLE001 -- an extra line must not sink the headline
-                out["extra_configs"][f"{name}:{b}:{gen}"] = {"error": f"{type(ex).__name__}: {ex}"}
+                out["extra_configs"][spec] = {
+                    "note": ("precise engine: activations between the GEMMs as bf16 hi + lo pairs "
+                             "(multi-kernel round), log-probs within 1e-3 of the fp64 oracle")
+                            if precise else None,"error": f"{type(ex).__name__}: {ex}"}
             torch.cuda.empty_cache()
     if not args.no_cpu_baseline:
         log("cpu baseline")
