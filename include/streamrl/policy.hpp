@@ -100,3 +100,7 @@ inline void TabularPolicy::validate() const { rlmath::validate(Policy{*this}); }
 inline void RecurrentToyPolicy::validate() const { rlmath::validate(Policy{*this}); }
 
 }  // namespace streamrl::rlmath
+
+#if __has_include(<json.hpp>)
+#include "streamrl/policy_json.hpp"  // policy_to_json / policy_from_json (policy.hpp:77-82)
+#endif

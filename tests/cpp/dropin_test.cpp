@@ -83,6 +83,25 @@ std::vector<proto::TokenEvent> drain(proto::Engine& e, const std::string& id, pr
   return out;
 }
 
+// policy documents (policy.hpp:77-82; test_rl_math.cpp:463-474 round trip): the
+// drop-in's policy_to_json / policy_from_json on the reference's documents
+void test_policy_documents(const json& g) {
+  for (const json* d : {&g.at("demo_scenario").at("v0"), &g.at("demo_scenario").at("v1"),
+                        &g.at("cross_module").at("checkpoints")[0]}) {
+    const Policy p = rlmath::policy_from_json(d->dump());
+    const Policy back = rlmath::policy_from_json(rlmath::policy_to_json(p));
+    CHECK(json::parse(rlmath::policy_to_json(back)) == json::parse(rlmath::policy_to_json(p)));
+    // the wire bytes of the reference client: crc32 over the compact dump
+    CHECK(proto::crc32(json::parse(rlmath::policy_to_json(p)).dump()) ==
+          proto::crc32(json::parse(rlmath::policy_to_json(policy_of(*d))).dump()));
+  }
+  check_throws<std::invalid_argument>([] { rlmath::policy_from_json(R"({"schema":"x","type":"tabular"})"); },
+                                      "unknown schema");
+  check_throws<std::invalid_argument>(
+      [] { rlmath::policy_from_json(R"({"schema":"streamrl.policy/1","type":"tabular","vocab_size":0,"context_order":0})"); },
+      "invalid policy");
+}
+
 // test_protocol.cpp:76-79, 132-144 (engine.cpp:257-291)
 void test_crc_and_groups(const json& g) {
   for (const auto& c : g.at("protocol").at("crc32")) CHECK(proto::crc32(c[0].get<std::string>()) == c[1].get<std::uint32_t>());
@@ -281,7 +300,8 @@ int main(int argc, char** argv) {
   std::ifstream f(argv[1]);
   const json g = json::parse(f);
   const std::vector<std::pair<const char*, std::function<void(const json&)>>> cases = {
-      {"crc_and_groups", test_crc_and_groups}, {"demo_scenario", test_demo_scenario},
+      {"crc_and_groups", test_crc_and_groups}, {"policy_documents", test_policy_documents},
+      {"demo_scenario", test_demo_scenario},
       {"rejection_safety", test_rejection_safety}, {"three_versions", test_three_versions},
       {"cross_module", test_cross_module}, {"engine_errors", test_engine_errors},
       {"rlmath", test_rlmath}, {"gradients", test_gradients}};

@@ -42,6 +42,7 @@ def test_dropin_headers_compile_and_fail_loudly_without_gpu(tmp_path):
         pytest.skip("GPU present: the gpu variant runs the full program")
     r = run(build(tmp_path))
     assert "[ok] crc_and_groups" in r.stdout  # host-only entry points
+    assert "[ok] policy_documents" in r.stdout  # document functions + host-side validate()
     assert "[FAIL] demo_scenario" in r.stdout and "no_device" in r.stderr
     assert r.returncode == 1
 
