@@ -403,7 +403,8 @@ def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(side):
                 e0.record(side)
-                # copy engines, not a copy kernel: the persistent megakernel holds every SM
+                # D2D cudaMemcpyAsync on the side stream: it advances in the gaps between the
+                # megakernel's rounds (which hold every SM); decode_stall_ms is its cost
                 _lib.call("srl_device_copy_async", ptr, src, n, side.cuda_stream)
                 e1.record(side)
         emitted = eng.advance(R)
@@ -489,8 +490,10 @@ def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use
         "transfer_ms": float(np.median([r["copy_ms"] for r in rec])),
         "transfer_gbs": nbytes / (float(np.median([r["copy_ms"] for r in rec])) * 1e-3) / 1e9,
         "payload_bytes": nbytes,
-        "transfer": "copy-engine D2D copy (cudaMemcpyAsync) into the standby buffer on a side "
-                    "stream, overlapped with the decode rounds (N = 1: the trainer shares the GPU)",
+        "transfer": "D2D cudaMemcpyAsync into the standby buffer on a side stream, overlapped with "
+                    "the decode rounds: it advances between rounds (the megakernel holds every SM), "
+                    "so transfer_ms spans the step and decode_stall_ms is what it costs decode "
+                    "(N = 1: the trainer shares the GPU; N > 1: ncclBroadcast over NVLink)",
     }
     if lag and consumed:
         # lag of every consumed sequence (sim.cpp:63-104), on the device

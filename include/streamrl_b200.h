@@ -413,8 +413,8 @@ int srl_kernel_attention_decode(const void* q, const void* kc, const void* vc, c
                                 int32_t pages_per_seq, const int32_t* row_slot, const int32_t* row_pos,
                                 int32_t rows, int32_t nq, int32_t nkv, int32_t hd, int32_t max_ctx, void* out,
                                 void* stream);
-/* Device-to-device copy on the copy engines (no SM: runs beside the decode
- * megakernel), e.g. a one-GPU update into the standby buffer. */
+/* Device-to-device cudaMemcpyAsync on the given stream, e.g. a one-GPU
+ * update into the standby buffer on a side stream while decode runs. */
 int srl_device_copy_async(void* dst, const void* src, size_t nbytes, void* stream);
 int srl_kernel_sample_logits(const float* logits, int32_t vocab, int32_t rows,
                              const uint64_t* seeds, const int32_t* draw_index, int32_t greedy,
