@@ -225,3 +225,18 @@ def test_wait_events_many_matches_per_stream_drain(cuda):
         assert c.logprob.tolist() == [e.logprob for e in evs] and c.position.tolist() == [e.position for e in evs]
         assert c.weight_version.tolist() == [e.weight_version for e in evs]
     eng.close()
+
+
+def test_poll_events_does_not_block(cuda):
+    """srl_engine_poll_events_many: a paused engine's fresh stream has nothing
+    queued -- polling returns at once (no events, still running) where
+    wait_events would block; after advance() the events arrive in order."""
+    g = GOLDEN["demo_scenario"]
+    eng = Engine(policy_from_dict(g["v0"]), start_paused=True, max_streams=4, max_seq_len=64)
+    sid = eng.open_stream("demo", 5, 7)
+    got = eng.wait_events_many([sid], columns=True, block=False)[sid]
+    assert len(got[0]) == 0 and got[1] == "running" and got[2]
+    eng.advance(5)
+    evs, reason, more = eng.wait_events_many([sid], columns=True, block=False)[sid]
+    assert evs.position.tolist() == [0, 1, 2, 3, 4]
+    eng.close()
