@@ -81,8 +81,8 @@ class WeightChannel:
             import torch
 
             n = engine.standby_bytes() if hasattr(engine, "standby_bytes") else standby_view.numel()
-            standby_view = torch.empty(n, dtype=torch.uint8, device=standby_view.device
-                                       if standby_view is not None else "cpu")
+            dev = standby_view.device if standby_view is not None else getattr(engine, "device", "cpu")
+            standby_view = torch.empty(n, dtype=torch.uint8, device=dev)  # the collective's device
         if rank == self.src and payload is not None and payload.data_ptr() != standby_view.data_ptr():
             standby_view.copy_(payload)
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
