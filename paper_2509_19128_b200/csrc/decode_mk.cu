@@ -424,8 +424,8 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   const int warp = ct >> 5, lane = ct & 31;
   const int splits = P.attn_splits, nq = P.nq, nkv = P.nkv;
   const int slot = s_rows[m].x;
-  if (slot < 0) {  // every split still arrives: the counters are monotonic
-    if (splits > 1 && ct == 0) atomicAdd(&ctr[m * nkv + kh], 1u);
+  if (slot < 0) {  // a free slot: split 0 arrives for all of its splits (monotonic counters)
+    if (splits > 1 && split == 0 && ct == 0) atomicAdd(&ctr[m * nkv + kh], (unsigned)splits);
     return;
   }
   const int pos = s_rows[m].y;  // position of the new token; ctx = pos + 1 keys
@@ -437,12 +437,15 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   const bool owner = pos >= k0 && pos < k0 + P.attn_chunk;  // this split holds the new key
   const int qend = nq * HD, kend = qend + nkv * HD;
   constexpr size_t rec = (size_t)G * (HD + 2);
-  // split arrival; the last split to arrive merges the used ones in split order
+  // split arrival; the last split to arrive merges the used ones in split order.
+  // The split holding the new key (the row's last non-empty one) arrives for
+  // itself and for every empty split after it, which then do nothing at all.
+  const unsigned weight = owner ? (unsigned)(splits - split) : 1u;
   auto arrive_and_merge = [&]() {
     csync();
     if (ct == 0) {
       __threadfence();
-      *s_flag = (atomicAdd(&ctr[m * nkv + kh], 1u) + 1u == ep1 * (unsigned)splits);
+      *s_flag = (atomicAdd(&ctr[m * nkv + kh], weight) + weight == ep1 * (unsigned)splits);
     }
     csync();
     if (*s_flag) {
@@ -465,10 +468,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
     }
     csync();
   };
-  if (nkeys == 0) {  // a split past the context: no q / K / V work, only its arrival
-    arrive_and_merge();
-    return;
-  }
+  if (nkeys == 0) return;  // a split past the context: the owner split arrived for it
 
   // K/V tiles: warp w streams tiles w, w + 8, ... into buffer slot 7 - w, so the
   // first tiles land in the slots the QKV partial staging does not alias and
@@ -809,6 +809,66 @@ __device__ void mk_embed(const MkParams& P, int m, int ct, float* red) {
   csync();
   for (int p = ct; p < P.parts; p += kCT)
     P.ssq[(size_t)m * P.parts + p] = red[p * 4] + red[p * 4 + 1] + red[p * 4 + 2] + red[p * 4 + 3];
+  csync();
+}
+
+// This round's attention items, longest first (one CTA, in the embed phase;
+// the plan of the round is P.next until the embed items copy it): the full
+// attn_chunk-key splits in split-major order, then the partial splits by key
+// count (descending), then the empty ones -- the work queue of every attention
+// phase hands them out in this order, so the phase ends on short items
+// instead of a full split started late.  sm: >= 2 n + 2 ints of scratch.
+__device__ void mk_attn_order(const MkParams& P, int ct, int* sm) {
+  const int rowheads = P.S * P.nkv, n = rowheads * P.attn_splits, chunk = P.attn_chunk;
+  int* cnt = sm;       // [n] keys of each item (-1: free slot)
+  int* part = sm + n;  // the partial items, index order
+  for (int i = ct; i < n; i += kCT) {
+    const int split = i / rowheads, m = (i % rowheads) / P.nkv;
+    int c = -1;
+    if (P.next.row_slot[m] >= 0) c = min(chunk, max(0, P.next.row_pos[m] + 1 - split * chunk));
+    cnt[i] = c;
+  }
+  csync();
+  if (ct < 32) {  // ballot compaction: full items into the order, partial ones into part[]
+    int nf = 0, np = 0;
+    const unsigned lower = (1u << ct) - 1u;
+    for (int b = 0; b < n; b += 32) {
+      const int i = b + ct;
+      const int c = i < n ? cnt[i] : -1;
+      const bool full = c == chunk, partial = c > 0 && c < chunk;
+      const unsigned mf = __ballot_sync(0xffffffffu, full), mp = __ballot_sync(0xffffffffu, partial);
+      if (full) P.attn_order[nf + __popc(mf & lower)] = i;
+      if (partial) part[np + __popc(mp & lower)] = i;
+      nf += __popc(mf);
+      np += __popc(mp);
+    }
+    if (ct == 0) {
+      sm[2 * n] = nf;
+      sm[2 * n + 1] = np;
+    }
+  }
+  csync();
+  const int nf = sm[2 * n], np = sm[2 * n + 1];
+  for (int j = ct; j < np; j += kCT) {  // rank of a partial item by key count, ties by index
+    const int c = cnt[part[j]];
+    int r = 0;
+    for (int k = 0; k < np; ++k) {
+      const int ck = cnt[part[k]];
+      r += (ck > c) || (ck == c && k < j);
+    }
+    P.attn_order[nf + r] = part[j];
+  }
+  if (ct < 32) {  // empty splits and free slots last
+    int ne = 0;
+    const unsigned lower = (1u << ct) - 1u;
+    for (int b = 0; b < n; b += 32) {
+      const int i = b + ct;
+      const bool rest = i < n && cnt[i] <= 0;
+      const unsigned mr = __ballot_sync(0xffffffffu, rest);
+      if (rest) P.attn_order[nf + np + ne + __popc(mr & lower)] = i;
+      ne += __popc(mr);
+    }
+  }
   csync();
 }
 
@@ -1219,6 +1279,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
         if (c == 0 && ct == 0) *P.round_ctr += 1;
         for (int m = first_item(c, F.rot, GR); m < F.n_items; m += GR)
           mk_embed(P, m, ct, reinterpret_cast<float*>(scratch));
+        if (c == GR - 1) mk_attn_order(P, ct, reinterpret_cast<int*>(scratch + 8192));
       } else if (F.kind == MK_ATTN) {
         if (!rows_ready) {  // the round's plan, once per CTA
           for (int j = ct; j < P.S; j += kCT) s_rows[j] = make_int2(P.plan.row_slot[j], P.plan.row_pos[j]);
@@ -1229,17 +1290,18 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
         // after its split counters): item cost follows the row's context, so a
         // static deal left CTAs idle at the phase barrier.  Every CTA makes
         // exactly one failing grab, so a launch adds n_items + grid to the
-        // counter and (epoch x that) is this launch's base.  Split-major order:
-        // the full 1024-key splits first, partial and empty ones last.
+        // counter and (epoch x that) is this launch's base.  The queue position
+        // maps through attn_order (longest items first, built in the embed phase).
         unsigned* queue = P.tile_ctr + F.ctr_base + P.S * P.nkv;
         const unsigned qbase = (ep1 - 1u) * (unsigned)(F.n_items + GR);
         const int rowheads = P.S * P.nkv;
         while (true) {
           if (ct == 0) *s_flag = (int)(atomicAdd(queue, 1u) - qbase);
           csync();
-          const int i = *s_flag;
+          const int iq = *s_flag;
           csync();  // s_flag is reused inside the item
-          if (i >= F.n_items) break;
+          if (iq >= F.n_items) break;
+          const int i = __ldcg(P.attn_order + iq);  // longest first (mk_attn_order)
           const int split = i / rowheads;
           const int rest = i % rowheads;
           const long long a_c0 = clock64();

@@ -81,6 +81,7 @@ struct MkParams {
   unsigned* phase_done;         // [n_phases][8] monotonic arrival counters
   unsigned* epoch;              // rounds completed by this kernel (device scalar)
   unsigned* tile_ctr;           // split-K / split-KV arrival counters (monotonic)
+  int32_t* attn_order;          // this round's attention items, longest first (built in the embed phase)
   float* ws;                    // split-K and split-KV partials
   float* qkv_part;              // QKV split partials [S][nkv][cs][(G+2) hd] (reduced by attention)
   const MkPhase* phases;

@@ -475,7 +475,8 @@ int DecoderBackend::mega_init() {
   const size_t o_ph = 0, o_ly = al(o_ph + sizeof(MkPhase) * n), o_xm = al(o_ly + sizeof(MkLayer) * L),
                o_pd = al(o_xm + sizeof(CUtensorMap) * 3), o_ep = al(o_pd + 4 * 8 * (size_t)n)  /* room for 8 barrier lanes */,
                o_tc = al(o_ep + 4), o_st = al(o_tc + 4 * (size_t)std::max(ctr, 1)),
-               total = al(o_st + 8 * (size_t)(n + 1));
+               o_ao = al(o_st + 8 * (size_t)(n + 1)),
+               total = al(o_ao + 4 * (size_t)S_ * d_.nkv * splits);
   SRL_CUDA(cudaMalloc(&mk_.mem, total));
   SRL_CUDA(cudaMemset(mk_.mem, 0, total));
   SRL_CUDA(cudaMalloc(&mk_.ws, std::max<size_t>(ws, 1) * sizeof(float)));
@@ -523,6 +524,7 @@ int DecoderBackend::mega_init() {
     P.phase_done = reinterpret_cast<unsigned*>(base + o_pd);
     P.epoch = reinterpret_cast<unsigned*>(base + o_ep);
     P.tile_ctr = reinterpret_cast<unsigned*>(base + o_tc);
+    P.attn_order = reinterpret_cast<int32_t*>(base + o_ao);
     P.ws = mk_.ws;
     P.qkv_part = mk_.qkv_part;
     P.phases = reinterpret_cast<const MkPhase*>(base + o_ph);
