@@ -386,8 +386,10 @@ int DecoderBackend::mega_init() {
   if (megakernel_occupancy(d_) < 1) return SRL_OK;  // not co-resident: multi-kernel round
   if (opts_.precise) return SRL_OK;                  // precise engine: the multi-kernel round
   // keys per attention item (SRL_MK_ATTN_CHUNK: 64..8192, a multiple of 64).  A
-  // 1.5B round at steady-state 8k contexts: 512 -> 4.59 ms, 1024 -> 3.75, 2048 ->
-  // 3.45 (the item's q / k / v prologue and split merge amortised over more keys)
+  // 1.5B round at steady-state 8k contexts, items handed out longest first:
+  // 1024 -> 3.49 ms, 2048 -> 3.12, 4096 -> 2.88, 6144 -> 3.47, 8192 -> 3.95 (the
+  // item's q / k / v prologue and split merge amortised over more keys, until
+  // there are fewer items than SMs)
   static const int attn_chunk = [] {
     const char* v = std::getenv("SRL_MK_ATTN_CHUNK");
     const int c = v ? std::atoi(v) : kMkAttnChunk;
