@@ -459,8 +459,9 @@ def generator_measure(cfg, *, B, prompt, gen, R, steps, warmup, steady=True, use
     h2d0, d2h0 = h2d[0], d2h[0]
     torch.cuda.synchronize()
     rec = []
-    # NVTX range around the timed steps: `ncu --nvtx --nvtx-include "timed/"`
-    # lists exactly the launches of the timed region (not the setup prefill)
+    # NVTX range around the timed steps: `ncu --nvtx --nvtx-push-pop-scope process
+    # --nvtx-include "timed/"` lists exactly the launches of the timed region (the
+    # engine launches from its own thread, hence process scope; not the setup prefill)
     torch.cuda.nvtx.range_push("timed")
     for _ in range(steps):
         step(rec)
