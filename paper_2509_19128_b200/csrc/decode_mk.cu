@@ -252,6 +252,7 @@ struct MkLayout {
   static constexpr size_t total = rows + kTok * 8;
   static constexpr size_t alloc = total + 1024;
   static_assert(alloc <= 232448, "shared memory budget");
+  static_assert(scratch >= 8192 + (2 * (size_t)kMkMaxAttnItems + 2) * 4, "mk_attn_order scratch");
 };
 
 // ----------------------------------------------------------- compute ---
@@ -817,7 +818,8 @@ __device__ void mk_embed(const MkParams& P, int m, int ct, float* red) {
 // attn_chunk-key splits in split-major order, then the partial splits by key
 // count (descending), then the empty ones -- the work queue of every attention
 // phase hands them out in this order, so the phase ends on short items
-// instead of a full split started late.  sm: >= 2 n + 2 ints of scratch.
+// instead of a full split started late.  sm: >= 2 n + 2 ints of scratch
+// (n <= kMkMaxAttnItems: 32 KB at 8 KB into the scratch area).
 __device__ void mk_attn_order(const MkParams& P, int ct, int* sm) {
   const int rowheads = P.S * P.nkv, n = rowheads * P.attn_splits, chunk = P.attn_chunk;
   int* cnt = sm;       // [n] keys of each item (-1: free slot)

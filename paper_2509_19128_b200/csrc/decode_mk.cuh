@@ -24,6 +24,7 @@
 namespace srl {
 
 constexpr int kMkAttnChunk = 4096;  // keys per attention item (longer contexts split)
+constexpr int kMkMaxAttnItems = 4096;  // items of one attention phase (the order's scratch)
 
 enum MkKind : int { MK_EMBED = 0, MK_QKV = 1, MK_ATTN = 2, MK_O = 3, MK_GU = 4, MK_DOWN = 5,
                     MK_LM = 6, MK_SAMPLE = 7 };

@@ -390,11 +390,16 @@ int DecoderBackend::mega_init() {
   // 1024 -> 3.49 ms, 2048 -> 3.12, 4096 -> 2.88, 6144 -> 3.47, 8192 -> 3.95 (the
   // item's q / k / v prologue and split merge amortised over more keys, until
   // there are fewer items than SMs)
-  static const int attn_chunk = [] {
+  static const int chunk_env = [] {
     const char* v = std::getenv("SRL_MK_ATTN_CHUNK");
     const int c = v ? std::atoi(v) : kMkAttnChunk;
     return std::max(64, std::min(8192, c / 64 * 64));
   }();
+  // the per-round item order (mk_attn_order) keeps 2 ints per item in the
+  // scratch area: at most kMkMaxAttnItems items, so coarser splits if needed
+  int attn_chunk = chunk_env;
+  while ((size_t)S_ * d_.nkv * ((max_seq_ + attn_chunk - 1) / attn_chunk) > (size_t)kMkMaxAttnItems)
+    attn_chunk += 64;
   const int L = d_.L, splits = (max_seq_ + attn_chunk - 1) / attn_chunk;
   // pair mode (SRL_MK_PAIRS=1): cluster of two CTAs, DSMEM split-K for QKV and
   // O, attention reads finished q / K / V
