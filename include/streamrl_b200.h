@@ -413,6 +413,20 @@ int srl_kernel_attention_decode(const void* q, const void* kc, const void* vc, c
                                 int32_t pages_per_seq, const int32_t* row_slot, const int32_t* row_pos,
                                 int32_t rows, int32_t nq, int32_t nkv, int32_t hd, int32_t max_ctx, void* out,
                                 void* stream);
+/* Causal paged GQA attention over packed query segments (train_attn.cu
+ * attn_fwd_mma: the trainer's forward, a prefill round's prompt rows).
+ * Segment y: query rows seq_start[y] .. + seq_len[y] of q [T x nq x hd] at
+ * positions seg_pos0[y] .. (0 when null) of slot seg_slot[y] (y when null),
+ * attending to keys 0 .. its position from the slot's pages (caches
+ * [pages][nkv][64][hd] bf16, block_table [slots x pages_per_seq]); max_rows
+ * >= every seq_len.  out [T x (nq hd + out_lo)] bf16 (out_lo > 0: the
+ * rounding residual at + out_lo), lse [T x nq] (natural log of the scaled
+ * scores' partition sum; may be null).  hd 64 or 128. */
+int srl_kernel_attention_prefill(const void* q, const void* kc, const void* vc, const int32_t* block_table,
+                                 int32_t pages_per_seq, const int32_t* seq_start, const int32_t* seq_len,
+                                 const int32_t* seg_pos0, const int32_t* seg_slot, int32_t n_seg,
+                                 int32_t max_rows, int32_t nq, int32_t nkv, int32_t hd, void* out, float* lse,
+                                 int32_t out_lo, void* stream);
 /* Device-to-device cudaMemcpyAsync on the given stream, e.g. a one-GPU
  * update into the standby buffer on a side stream while decode runs. */
 int srl_device_copy_async(void* dst, const void* src, size_t nbytes, void* stream);

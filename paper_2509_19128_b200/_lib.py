@@ -133,6 +133,8 @@ SIGNATURES: dict[str, tuple] = {
     "srl_crc32": (C.c_uint32, [vp, sz]),
     "srl_process_group_id": (I, [P(cp), i32, cp, sz]),
     "srl_kernel_attention_decode": (I, [vp, vp, vp, vp, i32, vp, vp, i32, i32, i32, i32, i32, vp, vp]),
+    "srl_kernel_attention_prefill": (I, [vp, vp, vp, vp, i32, vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, vp,
+                                         i32, vp]),
     "srl_device_copy_async": (I, [vp, vp, sz, vp]),
     "srl_kernel_sample_logits": (I, [vp, i32, i32, vp, vp, i32, vp, vp, vp]),
     "srl_engine_profile_next_round": (I, [vp]),

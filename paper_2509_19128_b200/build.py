@@ -21,6 +21,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
           "--expt-relaxed-constexpr", "-I", str(HERE.parent / "include"), "-I", str(CSRC)]
+# tuning experiments only (e.g. SRL_NVCC_EXTRA="-DSRL_MK_KT128=32 -DSRL_MK_STAGES128=3" with -f)
+EXTRA = os.environ.get("SRL_NVCC_EXTRA", "").split()
 
 
 def _sources():
@@ -34,7 +36,7 @@ def _headers_mtime():
 
 
 def _compile(src: Path, obj: Path, verbose: bool):
-    cmd = [NVCC, *ARCH, *COMMON, "-c", str(src), "-o", str(obj)]
+    cmd = [NVCC, *ARCH, *COMMON, *EXTRA, "-c", str(src), "-o", str(obj)]
     if src.suffix == ".cu" and verbose:
         cmd[1:1] = ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

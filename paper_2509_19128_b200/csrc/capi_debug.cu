@@ -5,6 +5,7 @@
 
 #include "decoder.cuh"
 #include "gemm.cuh"
+#include "train.cuh"
 #include "streamrl_b200.h"
 
 using namespace srl;
@@ -141,6 +142,24 @@ extern "C" int srl_kernel_attention_decode(const void* q, const void* kc, const 
   cudaFreeAsync(ws, st);
   cudaFreeAsync(ctr, st);
   return cuda_status(cudaGetLastError());
+}
+
+// Causal multi-query attention over packed segments (train_attn.cu
+// attn_fwd_mma): the trainer's forward and a prefill round's prompt rows.
+extern "C" int srl_kernel_attention_prefill(const void* q, const void* kc, const void* vc,
+                                            const int32_t* block_table, int32_t pages_per_seq,
+                                            const int32_t* seq_start, const int32_t* seq_len,
+                                            const int32_t* seg_pos0, const int32_t* seg_slot, int32_t n_seg,
+                                            int32_t max_rows, int32_t nq, int32_t nkv, int32_t hd, void* out,
+                                            float* lse, int32_t out_lo, void* stream) {
+  if (!q || !kc || !vc || !block_table || !seq_start || !seq_len || !out || n_seg < 1 || max_rows < 1 ||
+      nkv < 1 || nq % nkv != 0 || (hd != 64 && hd != 128) || out_lo < 0 || pages_per_seq < 1)
+    return SRL_INVALID_ARGUMENT;
+  return cuda_status(launch_attention_fwd_mma(
+      static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(kc),
+      static_cast<const __nv_bfloat16*>(vc), seq_start, seq_len, block_table, pages_per_seq, n_seg, nq, nkv, hd,
+      static_cast<__nv_bfloat16*>(out), lse, static_cast<cudaStream_t>(stream), seg_pos0, seg_slot, max_rows,
+      out_lo));
 }
 
 // Device-to-device cudaMemcpyAsync on the caller's stream (e.g. a one-GPU

@@ -249,7 +249,13 @@ struct MkLayout {
   static constexpr size_t misc = bar + (2 * STAGES + 6) * 8;
   static constexpr size_t rstd = misc + 32;
   static constexpr size_t rows = rstd + kTok * 4;  // round-constant (slot, pos) of every row
-  static constexpr size_t total = rows + kTok * 8;
+  static constexpr size_t anx = rows + kTok * 8;     // attention lookahead mailbox (MkAnx, 64 B)
+  // the next attention item's QKV partials, bulk-copied by the lookahead warp
+  // while the current item finishes (hd 128; hd 64 has no room beside its
+  // 6-stage ring: its items stage the partials in the K/V buffers)
+  static constexpr size_t qpre = (anx + 64 + 127) & ~size_t(127);
+  static constexpr size_t qpre_bytes = HD == 128 ? 20480 : 0;
+  static constexpr size_t total = qpre + qpre_bytes;
   static constexpr size_t alloc = total + 1024;
   static_assert(alloc <= 232448, "shared memory budget");
   static_assert(scratch >= 8192 + (2 * (size_t)kMkMaxAttnItems + 2) * 4, "mk_attn_order scratch");
@@ -403,11 +409,51 @@ __device__ __forceinline__ void mk_epilogue(const MkParams& P, const MkPhase& ph
 //     online softmax (lane = key for scores, lane = dims for P.V);
 //  3. warps merged in shared memory; several splits (long contexts) merged by
 //     the last-arriving split in split order (deterministic).
+// Work queue of an attention phase: the next item (attn_order index) or -1
+// once the queue is drained.  next_item: ct 0 only.
+struct MkQueue {
+  unsigned* ctr;
+  unsigned base;
+  int n_items;
+  const int32_t* order;
+  __device__ __forceinline__ unsigned grab() const { return atomicAdd(ctr, 1u) - base; }
+  __device__ __forceinline__ int resolve(unsigned iq) const {
+    return iq < (unsigned)n_items ? __ldcg(order + iq) : -1;
+  }
+};
+// Every CTA makes exactly one failing grab per attention phase, so a launch
+// adds n_items + grid to the phase's counter: (epoch x that) is its base.
+__device__ __forceinline__ MkQueue mk_queue(const MkParams& P, const MkPhase& F, unsigned ep1, int grid) {
+  return MkQueue{P.tile_ctr + F.ctr_base + P.S * P.nkv, (ep1 - 1u) * (unsigned)(F.n_items + grid), F.n_items,
+                 P.attn_order};
+}
+
+// Attention lookahead mailbox (shared memory) between the compute warps and
+// the otherwise idle warp 3: when compute warp 0 starts its last key tile of
+// an item it posts a request; warp 3 takes the next queue item, resolves it,
+// loads the block-table pages of its first kCW x KT keys and the new key's
+// page, and (hd 128) bulk-copies its QKV partials into the qpre buffer on
+// cbar -- so the next item starts with its first K/V tiles issued at once and
+// its q operand one reduction away, instead of ~4 us of dependent round trips.
+struct MkAnx {
+  int req, done;    // request sequence (compute warp 0) / completed request (warp 3)
+  int item, bulk;   // resolved item (attn_order value, -1: queue drained); 1: partials issued on cbar
+  int cpage, phase; // the new key's page; the request's phase (-1: exit)
+  int pad[2];
+  int pages[8];     // pages of the item's first kCW x KT keys
+};
+static_assert(sizeof(MkAnx) == 64, "mailbox");
+
+// Returns true when the lookahead warp has taken the next queue item (in
+// *s_next); false on the early exits (the caller grabs).  pre: this item
+// was resolved by the lookahead warp (pages in the mailbox; partials already
+// in flight on cbar when anx->bulk).
 template <int HD, int G>
-__device__ void mk_attention(const MkParams& P, int layer, long long bias_off, int qkv_cs, int m, int kh, int split,
+__device__ bool mk_attention(const MkParams& P, int layer, long long bias_off, int qkv_cs, int m, int kh, int split,
                              uint8_t* scr, const int2* s_rows, unsigned* ctr, unsigned ep1,
                              float* ws, int ct, int* s_flag, uint64_t* cbar, uint32_t& cph,
-                             unsigned long long* tr) {
+                             unsigned long long* tr, MkAnx* anx, bool pre, float* qpre, int p, int& seq,
+                             int* s_next) {
   using A = AttnSmem<HD, G>;
   const long long c_start = clock64();
   constexpr int KT = A::KT, V4 = HD / 8, PER = KT * V4 / 32;
@@ -427,7 +473,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   const int slot = s_rows[m].x;
   if (slot < 0) {  // a free slot: split 0 arrives for all of its splits (monotonic counters)
     if (splits > 1 && split == 0 && ct == 0) atomicAdd(&ctr[m * nkv + kh], (unsigned)splits);
-    return;
+    return false;
   }
   const int pos = s_rows[m].y;  // position of the new token; ctx = pos + 1 keys
   const int ctx = pos + 1;
@@ -438,38 +484,18 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   const bool owner = pos >= k0 && pos < k0 + P.attn_chunk;  // this split holds the new key
   const int qend = nq * HD, kend = qend + nkv * HD;
   constexpr size_t rec = (size_t)G * (HD + 2);
-  // split arrival; the last split to arrive merges the used ones in split order.
-  // The split holding the new key (the row's last non-empty one) arrives for
-  // itself and for every empty split after it, which then do nothing at all.
+  // Split merge (deterministic, split order): the last split to arrive
+  // merges the used ones.  The split holding the new key (the row's last
+  // non-empty one) arrives for itself and for every empty split after it,
+  // which then do nothing at all; a row whose only split is split 0 writes
+  // its output directly.  Every round adds exactly `splits` per (row, kv
+  // head) counter (monotonic over epochs).  An owner-merges variant (the
+  // others leave without the atomic's round trip) measured far slower: with
+  // the longest items first, the short owner split waits for full splits
+  // still streaming (attention 64 -> 94 us per layer at 1.5B).
+  unsigned* my_ctr = &ctr[m * nkv + kh];
   const unsigned weight = owner ? (unsigned)(splits - split) : 1u;
-  auto arrive_and_merge = [&]() {
-    csync();
-    if (ct == 0) {
-      __threadfence();
-      *s_flag = (atomicAdd(&ctr[m * nkv + kh], weight) + weight == ep1 * (unsigned)splits);
-    }
-    csync();
-    if (*s_flag) {
-      __threadfence();
-      const float* base = ws + ((size_t)m * nkv + kh) * splits * rec;
-      const int used = min(splits, (ctx + P.attn_chunk - 1) / P.attn_chunk);
-      for (int i = ct; i < G * HD; i += kCT) {
-        const int g = i / HD, d = i % HD;
-        float M = -INFINITY;
-        for (int q = 0; q < used; ++q) M = fmaxf(M, __ldcg(&base[q * rec + g * (HD + 2)]));
-        float L = 0.f, Acc = 0.f;
-        for (int q = 0; q < used; ++q) {
-          const float ms = __ldcg(&base[q * rec + g * (HD + 2)]);
-          const float a = (ms == -INFINITY) ? 0.f : __expf(ms - M);
-          L += __ldcg(&base[q * rec + g * (HD + 2) + 1]) * a;
-          Acc += __ldcg(&base[q * rec + g * (HD + 2) + 2 + d]) * a;
-        }
-        P.attn[(size_t)m * nq * HD + (kh * G + g) * HD + d] = __float2bfloat16(L > 0.f ? Acc / L : 0.f);
-      }
-    }
-    csync();
-  };
-  if (nkeys == 0) return;  // a split past the context: the owner split arrived for it
+  if (nkeys == 0) return false;  // a split past the context: the owner split arrived for it
 
   // K/V tiles: warp w streams tiles w, w + 8, ... into buffer slot 7 - w, so the
   // first tiles land in the slots the QKV partial staging does not alias and
@@ -512,7 +538,10 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
     load_v(t, page);
   };
   auto tile_page = [&](int t) { return P.block_table[(size_t)slot * P.pps + (k0 + t * KT) / kPageTokens]; };
-  const int free_slot0 = P.pairs ? 0 : (qkv_cs * W * 4 + (int)A::warp_bytes - 1) / (int)A::warp_bytes;
+  const bool use_qpre = qpre != nullptr;  // partials in their own buffer: every warp's first tile loads early
+  const bool pre_bulk = pre && anx->bulk;
+  const int free_slot0 =
+      (P.pairs || use_qpre) ? 0 : (qkv_cs * W * 4 + (int)A::warp_bytes - 1) / (int)A::warp_bytes;
   const bool early = warp < ntiles && kCW - 1 - warp >= free_slot0;
   if (P.pairs) {
     if (early) load_tile(warp, P.block_table[(size_t)slot * P.pps + (k0 + warp * KT) / kPageTokens]);
@@ -524,8 +553,8 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
     csync();
   } else {
   // ---- (1) operands: split partials (bulk), pages, bias, rope, rstd -- all in flight
-  float* stage = reinterpret_cast<float*>(tiles);  // [qkv_cs][W], free until the K/V tiles
-  if (ct == 0) {  // the row's partials are contiguous: [m][kh][split][W]
+  float* stage = use_qpre ? qpre : reinterpret_cast<float*>(tiles);  // [qkv_cs][W]
+  if (ct == 0 && !pre_bulk) {  // the row's partials are contiguous: [m][kh][split][W]
     // (the writers fenced generic -> async proxy before their phase arrival)
     mbar_arrive_expect_tx(cbar, (uint32_t)(qkv_cs * W * 4));
     bulk_g2s(stage, P.qkv_part + ((size_t)m * nkv + kh) * qkv_cs * W, qkv_cs * W * 4, cbar);
@@ -534,8 +563,10 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   // every independent load first (one L2 round trip for all of them), the
   // consumers after: the early tile's page, the new token's page, the bias
   // (raw bf16 bits), RoPE cos / sin, the row's x^2 partials
-  const int page_early = early ? P.block_table[(size_t)slot * P.pps + (k0 + warp * KT) / kPageTokens] : 0;
-  const int cpage = P.block_table[(size_t)slot * P.pps + pos / kPageTokens];
+  const int page_early = !early ? 0
+                         : pre ? anx->pages[(warp * KT) / kPageTokens]
+                               : P.block_table[(size_t)slot * P.pps + (k0 + warp * KT) / kPageTokens];
+  const int cpage = pre ? anx->cpage : P.block_table[(size_t)slot * P.pps + pos / kPageTokens];
   constexpr int half = HD / 2;
   const unsigned short* bias = reinterpret_cast<const unsigned short*>(P.w + bias_off);
   unsigned short bbits[WPT];
@@ -632,6 +663,10 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
     const bool has_next = t + kCW < ntiles;
     const int next_page = has_next ? tile_page(t + kCW) : 0;  // lookup latency under this tile
     const bool new_key = !P.pairs && owner && pos >= key0 && pos < key0 + nv;
+    if (ct == 0 && !has_next && !(P.dbg & 2)) {  // last tiles: the lookahead warp resolves the next item
+      anx->phase = p;
+      st_release_cta(&anx->req, ++seq);
+    }
     cp_async_wait_1();  // pending: K(t), V(t) -> K(t) landed
     __syncwarp();
     if (new_key) {  // the new key from shared memory
@@ -752,6 +787,8 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
   }
   csync();
   float* my_ws = ws + (((size_t)m * nkv + kh) * splits + split) * rec;
+  // single-split rows (split 0 holds the new key) need no partials at all
+  const bool direct = splits == 1 || (owner && split == 0);
   for (int i = ct; i < G * HD; i += kCT) {
     const int g = i / HD, d = i % HD;
     float M = -INFINITY;
@@ -764,7 +801,7 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
       L += sm_l[w][g] * a;
       Acc += sm_acc[w][g][d] * a;
     }
-    if (splits == 1) {
+    if (direct) {
       P.attn[(size_t)m * nq * HD + (kh * G + g) * HD + d] = __float2bfloat16(L > 0.f ? Acc / L : 0.f);
     } else {
       __stcg(&my_ws[g * (HD + 2) + 2 + d], Acc);
@@ -774,12 +811,46 @@ __device__ void mk_attention(const MkParams& P, int layer, long long bias_off, i
       }
     }
   }
-  if (splits == 1) {
+  if (!direct) {
     csync();
-    if (tr && ct == 0 && tr[14] == 0) tr[14] = clock64() - c_start;
-    return;
+    if (ct == 0) {
+      __threadfence();
+      *s_flag = (atomicAdd(my_ctr, weight) + weight == ep1 * (unsigned)splits);
+    }
+    csync();
+    if (*s_flag) {  // last to arrive: merge the used splits in split order
+      __threadfence();
+      const float* base = ws + ((size_t)m * nkv + kh) * splits * rec;
+      const int used = min(splits, (ctx + P.attn_chunk - 1) / P.attn_chunk);
+      for (int i = ct; i < G * HD; i += kCT) {
+        const int g = i / HD, d = i % HD;
+        float M = -INFINITY;
+        for (int q = 0; q < used; ++q) M = fmaxf(M, __ldcg(&base[q * rec + g * (HD + 2)]));
+        float L = 0.f, Acc = 0.f;
+        for (int q = 0; q < used; ++q) {
+          const float ms = __ldcg(&base[q * rec + g * (HD + 2)]);
+          const float a = (ms == -INFINITY) ? 0.f : __expf(ms - M);
+          L += __ldcg(&base[q * rec + g * (HD + 2) + 1]) * a;
+          Acc += __ldcg(&base[q * rec + g * (HD + 2) + 2 + d]) * a;
+        }
+        P.attn[(size_t)m * nq * HD + (kh * G + g) * HD + d] = __float2bfloat16(L > 0.f ? Acc / L : 0.f);
+      }
+    }
+  } else if (splits > 1 && ct == 0) {  // nobody waits on this arrival
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(my_ctr), "r"(weight) : "memory");
   }
-  arrive_and_merge();
+  if (P.dbg & 2) {  // SRL_MK_DBG=2: no lookahead (A/B), the caller grabs
+    csync();
+    return false;
+  }
+  if (ct == 0) {  // the lookahead warp's answer (normally long ready)
+    SpinGuard g;
+    while (ld_acquire_cta(&anx->done) != seq) g.tick();
+    *s_next = anx->item;
+  }
+  csync();  // (the tiles / sm_acc and s_flag are reused by the next item; *s_next is published)
+  if (tr && ct == 0 && tr[14] == 0) tr[14] = clock64() - c_start;
+  return true;
 }
 
 // plan copy + embedding + first RMSNorm statistics for row m.  red: one
@@ -1105,6 +1176,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Lo::misc);
   int* s_flag = reinterpret_cast<int*>(smem + Lo::misc + 4);
   int* s_seen = reinterpret_cast<int*>(smem + Lo::misc + 8);  // last phase seen complete
+  int* s_next = reinterpret_cast<int*>(smem + Lo::misc + 12);  // attention: the CTA's next queue item
+  MkAnx* anx = reinterpret_cast<MkAnx*>(smem + Lo::anx);
   float* s_rstd = reinterpret_cast<float*>(smem + Lo::rstd);
   int2* s_rows = reinterpret_cast<int2*>(smem + Lo::rows);
 
@@ -1113,7 +1186,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
   const unsigned ep1 = *P.epoch + 1u;
   const unsigned target = ep1 * (unsigned)GR;
 
-  if (threadIdx.x == 64) *s_seen = 0;
+  if (threadIdx.x == 64) {
+    *s_seen = 0;
+    anx->req = 0;
+    anx->done = 0;
+  }
   if (warp == 0) {
     tmem_alloc<128>(tmem_slot);  // two 64-column fp32 accumulators
   } else if (warp == 1) {
@@ -1174,6 +1251,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             fence_proxy_async_global();  // generic-proxy results -> TMA reads
             flow_seen = t;
           };
+          // the rest of the first item's weight boxes go to L2 while the
+          // previous phase finishes (its HBM time is mostly idle: split-K
+          // exchanges, barriers), so this phase streams them from L2
+          // (SRL_MK_L2PF=0: off, A/B)
+          if (!dep_ok && P.l2_prefetch)
+            for (int k = pre; k < nkb; ++k) tma_prefetch_2d_l2(tw, (kb0 + k) * kBK, n0);
           if (!dep_ok && !flow) {
             // the compute warps' poller publishes each completed phase here
             // (one global poller per CTA)
@@ -1240,6 +1323,57 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
       }
     }
     __syncwarp();
+  } else if (warp == 3) {
+    // ------------------------------------------- attention lookahead (MkAnx)
+    if (elect_one()) {
+      int seen = 0;
+      constexpr int W = (G + 2) * HD, KT = AttnSmem<HD, G>::KT, NPG = kCW * KT / kPageTokens;
+      static_assert(NPG <= 8, "mailbox pages");
+      while (true) {
+        int r;
+        {
+          SpinGuard g;
+          while ((r = ld_acquire_cta(&anx->req)) == seen) {
+            __nanosleep(32);
+            g.tick();
+          }
+        }
+        seen = r;
+        const int p = anx->phase;
+        if (p < 0) break;  // the compute warps are done
+        const MkPhase& F = P.phases[p];
+        const int i = mk_queue(P, F, ep1, GR).resolve(mk_queue(P, F, ep1, GR).grab());
+        int bulk = 0;
+        if (i >= 0) {
+          const int rowheads = P.S * P.nkv, split = i / rowheads, rest = i % rowheads;
+          const int m = rest / P.nkv, kh = rest % P.nkv;
+          const int2 sr = s_rows[m];
+          const int k0 = split * P.attn_chunk, k1 = min(sr.y + 1, k0 + P.attn_chunk);
+          if (sr.x >= 0 && k1 > k0) {
+            const int32_t* btr = P.block_table + (size_t)sr.x * P.pps;
+            const int pg0 = k0 / kPageTokens;
+            int pg[NPG];
+#pragma unroll
+            for (int w = 0; w < NPG; ++w) pg[w] = (pg0 + w) * kPageTokens < k1 ? btr[pg0 + w] : 0;
+            const int cp = btr[sr.y / kPageTokens];
+            const uint32_t bytes = (uint32_t)(F.cs * W * 4);
+            if (Lo::qpre_bytes >= bytes) {
+              fence_proxy_async_shared();  // the previous item's generic reads of qpre, then the bulk write
+              mbar_arrive_expect_tx(cbar, bytes);
+              bulk_g2s(smem + Lo::qpre, P.qkv_part + ((size_t)m * P.nkv + kh) * F.cs * W, bytes, cbar);
+              bulk = 1;
+            }
+#pragma unroll
+            for (int w = 0; w < NPG; ++w) anx->pages[w] = pg[w];
+            anx->cpage = cp;
+          }
+        }
+        anx->item = i;
+        anx->bulk = bulk;
+        st_release_cta(&anx->done, r);
+      }
+    }
+    __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------ compute
     const int ct = threadIdx.x - 128, cw = ct >> 5, lane = ct & 31;
@@ -1248,6 +1382,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
     uint32_t cph = 0;                    // cbar phase
     uint32_t xph = 0;                    // xbar phase
     bool rows_ready = false;
+    int seq = 0;  // lookahead requests posted (ct 0)
     const bool stamp = P.stamps != nullptr && c == 0 && ct == 0;
     int acc = 0;
     uint32_t aph = 0;
@@ -1294,22 +1429,33 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
         // exactly one failing grab, so a launch adds n_items + grid to the
         // counter and (epoch x that) is this launch's base.  The queue position
         // maps through attn_order (longest items first, built in the embed phase).
-        unsigned* queue = P.tile_ctr + F.ctr_base + P.S * P.nkv;
-        const unsigned qbase = (ep1 - 1u) * (unsigned)(F.n_items + GR);
+        const MkQueue qu = mk_queue(P, F, ep1, GR);
         const int rowheads = P.S * P.nkv;
+        float* qpre = (Lo::qpre_bytes >= (size_t)F.cs * (G + 2) * HD * 4)
+                          ? reinterpret_cast<float*>(smem + Lo::qpre) : nullptr;
+        if (ct == 0) *s_next = qu.resolve(qu.grab());  // the phase's first item
+        csync();
+        bool pre = false;
+        int ordinal = 0;  // items taken by this CTA in the phase (trace: stamps of item P.trace_item)
         while (true) {
-          if (ct == 0) *s_flag = (int)(atomicAdd(queue, 1u) - qbase);
-          csync();
-          const int iq = *s_flag;
-          csync();  // s_flag is reused inside the item
-          if (iq >= F.n_items) break;
-          const int i = __ldcg(P.attn_order + iq);  // longest first (mk_attn_order)
+          const int i = *s_next;  // longest first (mk_attn_order)
+          csync();  // everyone has read it
+          if (i < 0) break;
+          unsigned long long* tri = (tr && ordinal == P.trace_item) ? tr : nullptr;
+          ++ordinal;
+          if (tr && ct == 0) tr[15] = (unsigned long long)ordinal;
           const int split = i / rowheads;
           const int rest = i % rowheads;
           const long long a_c0 = clock64();
-          mk_attention<HD, G>(P, F.layer, F.colv, F.cs, rest / P.nkv, rest % P.nkv, split, scratch, s_rows,
-                              P.tile_ctr + F.ctr_base, ep1, P.ws, ct, s_flag, cbar, cph, tr);
-          if (tr && ct == 0 && tr[10] == 0) tr[10] = clock64() - a_c0;
+          const bool took = mk_attention<HD, G>(P, F.layer, F.colv, F.cs, rest / P.nkv, rest % P.nkv, split,
+                                                scratch, s_rows, P.tile_ctr + F.ctr_base, ep1, P.ws, ct, s_flag,
+                                                cbar, cph, tri, anx, pre, qpre, p, seq, s_next);
+          if (tri && ct == 0 && tri[10] == 0) tri[10] = clock64() - a_c0;
+          pre = took;
+          if (!took) {
+            if (ct == 0) *s_next = qu.resolve(qu.grab());
+            csync();
+          }
         }
       } else if (F.kind == MK_SAMPLE) {
         for (int s = first_item(c, F.rot, GR); s < F.n_items; s += GR) mk_sample(P, s, ct, scratch, tr);
@@ -1497,6 +1643,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
         phase_arrive(P.phase_done, p, c);
         if (tr) tr[7] = globaltimer();
       }
+    }
+    if (ct == 0) {  // release the lookahead warp
+      anx->phase = -1;
+      st_release_cta(&anx->req, ++seq);
     }
     if (stamp) {
       phase_wait(P.phase_done, P.n_phases - 1, target);

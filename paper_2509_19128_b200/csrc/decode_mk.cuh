@@ -89,7 +89,8 @@ struct MkParams {
   int n_phases;
   unsigned long long* stamps;   // profiling: [n_phases + 1] globaltimer (ns) or nullptr
   int dbg;                      // experiments
-  int pf_blocks;                // L2 weight prefetch distance (16 KB k-blocks per CTA)
+  int trace_item;               // SRL_MK_TRACE_ITEM: which attention item of a CTA the trace stamps (0: first)
+  int l2_prefetch;              // GEMM phases: the first item's remaining weight boxes to L2 early
   int pairs;                    // launched as CTA pairs (cluster 2): QKV and O reduce split-K
                                 // through DSMEM; attention reads finished q / K / V
   unsigned long long* trace;    // debugging: [n_phases][grid][8] per-CTA timestamps or nullptr

@@ -538,8 +538,12 @@ int DecoderBackend::mega_init() {
     P.n_phases = n;
     P.stamps = nullptr;
     if (const char* dbg = std::getenv("SRL_MK_DBG")) P.dbg = std::atoi(dbg);
-    P.pf_blocks = 0;  // L2 weight prefetch: off (measured slower; SRL_MK_PF_KB to experiment)
-    if (const char* pf = std::getenv("SRL_MK_PF_KB")) P.pf_blocks = std::max(0, std::atoi(pf) / 16);
+    P.trace_item = 0;
+    if (const char* ti = std::getenv("SRL_MK_TRACE_ITEM")) P.trace_item = std::max(0, std::atoi(ti));
+    {
+      const char* pf = std::getenv("SRL_MK_L2PF");
+      P.l2_prefetch = pf ? (pf[0] != '0') : 0;
+    }
     P.pairs = pairs ? 1 : 0;
   }
   mk_.stamps = reinterpret_cast<unsigned long long*>(base + o_st);

@@ -64,8 +64,13 @@ struct EpiParams {
   const double* lse_in = nullptr;
   const float* row_coef = nullptr;
   __nv_bfloat16* outT_bf16 = nullptr;
-  __nv_bfloat16* out2_bf16 = nullptr;   // EPI_SWIGLU: also the rstd-scaled gate | up [M x N] (bf16)
-  const __nv_bfloat16* gu_in = nullptr; // EPI_SWIGLU_BWD: gate | up pre-activations [M x 2N]
+  // EPI_SWIGLU also keeps the rstd-scaled gate | up for the backward, and
+  // EPI_SWIGLU_BWD reads it back, in the token-blocked layout of gu_index():
+  // a (32-token block, column) pair is 32 contiguous values, which is exactly
+  // what one epilogue thread holds (column = TMEM lane, 32 tokens) -- 16-byte
+  // vector stores / loads instead of 32 strided scalars.  Rows padded to 32.
+  __nv_bfloat16* out2_bf16 = nullptr;   // EPI_SWIGLU: bf16 gate | up [M x N], gu_index layout
+  const __nv_bfloat16* gu_in = nullptr; // EPI_SWIGLU_BWD: gate | up pre-activations [M x 2N], gu_index layout
   int ldT = 0;
   int* tile_flags = nullptr;            // gemm_mn_launch split-K ordering (>= tiles ints, zeroed once)
   // Split operands (gemm_big only; the trainer's precise mode carries a value
@@ -82,13 +87,21 @@ struct EpiParams {
   // hi at column c, lo = bf16(v - hi) at column c + lo_off (0: hi only).
   // EPI_RESID's xg row stride is N + lo_off.
   int lo_off = 0;
-  float* out2_f32 = nullptr;            // EPI_SWIGLU: fp32 rstd-scaled gate | up [M x N]
-  const float* gu_in_f32 = nullptr;     // EPI_SWIGLU_BWD: fp32 gate | up (instead of gu_in)
+  float* out2_f32 = nullptr;            // EPI_SWIGLU: fp32 gate | up [M x N], gu_index layout
+  const float* gu_in_f32 = nullptr;     // EPI_SWIGLU_BWD: fp32 gate | up (instead of gu_in), gu_index layout
   const float* row_scale = nullptr;     // EPI_SWIGLU_BWD: dgu[m, :] *= row_scale[m]
   int fold_rstd = 0;                    // EPI_DLOGITS: d *= rstd[m] (the LM head's rstd folded in)
   // debug: per-CTA %globaltimer phase stamps [ctas x 8] (null = off)
   unsigned long long* stamps = nullptr;
 };
+
+// token-blocked gate | up layout (EPI_SWIGLU out2_*, EPI_SWIGLU_BWD gu_in*):
+// element (m, col) of an [M x N] matrix, M padded to a multiple of 32
+__host__ __device__ __forceinline__ size_t gu_index(size_t m, size_t col, size_t N) {
+  return (((m >> 5) * N + col) << 5) + (m & 31);
+}
+__host__ __device__ __forceinline__ size_t gu_rows_padded(size_t M) { return (M + 31) & ~size_t(31); }
+
 
 // Build a 2-D bf16 TMA descriptor for a row-major [rows x cols] matrix with a
 // box of [box_rows x 64] elements and 128-B swizzle (the UMMA K-major layout).

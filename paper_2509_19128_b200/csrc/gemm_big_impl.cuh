@@ -509,37 +509,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           if (kind == EPI_SWIGLU) {
-            // tile = 64 gate | 64 up columns: stage the rstd-scaled values, then
-            // 16-byte stores: the bf16 gate|up copy (8 columns x 1 token per
-            // thread-step) and act = silu(g) u (8 act columns x 1 token)
+            // tile = 64 gate | 64 up columns: the rstd-scaled values go to the
+            // gate|up copy straight from registers (this thread's column, 32
+            // tokens: contiguous in the gu_index layout) and are staged for
+            // act = silu(g) u (16-byte stores of 8 act columns x 1 token)
+            float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const float rj = __shfl_sync(0xffffffffu, rs, j);
-              tile[j * kPitch + tid] = __uint_as_float(r[j]) * rj;
+              v[j] = __uint_as_float(r[j]) * rj;
+              tile[j * kPitch + tid] = v[j];
+            }
+            if (epi.out2_f32 && n < N) {  // fp32 gate | up copy (precise backward)
+              float4* dst = reinterpret_cast<float4*>(epi.out2_f32 + gu_index(tc0, n, N));
+#pragma unroll
+              for (int k = 0; k < 8; ++k) dst[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            }
+            if (epi.out2_bf16 && n < N) {
+              uint4* dst = reinterpret_cast<uint4*>(epi.out2_bf16 + gu_index(tc0, n, N));
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                dst[k] = make_uint4(bf2_bits(v[8 * k], v[8 * k + 1]), bf2_bits(v[8 * k + 2], v[8 * k + 3]),
+                                    bf2_bits(v[8 * k + 4], v[8 * k + 5]), bf2_bits(v[8 * k + 6], v[8 * k + 7]));
             }
             sync();
-            if (epi.out2_f32) {  // fp32 gate | up copy (precise backward)
-#pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                const int idx = tid + 128 * k, j = idx >> 5, c4 = (idx & 31) * 4;
-                if (j >= jn) continue;
-                *reinterpret_cast<float4*>(epi.out2_f32 + (size_t)(tc0 + j) * N + n0 + c4) =
-                    *reinterpret_cast<const float4*>(&tile[j * kPitch + c4]);
-              }
-            }
-            if (epi.out2_bf16) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int idx = tid + 128 * k, j = idx >> 4, c8 = (idx & 15) * 8;
-                if (j >= jn) continue;
-                const float4 x0 = *reinterpret_cast<const float4*>(&tile[j * kPitch + c8]);
-                const float4 x1 = *reinterpret_cast<const float4*>(&tile[j * kPitch + c8 + 4]);
-                uint4 o;
-                o.x = bf2_bits(x0.x, x0.y); o.y = bf2_bits(x0.z, x0.w);
-                o.z = bf2_bits(x1.x, x1.y); o.w = bf2_bits(x1.z, x1.w);
-                *reinterpret_cast<uint4*>(epi.out2_bf16 + (size_t)(tc0 + j) * N + n0 + c8) = o;
-              }
-            }
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const int idx = tid + 128 * k, j = idx >> 3, c8 = (idx & 7) * 8;
@@ -581,22 +574,44 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int lc = (tid >> 6) * 128 + (tid & 63);  // tile-local gate column
             uint16_t* st16 = reinterpret_cast<uint16_t*>(tile);  // [32][256]
             const size_t gcol = (size_t)2 * n0 + lc;
-            // all 64 gate / up loads in flight before the first store
+            // this thread's gate and up columns for the chunk's 32 tokens: 2 x 32
+            // contiguous values (gu_index layout), all in flight together
             float gf[32], uf[32];
-            if (epi.gu_in_f32) {  // precise: fp32 gate | up, row stride 2N
+            const size_t gidx = gu_index(tc0, gcol, 2 * (size_t)N), uidx = gu_index(tc0, gcol + 64, 2 * (size_t)N);
+            if (epi.gu_in_f32) {  // precise: fp32 gate | up
+              const float4* g4 = reinterpret_cast<const float4*>(epi.gu_in_f32 + gidx);
+              const float4* u4 = reinterpret_cast<const float4*>(epi.gu_in_f32 + uidx);
+              float4 gv4[8], uv4[8];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const size_t row = (size_t)(tc0 + (j < jn ? j : 0)) * (2 * (size_t)N);
-                gf[j] = n < N ? __ldg(epi.gu_in_f32 + row + gcol) : 0.f;
-                uf[j] = n < N ? __ldg(epi.gu_in_f32 + row + gcol + 64) : 0.f;
+              for (int k = 0; k < 8; ++k) {
+                gv4[k] = n < N ? __ldg(g4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+                uv4[k] = n < N ? __ldg(u4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                gf[4 * k] = gv4[k].x; gf[4 * k + 1] = gv4[k].y; gf[4 * k + 2] = gv4[k].z; gf[4 * k + 3] = gv4[k].w;
+                uf[4 * k] = uv4[k].x; uf[4 * k + 1] = uv4[k].y; uf[4 * k + 2] = uv4[k].z; uf[4 * k + 3] = uv4[k].w;
               }
             } else {
-              const uint16_t* gu = reinterpret_cast<const uint16_t*>(epi.gu_in);
+              const uint4* g8 = reinterpret_cast<const uint4*>(epi.gu_in + gidx);
+              const uint4* u8 = reinterpret_cast<const uint4*>(epi.gu_in + uidx);
+              uint4 gv8[4], uv8[4];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const size_t row = (size_t)(tc0 + (j < jn ? j : 0)) * epi.ld_bf16;
-                gf[j] = n < N ? __bfloat162float(__ushort_as_bfloat16(__ldg(gu + row + gcol))) : 0.f;
-                uf[j] = n < N ? __bfloat162float(__ushort_as_bfloat16(__ldg(gu + row + gcol + 64))) : 0.f;
+              for (int k = 0; k < 4; ++k) {
+                gv8[k] = n < N ? __ldg(g8 + k) : make_uint4(0u, 0u, 0u, 0u);
+                uv8[k] = n < N ? __ldg(u8 + k) : make_uint4(0u, 0u, 0u, 0u);
+              }
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t gw[4] = {gv8[k].x, gv8[k].y, gv8[k].z, gv8[k].w};
+                const uint32_t uw[4] = {uv8[k].x, uv8[k].y, uv8[k].z, uv8[k].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  gf[8 * k + 2 * e] = __uint_as_float(gw[e] << 16);
+                  gf[8 * k + 2 * e + 1] = __uint_as_float(gw[e] & 0xffff0000u);
+                  uf[8 * k + 2 * e] = __uint_as_float(uw[e] << 16);
+                  uf[8 * k + 2 * e + 1] = __uint_as_float(uw[e] & 0xffff0000u);
+                }
               }
             }
             float rsc = 1.f;

@@ -124,8 +124,8 @@ __device__ __forceinline__ void epi_apply(const EpiParams& epi, float* tile, int
       const float a = g / (1.f + expf(-g)) * u;
       epi.out_bf16[(size_t)m * epi.ld_bf16 + (n0 >> 1) + c] = __float2bfloat16(a);
       if (epi.out2_bf16) {
-        epi.out2_bf16[(size_t)m * N + n0 + c] = __float2bfloat16(g);
-        epi.out2_bf16[(size_t)m * N + n0 + 64 + c] = __float2bfloat16(u);
+        epi.out2_bf16[gu_index(m, n0 + c, N)] = __float2bfloat16(g);
+        epi.out2_bf16[gu_index(m, n0 + 64 + c, N)] = __float2bfloat16(u);
       }
     }
   } else if (kind == EPI_QKV && (nthr & 127) == 0) {

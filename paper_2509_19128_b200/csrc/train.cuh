@@ -55,7 +55,8 @@ void launch_split_bf16(const float* src, int rows, int cols, const float* row_sc
 // rstd[t] = 1/sqrt(mean(x^2) + eps)
 void launch_row_rstd(const float* x, int T, int H, float eps, float* rstd, cudaStream_t st);
 
-// SwiGLU backward (interleaved 64-col gate|up blocks): dgu = d[silu(g) u].
+// SwiGLU backward (interleaved 64-col gate|up blocks): dgu = d[silu(g) u];
+// gu in the token-blocked layout (gemm.cuh gu_index), dgu row-major.
 void launch_swiglu_bwd(const float* dact, const __nv_bfloat16* gu, int T, int I, __nv_bfloat16* dgu,
                        float* dgu_f32, cudaStream_t st);
 

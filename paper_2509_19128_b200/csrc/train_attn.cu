@@ -517,13 +517,34 @@ __global__ void __launch_bounds__(kWarps * 32)
 // Forward over packed sequences: CTA = (64-query block, sequence, query head),
 // online softmax over the causal key blocks; O (bf16) and lse (natural log of
 // the scaled scores' partition sum) per (row, head), as the backward expects.
+// A key block is one 64-token page: K and V arrive row-major by cp.async into
+// a double buffer (block j + 1 streams in while block j is computed), Q lives
+// in registers as ldmatrix fragments, K^T and V are read with ldmatrix
+// (.trans for V) -- no transposed staging.  Only blocks that reach past the
+// block's first query position (or past the context) are masked.
 template <int HD>
 struct FwdSmem {
-  static constexpr int P = HD + 8;
+  static constexpr int P = HD + 8;  // row pitch (elements): conflict-free ldmatrix
   static constexpr size_t tile = sizeof(__nv_bfloat16) * kBlk * P;
-  static constexpr size_t tileT = sizeof(__nv_bfloat16) * HD * kPadT;
-  static constexpr size_t total = 2 * tile + tileT;  // Q, K, V^T
+  static constexpr size_t total = 4 * tile;  // K0 V0 K1 V1 (Q is staged in K1 first)
 };
+
+__device__ __forceinline__ void cp16_zfill(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(
+                   __cvta_generic_to_shared(dst))),
+               "l"(src), "r"(ok ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const __nv_bfloat16* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+}
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t (&r)[4], const __nv_bfloat16* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+}
 
 // Segment y: query rows seq_start[y] .. + seq_len[y] at positions pos0[y] ..
 // (0 when pos0 is null) of slot seg_slot[y] (y when null); keys 0 .. the last
@@ -538,11 +559,11 @@ __global__ void __launch_bounds__(kWarps * 32)
                  int nkv, float scale, __nv_bfloat16* __restrict__ out, float* __restrict__ lse_out,
                  int split_p, int out_lo) {
   using S = FwdSmem<HD>;
-  constexpr int P = S::P, NT = HD / 8;
+  constexpr int P = S::P, NT = HD / 8, C8 = HD / 8;
+  static_assert(kBlk == kPageTokens, "a key block is one page");
   extern __shared__ __align__(16) uint8_t smem[];
-  __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smem);
-  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem + S::tile);
-  __nv_bfloat16* Vt = reinterpret_cast<__nv_bfloat16*>(smem + 2 * S::tile);
+  __nv_bfloat16* const sb = reinterpret_cast<__nv_bfloat16*>(smem);
+  constexpr int TE = kBlk * P;  // elements per tile
   const int y = blockIdx.y, h = blockIdx.z;
   const int nrows = seq_len[y], s0 = seq_start[y];
   const int slot = seg_slot ? seg_slot[y] : y, p0 = seg_pos0 ? seg_pos0[y] : 0;
@@ -552,8 +573,44 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qvalid = min(kBlk, nrows - q0);
   const int kend = p0 + q0 + qvalid;  // keys [0, kend): up to the block's last query position
-  stage_bf16<HD>(Qs, nullptr, qvalid, [&](int r) { return q + ((size_t)(s0 + q0 + r) * nq + h) * HD; });
+  const int nblk = (kend + kBlk - 1) / kBlk;
+  // key block j (page j of the slot) -> K / V buffers (j & 1); rows past the
+  // context are zero-filled (P is 0 there, but 0 x stale NaN bits is NaN)
+  auto load_block = [&](int j) {
+    const int valid = min(kBlk, kend - j * kBlk);
+    const size_t page = (size_t)bt[(size_t)slot * pps + j];
+    const __nv_bfloat16* kg = kc + (page * nkv + kh) * kPageTokens * HD;
+    const __nv_bfloat16* vg = vc + (page * nkv + kh) * kPageTokens * HD;
+    __nv_bfloat16* kd = sb + (size_t)(2 * (j & 1)) * TE;
+    __nv_bfloat16* vd = kd + TE;
+#pragma unroll
+    for (int it = 0; it < kBlk * C8 / (kWarps * 32); ++it) {
+      const int e = threadIdx.x + it * kWarps * 32, r = e / C8, c = (e % C8) * 8;
+      const bool ok = r < valid;
+      cp16_zfill(kd + r * P + c, ok ? kg + r * HD + c : kg, ok);
+      cp16_zfill(vd + r * P + c, ok ? vg + r * HD + c : vg, ok);
+    }
+  };
+  {  // Q -> the K1 buffer, with block 0
+    __nv_bfloat16* qd = sb + 2 * TE;
+    const __nv_bfloat16* qg = q + ((size_t)(s0 + q0) * nq + h) * HD;
+#pragma unroll
+    for (int it = 0; it < kBlk * C8 / (kWarps * 32); ++it) {
+      const int e = threadIdx.x + it * kWarps * 32, r = e / C8, c = (e % C8) * 8;
+      const bool ok = r < qvalid;
+      cp16_zfill(qd + r * P + c, ok ? qg + (size_t)r * nq * HD + c : qg, ok);
+    }
+  }
+  load_block(0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
   const int qr = warp * 16;
+  uint32_t qf[HD / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < HD / 16; ++kk)
+    ldsm_x4(qf[kk], sb + 2 * TE + (qr + (lane & 15)) * P + kk * 16 + (lane >> 4) * 8);
+  __syncthreads();  // the Q staging (buffer 1) is refilled below
   const int ql_lo = qr + (lane >> 2), ql_hi = ql_lo + 8;
   float o[NT][4];
 #pragma unroll
@@ -562,28 +619,19 @@ __global__ void __launch_bounds__(kWarps * 32)
     for (int i = 0; i < 4; ++i) o[n][i] = 0.f;
   float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
 
-  for (int k0 = 0; k0 < kend; k0 += kBlk) {
-    const int kvalid = min(kBlk, kend - k0);
-    __syncthreads();
-    stage_bf16<HD>(Ks, nullptr, kvalid, [&](int r) { return page_row(kc, bt, pps, slot, k0 + r, nkv, kh, HD); });
-    {  // V^T [HD][64]
-      constexpr int V8 = HD / 8, NV = kBlk * V8 / (kWarps * 32);
-      uint4 v[NV];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int e = threadIdx.x + k * kWarps * 32, r = e / V8, c = (e % V8) * 8;
-        v[k] = r < kvalid ? *reinterpret_cast<const uint4*>(page_row(vc, bt, pps, slot, k0 + r, nkv, kh, HD) + c)
-                          : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int e = threadIdx.x + k * kWarps * 32, r = e / V8, c = (e % V8) * 8;
-        const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&v[k]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) Vt[(c + i) * kPadT + r] = hv[i];
-      }
+  for (int j = 0; j < nblk; ++j) {
+    if (j + 1 < nblk) {
+      load_block(j + 1);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    const __nv_bfloat16* Ks = sb + (size_t)(2 * (j & 1)) * TE;
+    const __nv_bfloat16* Vs = Ks + TE;
+    const int k0 = j * kBlk;
+    const int kvalid = min(kBlk, kend - k0);
     float s[8][4];
 #pragma unroll
     for (int n = 0; n < 8; ++n)
@@ -591,17 +639,18 @@ __global__ void __launch_bounds__(kWarps * 32)
       for (int i = 0; i < 4; ++i) s[n][i] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk) {
-      uint32_t a[4];
-      frag_a(a, Qs, P, qr, kk * 16, lane);
 #pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        uint32_t b0, b1;
-        frag_b(b0, b1, Ks, P, n * 8, kk * 16, lane);
-        mma16816(s[n], a, b0, b1);
+      for (int n = 0; n < 8; n += 2) {  // two 8-key column blocks per ldmatrix.x4
+        uint32_t b[4];
+        ldsm_x4(b, Ks + (n * 8 + (lane & 7) + ((lane >> 4) << 3)) * P + kk * 16 + ((lane >> 3) & 1) * 8);
+        mma16816(s[n], qf[kk], b[0], b[1]);
+        mma16816(s[n + 1], qf[kk], b[2], b[3]);
       }
     }
-    // scale + causal mask, new running max per row (a row's 64 columns live
-    // on the 4 lanes of a quad)
+    // scale (+ causal / context mask where the block reaches past the first
+    // query's position), new running max per row (a row's 64 columns live on
+    // the 4 lanes of a quad)
+    const bool masked = k0 + kBlk - 1 > p0 + q0 || kvalid < kBlk;
     float mx_lo = m_lo, mx_hi = m_hi;
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
@@ -609,7 +658,7 @@ __global__ void __launch_bounds__(kWarps * 32)
       for (int i = 0; i < 4; ++i) {
         const int kl = n * 8 + (lane & 3) * 2 + (i & 1);
         const int ql = i < 2 ? ql_lo : ql_hi;
-        const bool ok = kl < kvalid && k0 + kl <= p0 + q0 + ql;
+        const bool ok = !masked || (kl < kvalid && k0 + kl <= p0 + q0 + ql);
         s[n][i] = ok ? s[n][i] * scale : -INFINITY;
         if (i < 2) mx_lo = fmaxf(mx_lo, s[n][i]);
         else mx_hi = fmaxf(mx_hi, s[n][i]);
@@ -643,7 +692,8 @@ __global__ void __launch_bounds__(kWarps * 32)
       o[n][0] *= c_lo; o[n][1] *= c_lo;
       o[n][2] *= c_hi; o[n][3] *= c_hi;
     }
-    // P enters as bf16 (optionally + its lo residual, split_p)
+    // O += P V: P enters as bf16 (optionally + its lo residual, split_p); V[key][d]
+    // is the row-major B operand, read transposed by ldmatrix .trans
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
       uint32_t ah[4], al[4];
@@ -652,13 +702,18 @@ __global__ void __launch_bounds__(kWarps * 32)
       split2(s[2 * ks + 1][0], s[2 * ks + 1][1], ah[2], al[2]);
       split2(s[2 * ks + 1][2], s[2 * ks + 1][3], ah[3], al[3]);
 #pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        uint32_t b0, b1;
-        frag_b(b0, b1, Vt, kPadT, n * 8, ks * 16, lane);
-        mma16816(o[n], ah, b0, b1);
-        if (split_p) mma16816(o[n], al, b0, b1);
+      for (int n = 0; n < NT; n += 2) {  // two 8-dim column blocks per ldmatrix.x4.trans
+        uint32_t b[4];
+        ldsm_x4_trans(b, Vs + (ks * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * P + n * 8 + (lane >> 4) * 8);
+        mma16816(o[n], ah, b[0], b[1]);
+        mma16816(o[n + 1], ah, b[2], b[3]);
+        if (split_p) {
+          mma16816(o[n], al, b[0], b[1]);
+          mma16816(o[n + 1], al, b[2], b[3]);
+        }
       }
     }
+    __syncthreads();  // buffer (j & 1) is refilled with block j + 2 next iteration
   }
 #pragma unroll
   for (int off = 1; off <= 2; off <<= 1) {

@@ -7,6 +7,7 @@
 #include <cmath>
 
 #include "decoder.cuh"
+#include "gemm.cuh"
 #include "train.cuh"
 
 namespace srl {
@@ -324,7 +325,9 @@ __global__ void swiglu_bwd_kernel(const float* __restrict__ dact, const __nv_bfl
     const int j = (int)(e % I);
     const int blk = j >> 6, c = j & 63;
     const size_t gi = t * 2 * I + (size_t)blk * 128 + c, ui = gi + 64;
-    const float gv = __bfloat162float(gu[gi]), uv = __bfloat162float(gu[ui]), da = dact[e];
+    const float gv = __bfloat162float(gu[gu_index(t, (size_t)blk * 128 + c, 2 * (size_t)I)]);
+    const float uv = __bfloat162float(gu[gu_index(t, (size_t)blk * 128 + c + 64, 2 * (size_t)I)]);
+    const float da = dact[e];
     const float sg = 1.f / (1.f + expf(-gv));
     const float silu = gv * sg;
     const float dg = da * uv * (sg * (1.f + gv * (1.f - sg)));

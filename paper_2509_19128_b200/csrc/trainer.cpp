@@ -142,7 +142,8 @@ int DecoderTrainer::init(const DecoderWeights& w, const srl_trainer_options& o) 
         (st = alloc(&a.x_mid, (size_t)T_max_ * H)) || (st = alloc(&a.xg2, (size_t)T_max_ * H * sp_)) ||
         (st = alloc(&a.rstd2, T_max_)) || (st = alloc(&a.act, (size_t)T_max_ * I * sp_)))
       return st;
-    if (precise_ ? (st = alloc(&a.gu32, (size_t)T_max_ * 2 * I)) : (st = alloc(&a.gu, (size_t)T_max_ * 2 * I)))
+    const size_t gu_elems = gu_rows_padded((size_t)T_max_) * 2 * I;  // token-blocked (gemm.cuh gu_index)
+    if (precise_ ? (st = alloc(&a.gu32, gu_elems)) : (st = alloc(&a.gu, gu_elems)))
       return st;
   }
   if ((st = alloc(&x_, (size_t)T_max_ * H)) || (st = alloc(&xgF_, (size_t)T_max_ * H * sp_)) ||

@@ -38,7 +38,8 @@ class DecoderTrainer {
   struct LayerActs {
     float *x_in = nullptr, *rstd1 = nullptr, *lse = nullptr, *x_mid = nullptr, *rstd2 = nullptr;
     __nv_bfloat16 *xg1 = nullptr, *q = nullptr, *attn = nullptr, *xg2 = nullptr, *act = nullptr,
-                  *gu = nullptr;  // rstd-scaled gate | up pre-activations (bf16, 64-row interleave)
+                  *gu = nullptr;  // rstd-scaled gate | up pre-activations (bf16, 64-row interleave,
+                                      // token-blocked: gemm.cuh gu_index)
     float* gu32 = nullptr;        // the same in fp32 (precise mode)
   };
   // Split operands of the precise mode (EpiParams::seg_kb): up to 3 segments

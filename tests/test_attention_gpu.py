@@ -48,3 +48,58 @@ def test_attention_decode_matches_torch(cuda, nq, nkv, hd):
         err = (out[r].float() - ref).abs().max().item()
         # the output is bf16: half an ulp is 2^-9 relative, up to 3.9e-3 for values in [1, 2)
         assert err <= 5e-3 * max(1.0, ref.abs().max().item()), (c, err)
+
+
+@pytest.mark.parametrize("nq,nkv,hd", [(14, 2, 64), (12, 2, 128), (28, 4, 128)])
+def test_attention_prefill_matches_torch(cuda, nq, nkv, hd):
+    """attn_fwd_mma (srl_kernel_attention_prefill): the trainer's forward and a
+    prefill round's prompt rows.  Ragged packed segments (1 .. 321 rows, inside
+    one 64-key block, on and across block / page boundaries), segments that
+    start mid-context (seg_pos0: recompute chunks, continued prompts), paged
+    caches, GQA groups of 7 / 6 / 7.  O against fp32 at the bf16 output bar,
+    the split output (hi + lo, the trainer's precise mode) at 1e-4, lse 1e-4."""
+    g = torch.Generator(device="cuda").manual_seed(7 * nq + hd)
+    lens = [1, 5, 63, 64, 65, 200, 321, 130]
+    pos0 = [0, 0, 0, 10, 64, 0, 0, 700]
+    n = len(lens)
+    pps = (max(p + l for p, l in zip(pos0, lens)) + 63) // 64
+    slots = [(3 * y + 1) % n for y in range(n)]  # segments read other slots' pages
+    perm = torch.randperm(n * pps, generator=g, device="cuda").to(torch.int32)
+    bt = perm.view(n, pps).contiguous()
+    kc = (torch.randn(n * pps, nkv, 64, hd, generator=g, device="cuda") * 0.5).to(torch.bfloat16)
+    vc = torch.randn(n * pps, nkv, 64, hd, generator=g, device="cuda").to(torch.bfloat16)
+    starts = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int32)
+    T = int(sum(lens))
+    q = torch.randn(T, nq, hd, generator=g, device="cuda").to(torch.bfloat16)
+    d_start = torch.tensor(starts, dtype=torch.int32, device="cuda")
+    d_len = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    d_pos0 = torch.tensor(pos0, dtype=torch.int32, device="cuda")
+    d_slot = torch.tensor(slots, dtype=torch.int32, device="cuda")
+    W = nq * hd
+    out = torch.full((T, 2 * W), float("nan"), dtype=torch.bfloat16, device="cuda")
+    lse = torch.full((T, nq), float("nan"), dtype=torch.float32, device="cuda")
+    _lib.call("srl_kernel_attention_prefill", q.data_ptr(), kc.data_ptr(), vc.data_ptr(), bt.data_ptr(), pps,
+              d_start.data_ptr(), d_len.data_ptr(), d_pos0.data_ptr(), d_slot.data_ptr(), n, max(lens), nq, nkv, hd,
+              out.data_ptr(), lse.data_ptr(), W, None)
+    torch.cuda.synchronize()
+    G = nq // nkv
+    scale = 1.0 / math.sqrt(hd)
+    for y in range(n):
+        L, p0, s0 = lens[y], pos0[y], int(starts[y])
+        ctx = p0 + L
+        pages = bt[slots[y], :(ctx + 63) // 64].long()
+        K = kc[pages].float().permute(1, 0, 2, 3).reshape(nkv, -1, hd)[:, :ctx]  # [nkv, ctx, hd]
+        V = vc[pages].float().permute(1, 0, 2, 3).reshape(nkv, -1, hd)[:, :ctx]
+        qh = q[s0:s0 + L].float().view(L, nkv, G, hd)
+        s = torch.einsum("tkgd,kcd->tkgc", qh, K) * scale
+        keypos = torch.arange(ctx, device="cuda")
+        qpos = p0 + torch.arange(L, device="cuda")
+        s = s.masked_fill((keypos[None, :] > qpos[:, None])[:, None, None, :], float("-inf"))
+        ref_lse = torch.logsumexp(s, -1).reshape(L, nq)
+        ref = torch.einsum("tkgc,kcd->tkgd", torch.softmax(s, -1), V).reshape(L, W)
+        hi = out[s0:s0 + L, :W].float()
+        lo = out[s0:s0 + L, W:].float()
+        sc = max(1.0, ref.abs().max().item())
+        assert (hi - ref).abs().max().item() <= 5e-3 * sc, y
+        assert (hi + lo - ref).abs().max().item() <= 1e-4 * sc, y
+        assert torch.allclose(lse[s0:s0 + L], ref_lse, rtol=1e-4, atol=1e-4), y

@@ -57,6 +57,7 @@ def analyse(meta, tr):
         r["period"] = last - prev_last if prev_last is not None else last
         r["arrive"] = float(np.median(tr[p, :, 7][active] - tr[p, :, 3][active]))
         r["spans"] = (tr[p, :, 7][active] - t0[p][active]).astype(np.float64)
+        r["items_per_cta"] = tr[p, :, 15][active] if kind == "attn" else np.zeros(0)
         fields = ATTN_FIELDS if kind == "attn" else GEMM_FIELDS
         for k, name in fields:
             v = tr[p, :, k].copy()
@@ -89,6 +90,9 @@ def report(rows):
             spans = np.concatenate([x["spans"] for x in rs]) / 1e3
             print(f"attn   per-CTA phase span (us): min {spans.min():.1f} median {np.median(spans):.1f} "
                   f"p90 {np.percentile(spans, 90):.1f} max {spans.max():.1f}")
+            items = np.concatenate([x["items_per_cta"] for x in rs])
+            print(f"attn   items per CTA: mean {items.mean():.2f} max {items.max()} "
+                  f"(stamps below: item #{os.environ.get('SRL_MK_TRACE_ITEM', '0')} of each CTA)")
         print(f"{k:6s} n={len(rs):2d} cs={rs[0]['cs']:2d} items={rs[0]['items']:4d} "
               f"period={med('period'):6.0f} barrier={med('bar'):5.0f} arrive={med('arrive'):4.0f} | {inner}"
               f"  [sum period {sum(x['period'] for x in rs) / 1e3:.1f} us]")
