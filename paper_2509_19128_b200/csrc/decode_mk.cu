@@ -254,7 +254,8 @@ struct MkLayout {
   // while the current item finishes (hd 128; hd 64 has no room beside its
   // 6-stage ring: its items stage the partials in the K/V buffers)
   static constexpr size_t qpre = (anx + 64 + 127) & ~size_t(127);
-  static constexpr size_t qpre_bytes = HD == 128 ? 20480 : 0;
+  static constexpr size_t qpre_want = HD == 128 ? 24576 : 0;
+  static constexpr size_t qpre_bytes = qpre + qpre_want + 1024 <= 232448 ? qpre_want : 0;  // (if it fits)
   static constexpr size_t total = qpre + qpre_bytes;
   static constexpr size_t alloc = total + 1024;
   static_assert(alloc <= 232448, "shared memory budget");
@@ -437,7 +438,8 @@ __device__ __forceinline__ MkQueue mk_queue(const MkParams& P, const MkPhase& F,
 // its q operand one reduction away, instead of ~4 us of dependent round trips.
 struct MkAnx {
   int req, done;    // request sequence (compute warp 0) / completed request (warp 3)
-  int item, bulk;   // resolved item (attn_order value, -1: queue drained); 1: partials issued on cbar
+  int item, bulk;   // resolved item (attn_order value, -1: queue drained); on cbar: 1 the QKV
+                    // partials, 2 also the extras (bias slice, cos / sin row, x^2 partials)
   int cpage, phase; // the new key's page; the request's phase (-1: exit)
   int pad[2];
   int pages[8];     // pages of the item's first kCW x KT keys
@@ -568,39 +570,71 @@ __device__ bool mk_attention(const MkParams& P, int layer, long long bias_off, i
                                : P.block_table[(size_t)slot * P.pps + (k0 + warp * KT) / kPageTokens];
   const int cpage = pre ? anx->cpage : P.block_table[(size_t)slot * P.pps + pos / kPageTokens];
   constexpr int half = HD / 2;
-  const unsigned short* bias = reinterpret_cast<const unsigned short*>(P.w + bias_off);
   unsigned short bbits[WPT];
   float co[WPT], si[WPT];
+  float ss = 0.f;
+  if (pre && anx->bulk == 2) {
+    // the lookahead warp copied the partials AND the bias slice, the cos / sin
+    // row and the x^2 partials (mk_attn_extras): tiles first, then one wait
+    if (early) load_tile(warp, page_early);
+    for (int i = ct; i < (16 - G) * HD; i += kCT)
+      sqb[(G + i / HD) * A::QP + i % HD] = __float2bfloat16(0.f);
+    if (tr && ct == 0 && tr[1] == 0) tr[1] = clock64() - c_start;
+    mk_wait(cbar, cph);
+    cph ^= 1;
+    const uint8_t* ext = reinterpret_cast<const uint8_t*>(stage) + (size_t)qkv_cs * W * 4;
+    const unsigned short* sbias = reinterpret_cast<const unsigned short*>(ext);
+    const float* scs = reinterpret_cast<const float*>(ext + W * 2);
+    const float* sss = scs + HD;
+    for (int q = 0; q < P.parts; ++q) ss += sss[q];  // the order of gemm_detail::ssq_row_sum
 #pragma unroll
-  for (int u = 0; u < WPT; ++u) {
-    const int idx = ct + u * kCT;
-    bbits[u] = 0;
-    co[u] = 1.f;
-    si[u] = 0.f;
-    if (idx < W) {
-      const int col = idx < G * HD ? kh * G * HD + idx
-                      : idx < (G + 1) * HD ? qend + kh * HD + (idx - G * HD)
-                                           : kend + kh * HD + (idx - (G + 1) * HD);
-      bbits[u] = bias[col];
-      if (idx < (G + 1) * HD) {
-        const int jj = idx % HD, i = jj < half ? jj : jj - half;
-        co[u] = P.cos_sin[(size_t)pos * HD + i];
-        si[u] = P.cos_sin[(size_t)pos * HD + half + i];
+    for (int u = 0; u < WPT; ++u) {
+      const int idx = ct + u * kCT;
+      bbits[u] = 0;
+      co[u] = 1.f;
+      si[u] = 0.f;
+      if (idx < W) {
+        bbits[u] = sbias[idx];
+        if (idx < (G + 1) * HD) {
+          const int jj = idx % HD, i = jj < half ? jj : jj - half;
+          co[u] = scs[i];
+          si[u] = scs[half + i];
+        }
       }
     }
+  } else {
+    const unsigned short* bias = reinterpret_cast<const unsigned short*>(P.w + bias_off);
+#pragma unroll
+    for (int u = 0; u < WPT; ++u) {
+      const int idx = ct + u * kCT;
+      bbits[u] = 0;
+      co[u] = 1.f;
+      si[u] = 0.f;
+      if (idx < W) {
+        const int col = idx < G * HD ? kh * G * HD + idx
+                        : idx < (G + 1) * HD ? qend + kh * HD + (idx - G * HD)
+                                             : kend + kh * HD + (idx - (G + 1) * HD);
+        bbits[u] = bias[col];
+        if (idx < (G + 1) * HD) {
+          const int jj = idx % HD, i = jj < half ? jj : jj - half;
+          co[u] = P.cos_sin[(size_t)pos * HD + i];
+          si[u] = P.cos_sin[(size_t)pos * HD + half + i];
+        }
+      }
+    }
+    ss = gemm_detail::ssq_row_sum(P.ssq + (size_t)m * P.parts, P.parts);
+    if (tr && ct == 0 && tr[6] == 0) tr[6] = clock64() - c_start;
+    if (early) load_tile(warp, page_early);
+    for (int i = ct; i < (16 - G) * HD; i += kCT)
+      sqb[(G + i / HD) * A::QP + i % HD] = __float2bfloat16(0.f);
+    if (tr && ct == 0 && tr[1] == 0) tr[1] = clock64() - c_start;
+    mk_wait(cbar, cph);
+    cph ^= 1;
   }
-  const float ss = gemm_detail::ssq_row_sum(P.ssq + (size_t)m * P.parts, P.parts);
-  if (tr && ct == 0 && tr[6] == 0) tr[6] = clock64() - c_start;
-  if (early) load_tile(warp, page_early);
   float bia[WPT];
 #pragma unroll
   for (int u = 0; u < WPT; ++u) bia[u] = __uint_as_float((unsigned)bbits[u] << 16);
   const float rstd = rsqrtf(ss * P.inv_h + P.eps);
-  for (int i = ct; i < (16 - G) * HD; i += kCT)
-    sqb[(G + i / HD) * A::QP + i % HD] = __float2bfloat16(0.f);
-  if (tr && ct == 0 && tr[1] == 0) tr[1] = clock64() - c_start;
-  mk_wait(cbar, cph);
-  cph ^= 1;
   if (tr && ct == 0 && tr[2] == 0) tr[2] = clock64() - c_start;
 #pragma unroll
   for (int u = 0; u < WPT; ++u) {
@@ -1357,11 +1391,29 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
             for (int w = 0; w < NPG; ++w) pg[w] = (pg0 + w) * kPageTokens < k1 ? btr[pg0 + w] : 0;
             const int cp = btr[sr.y / kPageTokens];
             const uint32_t bytes = (uint32_t)(F.cs * W * 4);
+            // extras (mk_attention reads them when bulk == 2): the bias slice
+            // [q heads | k | v] of this kv head, the cos / sin row of the new
+            // position and the row's x^2 partials -- every operand of the item's
+            // q / k / v in one wait.  (Tensors are 128-byte aligned; the x^2
+            // row needs parts % 4 == 0.)
+            const uint32_t xb = (uint32_t)(W * 2 + HD * 4 + P.parts * 4);
+            const bool ext = (P.parts & 3) == 0 && Lo::qpre_bytes >= bytes + xb;
             if (Lo::qpre_bytes >= bytes) {
               fence_proxy_async_shared();  // the previous item's generic reads of qpre, then the bulk write
-              mbar_arrive_expect_tx(cbar, bytes);
-              bulk_g2s(smem + Lo::qpre, P.qkv_part + ((size_t)m * P.nkv + kh) * F.cs * W, bytes, cbar);
-              bulk = 1;
+              mbar_arrive_expect_tx(cbar, bytes + (ext ? xb : 0u));
+              uint8_t* dst = smem + Lo::qpre;
+              bulk_g2s(dst, P.qkv_part + ((size_t)m * P.nkv + kh) * F.cs * W, bytes, cbar);
+              if (ext) {
+                const int qend = P.nq * HD, kend = qend + P.nkv * HD;
+                const __nv_bfloat16* b = P.w + F.colv;
+                uint8_t* x = dst + bytes;
+                bulk_g2s(x, b + kh * G * HD, G * HD * 2, cbar);
+                bulk_g2s(x + G * HD * 2, b + qend + kh * HD, HD * 2, cbar);
+                bulk_g2s(x + (G + 1) * HD * 2, b + kend + kh * HD, HD * 2, cbar);
+                bulk_g2s(x + W * 2, P.cos_sin + (size_t)sr.y * HD, HD * 4, cbar);
+                bulk_g2s(x + W * 2 + HD * 4, P.ssq + (size_t)m * P.parts, P.parts * 4, cbar);
+              }
+              bulk = ext ? 2 : 1;
             }
 #pragma unroll
             for (int w = 0; w < NPG; ++w) anx->pages[w] = pg[w];

@@ -95,10 +95,21 @@ struct EpiParams {
   unsigned long long* stamps = nullptr;
 };
 
-// token-blocked gate | up layout (EPI_SWIGLU out2_*, EPI_SWIGLU_BWD gu_in*):
-// element (m, col) of an [M x N] matrix, M padded to a multiple of 32
-__host__ __device__ __forceinline__ size_t gu_index(size_t m, size_t col, size_t N) {
-  return (((m >> 5) * N + col) << 5) + (m & 31);
+// token-blocked gate | up layout (EPI_SWIGLU out2_*, EPI_SWIGLU_BWD gu_in*) of
+// an [M x N] matrix (M padded to 32, N % 32 == 0): 32 tokens x 32 columns
+// blocks, inside a block V-token groups (V = 4 fp32 / 8 bf16 = 16 bytes) of
+// the 32 columns, each column's V tokens contiguous.  An epilogue warp holds
+// 32 columns x 32 tokens (lane = column), so each 16-byte vector store / load
+// of the warp covers 512 contiguous bytes.
+template <int V>
+__host__ __device__ __forceinline__ size_t gu_index_v(size_t m, size_t col, size_t N) {
+  return ((((m >> 5) * (N >> 5) + (col >> 5)) * (32 / V) + ((m & 31) / V)) << 5 | (col & 31)) * V + (m % V);
+}
+__host__ __device__ __forceinline__ size_t gu_index(size_t m, size_t col, size_t N) {  // bf16
+  return gu_index_v<8>(m, col, N);
+}
+__host__ __device__ __forceinline__ size_t gu_index_f32(size_t m, size_t col, size_t N) {
+  return gu_index_v<4>(m, col, N);
 }
 __host__ __device__ __forceinline__ size_t gu_rows_padded(size_t M) { return (M + 31) & ~size_t(31); }
 

@@ -520,17 +520,19 @@ __global__ void __launch_bounds__(kThreads, 1)
               v[j] = __uint_as_float(r[j]) * rj;
               tile[j * kPitch + tid] = v[j];
             }
-            if (epi.out2_f32 && n < N) {  // fp32 gate | up copy (precise backward)
-              float4* dst = reinterpret_cast<float4*>(epi.out2_f32 + gu_index(tc0, n, N));
+            if (epi.out2_f32 && n < N) {  // fp32 gate | up copy (precise backward); token quad k is 128
+              float* dst = epi.out2_f32 + gu_index_f32(tc0, n, N);  // floats after quad k - 1
 #pragma unroll
-              for (int k = 0; k < 8; ++k) dst[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+              for (int k = 0; k < 8; ++k)
+                *reinterpret_cast<float4*>(dst + 128 * k) = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
             }
-            if (epi.out2_bf16 && n < N) {
-              uint4* dst = reinterpret_cast<uint4*>(epi.out2_bf16 + gu_index(tc0, n, N));
+            if (epi.out2_bf16 && n < N) {  // token octet k is 256 bf16 after octet k - 1
+              __nv_bfloat16* dst = epi.out2_bf16 + gu_index(tc0, n, N);
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                dst[k] = make_uint4(bf2_bits(v[8 * k], v[8 * k + 1]), bf2_bits(v[8 * k + 2], v[8 * k + 3]),
-                                    bf2_bits(v[8 * k + 4], v[8 * k + 5]), bf2_bits(v[8 * k + 6], v[8 * k + 7]));
+                *reinterpret_cast<uint4*>(dst + 256 * k) =
+                    make_uint4(bf2_bits(v[8 * k], v[8 * k + 1]), bf2_bits(v[8 * k + 2], v[8 * k + 3]),
+                               bf2_bits(v[8 * k + 4], v[8 * k + 5]), bf2_bits(v[8 * k + 6], v[8 * k + 7]));
             }
             sync();
 #pragma unroll
@@ -577,29 +579,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             // this thread's gate and up columns for the chunk's 32 tokens: 2 x 32
             // contiguous values (gu_index layout), all in flight together
             float gf[32], uf[32];
-            const size_t gidx = gu_index(tc0, gcol, 2 * (size_t)N), uidx = gu_index(tc0, gcol + 64, 2 * (size_t)N);
-            if (epi.gu_in_f32) {  // precise: fp32 gate | up
-              const float4* g4 = reinterpret_cast<const float4*>(epi.gu_in_f32 + gidx);
-              const float4* u4 = reinterpret_cast<const float4*>(epi.gu_in_f32 + uidx);
+            if (epi.gu_in_f32) {  // precise: fp32 gate | up (token quad k: + 128 k floats)
+              const float* g4 = epi.gu_in_f32 + gu_index_f32(tc0, gcol, 2 * (size_t)N);
+              const float* u4 = epi.gu_in_f32 + gu_index_f32(tc0, gcol + 64, 2 * (size_t)N);
               float4 gv4[8], uv4[8];
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
-                gv4[k] = n < N ? __ldg(g4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
-                uv4[k] = n < N ? __ldg(u4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+                gv4[k] = n < N ? __ldg(reinterpret_cast<const float4*>(g4 + 128 * k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                uv4[k] = n < N ? __ldg(reinterpret_cast<const float4*>(u4 + 128 * k)) : make_float4(0.f, 0.f, 0.f, 0.f);
               }
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
                 gf[4 * k] = gv4[k].x; gf[4 * k + 1] = gv4[k].y; gf[4 * k + 2] = gv4[k].z; gf[4 * k + 3] = gv4[k].w;
                 uf[4 * k] = uv4[k].x; uf[4 * k + 1] = uv4[k].y; uf[4 * k + 2] = uv4[k].z; uf[4 * k + 3] = uv4[k].w;
               }
-            } else {
-              const uint4* g8 = reinterpret_cast<const uint4*>(epi.gu_in + gidx);
-              const uint4* u8 = reinterpret_cast<const uint4*>(epi.gu_in + uidx);
+            } else {  // token octet k: + 256 k bf16
+              const __nv_bfloat16* g8 = epi.gu_in + gu_index(tc0, gcol, 2 * (size_t)N);
+              const __nv_bfloat16* u8 = epi.gu_in + gu_index(tc0, gcol + 64, 2 * (size_t)N);
               uint4 gv8[4], uv8[4];
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                gv8[k] = n < N ? __ldg(g8 + k) : make_uint4(0u, 0u, 0u, 0u);
-                uv8[k] = n < N ? __ldg(u8 + k) : make_uint4(0u, 0u, 0u, 0u);
+                gv8[k] = n < N ? __ldg(reinterpret_cast<const uint4*>(g8 + 256 * k)) : make_uint4(0u, 0u, 0u, 0u);
+                uv8[k] = n < N ? __ldg(reinterpret_cast<const uint4*>(u8 + 256 * k)) : make_uint4(0u, 0u, 0u, 0u);
               }
 #pragma unroll
               for (int k = 0; k < 4; ++k) {

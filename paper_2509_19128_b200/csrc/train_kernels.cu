@@ -315,6 +315,84 @@ __global__ void __launch_bounds__(256)
   for (int k = threadIdx.x; k < H; k += blockDim.x) atomicAdd(&dg[k], s_dg[k]);
 }
 
+// The same for 1024 < H <= 32 * 4 * NV (1.5B: H = 1536, NV = 12): the row's
+// dz and x and the gain-gradient partials stay in registers, the gain and dx
+// are read where they are used -- one pass over dz / x, one shared atomic
+// per column per warp (the generic kernel above: two passes and a shared
+// atomic per element, 166 us per 20480-row call at H = 1536).
+template <int NV>
+__global__ void __launch_bounds__(256)
+    rmsnorm_bwd_reg2_kernel(const float* __restrict__ dzw, const float* __restrict__ x,
+                            const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd, int T,
+                            int H, float* __restrict__ dx, float* __restrict__ dg, int pre) {
+  extern __shared__ float s_dg[];
+  for (int k = threadIdx.x; k < H; k += blockDim.x) s_dg[k] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int H4 = H / 4;
+  float4 acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto gain = [&](int k) {
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(g + 4 * k);
+    const float2 ga = __bfloat1622float2(g2[0]), gb = __bfloat1622float2(g2[1]);
+    return make_float4(ga.x, ga.y, gb.x, gb.y);
+  };
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < T; r += gridDim.x * (blockDim.x >> 5)) {
+    const float4* dz4 = reinterpret_cast<const float4*>(dzw + (size_t)r * H);
+    const float4* x4 = reinterpret_cast<const float4*>(x + (size_t)r * H);
+    float4* dx4 = reinterpret_cast<float4*>(dx + (size_t)r * H);
+    const float rstd_r = rstd[r];
+    const float rs = pre ? 1.f : rstd_r;
+    float4 d[NV], v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int k = lane + 32 * i;
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      d[i] = k < H4 ? dz4[k] : z;
+      v[i] = k < H4 ? x4[k] : z;
+    }
+    float dr = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int k = lane + 32 * i;
+      if (k >= H4) continue;
+      const float4 gv = gain(k);
+      dr += d[i].x * v[i].x * gv.x + d[i].y * v[i].y * gv.y + d[i].z * v[i].z * gv.z + d[i].w * v[i].w * gv.w;
+    }
+#pragma unroll
+    for (int s = 16; s; s >>= 1) dr += __shfl_xor_sync(0xffffffffu, dr, s);
+    const float coef = -rstd_r * rstd_r * rs / (float)H * dr;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int k = lane + 32 * i;
+      if (k >= H4) continue;
+      const float4 gv = gain(k);
+      float4 o = dx4[k];
+      o.x += rs * d[i].x * gv.x + coef * v[i].x;
+      o.y += rs * d[i].y * gv.y + coef * v[i].y;
+      o.z += rs * d[i].z * gv.z + coef * v[i].z;
+      o.w += rs * d[i].w * gv.w + coef * v[i].w;
+      dx4[k] = o;
+      acc[i].x += rs * d[i].x * v[i].x;
+      acc[i].y += rs * d[i].y * v[i].y;
+      acc[i].z += rs * d[i].z * v[i].z;
+      acc[i].w += rs * d[i].w * v[i].w;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int k = lane + 32 * i;
+    if (k >= H4) continue;
+    atomicAdd(&s_dg[4 * k], acc[i].x);
+    atomicAdd(&s_dg[4 * k + 1], acc[i].y);
+    atomicAdd(&s_dg[4 * k + 2], acc[i].z);
+    atomicAdd(&s_dg[4 * k + 3], acc[i].w);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < H; k += blockDim.x) atomicAdd(&dg[k], s_dg[k]);
+}
+
 __global__ void swiglu_bwd_kernel(const float* __restrict__ dact, const __nv_bfloat16* __restrict__ gu,
                                   int T, int I, __nv_bfloat16* __restrict__ dgu,
                                   float* __restrict__ dgu_f32) {
@@ -681,6 +759,10 @@ void launch_rmsnorm_bwd(const float* dzw, const float* x, const __nv_bfloat16* g
     case 6: rmsnorm_bwd_reg_kernel<6><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
     case 7: rmsnorm_bwd_reg_kernel<7><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
     case 8: rmsnorm_bwd_reg_kernel<8><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
+    case 9: case 10: case 11: case 12:
+      rmsnorm_bwd_reg2_kernel<12><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
+    case 13: case 14: case 15: case 16:
+      rmsnorm_bwd_reg2_kernel<16><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
     default: rmsnorm_bwd_kernel<<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre);
   }
 }

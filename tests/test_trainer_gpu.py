@@ -40,6 +40,9 @@ def make_trajs(rng, V, n, lens, prompts):
 # head_dim 128 with 3 query heads per KV head (the 1.5B / 7B attention layout)
 # and an untied LM head: the tensor-core attention kernels' other instance
 TINY128 = DecoderConfig("tiny-hd128", 256, 256, 2, 6, 2, 128, 512, False, 0, 4096, 10000.0, 1e-6)
+# the 1.5B widths (H 1536, 12 / 2 heads of 128) in one layer: the RMSNorm
+# backward's register path for 1024 < H <= 2048 and the 1.5B attention layout
+TINY1536 = DecoderConfig("tiny-h1536", 256, 1536, 1, 12, 2, 128, 512, False, 0, 4096, 10000.0, 1e-6)
 
 
 def check_precise(res, g_dev, lps, J, g_ref, off, bar=1e-3):
@@ -64,7 +67,7 @@ def check_precise(res, g_dev, lps, J, g_ref, off, bar=1e-3):
 
 @pytest.mark.parametrize("cfg,granularity,chunk", [(TINY, "sequence", 0), (TINY, "per_token", 0),
                                                    (TINY128, "sequence", 0), (TINY, "sequence", 64),
-                                                   (TINY128, "per_token", 64)])
+                                                   (TINY128, "per_token", 64), (TINY1536, "sequence", 0)])
 def test_trainer_precise_gradient_within_1e3(cuda, cfg, granularity, chunk):
     """chunk = 64: the LM head runs in 64-row passes (three chunk boundaries in
     the 131-row batch), the path the bench's 20480-row step takes at 16384."""
@@ -81,7 +84,7 @@ def test_trainer_precise_gradient_within_1e3(cuda, cfg, granularity, chunk):
 
 
 @pytest.mark.parametrize("cfg,granularity", [(TINY, "sequence"), (TINY, "per_token"),
-                                             (TINY128, "sequence")])
+                                             (TINY128, "sequence"), (TINY1536, "per_token")])
 def test_trainer_fast_bf16_gradient_matches_torch_fp64(cuda, cfg, granularity):
     pol = DecoderPolicy.random(cfg, seed=11, scale=0.03)
     w16 = pol.torch_weights().cpu().view(torch.int16).numpy().view(np.uint16)
