@@ -545,8 +545,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               *reinterpret_cast<float4*>(&u[0]) = *reinterpret_cast<const float4*>(&tile[j * kPitch + 64 + c8]);
               *reinterpret_cast<float4*>(&u[4]) = *reinterpret_cast<const float4*>(&tile[j * kPitch + 64 + c8 + 4]);
               float a[8];
+              // split output (precise mode, ~2^-17): the SFU sigmoid (ex2 + rcp, ~2 ulp)
+              // is far below the pair's resolution; a single bf16 act keeps the IEEE
+              // sigmoid so its rounding decisions track the fp64 oracle's (the
+              // trainer's fast-mode log-probs sit at that bf16 floor)
+              if (epi.lo_off) {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) a[e] = g[e] / (1.f + expf(-g[e])) * u[e];
+                for (int e = 0; e < 8; ++e) a[e] = __fdividef(g[e], 1.f + __expf(-g[e])) * u[e];
+              } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) a[e] = g[e] / (1.f + expf(-g[e])) * u[e];
+              }
               uint4 o;
               o.x = bf2_bits(a[0], a[1]); o.y = bf2_bits(a[2], a[3]);
               o.z = bf2_bits(a[4], a[5]); o.w = bf2_bits(a[6], a[7]);
@@ -621,7 +630,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 32; ++j) {
               const float gv = gf[j], uv = uf[j];
               const float da = __uint_as_float(r[j]) * __shfl_sync(0xffffffffu, rsc, j);
-              const float sg = 1.f / (1.f + expf(-gv));  // as swiglu_bwd_kernel
+              // sigmoid by the SFU (ex2 + rcp, ~2 ulp): the IEEE expf / divide sequences
+              // made this epilogue instruction-bound
+              const float sg = __fdividef(1.f, 1.f + __expf(-gv));
               const float silu = gv * sg;
               gf[j] = da * uv * (sg * (1.f + gv * (1.f - sg)));  // d gate
               uf[j] = da * silu;                                  // d up

