@@ -455,7 +455,7 @@ __device__ bool mk_attention(const MkParams& P, int layer, long long bias_off, i
                              uint8_t* scr, const int2* s_rows, unsigned* ctr, unsigned ep1,
                              float* ws, int ct, int* s_flag, uint64_t* cbar, uint32_t& cph,
                              unsigned long long* tr, MkAnx* anx, bool pre, float* qpre, int p, int& seq,
-                             int* s_next) {
+                             int* s_next, bool lookahead) {
   using A = AttnSmem<HD, G>;
   const long long c_start = clock64();
   constexpr int KT = A::KT, V4 = HD / 8, PER = KT * V4 / 32;
@@ -697,7 +697,7 @@ __device__ bool mk_attention(const MkParams& P, int layer, long long bias_off, i
     const bool has_next = t + kCW < ntiles;
     const int next_page = has_next ? tile_page(t + kCW) : 0;  // lookup latency under this tile
     const bool new_key = !P.pairs && owner && pos >= key0 && pos < key0 + nv;
-    if (ct == 0 && !has_next && !(P.dbg & 2)) {  // last tiles: the lookahead warp resolves the next item
+    if (ct == 0 && !has_next && lookahead) {  // last tiles: the lookahead warp resolves the next item
       anx->phase = p;
       st_release_cta(&anx->req, ++seq);
     }
@@ -873,7 +873,7 @@ __device__ bool mk_attention(const MkParams& P, int layer, long long bias_off, i
   } else if (splits > 1 && ct == 0) {  // nobody waits on this arrival
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(my_ctr), "r"(weight) : "memory");
   }
-  if (P.dbg & 2) {  // SRL_MK_DBG=2: no lookahead (A/B), the caller grabs
+  if (!lookahead) {  // the caller grabs (or the phase is a static deal)
     csync();
     return false;
   }
@@ -1468,7 +1468,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
         if (c == 0 && ct == 0) *P.round_ctr += 1;
         for (int m = first_item(c, F.rot, GR); m < F.n_items; m += GR)
           mk_embed(P, m, ct, reinterpret_cast<float*>(scratch));
-        if (c == GR - 1) mk_attn_order(P, ct, reinterpret_cast<int*>(scratch + 8192));
+        if (c == GR - 1 && P.S * P.nkv * P.attn_splits > GR)  // (a static deal needs no order)
+          mk_attn_order(P, ct, reinterpret_cast<int*>(scratch + 8192));
       } else if (F.kind == MK_ATTN) {
         if (!rows_ready) {  // the round's plan, once per CTA
           for (int j = ct; j < P.S; j += kCT) s_rows[j] = make_int2(P.plan.row_slot[j], P.plan.row_pos[j]);
@@ -1485,7 +1486,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
         const int rowheads = P.S * P.nkv;
         float* qpre = (Lo::qpre_bytes >= (size_t)F.cs * (G + 2) * HD * 4)
                           ? reinterpret_cast<float*>(smem + Lo::qpre) : nullptr;
-        if (ct == 0) *s_next = qu.resolve(qu.grab());  // the phase's first item
+        // at most one item per CTA (short contexts, e.g. 0.5B / 256-token
+        // rollouts): a static deal -- no queue atomic, no order lookup, no
+        // lookahead (the queue counter of such a phase is never touched)
+        const bool deal = F.n_items <= GR;
+        if (deal) {
+          if (ct == 0) *s_next = c < F.n_items ? c : -1;
+        } else if (ct == 0) {
+          *s_next = qu.resolve(qu.grab());  // the phase's first item
+        }
         csync();
         bool pre = false;
         int ordinal = 0;  // items taken by this CTA in the phase (trace: stamps of item P.trace_item)
@@ -1501,8 +1510,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_megakernel(const __grid_co
           const long long a_c0 = clock64();
           const bool took = mk_attention<HD, G>(P, F.layer, F.colv, F.cs, rest / P.nkv, rest % P.nkv, split,
                                                 scratch, s_rows, P.tile_ctr + F.ctr_base, ep1, P.ws, ct, s_flag,
-                                                cbar, cph, tri, anx, pre, qpre, p, seq, s_next);
+                                                cbar, cph, tri, anx, pre, qpre, p, seq, s_next,
+                                                !deal && !(P.dbg & 2));  // SRL_MK_DBG=2: no lookahead (A/B)
           if (tri && ct == 0 && tri[10] == 0) tri[10] = clock64() - a_c0;
+          if (deal) break;
           pre = took;
           if (!took) {
             if (ct == 0) *s_next = qu.resolve(qu.grab());

@@ -106,6 +106,49 @@ def test_mid_stream_update_splits_versions_at_the_pause_boundary(live):
         toks.append(e["token"])
 
 
+def recompute_and_check(docs, evs, prompt="demo"):
+    """Every event's log-prob recomputed offline under the version it carries
+    (test_protocol.cpp recompute_and_check), positions contiguous."""
+    orc = Oracle()
+    toks = []
+    assert [e["position"] for e in evs] == list(range(len(evs)))
+    for e in evs:
+        lp = orc.policy_logprobs(docs[e["weight_version"]], prompt, toks + [e["token"]])[-1]
+        assert abs(lp - e["logprob"]) <= 1e-9 * max(1.0, abs(lp))
+        toks.append(e["token"])
+
+
+def test_two_concurrent_streams_complete_with_contiguous_positions(live):
+    """test_protocol.cpp:93-104: two HTTP streams at once on a free-running
+    engine (the per-thread event buffers of Engine.wait_events)."""
+    eng, c = live(False)
+    runs = [stream_async(c, "demo", 16, s) for s in (1, 2)]
+    for t, out in runs:
+        t.join(60)
+        evs, reason = out["res"]
+        assert len(evs) == 16 and reason == "length"
+        assert [e["position"] for e in evs] == list(range(16))
+
+
+def test_eight_concurrent_streams_with_four_free_running_updates(live):
+    """test_protocol.cpp:314-336: eight streams while four updates land on the
+    free-running engine; every event's log-prob matches its version."""
+    eng, c = live(False)
+    runs = [stream_async(c, "demo", 48, 1000 + i) for i in range(8)]
+    docs = {0: V0}
+    for v in range(1, 5):
+        nxt = V1 if v % 2 == 1 else V0
+        docs[v] = nxt
+        st, body = c.update(v, nxt)
+        assert st == 200 and body == {"applied_version": v}
+    for t, out in runs:
+        t.join(120)
+        evs, reason = out["res"]
+        assert len(evs) == 48
+        recompute_and_check(docs, evs)
+    assert c.get("/admin/state")[1]["active_streams"] == 0
+
+
 def test_three_versions_in_order(live):
     eng, c = live(True)
     t, out = stream_async(c, "demo", 12, 8)
