@@ -2,7 +2,9 @@
 // embedding + first RMSNorm statistics, RoPE + paged-KV append, causal paged
 // GQA attention (split-KV, deterministic combine), last-row gather, the fp64
 // log-softmax/SplitMix64 sampler, and device lag statistics.
+#include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 
@@ -143,15 +145,25 @@ __global__ void rope_append_kernel(const float* __restrict__ qkv, int nq, int nk
 }
 
 // --------------------------------------------------------- attention ---
-// One CTA per (row, kv head, 128-key split); 4 warps x one 32-key tile each.
-// A warp stages its tile's K and V rows (contiguous inside a KV page) with
+// One CTA per (row, kv head, key split) -- splits sized by attention_splits;
+// 4 warps, each streaming 32-key tiles w, w + 4, ... of the split.  A warp stages its tile's K and V rows (contiguous inside a KV page) with
 // coalesced 16-B loads into shared memory, scores all G = nq/nkv query heads
 // of the group (lane = key), runs an online softmax per head and accumulates
 // P.V with lane = head dims.  Split partials are combined by the last CTA of
 // the (row, head) in split order (deterministic).
 constexpr int kAttnWarps = 4;
-constexpr int kAttnTilesPerWarp = 4;                           // 32-key tiles per warp per split
-constexpr int kAttnChunk = 32 * kAttnWarps * kAttnTilesPerWarp;  // keys per split
+constexpr int kAttnKeyStep = 32 * kAttnWarps;  // a split is a multiple of this many keys
+constexpr int kAttnMinChunk = 512;             // smallest split (sizes the merge workspace)
+constexpr int kAttnTargetCtas = 600;           // ~1.4 waves of 148 SMs x 3 resident CTAs
+// SRL_ATTN_CHUNK: a fixed split size instead of the heuristic (read once)
+int attn_chunk_override() {
+  static const int c = [] {
+    const char* v = std::getenv("SRL_ATTN_CHUNK");
+    const int k = v ? std::atoi(v) : 0;
+    return k <= 0 ? 0 : std::max(kAttnMinChunk, (k + kAttnKeyStep - 1) / kAttnKeyStep * kAttnKeyStep);
+  }();
+  return c;
+}
 __device__ __forceinline__ void att_cp16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
                "l"(gmem)
@@ -184,7 +196,8 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
                      const int32_t* __restrict__ block_table, int pages_per_seq,
                      const __nv_bfloat16* __restrict__ kc, const __nv_bfloat16* __restrict__ vc,
                      float scale, float* __restrict__ ws, int* __restrict__ counters,
-                     __nv_bfloat16* __restrict__ out, float* __restrict__ lse_out, int out_lo) {
+                     __nv_bfloat16* __restrict__ out, float* __restrict__ lse_out, int out_lo,
+                     int chunk) {
   // S = Q K^T and O = P V on the tensor cores (mma.sync m16n8k16): the G
   // query heads of the KV head are the A rows (padded to 16), each warp one
   // 32-key tile; P enters as hi + lo bf16 halves (fp32-class accuracy)
@@ -212,11 +225,9 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
   const int slot = row_slot[m];
   if (slot < 0) return;  // padding / finished row
   const int ctx = row_pos[m] + 1;
-  const int k_begin = split * kAttnChunk;
+  const int k_begin = split * chunk;
   if (k_begin >= ctx && splits == 1) return;
 
-  for (int i = threadIdx.x; i < 16 * HD; i += blockDim.x)
-    sq[i / HD][i % HD] = i < G * HD ? q[(size_t)m * nq * HD + (kh * G) * HD + i] : __float2bfloat16(0.f);
 
   float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;  // heads lane/4, lane/4 + 8
   float o[NDT][4];
@@ -228,7 +239,7 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
   // keys [k_begin, k_end) in 32-key tiles, warp w takes tiles w, w + 4, ...; K and
   // V of a tile are two cp.async groups: the next tile's K streams in under this
   // tile's softmax and P.V, its V under the next Q K^T (online softmax per warp)
-  const int k_end = min(ctx, k_begin + kAttnChunk);
+  const int k_end = min(ctx, k_begin + chunk);
   const int ntiles = k_end > k_begin ? (k_end - k_begin + 31) / 32 : 0;
   uint8_t* kb = sk[warp];
   uint8_t* vb = sv[warp];
@@ -258,6 +269,8 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
     }
     att_commit();
   };
+  for (int i = threadIdx.x; i < 16 * HD; i += blockDim.x)
+    sq[i / HD][i % HD] = i < G * HD ? q[(size_t)m * nq * HD + (kh * G) * HD + i] : __float2bfloat16(0.f);
   if (warp < ntiles) {
     load_k(warp);
     load_v(warp);
@@ -412,7 +425,7 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
   if (!s_last) return;
   __threadfence();
   const float* base = ws + ((size_t)m * nkv + kh) * splits * rec;
-  const int used = min(splits, (ctx + kAttnChunk - 1) / kAttnChunk);  // later splits are empty
+  const int used = min(splits, (ctx + chunk - 1) / chunk);  // later splits are empty
   for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
     const int g = i / HD, d = i % HD;
     float M = -INFINITY;
@@ -430,8 +443,21 @@ __global__ void __launch_bounds__(32 * kAttnWarps)
   if (threadIdx.x == 0) counters[cidx] = 0;
 }
 
-int attention_splits(const DecoderDims&, int, int max_ctx) {
-  return (max_ctx + kAttnChunk - 1) / kAttnChunk;
+// Key splits of a launch.  Few long splits beat many short ones (each split
+// pays the q load, the first tile's latency and the workspace merge): as few
+// as give ~kAttnTargetCtas CTAs, none shorter than kAttnMinChunk keys.
+// 7B, 256 rows x 4 KV heads, 1088-key contexts: one split (merge-free) --
+// attention 3.31 -> 2.07 ms per round against 512-key splits.
+int attention_splits(const DecoderDims& d, int M, int max_ctx) {
+  const int most = std::max(1, (max_ctx + kAttnMinChunk - 1) / kAttnMinChunk);
+  if (const int c = attn_chunk_override()) return std::min(most, std::max(1, (max_ctx + c - 1) / c));
+  const int units = std::max(1, M * d.nkv);
+  return std::min(most, std::max(1, (kAttnTargetCtas + units - 1) / units));
+}
+// keys per split for `splits` splits (a multiple of kAttnKeyStep)
+static int attention_chunk(int max_ctx, int splits) {
+  const int c = (max_ctx + splits - 1) / splits;
+  return std::max(kAttnKeyStep, (c + kAttnKeyStep - 1) / kAttnKeyStep * kAttnKeyStep);
 }
 
 // ------------------------------------------------------------- gather ---
@@ -950,7 +976,8 @@ void launch_rope_append(const float* qkv, const DecoderDims& d, const RoundPlan&
 }
 
 size_t attention_ws_floats(const DecoderDims& d, int M, int max_ctx) {
-  const int splits = attention_splits(d, M, max_ctx);
+  // any launch of <= M rows: at most one split per kAttnMinChunk keys
+  const int splits = std::max(1, (max_ctx + kAttnMinChunk - 1) / kAttnMinChunk);
   return (size_t)M * d.nkv * splits * (d.nq / d.nkv) * (d.hd + 2);
 }
 
@@ -967,7 +994,7 @@ template <int G, int HD>
 void attention_launch_t(dim3 grid, cudaStream_t st, const __nv_bfloat16* q, int nq, int nkv,
                         const RoundPlan& plan, const int32_t* bt, int pps, const __nv_bfloat16* kc,
                         const __nv_bfloat16* vc, float scale, float* ws, int* counters,
-                        __nv_bfloat16* out, float* lse_out, int out_lo) {
+                        __nv_bfloat16* out, float* lse_out, int out_lo, int chunk) {
   constexpr size_t smem = attention_smem<G, HD>();
   static bool once = [] {
     cudaFuncSetAttribute(attention_kernel<G, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -977,17 +1004,17 @@ void attention_launch_t(dim3 grid, cudaStream_t st, const __nv_bfloat16* q, int 
   (void)once;
   launch_pdl(attention_kernel<G, HD>, grid, dim3(32 * kAttnWarps), smem, st, dim3(1, 1, 1), q, nq,
              nkv, (const int32_t*)plan.row_slot, (const int32_t*)plan.row_pos, bt, pps, kc, vc,
-             scale, ws, counters, out, lse_out, out_lo);
+             scale, ws, counters, out, lse_out, out_lo, chunk);
 }
 
 template <int HD>
 void attention_dispatch_g(int G, dim3 grid, cudaStream_t st, const __nv_bfloat16* q, int nq,
                           int nkv, const RoundPlan& plan, const int32_t* bt, int pps,
                           const __nv_bfloat16* kc, const __nv_bfloat16* vc, float scale, float* ws,
-                          int* counters, __nv_bfloat16* out, float* lse_out, int out_lo) {
+                          int* counters, __nv_bfloat16* out, float* lse_out, int out_lo, int chunk) {
   switch (G) {
 #define SRL_ATTN_G(g) \
-  case g: attention_launch_t<g, HD>(grid, st, q, nq, nkv, plan, bt, pps, kc, vc, scale, ws, counters, out, lse_out, out_lo); break;
+  case g: attention_launch_t<g, HD>(grid, st, q, nq, nkv, plan, bt, pps, kc, vc, scale, ws, counters, out, lse_out, out_lo, chunk); break;
     SRL_ATTN_G(1) SRL_ATTN_G(2) SRL_ATTN_G(3) SRL_ATTN_G(4)
     SRL_ATTN_G(5) SRL_ATTN_G(6) SRL_ATTN_G(7) SRL_ATTN_G(8)
 #undef SRL_ATTN_G
@@ -1000,16 +1027,17 @@ void launch_attention(const __nv_bfloat16* q, const DecoderDims& d, const RoundP
                       const __nv_bfloat16* vc, int max_ctx, float* ws, int* counters,
                       size_t ws_floats, __nv_bfloat16* out, cudaStream_t st, float* lse_out, int out_lo) {
   const int splits = attention_splits(d, M, max_ctx);
+  const int chunk = attention_chunk(max_ctx, splits);
   (void)ws_floats;
   dim3 grid(M, d.nkv, splits);
   const float scale = 1.0f / sqrtf((float)d.hd);
   const int G = d.nq / d.nkv;
   if (d.hd == 64)
     attention_dispatch_g<64>(G, grid, st, q, d.nq, d.nkv, plan, block_table, pages_per_seq, kc,
-                             vc, scale, ws, counters, out, lse_out, out_lo);
+                             vc, scale, ws, counters, out, lse_out, out_lo, chunk);
   else
     attention_dispatch_g<128>(G, grid, st, q, d.nq, d.nkv, plan, block_table, pages_per_seq, kc,
-                              vc, scale, ws, counters, out, lse_out, out_lo);
+                              vc, scale, ws, counters, out, lse_out, out_lo, chunk);
 }
 
 // Slot bookkeeping written by a one-thread kernel (values travel as kernel
