@@ -130,3 +130,34 @@ def test_gemm_mn_w_kmajor_x_store(cuda, M, N, k_rows):
     out = torch.full((M, N), float("nan"), device=cuda)
     run_mn(w, x, M, N, k_rows, True, out, splits=1, accumulate=False)
     close(out, x.float() @ w.float(), tol=1e-4 * max(1.0, (k_rows / 64) ** 0.5))
+
+
+# 128 < M <= 256 rows with a long K (the 7B batch-256 decode's down GEMM): the
+# skinny path -- one 256-token tile, two 128-row weight tiles per CTA, split-K
+# over a cluster of 4-8 (gemm.cu skinny256_splits); ragged M and N
+@pytest.mark.parametrize("M,N,K", [(256, 3584, 18944), (200, 4608, 16384), (129, 1000, 8192)])
+def test_gemm_skinny256_store_and_residual(cuda, M, N, K):
+    g = torch.Generator(device=cuda).manual_seed(M + N + K)
+    w = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
+    x = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    bias = torch.randn(N, device=cuda, generator=g).bfloat16()
+    ref = x.float() @ w.float().T
+    outs = []
+    for _ in range(2):  # deterministic split-K order
+        out = torch.full((M, N), float("nan"), device=cuda)
+        run(w, x, EPI_F32, splits=0, bias=bias, out=out)
+        outs.append(out)
+    close(outs[0], ref + bias.float())
+    assert torch.equal(outs[0], outs[1])
+    if N % 128 == 0:
+        parts = N // 128
+        resid = torch.randn(M, N, device=cuda, generator=g)
+        resid0 = resid.clone()
+        gain = (torch.rand(N, device=cuda, generator=g) + 0.5).bfloat16()
+        xg = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+        ssq = torch.empty(M, parts, device=cuda)
+        run(w, x, EPI_RESID, splits=0, resid=resid, gain=gain, xg=xg, ssq_out=ssq)
+        r = resid0 + ref
+        close(resid, r)
+        close(xg, r * gain.float(), tol=1e-2)
+        close(ssq, (r.view(M, parts, 128) ** 2).sum(-1), tol=3e-3)
