@@ -1,4 +1,3 @@
-#include <cstdlib>
 // trainer.cpp -- trainer-side device computations of the decoder policy.
 //
 //  * decoder_policy_logprobs: per-token current-policy log-prob recompute
@@ -21,6 +20,7 @@
 //    receives (ncclBroadcast payload).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "decoder_engine.hpp"
