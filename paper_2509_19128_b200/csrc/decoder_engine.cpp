@@ -390,7 +390,7 @@ int DecoderBackend::mega_init() {
   // 1024 -> 3.49 ms, 2048 -> 3.12, 4096 -> 2.88, 6144 -> 3.47, 8192 -> 3.95 (the
   // item's q / k / v prologue and split merge amortised over more keys, until
   // there are fewer items than SMs)
-  static const int chunk_env = [] {
+  const int chunk_env = [] {  // read per engine (tests set it)
     const char* v = std::getenv("SRL_MK_ATTN_CHUNK");
     const int c = v ? std::atoi(v) : kMkAttnChunk;
     return std::max(64, std::min(8192, c / 64 * 64));

@@ -76,7 +76,8 @@ def test_megakernel_ragged_batch_matches_oracle(cuda, cfg, long_prompt):
 def test_megakernel_long_context_hd128_matches_multikernel_round(cuda, monkeypatch):
     """1.5B shape (head_dim 128, 6 query heads per KV head) with streams past
     2048 keys: the megakernel's attention items split the context (1024-key
-    splits merged by the last arrival) -- against the multi-kernel round's
+    items here, SRL_MK_ATTN_CHUNK: 2600 keys = 1024 + 1024 + 552, merged by the
+    last arrival) -- against the multi-kernel round's
     attention kernel (itself checked against torch up to 4100 keys,
     tests/test_attention_gpu.py) on the same prompts, greedy: tokens agree
     until a near-tie, log-probs within 4e-3 relative (two fp32 summation
@@ -87,6 +88,7 @@ def test_megakernel_long_context_hd128_matches_multikernel_round(cuda, monkeypat
     lens = [2600, 2100, 1030, 40] + list(rng.integers(2, 60, size=12))
     prompts = [rng.integers(0, cfg.vocab_size, size=int(n)).tolist() for n in lens]
     res = []
+    monkeypatch.setenv("SRL_MK_ATTN_CHUNK", "1024")
     for mk in ("1", "0"):
         monkeypatch.setenv("SRL_MEGAKERNEL", mk)
         eng = Engine(pol, start_paused=True, greedy=True, max_streams=16, max_seq_len=2700)
